@@ -1,0 +1,523 @@
+// oracle/ref_shim.cpp -- TEST INFRASTRUCTURE ONLY (never shipped, never on the product path).
+//
+// extern "C" entry points over the UNMODIFIED reference library `paramd`
+// (compiled by oracle/Makefile straight from /root/reference/proj/src/*.cpp into
+// oracle/_ref/libparamd_ref.so).  Used by tests/ as the parity checker, by
+// tests/golden/make_golden.py to write golden vectors, and by bench.py's
+// cpu_baseline / `--impl reference` legs to time the reference's own CPU path.
+//
+// Every function forwards to the reference's public API:
+//   msm_potential        include/paramd/msm.hpp:24-25, src/msm.cpp:52-90
+//   short_range          include/paramd/msm_phases.hpp:37, src/msm_phases.cpp:224-252
+//   phases               include/paramd/msm_phases.hpp:11-34, src/msm_phases.cpp:39-222
+//   build_grid_hierarchy src/msm_grid.cpp:24-54
+//   propagate            include/paramd/integrate.hpp:27-28, src/integrate.cpp:13-36
+//   parareal_*           include/paramd/parareal.hpp:131-144, src/parareal.cpp:94-239
+//   generate_random_system src/generate.cpp:40-93
+// Errors are mapped to the same integer codes as include/msmb.h.
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "paramd/electrostatics.hpp"
+#include "paramd/errors.hpp"
+#include "paramd/force_field.hpp"
+#include "paramd/generate.hpp"
+#include "paramd/integrate.hpp"
+#include "paramd/msm.hpp"
+#include "paramd/msm_grid.hpp"
+#include "paramd/msm_kernels.hpp"
+#include "paramd/msm_phases.hpp"
+#include "paramd/parareal.hpp"
+#include "paramd/cost_model.hpp"
+
+using namespace paramd;
+
+namespace {
+
+enum {
+    OK = 0,
+    E_CONFIG = 1,
+    E_DOMAIN = 2,
+    E_COVERAGE = 3,
+    E_COINCIDENT = 4,
+    E_HIERARCHY = 5,
+    E_RUNTIME = 6,
+    E_NONCONV = 7,
+    E_OTHER = 9
+};
+
+void put_msg(char* buf, int cap, const char* s) {
+    if (!buf || cap <= 0) return;
+    std::strncpy(buf, s, static_cast<std::size_t>(cap - 1));
+    buf[cap - 1] = 0;
+}
+
+template <class F>
+int guarded(char* msg, int cap, F&& f) {
+    try {
+        f();
+        put_msg(msg, cap, "");
+        return OK;
+    } catch (const NonConvergenceError& e) {
+        put_msg(msg, cap, e.what());
+        return E_NONCONV;
+    } catch (const ConfigError& e) {
+        put_msg(msg, cap, e.what());
+        return E_CONFIG;
+    } catch (const DomainError& e) {
+        put_msg(msg, cap, e.what());
+        return E_DOMAIN;
+    } catch (const CoverageError& e) {
+        put_msg(msg, cap, e.what());
+        return E_COVERAGE;
+    } catch (const CoincidentParticlesError& e) {
+        put_msg(msg, cap, e.what());
+        return E_COINCIDENT;
+    } catch (const HierarchyError& e) {
+        put_msg(msg, cap, e.what());
+        return E_HIERARCHY;
+    } catch (const RuntimeFault& e) {
+        put_msg(msg, cap, e.what());
+        return E_RUNTIME;
+    } catch (const std::exception& e) {
+        put_msg(msg, cap, e.what());
+        return E_OTHER;
+    }
+}
+
+ParticleSystem make_system(int64_t n, const double* pos, const double* vel, const double* q,
+                           const double* mass, const double* box) {
+    ParticleSystem s;
+    s.positions.resize(static_cast<std::size_t>(n));
+    s.velocities.assign(static_cast<std::size_t>(n), Vec3{});
+    s.charges.assign(q, q + n);
+    s.masses.assign(static_cast<std::size_t>(n), 1.0);
+    for (int64_t i = 0; i < n; ++i) {
+        s.positions[i] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+        if (vel) s.velocities[i] = {vel[3 * i], vel[3 * i + 1], vel[3 * i + 2]};
+        if (mass) s.masses[i] = mass[i];
+    }
+    s.box = {box[0], box[1], box[2]};
+    return s;
+}
+
+MsmConfig make_cfg(double a, double h, int levels, int p, int m) {
+    MsmConfig c;
+    c.cutoff_a = a;
+    c.spacing_h = h;
+    c.levels_l = levels;
+    c.interp_order_p = p;
+    c.smoothing_m = m;
+    return c;
+}
+
+void store_state(const ParticleSystem& s, double* pos, double* vel) {
+    for (std::size_t i = 0; i < s.size(); ++i) {
+        if (pos) {
+            pos[3 * i] = s.positions[i].x;
+            pos[3 * i + 1] = s.positions[i].y;
+            pos[3 * i + 2] = s.positions[i].z;
+        }
+        if (vel) {
+            vel[3 * i] = s.velocities[i].x;
+            vel[3 * i + 1] = s.velocities[i].y;
+            vel[3 * i + 2] = s.velocities[i].z;
+        }
+    }
+}
+
+// Level geometry straight from the reference's own build_grid_hierarchy.
+std::vector<MsmGridLevel> levels_for(const double* box, const MsmConfig& cfg) {
+    ParticleSystem s;
+    s.box = {box[0], box[1], box[2]};
+    return build_grid_hierarchy(s, cfg);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_version() { return 1; }
+
+// ---- kernel math KATs (include/paramd/msm_kernels.hpp:14-92) -------------------
+int ref_kernel_eval(int which, double x, double a, int k, int l, double* out, char* msg,
+                    int cap) {
+    return guarded(msg, cap, [&] {
+        switch (which) {
+            case 0: *out = smoothing_gamma(x); break;
+            case 1: *out = smoothing_gamma_deriv(x); break;
+            case 2: *out = kernel_g_star(x, a); break;
+            case 3: *out = kernel_g_star_deriv(x, a); break;
+            case 4: *out = kernel_g_level(x, a, k, l); break;
+            case 5: *out = basis_phi(x); break;
+            case 6: *out = basis_phi_deriv(x); break;
+            default: throw ConfigError("unknown kernel");
+        }
+    });
+}
+
+// ---- grid geometry (src/msm_grid.cpp:24-54) -------------------------------------
+// dims_out[3*levels], spacing_out[levels], origin_out[3*levels]
+int ref_grid_geometry(const double* box, double a, double h, int levels, int p, int m,
+                      int* dims_out, double* spacing_out, double* origin_out, char* msg,
+                      int cap) {
+    return guarded(msg, cap, [&] {
+        auto lv = levels_for(box, make_cfg(a, h, levels, p, m));
+        for (int k = 0; k < levels; ++k) {
+            for (int ax = 0; ax < 3; ++ax) dims_out[3 * k + ax] = lv[k].dims[ax];
+            spacing_out[k] = lv[k].spacing;
+            origin_out[3 * k] = lv[k].origin.x;
+            origin_out[3 * k + 1] = lv[k].origin.y;
+            origin_out[3 * k + 2] = lv[k].origin.z;
+        }
+    });
+}
+
+// ---- full evaluation (src/msm.cpp:52-90) ----------------------------------------
+int ref_msm_potential(int64_t n, const double* pos, const double* q, const double* box,
+                      double a, double h, int levels, int p, int m, double kc, double conv,
+                      double* phi, double* phi_short, double* phi_long, double* force,
+                      double* energy, double* level_charge, double* level_potential,
+                      char* msg, int cap) {
+    return guarded(msg, cap, [&] {
+        ParticleSystem s = make_system(n, pos, nullptr, q, nullptr, box);
+        UnitsConfig u{kc, conv};
+        MsmDiagnostics diag;
+        const bool want_diag = level_charge || level_potential;
+        PotentialResult r = msm_potential(s, make_cfg(a, h, levels, p, m), u,
+                                          want_diag ? &diag : nullptr);
+        for (int64_t i = 0; i < n; ++i) {
+            if (phi) phi[i] = r.per_particle_potential[i];
+            if (phi_short) phi_short[i] = (*r.short_part)[i];
+            if (phi_long) phi_long[i] = (*r.long_part)[i];
+            if (force) {
+                force[3 * i] = r.per_particle_force[i].x;
+                force[3 * i + 1] = r.per_particle_force[i].y;
+                force[3 * i + 2] = r.per_particle_force[i].z;
+            }
+        }
+        if (energy) *energy = r.total_energy;
+        if (want_diag) {
+            std::size_t off = 0;
+            for (const auto& lv : diag.levels) {
+                const std::size_t sz = lv.charge.data.size();
+                if (level_charge) std::memcpy(level_charge + off, lv.charge.data.data(), sz * 8);
+                if (level_potential)
+                    std::memcpy(level_potential + off, lv.potential.data.data(), sz * 8);
+                off += sz;
+            }
+        }
+    });
+}
+
+// ---- individual phases on caller-provided lattices (src/msm_phases.cpp) ---------
+int ref_short_range(int64_t n, const double* pos, const double* q, double a, double kc,
+                    double* phi, double* force, char* msg, int cap) {
+    return guarded(msg, cap, [&] {
+        const double box[3] = {1, 1, 1};
+        ParticleSystem s = make_system(n, pos, nullptr, q, nullptr, box);
+        MsmConfig c;
+        c.cutoff_a = a;
+        UnitsConfig u{kc, 4.184e-4};
+        ShortRangeResult r = short_range(s, c, u);
+        for (int64_t i = 0; i < n; ++i) {
+            phi[i] = r.potential[i];
+            force[3 * i] = r.force[i].x;
+            force[3 * i + 1] = r.force[i].y;
+            force[3 * i + 2] = r.force[i].z;
+        }
+    });
+}
+
+int ref_anterpolate(int64_t n, const double* pos, const double* q, const double* box, double a,
+                    double h, int levels, double* q0_out, char* msg, int cap) {
+    return guarded(msg, cap, [&] {
+        ParticleSystem s = make_system(n, pos, nullptr, q, nullptr, box);
+        auto lv = build_grid_hierarchy(s, make_cfg(a, h, levels, 3, 2));
+        anterpolate(s, lv[0]);
+        std::memcpy(q0_out, lv[0].charge.data.data(), lv[0].charge.data.size() * 8);
+    });
+}
+
+// fine level k -> coarse level k+1
+int ref_restrict(const double* box, double a, double h, int levels, int k,
+                 const double* fine_charge, double* coarse_out, char* msg, int cap) {
+    return guarded(msg, cap, [&] {
+        auto lv = levels_for(box, make_cfg(a, h, levels, 3, 2));
+        std::memcpy(lv[k].charge.data.data(), fine_charge, lv[k].charge.data.size() * 8);
+        restrict_charges(lv[k], lv[k + 1]);
+        std::memcpy(coarse_out, lv[k + 1].charge.data.data(), lv[k + 1].charge.data.size() * 8);
+    });
+}
+
+int ref_lattice_cutoff(const double* box, double a, double h, int levels, int k,
+                       const double* charge, double* pot_out, char* msg, int cap) {
+    return guarded(msg, cap, [&] {
+        MsmConfig c = make_cfg(a, h, levels, 3, 2);
+        auto lv = levels_for(box, c);
+        std::memcpy(lv[k].charge.data.data(), charge, lv[k].charge.data.size() * 8);
+        lattice_cutoff(lv[k], c);
+        std::memcpy(pot_out, lv[k].potential.data.data(), lv[k].potential.data.size() * 8);
+    });
+}
+
+int ref_top_level(const double* box, double a, double h, int levels, const double* charge,
+                  double* pot_out, char* msg, int cap) {
+    return guarded(msg, cap, [&] {
+        MsmConfig c = make_cfg(a, h, levels, 3, 2);
+        auto lv = levels_for(box, c);
+        auto& top = lv.back();
+        std::memcpy(top.charge.data.data(), charge, top.charge.data.size() * 8);
+        top_level(top, c);
+        std::memcpy(pot_out, top.potential.data.data(), top.potential.data.size() * 8);
+    });
+}
+
+// coarse level k+1 -> fine level k; fine_pot is read and updated in place
+int ref_prolongate(const double* box, double a, double h, int levels, int k,
+                   const double* coarse_pot, double* fine_pot, char* msg, int cap) {
+    return guarded(msg, cap, [&] {
+        auto lv = levels_for(box, make_cfg(a, h, levels, 3, 2));
+        std::memcpy(lv[k + 1].potential.data.data(), coarse_pot,
+                    lv[k + 1].potential.data.size() * 8);
+        std::memcpy(lv[k].potential.data.data(), fine_pot, lv[k].potential.data.size() * 8);
+        prolongate(lv[k + 1], lv[k]);
+        std::memcpy(fine_pot, lv[k].potential.data.data(), lv[k].potential.data.size() * 8);
+    });
+}
+
+int ref_interpolate(int64_t n, const double* pos, const double* box, double a, double h,
+                    int levels, const double* pot0, double* u_out, char* msg, int cap) {
+    return guarded(msg, cap, [&] {
+        std::vector<double> q(static_cast<std::size_t>(n), 0.0);
+        ParticleSystem s = make_system(n, pos, nullptr, q.data(), nullptr, box);
+        auto lv = build_grid_hierarchy(s, make_cfg(a, h, levels, 3, 2));
+        std::memcpy(lv[0].potential.data.data(), pot0, lv[0].potential.data.size() * 8);
+        auto u = interpolate_to_atoms(lv[0], s);
+        std::memcpy(u_out, u.data(), u.size() * 8);
+    });
+}
+
+int ref_direct_coulomb(int64_t n, const double* pos, const double* q, double kc, double* phi,
+                       double* force, double* energy, char* msg, int cap) {
+    return guarded(msg, cap, [&] {
+        const double box[3] = {1, 1, 1};
+        ParticleSystem s = make_system(n, pos, nullptr, q, nullptr, box);
+        PotentialResult r = direct_coulomb(s, UnitsConfig{kc, 4.184e-4});
+        for (int64_t i = 0; i < n; ++i) {
+            if (phi) phi[i] = r.per_particle_potential[i];
+            if (force) {
+                force[3 * i] = r.per_particle_force[i].x;
+                force[3 * i + 1] = r.per_particle_force[i].y;
+                force[3 * i + 2] = r.per_particle_force[i].z;
+            }
+        }
+        if (energy) *energy = r.total_energy;
+    });
+}
+
+// ---- integrator (src/integrate.cpp:13-36) ---------------------------------------
+// pos/vel are inputs and are overwritten with the propagated state.
+int ref_propagate(int64_t n, double* pos, double* vel, const double* q, const double* mass,
+                  const double* box, double a, double h, int levels, double kc, double conv,
+                  double dt, int steps, char* msg, int cap) {
+    return guarded(msg, cap, [&] {
+        ParticleSystem s = make_system(n, pos, vel, q, mass, box);
+        UnitsConfig u{kc, conv};
+        PropagatorSpec spec;
+        spec.force_field = std::make_shared<MsmField>(make_cfg(a, h, levels, 3, 2), u);
+        spec.dt = dt;
+        spec.steps_per_slice = steps;
+        ParticleSystem out = propagate(spec, s, u);
+        store_state(out, pos, vel);
+    });
+}
+
+// Runs the reference trajectory one Verlet step at a time (propagate with
+// steps_per_slice = 1; bitwise the same trajectory as one long call because
+// the re-evaluated initial force of each call is the same pure function of
+// the same state).  *steps_done = number of completed steps; on an exception
+// the state of the last completed step is kept and the error code returned.
+int ref_propagate_trace(int64_t n, double* pos, double* vel, const double* q,
+                        const double* mass, const double* box, double a, double h, int levels,
+                        double kc, double conv, double dt, int steps, int* steps_done,
+                        char* msg, int cap) {
+    *steps_done = 0;
+    ParticleSystem s = make_system(n, pos, vel, q, mass, box);
+    UnitsConfig u{kc, conv};
+    PropagatorSpec spec;
+    spec.force_field = std::make_shared<MsmField>(make_cfg(a, h, levels, 3, 2), u);
+    spec.dt = dt;
+    spec.steps_per_slice = 1;
+    int rc = OK;
+    for (int st = 0; st < steps; ++st) {
+        rc = guarded(msg, cap, [&] { s = propagate(spec, s, u); });
+        if (rc != OK) break;
+        *steps_done = st + 1;
+    }
+    store_state(s, pos, vel);
+    return rc;
+}
+
+// ---- parareal (src/parareal.cpp:94-239) -----------------------------------------
+// Runs parareal_init + k_iters x parareal_iterate on one window of t points
+// (no convergence logic) and returns the final lambda row (t+1 states, row
+// order n = 0..t) plus per-slice delta rms of the last iteration and the
+// evaluation counts [g_evals, f_evals, f_skipped].
+int ref_parareal_window(int64_t n, const double* pos, const double* vel, const double* q,
+                        const double* mass, const double* box, double fa, double fh, int fl,
+                        double fdt, int fsteps, double ga, double gh, int gl, double gdt,
+                        int gsteps, double kc, double conv, int t_points, int k_iters,
+                        int threads, double* row_pos, double* row_vel, double* delta_rms,
+                        int64_t* counts, char* msg, int cap) {
+    return guarded(msg, cap, [&] {
+        ParticleSystem s = make_system(n, pos, vel, q, mass, box);
+        UnitsConfig u{kc, conv};
+        PararealConfig cfg;
+        cfg.window_points = t_points;
+        cfg.max_iter = k_iters;
+        cfg.tol = 1e300;
+        cfg.units = u;
+        cfg.fine.force_field = std::make_shared<MsmField>(make_cfg(fa, fh, fl, 3, 2), u);
+        cfg.fine.dt = fdt;
+        cfg.fine.steps_per_slice = fsteps;
+        cfg.coarse.force_field = std::make_shared<MsmField>(make_cfg(ga, gh, gl, 3, 2), u);
+        cfg.coarse.dt = gdt;
+        cfg.coarse.steps_per_slice = gsteps;
+        cfg.short_circuit = false;
+        PararealWindow w = parareal_init(s, cfg);
+        std::unique_ptr<Executor> ex;
+        if (threads > 1)
+            ex = std::make_unique<AsyncExecutor>(threads);
+        else
+            ex = std::make_unique<SequentialExecutor>();
+        for (int k = 0; k < k_iters; ++k) parareal_iterate(w, cfg, *ex);
+        const auto& row = w.lambda.back();
+        for (int i = 0; i <= t_points; ++i)
+            store_state(row[i], row_pos ? row_pos + 3 * n * i : nullptr,
+                        row_vel ? row_vel + 3 * n * i : nullptr);
+        if (delta_rms)
+            for (int i = 1; i <= t_points; ++i) delta_rms[i] = w.delta_rows.back()[i].rms_pos;
+        if (counts) {
+            counts[0] = static_cast<int64_t>(w.counts.g_evals);
+            counts[1] = static_cast<int64_t>(w.counts.f_evals);
+            counts[2] = static_cast<int64_t>(w.counts.f_skipped);
+        }
+    });
+}
+
+// parareal_run with convergence / sliding windows.  traj_pos/vel receive
+// total_points states; counts = [g_evals, f_evals, f_skipped, windows, converged].
+int ref_parareal_run(int64_t n, const double* pos, const double* vel, const double* q,
+                     const double* mass, const double* box, double fa, double fh, int fl,
+                     double fdt, int fsteps, double ga, double gh, int gl, double gdt,
+                     int gsteps, double kc, double conv, int window, int max_iter, double tol,
+                     int short_circuit, double skip_threshold, int total_points, int threads,
+                     double* traj_pos, double* traj_vel, int64_t* counts, char* msg, int cap) {
+    return guarded(msg, cap, [&] {
+        ParticleSystem s = make_system(n, pos, vel, q, mass, box);
+        UnitsConfig u{kc, conv};
+        PararealConfig cfg;
+        cfg.window_points = window;
+        cfg.max_iter = max_iter;
+        cfg.tol = tol;
+        cfg.units = u;
+        cfg.fine.force_field = std::make_shared<MsmField>(make_cfg(fa, fh, fl, 3, 2), u);
+        cfg.fine.dt = fdt;
+        cfg.fine.steps_per_slice = fsteps;
+        cfg.coarse.force_field = std::make_shared<MsmField>(make_cfg(ga, gh, gl, 3, 2), u);
+        cfg.coarse.dt = gdt;
+        cfg.coarse.steps_per_slice = gsteps;
+        cfg.short_circuit = short_circuit != 0;
+        if (skip_threshold >= 0.0) cfg.skip_threshold = skip_threshold;
+        std::unique_ptr<Executor> ex;
+        if (threads > 1)
+            ex = std::make_unique<AsyncExecutor>(threads);
+        else
+            ex = std::make_unique<SequentialExecutor>();
+        PararealResult r;
+        try {
+            r = parareal_run(s, total_points, cfg, *ex);
+        } catch (const NonConvergenceError& e) {
+            if (counts) {
+                counts[0] = static_cast<int64_t>(e.report.counts.g_evals);
+                counts[1] = static_cast<int64_t>(e.report.counts.f_evals);
+                counts[2] = static_cast<int64_t>(e.report.counts.f_skipped);
+                counts[3] = e.report.windows;
+                counts[4] = 0;
+            }
+            throw;
+        }
+        for (int i = 0; i < total_points; ++i)
+            store_state(r.trajectory[i], traj_pos ? traj_pos + 3 * n * i : nullptr,
+                        traj_vel ? traj_vel + 3 * n * i : nullptr);
+        if (counts) {
+            counts[0] = static_cast<int64_t>(r.report.counts.g_evals);
+            counts[1] = static_cast<int64_t>(r.report.counts.f_evals);
+            counts[2] = static_cast<int64_t>(r.report.counts.f_skipped);
+            counts[3] = r.report.windows;
+            counts[4] = r.report.converged ? 1 : 0;
+        }
+    });
+}
+
+// ---- fixture generator (src/generate.cpp:40-93) ---------------------------------
+int ref_generate_random_system(int64_t n, const double* box, int scheme, double min_sep,
+                               uint64_t seed, double* pos, double* q, char* msg, int cap) {
+    return guarded(msg, cap, [&] {
+        ChargeScheme cs = scheme == 0   ? ChargeScheme::AllPlusOne
+                          : scheme == 1 ? ChargeScheme::Alternating
+                                        : ChargeScheme::RandomNeutral;
+        ParticleSystem s = generate_random_system(static_cast<std::size_t>(n),
+                                                  Vec3{box[0], box[1], box[2]}, cs, min_sep,
+                                                  seed);
+        store_state(s, pos, nullptr);
+        std::memcpy(q, s.charges.data(), static_cast<std::size_t>(n) * 8);
+    });
+}
+
+// ---- analytic flop model (src/cost_model.cpp:19-43), for the roofline cross-check
+double ref_msm_flops_general(double n, double box_l, double a, double h, double h_star) {
+    FlopParams p;
+    p.n = n;
+    p.box_l = box_l;
+    p.a = a;
+    p.h = h;
+    p.h_star = h_star;
+    return msm_flops_general(p).total;
+}
+
+double ref_msm_flops_simplified(double a, double h, double n) {
+    return msm_flops_simplified(a, h, n);
+}
+
+// Wall-clock seconds of `reps` reference short_range calls on the given atoms
+// (used by bench.py to time the reference's O(N^2) pair loop on a bounded sample).
+double ref_time_short_range(int64_t n, const double* pos, const double* q, double a, double kc,
+                            int reps) {
+    const double box[3] = {1, 1, 1};
+    ParticleSystem s = make_system(n, pos, nullptr, q, nullptr, box);
+    MsmConfig c;
+    c.cutoff_a = a;
+    UnitsConfig u{kc, 4.184e-4};
+    auto t0 = std::chrono::steady_clock::now();
+    double sink = 0.0;
+    for (int r = 0; r < reps; ++r) {
+        try {
+            ShortRangeResult res = short_range(s, c, u);
+            sink += res.potential.empty() ? 0.0 : res.potential[0];
+        } catch (const std::exception&) {
+            return -1.0;
+        }
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    if (sink == 12345.678) return -2.0;
+    return std::chrono::duration<double>(t1 - t0).count();
+}
+
+}  // extern "C"
