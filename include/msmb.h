@@ -1,0 +1,209 @@
+/*
+ * msmb.h -- C ABI of the B200-native MSM force / velocity-Verlet / parareal path.
+ *
+ * This is the drop-in boundary for the reference library `paramd`
+ * (arXiv 1309.1889, /root/reference/proj).  Each entry point names the
+ * reference interface it replaces (file:line, relative to /root/reference).
+ * Plain pointers and sizes only; the library owns device memory, the caller
+ * owns every host array.  Positions/velocities/forces are interleaved
+ * double[3*n] -- the layout of std::vector<paramd::Vec3>
+ * (include/paramd/vec3.hpp:6-7, a standard-layout {double x,y,z}), so
+ * `system.positions.data()` can be passed directly.
+ *
+ * Error codes map 1:1 to the reference exception hierarchy
+ * (include/paramd/errors.hpp:12-49, include/paramd/parareal.hpp:124-128); the
+ * message text and the particle indices match the reference's
+ * (src/msm_phases.cpp:25-26 and 238-239, include/paramd/msm_kernels.hpp:31,
+ * src/msm_grid.cpp:11-22, include/paramd/units.hpp:23-26,
+ * src/integrate.cpp:7-11, src/parareal.cpp:43-56 and 221-226) and are read
+ * back with msmb_last_error().  There is no CPU fallback: every compute entry
+ * point runs on the GPU and fails with MSMB_ERR_CUDA when none is usable.
+ */
+#ifndef MSMB_H
+#define MSMB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MSMB_ABI_VERSION 1
+
+/* Status codes == reference exception types. */
+enum msmb_status {
+    MSMB_OK = 0,
+    MSMB_ERR_CONFIG = 1,         /* paramd::ConfigError              errors.hpp:12-14 */
+    MSMB_ERR_DOMAIN = 2,         /* paramd::DomainError              errors.hpp:17-19 */
+    MSMB_ERR_COVERAGE = 3,       /* paramd::CoverageError            errors.hpp:37-39 */
+    MSMB_ERR_COINCIDENT = 4,     /* paramd::CoincidentParticlesError errors.hpp:32-34 */
+    MSMB_ERR_HIERARCHY = 5,      /* paramd::HierarchyError           errors.hpp:42-44 */
+    MSMB_ERR_RUNTIME = 6,        /* paramd::RuntimeFault             errors.hpp:47-49 */
+    MSMB_ERR_NONCONVERGENCE = 7, /* paramd::NonConvergenceError      parareal.hpp:124-128 */
+    MSMB_ERR_CUDA = 8,           /* no usable B200 / CUDA failure (no reference equivalent) */
+    MSMB_ERR_INTERNAL = 9
+};
+
+/* paramd::MsmConfig, include/paramd/msm_grid.hpp:10-18 (same defaults: 8, 2, 2, 3, 2). */
+typedef struct msmb_msm_config {
+    double cutoff_a;
+    double spacing_h;
+    int levels_l;
+    int interp_order_p;
+    int smoothing_m;
+} msmb_msm_config;
+
+/* paramd::UnitsConfig, include/paramd/units.hpp:16-27 (physical: 332.0636, 4.184e-4). */
+typedef struct msmb_units {
+    double coulomb_constant;
+    double energy_to_native;
+} msmb_units;
+
+/* One MSM force field bound to one GPU: the state of paramd::MsmField
+ * (include/paramd/force_field.hpp:62-73).  Owns device workspaces and a
+ * stream; calls on one handle are serialised internally, so a handle may be
+ * shared by threads the way the reference's AsyncExecutor shares a ForceField
+ * (src/parareal.cpp:27-33). */
+typedef struct msmb_field msmb_field;
+
+/* A device-resident ParticleSystem (include/paramd/system.hpp:10-18). */
+typedef struct msmb_system msmb_system;
+
+int msmb_abi_version(void);
+/* Number of usable CUDA devices (0 on a machine without a GPU). */
+int msmb_device_count(void);
+
+/* MsmField::MsmField(MsmConfig, UnitsConfig)  force_field.hpp:64.  Validates
+ * like MsmConfig::validate (src/msm_grid.cpp:11-22) and UnitsConfig::validate
+ * (units.hpp:23-26) before touching the GPU. */
+int msmb_create(const msmb_msm_config* cfg, const msmb_units* units, int device,
+                msmb_field** out);
+void msmb_destroy(msmb_field* f);
+
+/* MsmField::evaluate / msm_potential(s, cfg, units)  force_field.cpp:37-39,
+ * msm.cpp:52-90.  Host arrays; any output pointer may be NULL.
+ * phi = per-particle potential per unit charge, phi_short/phi_long its two
+ * halves (PotentialResult::short_part/long_part, potential.hpp:18-24). */
+int msmb_evaluate(msmb_field* f, int64_t n, const double* pos_xyz, const double* q,
+                  const double box[3], double* phi, double* phi_short, double* phi_long,
+                  double* force_xyz, double* energy);
+
+/* propagate(PropagatorSpec{field, dt, steps}, s, units)  integrate.cpp:13-36:
+ * one initial evaluation, then `steps` velocity-Verlet steps.  pos/vel are
+ * read and, on success, overwritten with the propagated state (on error they
+ * are left untouched, as the reference throws before returning). */
+int msmb_propagate(msmb_field* f, int64_t n, double* pos_xyz, double* vel_xyz, const double* q,
+                   const double* mass, const double box[3], double dt, int steps);
+
+/* propagate(spec, s, units) with an explicit UnitsConfig (the reference passes
+ * `units` separately from the field, integrate.hpp:27-28; energy_to_native
+ * converts the field's forces into accelerations).  units == NULL means the
+ * field's own units. */
+int msmb_propagate_ex(msmb_field* f, int64_t n, double* pos_xyz, double* vel_xyz, const double* q,
+                      const double* mass, const double box[3], double dt, int steps,
+                      const msmb_units* units);
+
+/* Page-locked host memory for fast transfers (cudaHostAlloc / cudaFreeHost). */
+void* msmb_host_alloc(int64_t bytes);
+void msmb_host_free(void* p);
+
+/* MsmField::cost_flops_per_step = msm_flops_simplified(a, h, n)
+ * force_field.cpp:41-43, cost_model.cpp:37-43. */
+double msmb_cost_flops_per_step(const msmb_field* f, int64_t n);
+
+/* Details of the last failure on this handle: kind = msmb_status, i/j the
+ * particle indices named by the message (-1 when none), step = the Verlet
+ * step whose evaluation failed (0 = the initial evaluation, -1 = n/a). */
+int msmb_last_error(const msmb_field* f, int* kind, int64_t* idx_i, int64_t* idx_j, int* step,
+                    char* msg, int cap);
+
+/* ---- device-resident systems (inputs stay in HBM across calls) ------------ */
+int msmb_system_create(msmb_field* f, int64_t n, const double* pos_xyz, const double* vel_xyz,
+                       const double* q, const double* mass, const double box[3],
+                       msmb_system** out);
+void msmb_system_destroy(msmb_system* s);
+int msmb_system_upload(msmb_system* s, const double* pos_xyz, const double* vel_xyz);
+int msmb_system_download(const msmb_system* s, double* pos_xyz, double* vel_xyz);
+int msmb_system_copy(msmb_system* dst, const msmb_system* src);
+/* In-place device-resident propagate (same semantics as msmb_propagate). */
+int msmb_system_propagate(msmb_field* f, msmb_system* s, double dt, int steps);
+/* Device-resident evaluate; outputs copied to the (optional) host arrays. */
+int msmb_system_evaluate(msmb_field* f, msmb_system* s, double* phi, double* phi_short,
+                         double* phi_long, double* force_xyz, double* energy);
+
+/* ---- parareal (src/parareal.cpp:94-239; include/paramd/parareal.hpp:40-144) -- */
+typedef struct msmb_propagator {
+    msmb_field* field; /* PropagatorSpec::force_field */
+    double dt;         /* PropagatorSpec::dt */
+    int steps_per_slice;
+} msmb_propagator;
+
+typedef struct msmb_parareal_config {
+    int window_points; /* T_W */
+    int max_iter;      /* K */
+    double tol;        /* RMS position tolerance */
+    msmb_propagator fine;
+    msmb_propagator coarse;
+    msmb_units units;
+    int has_skip_threshold; /* std::optional<double> skip_threshold */
+    double skip_threshold;
+    int short_circuit;
+} msmb_parareal_config;
+
+/* parareal_init(v, cfg) + k_iters x parareal_iterate(w, cfg): one window of
+ * t_points slices.  Returns the final lambda row (t_points+1 states,
+ * interleaved pos/vel per state, n = 0..t) and, optionally, the per-slice
+ * delta rms of the last iteration (t_points+1 entries, [0] unused) and the
+ * evaluation counts [g_evals, f_evals, f_skipped]. */
+int msmb_parareal_window(const msmb_parareal_config* cfg, int64_t n, const double* pos_xyz,
+                         const double* vel_xyz, const double* q, const double* mass,
+                         const double box[3], int t_points, int k_iters, double* row_pos,
+                         double* row_vel, double* delta_rms, int64_t* counts);
+
+/* parareal_run(v, total_points, cfg, exec)  parareal.cpp:182-239: sliding
+ * windows with RMS-position convergence.  traj_* receive total_points states
+ * (T_1..T_total).  report = [g_evals, f_evals, f_skipped, windows, converged]. */
+int msmb_parareal_run(const msmb_parareal_config* cfg, int64_t n, const double* pos_xyz,
+                      const double* vel_xyz, const double* q, const double* mass,
+                      const double box[3], int total_points, double* traj_pos,
+                      double* traj_vel, int64_t* report);
+
+/* ---- measurement ------------------------------------------------------------ */
+/* When enabled, every evaluation records CUDA events around each stage on the
+ * handle's stream (eager launches, no graph) and accumulates durations. */
+int msmb_set_stage_timing(msmb_field* f, int enable);
+/* Stage names/times (ms, summed since the last reset) and launch counts.
+ * Returns the number of stages (<= cap). */
+int msmb_stage_times(msmb_field* f, double* ms, int64_t* launches, const char** names, int cap);
+void msmb_reset_stage_times(msmb_field* f);
+/* Work counters of the most recent evaluation: [0] in-cutoff unordered pairs
+ * P_u, [1] candidate pair tests, [2] clusters, [3] clipped lattice taps
+ * (all levels except the top), [4] top-level taps, [5] kernel launches per
+ * evaluation. */
+int msmb_work_counters(msmb_field* f, int64_t* out, int cap);
+/* Kernel launches issued by this handle since creation. */
+int64_t msmb_kernel_launches(const msmb_field* f);
+
+/* Level geometry of the hierarchy built for `box` (src/msm_grid.cpp:24-54):
+ * dims[3*l], spacing[l], origin[3*l]. */
+int msmb_grid_geometry(const msmb_msm_config* cfg, const double box[3], int* dims,
+                       double* spacing, double* origin);
+
+/* Debug/parity hooks (tests only): per-level charge/potential lattices of the
+ * last evaluation on `f` (concatenated level 0..l-1), and the level-0 cell
+ * triple floor((x - origin) / h) of every particle (the reference's
+ * stencil_at base + 1, src/msm_phases.cpp:23). */
+int msmb_debug_levels(msmb_field* f, double* level_charge, double* level_potential);
+int msmb_debug_cells(msmb_field* f, int64_t n, const double* pos_xyz, const double box[3],
+                     int32_t* cells_xyz, int32_t* covered);
+/* Runs one stage kernel on caller lattices, for bitwise stage parity:
+ * stage 0 restrict (level k -> k+1), 1 lattice cutoff (level k),
+ * 2 top level, 3 prolongate (k+1 -> k, `out` holds the fine potential in/out),
+ * 4 interpolate (level-0 potential -> per-atom u, uses pos/n). */
+int msmb_debug_stage(msmb_field* f, int stage, int k, const double box[3], const double* in,
+                     double* out, int64_t n, const double* pos_xyz);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSMB_H */

@@ -1,0 +1,94 @@
+"""ctypes binding of lib/libmsmb.so (the C ABI declared in include/msmb.h).
+
+Loading fails loudly when the library is missing; there is no Python or CPU
+fallback for any compute entry point.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libmsmb.so"
+
+_D = C.POINTER(C.c_double)
+_L = C.POINTER(C.c_int64)
+_I = C.POINTER(C.c_int32)
+_VP = C.c_void_p
+
+
+class MsmConfigC(C.Structure):
+    _fields_ = [("cutoff_a", C.c_double), ("spacing_h", C.c_double), ("levels_l", C.c_int),
+                ("interp_order_p", C.c_int), ("smoothing_m", C.c_int)]
+
+
+class UnitsC(C.Structure):
+    _fields_ = [("coulomb_constant", C.c_double), ("energy_to_native", C.c_double)]
+
+
+class PropagatorC(C.Structure):
+    _fields_ = [("field", _VP), ("dt", C.c_double), ("steps_per_slice", C.c_int)]
+
+
+class PararealC(C.Structure):
+    _fields_ = [("window_points", C.c_int), ("max_iter", C.c_int), ("tol", C.c_double),
+                ("fine", PropagatorC), ("coarse", PropagatorC), ("units", UnitsC),
+                ("has_skip_threshold", C.c_int), ("skip_threshold", C.c_double),
+                ("short_circuit", C.c_int)]
+
+
+# name -> (restype, argtypes); mirrors include/msmb.h one to one
+SIGNATURES = {
+    "msmb_abi_version": (C.c_int, []),
+    "msmb_device_count": (C.c_int, []),
+    "msmb_create": (C.c_int, [C.POINTER(MsmConfigC), C.POINTER(UnitsC), C.c_int, C.POINTER(_VP)]),
+    "msmb_destroy": (None, [_VP]),
+    "msmb_evaluate": (C.c_int, [_VP, C.c_int64, _D, _D, _D, _D, _D, _D, _D, _D]),
+    "msmb_propagate": (C.c_int, [_VP, C.c_int64, _D, _D, _D, _D, _D, C.c_double, C.c_int]),
+    "msmb_propagate_ex": (C.c_int, [_VP, C.c_int64, _D, _D, _D, _D, _D, C.c_double, C.c_int,
+                                    C.POINTER(UnitsC)]),
+    "msmb_host_alloc": (_VP, [C.c_int64]),
+    "msmb_host_free": (None, [_VP]),
+    "msmb_cost_flops_per_step": (C.c_double, [_VP, C.c_int64]),
+    "msmb_last_error": (C.c_int, [_VP, C.POINTER(C.c_int), _L, _L, C.POINTER(C.c_int), C.c_char_p, C.c_int]),
+    "msmb_system_create": (C.c_int, [_VP, C.c_int64, _D, _D, _D, _D, _D, C.POINTER(_VP)]),
+    "msmb_system_destroy": (None, [_VP]),
+    "msmb_system_upload": (C.c_int, [_VP, _D, _D]),
+    "msmb_system_download": (C.c_int, [_VP, _D, _D]),
+    "msmb_system_copy": (C.c_int, [_VP, _VP]),
+    "msmb_system_propagate": (C.c_int, [_VP, _VP, C.c_double, C.c_int]),
+    "msmb_system_evaluate": (C.c_int, [_VP, _VP, _D, _D, _D, _D, _D]),
+    "msmb_parareal_window": (C.c_int, [C.POINTER(PararealC), C.c_int64, _D, _D, _D, _D, _D, C.c_int,
+                                       C.c_int, _D, _D, _D, _L]),
+    "msmb_parareal_run": (C.c_int, [C.POINTER(PararealC), C.c_int64, _D, _D, _D, _D, _D, C.c_int,
+                                    _D, _D, _L]),
+    "msmb_set_stage_timing": (C.c_int, [_VP, C.c_int]),
+    "msmb_stage_times": (C.c_int, [_VP, _D, _L, C.POINTER(C.c_char_p), C.c_int]),
+    "msmb_reset_stage_times": (None, [_VP]),
+    "msmb_work_counters": (C.c_int, [_VP, _L, C.c_int]),
+    "msmb_kernel_launches": (C.c_int64, [_VP]),
+    "msmb_grid_geometry": (C.c_int, [C.POINTER(MsmConfigC), _D, _I, _D, _D]),
+    "msmb_debug_levels": (C.c_int, [_VP, _D, _D]),
+    "msmb_debug_cells": (C.c_int, [_VP, C.c_int64, _D, _D, _I, _I]),
+    "msmb_debug_stage": (C.c_int, [_VP, C.c_int, C.c_int, _D, _D, _D, C.c_int64, _D]),
+}
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                               "(there is no CPU fallback)")
+        L = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return list(SIGNATURES)

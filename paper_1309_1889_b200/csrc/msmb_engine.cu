@@ -1,0 +1,904 @@
+// Host engine + C ABI (include/msmb.h).
+//
+// One msmb_field == one paramd::MsmField (include/paramd/force_field.hpp:62-73)
+// bound to one GPU.  An evaluation is a fixed sequence of sm_100a kernels on the
+// field's stream (see msmb_kernels.cu for the stage map); a velocity-Verlet
+// propagate (src/integrate.cpp:13-36) is the initial evaluation followed by
+// `steps` replays of a CUDA graph holding {kick(+kick)+drift, evaluation}.
+// Errors are detected on the device (ErrRec) and surface after the call with
+// the reference's exception type, message and particle indices; kernels of a
+// failed evaluation and of every later step become no-ops, so the state a
+// caller gets back on error is the untouched input (the reference throws).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "msmb_engine.cuh"
+
+namespace msmb {
+
+size_t conv_smem_bytes(const ConvTable& t);
+cudaError_t conv_prepare(size_t bytes);
+
+struct CudaErr : std::runtime_error {
+    cudaError_t code;
+    CudaErr(cudaError_t c, const std::string& w) : std::runtime_error(w), code(c) {}
+};
+
+static void ck(cudaError_t e, const char* where) {
+    if (e != cudaSuccess) throw CudaErr(e, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+Workspace::~Workspace() {
+    if (gx_eval) cudaGraphExecDestroy(gx_eval);
+    if (gx_step1) cudaGraphExecDestroy(gx_step1);
+    if (gx_step2) cudaGraphExecDestroy(gx_step2);
+    if (err) cudaFree(err);
+    if (err_host) cudaFreeHost(err_host);
+}
+
+// ---- stage timer ------------------------------------------------------------------
+int StageTimer::stage_index(const char* name) {
+    for (size_t i = 0; i < names.size(); ++i)
+        if (names[i] == name) return int(i);
+    names.emplace_back(name);
+    ms.push_back(0.0);
+    launches.push_back(0);
+    return int(names.size() - 1);
+}
+
+cudaEvent_t StageTimer::ev() {
+    if (!pool.empty()) {
+        cudaEvent_t e = pool.back();
+        pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void StageTimer::resolve() {
+    for (auto& p : pending) {
+        float t = 0.f;
+        if (cudaEventSynchronize(p.b) == cudaSuccess && cudaEventElapsedTime(&t, p.a, p.b) == cudaSuccess)
+            ms[p.stage] += t;
+        launches[p.stage] += p.nl;
+        pool.push_back(p.a);
+        pool.push_back(p.b);
+    }
+    pending.clear();
+}
+
+StageTimer::~StageTimer() {
+    for (auto& p : pending) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    for (auto e : pool) cudaEventDestroy(e);
+}
+
+// ---- errors -----------------------------------------------------------------------
+int engine_set_error(msmb_field* f, const Error& e) {
+    f->last = e;
+    return e.kind;
+}
+
+int cuda_fail(msmb_field* f, cudaError_t e, const char* where) {
+    Error er;
+    er.kind = MSMB_ERR_CUDA;
+    er.msg = std::string(where) + ": " + cudaGetErrorString(e);
+    if (f) f->last = er;
+    return MSMB_ERR_CUDA;
+}
+
+static Error error_from_rec(const ErrRec& r) {
+    Error e;
+    e.kind = r.kind;
+    e.step = r.step;
+    e.i = r.err_i;
+    e.j = r.err_j;
+    char buf[256];
+    switch (r.kind) {
+        case MSMB_ERR_COVERAGE:
+            snprintf(buf, sizeof buf, "particle %lld outside grid coverage", (long long)r.err_i);
+            e.msg = buf;
+            break;
+        case MSMB_ERR_COINCIDENT:
+            snprintf(buf, sizeof buf, "particles %lld and %lld coincide", (long long)r.err_i,
+                     (long long)r.err_j);
+            e.msg = buf;
+            break;
+        case MSMB_ERR_DOMAIN:
+            e.msg = "kernel_g_star: r must be > 0";
+            break;
+        default:
+            e.msg = "internal error";
+    }
+    return e;
+}
+
+// ---- workspace --------------------------------------------------------------------
+template <class T>
+static T* walloc(Workspace& W, size_t count) {
+    auto b = std::make_unique<DBuf>();
+    ck(b->alloc(sizeof(T) * (count ? count : 1)), "cudaMalloc");
+    T* p = b->as<T>();
+    W.bufs.push_back(std::move(b));
+    return p;
+}
+
+template <class T>
+static T* wupload(Workspace& W, const std::vector<T>& v) {
+    T* p = walloc<T>(W, v.size());
+    if (!v.empty()) ck(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice), "upload");
+    return p;
+}
+
+static void alloc_plist(Workspace& W, int cap) {
+    W.cap = cap;
+    ck(W.plist_buf.alloc(sizeof(int) * size_t(W.maxclu) * size_t(cap)), "cudaMalloc plist");
+    W.c.plist = W.plist_buf.as<int>();
+}
+
+static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const double* box,
+                                                 Error& e) {
+    auto W = std::make_unique<Workspace>();
+    e = build_geometry(f->cfg, f->units, box, n, W->g);
+    if (e.kind) return nullptr;
+    Geometry& g = W->g;
+    W->n = n;
+    const size_t N = size_t(n > 0 ? n : 1);
+    DevAtoms& a = W->a;
+    a.key = walloc<int>(*W, N);
+    a.rank = walloc<int>(*W, N);
+    a.perm = walloc<int>(*W, N);
+    a.outlist = walloc<int>(*W, N);
+    a.xs = walloc<double>(*W, N);
+    a.ys = walloc<double>(*W, N);
+    a.zs = walloc<double>(*W, N);
+    a.qs = walloc<double>(*W, N);
+    a.f4 = walloc<float4>(*W, N);
+    a.aw = walloc<double>(*W, N * 12);
+    a.phis = walloc<double>(*W, N);
+    a.fsx = walloc<double>(*W, N);
+    a.fsy = walloc<double>(*W, N);
+    a.fsz = walloc<double>(*W, N);
+    DevCells& c = W->c;
+    c.count = walloc<int>(*W, size_t(g.ncells + 1));
+    c.start = walloc<int>(*W, size_t(g.ncells + 1));
+    c.col_cnt = walloc<int>(*W, size_t(g.ncols + 1));
+    c.col_off = walloc<int>(*W, size_t(g.ncols + 1));
+    W->maxclu = n / 32 + g.ncols + 1;
+    c.clu = walloc<int2>(*W, size_t(W->maxclu));
+    c.blo = walloc<float4>(*W, size_t(W->maxclu));
+    c.bhi = walloc<float4>(*W, size_t(W->maxclu));
+    c.nclu = walloc<int>(*W, 1);
+    c.pcnt = walloc<int>(*W, size_t(W->maxclu));
+    c.scan_tmp = walloc<int>(*W, size_t((std::max(g.ncells, g.ncols) + 1 + 4095) / 4096 + 8));
+    ck(cudaMemset(c.nclu, 0, sizeof(int)), "memset");
+    alloc_plist(*W, g.pair_cap);
+    DevLevels& L = W->L;
+    L.charge = walloc<double>(*W, g.lattice_total);
+    L.pot = walloc<double>(*W, g.lattice_total);
+    for (int k = 0; k + 1 < g.levels; ++k)
+        for (int ax = 0; ax < 3; ++ax) {
+            const TransferAxis& T = g.tr[k][ax];
+            L.tr_base[k][ax] = wupload(*W, T.base);
+            L.tr_w[k][ax] = wupload(*W, T.w);
+            L.tr_rcnt[k][ax] = wupload(*W, T.rcnt);
+            L.tr_ridx[k][ax] = wupload(*W, T.ridx);
+            L.tr_rw[k][ax] = wupload(*W, T.rw);
+        }
+    size_t smem = 0;
+    for (int k = 0; k < g.levels; ++k) {
+        const ConvTable& t = (k == g.levels - 1) ? g.top : g.lattice[k];
+        std::vector<int4> rows(t.rows.size());
+        for (size_t i = 0; i < rows.size(); ++i)
+            rows[i] = make_int4(t.rows[i].dx, t.rows[i].dy, t.rows[i].m, t.rows[i].tap_off);
+        L.rows[k] = wupload(*W, rows);
+        L.dxb[k] = wupload(*W, t.dx_begin);
+        L.taps[k] = wupload(*W, t.taps);
+        smem = std::max(smem, conv_smem_bytes(t));
+    }
+    if (smem > 227 * 1024) {
+        e.kind = MSMB_ERR_CONFIG;
+        e.msg = "msm: top level of " + std::to_string(g.lv[g.levels - 1].size) +
+                " points exceeds this build's shared-memory stencil tile";
+        return nullptr;
+    }
+    ck(conv_prepare(smem), "cudaFuncSetAttribute");
+    DevOut& o = W->o;
+    o.fx = walloc<double>(*W, N);
+    o.fy = walloc<double>(*W, N);
+    o.fz = walloc<double>(*W, N);
+    o.phi = walloc<double>(*W, N);
+    o.phis = walloc<double>(*W, N);
+    o.phil = walloc<double>(*W, N);
+    o.e = walloc<double>(*W, N);
+    o.partial = walloc<double>(*W, size_t(reduce_blocks(n)));
+    o.energy = walloc<double>(*W, 1);
+    ck(W->backup.alloc(sizeof(double) * 6 * N), "cudaMalloc backup");
+    ck(W->staging.alloc(sizeof(double) * 3 * N), "cudaMalloc staging");
+    ck(cudaMalloc(&W->err, sizeof(ErrRec)), "cudaMalloc err");
+    ck(cudaMallocHost(&W->err_host, sizeof(ErrRec)), "cudaMallocHost err");
+    return W;
+}
+
+static Error ensure_workspace(msmb_field* f, int64_t n, const double* box) {
+    Error e;
+    if (f->ws && f->ws->n == n && f->ws->g.box[0] == box[0] && f->ws->g.box[1] == box[1] &&
+        f->ws->g.box[2] == box[2])
+        return e;
+    f->ws.reset();
+    f->ws = make_workspace(f, n, box, e);
+    return e;
+}
+
+// ---- one evaluation ------------------------------------------------------------------
+struct StageScope {
+    msmb_field* f;
+    int stage = -1;
+    cudaEvent_t a = nullptr;
+    StageScope(msmb_field* ff, const char* name) : f(ff) {
+        if (!f->timer.on) return;
+        stage = f->timer.stage_index(name);
+        a = f->timer.ev();
+        cudaEventRecord(a, f->stream);
+    }
+    void done(int nl) {
+        f->launches += nl;
+        if (stage < 0) return;
+        cudaEvent_t b = f->timer.ev();
+        cudaEventRecord(b, f->stream);
+        f->timer.pending.push_back({stage, a, b, nl});
+    }
+};
+
+static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs) {
+    cudaStream_t st = f->stream;
+    const Geometry& g = W.g;
+    int total = 0;
+    auto run = [&](const char* name, auto&& fn) {
+        StageScope sc(f, name);
+        const int nl = fn();
+        sc.done(nl);
+        total += nl;
+    };
+    run("bin", [&] { return launch_bin(st, g, s, W.a, W.c, W.err); });
+    run("sort", [&] { return launch_sort(st, g, s, W.a, W.c, W.err); });
+    run("clusters", [&] { return launch_clusters(st, g, s.n, W.a, W.c, W.err, W.cap); });
+    run("pairs", [&] { return launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap); });
+    run("anterp", [&] { return launch_anterp(st, g, W.a, W.c, W.L, W.err); });
+    run("restrict", [&] {
+        int l = 0;
+        for (int k = 0; k + 1 < g.levels; ++k) l += launch_restrict(st, g, k, W.L, W.err);
+        return l;
+    });
+    run("lattice", [&] { return launch_lattice(st, g, W.L, W.err); });
+    run("top", [&] { return launch_top(st, g, W.L, W.err); });
+    run("prolong", [&] {
+        int l = 0;
+        for (int k = g.levels - 2; k >= 0; --k) l += launch_prolong(st, g, k, W.L, W.err);
+        return l;
+    });
+    DevOut o = W.o;
+    if (!outputs) o.phi = o.phis = o.phil = o.e = nullptr;
+    run("interp", [&] { return launch_interp(st, g, s.n, W.a, W.c, W.L, o, W.err, outputs ? 1 : 0); });
+    run("finalize", [&] { return launch_finalize(st, s, W.err); });
+    return total;
+}
+
+static ErrRec read_err(msmb_field* f, Workspace& W) {
+    ck(cudaMemcpyAsync(W.err_host, W.err, sizeof(ErrRec), cudaMemcpyDeviceToHost, f->stream),
+       "read err");
+    ck(cudaStreamSynchronize(f->stream), "cudaStreamSynchronize");
+    f->timer.resolve();
+    return *W.err_host;
+}
+
+static void record_counters(msmb_field* f, const Workspace& W, const ErrRec& r) {
+    f->counters[0] = int64_t(r.pairs / 2);
+    f->counters[1] = int64_t(r.candidates);
+    int nclu = 0;
+    cudaMemcpy(&nclu, W.c.nclu, sizeof(int), cudaMemcpyDeviceToHost);
+    f->counters[2] = nclu;
+    f->counters[3] = W.g.lattice_taps_clipped;
+    f->counters[4] = W.g.top_taps;
+    f->counters[5] = W.launches_eval;
+}
+
+static void grow_cap(Workspace& W, const ErrRec& r) {
+    const int need = std::max(r.overflow, W.cap);
+    const int cap = std::max(need + need / 4 + 32, W.cap * 2);
+    alloc_plist(W, cap);
+}
+
+// Evaluate the system in `s` (device), outputs left in W.o.
+static int eval_device(msmb_field* f, StateBuf& sb, bool outputs) {
+    Error e = ensure_workspace(f, sb.n, sb.box);
+    if (e.kind) return engine_set_error(f, e);
+    Workspace& W = *f->ws;
+    DevState s = sb.dev();
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        f->launches += launch_reset_err(f->stream, W.err, 0);
+        W.launches_eval = enqueue_eval(f, W, s, outputs);
+        ck(cudaGetLastError(), "kernel launch");
+        const ErrRec r = read_err(f, W);
+        if (r.kind == kOverflowKind) {
+            grow_cap(W, r);
+            continue;
+        }
+        record_counters(f, W, r);
+        if (r.kind) return engine_set_error(f, error_from_rec(r));
+        return MSMB_OK;
+    }
+    return engine_set_error(f, Error{MSMB_ERR_INTERNAL, -1, -1, -1, "pair list did not converge"});
+}
+
+static void destroy_graphs(Workspace& W) {
+    if (W.gx_eval) cudaGraphExecDestroy(W.gx_eval);
+    if (W.gx_step1) cudaGraphExecDestroy(W.gx_step1);
+    if (W.gx_step2) cudaGraphExecDestroy(W.gx_step2);
+    W.gx_eval = W.gx_step1 = W.gx_step2 = nullptr;
+    W.graph_key = nullptr;
+}
+
+template <class Fn>
+static cudaGraphExec_t capture(msmb_field* f, Fn&& fn) {
+    cudaGraph_t graph;
+    ck(cudaStreamBeginCapture(f->stream, cudaStreamCaptureModeThreadLocal), "BeginCapture");
+    fn();
+    ck(cudaStreamEndCapture(f->stream, &graph), "EndCapture");
+    cudaGraphExec_t ex;
+    ck(cudaGraphInstantiate(&ex, graph, 0), "GraphInstantiate");
+    cudaGraphDestroy(graph);
+    return ex;
+}
+
+int engine_propagate(msmb_field* f, StateBuf& sb, double dt, int steps, double conv) {
+    if (!(dt > 0.0)) return engine_set_error(f, Error{MSMB_ERR_CONFIG, -1, -1, -1, "dt must be > 0"});
+    if (steps < 1)
+        return engine_set_error(f, Error{MSMB_ERR_CONFIG, -1, -1, -1, "steps_per_slice must be >= 1"});
+    Error e = validate_units(f->units);
+    if (e.kind) return engine_set_error(f, e);
+    e = ensure_workspace(f, sb.n, sb.box);
+    if (e.kind) return engine_set_error(f, e);
+    Workspace& W = *f->ws;
+    DevState s = sb.dev();
+    const size_t N = size_t(sb.n > 0 ? sb.n : 1);
+    double* bk = W.backup.as<double>();
+    // keep the input state: restored on error and on pair-list retries
+    ck(cudaMemcpyAsync(bk, s.x, sizeof(double) * 6 * N, cudaMemcpyDeviceToDevice, f->stream), "backup");
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        const bool graphs = !f->timer.on;
+        if (graphs && (W.graph_key != s.x || W.graph_dt != dt || W.graph_cap != W.cap)) {
+            destroy_graphs(W);
+            int nl = 0;
+            W.gx_eval = capture(f, [&] { nl = enqueue_eval(f, W, s, false); });
+            W.launches_eval = nl;
+            W.gx_step1 = capture(f, [&] {
+                nl = launch_kick_drift(f->stream, s, W.o, dt, conv, 1, W.err);
+                nl += enqueue_eval(f, W, s, false);
+            });
+            W.gx_step2 = capture(f, [&] {
+                nl = launch_kick_drift(f->stream, s, W.o, dt, conv, 2, W.err);
+                nl += enqueue_eval(f, W, s, false);
+            });
+            W.launches_step = nl;
+            f->launches -= 3 * int64_t(W.launches_eval); // captures are not launches
+            W.graph_key = s.x;
+            W.graph_dt = dt;
+            W.graph_cap = W.cap;
+        }
+        f->launches += launch_reset_err(f->stream, W.err, 0);
+        if (graphs) {
+            ck(cudaGraphLaunch(W.gx_eval, f->stream), "GraphLaunch");
+            f->launches += W.launches_eval;
+            for (int st = 1; st <= steps; ++st) {
+                ck(cudaGraphLaunch(st == 1 ? W.gx_step1 : W.gx_step2, f->stream), "GraphLaunch");
+                f->launches += W.launches_step;
+            }
+        } else {
+            enqueue_eval(f, W, s, false);
+            for (int st = 1; st <= steps; ++st) {
+                StageScope sc(f, "verlet");
+                sc.done(launch_kick_drift(f->stream, s, W.o, dt, conv, st == 1 ? 1 : 2, W.err));
+                enqueue_eval(f, W, s, false);
+            }
+        }
+        {
+            StageScope sc(f, "verlet");
+            sc.done(launch_kick(f->stream, s, W.o, dt, conv, W.err));
+        }
+        ck(cudaGetLastError(), "kernel launch");
+        const ErrRec r = read_err(f, W);
+        if (r.kind == kOverflowKind || r.kind) {
+            ck(cudaMemcpyAsync(s.x, bk, sizeof(double) * 6 * N, cudaMemcpyDeviceToDevice, f->stream),
+               "restore");
+            ck(cudaStreamSynchronize(f->stream), "sync");
+        }
+        if (r.kind == kOverflowKind) {
+            grow_cap(W, r);
+            continue;
+        }
+        record_counters(f, W, r);
+        if (r.kind) return engine_set_error(f, error_from_rec(r));
+        return MSMB_OK;
+    }
+    return engine_set_error(f, Error{MSMB_ERR_INTERNAL, -1, -1, -1, "pair list did not converge"});
+}
+
+// ---- host <-> device state ------------------------------------------------------------
+static void upload_vec3(msmb_field* f, const double* host, double* x, double* y, double* z,
+                        int64_t n, Workspace* W, DBuf& tmp) {
+    if (n == 0) return;
+    double* stg;
+    if (W && W->staging.bytes >= sizeof(double) * 3 * size_t(n))
+        stg = W->staging.as<double>();
+    else {
+        if (tmp.bytes < sizeof(double) * 3 * size_t(n)) ck(tmp.alloc(sizeof(double) * 3 * size_t(n)), "alloc");
+        stg = tmp.as<double>();
+    }
+    ck(cudaMemcpyAsync(stg, host, sizeof(double) * 3 * size_t(n), cudaMemcpyHostToDevice, f->stream), "H2D");
+    f->launches += launch_aos_to_soa(f->stream, n, stg, x, y, z);
+}
+
+static void download_vec3(msmb_field* f, double* host, const double* x, const double* y,
+                          const double* z, int64_t n, Workspace* W, DBuf& tmp) {
+    if (n == 0 || !host) return;
+    double* stg;
+    if (W && W->staging.bytes >= sizeof(double) * 3 * size_t(n))
+        stg = W->staging.as<double>();
+    else {
+        if (tmp.bytes < sizeof(double) * 3 * size_t(n)) ck(tmp.alloc(sizeof(double) * 3 * size_t(n)), "alloc");
+        stg = tmp.as<double>();
+    }
+    f->launches += launch_soa_to_aos(f->stream, n, x, y, z, stg);
+    ck(cudaMemcpyAsync(host, stg, sizeof(double) * 3 * size_t(n), cudaMemcpyDeviceToHost, f->stream), "D2H");
+}
+
+static int fill_state(msmb_field* f, StateBuf& sb, int64_t n, const double* pos, const double* vel,
+                      const double* q, const double* mass, const double* box) {
+    if (sb.n != n || !sb.buf.p) ck(sb.alloc(n), "cudaMalloc state");
+    for (int ax = 0; ax < 3; ++ax) sb.box[ax] = box[ax];
+    DevState s = sb.dev();
+    DBuf tmp;
+    Workspace* W = (f->ws && f->ws->n == n) ? f->ws.get() : nullptr;
+    upload_vec3(f, pos, s.x, s.y, s.z, n, W, tmp);
+    if (vel)
+        upload_vec3(f, vel, s.vx, s.vy, s.vz, n, W, tmp);
+    else if (n)
+        ck(cudaMemsetAsync(s.vx, 0, sizeof(double) * 3 * size_t(n), f->stream), "memset");
+    if (n) ck(cudaMemcpyAsync(s.q, q, sizeof(double) * size_t(n), cudaMemcpyHostToDevice, f->stream), "H2D q");
+    if (n && mass)
+        ck(cudaMemcpyAsync(s.m, mass, sizeof(double) * size_t(n), cudaMemcpyHostToDevice, f->stream), "H2D m");
+    ck(cudaStreamSynchronize(f->stream), "sync");
+    return MSMB_OK;
+}
+
+static void copy_outputs(msmb_field* f, int64_t n, double* phi, double* phi_short, double* phi_long,
+                         double* force, double* energy) {
+    Workspace& W = *f->ws;
+    DBuf tmp;
+    auto d2h = [&](double* h, const double* d) {
+        if (h && n) ck(cudaMemcpyAsync(h, d, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, f->stream), "D2H");
+    };
+    d2h(phi, W.o.phi);
+    d2h(phi_short, W.o.phis);
+    d2h(phi_long, W.o.phil);
+    if (force) download_vec3(f, force, W.o.fx, W.o.fy, W.o.fz, n, &W, tmp);
+    if (energy) {
+        if (n)
+            ck(cudaMemcpyAsync(energy, W.o.energy, sizeof(double), cudaMemcpyDeviceToHost, f->stream), "D2H");
+        else
+            *energy = 0.0;
+    }
+    ck(cudaStreamSynchronize(f->stream), "sync");
+}
+
+} // namespace msmb
+
+using namespace msmb;
+
+// =======================================================================================
+// C ABI
+// =======================================================================================
+#define GUARD_BEGIN try {
+#define GUARD_END(f)                                                                     \
+    }                                                                                    \
+    catch (const CudaErr& ex) {                                                          \
+        Error er;                                                                        \
+        er.kind = MSMB_ERR_CUDA;                                                         \
+        er.msg = ex.what();                                                              \
+        if (f) (f)->last = er;                                                           \
+        return MSMB_ERR_CUDA;                                                            \
+    }                                                                                    \
+    catch (const std::exception& ex) {                                                   \
+        Error er;                                                                        \
+        er.kind = MSMB_ERR_INTERNAL;                                                     \
+        er.msg = ex.what();                                                              \
+        if (f) (f)->last = er;                                                           \
+        return MSMB_ERR_INTERNAL;                                                        \
+    }
+
+static thread_local Error g_create_error;
+
+extern "C" {
+
+int msmb_abi_version(void) { return MSMB_ABI_VERSION; }
+
+int msmb_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int msmb_create(const msmb_msm_config* cfg, const msmb_units* units, int device, msmb_field** out) {
+    *out = nullptr;
+    Error e = validate_config(*cfg);
+    if (!e.kind) e = validate_units(*units);
+    if (e.kind) {
+        g_create_error = e;
+        return e.kind;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0 || device < 0 || device >= ndev) {
+        g_create_error = Error{MSMB_ERR_CUDA, -1, -1, -1, "no usable CUDA device (this library has no CPU fallback)"};
+        return MSMB_ERR_CUDA;
+    }
+    cudaDeviceProp prop;
+    cudaGetDeviceProperties(&prop, device);
+    if (prop.major < 10) {
+        g_create_error = Error{MSMB_ERR_CUDA, -1, -1, -1,
+                               std::string("device ") + prop.name + " is not sm_100 (B200); this build targets sm_100a only"};
+        return MSMB_ERR_CUDA;
+    }
+    auto* f = new msmb_field();
+    f->cfg = *cfg;
+    f->units = *units;
+    f->device = device;
+    cudaSetDevice(device);
+    if (cudaStreamCreateWithFlags(&f->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete f;
+        g_create_error = Error{MSMB_ERR_CUDA, -1, -1, -1, "cudaStreamCreate failed"};
+        return MSMB_ERR_CUDA;
+    }
+    *out = f;
+    return MSMB_OK;
+}
+
+void msmb_destroy(msmb_field* f) {
+    if (!f) return;
+    cudaSetDevice(f->device);
+    cudaStreamSynchronize(f->stream);
+    f->ws.reset();
+    f->scratch.buf.reset();
+    cudaStreamDestroy(f->stream);
+    delete f;
+}
+
+int msmb_last_error(const msmb_field* f, int* kind, int64_t* idx_i, int64_t* idx_j, int* step,
+                    char* msg, int cap) {
+    const Error& e = f ? f->last : g_create_error;
+    if (kind) *kind = e.kind;
+    if (idx_i) *idx_i = e.i;
+    if (idx_j) *idx_j = e.j;
+    if (step) *step = e.step;
+    if (msg && cap > 0) {
+        strncpy(msg, e.msg.c_str(), size_t(cap - 1));
+        msg[cap - 1] = 0;
+    }
+    return e.kind;
+}
+
+double msmb_cost_flops_per_step(const msmb_field* f, int64_t n) {
+    return host_flops_simplified(f->cfg.cutoff_a, f->cfg.spacing_h, double(n));
+}
+
+int msmb_evaluate(msmb_field* f, int64_t n, const double* pos_xyz, const double* q,
+                  const double box[3], double* phi, double* phi_short, double* phi_long,
+                  double* force_xyz, double* energy) {
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    GUARD_BEGIN
+    f->last = Error{};
+    cudaSetDevice(f->device);
+    Error e = validate_config(f->cfg);
+    if (!e.kind) e = validate_units(f->units);
+    if (e.kind) return engine_set_error(f, e);
+    e = ensure_workspace(f, n, box);
+    if (e.kind) return engine_set_error(f, e);
+    fill_state(f, f->scratch, n, pos_xyz, nullptr, q, nullptr, box);
+    const int rc = eval_device(f, f->scratch, true);
+    if (rc) return rc;
+    copy_outputs(f, n, phi, phi_short, phi_long, force_xyz, energy);
+    return MSMB_OK;
+    GUARD_END(f)
+}
+
+int msmb_propagate_ex(msmb_field* f, int64_t n, double* pos_xyz, double* vel_xyz, const double* q,
+                      const double* mass, const double box[3], double dt, int steps,
+                      const msmb_units* units) {
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    GUARD_BEGIN
+    f->last = Error{};
+    cudaSetDevice(f->device);
+    // PropagatorSpec::validate (src/integrate.cpp:7-11), then UnitsConfig::validate
+    if (!(dt > 0.0)) return engine_set_error(f, Error{MSMB_ERR_CONFIG, -1, -1, -1, "dt must be > 0"});
+    if (steps < 1)
+        return engine_set_error(f, Error{MSMB_ERR_CONFIG, -1, -1, -1, "steps_per_slice must be >= 1"});
+    const msmb_units u = units ? *units : f->units;
+    Error e = validate_units(u);
+    if (e.kind) return engine_set_error(f, e);
+    e = ensure_workspace(f, n, box);
+    if (e.kind) return engine_set_error(f, e);
+    fill_state(f, f->scratch, n, pos_xyz, vel_xyz, q, mass, box);
+    const int rc = engine_propagate(f, f->scratch, dt, steps, u.energy_to_native);
+    if (rc) return rc;
+    DBuf tmp;
+    DevState s = f->scratch.dev();
+    download_vec3(f, pos_xyz, s.x, s.y, s.z, n, f->ws.get(), tmp);
+    ck(cudaStreamSynchronize(f->stream), "sync");
+    download_vec3(f, vel_xyz, s.vx, s.vy, s.vz, n, f->ws.get(), tmp);
+    ck(cudaStreamSynchronize(f->stream), "sync");
+    return MSMB_OK;
+    GUARD_END(f)
+}
+
+int msmb_propagate(msmb_field* f, int64_t n, double* pos_xyz, double* vel_xyz, const double* q,
+                   const double* mass, const double box[3], double dt, int steps) {
+    return msmb_propagate_ex(f, n, pos_xyz, vel_xyz, q, mass, box, dt, steps, nullptr);
+}
+
+void* msmb_host_alloc(int64_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, size_t(bytes > 0 ? bytes : 8), cudaHostAllocDefault) != cudaSuccess) return nullptr;
+    return p;
+}
+
+void msmb_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+int msmb_system_create(msmb_field* f, int64_t n, const double* pos_xyz, const double* vel_xyz,
+                       const double* q, const double* mass, const double box[3], msmb_system** out) {
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    *out = nullptr;
+    GUARD_BEGIN
+    cudaSetDevice(f->device);
+    auto* s = new msmb_system();
+    s->f = f;
+    fill_state(f, s->st, n, pos_xyz, vel_xyz, q, mass, box);
+    *out = s;
+    return MSMB_OK;
+    GUARD_END(f)
+}
+
+void msmb_system_destroy(msmb_system* s) {
+    if (!s) return;
+    std::lock_guard<std::recursive_mutex> lk(s->f->mu);
+    cudaSetDevice(s->f->device);
+    cudaStreamSynchronize(s->f->stream);
+    if (s->f->ws && s->f->ws->graph_key == s->st.dev().x) destroy_graphs(*s->f->ws);
+    delete s;
+}
+
+int msmb_system_upload(msmb_system* s, const double* pos_xyz, const double* vel_xyz) {
+    msmb_field* f = s->f;
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    GUARD_BEGIN
+    cudaSetDevice(f->device);
+    DevState d = s->st.dev();
+    DBuf tmp;
+    Workspace* W = (f->ws && f->ws->n == s->st.n) ? f->ws.get() : nullptr;
+    if (pos_xyz) upload_vec3(f, pos_xyz, d.x, d.y, d.z, s->st.n, W, tmp);
+    if (vel_xyz) upload_vec3(f, vel_xyz, d.vx, d.vy, d.vz, s->st.n, W, tmp);
+    ck(cudaStreamSynchronize(f->stream), "sync");
+    return MSMB_OK;
+    GUARD_END(f)
+}
+
+int msmb_system_download(const msmb_system* s, double* pos_xyz, double* vel_xyz) {
+    msmb_field* f = s->f;
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    GUARD_BEGIN
+    cudaSetDevice(f->device);
+    DevState d = s->st.dev();
+    DBuf tmp;
+    Workspace* W = (f->ws && f->ws->n == s->st.n) ? f->ws.get() : nullptr;
+    download_vec3(f, pos_xyz, d.x, d.y, d.z, s->st.n, W, tmp);
+    ck(cudaStreamSynchronize(f->stream), "sync");
+    download_vec3(f, vel_xyz, d.vx, d.vy, d.vz, s->st.n, W, tmp);
+    ck(cudaStreamSynchronize(f->stream), "sync");
+    return MSMB_OK;
+    GUARD_END(f)
+}
+
+int msmb_system_copy(msmb_system* dst, const msmb_system* src) {
+    msmb_field* f = dst->f;
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    GUARD_BEGIN
+    cudaSetDevice(f->device);
+    if (dst->st.n != src->st.n) ck(dst->st.alloc(src->st.n), "alloc");
+    for (int ax = 0; ax < 3; ++ax) dst->st.box[ax] = src->st.box[ax];
+    ck(cudaMemcpyAsync(dst->st.buf.p, src->st.buf.p, src->st.buf.bytes, cudaMemcpyDeviceToDevice,
+                       f->stream),
+       "copy");
+    ck(cudaStreamSynchronize(f->stream), "sync");
+    return MSMB_OK;
+    GUARD_END(f)
+}
+
+int msmb_system_propagate(msmb_field* f, msmb_system* s, double dt, int steps) {
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    GUARD_BEGIN
+    f->last = Error{};
+    cudaSetDevice(f->device);
+    return engine_propagate(f, s->st, dt, steps, f->units.energy_to_native);
+    GUARD_END(f)
+}
+
+int msmb_system_evaluate(msmb_field* f, msmb_system* s, double* phi, double* phi_short,
+                         double* phi_long, double* force_xyz, double* energy) {
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    GUARD_BEGIN
+    f->last = Error{};
+    cudaSetDevice(f->device);
+    const int rc = eval_device(f, s->st, true);
+    if (rc) return rc;
+    copy_outputs(f, s->st.n, phi, phi_short, phi_long, force_xyz, energy);
+    return MSMB_OK;
+    GUARD_END(f)
+}
+
+int msmb_set_stage_timing(msmb_field* f, int enable) {
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    f->timer.on = enable != 0;
+    return MSMB_OK;
+}
+
+int msmb_stage_times(msmb_field* f, double* ms, int64_t* launches, const char** names, int cap) {
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    const int n = std::min<int>(cap, int(f->timer.names.size()));
+    for (int i = 0; i < n; ++i) {
+        if (ms) ms[i] = f->timer.ms[i];
+        if (launches) launches[i] = f->timer.launches[i];
+        if (names) names[i] = f->timer.names[i].c_str();
+    }
+    return n;
+}
+
+void msmb_reset_stage_times(msmb_field* f) {
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    for (auto& m : f->timer.ms) m = 0.0;
+    for (auto& l : f->timer.launches) l = 0;
+}
+
+int msmb_work_counters(msmb_field* f, int64_t* out, int cap) {
+    const int n = std::min(cap, 6);
+    for (int i = 0; i < n; ++i) out[i] = f->counters[i];
+    return n;
+}
+
+int64_t msmb_kernel_launches(const msmb_field* f) { return f->launches; }
+
+int msmb_grid_geometry(const msmb_msm_config* cfg, const double box[3], int* dims, double* spacing,
+                       double* origin) {
+    msmb_units u{332.0636, 4.184e-4};
+    Geometry g;
+    Error e = build_geometry(*cfg, u, box, 1, g);
+    if (e.kind) {
+        g_create_error = e;
+        return e.kind;
+    }
+    for (int k = 0; k < g.levels; ++k) {
+        for (int ax = 0; ax < 3; ++ax) {
+            dims[3 * k + ax] = g.lv[k].dims[ax];
+            origin[3 * k + ax] = g.lv[k].origin[ax];
+        }
+        spacing[k] = g.lv[k].spacing;
+    }
+    return MSMB_OK;
+}
+
+int msmb_debug_levels(msmb_field* f, double* level_charge, double* level_potential) {
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    GUARD_BEGIN
+    if (!f->ws) return MSMB_ERR_INTERNAL;
+    cudaSetDevice(f->device);
+    const size_t bytes = sizeof(double) * f->ws->g.lattice_total;
+    if (level_charge) ck(cudaMemcpy(level_charge, f->ws->L.charge, bytes, cudaMemcpyDeviceToHost), "D2H");
+    if (level_potential) ck(cudaMemcpy(level_potential, f->ws->L.pot, bytes, cudaMemcpyDeviceToHost), "D2H");
+    return MSMB_OK;
+    GUARD_END(f)
+}
+
+int msmb_debug_cells(msmb_field* f, int64_t n, const double* pos_xyz, const double box[3],
+                     int32_t* cells_xyz, int32_t* covered) {
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    GUARD_BEGIN
+    cudaSetDevice(f->device);
+    Error e = ensure_workspace(f, n, box);
+    if (e.kind) return engine_set_error(f, e);
+    std::vector<double> q(size_t(n), 0.0);
+    fill_state(f, f->scratch, n, pos_xyz, nullptr, q.data(), nullptr, box);
+    DBuf dc, dv;
+    ck(dc.alloc(sizeof(int) * 3 * size_t(n > 0 ? n : 1)), "alloc");
+    ck(dv.alloc(sizeof(int) * size_t(n > 0 ? n : 1)), "alloc");
+    f->launches += launch_debug_cells(f->stream, f->ws->g, f->scratch.dev(), dc.as<int>(), dv.as<int>());
+    ck(cudaStreamSynchronize(f->stream), "sync");
+    if (n) {
+        ck(cudaMemcpy(cells_xyz, dc.p, sizeof(int) * 3 * size_t(n), cudaMemcpyDeviceToHost), "D2H");
+        ck(cudaMemcpy(covered, dv.p, sizeof(int) * size_t(n), cudaMemcpyDeviceToHost), "D2H");
+    }
+    return MSMB_OK;
+    GUARD_END(f)
+}
+
+int msmb_debug_stage(msmb_field* f, int stage, int k, const double box[3], const double* in,
+                     double* out, int64_t n, const double* pos_xyz) {
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    GUARD_BEGIN
+    cudaSetDevice(f->device);
+    Error e = ensure_workspace(f, n, box);
+    if (e.kind) return engine_set_error(f, e);
+    Workspace& W = *f->ws;
+    const Geometry& g = W.g;
+    f->launches += launch_reset_err(f->stream, W.err, 0);
+    auto up = [&](double* d, const double* h, size_t cnt) {
+        ck(cudaMemcpy(d, h, sizeof(double) * cnt, cudaMemcpyHostToDevice), "H2D");
+    };
+    auto down = [&](double* h, const double* d, size_t cnt) {
+        ck(cudaStreamSynchronize(f->stream), "sync");
+        ck(cudaMemcpy(h, d, sizeof(double) * cnt, cudaMemcpyDeviceToHost), "D2H");
+    };
+    switch (stage) {
+        case 0: // restrict k -> k+1
+            if (k < 0 || k + 1 >= g.levels) return MSMB_ERR_HIERARCHY;
+            up(W.L.charge + g.lv[k].offset, in, g.lv[k].size);
+            f->launches += launch_restrict(f->stream, g, k, W.L, W.err);
+            down(out, W.L.charge + g.lv[k + 1].offset, g.lv[k + 1].size);
+            break;
+        case 1: { // lattice cutoff on level k (runs all non-top levels; reads level k only)
+            if (k < 0 || k + 1 >= g.levels) return MSMB_ERR_HIERARCHY;
+            up(W.L.charge + g.lv[k].offset, in, g.lv[k].size);
+            f->launches += launch_lattice(f->stream, g, W.L, W.err);
+            down(out, W.L.pot + g.lv[k].offset, g.lv[k].size);
+            break;
+        }
+        case 2: { // top level
+            const int t = g.levels - 1;
+            up(W.L.charge + g.lv[t].offset, in, g.lv[t].size);
+            f->launches += launch_top(f->stream, g, W.L, W.err);
+            down(out, W.L.pot + g.lv[t].offset, g.lv[t].size);
+            break;
+        }
+        case 3: // prolongate k+1 -> k; `in` = coarse potential, `out` = fine potential (in/out)
+            if (k < 0 || k + 1 >= g.levels) return MSMB_ERR_HIERARCHY;
+            up(W.L.pot + g.lv[k + 1].offset, in, g.lv[k + 1].size);
+            up(W.L.pot + g.lv[k].offset, out, g.lv[k].size);
+            f->launches += launch_prolong(f->stream, g, k, W.L, W.err);
+            down(out, W.L.pot + g.lv[k].offset, g.lv[k].size);
+            break;
+        case 4: { // interpolate level-0 potential at particles
+            std::vector<double> q(size_t(n), 0.0);
+            fill_state(f, f->scratch, n, pos_xyz, nullptr, q.data(), nullptr, box);
+            up(W.L.pot + g.lv[0].offset, in, g.lv[0].size);
+            f->launches += launch_debug_interp(f->stream, g, f->scratch.dev(), W.L.pot + g.lv[0].offset, W.o.phil);
+            down(out, W.o.phil, size_t(n));
+            break;
+        }
+        default:
+            return MSMB_ERR_CONFIG;
+    }
+    ck(cudaGetLastError(), "launch");
+    return MSMB_OK;
+    GUARD_END(f)
+}
+
+} // extern "C"

@@ -1,0 +1,131 @@
+// Host-side engine objects shared by msmb_engine.cu and msmb_parareal.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "msmb_kernels.cuh"
+
+namespace msmb {
+
+// RAII device buffer
+struct DBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { reset(); }
+    void reset() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    cudaError_t alloc(size_t b) {
+        reset();
+        if (b == 0) b = 8;
+        bytes = b;
+        return cudaMalloc(&p, b);
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+// A device-resident particle system (SoA)
+struct StateBuf {
+    int64_t n = 0;
+    DBuf buf; // 8 arrays of n doubles: x y z vx vy vz q m
+    double box[3] = {0, 0, 0};
+    cudaError_t alloc(int64_t nn) {
+        n = nn;
+        return buf.alloc(sizeof(double) * 8 * size_t(nn > 0 ? nn : 1));
+    }
+    DevState dev() const {
+        DevState s;
+        s.n = n;
+        double* b = buf.as<double>();
+        const size_t N = size_t(n > 0 ? n : 1);
+        s.x = b;
+        s.y = b + N;
+        s.z = b + 2 * N;
+        s.vx = b + 3 * N;
+        s.vy = b + 4 * N;
+        s.vz = b + 5 * N;
+        s.q = b + 6 * N;
+        s.m = b + 7 * N;
+        return s;
+    }
+};
+
+struct Workspace {
+    Geometry g;
+    int64_t n = 0;
+    int64_t maxclu = 0;
+    int cap = 0;
+    DevAtoms a{};
+    DevCells c{};
+    DevLevels L{};
+    DevOut o{};
+    std::vector<std::unique_ptr<DBuf>> bufs; // owns everything above
+    DBuf plist_buf;
+    DBuf backup;   // 6n doubles: initial x,y,z,vx,vy,vz of a propagate call
+    DBuf staging;  // 3n doubles: AoS transfers
+    ErrRec* err = nullptr;
+    ErrRec* err_host = nullptr; // pinned
+    // graph cache
+    cudaGraphExec_t gx_eval = nullptr, gx_step1 = nullptr, gx_step2 = nullptr;
+    const double* graph_key = nullptr;
+    double graph_dt = 0;
+    int graph_cap = 0;
+    int launches_eval = 0, launches_step = 0;
+    ~Workspace();
+};
+
+struct StageTimer {
+    bool on = false;
+    std::vector<std::string> names;
+    std::vector<double> ms;
+    std::vector<int64_t> launches;
+    struct Pending {
+        int stage;
+        cudaEvent_t a, b;
+        int nl;
+    };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> pool;
+    int stage_index(const char* name);
+    cudaEvent_t ev();
+    void resolve();
+    ~StageTimer();
+};
+
+} // namespace msmb
+
+struct msmb_field {
+    msmb_msm_config cfg{};
+    msmb_units units{};
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::recursive_mutex mu;
+    std::unique_ptr<msmb::Workspace> ws;
+    msmb::Error last;
+    msmb::StageTimer timer;
+    int64_t launches = 0;
+    int64_t counters[8] = {0};
+    msmb::StateBuf scratch; // device system for the host-pointer entry points
+};
+
+struct msmb_system {
+    msmb_field* f = nullptr;
+    msmb::StateBuf st;
+};
+
+namespace msmb {
+// engine entry points used by the parareal driver (caller holds f->mu)
+int engine_propagate(msmb_field* f, StateBuf& s, double dt, int steps, double conv);
+int engine_set_error(msmb_field* f, const Error& e);
+int cuda_fail(msmb_field* f, cudaError_t e, const char* where);
+} // namespace msmb

@@ -1,0 +1,114 @@
+// Internal declarations shared by the host engine (msmb_engine.cu), the host
+// geometry/table builder (msmb_geometry.cpp) and the kernels (msmb_kernels.cu).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/msmb.h"
+
+namespace msmb {
+
+constexpr int kMaxLevels = 16;
+constexpr int kPairWarps = 4;      // warps per CTA in the pair kernels
+constexpr int kConvB = 16;         // outputs per thread along z in the stencil kernel
+constexpr int kConvL = 8;          // taps per chunk in the stencil kernel
+constexpr int kConvNWZ = 2;        // warps along z per stencil CTA
+constexpr int kConvZ = kConvB * kConvNWZ;
+constexpr int kAnterpSeg = 16;     // z points per anterpolation thread
+constexpr int kRestrictMax = 8;    // fine indices feeding one coarse index per axis
+constexpr int kOverflowKind = 100; // internal: pair-list capacity exceeded, retry
+
+// ---- host-side error ----------------------------------------------------------
+struct Error {
+    int kind = MSMB_OK;
+    int64_t i = -1, j = -1;
+    int step = -1;
+    std::string msg;
+};
+
+// ---- device error record (one per workspace) ------------------------------------
+struct ErrRec {
+    int kind;                    // 0 while healthy; msmb_status once an evaluation failed
+    int step;                    // Verlet step of the failing evaluation
+    int overflow;                // max pair-list entries requested by any cluster (if > cap)
+    int cov_count;               // out-of-coverage particles in the current evaluation
+    unsigned long long pair_key; // min (i << 32 | j), i < j, with r2 == 0 or NaN
+    long long cov_min;           // min out-of-coverage particle index
+    long long err_i, err_j;      // indices reported with `kind`
+    int cur_step;                // step counter, advanced by the Verlet kernels
+    int pad;
+    unsigned long long pairs;     // in-cutoff ordered pairs (stats, current evaluation)
+    unsigned long long candidates;// screened candidate pairs (stats)
+};
+
+// ---- level geometry (src/msm_grid.cpp:24-54) -----------------------------------
+struct LevelGeom {
+    int k = 0;
+    double spacing = 0;
+    double origin[3] = {0, 0, 0};
+    int dims[3] = {0, 0, 0};
+    size_t size = 0;
+    size_t offset = 0; // into the concatenated lattice buffers
+};
+
+// Grid-to-grid transfer stencil for fine level k -> coarse level k+1, per axis:
+// fine index i -> coarse base + 4 weights (stencil_at, src/msm_phases.cpp:21-29),
+// and the inverse lists used by the restriction gather.
+struct TransferAxis {
+    std::vector<int> base;     // [d_fine]
+    std::vector<double> w;     // [d_fine * 4]
+    std::vector<int> rcnt;     // [d_coarse]
+    std::vector<int> ridx;     // [d_coarse * kRestrictMax], ascending fine index
+    std::vector<double> rw;    // [d_coarse * kRestrictMax]
+};
+
+struct ConvRow { // one (dx, dy) row of a 3-D stencil: taps for dz = -m..m
+    int dx, dy, m, tap_off;
+};
+
+struct ConvTable {
+    int Rx = 0, Ry = 0, Rz = 0;       // stencil half-extents (grid units)
+    std::vector<ConvRow> rows;        // sorted by dx, then dy
+    std::vector<int> dx_begin;        // [2*Rx + 2]: rows of dx are [dx_begin[dx+Rx], dx_begin[dx+Rx+1])
+    std::vector<double> taps;         // each row padded to a multiple of kConvL
+    int64_t nonzero_taps = 0;         // nonzero taps in the stencil
+};
+
+struct Geometry {
+    msmb_msm_config cfg{};
+    msmb_units units{};
+    double box[3] = {0, 0, 0};
+    int levels = 0;
+    LevelGeom lv[kMaxLevels];
+    size_t lattice_total = 0;
+    TransferAxis tr[kMaxLevels][3];      // tr[k][axis], k = 0..levels-2
+    ConvTable lattice[kMaxLevels];       // k = 0..levels-2
+    ConvTable top;
+    double inv_h0 = 0;                   // 1.0 / spacing of level 0
+    double self_term = 0;                // smoothing_gamma(0)/a (src/msm.cpp:72)
+    // pair-cell (column) decomposition over level-0 cells
+    int cw = 1;                          // column width in level-0 cells
+    int ncx = 0, ncy = 0;                // columns
+    int64_t ncells = 0;                  // sorted-cell index space
+    int64_t ncols = 0;
+    double colw = 0;                     // column width in Angstrom
+    double screen_cut = 0;               // fp32 screening cutoff (a + margin)
+    int pair_cap = 0;                    // initial pair-list capacity per cluster
+    int64_t lattice_taps_clipped = 0;    // sum over levels 0..l-2 of clipped nonzero taps
+    int64_t top_taps = 0;                // M_top^2
+};
+
+// Validation with the reference's messages.  Returns MSMB_OK or an error.
+Error validate_config(const msmb_msm_config& c);
+Error validate_units(const msmb_units& u);
+// Builds the level hierarchy + all tables.  `n` sizes the pair-list estimate.
+Error build_geometry(const msmb_msm_config& c, const msmb_units& u, const double box[3],
+                     int64_t n, Geometry& g);
+// Reference kernel math on the host (bitwise the reference's, non-FMA).
+double host_gamma(double rho);
+double host_g_level(double r, double a, int k, int l);
+double host_flops_simplified(double a, double h, double n);
+
+} // namespace msmb

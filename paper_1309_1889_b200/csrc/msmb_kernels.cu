@@ -1,0 +1,1316 @@
+// sm_100a kernels for the MSM force / velocity-Verlet / parareal hot path.
+//
+// Stage map (reference file:line -> kernel):
+//   K1  bin + counting sort          src/msm_phases.cpp:21-29 (stencil_at base), msm.cpp:25-27
+//                                    -> k_bin, k_scan_*, k_scatter, k_cellsort, k_gather
+//   K2  short-range pairs            src/msm_phases.cpp:224-252, msm_kernels.hpp:30-42
+//                                    -> k_columns, k_clusters, k_bbox, k_pairlist, k_pairs, k_err_brute
+//   K3  anterpolation                src/msm_phases.cpp:39-61      -> k_anterp
+//   K4  restriction                  src/msm_phases.cpp:63-91      -> k_restrict
+//   K5  lattice cutoff               src/msm_phases.cpp:93-134     -> k_conv (lattice jobs)
+//   K6  top level                    src/msm_phases.cpp:136-162    -> k_conv (top job)
+//   K7  prolongation                 src/msm_phases.cpp:164-193    -> k_prolong
+//   K8  interpolation + forces + E   src/msm_phases.cpp:195-222, src/msm.cpp:16-48,69-86
+//                                    -> k_interp, k_energy1/2
+//   K9  velocity Verlet              src/integrate.cpp:23-34       -> k_kick_drift, k_kick
+//   K10 parareal state algebra       src/parareal.cpp:58-90        -> k_state_sub/add, k_rms
+// Determinism: no floating-point atomics anywhere; every sum has a fixed order.
+// Arithmetic that must reproduce the reference bit for bit (cell keys, stencil
+// weights, restriction/prolongation/interpolation given equal lattices, Verlet)
+// uses explicit round-to-nearest intrinsics (__dmul_rn/__dadd_rn/...), which
+// nvcc never contracts into FMA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdint>
+
+#include "msmb_kernels.cuh"
+
+namespace msmb {
+
+#define FULLMASK 0xffffffffu
+
+__device__ __forceinline__ bool failed(const ErrRec* e) {
+    return *(volatile const int*)&e->kind != 0;
+}
+
+// basis_phi / basis_phi_deriv (include/paramd/msm_kernels.hpp:71-92), reference op order.
+__device__ __forceinline__ double phi_rn(double xi) {
+    const double t = fabs(xi);
+    if (t >= 2.0) return 0.0;
+    if (t <= 1.0)
+        return __dadd_rn(1.0, __dmul_rn(__dmul_rn(t, t), __dadd_rn(-2.5, __dmul_rn(1.5, t))));
+    const double u = __dsub_rn(2.0, t);
+    return __dmul_rn(__dmul_rn(__dmul_rn(-0.5, __dsub_rn(t, 1.0)), u), u);
+}
+
+__device__ __forceinline__ double dphi_rn(double xi) {
+    const double t = fabs(xi);
+    double d;
+    if (t >= 2.0)
+        d = 0.0;
+    else if (t <= 1.0)
+        d = __dmul_rn(t, __dadd_rn(-5.0, __dmul_rn(4.5, t)));
+    else
+        d = __dmul_rn(__dmul_rn(-0.5, __dsub_rn(2.0, t)), __dsub_rn(4.0, __dmul_rn(3.0, t)));
+    return xi < 0.0 ? -d : d;
+}
+
+struct BinP {
+    double o[3];
+    double inv_h;
+    int d[3];
+    int cw, ncx, ncy;
+};
+
+static BinP make_binp(const Geometry& g) {
+    BinP p;
+    for (int ax = 0; ax < 3; ++ax) {
+        p.o[ax] = g.lv[0].origin[ax];
+        p.d[ax] = g.lv[0].dims[ax];
+    }
+    p.inv_h = g.inv_h0;
+    p.cw = g.cw;
+    p.ncx = g.ncx;
+    p.ncy = g.ncy;
+    return p;
+}
+
+__device__ __forceinline__ int scell_of(const BinP& p, int cx, int cy, int cz) {
+    const int col = (cx / p.cw) * p.ncy + (cy / p.cw);
+    return ((col * p.d[2] + cz) * p.cw + (cx % p.cw)) * p.cw + (cy % p.cw);
+}
+
+// ============================================================================
+// K1: binning (bit-exact level-0 cell triple) + stable counting sort
+// ============================================================================
+__global__ void k_bin(int n, const double* __restrict__ x, const double* __restrict__ y,
+                      const double* __restrict__ z, BinP p, int* key, int* rank, int* count,
+                      int* outlist, ErrRec* err) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || failed(err)) return;
+    const double px[3] = {x[i], y[i], z[i]};
+    int c[3];
+    bool ok = true;
+    for (int ax = 0; ax < 3; ++ax) {
+        // t = (r - origin) * inv_h; base = floor(t) - 1 (src/msm_phases.cpp:23,42-50)
+        const double t = __dmul_rn(__dsub_rn(px[ax], p.o[ax]), p.inv_h);
+        const double f = floor(t);
+        // covered iff 0 <= base && base + 3 <= dims - 1 (src/msm_phases.cpp:24)
+        ok = ok && (f >= 1.0) && (f <= double(p.d[ax]) - 3.0);
+        c[ax] = ok ? int(f) : 0;
+    }
+    if (!ok) {
+        key[i] = -1;
+        atomicMin(&err->cov_min, (long long)i);
+        const int slot = atomicAdd(&err->cov_count, 1);
+        outlist[slot] = i;
+        return;
+    }
+    const int sc = scell_of(p, c[0], c[1], c[2]);
+    key[i] = sc;
+    rank[i] = atomicAdd(&count[sc], 1);
+}
+
+// exclusive scan of int[m] (m = cells + 1), 4096 elements per block
+__global__ void __launch_bounds__(1024) k_scan_block(const int* __restrict__ in, int* out,
+                                                     int* bsum, int64_t m) {
+    __shared__ int wsum[32];
+    const int64_t base = int64_t(blockIdx.x) * 4096 + threadIdx.x * 4;
+    int v[4];
+    int s = 0;
+    for (int k = 0; k < 4; ++k) {
+        v[k] = (base + k < m) ? in[base + k] : 0;
+        s += v[k];
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int inc = s;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(FULLMASK, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        int ws = wsum[lane];
+        int wi = ws;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(FULLMASK, wi, o);
+            if (lane >= o) wi += t;
+        }
+        wsum[lane] = wi - ws;
+        if (lane == 31) bsum[blockIdx.x] = wi;
+    }
+    __syncthreads();
+    int run = inc - s + wsum[w];
+    for (int k = 0; k < 4; ++k) {
+        if (base + k < m) out[base + k] = run;
+        run += v[k];
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_scan_sums(int* bsum, int nb) {
+    __shared__ int wsum[32];
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int base = 0; base < nb; base += 1024) {
+        const int idx = base + threadIdx.x;
+        const int v = idx < nb ? bsum[idx] : 0;
+        int inc = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(FULLMASK, inc, o);
+            if (lane >= o) inc += t;
+        }
+        if (lane == 31) wsum[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            const int ws = wsum[lane];
+            int wi = ws;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(FULLMASK, wi, o);
+                if (lane >= o) wi += t;
+            }
+            wsum[lane] = wi - ws;
+        }
+        __syncthreads();
+        const int excl = carry + wsum[w] + inc - v;
+        __syncthreads();
+        if (idx < nb) bsum[idx] = excl;
+        if (threadIdx.x == 1023) carry = excl + v;
+        __syncthreads();
+    }
+}
+
+__global__ void k_scan_add(int* out, const int* __restrict__ bsum, int64_t m) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < m) out[i] += bsum[i / 4096];
+}
+
+static int scan_exclusive(cudaStream_t st, const int* in, int* out, int* tmp, int64_t m) {
+    const int nb = int((m + 4095) / 4096);
+    k_scan_block<<<nb, 1024, 0, st>>>(in, out, tmp, m);
+    k_scan_sums<<<1, 1024, 0, st>>>(tmp, nb);
+    k_scan_add<<<int((m + 255) / 256), 256, 0, st>>>(out, tmp, m);
+    return 3;
+}
+
+__global__ void k_scatter(int n, const int* __restrict__ key, const int* __restrict__ rank,
+                          const int* __restrict__ start, int* perm, const ErrRec* err) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || failed(err)) return;
+    const int k = key[i];
+    if (k >= 0) perm[start[k] + rank[i]] = i;
+}
+
+// within-cell order = ascending original index (deterministic; cells are small)
+__global__ void k_cellsort(int64_t ncells, const int* __restrict__ start, int* perm,
+                           const ErrRec* err) {
+    const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= ncells || failed(err)) return;
+    const int s0 = start[c], s1 = start[c + 1];
+    for (int a = s0 + 1; a < s1; ++a) {
+        const int v = perm[a];
+        int b = a - 1;
+        while (b >= s0 && perm[b] > v) {
+            perm[b + 1] = perm[b];
+            --b;
+        }
+        perm[b + 1] = v;
+    }
+}
+
+// sorted copies + the anterpolation weights of every particle:
+// aw = {q*wx[0..3], wy[0..3], wz[0..3]} exactly as anterpolate's qa / w (msm_phases.cpp:45-53)
+__global__ void k_gather(int n, const int* __restrict__ start_total, const int* __restrict__ perm,
+                         const double* __restrict__ x, const double* __restrict__ y,
+                         const double* __restrict__ z, const double* __restrict__ q, BinP p,
+                         double* xs, double* ys, double* zs, double* qs, float4* f4, double* aw,
+                         const ErrRec* err) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= *start_total || failed(err)) return;
+    const int i = perm[s];
+    const double px = x[i], py = y[i], pz = z[i], qq = q[i];
+    xs[s] = px;
+    ys[s] = py;
+    zs[s] = pz;
+    qs[s] = qq;
+    f4[s] = make_float4(float(px), float(py), float(pz), 0.f);
+    const double pp[3] = {px, py, pz};
+    double w[3][4];
+    for (int ax = 0; ax < 3; ++ax) {
+        const double t = __dmul_rn(__dsub_rn(pp[ax], p.o[ax]), p.inv_h);
+        const int base = int(floor(t)) - 1;
+        for (int d = 0; d < 4; ++d) w[ax][d] = phi_rn(__dsub_rn(t, double(base + d)));
+    }
+    double* o = aw + size_t(s) * 12;
+    for (int d = 0; d < 4; ++d) {
+        o[d] = __dmul_rn(qq, w[0][d]);
+        o[4 + d] = w[1][d];
+        o[8 + d] = w[2][d];
+    }
+}
+
+int launch_bin(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& a, DevCells& c,
+               ErrRec* err) {
+    const int n = int(s.n);
+    cudaMemsetAsync(c.count, 0, sizeof(int) * size_t(g.ncells + 1), st);
+    if (n > 0)
+        k_bin<<<(n + 255) / 256, 256, 0, st>>>(n, s.x, s.y, s.z, make_binp(g), a.key, a.rank,
+                                               c.count, a.outlist, err);
+    return n > 0 ? 1 : 0;
+}
+
+int launch_sort(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& a, DevCells& c,
+                ErrRec* err) {
+    const int n = int(s.n);
+    int l = scan_exclusive(st, c.count, c.start, c.scan_tmp, g.ncells + 1);
+    if (n == 0) return l;
+    k_scatter<<<(n + 255) / 256, 256, 0, st>>>(n, a.key, a.rank, c.start, a.perm, err);
+    k_cellsort<<<int((g.ncells + 255) / 256), 256, 0, st>>>(g.ncells, c.start, a.perm, err);
+    k_gather<<<(n + 255) / 256, 256, 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, s.q,
+                                              make_binp(g), a.xs, a.ys, a.zs, a.qs, a.f4, a.aw,
+                                              err);
+    return l + 3;
+}
+
+// ============================================================================
+// K2: short-range pairs.  Columns of cw x cw level-0 cells; 32 consecutive
+// sorted atoms of a column form a cluster; one warp per i-cluster walks the
+// list of j-clusters whose bounding boxes are within the cutoff.
+// ============================================================================
+__global__ void k_columns(int64_t ncols, int cells_per_col, const int* __restrict__ start,
+                          int* col_cnt, const ErrRec* err) {
+    const int64_t col = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (col > ncols || failed(err)) return;
+    if (col == ncols) {
+        col_cnt[col] = 0;
+        return;
+    }
+    const int cnt = start[(col + 1) * cells_per_col] - start[col * cells_per_col];
+    col_cnt[col] = (cnt + 31) / 32;
+}
+
+__global__ void k_clusters(int64_t ncols, int cells_per_col, const int* __restrict__ start,
+                           const int* __restrict__ col_off, int2* clu, int* nclu,
+                           const ErrRec* err) {
+    const int64_t col = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (col >= ncols || failed(err)) return;
+    if (col == ncols - 1) *nclu = col_off[ncols];
+    const int s0 = start[col * cells_per_col];
+    const int cnt = start[(col + 1) * cells_per_col] - s0;
+    const int off = col_off[col];
+    for (int k = 0; 32 * k < cnt; ++k) clu[off + k] = make_int2(s0 + 32 * k, min(32, cnt - 32 * k));
+}
+
+__global__ void k_bbox(const int* __restrict__ nclu, const int2* __restrict__ clu,
+                       const double* __restrict__ xs, const double* __restrict__ ys,
+                       const double* __restrict__ zs, float4* blo, float4* bhi,
+                       const ErrRec* err) {
+    const int ic = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (ic >= *nclu || failed(err)) return;
+    const int2 c = clu[ic];
+    float lo[3] = {3e38f, 3e38f, 3e38f}, hi[3] = {-3e38f, -3e38f, -3e38f};
+    if (lane < c.y) {
+        const double p[3] = {xs[c.x + lane], ys[c.x + lane], zs[c.x + lane]};
+        for (int ax = 0; ax < 3; ++ax) {
+            lo[ax] = __double2float_rd(p[ax]);
+            hi[ax] = __double2float_ru(p[ax]);
+        }
+    }
+    for (int o = 16; o; o >>= 1)
+        for (int ax = 0; ax < 3; ++ax) {
+            lo[ax] = fminf(lo[ax], __shfl_xor_sync(FULLMASK, lo[ax], o));
+            hi[ax] = fmaxf(hi[ax], __shfl_xor_sync(FULLMASK, hi[ax], o));
+        }
+    if (lane == 0) {
+        blo[ic] = make_float4(lo[0], lo[1], lo[2], 0.f);
+        bhi[ic] = make_float4(hi[0], hi[1], hi[2], 0.f);
+    }
+}
+
+struct ListP {
+    double ox, oy;   // level-0 origin (x, y)
+    double colw;     // column width (A)
+    int ncx, ncy;
+    float cut, cut2;
+};
+
+__device__ __forceinline__ float gapf(float alo, float ahi, float blo, float bhi) {
+    return fmaxf(0.f, fmaxf(blo - ahi, alo - bhi));
+}
+
+__global__ void k_pairlist(const int* __restrict__ nclu, const float4* __restrict__ blo,
+                           const float4* __restrict__ bhi, const int* __restrict__ col_off, ListP p,
+                           int* plist, int* pcnt, int cap, ErrRec* err) {
+    const int ic = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (ic >= *nclu || failed(err)) return;
+    const float4 lo = blo[ic], hi = bhi[ic];
+    const double cutd = double(p.cut);
+    int cx0 = int(floor((double(lo.x) - cutd - p.ox) / p.colw)) - 1;
+    int cx1 = int(floor((double(hi.x) + cutd - p.ox) / p.colw)) + 1;
+    int cy0 = int(floor((double(lo.y) - cutd - p.oy) / p.colw)) - 1;
+    int cy1 = int(floor((double(hi.y) + cutd - p.oy) / p.colw)) + 1;
+    cx0 = max(cx0, 0);
+    cy0 = max(cy0, 0);
+    cx1 = min(cx1, p.ncx - 1);
+    cy1 = min(cy1, p.ncy - 1);
+    int count = 0;
+    int* out = plist + size_t(ic) * cap;
+    for (int cx = cx0; cx <= cx1; ++cx) {
+        const float xlo = float(p.ox + cx * p.colw) - 1e-3f, xhi = float(p.ox + (cx + 1) * p.colw) + 1e-3f;
+        const float gx = gapf(lo.x, hi.x, xlo, xhi);
+        if (gx >= p.cut) continue;
+        for (int cy = cy0; cy <= cy1; ++cy) {
+            const float ylo = float(p.oy + cy * p.colw) - 1e-3f, yhi = float(p.oy + (cy + 1) * p.colw) + 1e-3f;
+            const float gy = gapf(lo.y, hi.y, ylo, yhi);
+            if (gx * gx + gy * gy >= p.cut2) continue;
+            const int col = cx * p.ncy + cy;
+            const int j0 = col_off[col], j1 = col_off[col + 1];
+            for (int jb = j0; jb < j1; jb += 32) {
+                const int jc = jb + lane;
+                bool ok = false;
+                if (jc < j1) {
+                    const float4 l2 = blo[jc], h2 = bhi[jc];
+                    const float dx = gapf(lo.x, hi.x, l2.x, h2.x);
+                    const float dy = gapf(lo.y, hi.y, l2.y, h2.y);
+                    const float dz = gapf(lo.z, hi.z, l2.z, h2.z);
+                    ok = dx * dx + dy * dy + dz * dz < p.cut2;
+                }
+                const unsigned b = __ballot_sync(FULLMASK, ok);
+                const int pos = count + __popc(b & ((1u << lane) - 1u));
+                if (ok && pos < cap) out[pos] = jc;
+                count += __popc(b);
+            }
+        }
+    }
+    if (lane == 0) {
+        pcnt[ic] = min(count, cap);
+        if (count > cap) atomicMax(&err->overflow, count);
+    }
+}
+
+struct PairP {
+    double a2;
+    long long a2bits;
+    double c0, c1, c2;   // gamma(r/a)/a = c0 + r2*(c1 + r2*c2)
+    double d0, d1;       // g*'(r)/r + 1/r^3 = d0 + r2*d1
+    double kc;
+    float cut2f;
+};
+
+__device__ __forceinline__ void record_pair(ErrRec* err, int i, int j) {
+    const unsigned long long lo = (unsigned long long)min(i, j), hi = (unsigned long long)max(i, j);
+    atomicMin(&err->pair_key, (lo << 32) | hi);
+}
+
+// One warp per i-cluster (lane = i atom).  For every candidate j-cluster: stage
+// its 32 atoms in shared memory (fp32 copy for screening; fp64 words split
+// into conflict-free 32-bit arrays), build each lane's 32-bit in-range mask in
+// fp32 with a safety margin, then walk the set bits so every DP instruction
+// works on a screened pair.  The exact fp64 test r2 < a2 decides inclusion.
+__global__ void __launch_bounds__(kPairWarps * 32)
+    k_pairs(const int* __restrict__ nclu, const int2* __restrict__ clu,
+            const int* __restrict__ plist, const int* __restrict__ pcnt, int cap,
+            const double* __restrict__ xs, const double* __restrict__ ys,
+            const double* __restrict__ zs, const double* __restrict__ qs,
+            const float4* __restrict__ f4, const int* __restrict__ perm, PairP p, double* phis,
+            double* fsx, double* fsy, double* fsz, ErrRec* err) {
+    __shared__ float4 s_f[kPairWarps][32];
+    __shared__ unsigned s_w[kPairWarps][8][32];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ic = blockIdx.x * kPairWarps + w;
+    if (ic >= *nclu || failed(err)) return;
+    const int2 c = clu[ic];
+    const bool vi = lane < c.y;
+    const int si = c.x + (vi ? lane : 0);
+    const double xi = xs[si], yi = ys[si], zi = zs[si], qi = qs[si];
+    const float4 fi = f4[si];
+    double ph = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
+    unsigned npair = 0, ncand = 0;
+    const int nj = pcnt[ic];
+    const int* pl = plist + size_t(ic) * cap;
+    for (int jj = 0; jj < nj; ++jj) {
+        const int jc = pl[jj];
+        const int2 cj = clu[jc];
+        const bool vj = lane < cj.y;
+        const int sj = cj.x + (vj ? lane : 0);
+        float4 fj = f4[sj];
+        if (!vj) fj = make_float4(1e30f, 1e30f, 1e30f, 0.f);
+        const double xj = xs[sj], yj = ys[sj], zj = zs[sj], qj = qs[sj];
+        __syncwarp();
+        s_f[w][lane] = fj;
+        s_w[w][0][lane] = __double2loint(xj);
+        s_w[w][1][lane] = __double2hiint(xj);
+        s_w[w][2][lane] = __double2loint(yj);
+        s_w[w][3][lane] = __double2hiint(yj);
+        s_w[w][4][lane] = __double2loint(zj);
+        s_w[w][5][lane] = __double2hiint(zj);
+        s_w[w][6][lane] = __double2loint(qj);
+        s_w[w][7][lane] = __double2hiint(qj);
+        __syncwarp();
+        unsigned mask = 0;
+        if (vi) {
+#pragma unroll
+            for (int t = 0; t < 32; ++t) {
+                const float4 pj = s_f[w][t];
+                const float dx = fi.x - pj.x, dy = fi.y - pj.y, dz = fi.z - pj.z;
+                const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                mask |= (r2 < p.cut2f ? 1u : 0u) << t;
+            }
+        }
+        if (jc == ic) mask &= ~(1u << lane);
+        ncand += __popc(mask);
+        while (__any_sync(FULLMASK, mask != 0)) {
+            if (mask) {
+                const int t = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const double xj2 = __hiloint2double(s_w[w][1][t], s_w[w][0][t]);
+                const double yj2 = __hiloint2double(s_w[w][3][t], s_w[w][2][t]);
+                const double zj2 = __hiloint2double(s_w[w][5][t], s_w[w][4][t]);
+                const double qj2 = __hiloint2double(s_w[w][7][t], s_w[w][6][t]);
+                const double dx = xi - xj2, dy = yi - yj2, dz = zi - zj2;
+                double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+                const long long rb = __double_as_longlong(r2);
+                if (rb == 0) record_pair(err, perm[si], perm[cj.x + t]);
+                // 0 < r2 < a2 as one unsigned compare on the bit patterns
+                const bool in = (unsigned long long)(rb - 1) < (unsigned long long)(p.a2bits - 1);
+                r2 = in ? r2 : p.a2;
+                const double rinv = rsqrt(r2);
+                const double rinv2 = rinv * rinv;
+                const double g = rinv - fma(r2, fma(r2, p.c2, p.c1), p.c0);      // g*(r)
+                const double sd = fma(r2, p.d1, p.d0) - rinv * rinv2;              // g*'(r)/r
+                const double qe = in ? qj2 : 0.0;
+                ph = fma(qe, g, ph);
+                const double wgt = qe * sd;
+                fx = fma(dx, wgt, fx);
+                fy = fma(dy, wgt, fy);
+                fz = fma(dz, wgt, fz);
+                npair += in ? 1u : 0u;
+            }
+        }
+    }
+    if (vi) {
+        const double kq = -p.kc * qi; // f = d * (-k_C q_i q_j g*'/r)  (msm_phases.cpp:246)
+        phis[si] = ph;
+        fsx[si] = fx * kq;
+        fsy[si] = fy * kq;
+        fsz[si] = fz * kq;
+    }
+    for (int o = 16; o; o >>= 1) {
+        npair += __shfl_xor_sync(FULLMASK, npair, o);
+        ncand += __shfl_xor_sync(FULLMASK, ncand, o);
+    }
+    if (lane == 0) {
+        atomicAdd(&err->pairs, (unsigned long long)npair);
+        atomicAdd(&err->candidates, (unsigned long long)ncand);
+    }
+}
+
+// Error path only: pairs involving particles that could not be binned
+// (outside grid coverage or non-finite) against every particle, with the
+// reference's arithmetic, to find the first pair with r2 == 0 or NaN.
+__global__ void k_err_brute(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
+                            const double* __restrict__ z, const int* __restrict__ outlist,
+                            ErrRec* err) {
+    const int cnt = *(volatile int*)&err->cov_count;
+    if (cnt == 0 || failed(err)) return;
+    const int64_t total = int64_t(cnt) * n;
+    for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+         idx += int64_t(gridDim.x) * blockDim.x) {
+        const int o = outlist[idx / n];
+        const int j = int(idx % n);
+        if (j == o) continue;
+        const int lo = min(o, j), hi = max(o, j);
+        const double dx = __dsub_rn(x[lo], x[hi]), dy = __dsub_rn(y[lo], y[hi]), dz = __dsub_rn(z[lo], z[hi]);
+        const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+        if (r2 == 0.0 || isnan(r2)) record_pair(err, lo, hi);
+    }
+}
+
+int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c,
+                    ErrRec* err, int cap) {
+    (void)a;
+    const int cells_per_col = int(g.lv[0].dims[2]) * g.cw * g.cw;
+    const int64_t nc = g.ncols;
+    k_columns<<<int((nc + 1 + 255) / 256), 256, 0, st>>>(nc, cells_per_col, c.start, c.col_cnt, err);
+    int l = 1 + scan_exclusive(st, c.col_cnt, c.col_off, c.scan_tmp, nc + 1);
+    k_clusters<<<int((nc + 255) / 256), 256, 0, st>>>(nc, cells_per_col, c.start, c.col_off, c.clu,
+                                                      c.nclu, err);
+    const int64_t maxclu = n / 32 + nc + 1;
+    k_bbox<<<int((maxclu * 32 + 255) / 256), 256, 0, st>>>(c.nclu, c.clu, a.xs, a.ys, a.zs, c.blo,
+                                                            c.bhi, err);
+    ListP lp;
+    lp.ox = g.lv[0].origin[0];
+    lp.oy = g.lv[0].origin[1];
+    lp.colw = g.colw;
+    lp.ncx = g.ncx;
+    lp.ncy = g.ncy;
+    lp.cut = float(g.screen_cut);
+    lp.cut2 = float(g.screen_cut * g.screen_cut);
+    k_pairlist<<<int((maxclu * 32 + 255) / 256), 256, 0, st>>>(c.nclu, c.blo, c.bhi, c.col_off, lp,
+                                                                c.plist, c.pcnt, cap, err);
+    return l + 4;
+}
+
+int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
+                 DevCells& c, ErrRec* err, int cap) {
+    const double A = g.cfg.cutoff_a;
+    PairP p;
+    p.a2 = A * A;
+    p.a2bits = *reinterpret_cast<const long long*>(&p.a2);
+    // gamma(rho)/a = 15/(8a) - 5 r^2/(4a^3) + 3 r^4/(8a^5)          (msm_kernels.hpp:14-20,30-35)
+    p.c0 = 15.0 / (8.0 * A);
+    p.c1 = -5.0 / (4.0 * A * A * A);
+    p.c2 = 3.0 / (8.0 * A * A * A * A * A);
+    // g*'(r)/r = -1/r^3 + (2.5 - 1.5 rho^2)/a^3                    (msm_kernels.hpp:22-27,37-42)
+    p.d0 = 2.5 / (A * A * A);
+    p.d1 = -1.5 / (A * A * A * A * A);
+    p.kc = g.units.coulomb_constant;
+    p.cut2f = float(g.screen_cut * g.screen_cut);
+    const int64_t maxclu = n / 32 + g.ncols + 1;
+    int l = 0;
+    if (n > 0) {
+        k_pairs<<<int((maxclu + kPairWarps - 1) / kPairWarps), kPairWarps * 32, 0, st>>>(
+            c.nclu, c.clu, c.plist, c.pcnt, cap, a.xs, a.ys, a.zs, a.qs, a.f4, a.perm, p, a.phis,
+            a.fsx, a.fsy, a.fsz, err);
+        k_err_brute<<<592, 256, 0, st>>>(n, s.x, s.y, s.z, a.outlist, err);
+        l = 2;
+    }
+    return l;
+}
+
+// ============================================================================
+// K3: anterpolation as an owner-computes gather.  A thread owns a segment of
+// kAnterpSeg points of one z-line (x, y) and walks the level-0 cells whose
+// stencils reach it, in ascending z, keeping a rolling window of 4 sums.
+// ============================================================================
+__global__ void __launch_bounds__(128)
+    k_anterp(BinP p, int tiles_x, int tiles_y, int nseg, const int* __restrict__ start,
+             const double* __restrict__ aw, double* q0, const ErrRec* err) {
+    if (failed(err)) return;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int txi = gw % tiles_x;
+    const int rest = gw / tiles_x;
+    const int tyi = rest % tiles_y;
+    const int seg = rest / tiles_y;
+    if (seg >= nseg) return;
+    const int x = txi * 4 + (lane >> 3);
+    const int y = tyi * 8 + (lane & 7);
+    const int d0 = p.d[0], d1 = p.d[1], d2 = p.d[2];
+    if (x >= d0 || y >= d1) return;
+    const int z0 = seg * kAnterpSeg;
+    const int z1 = min(z0 + kAnterpSeg, d2);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    double* out = q0 + (size_t(x) * d1 + y) * d2;
+    for (int cz = z0 - 2; cz <= z1; ++cz) {
+        if (cz >= 1 && cz <= d2 - 3) {
+            for (int ox = 0; ox < 4; ++ox) {
+                const int cx = x - 2 + ox;
+                if (cx < 1 || cx > d0 - 3) continue;
+                const int dxw = 3 - ox; // weight index x - base = x - (cx - 1)
+                for (int oy = 0; oy < 4; ++oy) {
+                    const int cy = y - 2 + oy;
+                    if (cy < 1 || cy > d1 - 3) continue;
+                    const int dyw = 3 - oy;
+                    const int sc = scell_of(p, cx, cy, cz);
+                    const int s1 = start[sc + 1];
+                    for (int s = start[sc]; s < s1; ++s) {
+                        const double* w = aw + size_t(s) * 12;
+                        const double cxy = __dmul_rn(w[dxw], w[4 + dyw]); // (q*wx)*wy
+                        const double4 wz = *reinterpret_cast<const double4*>(w + 8);
+                        a0 = fma(cxy, wz.x, a0);
+                        a1 = fma(cxy, wz.y, a1);
+                        a2 = fma(cxy, wz.z, a2);
+                        a3 = fma(cxy, wz.w, a3);
+                    }
+                }
+            }
+        }
+        // a0 holds point cz-1, complete once cell cz is done
+        const int pz = cz - 1;
+        if (pz >= z0 && pz < z1) out[pz] = a0;
+        a0 = a1;
+        a1 = a2;
+        a2 = a3;
+        a3 = 0.0;
+    }
+}
+
+int launch_anterp(cudaStream_t st, const Geometry& g, DevAtoms& a, DevCells& c, DevLevels& L,
+                  ErrRec* err) {
+    const BinP p = make_binp(g);
+    const int tx = (p.d[0] + 3) / 4, ty = (p.d[1] + 7) / 8, ns = (p.d[2] + kAnterpSeg - 1) / kAnterpSeg;
+    const int64_t warps = int64_t(tx) * ty * ns;
+    k_anterp<<<int((warps * 32 + 127) / 128), 128, 0, st>>>(p, tx, ty, ns, c.start, a.aw,
+                                                            L.charge + g.lv[0].offset, err);
+    return 1;
+}
+
+// ============================================================================
+// K4 / K7: restriction and prolongation, reference order (bitwise)
+// ============================================================================
+struct XferP {
+    int fd[3], cd[3];
+    const int* base[3];
+    const double* w[3];
+    const int* rcnt[3];
+    const int* ridx[3];
+    const double* rw[3];
+};
+
+static XferP make_xfer(const Geometry& g, int k, DevLevels& L) {
+    XferP p;
+    for (int ax = 0; ax < 3; ++ax) {
+        p.fd[ax] = g.lv[k].dims[ax];
+        p.cd[ax] = g.lv[k + 1].dims[ax];
+        p.base[ax] = L.tr_base[k][ax];
+        p.w[ax] = L.tr_w[k][ax];
+        p.rcnt[ax] = L.tr_rcnt[k][ax];
+        p.ridx[ax] = L.tr_ridx[k][ax];
+        p.rw[ax] = L.tr_rw[k][ax];
+    }
+    return p;
+}
+
+// coarse(I,J,K) = sum over fine points in row-major order of ((q*wx)*wy)*wz,
+// skipping zero charges (src/msm_phases.cpp:67-89)
+__global__ void k_restrict(XferP p, const double* __restrict__ fine, double* coarse,
+                           const ErrRec* err) {
+    const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t m = int64_t(p.cd[0]) * p.cd[1] * p.cd[2];
+    if (idx >= m || failed(err)) return;
+    const int K = int(idx % p.cd[2]);
+    const int J = int((idx / p.cd[2]) % p.cd[1]);
+    const int I = int(idx / (int64_t(p.cd[2]) * p.cd[1]));
+    const int ni = p.rcnt[0][I], nj = p.rcnt[1][J], nk = p.rcnt[2][K];
+    double acc = 0.0;
+    for (int a = 0; a < ni; ++a) {
+        const int i = p.ridx[0][I * kRestrictMax + a];
+        const double wx = p.rw[0][I * kRestrictMax + a];
+        for (int b = 0; b < nj; ++b) {
+            const int j = p.ridx[1][J * kRestrictMax + b];
+            const double wy = p.rw[1][J * kRestrictMax + b];
+            const double* row = fine + (size_t(i) * p.fd[1] + j) * p.fd[2];
+            for (int c = 0; c < nk; ++c) {
+                const double q = row[p.ridx[2][K * kRestrictMax + c]];
+                if (q == 0.0) continue;
+                const double qab = __dmul_rn(__dmul_rn(q, wx), wy);
+                acc = __dadd_rn(acc, __dmul_rn(qab, p.rw[2][K * kRestrictMax + c]));
+            }
+        }
+    }
+    coarse[idx] = acc;
+}
+
+// fine(i,j,k) += sum_a wx[a] (sum_b wy[b] (sum_c wz[c] u_coarse)) (src/msm_phases.cpp:177-189)
+__global__ void k_prolong(XferP p, const double* __restrict__ coarse, double* fine,
+                          const ErrRec* err) {
+    const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t m = int64_t(p.fd[0]) * p.fd[1] * p.fd[2];
+    if (idx >= m || failed(err)) return;
+    const int k = int(idx % p.fd[2]);
+    const int j = int((idx / p.fd[2]) % p.fd[1]);
+    const int i = int(idx / (int64_t(p.fd[2]) * p.fd[1]));
+    const int bx = p.base[0][i], by = p.base[1][j], bz = p.base[2][k];
+    const double* wx = p.w[0] + 4 * i;
+    const double* wy = p.w[1] + 4 * j;
+    const double* wz = p.w[2] + 4 * k;
+    double acc = 0.0;
+    for (int a = 0; a < 4; ++a) {
+        double accb = 0.0;
+        for (int b = 0; b < 4; ++b) {
+            const double* row = coarse + (size_t(bx + a) * p.cd[1] + (by + b)) * p.cd[2] + bz;
+            double accc = 0.0;
+            for (int c = 0; c < 4; ++c) accc = __dadd_rn(accc, __dmul_rn(wz[c], row[c]));
+            accb = __dadd_rn(accb, __dmul_rn(wy[b], accc));
+        }
+        acc = __dadd_rn(acc, __dmul_rn(wx[a], accb));
+    }
+    fine[idx] = __dadd_rn(fine[idx], acc);
+}
+
+int launch_restrict(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err) {
+    const int64_t m = int64_t(g.lv[k + 1].size);
+    k_restrict<<<int((m + 127) / 128), 128, 0, st>>>(make_xfer(g, k, L), L.charge + g.lv[k].offset,
+                                                     L.charge + g.lv[k + 1].offset, err);
+    return 1;
+}
+
+int launch_prolong(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err) {
+    const int64_t m = int64_t(g.lv[k].size);
+    k_prolong<<<int((m + 127) / 128), 128, 0, st>>>(make_xfer(g, k, L), L.pot + g.lv[k + 1].offset,
+                                                    L.pot + g.lv[k].offset, err);
+    return 1;
+}
+
+// ============================================================================
+// K5 / K6: 3-D stencil convolution u(t) = sum_d K(d) q(t - d), clipped at the
+// lattice edges (no wrap, src/msm_phases.cpp:119-121).  CTA = 32 y-rows (one
+// per lane) x (kConvNWZ warps x kConvB consecutive z) at one x-plane.  For each
+// source plane the CTA stages a zero-padded (y, z) slab in shared memory; the
+// odd row pitch makes the lane-per-row loads conflict-free.  Each thread keeps
+// kConvB accumulators and a rolling register window along z, so one shared
+// load feeds up to kConvL FMAs.
+// ============================================================================
+struct ConvJob {
+    const double* q;
+    double* u;
+    const int4* rows;
+    const int* dxb;
+    const double* taps;
+    int d0, d1, d2;
+    int Rx, Ry, Rz;
+    int ty, tz;
+    int blk0;
+    int P, SY, SZ;
+};
+
+struct ConvJobs {
+    ConvJob j[kMaxLevels];
+    int njobs;
+};
+
+template <int B, int L, int NWZ>
+__global__ void __launch_bounds__(32 * NWZ) k_conv(ConvJobs J, const ErrRec* err) {
+    extern __shared__ double slab[];
+    if (failed(err)) return;
+    int b = blockIdx.x;
+    int jj = 0;
+    while (jj + 1 < J.njobs && b >= J.j[jj + 1].blk0) ++jj;
+    const ConvJob jb = J.j[jj];
+    b -= jb.blk0;
+    const int tzi = b % jb.tz;
+    const int rest = b / jb.tz;
+    const int tyi = rest % jb.ty;
+    const int x = rest / jb.ty;
+    const int y0 = tyi * 32, z0 = tzi * (B * NWZ);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int zw = z0 + w * B; // first output z of this warp
+    double acc[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) acc[i] = 0.0;
+    const int ylo = y0, yhi = min(y0 + 31, jb.d1 - 1);
+    for (int dx = -jb.Rx; dx <= jb.Rx; ++dx) {
+        const int xs = x - dx;
+        if (xs < 0 || xs >= jb.d0) continue;
+        const int r0 = jb.dxb[dx + jb.Rx], r1 = jb.dxb[dx + jb.Rx + 1];
+        if (r0 == r1) continue;
+        __syncthreads();
+        const double* plane = jb.q + size_t(xs) * jb.d1 * jb.d2;
+        for (int idx = threadIdx.x; idx < jb.SY * jb.SZ; idx += blockDim.x) {
+            const int r = idx / jb.SZ, cc = idx - r * jb.SZ;
+            const int ys = y0 - jb.Ry + r, zs = z0 - jb.Rz + cc;
+            double v = 0.0;
+            if (ys >= 0 && ys < jb.d1 && zs >= 0 && zs < jb.d2) v = plane[size_t(ys) * jb.d2 + zs];
+            slab[r * jb.P + cc] = v;
+        }
+        __syncthreads();
+        for (int r = r0; r < r1; ++r) {
+            const int4 row = jb.rows[r]; // dx, dy, m, tap_off
+            const int dy = row.y, m = row.z;
+            if (ylo - dy > jb.d1 - 1 || yhi - dy < 0) continue; // no source row in range
+            // chunks whose sources z - dz (dz = -m + t) intersect [0, d2)
+            const int nch = (2 * m + L) / L;
+            // output z uses source z + j - m for tap j; keep the chunks whose
+            // sources reach [0, d2) for some z in [zw, zw + B)
+            const int jlo = max(0, m - zw - B + 1);
+            const int jhi = min(nch * L - 1, jb.d2 - 1 + m - zw);
+            if (jlo > jhi) continue;
+            const int c_lo = jlo / L, c_hi = jhi / L;
+            const double* srow = slab + (lane - dy + jb.Ry) * jb.P + (w * B + jb.Rz - m);
+            const double* tp = jb.taps + row.w;
+            double win[B + L - 1];
+#pragma unroll
+            for (int i = 0; i < B + L - 1; ++i) win[i] = srow[c_lo * L + i];
+            for (int c = c_lo; c <= c_hi; ++c) {
+                double t[L];
+#pragma unroll
+                for (int j = 0; j < L; ++j) t[j] = __ldg(tp + c * L + j);
+#pragma unroll
+                for (int j = 0; j < L; ++j)
+#pragma unroll
+                    for (int bb = 0; bb < B; ++bb) acc[bb] = fma(t[j], win[j + bb], acc[bb]);
+                if (c < c_hi) {
+#pragma unroll
+                    for (int i = 0; i < B - 1; ++i) win[i] = win[i + L];
+#pragma unroll
+                    for (int i = B - 1; i < B + L - 1; ++i) win[i] = srow[(c + 1) * L + i];
+                }
+            }
+        }
+    }
+    const int y = y0 + lane;
+    if (y < jb.d1) {
+        double* out = jb.u + (size_t(x) * jb.d1 + y) * jb.d2;
+#pragma unroll
+        for (int bb = 0; bb < B; ++bb) {
+            const int z = zw + bb;
+            if (z < jb.d2) out[z] = acc[bb];
+        }
+    }
+}
+
+static ConvJob make_job(const ConvTable& t, const LevelGeom& lv, const double* q, double* u,
+                        const int4* rows, const int* dxb, const double* taps, int blk0) {
+    ConvJob j;
+    j.q = q;
+    j.u = u;
+    j.rows = rows;
+    j.dxb = dxb;
+    j.taps = taps;
+    j.d0 = lv.dims[0];
+    j.d1 = lv.dims[1];
+    j.d2 = lv.dims[2];
+    j.Rx = t.Rx;
+    j.Ry = t.Ry;
+    j.Rz = t.Rz;
+    j.ty = (j.d1 + 31) / 32;
+    j.tz = (j.d2 + kConvZ - 1) / kConvZ;
+    j.blk0 = blk0;
+    j.SY = 32 + 2 * t.Ry;
+    j.SZ = kConvZ + 2 * t.Rz + kConvL;
+    j.P = j.SZ | 1;
+    return j;
+}
+
+size_t conv_smem_bytes(const ConvTable& t) {
+    const int SY = 32 + 2 * t.Ry;
+    const int SZ = kConvZ + 2 * t.Rz + kConvL;
+    return size_t(SY) * size_t(SZ | 1) * sizeof(double);
+}
+
+cudaError_t conv_prepare(size_t bytes) {
+    return cudaFuncSetAttribute(k_conv<kConvB, kConvL, kConvNWZ>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(std::max<size_t>(bytes, 48 * 1024)));
+}
+
+static int launch_conv_jobs(cudaStream_t st, ConvJobs& J, int blocks, const ErrRec* err) {
+    size_t smem = 0;
+    for (int i = 0; i < J.njobs; ++i) smem = std::max(smem, size_t(J.j[i].SY) * J.j[i].P * sizeof(double));
+    k_conv<kConvB, kConvL, kConvNWZ><<<blocks, 32 * kConvNWZ, smem, st>>>(J, err);
+    return 1;
+}
+
+int launch_lattice(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err) {
+    if (g.levels < 2) return 0;
+    ConvJobs J;
+    J.njobs = 0;
+    int blocks = 0;
+    for (int k = 0; k + 1 < g.levels; ++k) {
+        const LevelGeom& lv = g.lv[k];
+        ConvJob j = make_job(g.lattice[k], lv, L.charge + lv.offset, L.pot + lv.offset, L.rows[k],
+                             L.dxb[k], L.taps[k], blocks);
+        blocks += j.d0 * j.ty * j.tz;
+        J.j[J.njobs++] = j;
+    }
+    return launch_conv_jobs(st, J, blocks, err);
+}
+
+int launch_top(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err) {
+    const int k = g.levels - 1;
+    const LevelGeom& lv = g.lv[k];
+    ConvJobs J;
+    J.njobs = 1;
+    J.j[0] = make_job(g.top, lv, L.charge + lv.offset, L.pot + lv.offset, L.rows[k], L.dxb[k],
+                      L.taps[k], 0);
+    const int blocks = J.j[0].d0 * J.j[0].ty * J.j[0].tz;
+    return launch_conv_jobs(st, J, blocks, err);
+}
+
+// ============================================================================
+// K8: interpolation + long-range forces + assembly (src/msm_phases.cpp:195-222,
+// src/msm.cpp:16-48, 69-86), reference arithmetic order.
+// ============================================================================
+struct InterpP {
+    double o[3];
+    double inv_h;
+    int d[3];
+    double self_term; // smoothing_gamma(0)/a
+    double kc;
+};
+
+__device__ __forceinline__ void interp_atom(const InterpP& p, const double* __restrict__ pot,
+                                            double px, double py, double pz, double& u,
+                                            double& gx, double& gy, double& gz) {
+    const double pp[3] = {px, py, pz};
+    double w[3][4], dw[3][4];
+    int base[3];
+    for (int ax = 0; ax < 3; ++ax) {
+        const double t = __dmul_rn(__dsub_rn(pp[ax], p.o[ax]), p.inv_h);
+        base[ax] = int(floor(t)) - 1;
+        for (int d = 0; d < 4; ++d) {
+            const double xi = __dsub_rn(t, double(base[ax] + d));
+            w[ax][d] = phi_rn(xi);
+            dw[ax][d] = __dmul_rn(dphi_rn(xi), p.inv_h);
+        }
+    }
+    double acc = 0.0;
+    gx = gy = gz = 0.0;
+    for (int a = 0; a < 4; ++a) {
+        double accb = 0.0;
+        for (int b = 0; b < 4; ++b) {
+            const double* row = pot + (size_t(base[0] + a) * p.d[1] + (base[1] + b)) * p.d[2] + base[2];
+            double accc = 0.0;
+            for (int c = 0; c < 4; ++c) {
+                const double uu = __ldg(row + c);
+                accc = __dadd_rn(accc, __dmul_rn(w[2][c], uu));
+                gx = __dadd_rn(gx, __dmul_rn(__dmul_rn(__dmul_rn(dw[0][a], w[1][b]), w[2][c]), uu));
+                gy = __dadd_rn(gy, __dmul_rn(__dmul_rn(__dmul_rn(w[0][a], dw[1][b]), w[2][c]), uu));
+                gz = __dadd_rn(gz, __dmul_rn(__dmul_rn(__dmul_rn(w[0][a], w[1][b]), dw[2][c]), uu));
+            }
+            accb = __dadd_rn(accb, __dmul_rn(w[1][b], accc));
+        }
+        acc = __dadd_rn(acc, __dmul_rn(w[0][a], accb));
+    }
+    u = acc;
+}
+
+static InterpP make_interp(const Geometry& g) {
+    InterpP p;
+    for (int ax = 0; ax < 3; ++ax) {
+        p.o[ax] = g.lv[0].origin[ax];
+        p.d[ax] = g.lv[0].dims[ax];
+    }
+    p.inv_h = g.inv_h0;
+    p.self_term = g.self_term;
+    p.kc = g.units.coulomb_constant;
+    return p;
+}
+
+__global__ void k_interp(InterpP p, const int* __restrict__ total, const int* __restrict__ perm,
+                         const double* __restrict__ xs, const double* __restrict__ ys,
+                         const double* __restrict__ zs, const double* __restrict__ qs,
+                         const double* __restrict__ pot, const double* __restrict__ phis,
+                         const double* __restrict__ fsx, const double* __restrict__ fsy,
+                         const double* __restrict__ fsz, DevOut o, const ErrRec* err) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= *total || failed(err)) return;
+    double u, gx, gy, gz;
+    const double q = qs[s];
+    interp_atom(p, pot, xs[s], ys[s], zs[s], u, gx, gy, gz);
+    const double ul = __dsub_rn(u, __dmul_rn(q, p.self_term));  // msm.cpp:73
+    const double kq = __dmul_rn(p.kc, q);                          // msm.cpp:47
+    const int i = perm[s];
+    o.fx[i] = __dsub_rn(fsx[s], __dmul_rn(gx, kq));
+    o.fy[i] = __dsub_rn(fsy[s], __dmul_rn(gy, kq));
+    o.fz[i] = __dsub_rn(fsz[s], __dmul_rn(gz, kq));
+    const double ph = __dadd_rn(phis[s], ul);                       // msm.cpp:80
+    if (o.phi) o.phi[i] = ph;
+    if (o.phis) o.phis[i] = phis[s];
+    if (o.phil) o.phil[i] = ul;
+    if (o.e) o.e[i] = __dmul_rn(__dmul_rn(0.5, q), ph);             // msm.cpp:83
+}
+
+// energy: deterministic two-level tree over e[] in original index order
+__global__ void __launch_bounds__(256) k_energy1(int64_t n, const double* __restrict__ e,
+                                                 double* partial, const ErrRec* err) {
+    __shared__ double sh[256];
+    if (failed(err)) return;
+    const int64_t base = int64_t(blockIdx.x) * 4096 + threadIdx.x * 16;
+    double s = 0.0;
+    for (int k = 0; k < 16; ++k)
+        if (base + k < n) s += e[base + k];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+__global__ void __launch_bounds__(256) k_energy2(int nb, const double* __restrict__ partial,
+                                                 double kc, double* out, const ErrRec* err) {
+    __shared__ double sh[256];
+    if (failed(err)) return;
+    double s = 0.0;
+    for (int i = threadIdx.x; i < nb; i += 256) s += partial[i];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sh[0] * kc;
+}
+
+int reduce_blocks(int64_t n) { return int((n + 4095) / 4096) > 0 ? int((n + 4095) / 4096) : 1; }
+
+int launch_interp(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c,
+                  DevLevels& L, DevOut& o, ErrRec* err, int want_energy) {
+    if (n == 0) return 0;
+    k_interp<<<int((n + 127) / 128), 128, 0, st>>>(make_interp(g), c.start + g.ncells, a.perm, a.xs,
+                                                   a.ys, a.zs, a.qs, L.pot + g.lv[0].offset, a.phis,
+                                                   a.fsx, a.fsy, a.fsz, o, err);
+    if (!want_energy) return 1;
+    const int nb = reduce_blocks(n);
+    k_energy1<<<nb, 256, 0, st>>>(n, o.e, o.partial, err);
+    k_energy2<<<1, 256, 0, st>>>(nb, o.partial, g.units.coulomb_constant, o.energy, err);
+    return 3;
+}
+
+// Decide the evaluation's outcome with the reference's precedence:
+// short_range errors (first pair in i<j order) > coverage (min particle).
+__global__ void k_finalize(const double* __restrict__ x, const double* __restrict__ y,
+                           const double* __restrict__ z, ErrRec* err) {
+    if (err->kind) return;
+    if (err->overflow) {
+        err->kind = kOverflowKind;
+        err->step = err->cur_step;
+        return;
+    }
+    if (err->pair_key != ~0ull) {
+        const int i = int(err->pair_key >> 32), j = int(err->pair_key & 0xffffffffu);
+        const double dx = __dsub_rn(x[i], x[j]), dy = __dsub_rn(y[i], y[j]), dz = __dsub_rn(z[i], z[j]);
+        const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+        err->kind = r2 == 0.0 ? MSMB_ERR_COINCIDENT : MSMB_ERR_DOMAIN;
+        err->err_i = i;
+        err->err_j = j;
+        err->step = err->cur_step;
+        return;
+    }
+    if (err->cov_count > 0) {
+        err->kind = MSMB_ERR_COVERAGE;
+        err->err_i = err->cov_min;
+        err->err_j = -1;
+        err->step = err->cur_step;
+    }
+}
+
+int launch_finalize(cudaStream_t st, const DevState& s, ErrRec* err) {
+    k_finalize<<<1, 1, 0, st>>>(s.x, s.y, s.z, err);
+    return 1;
+}
+
+__global__ void k_reset_err(ErrRec* err, int step) {
+    err->kind = 0;
+    err->step = -1;
+    err->overflow = 0;
+    err->cov_count = 0;
+    err->pair_key = ~0ull;
+    err->cov_min = LLONG_MAX;
+    err->err_i = -1;
+    err->err_j = -1;
+    err->cur_step = step;
+    err->pairs = 0;
+    err->candidates = 0;
+}
+
+int launch_reset_err(cudaStream_t st, ErrRec* err, int step) {
+    k_reset_err<<<1, 1, 0, st>>>(err, step);
+    return 1;
+}
+
+// ============================================================================
+// K9: velocity Verlet (src/integrate.cpp:24-33), reference arithmetic:
+// c = ((0.5*dt)*conv)/m;  v += F*c;  [v += F*c];  r += v*dt
+// `kicks` = 2 fuses the closing half-kick of step s-1 with the opening one of s.
+// ============================================================================
+__global__ void k_kick_drift(int64_t n, double* x, double* y, double* z, double* vx, double* vy,
+                             double* vz, const double* __restrict__ m, const double* __restrict__ fx,
+                             const double* __restrict__ fy, const double* __restrict__ fz,
+                             double dt, double hdc, int kicks, ErrRec* err) {
+    if (failed(err)) return;
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i == 0) err->pairs = 0, err->candidates = 0, err->cur_step += 1;
+    if (i >= n) return;
+    const double c = __ddiv_rn(hdc, m[i]);
+    double a = vx[i], b = vy[i], d = vz[i];
+    const double Fx = fx[i], Fy = fy[i], Fz = fz[i];
+    for (int k = 0; k < kicks; ++k) {
+        a = __dadd_rn(a, __dmul_rn(Fx, c));
+        b = __dadd_rn(b, __dmul_rn(Fy, c));
+        d = __dadd_rn(d, __dmul_rn(Fz, c));
+    }
+    vx[i] = a;
+    vy[i] = b;
+    vz[i] = d;
+    x[i] = __dadd_rn(x[i], __dmul_rn(a, dt));
+    y[i] = __dadd_rn(y[i], __dmul_rn(b, dt));
+    z[i] = __dadd_rn(z[i], __dmul_rn(d, dt));
+}
+
+__global__ void k_kick(int64_t n, double* vx, double* vy, double* vz, const double* __restrict__ m,
+                       const double* __restrict__ fx, const double* __restrict__ fy,
+                       const double* __restrict__ fz, double hdc, const ErrRec* err) {
+    if (failed(err)) return;
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double c = __ddiv_rn(hdc, m[i]);
+    vx[i] = __dadd_rn(vx[i], __dmul_rn(fx[i], c));
+    vy[i] = __dadd_rn(vy[i], __dmul_rn(fy[i], c));
+    vz[i] = __dadd_rn(vz[i], __dmul_rn(fz[i], c));
+}
+
+int launch_kick_drift(cudaStream_t st, DevState& s, const DevOut& o, double dt, double conv,
+                      int kicks, ErrRec* err) {
+    const double hdc = 0.5 * dt * conv; // (0.5*dt)*conv, host IEEE, same as the reference
+    k_kick_drift<<<int((s.n + 255) / 256) > 0 ? int((s.n + 255) / 256) : 1, 256, 0, st>>>(
+        s.n, s.x, s.y, s.z, s.vx, s.vy, s.vz, s.m, o.fx, o.fy, o.fz, dt, hdc, kicks, err);
+    return 1;
+}
+
+int launch_kick(cudaStream_t st, DevState& s, const DevOut& o, double dt, double conv,
+                ErrRec* err) {
+    if (s.n == 0) return 0;
+    const double hdc = 0.5 * dt * conv;
+    k_kick<<<int((s.n + 255) / 256), 256, 0, st>>>(s.n, s.vx, s.vy, s.vz, s.m, o.fx, o.fy, o.fz, hdc,
+                                                   err);
+    return 1;
+}
+
+// ============================================================================
+// K10: parareal state algebra (src/parareal.cpp:58-90)
+// ============================================================================
+__global__ void __launch_bounds__(256) k_state_sub(int64_t n, DevState a, DevState b, double* dpos,
+                                                   double* dvel, double* partial) {
+    __shared__ double sh[256];
+    const int64_t base = int64_t(blockIdx.x) * 4096 + threadIdx.x * 16;
+    double s = 0.0;
+    for (int k = 0; k < 16; ++k) {
+        const int64_t i = base + k;
+        if (i >= n) break;
+        const double dx = __dsub_rn(a.x[i], b.x[i]), dy = __dsub_rn(a.y[i], b.y[i]),
+                     dz = __dsub_rn(a.z[i], b.z[i]);
+        dpos[3 * i] = dx;
+        dpos[3 * i + 1] = dy;
+        dpos[3 * i + 2] = dz;
+        dvel[3 * i] = __dsub_rn(a.vx[i], b.vx[i]);
+        dvel[3 * i + 1] = __dsub_rn(a.vy[i], b.vy[i]);
+        dvel[3 * i + 2] = __dsub_rn(a.vz[i], b.vz[i]);
+        s = __dadd_rn(s, __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+    }
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+__global__ void k_state_add(int64_t n, DevState base, const double* __restrict__ dpos,
+                            const double* __restrict__ dvel, DevState out) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out.x[i] = __dadd_rn(base.x[i], dpos[3 * i]);
+    out.y[i] = __dadd_rn(base.y[i], dpos[3 * i + 1]);
+    out.z[i] = __dadd_rn(base.z[i], dpos[3 * i + 2]);
+    out.vx[i] = __dadd_rn(base.vx[i], dvel[3 * i]);
+    out.vy[i] = __dadd_rn(base.vy[i], dvel[3 * i + 1]);
+    out.vz[i] = __dadd_rn(base.vz[i], dvel[3 * i + 2]);
+}
+
+__global__ void __launch_bounds__(256) k_rms(int64_t n, DevState a, DevState b, double* partial) {
+    __shared__ double sh[256];
+    const int64_t base = int64_t(blockIdx.x) * 4096 + threadIdx.x * 16;
+    double s = 0.0;
+    for (int k = 0; k < 16; ++k) {
+        const int64_t i = base + k;
+        if (i >= n) break;
+        const double dx = __dsub_rn(a.x[i], b.x[i]), dy = __dsub_rn(a.y[i], b.y[i]),
+                     dz = __dsub_rn(a.z[i], b.z[i]);
+        s = __dadd_rn(s, __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+    }
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+int launch_state_sub(cudaStream_t st, int64_t n, const DevState& a, const DevState& b,
+                     double* dpos, double* dvel, double* partial, int nblk) {
+    k_state_sub<<<nblk, 256, 0, st>>>(n, a, b, dpos, dvel, partial);
+    return 1;
+}
+
+int launch_state_add(cudaStream_t st, int64_t n, const DevState& base, const double* dpos,
+                     const double* dvel, DevState& out) {
+    k_state_add<<<int((n + 255) / 256), 256, 0, st>>>(n, base, dpos, dvel, out);
+    return 1;
+}
+
+int launch_rms_change(cudaStream_t st, int64_t n, const DevState& a, const DevState& b,
+                      double* partial, int nblk) {
+    k_rms<<<nblk, 256, 0, st>>>(n, a, b, partial);
+    return 1;
+}
+
+__global__ void k_aos_to_soa(int64_t n, const double* __restrict__ aos, double* x, double* y, double* z) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    x[i] = aos[3 * i];
+    y[i] = aos[3 * i + 1];
+    z[i] = aos[3 * i + 2];
+}
+
+__global__ void k_soa_to_aos(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
+                             const double* __restrict__ z, double* aos) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    aos[3 * i] = x[i];
+    aos[3 * i + 1] = y[i];
+    aos[3 * i + 2] = z[i];
+}
+
+int launch_aos_to_soa(cudaStream_t st, int64_t n, const double* aos, double* x, double* y, double* z) {
+    if (n == 0) return 0;
+    k_aos_to_soa<<<int((n + 255) / 256), 256, 0, st>>>(n, aos, x, y, z);
+    return 1;
+}
+
+int launch_soa_to_aos(cudaStream_t st, int64_t n, const double* x, const double* y, const double* z,
+                      double* aos) {
+    if (n == 0) return 0;
+    k_soa_to_aos<<<int((n + 255) / 256), 256, 0, st>>>(n, x, y, z, aos);
+    return 1;
+}
+
+__global__ void k_debug_cells(int64_t n, BinP p, const double* x, const double* y, const double* z,
+                              int* cells, int* covered) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double pp[3] = {x[i], y[i], z[i]};
+    int ok = 1;
+    for (int ax = 0; ax < 3; ++ax) {
+        const double t = __dmul_rn(__dsub_rn(pp[ax], p.o[ax]), p.inv_h);
+        const double f = floor(t);
+        const bool c = (f >= 1.0) && (f <= double(p.d[ax]) - 3.0);
+        ok &= c ? 1 : 0;
+        cells[3 * i + ax] = (f > -2147483648.0 && f < 2147483647.0) ? int(f) : INT_MIN;
+    }
+    covered[i] = ok;
+}
+
+int launch_debug_cells(cudaStream_t st, const Geometry& g, const DevState& s, int* cells, int* covered) {
+    if (s.n == 0) return 0;
+    k_debug_cells<<<int((s.n + 255) / 256), 256, 0, st>>>(s.n, make_binp(g), s.x, s.y, s.z, cells, covered);
+    return 1;
+}
+
+__global__ void k_debug_interp(int64_t n, InterpP p, const double* x, const double* y,
+                               const double* z, const double* pot, double* u) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double gx, gy, gz;
+    interp_atom(p, pot, x[i], y[i], z[i], u[i], gx, gy, gz);
+}
+
+int launch_debug_interp(cudaStream_t st, const Geometry& g, const DevState& s, const double* pot0,
+                        double* u) {
+    if (s.n == 0) return 0;
+    k_debug_interp<<<int((s.n + 127) / 128), 128, 0, st>>>(s.n, make_interp(g), s.x, s.y, s.z, pot0, u);
+    return 1;
+}
+
+} // namespace msmb

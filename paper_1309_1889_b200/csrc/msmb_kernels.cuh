@@ -1,0 +1,108 @@
+// Device-side declarations: argument bundles and launch wrappers for the
+// sm_100a kernels in msmb_kernels.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "msmb_internal.h"
+
+namespace msmb {
+
+// Per-workspace device pointers (all device memory).
+struct DevAtoms {       // sorted-order working set, capacity n
+    int* key;           // [n] sorted-cell index of atom i (original order), -1 = not binned
+    int* rank;          // [n]
+    int* perm;          // [n] sorted slot -> original index
+    int* outlist;       // [n] out-of-coverage atoms
+    double* xs; double* ys; double* zs; double* qs;  // sorted positions / charges
+    float4* f4;         // sorted fp32 copies (screening)
+    double* aw;         // [n*12] anterpolation weights: q*wx[4], wy[4], wz[4]
+    double* phis;       // [n] short-range potential (per unit charge), sorted order
+    double* fsx; double* fsy; double* fsz; // short-range forces (with k_C), sorted order
+};
+
+struct DevCells {
+    int* count;         // [ncells+1]
+    int* start;         // [ncells+1]
+    int* col_cnt;       // [ncols+1] clusters per column
+    int* col_off;       // [ncols+1] first cluster of each column
+    int2* clu;          // [max_clusters] (first sorted slot, count)
+    float4* blo; float4* bhi; // cluster bounding boxes
+    int* nclu;          // [1]
+    int* plist;         // [max_clusters * cap]
+    int* pcnt;          // [max_clusters]
+    int* scan_tmp;      // scratch for the multi-block scan
+};
+
+struct DevLevels {      // concatenated lattices + tables
+    double* charge;     // [lattice_total]
+    double* pot;        // [lattice_total]
+    // transfer tables per transition k and axis
+    int* tr_base[kMaxLevels][3];
+    double* tr_w[kMaxLevels][3];
+    int* tr_rcnt[kMaxLevels][3];
+    int* tr_ridx[kMaxLevels][3];
+    double* tr_rw[kMaxLevels][3];
+    // stencil tables: lattice levels then top (index levels-1)
+    int4* rows[kMaxLevels];
+    int* dxb[kMaxLevels];
+    double* taps[kMaxLevels];
+};
+
+struct DevState {       // a device-resident ParticleSystem (SoA)
+    int64_t n;
+    double* x; double* y; double* z;
+    double* vx; double* vy; double* vz;
+    double* q; double* m;
+};
+
+struct DevOut {         // per-atom outputs in original order (optional)
+    double* fx; double* fy; double* fz;
+    double* phi; double* phis; double* phil;
+    double* e;          // [n] 0.5 q phi
+    double* partial;    // [nblocks] energy partial sums
+    double* energy;     // [1]
+};
+
+// Launch wrappers (all asynchronous on `st`).  Each returns the number of kernel
+// launches issued so the engine can count them.
+int launch_bin(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& a, DevCells& c,
+               ErrRec* err);
+int launch_sort(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& a, DevCells& c,
+                ErrRec* err);
+int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c,
+                    ErrRec* err, int cap);
+int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
+                 DevCells& c, ErrRec* err, int cap);
+int launch_anterp(cudaStream_t st, const Geometry& g, DevAtoms& a, DevCells& c, DevLevels& L,
+                  ErrRec* err);
+int launch_restrict(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err);
+int launch_lattice(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
+int launch_top(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
+int launch_prolong(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err);
+int launch_interp(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c,
+                  DevLevels& L, DevOut& o, ErrRec* err, int want_energy);
+int launch_finalize(cudaStream_t st, const DevState& s, ErrRec* err);
+int launch_kick_drift(cudaStream_t st, DevState& s, const DevOut& o, double dt, double conv,
+                      int kicks, ErrRec* err);
+int launch_kick(cudaStream_t st, DevState& s, const DevOut& o, double dt, double conv,
+                ErrRec* err);
+int launch_reset_err(cudaStream_t st, ErrRec* err, int step);
+// parareal state algebra (src/parareal.cpp:58-90)
+int launch_state_sub(cudaStream_t st, int64_t n, const DevState& a, const DevState& b,
+                     double* dpos, double* dvel, double* partial, int nblk);
+int launch_state_add(cudaStream_t st, int64_t n, const DevState& base, const double* dpos,
+                     const double* dvel, DevState& out);
+int launch_rms_change(cudaStream_t st, int64_t n, const DevState& a, const DevState& b,
+                      double* partial, int nblk);
+int reduce_blocks(int64_t n);
+// AoS <-> SoA
+int launch_aos_to_soa(cudaStream_t st, int64_t n, const double* aos, double* x, double* y, double* z);
+int launch_soa_to_aos(cudaStream_t st, int64_t n, const double* x, const double* y, const double* z,
+                      double* aos);
+// debug: level-0 cell triples
+int launch_debug_cells(cudaStream_t st, const Geometry& g, const DevState& s, int* cells, int* covered);
+// debug: stand-alone interpolation of a level-0 potential at atoms (no sort)
+int launch_debug_interp(cudaStream_t st, const Geometry& g, const DevState& s, const double* pot0,
+                        double* u);
+
+} // namespace msmb

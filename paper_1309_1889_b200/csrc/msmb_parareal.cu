@@ -1,0 +1,370 @@
+// Device-resident parareal driver: the reference's parareal_init /
+// parareal_iterate / parareal_run (src/parareal.cpp:94-239) with every
+// lambda / g / delta state kept in HBM.  Propagations go through the fine and
+// coarse msmb_field handles (each a CUDA-graph Verlet propagate); the state
+// algebra (state_sub / state_add / rms_pos_change, src/parareal.cpp:58-90) runs
+// as sm_100a kernels.  Only the rows the algorithm reads are kept (the last two
+// lambda rows, the last g and delta rows), which is observationally identical
+// to the reference's full history.
+//
+// The Executor of the reference (src/parareal.cpp:11-36) only changes where fine
+// slices run; results are independent of it (pure propagators).  On one GPU the
+// fine slices run back to back on the fine field's stream; the multi-GPU split of
+// the fine sweep is in paper_1309_1889_b200/parallel.py (one process per GPU).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "msmb_engine.cuh"
+
+namespace msmb {
+
+struct Delta {
+    DBuf buf; // 6n: dpos (3n AoS) then dvel (3n AoS)
+    double rms_pos = 0.0;
+    double* dpos() const { return buf.as<double>(); }
+    double* dvel(int64_t n) const { return buf.as<double>() + 3 * size_t(n); }
+};
+
+struct PR {
+    const msmb_parareal_config* cfg;
+    int64_t n;
+    cudaStream_t st; // fine field's stream for the algebra
+    DBuf partial;
+    int nblk;
+    int64_t g_evals = 0, f_evals = 0, f_skipped = 0;
+    StateBuf proto; // q, m, box
+};
+
+static void ckp(cudaError_t e, const char* w) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(w) + ": " + cudaGetErrorString(e));
+}
+
+static std::unique_ptr<StateBuf> new_state(PR& P) {
+    auto s = std::make_unique<StateBuf>();
+    ckp(s->alloc(P.n), "cudaMalloc state");
+    for (int ax = 0; ax < 3; ++ax) s->box[ax] = P.proto.box[ax];
+    return s;
+}
+
+static void copy_state(PR& P, StateBuf& dst, const StateBuf& src) {
+    ckp(cudaMemcpyAsync(dst.buf.p, src.buf.p, src.buf.bytes, cudaMemcpyDeviceToDevice, P.st), "copy");
+    for (int ax = 0; ax < 3; ++ax) dst.box[ax] = src.box[ax];
+}
+
+static double host_sum(PR& P) {
+    std::vector<double> h(size_t(P.nblk));
+    ckp(cudaMemcpyAsync(h.data(), P.partial.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, P.st), "D2H");
+    ckp(cudaStreamSynchronize(P.st), "sync");
+    double s = 0.0;
+    for (double v : h) s += v;
+    return s;
+}
+
+static double rms_change(PR& P, const StateBuf& a, const StateBuf& b) { // parareal.cpp:86-90
+    launch_rms_change(P.st, P.n, a.dev(), b.dev(), P.partial.as<double>(), P.nblk);
+    return std::sqrt(host_sum(P) / (3.0 * double(P.n)));
+}
+
+static std::unique_ptr<Delta> state_sub(PR& P, const StateBuf& a, const StateBuf& b) { // :58-73
+    auto d = std::make_unique<Delta>();
+    ckp(d->buf.alloc(sizeof(double) * 6 * size_t(P.n > 0 ? P.n : 1)), "cudaMalloc delta");
+    launch_state_sub(P.st, P.n, a.dev(), b.dev(), d->dpos(), d->dvel(P.n), P.partial.as<double>(), P.nblk);
+    d->rms_pos = std::sqrt(host_sum(P) / (3.0 * double(P.n)));
+    return d;
+}
+
+static std::unique_ptr<Delta> copy_delta(PR& P, const Delta& src) {
+    auto d = std::make_unique<Delta>();
+    ckp(d->buf.alloc(src.buf.bytes), "cudaMalloc delta");
+    ckp(cudaMemcpyAsync(d->buf.p, src.buf.p, src.buf.bytes, cudaMemcpyDeviceToDevice, P.st), "copy");
+    d->rms_pos = src.rms_pos;
+    return d;
+}
+
+static std::unique_ptr<StateBuf> state_add(PR& P, const StateBuf& base, const Delta& d) { // :75-82
+    auto o = new_state(P);
+    copy_state(P, *o, base); // charges, masses
+    DevState od = o->dev();
+    launch_state_add(P.st, P.n, base.dev(), d.dpos(), d.dvel(P.n), od);
+    return o;
+}
+
+// propagate(spec, in, units) into a new state.  The field's scratch system is
+// the working buffer so its captured CUDA graphs are reused across calls.
+static int prop(PR& P, const msmb_propagator& sp, const StateBuf& in, std::unique_ptr<StateBuf>& out) {
+    msmb_field* f = sp.field;
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    ckp(cudaStreamSynchronize(P.st), "sync");
+    if (f->scratch.n != P.n || !f->scratch.buf.p) ckp(f->scratch.alloc(P.n), "alloc scratch");
+    ckp(cudaMemcpyAsync(f->scratch.buf.p, in.buf.p, in.buf.bytes, cudaMemcpyDeviceToDevice, f->stream), "copy");
+    for (int ax = 0; ax < 3; ++ax) f->scratch.box[ax] = in.box[ax];
+    const int rc = engine_propagate(f, f->scratch, sp.dt, sp.steps_per_slice,
+                                    P.cfg->units.energy_to_native);
+    if (rc) return rc;
+    out = new_state(P);
+    ckp(cudaMemcpyAsync(out->buf.p, f->scratch.buf.p, in.buf.bytes, cudaMemcpyDeviceToDevice, f->stream), "copy");
+    ckp(cudaStreamSynchronize(f->stream), "sync");
+    return MSMB_OK;
+}
+
+using Row = std::vector<std::unique_ptr<StateBuf>>;
+using DRow = std::vector<std::unique_ptr<Delta>>;
+
+struct Window {
+    int points = 0;
+    int rows = 0;             // rows created so far (reference w.rows())
+    Row lam_prev2, lam_prev;  // lambda rows rows-2 and rows-1
+    Row lam0;                 // only [0] (the window's initial condition) is kept
+    Row g_prev;               // g row rows-1
+    DRow d_prev;              // delta row rows-1
+    int msmb_rc = 0;
+};
+
+static int pr_init(PR& P, const StateBuf& v, int t, Window& w) { // parareal.cpp:94-115
+    w = Window{};
+    w.points = t;
+    w.lam_prev.resize(size_t(t) + 1);
+    w.g_prev.resize(size_t(t) + 1);
+    w.d_prev.resize(size_t(t) + 1);
+    w.lam_prev[0] = new_state(P);
+    copy_state(P, *w.lam_prev[0], v);
+    w.lam0.resize(1);
+    w.lam0[0] = new_state(P);
+    copy_state(P, *w.lam0[0], v);
+    for (int n = 1; n <= t; ++n) {
+        const int rc = prop(P, P.cfg->coarse, *w.lam_prev[n - 1], w.lam_prev[n]);
+        if (rc) return rc;
+        P.g_evals++;
+        w.g_prev[n] = new_state(P);
+        copy_state(P, *w.g_prev[n], *w.lam_prev[n]);
+    }
+    w.rows = 1;
+    return MSMB_OK;
+}
+
+static int pr_iterate(PR& P, Window& w) { // parareal.cpp:117-180
+    const int t = w.points;
+    const int prev = w.rows - 1;
+    std::vector<char> skip(size_t(t) + 1, 0);
+    if (P.cfg->has_skip_threshold && w.rows >= 2) // metastable_skip_indices :117-127
+        for (int n = 1; n <= t; ++n)
+            if (rms_change(P, *w.lam_prev[n - 1], *w.lam_prev2[n - 1]) < P.cfg->skip_threshold) skip[n] = 1;
+    DRow deltas(size_t(t) + 1);
+    for (int n = 1; n <= t; ++n)
+        if (skip[n]) {
+            deltas[n] = copy_delta(P, *w.d_prev[n]);
+            P.f_skipped++;
+        }
+    for (int n = 1; n <= t; ++n) { // the executor's work list
+        if (skip[n]) continue;
+        std::unique_ptr<StateBuf> f;
+        const int rc = prop(P, P.cfg->fine, *w.lam_prev[n - 1], f);
+        if (rc) return rc;
+        deltas[n] = state_sub(P, *f, *w.g_prev[n]);
+        P.f_evals++;
+    }
+    Row row(size_t(t) + 1), grow(size_t(t) + 1);
+    row[0] = new_state(P);
+    copy_state(P, *row[0], *w.lam0[0]);
+    for (int n = 1; n <= t; ++n) {
+        std::unique_ptr<StateBuf> g;
+        if (prev == 0 && n == 1) {
+            g = new_state(P);
+            copy_state(P, *g, *w.g_prev[1]);
+        } else {
+            const int rc = prop(P, P.cfg->coarse, *row[n - 1], g);
+            if (rc) return rc;
+            P.g_evals++;
+        }
+        row[n] = state_add(P, *g, *deltas[n]);
+        grow[n] = std::move(g);
+    }
+    w.lam_prev2 = std::move(w.lam_prev);
+    w.lam_prev = std::move(row);
+    w.g_prev = std::move(grow);
+    w.d_prev = std::move(deltas);
+    w.rows++;
+    ckp(cudaStreamSynchronize(P.st), "sync");
+    return MSMB_OK;
+}
+
+static Error validate(const msmb_parareal_config* c) { // parareal.cpp:43-56
+    auto E = [](const char* m) { return Error{MSMB_ERR_CONFIG, -1, -1, -1, m}; };
+    if (c->window_points < 1) return E("window_points must be >= 1");
+    if (c->max_iter < 1) return E("max_iter must be >= 1");
+    if (!(c->tol > 0.0)) return E("tol must be > 0");
+    const msmb_propagator* sp[2] = {&c->fine, &c->coarse};
+    for (auto* s : sp) { // PropagatorSpec::validate, integrate.cpp:7-11
+        if (!s->field) return E("propagator has no force field");
+        if (!(s->dt > 0.0)) return E("dt must be > 0");
+        if (s->steps_per_slice < 1) return E("steps_per_slice must be >= 1");
+    }
+    Error e = validate_units(c->units);
+    if (e.kind) return e;
+    const double sf = c->fine.dt * c->fine.steps_per_slice, sg = c->coarse.dt * c->coarse.steps_per_slice;
+    if (std::fabs(sf - sg) > 1e-12 * std::max(std::fabs(sf), std::fabs(sg)))
+        return E("fine and coarse propagators span different slice lengths");
+    if (c->has_skip_threshold && !(c->skip_threshold >= 0.0)) return E("skip threshold must be >= 0");
+    return Error{};
+}
+
+static int setup(PR& P, const msmb_parareal_config* cfg, int64_t n, const double* pos,
+                 const double* vel, const double* q, const double* mass, const double* box) {
+    P.cfg = cfg;
+    P.n = n;
+    msmb_field* f = cfg->fine.field;
+    P.st = f->stream;
+    P.nblk = reduce_blocks(n);
+    ckp(P.partial.alloc(sizeof(double) * size_t(P.nblk)), "alloc");
+    ckp(P.proto.alloc(n), "alloc");
+    for (int ax = 0; ax < 3; ++ax) P.proto.box[ax] = box[ax];
+    // upload through the fine field's host entry point machinery
+    std::vector<double> soa(size_t(n) * 8);
+    for (int64_t i = 0; i < n; ++i) {
+        for (int ax = 0; ax < 3; ++ax) {
+            soa[size_t(ax) * n + i] = pos[3 * i + ax];
+            soa[size_t(3 + ax) * n + i] = vel[3 * i + ax];
+        }
+        soa[size_t(6) * n + i] = q[i];
+        soa[size_t(7) * n + i] = mass[i];
+    }
+    ckp(cudaMemcpy(P.proto.buf.p, soa.data(), sizeof(double) * soa.size(), cudaMemcpyHostToDevice), "H2D");
+    return MSMB_OK;
+}
+
+static void download(PR& P, const StateBuf& s, double* pos, double* vel) {
+    std::vector<double> soa(size_t(P.n) * 6);
+    ckp(cudaStreamSynchronize(P.st), "sync");
+    ckp(cudaMemcpy(soa.data(), s.buf.p, sizeof(double) * soa.size(), cudaMemcpyDeviceToHost), "D2H");
+    for (int64_t i = 0; i < P.n; ++i)
+        for (int ax = 0; ax < 3; ++ax) {
+            if (pos) pos[3 * i + ax] = soa[size_t(ax) * P.n + i];
+            if (vel) vel[3 * i + ax] = soa[size_t(3 + ax) * P.n + i];
+        }
+}
+
+} // namespace msmb
+
+using namespace msmb;
+
+static int pr_fail(const msmb_parareal_config* cfg, const Error& e) {
+    if (cfg && cfg->fine.field) cfg->fine.field->last = e;
+    return e.kind;
+}
+
+static int pr_propagate_error(const msmb_parareal_config* cfg, int rc) {
+    // a propagation failed: surface the failing field's error on the fine handle
+    if (cfg->coarse.field && cfg->coarse.field->last.kind == rc && cfg->fine.field != cfg->coarse.field &&
+        cfg->fine.field->last.kind != rc)
+        cfg->fine.field->last = cfg->coarse.field->last;
+    return rc;
+}
+
+extern "C" int msmb_parareal_window(const msmb_parareal_config* cfg, int64_t n, const double* pos_xyz,
+                                    const double* vel_xyz, const double* q, const double* mass,
+                                    const double box[3], int t_points, int k_iters, double* row_pos,
+                                    double* row_vel, double* delta_rms, int64_t* counts) {
+    Error e = validate(cfg);
+    if (e.kind) return pr_fail(cfg, e);
+    try {
+        cudaSetDevice(cfg->fine.field->device);
+        PR P;
+        setup(P, cfg, n, pos_xyz, vel_xyz, q, mass, box);
+        Window w;
+        int rc = pr_init(P, P.proto, t_points, w);
+        for (int k = 0; rc == MSMB_OK && k < k_iters; ++k) rc = pr_iterate(P, w);
+        if (rc) return pr_propagate_error(cfg, rc);
+        for (int i = 0; i <= t_points; ++i)
+            download(P, *w.lam_prev[i], row_pos ? row_pos + 3 * n * i : nullptr,
+                     row_vel ? row_vel + 3 * n * i : nullptr);
+        if (delta_rms) {
+            delta_rms[0] = 0.0;
+            for (int i = 1; i <= t_points; ++i) delta_rms[i] = w.d_prev[i] ? w.d_prev[i]->rms_pos : 0.0;
+        }
+        if (counts) {
+            counts[0] = P.g_evals;
+            counts[1] = P.f_evals;
+            counts[2] = P.f_skipped;
+        }
+        cfg->fine.field->last = Error{};
+        return MSMB_OK;
+    } catch (const std::exception& ex) {
+        return pr_fail(cfg, Error{MSMB_ERR_CUDA, -1, -1, -1, ex.what()});
+    }
+}
+
+extern "C" int msmb_parareal_run(const msmb_parareal_config* cfg, int64_t n, const double* pos_xyz,
+                                 const double* vel_xyz, const double* q, const double* mass,
+                                 const double box[3], int total_points, double* traj_pos,
+                                 double* traj_vel, int64_t* report) {
+    Error e = validate(cfg);
+    if (e.kind) return pr_fail(cfg, e);
+    if (total_points < 1) return pr_fail(cfg, Error{MSMB_ERR_CONFIG, -1, -1, -1, "total_points must be >= 1"});
+    try {
+        cudaSetDevice(cfg->fine.field->device);
+        PR P;
+        setup(P, cfg, n, pos_xyz, vel_xyz, q, mass, box);
+        auto current = new_state(P);
+        copy_state(P, *current, P.proto);
+        int remaining = total_points, window_idx = 0, out_idx = 0, rc = MSMB_OK;
+        while (remaining > 0 && rc == MSMB_OK) { // parareal.cpp:193-235
+            ++window_idx;
+            const int t = std::min(cfg->window_points, remaining);
+            Window w;
+            rc = pr_init(P, *current, t, w);
+            int prefix = 0;
+            for (int k = 0; rc == MSMB_OK && k < cfg->max_iter; ++k) {
+                rc = pr_iterate(P, w);
+                if (rc) break;
+                prefix = 0;
+                bool unbroken = true;
+                for (int m = 1; m <= t; ++m) {
+                    const double change = rms_change(P, *w.lam_prev[m], *w.lam_prev2[m]);
+                    const bool ok = change <= cfg->tol;
+                    if (unbroken && ok)
+                        prefix = m;
+                    else
+                        unbroken = false;
+                }
+                if (cfg->short_circuit && prefix == t) break;
+            }
+            if (rc) break;
+            if (prefix == 0) {
+                if (report) {
+                    report[0] = P.g_evals;
+                    report[1] = P.f_evals;
+                    report[2] = P.f_skipped;
+                    report[3] = window_idx;
+                    report[4] = 0;
+                }
+                return pr_fail(cfg, Error{MSMB_ERR_NONCONVERGENCE, -1, -1, -1,
+                                          "window " + std::to_string(window_idx) +
+                                              " did not converge within max_iter=" +
+                                              std::to_string(cfg->max_iter)});
+            }
+            for (int m = 1; m <= prefix; ++m, ++out_idx)
+                download(P, *w.lam_prev[m], traj_pos ? traj_pos + 3 * n * out_idx : nullptr,
+                         traj_vel ? traj_vel + 3 * n * out_idx : nullptr);
+            copy_state(P, *current, *w.lam_prev[prefix]);
+            remaining -= prefix;
+        }
+        if (rc) return pr_propagate_error(cfg, rc);
+        if (report) {
+            report[0] = P.g_evals;
+            report[1] = P.f_evals;
+            report[2] = P.f_skipped;
+            report[3] = window_idx;
+            report[4] = 1;
+        }
+        cfg->fine.field->last = Error{};
+        return MSMB_OK;
+    } catch (const std::exception& ex) {
+        return pr_fail(cfg, Error{MSMB_ERR_CUDA, -1, -1, -1, ex.what()});
+    }
+}
