@@ -22,6 +22,7 @@ Reference interface -> here:
 from __future__ import annotations
 
 import ctypes as C
+import sys
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -305,6 +306,8 @@ class MsmField(ForceField):
 
     def __del__(self):
         h = getattr(self, "_h", None)
+        if sys.is_finalizing():  # process teardown releases the device anyway
+            return
         if h is not None and h.value:
             try:
                 _native.lib().msmb_destroy(h)
@@ -354,6 +357,8 @@ class DeviceSystem:
 
     def __del__(self):
         h = getattr(self, "_h", None)
+        if sys.is_finalizing():
+            return
         if h is not None and h.value:
             try:
                 _native.lib().msmb_system_destroy(h)
