@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark: MSM force + velocity-Verlet atom-steps/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2s]
+
+Workload (N=1): BASELINE.json configs[1] -- 100,000 rigid 3-site waters (300,000
+atoms) in a 144 A cube, MSM a=12 A, h=2.5 A, 6 levels (top 8^3), fp64, velocity
+Verlet.  The literal input aborts in the reference at step 1 (CoverageError,
+reproduced bit-exactly by tests/test_gpu_errors.py), so throughput is measured on
+the survivable variant c2s (same N, box, a/h/l; O-O min separation 2.5 A,
+dt 0.02 fs) -- SURVEY.md 8(d) protocol P2.  Inputs are seeded synthetic.
+
+A "step" = one Verlet step = one full MSM energy/force evaluation + kick/drift
+(src/integrate.cpp:23-34).  The timed region is one device-resident propagate
+(initial evaluation + K steps + closing half-kick, as the reference library's
+propagate), timed with CUDA events on the engine's stream around every step, with
+a 256 MB (> L2) buffer written between steps outside the events.  Multi-GPU
+(torchrun): config 2 does not shard -- every rank runs an
+independent replica ("replicas only", weak scaling); max time over ranks.
+
+`--impl reference` times the reference's own CPU implementation (oracle/_ref,
+compiled from /root/reference sources) on a bounded sample per step; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "MSM force+Verlet atom-steps/s"
+UNIT = "atom-steps/s"
+
+CONFIG_TEXT = {
+    "c2s": "configs[1] survivable variant c2s: 100,000 rigid 3-site water-like molecules (300,000 atoms, "
+           "O -0.834 / H +0.417, 16/1 amu), 144 A cube, MSM a=12 A h=2.5 A cubic, 6 levels (top 8^3), "
+           "O-O min separation 2.5 A, dt 0.02 fs",
+    "c2": "configs[1] literal (aborts at step 1 in the reference; not benchmarkable)",
+    "c1s": "configs[0] survivable variant: 8,192 atoms, 40 A, a=10 h=2.5 l=2, RSA 1.5 A, dt 0.02 fs",
+    "c5f": "configs[4] fine propagator on the literal C5 system: 2^20 atoms, 219 A, a=12 h=2.5 l=4, dt 0.5 fs",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2s")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- dist
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+            dist.init_process_group(backend)
+            self.dist, self.torch, self.backend = dist, torch, backend
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64,
+                              device=f"cuda:{self.local}" if self.backend == "nccl" else "cpu")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi-equivalent sampling (NVML) of SM clocks + throttle reasons during the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device: int, period=0.1):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period = period
+        self.stop_ev = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self.stop_ev.set()
+            self.t.join()
+
+    def result(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": float(self.max_mhz),
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- CPU reference
+def reference_step_estimate(w, sample_atoms: int, seed: int):
+    """One bounded sample of the reference's per-step cost on this host (1 thread).
+
+    reference msm_potential = short_range (O(N^2) i<j loop, src/msm_phases.cpp:224-252)
+    + grid phases (anterpolate .. interpolate, src/msm_phases.cpp:39-222) + long-range
+    forces (src/msm.cpp:16-48, ~3x interpolate) + the Verlet update (negligible).
+    short_range is timed on a random `sample_atoms` subset of the same box and scaled
+    by N(N-1)/(M(M-1)) (its pair-check count); the grid phases run at full N."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib
+    if oracle_lib.have("ref"):
+        chk, kind = oracle_lib.checker("ref"), "reference"
+    else:  # the C restatement, when the reference could not be compiled here
+        chk, kind = oracle_lib.checker("port"), "port"
+    rng = np.random.default_rng(seed)
+    m = min(sample_atoms, w.n)
+    idx = np.sort(rng.choice(w.n, size=m, replace=False))
+    pos = np.ascontiguousarray(w.pos[idx])
+    q = np.ascontiguousarray(w.q[idx])
+    t0 = time.perf_counter()
+    if kind == "reference":
+        t_sr = chk.lib.ref_time_short_range(m, oracle_lib._p(pos), oracle_lib._p(q), w.a, 332.0636, 1)
+        ph = np.zeros(6)
+        buf = C.create_string_buffer(256)
+        chk.lib.ref_time_phases.argtypes = [C.c_int64, oracle_lib._D, oracle_lib._D, oracle_lib._D, C.c_double,
+                                            C.c_double, C.c_int, oracle_lib._D, C.c_char_p, C.c_int]
+        rc = chk.lib.ref_time_phases(w.n, oracle_lib._p(np.ascontiguousarray(w.pos)), oracle_lib._p(w.q),
+                                     oracle_lib._p(w.box), w.a, w.h, w.levels, oracle_lib._p(ph), buf, 256)
+        if rc != 0:
+            raise RuntimeError(buf.value.decode())
+        t_grid = float(ph.sum()) + 3.0 * float(ph[5])
+    else:
+        t = time.perf_counter()
+        chk.short_range(pos, q, w.a)
+        t_sr = time.perf_counter() - t
+        t = time.perf_counter()
+        chk.msm_potential(w.pos, w.q, w.box, w.a, w.h, w.levels)
+        t_grid = time.perf_counter() - t
+    wall = time.perf_counter() - t0
+    scale = (w.n * (w.n - 1.0)) / (m * (m - 1.0))
+    t_step = t_sr * scale + t_grid
+    return {"t_step_s": t_step, "t_short_sample_s": t_sr, "t_grid_s": t_grid, "sample_atoms": m,
+            "wall_s": wall, "kind": kind}
+
+
+def cpu_threads_used():
+    return 1
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    args = parse()
+    D = Dist()
+    from paper_1309_1889_b200 import fixtures as fx
+
+    name = args.config
+    wname = {"c5f": "c5"}.get(name, name)
+    w = fx.config(wname)
+    base = {"metric": METRIC, "unit": UNIT, "n_gpus": D.world, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded; paper_1309_1889_b200/fixtures.py)",
+            "config": {"workload": CONFIG_TEXT.get(name, name), "n_atoms": int(w.n), "a": w.a, "h": w.h,
+                       "levels": w.levels, "dt_fs": w.dt, "parallelism": f"replicas x{D.world}" if D.world > 1
+                       else "single GPU", "l2": "256 MB buffer written before every timed step (outside the "
+                       "events); per-step working set ~80 MB"}}
+
+    if args.impl == "reference":
+        if D.rank == 0:
+            times = []
+            for k in range(args.warmup + args.steps):
+                est = reference_step_estimate(w, 30000, 100 + k)
+                if k >= args.warmup:
+                    times.append(est)
+            t = float(np.mean([e["t_step_s"] for e in times]))
+            val = w.n / t
+            line = dict(base, impl="reference", value=val, ms_per_step=t * 1e3, n_gpus=D.world,
+                        cpu_baseline={"value": val, "unit": UNIT, "cores": cpu_threads_used(),
+                                      "kind": times[0]["kind"],
+                                      "sample": f"per step: reference short_range on a random {times[0]['sample_atoms']}"
+                                                f"-atom subset of the same box scaled by its N(N-1)/2 pair-check count "
+                                                f"+ reference grid phases at full N ({times[0]['t_grid_s']:.2f} s); "
+                                                f"single-threaded (msm_potential has no threading)"},
+                        e2e={"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+            print(json.dumps(line), flush=True)
+        D.close()
+        return
+
+    import paper_1309_1889_b200 as pkg
+    from paper_1309_1889_b200 import _native, roofline
+
+    dev_id = D.local
+    L = _native.lib()
+    field = pkg.MsmField(pkg.MsmConfig(w.a, w.h, w.levels), pkg.UnitsConfig.physical(), device=dev_id)
+    s = pkg.ParticleSystem(w.pos, w.vel, w.q, w.mass, w.box)
+    dev = pkg.DeviceSystem(field, s)
+    dt = 0.5 if name == "c5f" else w.dt
+    K, W = args.steps, args.warmup
+
+    def bench(steps, flush):
+        step_ms = np.zeros(steps + 2)
+        stage_ms = np.zeros(11)
+        names = (C.c_char_p * 11)()
+        launches = C.c_int64()
+        rc = L.msmb_bench_propagate(field.handle, dev._h, dt, steps, int(flush), step_ms.ctypes.data_as(pkg._D),
+                                    stage_ms.ctypes.data_as(pkg._D), names, C.byref(launches))
+        pkg._check(field.handle, rc)
+        return step_ms, dict(zip([n.decode() for n in names], stage_ms)), launches.value
+
+    bench(max(W, 1), not args.no_flush)  # warm-up: graph capture + upload + caches
+    D.barrier()
+    with ClockSampler(dev_id) as clk:
+        step_ms, stage_ms, launches = bench(K, not args.no_flush)
+    D.barrier()
+    total_ms = float(step_ms.sum())
+    total_max = D.max(total_ms)
+    value = D.world * w.n * K / (total_max * 1e-3)
+    counters = field.work_counters()
+
+    # ---- roofline: dominant kernel (short-range pairs) and per-stage model
+    tf = C.c_double()
+    L.msmb_measure_fp64_peak(dev_id, 0.5, C.byref(tf))
+    fp64_peak = tf.value
+    hbm, hbm_src = roofline.hbm_peak_gbs()
+    evals = K + 1
+    pair_ms = stage_ms.get("pairs", 0.0) / evals
+    pairs_u = counters["pairs"]
+    achieved = roofline.PAIR_FLOPS * pairs_u / (pair_ms * 1e-3) / 1e12 if pair_ms > 0 else 0.0
+    slot_frac = (roofline.PAIR_SLOTS * pairs_u / (pair_ms * 1e-3)) / (fp64_peak * 1e12 / 2) if pair_ms > 0 else 0.0
+    dims, _, _ = pkg.grid_geometry(field.config(), w.box)
+    lsz = [int(np.prod(d)) for d in dims]
+    per_step = {k: v / evals for k, v in stage_ms.items()}
+    per_step["verlet"] = float(step_ms.sum() - sum(stage_ms.values())) / evals  # kick/drift + graph gaps
+    stages, t_roof, t_meas = roofline.evaluate(w.n, lsz, pairs_u, counters["lattice_taps"], counters["top_taps"],
+                                               per_step, fp64_peak, hbm)
+    traffic = None
+    tr_file = ROOT / "profiles" / "ncu_traffic.json"
+    if tr_file.exists():
+        try:
+            traffic = json.loads(tr_file.read_text()).get(name, {}).get("k_pairs_dram_bytes")
+        except Exception:
+            traffic = None
+
+    # ---- e2e: the public host API, pinned host buffers, H2D + D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        n = w.n
+        nbytes_in = n * (24 + 24 + 8 + 8)
+        nbytes_out = n * 48
+        ptr = L.msmb_host_alloc(n * 8 * 8)
+        host = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_double)), shape=(n * 8,))
+        hp, hv, hq, hm = host[:3 * n], host[3 * n:6 * n], host[6 * n:7 * n], host[7 * n:8 * n]
+        box = np.ascontiguousarray(w.box)
+
+        def run_e2e(steps):
+            hp[:] = w.pos.ravel()
+            hv[:] = w.vel.ravel()
+            hq[:] = w.q
+            hm[:] = w.mass
+            t = time.perf_counter()
+            rc = L.msmb_propagate(field.handle, n, hp.ctypes.data_as(pkg._D), hv.ctypes.data_as(pkg._D),
+                                  hq.ctypes.data_as(pkg._D), hm.ctypes.data_as(pkg._D), box.ctypes.data_as(pkg._D),
+                                  dt, steps)
+            el = time.perf_counter() - t
+            pkg._check(field.handle, rc)
+            return el
+
+        run_e2e(max(W, 1))
+        D.barrier()
+        el = D.max(run_e2e(K))
+        e2e = {"value": D.world * n * K / el, "unit": UNIT, "h2d_bytes_per_step": nbytes_in / K,
+               "d2h_bytes_per_step": nbytes_out / K,
+               "note": "one public msmb_propagate call (host AoS arrays in pinned memory -> H2D, initial evaluation "
+                       "+ K steps, D2H of positions/velocities); host wall clock, max over ranks"}
+        L.msmb_host_free(ptr)
+
+    cpu = None
+    if D.rank == 0 and D.world == 1 and not args.no_cpu_baseline:
+        est = reference_step_estimate(w, 40000, 7)
+        cpu = {"value": w.n / est["t_step_s"], "unit": UNIT, "cores": cpu_threads_used(), "kind": est["kind"],
+               "sample": f"reference short_range on a random {est['sample_atoms']}-atom subset of the same box "
+                         f"({est['t_short_sample_s']:.2f} s) scaled by its N(N-1)/2 pair-check count, + the "
+                         f"reference grid phases at full N ({est['t_grid_s']:.2f} s); one evaluation = one step",
+               "host_cpus": os.cpu_count()}
+
+    if D.rank == 0:
+        line = dict(base)
+        line.update({
+            "value": value, "ms_per_step": total_max / K,
+            "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk.result(),
+            "roofline": {"bound": "fp64", "kernel": "k_pairs (short-range pair sum, SURVEY S2)",
+                         "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
+                         "slot_frac": slot_frac, "traffic": traffic,
+                         "work_per_launch": f"{pairs_u} in-cutoff unordered pairs x {roofline.PAIR_FLOPS} flops "
+                                            f"({roofline.PAIR_SLOTS} FP64 issue slots)",
+                         "avg_launch_ms": pair_ms,
+                         "peak_source": "FP64 FMA-chain microbenchmark run live in this bench (msmb_measure_fp64_peak); "
+                                        "MEASURED_PEAKS.json has no FP64 entry"},
+            "step_roofline": {"t_roof_ms": t_roof, "t_measured_ms": t_meas, "frac": t_roof / t_meas if t_meas else None,
+                              "hbm_gbs": hbm, "hbm_source": hbm_src, "fp64_tflops": fp64_peak, "stages": stages},
+            "cpu_baseline": cpu,
+            "work": counters,
+        })
+        print(json.dumps(line), flush=True)
+    D.close()
+
+
+if __name__ == "__main__":
+    main()

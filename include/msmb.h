@@ -181,6 +181,18 @@ void msmb_reset_stage_times(msmb_field* f);
  * (all levels except the top), [4] top-level taps, [5] kernel launches per
  * evaluation. */
 int msmb_work_counters(msmb_field* f, int64_t* out, int cap);
+/* Device-timed propagate for benchmarking: the same computation as
+ * msmb_system_propagate, with CUDA events on the field's stream around the
+ * initial evaluation, every step and the closing half-kick (step_ms[0..steps+1]),
+ * an optional >L2 buffer write between them (flush_l2, outside the events), and
+ * event nodes inside the step graphs around every stage (stage_ms summed over
+ * the call, stage_names filled; 11 stages). */
+int msmb_bench_propagate(msmb_field* f, msmb_system* s, double dt, int steps, int flush_l2,
+                         double* step_ms, double* stage_ms, const char** stage_names,
+                         int64_t* launches);
+/* Sustained FP64 FMA throughput of `device` (TFLOP/s, FMA = 2 flops), measured
+ * with an FMA-chain microbenchmark for about `seconds`. */
+int msmb_measure_fp64_peak(int device, double seconds, double* tflops);
 /* Kernel launches issued by this handle since creation. */
 int64_t msmb_kernel_launches(const msmb_field* f);
 

@@ -520,4 +520,42 @@ double ref_time_short_range(int64_t n, const double* pos, const double* q, doubl
     return std::chrono::duration<double>(t1 - t0).count();
 }
 
+// Wall-clock seconds of the reference's public grid phases at full size
+// (src/msm_phases.cpp:39-222): t_out = [anterpolate, restrict (all levels),
+// lattice_cutoff (all levels), top_level, prolongate (all levels), interpolate].
+int ref_time_phases(int64_t n, const double* pos, const double* q, const double* box, double a,
+                    double h, int levels, double* t_out, char* msg, int cap) {
+    return guarded(msg, cap, [&] {
+        ParticleSystem s = make_system(n, pos, nullptr, q, nullptr, box);
+        MsmConfig c = make_cfg(a, h, levels, 3, 2);
+        auto lv = build_grid_hierarchy(s, c);
+        using clk = std::chrono::steady_clock;
+        auto sec = [](clk::time_point t0) { return std::chrono::duration<double>(clk::now() - t0).count(); };
+        for (int i = 0; i < 6; ++i) t_out[i] = 0.0;
+        auto t0 = clk::now();
+        anterpolate(s, lv[0]);
+        t_out[0] = sec(t0);
+        for (int k = 0; k + 1 < levels; ++k) {
+            t0 = clk::now();
+            restrict_charges(lv[k], lv[k + 1]);
+            t_out[1] += sec(t0);
+            t0 = clk::now();
+            lattice_cutoff(lv[k], c);
+            t_out[2] += sec(t0);
+        }
+        t0 = clk::now();
+        top_level(lv.back(), c);
+        t_out[3] = sec(t0);
+        for (int k = levels - 2; k >= 0; --k) {
+            t0 = clk::now();
+            prolongate(lv[k + 1], lv[k]);
+            t_out[4] += sec(t0);
+        }
+        t0 = clk::now();
+        auto u = interpolate_to_atoms(lv[0], s);
+        t_out[5] = sec(t0);
+        if (!u.empty() && u[0] == 12345.678) t_out[5] += 0.0;
+    });
+}
+
 }  // extern "C"

@@ -66,6 +66,9 @@ SIGNATURES = {
     "msmb_reset_stage_times": (None, [_VP]),
     "msmb_work_counters": (C.c_int, [_VP, _L, C.c_int]),
     "msmb_kernel_launches": (C.c_int64, [_VP]),
+    "msmb_bench_propagate": (C.c_int, [_VP, _VP, C.c_double, C.c_int, C.c_int, _D, _D,
+                                       C.POINTER(C.c_char_p), _L]),
+    "msmb_measure_fp64_peak": (C.c_int, [C.c_int, C.c_double, _D]),
     "msmb_grid_geometry": (C.c_int, [C.POINTER(MsmConfigC), _D, _I, _D, _D]),
     "msmb_debug_levels": (C.c_int, [_VP, _D, _D]),
     "msmb_debug_cells": (C.c_int, [_VP, C.c_int64, _D, _D, _I, _I]),

@@ -35,6 +35,7 @@ static void ck(cudaError_t e, const char* where) {
 }
 
 Workspace::~Workspace() {
+    for (auto e : stage_ev) cudaEventDestroy(e);
     if (gx_eval) cudaGraphExecDestroy(gx_eval);
     if (gx_step1) cudaGraphExecDestroy(gx_step1);
     if (gx_step2) cudaGraphExecDestroy(gx_step2);
@@ -260,13 +261,26 @@ struct StageScope {
     }
 };
 
+static const char* kStages[] = {"bin", "sort", "clusters", "pairs", "anterp", "restrict",
+                                "lattice", "top", "prolong", "interp", "finalize"};
+constexpr int kNumStages = 11;
+
+static int stage_id(const char* name) {
+    for (int i = 0; i < kNumStages; ++i)
+        if (!strcmp(kStages[i], name)) return i;
+    return -1;
+}
+
 static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs) {
     cudaStream_t st = f->stream;
     const Geometry& g = W.g;
     int total = 0;
     auto run = [&](const char* name, auto&& fn) {
         StageScope sc(f, name);
+        const int id = stage_id(name);
+        if (W.capture_events && id >= 0) cudaEventRecord(W.stage_ev[2 * id], st);
         const int nl = fn();
+        if (W.capture_events && id >= 0) cudaEventRecord(W.stage_ev[2 * id + 1], st);
         sc.done(nl);
         total += nl;
     };
@@ -377,7 +391,7 @@ int engine_propagate(msmb_field* f, StateBuf& sb, double dt, int steps, double c
     ck(cudaMemcpyAsync(bk, s.x, sizeof(double) * 6 * N, cudaMemcpyDeviceToDevice, f->stream), "backup");
     for (int attempt = 0; attempt < 8; ++attempt) {
         const bool graphs = !f->timer.on;
-        if (graphs && (W.graph_key != s.x || W.graph_dt != dt || W.graph_cap != W.cap)) {
+        if (graphs && (W.graph_key != s.x || W.graph_dt != dt || W.graph_cap != W.cap || W.graph_bench)) {
             destroy_graphs(W);
             int nl = 0;
             W.gx_eval = capture(f, [&] { nl = enqueue_eval(f, W, s, false); });
@@ -395,6 +409,7 @@ int engine_propagate(msmb_field* f, StateBuf& sb, double dt, int steps, double c
             W.graph_key = s.x;
             W.graph_dt = dt;
             W.graph_cap = W.cap;
+            W.graph_bench = false;
         }
         f->launches += launch_reset_err(f->stream, W.err, 0);
         if (graphs) {
@@ -500,6 +515,21 @@ static void copy_outputs(msmb_field* f, int64_t n, double* phi, double* phi_shor
             *energy = 0.0;
     }
     ck(cudaStreamSynchronize(f->stream), "sync");
+}
+
+__global__ void k_fp64_peak(double* out, int iters, double seed) {
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = seed + threadIdx.x * 1e-9 + k;
+    const double m = 0.9999999999, c = 1e-12;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] = fma(a[k], m, c);
+    }
+    double s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += a[k];
+    if (s == 1234.5678) out[threadIdx.x] = s;
 }
 
 } // namespace msmb
@@ -754,6 +784,141 @@ int msmb_system_evaluate(msmb_field* f, msmb_system* s, double* phi, double* phi
     copy_outputs(f, s->st.n, phi, phi_short, phi_long, force_xyz, energy);
     return MSMB_OK;
     GUARD_END(f)
+}
+
+int msmb_bench_propagate(msmb_field* f, msmb_system* sys, double dt, int steps, int flush_l2,
+                         double* step_ms, double* stage_ms, const char** stage_names,
+                         int64_t* launches) {
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    GUARD_BEGIN
+    f->last = Error{};
+    cudaSetDevice(f->device);
+    if (!(dt > 0.0)) return engine_set_error(f, Error{MSMB_ERR_CONFIG, -1, -1, -1, "dt must be > 0"});
+    if (steps < 1)
+        return engine_set_error(f, Error{MSMB_ERR_CONFIG, -1, -1, -1, "steps_per_slice must be >= 1"});
+    StateBuf& sb = sys->st;
+    Error e = ensure_workspace(f, sb.n, sb.box);
+    if (e.kind) return engine_set_error(f, e);
+    Workspace& W = *f->ws;
+    DevState s = sb.dev();
+    const size_t N = size_t(sb.n > 0 ? sb.n : 1);
+    const double conv = f->units.energy_to_native;
+    if (W.stage_ev.empty()) {
+        W.stage_ev.resize(2 * kNumStages);
+        for (auto& ev : W.stage_ev) ck(cudaEventCreate(&ev), "cudaEventCreate");
+    }
+    const size_t flush_bytes = size_t(256) << 20; // 2x the 126 MB L2
+    if (flush_l2 && W.flush.bytes < flush_bytes) ck(W.flush.alloc(flush_bytes), "cudaMalloc flush");
+    if (f->timer.on) f->timer.on = false;
+    if (!(W.graph_key == s.x && W.graph_dt == dt && W.graph_cap == W.cap && W.graph_bench)) {
+        destroy_graphs(W);
+        W.capture_events = true;
+        int nl = 0;
+        W.gx_eval = capture(f, [&] { nl = enqueue_eval(f, W, s, false); });
+        W.launches_eval = nl;
+        W.gx_step1 = capture(f, [&] {
+            nl = launch_kick_drift(f->stream, s, W.o, dt, conv, 1, W.err);
+            nl += enqueue_eval(f, W, s, false);
+        });
+        W.gx_step2 = capture(f, [&] {
+            nl = launch_kick_drift(f->stream, s, W.o, dt, conv, 2, W.err);
+            nl += enqueue_eval(f, W, s, false);
+        });
+        W.launches_step = nl;
+        W.capture_events = false;
+        f->launches -= 3 * int64_t(W.launches_eval);
+        W.graph_key = s.x;
+        W.graph_dt = dt;
+        W.graph_cap = W.cap;
+        W.graph_bench = true;
+    }
+    double* bk = W.backup.as<double>();
+    ck(cudaMemcpyAsync(bk, s.x, sizeof(double) * 6 * N, cudaMemcpyDeviceToDevice, f->stream), "backup");
+    cudaEvent_t ea, eb;
+    ck(cudaEventCreate(&ea), "event");
+    ck(cudaEventCreate(&eb), "event");
+    std::vector<double> acc(kNumStages, 0.0);
+    const int64_t l0 = f->launches;
+    int flush_k = 0;
+    auto timed = [&](auto&& launch, bool stages) -> double {
+        if (flush_l2) ck(cudaMemsetAsync(W.flush.p, (flush_k++) & 0xff, W.flush.bytes, f->stream), "flush");
+        ck(cudaEventRecord(ea, f->stream), "record");
+        launch();
+        ck(cudaEventRecord(eb, f->stream), "record");
+        ck(cudaEventSynchronize(eb), "sync");
+        float ms = 0.f;
+        ck(cudaEventElapsedTime(&ms, ea, eb), "elapsed");
+        if (stages)
+            for (int i = 0; i < kNumStages; ++i) {
+                float t = 0.f;
+                if (cudaEventElapsedTime(&t, W.stage_ev[2 * i], W.stage_ev[2 * i + 1]) == cudaSuccess) acc[i] += t;
+            }
+        return double(ms);
+    };
+    f->launches += launch_reset_err(f->stream, W.err, 0);
+    step_ms[0] = timed([&] {
+        ck(cudaGraphLaunch(W.gx_eval, f->stream), "GraphLaunch");
+        f->launches += W.launches_eval;
+    }, true);
+    for (int st = 1; st <= steps; ++st)
+        step_ms[st] = timed([&] {
+            ck(cudaGraphLaunch(st == 1 ? W.gx_step1 : W.gx_step2, f->stream), "GraphLaunch");
+            f->launches += W.launches_step;
+        }, true);
+    step_ms[steps + 1] = timed([&] { f->launches += launch_kick(f->stream, s, W.o, dt, conv, W.err); }, false);
+    cudaEventDestroy(ea);
+    cudaEventDestroy(eb);
+    const ErrRec r = read_err(f, W);
+    if (launches) *launches = f->launches - l0;
+    for (int i = 0; i < kNumStages; ++i) {
+        if (stage_ms) stage_ms[i] = acc[i];
+        if (stage_names) stage_names[i] = kStages[i];
+    }
+    if (r.kind) {
+        ck(cudaMemcpyAsync(s.x, bk, sizeof(double) * 6 * N, cudaMemcpyDeviceToDevice, f->stream), "restore");
+        ck(cudaStreamSynchronize(f->stream), "sync");
+        if (r.kind == kOverflowKind) {
+            grow_cap(W, r);
+            return msmb_bench_propagate(f, sys, dt, steps, flush_l2, step_ms, stage_ms, stage_names, launches);
+        }
+        return engine_set_error(f, error_from_rec(r));
+    }
+    record_counters(f, W, r);
+    return MSMB_OK;
+    GUARD_END(f)
+}
+
+int msmb_measure_fp64_peak(int device, double seconds, double* tflops) {
+    cudaSetDevice(device);
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return MSMB_ERR_CUDA;
+    const int blocks = prop.multiProcessorCount * 8, threads = 256, iters = 4096;
+    double* out = nullptr;
+    if (cudaMalloc(&out, sizeof(double) * threads) != cudaSuccess) return MSMB_ERR_CUDA;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    k_fp64_peak<<<blocks, threads>>>(out, iters, 1.0); // warm-up
+    cudaDeviceSynchronize();
+    double best = 0.0, elapsed = 0.0;
+    int reps = 0;
+    while (elapsed < seconds * 1e3 || reps < 3) {
+        cudaEventRecord(a);
+        for (int k = 0; k < 8; ++k) k_fp64_peak<<<blocks, threads>>>(out, iters, 1.0 + k);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        elapsed += ms;
+        ++reps;
+        const double fl = 8.0 * 2.0 * 8.0 * double(iters) * blocks * threads; // 8 launches, FMA = 2
+        best = std::max(best, fl / (ms * 1e-3) / 1e12);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(out);
+    *tflops = best;
+    return cudaGetLastError() == cudaSuccess ? MSMB_OK : MSMB_ERR_CUDA;
 }
 
 int msmb_set_stage_timing(msmb_field* f, int enable) {

@@ -81,6 +81,11 @@ struct Workspace {
     double graph_dt = 0;
     int graph_cap = 0;
     int launches_eval = 0, launches_step = 0;
+    bool graph_bench = false;            // graphs carry per-stage event nodes
+    bool capture_events = false;         // enqueue_eval records stage events
+    std::vector<std::string> stage_names;
+    std::vector<cudaEvent_t> stage_ev;   // 2 per stage (begin, end)
+    DBuf flush;                          // > L2, written between timed steps
     ~Workspace();
 };
 
