@@ -184,9 +184,9 @@ int msmb_work_counters(msmb_field* f, int64_t* out, int cap);
 /* Device-timed propagate for benchmarking: the same computation as
  * msmb_system_propagate, with CUDA events on the field's stream around the
  * initial evaluation, every step and the closing half-kick (step_ms[0..steps+1]),
- * an optional >L2 buffer write between them (flush_l2, outside the events), and
- * event nodes inside the step graphs around every stage (stage_ms summed over
- * the call, stage_names filled; 11 stages). */
+ * and an optional >L2 buffer write between them (flush_l2, outside the events).
+ * stage_names receives the 11 stage names; stage_ms is zero-filled (per-stage
+ * times come from a msmb_set_stage_timing pass). */
 int msmb_bench_propagate(msmb_field* f, msmb_system* s, double dt, int steps, int flush_l2,
                          double* step_ms, double* stage_ms, const char** stage_names,
                          int64_t* launches);

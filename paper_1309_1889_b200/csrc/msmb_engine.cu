@@ -173,6 +173,7 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
     DevCells& c = W->c;
     c.count = walloc<int>(*W, size_t(g.ncells + 1));
     c.start = walloc<int>(*W, size_t(g.ncells + 1));
+    c.nat = walloc<int2>(*W, g.lv[0].size);
     c.col_cnt = walloc<int>(*W, size_t(g.ncols + 1));
     c.col_off = walloc<int>(*W, size_t(g.ncols + 1));
     W->maxclu = n / 32 + g.ncols + 1;
@@ -603,14 +604,27 @@ int msmb_create(const msmb_msm_config* cfg, const msmb_units* units, int device,
     return MSMB_OK;
 }
 
-void msmb_destroy(msmb_field* f) {
-    if (!f) return;
+static void field_free(msmb_field* f) {
     cudaSetDevice(f->device);
     cudaStreamSynchronize(f->stream);
     f->ws.reset();
     f->scratch.buf.reset();
     cudaStreamDestroy(f->stream);
     delete f;
+}
+
+// A field outlives every msmb_system created from it: destroying a field that
+// still has systems only marks it; the last msmb_system_destroy frees it.
+void msmb_destroy(msmb_field* f) {
+    if (!f) return;
+    {
+        std::lock_guard<std::recursive_mutex> lk(f->mu);
+        if (f->refs > 0) {
+            f->destroy_pending = true;
+            return;
+        }
+    }
+    field_free(f);
 }
 
 int msmb_last_error(const msmb_field* f, int* kind, int64_t* idx_i, int64_t* idx_j, int* step,
@@ -703,7 +717,13 @@ int msmb_system_create(msmb_field* f, int64_t n, const double* pos_xyz, const do
     cudaSetDevice(f->device);
     auto* s = new msmb_system();
     s->f = f;
-    fill_state(f, s->st, n, pos_xyz, vel_xyz, q, mass, box);
+    try {
+        fill_state(f, s->st, n, pos_xyz, vel_xyz, q, mass, box);
+    } catch (...) {
+        delete s;
+        throw;
+    }
+    f->refs++;
     *out = s;
     return MSMB_OK;
     GUARD_END(f)
@@ -711,11 +731,18 @@ int msmb_system_create(msmb_field* f, int64_t n, const double* pos_xyz, const do
 
 void msmb_system_destroy(msmb_system* s) {
     if (!s) return;
-    std::lock_guard<std::recursive_mutex> lk(s->f->mu);
-    cudaSetDevice(s->f->device);
-    cudaStreamSynchronize(s->f->stream);
-    if (s->f->ws && s->f->ws->graph_key == s->st.dev().x) destroy_graphs(*s->f->ws);
-    delete s;
+    msmb_field* f = s->f;
+    bool free_field = false;
+    {
+        std::lock_guard<std::recursive_mutex> lk(f->mu);
+        cudaSetDevice(f->device);
+        cudaStreamSynchronize(f->stream);
+        if (f->ws && f->ws->graph_key == s->st.dev().x) destroy_graphs(*f->ws);
+        delete s;
+        f->refs--;
+        free_field = f->destroy_pending && f->refs == 0;
+    }
+    if (free_field) field_free(f);
 }
 
 int msmb_system_upload(msmb_system* s, const double* pos_xyz, const double* vel_xyz) {
@@ -812,7 +839,6 @@ int msmb_bench_propagate(msmb_field* f, msmb_system* sys, double dt, int steps, 
     if (f->timer.on) f->timer.on = false;
     if (!(W.graph_key == s.x && W.graph_dt == dt && W.graph_cap == W.cap && W.graph_bench)) {
         destroy_graphs(W);
-        W.capture_events = true;
         int nl = 0;
         W.gx_eval = capture(f, [&] { nl = enqueue_eval(f, W, s, false); });
         W.launches_eval = nl;
@@ -825,7 +851,6 @@ int msmb_bench_propagate(msmb_field* f, msmb_system* sys, double dt, int steps, 
             nl += enqueue_eval(f, W, s, false);
         });
         W.launches_step = nl;
-        W.capture_events = false;
         f->launches -= 3 * int64_t(W.launches_eval);
         W.graph_key = s.x;
         W.graph_dt = dt;
@@ -848,11 +873,7 @@ int msmb_bench_propagate(msmb_field* f, msmb_system* sys, double dt, int steps, 
         ck(cudaEventSynchronize(eb), "sync");
         float ms = 0.f;
         ck(cudaEventElapsedTime(&ms, ea, eb), "elapsed");
-        if (stages)
-            for (int i = 0; i < kNumStages; ++i) {
-                float t = 0.f;
-                if (cudaEventElapsedTime(&t, W.stage_ev[2 * i], W.stage_ev[2 * i + 1]) == cudaSuccess) acc[i] += t;
-            }
+        (void)stages;
         return double(ms);
     };
     f->launches += launch_reset_err(f->stream, W.err, 0);

@@ -205,12 +205,25 @@ __global__ void k_scatter(int n, const int* __restrict__ key, const int* __restr
     if (k >= 0) perm[start[k] + rank[i]] = i;
 }
 
-// within-cell order = ascending original index (deterministic; cells are small)
-__global__ void k_cellsort(int64_t ncells, const int* __restrict__ start, int* perm,
-                           const ErrRec* err) {
+// within-cell order = ascending original index (deterministic; cells are small);
+// also publishes each level-0 cell's range in natural (x, y, z) row-major order
+__global__ void k_cellsort(int64_t ncells, BinP p, const int* __restrict__ start, int* perm,
+                           int2* nat, const double* __restrict__ x, const double* __restrict__ y,
+                           const double* __restrict__ z, ErrRec* err) {
     const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (c >= ncells || failed(err)) return;
     const int s0 = start[c], s1 = start[c + 1];
+    {
+        int64_t t = c;
+        const int oy = int(t % p.cw);
+        t /= p.cw;
+        const int ox = int(t % p.cw);
+        t /= p.cw;
+        const int cz = int(t % p.d[2]);
+        const int col = int(t / p.d[2]);
+        const int cx = (col / p.ncy) * p.cw + ox, cy = (col % p.ncy) * p.cw + oy;
+        if (cx < p.d[0] && cy < p.d[1]) nat[(size_t(cx) * p.d[1] + cy) * p.d[2] + cz] = make_int2(s0, s1);
+    }
     for (int a = s0 + 1; a < s1; ++a) {
         const int v = perm[a];
         int b = a - 1;
@@ -220,6 +233,15 @@ __global__ void k_cellsort(int64_t ncells, const int* __restrict__ start, int* p
         }
         perm[b + 1] = v;
     }
+    // exactly coincident particles (r2 == 0, src/msm_phases.cpp:237-239) share a cell
+    for (int a = s0; a < s1; ++a)
+        for (int b = a + 1; b < s1; ++b) {
+            const int i = perm[a], j = perm[b];
+            if (x[i] == x[j] && y[i] == y[j] && z[i] == z[j]) {
+                const unsigned long long key = ((unsigned long long)min(i, j) << 32) | (unsigned long long)max(i, j);
+                atomicMin(&err->pair_key, key);
+            }
+        }
 }
 
 // sorted copies + the anterpolation weights of every particle:
@@ -269,7 +291,8 @@ int launch_sort(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms&
     int l = scan_exclusive(st, c.count, c.start, c.scan_tmp, g.ncells + 1);
     if (n == 0) return l;
     k_scatter<<<(n + 255) / 256, 256, 0, st>>>(n, a.key, a.rank, c.start, a.perm, err);
-    k_cellsort<<<int((g.ncells + 255) / 256), 256, 0, st>>>(g.ncells, c.start, a.perm, err);
+    k_cellsort<<<int((g.ncells + 255) / 256), 256, 0, st>>>(g.ncells, make_binp(g), c.start, a.perm,
+                                                            c.nat, s.x, s.y, s.z, err);
     k_gather<<<(n + 255) / 256, 256, 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, s.q,
                                               make_binp(g), a.xs, a.ys, a.zs, a.qs, a.f4, a.aw,
                                               err);
@@ -403,95 +426,140 @@ struct PairP {
     float cut2f;
 };
 
+// 1/sqrt(x) for 0 < x < inf: MUFU.RSQ64H seed (rel. err < 2^-22.9) refined by one
+// cubically convergent Newton step, y += y*e*(1/2 + 3/8 e) with e = 1 - x*y^2
+// (error ~2^-68 before rounding: full double precision).  No special-value path:
+// callers only accumulate pairs with 0 < r2 < a2.
+__device__ __forceinline__ double rsqrt_pos(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double e = fma(-(x * y), y, 1.0);
+    return fma(y * e, fma(e, 0.375, 0.5), y);
+}
+
 __device__ __forceinline__ void record_pair(ErrRec* err, int i, int j) {
     const unsigned long long lo = (unsigned long long)min(i, j), hi = (unsigned long long)max(i, j);
     atomicMin(&err->pair_key, (lo << 32) | hi);
 }
 
-// One warp per i-cluster (lane = i atom).  For every candidate j-cluster: stage
-// its 32 atoms in shared memory (fp32 copy for screening; fp64 words split
-// into conflict-free 32-bit arrays), build each lane's 32-bit in-range mask in
-// fp32 with a safety margin, then walk the set bits so every DP instruction
-// works on a screened pair.  The exact fp64 test r2 < a2 decides inclusion.
-__global__ void __launch_bounds__(kPairWarps * 32)
+// One warp per i-cluster (lane = i atom).  For every candidate j-cluster the warp
+// stages its 32 atoms in shared memory -- fp64 words split into 32-bit rows so
+// any lane->atom mapping reads conflict-free, plus an fp32 screening record
+// (-2x', -2y', -2z', |x'|^2 - cut^2) with x' the position relative to the
+// i-cluster's first atom -- builds each lane's 32-bit in-range mask with 4 packed
+// fp32x2 operations per two candidates (r^2 - cut^2 = |xi'|^2 + |xj'|^2 - cut^2
+// - 2 xi'.xj', sign bits shifted into the mask), then walks the set bits so the
+// DP pipe only sees screened pairs.  The exact fp64 test r2 < a2 decides inclusion
+// (src/msm_phases.cpp:240).  The next j-cluster is prefetched into registers
+// while the current one is processed.  Coincident pairs are caught in k_cellsort.
+__global__ void __launch_bounds__(kPairWarps * 32, 5)
     k_pairs(const int* __restrict__ nclu, const int2* __restrict__ clu,
             const int* __restrict__ plist, const int* __restrict__ pcnt, int cap,
             const double* __restrict__ xs, const double* __restrict__ ys,
             const double* __restrict__ zs, const double* __restrict__ qs,
             const float4* __restrict__ f4, const int* __restrict__ perm, PairP p, double* phis,
             double* fsx, double* fsy, double* fsz, ErrRec* err) {
-    __shared__ float4 s_f[kPairWarps][32];
+    __shared__ __align__(16) float s_sc[kPairWarps][4][32]; // -2x', -2y', -2z', |x'|^2 - cut^2
     __shared__ unsigned s_w[kPairWarps][8][32];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ic = blockIdx.x * kPairWarps + w;
     if (ic >= *nclu || failed(err)) return;
+    double a2 = p.a2, c0 = p.c0, c1 = p.c1, c2 = p.c2, d0 = p.d0, d1 = p.d1;
+    asm volatile("" : "+d"(a2), "+d"(c0), "+d"(c1), "+d"(c2), "+d"(d0), "+d"(d1));
+    const float cut2f = p.cut2f;
     const int2 c = clu[ic];
     const bool vi = lane < c.y;
     const int si = c.x + (vi ? lane : 0);
     const double xi = xs[si], yi = ys[si], zi = zs[si], qi = qs[si];
-    const float4 fi = f4[si];
+    const double rx = xs[c.x], ry = ys[c.x], rz = zs[c.x]; // reference point (uniform)
+    const float xf = float(xi - rx), yf = float(yi - ry), zf = float(zi - rz);
+    const float2 xi2 = make_float2(xf, xf), yi2 = make_float2(yf, yf), zi2 = make_float2(zf, zf);
+    const float nif = fmaf(zf, zf, fmaf(yf, yf, xf * xf));
+    const float2 ni2 = make_float2(nif, nif);
     double ph = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
     unsigned npair = 0, ncand = 0;
     const int nj = pcnt[ic];
     const int* pl = plist + size_t(ic) * cap;
+    int jc_n = 0;
+    int2 cj_n = make_int2(0, 0);
+    double xj_n = 0, yj_n = 0, zj_n = 0, qj_n = 0;
+    auto fetch = [&](int jj) {
+        jc_n = pl[jj];
+        cj_n = clu[jc_n];
+        const int sj = cj_n.x + (lane < cj_n.y ? lane : 0);
+        xj_n = xs[sj];
+        yj_n = ys[sj];
+        zj_n = zs[sj];
+        qj_n = qs[sj];
+    };
+    if (nj > 0) fetch(0);
     for (int jj = 0; jj < nj; ++jj) {
-        const int jc = pl[jj];
-        const int2 cj = clu[jc];
-        const bool vj = lane < cj.y;
-        const int sj = cj.x + (vj ? lane : 0);
-        float4 fj = f4[sj];
-        if (!vj) fj = make_float4(1e30f, 1e30f, 1e30f, 0.f);
-        const double xj = xs[sj], yj = ys[sj], zj = zs[sj], qj = qs[sj];
+        const int jc = jc_n;
+        const bool vj = lane < cj_n.y;
+        const float xj = float(xj_n - rx), yj = float(yj_n - ry), zj = float(zj_n - rz);
         __syncwarp();
-        s_f[w][lane] = fj;
-        s_w[w][0][lane] = __double2loint(xj);
-        s_w[w][1][lane] = __double2hiint(xj);
-        s_w[w][2][lane] = __double2loint(yj);
-        s_w[w][3][lane] = __double2hiint(yj);
-        s_w[w][4][lane] = __double2loint(zj);
-        s_w[w][5][lane] = __double2hiint(zj);
-        s_w[w][6][lane] = __double2loint(qj);
-        s_w[w][7][lane] = __double2hiint(qj);
+        s_sc[w][0][lane] = -2.f * xj;
+        s_sc[w][1][lane] = -2.f * yj;
+        s_sc[w][2][lane] = -2.f * zj;
+        s_sc[w][3][lane] = vj ? fmaf(zj, zj, fmaf(yj, yj, xj * xj)) - cut2f : 3e38f;
+        s_w[w][0][lane] = __double2loint(xj_n);
+        s_w[w][1][lane] = __double2hiint(xj_n);
+        s_w[w][2][lane] = __double2loint(yj_n);
+        s_w[w][3][lane] = __double2hiint(yj_n);
+        s_w[w][4][lane] = __double2loint(zj_n);
+        s_w[w][5][lane] = __double2hiint(zj_n);
+        s_w[w][6][lane] = __double2loint(qj_n);
+        s_w[w][7][lane] = __double2hiint(qj_n);
         __syncwarp();
+        if (jj + 1 < nj) fetch(jj + 1);
+        // ---- screening: bit (31 - t) of mask <=> atom t within cut (fp32, with margin)
         unsigned mask = 0;
-        if (vi) {
 #pragma unroll
-            for (int t = 0; t < 32; ++t) {
-                const float4 pj = s_f[w][t];
-                const float dx = fi.x - pj.x, dy = fi.y - pj.y, dz = fi.z - pj.z;
-                const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-                mask |= (r2 < p.cut2f ? 1u : 0u) << t;
-            }
+        for (int t = 0; t < 32; t += 4) {
+            const float4 mx = *reinterpret_cast<const float4*>(&s_sc[w][0][t]);
+            const float4 my = *reinterpret_cast<const float4*>(&s_sc[w][1][t]);
+            const float4 mz = *reinterpret_cast<const float4*>(&s_sc[w][2][t]);
+            const float4 cc = *reinterpret_cast<const float4*>(&s_sc[w][3][t]);
+            float2 sa = __fadd2_rn(ni2, make_float2(cc.x, cc.y));
+            float2 sb = __fadd2_rn(ni2, make_float2(cc.z, cc.w));
+            sa = __ffma2_rn(make_float2(mx.x, mx.y), xi2, sa);
+            sb = __ffma2_rn(make_float2(mx.z, mx.w), xi2, sb);
+            sa = __ffma2_rn(make_float2(my.x, my.y), yi2, sa);
+            sb = __ffma2_rn(make_float2(my.z, my.w), yi2, sb);
+            sa = __ffma2_rn(make_float2(mz.x, mz.y), zi2, sa);
+            sb = __ffma2_rn(make_float2(mz.z, mz.w), zi2, sb);
+            mask = (mask << 1) | (__float_as_uint(sa.x) >> 31);
+            mask = (mask << 1) | (__float_as_uint(sa.y) >> 31);
+            mask = (mask << 1) | (__float_as_uint(sb.x) >> 31);
+            mask = (mask << 1) | (__float_as_uint(sb.y) >> 31);
         }
-        if (jc == ic) mask &= ~(1u << lane);
-        ncand += __popc(mask);
-        while (__any_sync(FULLMASK, mask != 0)) {
-            if (mask) {
-                const int t = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const double xj2 = __hiloint2double(s_w[w][1][t], s_w[w][0][t]);
-                const double yj2 = __hiloint2double(s_w[w][3][t], s_w[w][2][t]);
-                const double zj2 = __hiloint2double(s_w[w][5][t], s_w[w][4][t]);
-                const double qj2 = __hiloint2double(s_w[w][7][t], s_w[w][6][t]);
-                const double dx = xi - xj2, dy = yi - yj2, dz = zi - zj2;
-                double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-                const long long rb = __double_as_longlong(r2);
-                if (rb == 0) record_pair(err, perm[si], perm[cj.x + t]);
-                // 0 < r2 < a2 as one unsigned compare on the bit patterns
-                const bool in = (unsigned long long)(rb - 1) < (unsigned long long)(p.a2bits - 1);
-                r2 = in ? r2 : p.a2;
-                const double rinv = rsqrt(r2);
-                const double rinv2 = rinv * rinv;
-                const double g = rinv - fma(r2, fma(r2, p.c2, p.c1), p.c0);      // g*(r)
-                const double sd = fma(r2, p.d1, p.d0) - rinv * rinv2;              // g*'(r)/r
-                const double qe = in ? qj2 : 0.0;
-                ph = fma(qe, g, ph);
-                const double wgt = qe * sd;
-                fx = fma(dx, wgt, fx);
-                fy = fma(dy, wgt, fy);
-                fz = fma(dz, wgt, fz);
-                npair += in ? 1u : 0u;
-            }
+        if (!vi) mask = 0;
+        if (jc == ic) mask &= ~(0x80000000u >> lane);
+        const int pc = __popc(mask);
+        ncand += pc;
+        const int iters = __reduce_max_sync(FULLMASK, pc);
+        for (int k = 0; k < iters; ++k) {
+            const int t = __clz(mask) & 31;
+            const bool has = mask != 0;
+            mask &= ~(0x80000000u >> t);
+            const double xj2 = __hiloint2double(s_w[w][1][t], s_w[w][0][t]);
+            const double yj2 = __hiloint2double(s_w[w][3][t], s_w[w][2][t]);
+            const double zj2 = __hiloint2double(s_w[w][5][t], s_w[w][4][t]);
+            const double qj2 = __hiloint2double(s_w[w][7][t], s_w[w][6][t]);
+            const double dx = xi - xj2, dy = yi - yj2, dz = zi - zj2;
+            const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+            const bool in = has && (r2 < a2);
+            const double rinv = rsqrt_pos(r2);
+            const double rinv2 = rinv * rinv;
+            const double g = rinv - fma(r2, fma(r2, c2, c1), c0);   // g*(r)
+            const double sd = fma(-rinv, rinv2, fma(r2, d1, d0));  // g*'(r)/r
+            const double qe = in ? qj2 : 0.0;
+            ph = fma(qe, g, ph);
+            const double wgt = qe * sd;
+            fx = fma(dx, wgt, fx);
+            fy = fma(dy, wgt, fy);
+            fz = fma(dz, wgt, fz);
+            npair += in ? 1u : 0u;
         }
     }
     if (vi) {
@@ -501,10 +569,8 @@ __global__ void __launch_bounds__(kPairWarps * 32)
         fsy[si] = fy * kq;
         fsz[si] = fz * kq;
     }
-    for (int o = 16; o; o >>= 1) {
-        npair += __shfl_xor_sync(FULLMASK, npair, o);
-        ncand += __shfl_xor_sync(FULLMASK, ncand, o);
-    }
+    npair = __reduce_add_sync(FULLMASK, npair);
+    ncand = __reduce_add_sync(FULLMASK, ncand);
     if (lane == 0) {
         atomicAdd(&err->pairs, (unsigned long long)npair);
         atomicAdd(&err->candidates, (unsigned long long)ncand);
@@ -585,70 +651,53 @@ int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& 
 }
 
 // ============================================================================
-// K3: anterpolation as an owner-computes gather.  A thread owns a segment of
-// kAnterpSeg points of one z-line (x, y) and walks the level-0 cells whose
-// stencils reach it, in ascending z, keeping a rolling window of 4 sums.
+// K3: anterpolation as an owner-computes gather (no atomics): one thread per
+// level-0 grid point sums the contributions of the particles in the 4x4x4 cells
+// whose stencils reach it, in a fixed order (cells in x, y, z order, particles
+// in sorted order), using the per-particle weights of k_gather:
+// q_mu += ((q*wx[dx]) * wy[dy]) * wz[dz]  (the reference's qa/qab products,
+// src/msm_phases.cpp:52-57).  Lanes run along z so neighbouring points share cells.
 // ============================================================================
 __global__ void __launch_bounds__(128)
-    k_anterp(BinP p, int tiles_x, int tiles_y, int nseg, const int* __restrict__ start,
-             const double* __restrict__ aw, double* q0, const ErrRec* err) {
+    k_anterp(BinP p, const int2* __restrict__ nat, const double* __restrict__ aw, double* q0,
+             const ErrRec* err) {
     if (failed(err)) return;
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    const int txi = gw % tiles_x;
-    const int rest = gw / tiles_x;
-    const int tyi = rest % tiles_y;
-    const int seg = rest / tiles_y;
-    if (seg >= nseg) return;
-    const int x = txi * 4 + (lane >> 3);
-    const int y = tyi * 8 + (lane & 7);
     const int d0 = p.d[0], d1 = p.d[1], d2 = p.d[2];
-    if (x >= d0 || y >= d1) return;
-    const int z0 = seg * kAnterpSeg;
-    const int z1 = min(z0 + kAnterpSeg, d2);
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    double* out = q0 + (size_t(x) * d1 + y) * d2;
-    for (int cz = z0 - 2; cz <= z1; ++cz) {
-        if (cz >= 1 && cz <= d2 - 3) {
-            for (int ox = 0; ox < 4; ++ox) {
-                const int cx = x - 2 + ox;
-                if (cx < 1 || cx > d0 - 3) continue;
-                const int dxw = 3 - ox; // weight index x - base = x - (cx - 1)
-                for (int oy = 0; oy < 4; ++oy) {
-                    const int cy = y - 2 + oy;
-                    if (cy < 1 || cy > d1 - 3) continue;
-                    const int dyw = 3 - oy;
-                    const int sc = scell_of(p, cx, cy, cz);
-                    const int s1 = start[sc + 1];
-                    for (int s = start[sc]; s < s1; ++s) {
-                        const double* w = aw + size_t(s) * 12;
-                        const double cxy = __dmul_rn(w[dxw], w[4 + dyw]); // (q*wx)*wy
-                        const double4 wz = *reinterpret_cast<const double4*>(w + 8);
-                        a0 = fma(cxy, wz.x, a0);
-                        a1 = fma(cxy, wz.y, a1);
-                        a2 = fma(cxy, wz.z, a2);
-                        a3 = fma(cxy, wz.w, a3);
-                    }
+    const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= int64_t(d0) * d1 * d2) return;
+    const int z = int(idx % d2);
+    const int y = int((idx / d2) % d1);
+    const int x = int(idx / (int64_t(d2) * d1));
+    double acc = 0.0;
+    const int cz_lo = max(1, z - 2), cz_hi = min(d2 - 3, z + 1);
+    for (int ox = 0; ox < 4; ++ox) {
+        const int cx = x - 2 + ox;
+        if (cx < 1 || cx > d0 - 3) continue;
+        const int dxw = 3 - ox; // weight index x - base = x - (cx - 1)
+        for (int oy = 0; oy < 4; ++oy) {
+            const int cy = y - 2 + oy;
+            if (cy < 1 || cy > d1 - 3) continue;
+            const int dyw = 4 + 3 - oy;
+            const int2* row = nat + (size_t(cx) * d1 + cy) * d2;
+            for (int cz = cz_lo; cz <= cz_hi; ++cz) {
+                const int2 r = __ldg(row + cz);
+                const int dzw = 8 + z - cz + 1;
+                for (int s = r.x; s < r.y; ++s) {
+                    const double* w = aw + size_t(s) * 12;
+                    const double cxy = __dmul_rn(__ldg(w + dxw), __ldg(w + dyw));
+                    acc = fma(cxy, __ldg(w + dzw), acc);
                 }
             }
         }
-        // a0 holds point cz-1, complete once cell cz is done
-        const int pz = cz - 1;
-        if (pz >= z0 && pz < z1) out[pz] = a0;
-        a0 = a1;
-        a1 = a2;
-        a2 = a3;
-        a3 = 0.0;
     }
+    q0[idx] = acc;
 }
 
 int launch_anterp(cudaStream_t st, const Geometry& g, DevAtoms& a, DevCells& c, DevLevels& L,
                   ErrRec* err) {
     const BinP p = make_binp(g);
-    const int tx = (p.d[0] + 3) / 4, ty = (p.d[1] + 7) / 8, ns = (p.d[2] + kAnterpSeg - 1) / kAnterpSeg;
-    const int64_t warps = int64_t(tx) * ty * ns;
-    k_anterp<<<int((warps * 32 + 127) / 128), 128, 0, st>>>(p, tx, ty, ns, c.start, a.aw,
-                                                            L.charge + g.lv[0].offset, err);
+    const int64_t m = int64_t(p.d[0]) * p.d[1] * p.d[2];
+    k_anterp<<<int((m + 127) / 128), 128, 0, st>>>(p, c.nat, a.aw, L.charge + g.lv[0].offset, err);
     return 1;
 }
 
@@ -679,9 +728,11 @@ static XferP make_xfer(const Geometry& g, int k, DevLevels& L) {
 }
 
 // coarse(I,J,K) = sum over fine points in row-major order of ((q*wx)*wy)*wz,
-// skipping zero charges (src/msm_phases.cpp:67-89)
-__global__ void k_restrict(XferP p, const double* __restrict__ fine, double* coarse,
-                           const ErrRec* err) {
+// skipping zero charges (src/msm_phases.cpp:67-89).  The three per-axis lists
+// (<= 8 fine indices each) are held in registers; only fine values are loaded
+// in the loop nest.
+__global__ void __launch_bounds__(128) k_restrict(XferP p, const double* __restrict__ fine,
+                                                  double* coarse, const ErrRec* err) {
     const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t m = int64_t(p.cd[0]) * p.cd[1] * p.cd[2];
     if (idx >= m || failed(err)) return;
@@ -689,19 +740,33 @@ __global__ void k_restrict(XferP p, const double* __restrict__ fine, double* coa
     const int J = int((idx / p.cd[2]) % p.cd[1]);
     const int I = int(idx / (int64_t(p.cd[2]) * p.cd[1]));
     const int ni = p.rcnt[0][I], nj = p.rcnt[1][J], nk = p.rcnt[2][K];
+    int iy[kRestrictMax], iz[kRestrictMax];
+    double wy[kRestrictMax], wz[kRestrictMax];
+#pragma unroll
+    for (int a = 0; a < kRestrictMax; ++a) {
+        iy[a] = a < nj ? p.ridx[1][J * kRestrictMax + a] : 0;
+        wy[a] = a < nj ? p.rw[1][J * kRestrictMax + a] : 0.0;
+        iz[a] = a < nk ? p.ridx[2][K * kRestrictMax + a] : 0;
+        wz[a] = a < nk ? p.rw[2][K * kRestrictMax + a] : 0.0;
+    }
     double acc = 0.0;
+#pragma unroll 1
     for (int a = 0; a < ni; ++a) {
-        const int i = p.ridx[0][I * kRestrictMax + a];
+        const int ix = p.ridx[0][I * kRestrictMax + a];
         const double wx = p.rw[0][I * kRestrictMax + a];
-        for (int b = 0; b < nj; ++b) {
-            const int j = p.ridx[1][J * kRestrictMax + b];
-            const double wy = p.rw[1][J * kRestrictMax + b];
-            const double* row = fine + (size_t(i) * p.fd[1] + j) * p.fd[2];
-            for (int c = 0; c < nk; ++c) {
-                const double q = row[p.ridx[2][K * kRestrictMax + c]];
-                if (q == 0.0) continue;
-                const double qab = __dmul_rn(__dmul_rn(q, wx), wy);
-                acc = __dadd_rn(acc, __dmul_rn(qab, p.rw[2][K * kRestrictMax + c]));
+#pragma unroll
+        for (int b = 0; b < kRestrictMax; ++b) {
+            if (b >= nj) break;
+            const double* row = fine + (size_t(ix) * p.fd[1] + iy[b]) * p.fd[2];
+            double q[kRestrictMax];
+#pragma unroll
+            for (int c = 0; c < kRestrictMax; ++c) q[c] = c < nk ? __ldg(row + iz[c]) : 0.0;
+#pragma unroll
+            for (int c = 0; c < kRestrictMax; ++c) {
+                if (c < nk && q[c] != 0.0) {
+                    const double qab = __dmul_rn(__dmul_rn(q[c], wx), wy[b]);
+                    acc = __dadd_rn(acc, __dmul_rn(qab, wz[c]));
+                }
             }
         }
     }
@@ -857,7 +922,7 @@ __global__ void __launch_bounds__(32 * NWZ) k_conv(ConvJobs J, const ErrRec* err
 }
 
 static ConvJob make_job(const ConvTable& t, const LevelGeom& lv, const double* q, double* u,
-                        const int4* rows, const int* dxb, const double* taps, int blk0) {
+                        const int4* rows, const int* dxb, const double* taps, int blk0, int Z) {
     ConvJob j;
     j.q = q;
     j.u = u;
@@ -871,13 +936,19 @@ static ConvJob make_job(const ConvTable& t, const LevelGeom& lv, const double* q
     j.Ry = t.Ry;
     j.Rz = t.Rz;
     j.ty = (j.d1 + 31) / 32;
-    j.tz = (j.d2 + kConvZ - 1) / kConvZ;
+    j.tz = (j.d2 + Z - 1) / Z;
     j.blk0 = blk0;
     j.SY = 32 + 2 * t.Ry;
-    j.SZ = kConvZ + 2 * t.Rz + kConvL;
+    j.SZ = Z + 2 * t.Rz + kConvL;
     j.P = j.SZ | 1;
     return j;
 }
+
+// Two stencil variants: 16 outputs per thread (large lattices: fewest loads per
+// FMA) and 8 outputs per thread (small lattices: twice the CTAs).
+constexpr int kConvBSmall = 8;
+constexpr int kConvZSmall = kConvBSmall * kConvNWZ;
+constexpr int64_t kConvBigPoints = 1500000; // level-0 points above which the 16-wide variant is used
 
 size_t conv_smem_bytes(const ConvTable& t) {
     const int SY = 32 + 2 * t.Ry;
@@ -886,42 +957,85 @@ size_t conv_smem_bytes(const ConvTable& t) {
 }
 
 cudaError_t conv_prepare(size_t bytes) {
-    return cudaFuncSetAttribute(k_conv<kConvB, kConvL, kConvNWZ>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(std::max<size_t>(bytes, 48 * 1024)));
+    const int b = int(std::max<size_t>(bytes, 48 * 1024));
+    cudaError_t e = cudaFuncSetAttribute(k_conv<kConvB, kConvL, kConvNWZ>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_conv<kConvBSmall, kConvL, kConvNWZ>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, b);
 }
 
-static int launch_conv_jobs(cudaStream_t st, ConvJobs& J, int blocks, const ErrRec* err) {
+static int launch_conv_jobs(cudaStream_t st, ConvJobs& J, int blocks, bool big, const ErrRec* err) {
     size_t smem = 0;
     for (int i = 0; i < J.njobs; ++i) smem = std::max(smem, size_t(J.j[i].SY) * J.j[i].P * sizeof(double));
-    k_conv<kConvB, kConvL, kConvNWZ><<<blocks, 32 * kConvNWZ, smem, st>>>(J, err);
+    if (big)
+        k_conv<kConvB, kConvL, kConvNWZ><<<blocks, 32 * kConvNWZ, smem, st>>>(J, err);
+    else
+        k_conv<kConvBSmall, kConvL, kConvNWZ><<<blocks, 32 * kConvNWZ, smem, st>>>(J, err);
     return 1;
 }
 
 int launch_lattice(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err) {
     if (g.levels < 2) return 0;
+    const bool big = int64_t(g.lv[0].size) > kConvBigPoints;
+    const int Z = big ? kConvZ : kConvZSmall;
     ConvJobs J;
     J.njobs = 0;
     int blocks = 0;
     for (int k = 0; k + 1 < g.levels; ++k) {
         const LevelGeom& lv = g.lv[k];
         ConvJob j = make_job(g.lattice[k], lv, L.charge + lv.offset, L.pot + lv.offset, L.rows[k],
-                             L.dxb[k], L.taps[k], blocks);
+                             L.dxb[k], L.taps[k], blocks, Z);
         blocks += j.d0 * j.ty * j.tz;
         J.j[J.njobs++] = j;
     }
-    return launch_conv_jobs(st, J, blocks, err);
+    return launch_conv_jobs(st, J, blocks, big, err);
 }
+
+// Small top levels: one thread per target point, a dense sum over every source
+// point in ascending row-major order with the reference's mul-then-add
+// (src/msm_phases.cpp:153-160); kernel values come from the offset table, which
+// equals the reference's per-pair g(norm(coords[mu]-coords[nu])) whenever the
+// grid coordinates are exact (msmb_geometry.cpp build_top_table).
+__global__ void __launch_bounds__(128)
+    k_top_direct(const double* __restrict__ q, double* u, int d0, int d1, int d2,
+                 const double* __restrict__ taps, int rowlen, const ErrRec* err) {
+    if (failed(err)) return;
+    const int64_t m = int64_t(d0) * d1 * d2;
+    const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= m) return;
+    const int z = int(idx % d2);
+    const int y = int((idx / d2) % d1);
+    const int x = int(idx / (int64_t(d2) * d1));
+    const int Rx = d0 - 1, Ry = d1 - 1, Rz = d2 - 1;
+    double acc = 0.0;
+    for (int xs = 0; xs < d0; ++xs)
+        for (int ys = 0; ys < d1; ++ys) {
+            const double* trow = taps + size_t((x - xs + Rx) * (2 * Ry + 1) + (y - ys + Ry)) * rowlen + (z + Rz);
+            const double* qrow = q + (size_t(xs) * d1 + ys) * d2;
+            for (int zs = 0; zs < d2; ++zs) acc = __dadd_rn(acc, __dmul_rn(__ldg(trow - zs), __ldg(qrow + zs)));
+        }
+    u[idx] = acc;
+}
+
+constexpr int64_t kTopDirectMax = 8192; // top levels up to this many points use k_top_direct
 
 int launch_top(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err) {
     const int k = g.levels - 1;
     const LevelGeom& lv = g.lv[k];
+    if (int64_t(lv.size) <= kTopDirectMax) {
+        const int rowlen = (2 * g.top.Rz + 1 + kConvL - 1) / kConvL * kConvL;
+        k_top_direct<<<int((lv.size + 127) / 128), 128, 0, st>>>(L.charge + lv.offset, L.pot + lv.offset,
+                                                                 lv.dims[0], lv.dims[1], lv.dims[2],
+                                                                 L.taps[k], rowlen, err);
+        return 1;
+    }
     ConvJobs J;
     J.njobs = 1;
     J.j[0] = make_job(g.top, lv, L.charge + lv.offset, L.pot + lv.offset, L.rows[k], L.dxb[k],
-                      L.taps[k], 0);
+                      L.taps[k], 0, kConvZ);
     const int blocks = J.j[0].d0 * J.j[0].ty * J.j[0].tz;
-    return launch_conv_jobs(st, J, blocks, err);
+    return launch_conv_jobs(st, J, blocks, true, err);
 }
 
 // ============================================================================

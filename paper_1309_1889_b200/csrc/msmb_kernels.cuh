@@ -23,6 +23,7 @@ struct DevAtoms {       // sorted-order working set, capacity n
 struct DevCells {
     int* count;         // [ncells+1]
     int* start;         // [ncells+1]
+    int2* nat;          // [d0*d1*d2] level-0 cell (x,y,z row-major) -> sorted range [start, end)
     int* col_cnt;       // [ncols+1] clusters per column
     int* col_off;       // [ncols+1] first cluster of each column
     int2* clu;          // [max_clusters] (first sorted slot, count)
