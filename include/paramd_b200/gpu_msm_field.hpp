@@ -1,0 +1,187 @@
+// paramd_b200/gpu_msm_field.hpp -- drop-in B200 MsmField for the reference
+// library `paramd` (arXiv 1309.1889).  Header-only C++ over the C ABI in msmb.h.
+//
+// The reference's plugin interface is paramd::ForceField
+// (include/paramd/force_field.hpp:14-21): a field evaluates potentials and
+// forces from positions and charges.  GpuMsmField implements it with the
+// sm_100a kernels of libmsmb.so, so any reference code that takes a
+// ForceField -- propagate (src/integrate.cpp:13-36), energy_report
+// (src/integrate.cpp:47-55), parareal_run (src/parareal.cpp:182-239) -- runs its
+// MSM evaluations on the GPU unchanged:
+//
+//     auto ff = std::make_shared<paramd::GpuMsmField>(cfg, units);   // was MsmField
+//     paramd::PropagatorSpec spec{ff, dt, steps};
+//     paramd::ParticleSystem out = paramd::propagate(spec, s, units);
+//
+// Each evaluate() uploads positions/charges and downloads results (the plugin
+// contract is host-side ParticleSystems).  For the device-resident hot path use
+// paramd_b200::propagate / paramd_b200::parareal_run below: same signatures and
+// semantics, the whole trajectory stays in HBM.
+//
+// Errors are rethrown as the reference's exception types with the reference's
+// messages (include/paramd/errors.hpp:12-49).
+#pragma once
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../msmb.h"
+#include "paramd/errors.hpp"
+#include "paramd/force_field.hpp"
+#include "paramd/integrate.hpp"
+#include "paramd/parareal.hpp"
+
+namespace paramd {
+
+namespace detail_b200 {
+[[noreturn]] inline void rethrow(const msmb_field* h, int rc) {
+    int kind = rc;
+    int64_t i = -1, j = -1;
+    int step = -1;
+    char msg[1024] = {0};
+    msmb_last_error(h, &kind, &i, &j, &step, msg, sizeof msg);
+    const std::string m(msg);
+    switch (rc) {
+        case MSMB_ERR_CONFIG: throw ConfigError(m);
+        case MSMB_ERR_DOMAIN: throw DomainError(m);
+        case MSMB_ERR_COVERAGE: throw CoverageError(m);
+        case MSMB_ERR_COINCIDENT: throw CoincidentParticlesError(m);
+        case MSMB_ERR_HIERARCHY: throw HierarchyError(m);
+        case MSMB_ERR_RUNTIME: throw RuntimeFault(m);
+        default: throw Error("msmb: " + m);
+    }
+}
+
+inline msmb_msm_config to_c(const MsmConfig& c) {
+    return msmb_msm_config{c.cutoff_a, c.spacing_h, c.levels_l, c.interp_order_p, c.smoothing_m};
+}
+inline msmb_units to_c(const UnitsConfig& u) { return msmb_units{u.coulomb_constant, u.energy_to_native}; }
+}  // namespace detail_b200
+
+/// paramd::MsmField (force_field.hpp:62-73) evaluated on a B200.
+class GpuMsmField final : public ForceField {
+  public:
+    GpuMsmField(MsmConfig config, UnitsConfig units, int device = 0)
+        : config_(config), units_(units) {
+        const msmb_msm_config c = detail_b200::to_c(config);
+        const msmb_units u = detail_b200::to_c(units);
+        const int rc = msmb_create(&c, &u, device, &h_);
+        if (rc) detail_b200::rethrow(nullptr, rc);
+    }
+    ~GpuMsmField() override { msmb_destroy(h_); }
+    GpuMsmField(const GpuMsmField&) = delete;
+    GpuMsmField& operator=(const GpuMsmField&) = delete;
+
+    PotentialResult evaluate(const ParticleSystem& s) const override {
+        const std::size_t n = s.size();
+        PotentialResult r;
+        r.per_particle_potential.assign(n, 0.0);
+        r.per_particle_force.assign(n, Vec3{});
+        std::vector<double> sp(n), lp(n);
+        const double box[3] = {s.box.x, s.box.y, s.box.z};
+        static_assert(sizeof(Vec3) == 3 * sizeof(double), "Vec3 must be {double x,y,z}");
+        const int rc = msmb_evaluate(h_, static_cast<int64_t>(n),
+                                     reinterpret_cast<const double*>(s.positions.data()),
+                                     s.charges.data(), box, r.per_particle_potential.data(),
+                                     sp.data(), lp.data(),
+                                     reinterpret_cast<double*>(r.per_particle_force.data()),
+                                     &r.total_energy);
+        if (rc) detail_b200::rethrow(h_, rc);
+        r.short_part = std::move(sp);
+        r.long_part = std::move(lp);
+        return r;
+    }
+    double cost_flops_per_step(std::size_t n) const override {
+        return msmb_cost_flops_per_step(h_, static_cast<int64_t>(n));
+    }
+    std::string name() const override { return "msm"; }
+    const MsmConfig& config() const { return config_; }
+    msmb_field* handle() const { return h_; }
+
+  private:
+    MsmConfig config_;
+    UnitsConfig units_;
+    msmb_field* h_ = nullptr;
+};
+
+}  // namespace paramd
+
+namespace paramd_b200 {
+
+/// paramd::propagate (src/integrate.cpp:13-36), device-resident when the spec's
+/// field is a GpuMsmField; any other field runs the reference's own propagate.
+inline paramd::ParticleSystem propagate(const paramd::PropagatorSpec& spec,
+                                        const paramd::ParticleSystem& s,
+                                        const paramd::UnitsConfig& units) {
+    auto* gf = dynamic_cast<const paramd::GpuMsmField*>(spec.force_field.get());
+    if (!gf) return paramd::propagate(spec, s, units);
+    spec.validate();
+    units.validate();
+    paramd::ParticleSystem out = s;
+    const double box[3] = {s.box.x, s.box.y, s.box.z};
+    const msmb_units u = paramd::detail_b200::to_c(units);
+    const int rc = msmb_propagate_ex(gf->handle(), static_cast<int64_t>(s.size()),
+                                     reinterpret_cast<double*>(out.positions.data()),
+                                     reinterpret_cast<double*>(out.velocities.data()),
+                                     out.charges.data(), out.masses.data(), box, spec.dt,
+                                     spec.steps_per_slice, &u);
+    if (rc) paramd::detail_b200::rethrow(gf->handle(), rc);
+    return out;
+}
+
+/// paramd::parareal_run (src/parareal.cpp:182-239) with device-resident states
+/// when both propagators use GpuMsmField.
+inline paramd::PararealResult parareal_run(const paramd::ParticleSystem& v, int total_points,
+                                           const paramd::PararealConfig& cfg) {
+    auto* F = dynamic_cast<const paramd::GpuMsmField*>(cfg.fine.force_field.get());
+    auto* G = dynamic_cast<const paramd::GpuMsmField*>(cfg.coarse.force_field.get());
+    if (!F || !G) return paramd::parareal_run(v, total_points, cfg);
+    msmb_parareal_config c{};
+    c.window_points = cfg.window_points;
+    c.max_iter = cfg.max_iter;
+    c.tol = cfg.tol;
+    c.fine = msmb_propagator{F->handle(), cfg.fine.dt, cfg.fine.steps_per_slice};
+    c.coarse = msmb_propagator{G->handle(), cfg.coarse.dt, cfg.coarse.steps_per_slice};
+    c.units = paramd::detail_b200::to_c(cfg.units);
+    c.has_skip_threshold = cfg.skip_threshold.has_value();
+    c.skip_threshold = cfg.skip_threshold.value_or(0.0);
+    c.short_circuit = cfg.short_circuit;
+    const std::size_t n = v.size();
+    std::vector<double> tp(3 * n * static_cast<std::size_t>(total_points > 0 ? total_points : 1));
+    std::vector<double> tv(tp.size());
+    int64_t rep[5] = {0, 0, 0, 0, 0};
+    const double box[3] = {v.box.x, v.box.y, v.box.z};
+    const int rc = msmb_parareal_run(&c, static_cast<int64_t>(n),
+                                     reinterpret_cast<const double*>(v.positions.data()),
+                                     reinterpret_cast<const double*>(v.velocities.data()),
+                                     v.charges.data(), v.masses.data(), box, total_points,
+                                     tp.data(), tv.data(), rep);
+    if (rc == MSMB_ERR_NONCONVERGENCE) {
+        paramd::ConvergenceReport r;
+        r.counts.g_evals = static_cast<std::size_t>(rep[0]);
+        r.counts.f_evals = static_cast<std::size_t>(rep[1]);
+        r.counts.f_skipped = static_cast<std::size_t>(rep[2]);
+        r.windows = static_cast<int>(rep[3]);
+        char msg[512] = {0};
+        msmb_last_error(F->handle(), nullptr, nullptr, nullptr, nullptr, msg, sizeof msg);
+        throw paramd::NonConvergenceError(msg, r);
+    }
+    if (rc) paramd::detail_b200::rethrow(F->handle(), rc);
+    paramd::PararealResult out;
+    for (int k = 0; k < total_points; ++k) {
+        paramd::ParticleSystem st = v;
+        std::memcpy(st.positions.data(), tp.data() + 3 * n * k, 3 * n * sizeof(double));
+        std::memcpy(st.velocities.data(), tv.data() + 3 * n * k, 3 * n * sizeof(double));
+        out.trajectory.push_back(std::move(st));
+    }
+    out.report.counts.g_evals = static_cast<std::size_t>(rep[0]);
+    out.report.counts.f_evals = static_cast<std::size_t>(rep[1]);
+    out.report.counts.f_skipped = static_cast<std::size_t>(rep[2]);
+    out.report.windows = static_cast<int>(rep[3]);
+    out.report.converged = rep[4] != 0;
+    return out;
+}
+
+}  // namespace paramd_b200

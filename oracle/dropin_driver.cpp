@@ -1,0 +1,134 @@
+// oracle/dropin_driver.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// Proves the drop-in at the reference's own plugin boundary: the UNMODIFIED
+// reference library (paramd, compiled from /root/reference/proj/src by
+// oracle/Makefile) drives paramd_b200::GpuMsmField through its ForceField
+// interface (include/paramd/force_field.hpp:14-21):
+//   1. MsmField::evaluate vs GpuMsmField::evaluate on the same system;
+//   2. paramd::propagate(spec{GpuMsmField}) -- the reference's own Verlet loop
+//      calling the GPU plugin every step -- vs paramd::propagate(spec{MsmField});
+//   3. paramd_b200::propagate (device-resident) vs the reference;
+//   4. paramd::parareal_run with GPU fine/coarse fields vs the reference's;
+//   5. error behaviour: the reference's exception types come back out.
+// Prints one JSON object; tests/test_gpu_dropin.py checks it.
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <memory>
+#include <random>
+#include <string>
+
+#include "paramd/force_field.hpp"
+#include "paramd/generate.hpp"
+#include "paramd/integrate.hpp"
+#include "paramd/msm.hpp"
+#include "paramd/parareal.hpp"
+#include "paramd_b200/gpu_msm_field.hpp"
+
+using namespace paramd;
+
+static double rel_rms(const std::vector<Vec3>& a, const std::vector<Vec3>& b) {
+    double num = 0, den = 0;
+    for (std::size_t i = 0; i < a.size(); ++i) {
+        const Vec3 d = a[i] - b[i];
+        num += norm2(d);
+        den += norm2(b[i]);
+    }
+    return std::sqrt(num / (den > 0 ? den : 1e-300));
+}
+
+int main() {
+    const UnitsConfig units = UnitsConfig::physical();
+    ParticleSystem s = generate_random_system(2048, Vec3{27.4, 27.4, 27.4}, ChargeScheme::RandomNeutral, 1.5, 77);
+    std::mt19937_64 rng(78);
+    std::normal_distribution<double> nd(0.0, 1.0);
+    const double kt = 0.0019872041 * 300.0 * 4.184e-4;
+    for (auto& m : s.masses) m = 18.0;
+    for (auto& v : s.velocities) v = Vec3{nd(rng), nd(rng), nd(rng)} * std::sqrt(kt / 18.0);
+
+    MsmConfig fcfg;
+    fcfg.cutoff_a = 12.0;
+    fcfg.spacing_h = 2.5;
+    fcfg.levels_l = 3;
+    MsmConfig gcfg;
+    gcfg.cutoff_a = 8.0;
+    gcfg.spacing_h = 5.0;
+    gcfg.levels_l = 2;
+    auto ref_f = std::make_shared<MsmField>(fcfg, units);
+    auto gpu_f = std::make_shared<GpuMsmField>(fcfg, units);
+    auto ref_g = std::make_shared<MsmField>(gcfg, units);
+    auto gpu_g = std::make_shared<GpuMsmField>(gcfg, units);
+
+    // 1. plugin evaluate
+    const ForceField& fr = *ref_f;
+    const ForceField& fg = *gpu_f;
+    PotentialResult a = fr.evaluate(s), b = fg.evaluate(s);
+    const double de = std::fabs(a.total_energy - b.total_energy) / std::fabs(a.total_energy);
+    const double df = rel_rms(b.per_particle_force, a.per_particle_force);
+
+    // 2. the reference's own propagate with the GPU plugin
+    PropagatorSpec sr{ref_f, 0.005, 20}, sg{gpu_f, 0.005, 20};
+    ParticleSystem pr = paramd::propagate(sr, s, units);
+    ParticleSystem pg = paramd::propagate(sg, s, units);
+    const double dx_plugin = rel_rms(pg.positions, pr.positions);
+    // 3. device-resident propagate
+    ParticleSystem pd = paramd_b200::propagate(sg, s, units);
+    const double dx_dev = rel_rms(pd.positions, pr.positions);
+
+    // 4. parareal_run (reference driver, GPU fields) and the device-resident driver
+    PararealConfig cr;
+    cr.window_points = 4;
+    cr.max_iter = 3;
+    cr.tol = 1e-9;
+    cr.units = units;
+    cr.fine = PropagatorSpec{ref_f, 0.005, 20};
+    cr.coarse = PropagatorSpec{ref_g, 0.02, 5};
+    PararealConfig cg = cr;
+    cg.fine = PropagatorSpec{gpu_f, 0.005, 20};
+    cg.coarse = PropagatorSpec{gpu_g, 0.02, 5};
+    int pr_ok = 1;
+    double dx_pr = -1, dx_pr_dev = -1;
+    std::size_t gref = 0, fref = 0, ggpu = 0, fgpu = 0, gdev = 0, fdev = 0;
+    try {
+        PararealResult rr = parareal_run(s, 6, cr, sequential_executor());
+        PararealResult rg = parareal_run(s, 6, cg, sequential_executor());
+        PararealResult rd = paramd_b200::parareal_run(s, 6, cg);
+        dx_pr = 0;
+        dx_pr_dev = 0;
+        for (int k = 0; k < 6; ++k) {
+            dx_pr = std::max(dx_pr, rel_rms(rg.trajectory[k].positions, rr.trajectory[k].positions));
+            dx_pr_dev = std::max(dx_pr_dev, rel_rms(rd.trajectory[k].positions, rr.trajectory[k].positions));
+        }
+        gref = rr.report.counts.g_evals;
+        fref = rr.report.counts.f_evals;
+        ggpu = rg.report.counts.g_evals;
+        fgpu = rg.report.counts.f_evals;
+        gdev = rd.report.counts.g_evals;
+        fdev = rd.report.counts.f_evals;
+    } catch (const std::exception& e) {
+        pr_ok = 0;
+        std::fprintf(stderr, "parareal: %s\n", e.what());
+    }
+
+    // 5. errors through the plugin
+    ParticleSystem bad = s;
+    bad.positions[100] = bad.positions[7];
+    std::string err_ref, err_gpu;
+    try { fr.evaluate(bad); } catch (const CoincidentParticlesError& e) { err_ref = e.what(); }
+    try { fg.evaluate(bad); } catch (const CoincidentParticlesError& e) { err_gpu = e.what(); }
+    bad = s;
+    bad.positions[300].x = 60.0;
+    std::string cov_ref, cov_gpu;
+    try { fr.evaluate(bad); } catch (const CoverageError& e) { cov_ref = e.what(); }
+    try { fg.evaluate(bad); } catch (const CoverageError& e) { cov_gpu = e.what(); }
+
+    std::printf(
+        "{\"de\": %.3e, \"df\": %.3e, \"dx_plugin_propagate\": %.3e, \"dx_device_propagate\": %.3e, "
+        "\"parareal_ok\": %d, \"dx_parareal_plugin\": %.3e, \"dx_parareal_device\": %.3e, "
+        "\"counts\": [%zu, %zu, %zu, %zu, %zu, %zu], \"coincident_ref\": \"%s\", \"coincident_gpu\": \"%s\", "
+        "\"coverage_ref\": \"%s\", \"coverage_gpu\": \"%s\", \"name\": \"%s\", \"cost\": %.6e, \"cost_ref\": %.6e}\n",
+        de, df, dx_plugin, dx_dev, pr_ok, dx_pr, dx_pr_dev, gref, fref, ggpu, fgpu, gdev, fdev,
+        err_ref.c_str(), err_gpu.c_str(), cov_ref.c_str(), cov_gpu.c_str(), fg.name().c_str(),
+        fg.cost_flops_per_step(2048), fr.cost_flops_per_step(2048));
+    return 0;
+}

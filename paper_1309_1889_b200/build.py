@@ -90,7 +90,7 @@ def build_oracle(verbose: bool = False) -> None:
     """CPU checkers (test infrastructure).  _ref needs the reference sources."""
     targets = ["port"]
     if Path("/root/reference/proj/src").is_dir():
-        targets.append("ref")
+        targets += ["ref", "dropin"]
     _run(["make", "-s", "-C", str(ROOT / "oracle"), *targets], verbose)
 
 

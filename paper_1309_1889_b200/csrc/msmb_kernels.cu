@@ -549,10 +549,11 @@ __global__ void __launch_bounds__(kPairWarps * 32, 5)
             const double dx = xi - xj2, dy = yi - yj2, dz = zi - zj2;
             const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
             const bool in = has && (r2 < a2);
-            const double rinv = rsqrt_pos(r2);
+            const double r2s = in ? r2 : a2; // excluded / idle lanes: finite dummy (0 * inf = NaN)
+            const double rinv = rsqrt_pos(r2s);
             const double rinv2 = rinv * rinv;
-            const double g = rinv - fma(r2, fma(r2, c2, c1), c0);   // g*(r)
-            const double sd = fma(-rinv, rinv2, fma(r2, d1, d0));  // g*'(r)/r
+            const double g = rinv - fma(r2s, fma(r2s, c2, c1), c0);   // g*(r)
+            const double sd = fma(-rinv, rinv2, fma(r2s, d1, d0));    // g*'(r)/r
             const double qe = in ? qj2 : 0.0;
             ph = fma(qe, g, ph);
             const double wgt = qe * sd;
