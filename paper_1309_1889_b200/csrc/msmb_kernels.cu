@@ -289,10 +289,11 @@ int launch_sort(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms&
                 ErrRec* err) {
     const int n = int(s.n);
     int l = scan_exclusive(st, c.count, c.start, c.scan_tmp, g.ncells + 1);
-    if (n == 0) return l;
-    k_scatter<<<(n + 255) / 256, 256, 0, st>>>(n, a.key, a.rank, c.start, a.perm, err);
+    if (n > 0) k_scatter<<<(n + 255) / 256, 256, 0, st>>>(n, a.key, a.rank, c.start, a.perm, err);
+    // always: also publishes the (possibly empty) natural-order cell ranges read by k_anterp
     k_cellsort<<<int((g.ncells + 255) / 256), 256, 0, st>>>(g.ncells, make_binp(g), c.start, a.perm,
                                                             c.nat, s.x, s.y, s.z, err);
+    if (n == 0) return l + 1;
     k_gather<<<(n + 255) / 256, 256, 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, s.q,
                                               make_binp(g), a.xs, a.ys, a.zs, a.qs, a.f4, a.aw,
                                               err);
