@@ -290,18 +290,10 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs) 
     run("clusters", [&] { return launch_clusters(st, g, s.n, W.a, W.c, W.err, W.cap); });
     run("pairs", [&] { return launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap); });
     run("anterp", [&] { return launch_anterp(st, g, W.a, W.c, W.L, W.err); });
-    run("restrict", [&] {
-        int l = 0;
-        for (int k = 0; k + 1 < g.levels; ++k) l += launch_restrict(st, g, k, W.L, W.err);
-        return l;
-    });
+    run("restrict", [&] { return launch_restrict_all(st, g, W.L, W.err); });
     run("lattice", [&] { return launch_lattice(st, g, W.L, W.err); });
     run("top", [&] { return launch_top(st, g, W.L, W.err); });
-    run("prolong", [&] {
-        int l = 0;
-        for (int k = g.levels - 2; k >= 0; --k) l += launch_prolong(st, g, k, W.L, W.err);
-        return l;
-    });
+    run("prolong", [&] { return launch_prolong_all(st, g, W.L, W.err); });
     DevOut o = W.o;
     if (!outputs) o.phi = o.phis = o.phil = o.e = nullptr;
     run("interp", [&] { return launch_interp(st, g, s.n, W.a, W.c, W.L, o, W.err, outputs ? 1 : 0); });

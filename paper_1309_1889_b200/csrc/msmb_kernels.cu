@@ -653,25 +653,30 @@ int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& 
 }
 
 // ============================================================================
-// K3: anterpolation as an owner-computes gather (no atomics): one thread per
-// level-0 grid point sums the contributions of the particles in the 4x4x4 cells
-// whose stencils reach it, in a fixed order (cells in x, y, z order, particles
-// in sorted order), using the per-particle weights of k_gather:
+// K3: anterpolation as an owner-computes gather (no atomics): a thread owns 4
+// consecutive level-0 points along z and sums the contributions of the particles
+// in the cells whose stencils reach them, in a fixed order (cells in x, y, z
+// order, particles in sorted order), using the per-particle weights of k_gather:
 // q_mu += ((q*wx[dx]) * wy[dy]) * wz[dz]  (the reference's qa/qab products,
-// src/msm_phases.cpp:52-57).  Lanes run along z so neighbouring points share cells.
+// src/msm_phases.cpp:52-57).  One weight fetch serves up to 4 points.
 // ============================================================================
+constexpr int kAQ = 4; // points per thread along z
+
 __global__ void __launch_bounds__(128)
     k_anterp(BinP p, const int2* __restrict__ nat, const double* __restrict__ aw, double* q0,
              const ErrRec* err) {
     if (failed(err)) return;
     const int d0 = p.d[0], d1 = p.d[1], d2 = p.d[2];
+    const int nzq = (d2 + kAQ - 1) / kAQ;
     const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= int64_t(d0) * d1 * d2) return;
-    const int z = int(idx % d2);
-    const int y = int((idx / d2) % d1);
-    const int x = int(idx / (int64_t(d2) * d1));
-    double acc = 0.0;
-    const int cz_lo = max(1, z - 2), cz_hi = min(d2 - 3, z + 1);
+    if (idx >= int64_t(d0) * d1 * nzq) return;
+    const int zq = int(idx % nzq);
+    const int y = int((idx / nzq) % d1);
+    const int x = int(idx / (int64_t(nzq) * d1));
+    const int z0 = zq * kAQ;
+    double acc[kAQ];
+#pragma unroll
+    for (int k = 0; k < kAQ; ++k) acc[k] = 0.0;
     for (int ox = 0; ox < 4; ++ox) {
         const int cx = x - 2 + ox;
         if (cx < 1 || cx > d0 - 3) continue;
@@ -681,24 +686,38 @@ __global__ void __launch_bounds__(128)
             if (cy < 1 || cy > d1 - 3) continue;
             const int dyw = 4 + 3 - oy;
             const int2* row = nat + (size_t(cx) * d1 + cy) * d2;
-            for (int cz = cz_lo; cz <= cz_hi; ++cz) {
+            // cells cz = z0 - 2 + u, u = 0 .. kAQ + 2, reach points z0 + k with dz = k - u + 3
+#pragma unroll
+            for (int u = 0; u < kAQ + 3; ++u) {
+                const int cz = z0 - 2 + u;
+                if (cz < 1 || cz > d2 - 3) continue;
                 const int2 r = __ldg(row + cz);
-                const int dzw = 8 + z - cz + 1;
                 for (int s = r.x; s < r.y; ++s) {
                     const double* w = aw + size_t(s) * 12;
                     const double cxy = __dmul_rn(__ldg(w + dxw), __ldg(w + dyw));
-                    acc = fma(cxy, __ldg(w + dzw), acc);
+                    const double2 wz01 = __ldg(reinterpret_cast<const double2*>(w + 8));
+                    const double2 wz23 = __ldg(reinterpret_cast<const double2*>(w + 10));
+                    const double4 wz = make_double4(wz01.x, wz01.y, wz23.x, wz23.y);
+                    const double wzv[4] = {wz.x, wz.y, wz.z, wz.w};
+#pragma unroll
+                    for (int k = 0; k < kAQ; ++k) {
+                        const int dz = k - u + 3;
+                        if (dz >= 0 && dz <= 3) acc[k] = fma(cxy, wzv[dz], acc[k]);
+                    }
                 }
             }
         }
     }
-    q0[idx] = acc;
+    double* out = q0 + (size_t(x) * d1 + y) * d2;
+#pragma unroll
+    for (int k = 0; k < kAQ; ++k)
+        if (z0 + k < d2) out[z0 + k] = acc[k];
 }
 
 int launch_anterp(cudaStream_t st, const Geometry& g, DevAtoms& a, DevCells& c, DevLevels& L,
                   ErrRec* err) {
     const BinP p = make_binp(g);
-    const int64_t m = int64_t(p.d[0]) * p.d[1] * p.d[2];
+    const int64_t m = int64_t(p.d[0]) * p.d[1] * ((p.d[2] + kAQ - 1) / kAQ);
     k_anterp<<<int((m + 127) / 128), 128, 0, st>>>(p, c.nat, a.aw, L.charge + g.lv[0].offset, err);
     return 1;
 }
@@ -729,18 +748,13 @@ static XferP make_xfer(const Geometry& g, int k, DevLevels& L) {
     return p;
 }
 
-// coarse(I,J,K) = sum over fine points in row-major order of ((q*wx)*wy)*wz,
-// skipping zero charges (src/msm_phases.cpp:67-89).  The three per-axis lists
-// (<= 8 fine indices each) are held in registers; only fine values are loaded
-// in the loop nest.
-__global__ void __launch_bounds__(128) k_restrict(XferP p, const double* __restrict__ fine,
-                                                  double* coarse, const ErrRec* err) {
-    const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t m = int64_t(p.cd[0]) * p.cd[1] * p.cd[2];
-    if (idx >= m || failed(err)) return;
-    const int K = int(idx % p.cd[2]);
-    const int J = int((idx / p.cd[2]) % p.cd[1]);
-    const int I = int(idx / (int64_t(p.cd[2]) * p.cd[1]));
+// Per-point restriction: coarse(I,J,K) = sum over the fine points feeding it in
+// row-major order of ((q*wx)*wy)*wz, skipping zero charges -- the order and
+// arithmetic of the reference's scatter (src/msm_phases.cpp:67-89), hence bit
+// for bit.  `fine_at(i, j, k)` abstracts where the fine values live (global
+// memory or a shared-memory tile).
+template <class FineAt>
+__device__ __forceinline__ double restrict_point(const XferP& p, int I, int J, int K, FineAt fine_at) {
     const int ni = p.rcnt[0][I], nj = p.rcnt[1][J], nk = p.rcnt[2][K];
     int iy[kRestrictMax], iz[kRestrictMax];
     double wy[kRestrictMax], wz[kRestrictMax];
@@ -759,10 +773,9 @@ __global__ void __launch_bounds__(128) k_restrict(XferP p, const double* __restr
 #pragma unroll
         for (int b = 0; b < kRestrictMax; ++b) {
             if (b >= nj) break;
-            const double* row = fine + (size_t(ix) * p.fd[1] + iy[b]) * p.fd[2];
             double q[kRestrictMax];
 #pragma unroll
-            for (int c = 0; c < kRestrictMax; ++c) q[c] = c < nk ? __ldg(row + iz[c]) : 0.0;
+            for (int c = 0; c < kRestrictMax; ++c) q[c] = c < nk ? fine_at(ix, iy[b], iz[c]) : 0.0;
 #pragma unroll
             for (int c = 0; c < kRestrictMax; ++c) {
                 if (c < nk && q[c] != 0.0) {
@@ -772,15 +785,43 @@ __global__ void __launch_bounds__(128) k_restrict(XferP p, const double* __restr
             }
         }
     }
-    coarse[idx] = acc;
+    return acc;
+}
+
+// Large levels: a CTA computes a 4x4x8 block of coarse points from a zero-padded
+// shared-memory tile of the fine lattice (fine i in [2I0-5, 2(I0+3)+1], etc.).
+constexpr int kRTx = 4, kRTy = 4, kRTz = 8;
+constexpr int kRFx = 2 * kRTx + 6, kRFy = 2 * kRTy + 6, kRFz = 2 * kRTz + 6;
+
+__global__ void __launch_bounds__(kRTx * kRTy * kRTz)
+    k_restrict_tile(XferP p, const double* __restrict__ fine, double* coarse, const ErrRec* err) {
+    __shared__ double tile[kRFx * kRFy * kRFz];
+    if (failed(err)) return;
+    const int tz_n = (p.cd[2] + kRTz - 1) / kRTz, ty_n = (p.cd[1] + kRTy - 1) / kRTy;
+    const int bz = blockIdx.x % tz_n, by = (blockIdx.x / tz_n) % ty_n, bx = blockIdx.x / (tz_n * ty_n);
+    const int I0 = bx * kRTx, J0 = by * kRTy, K0 = bz * kRTz;
+    const int fi0 = 2 * I0 - 5, fj0 = 2 * J0 - 5, fk0 = 2 * K0 - 5;
+    for (int e = threadIdx.x; e < kRFx * kRFy * kRFz; e += blockDim.x) {
+        const int kk = e % kRFz, jj = (e / kRFz) % kRFy, ii = e / (kRFz * kRFy);
+        const int i = fi0 + ii, j = fj0 + jj, k = fk0 + kk;
+        double v = 0.0;
+        if (i >= 0 && i < p.fd[0] && j >= 0 && j < p.fd[1] && k >= 0 && k < p.fd[2])
+            v = fine[(size_t(i) * p.fd[1] + j) * p.fd[2] + k];
+        tile[e] = v;
+    }
+    __syncthreads();
+    const int tz = threadIdx.x % kRTz, ty = (threadIdx.x / kRTz) % kRTy, tx = threadIdx.x / (kRTz * kRTy);
+    const int I = I0 + tx, J = J0 + ty, K = K0 + tz;
+    if (I >= p.cd[0] || J >= p.cd[1] || K >= p.cd[2]) return;
+    const double v = restrict_point(p, I, J, K, [&](int i, int j, int k) {
+        return tile[((i - fi0) * kRFy + (j - fj0)) * kRFz + (k - fk0)];
+    });
+    coarse[(size_t(I) * p.cd[1] + J) * p.cd[2] + K] = v;
 }
 
 // fine(i,j,k) += sum_a wx[a] (sum_b wy[b] (sum_c wz[c] u_coarse)) (src/msm_phases.cpp:177-189)
-__global__ void k_prolong(XferP p, const double* __restrict__ coarse, double* fine,
-                          const ErrRec* err) {
-    const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t m = int64_t(p.fd[0]) * p.fd[1] * p.fd[2];
-    if (idx >= m || failed(err)) return;
+__device__ __forceinline__ void prolong_point(const XferP& p, const double* __restrict__ coarse,
+                                              double* fine, int64_t idx) {
     const int k = int(idx % p.fd[2]);
     const int j = int((idx / p.fd[2]) % p.fd[1]);
     const int i = int(idx / (int64_t(p.fd[2]) * p.fd[1]));
@@ -802,10 +843,116 @@ __global__ void k_prolong(XferP p, const double* __restrict__ coarse, double* fi
     fine[idx] = __dadd_rn(fine[idx], acc);
 }
 
+__global__ void k_prolong(XferP p, const double* __restrict__ coarse, double* fine,
+                          const ErrRec* err) {
+    const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t m = int64_t(p.fd[0]) * p.fd[1] * p.fd[2];
+    if (idx >= m || failed(err)) return;
+    prolong_point(p, coarse, fine, idx);
+}
+
+// Small levels: one CTA walks a chain of transitions with a block barrier between
+// levels (restriction upwards / prolongation downwards), saving a launch and the
+// per-launch latency for every small level.
+struct XferChain {
+    XferP x[kMaxLevels];
+    const double* src[kMaxLevels];
+    double* dst[kMaxLevels];
+    int n;
+};
+
+__global__ void __launch_bounds__(512) k_restrict_chain(XferChain ch, const ErrRec* err) {
+    if (failed(err)) return;
+    for (int t = 0; t < ch.n; ++t) {
+        const XferP& p = ch.x[t];
+        const double* fine = ch.src[t];
+        const int64_t m = int64_t(p.cd[0]) * p.cd[1] * p.cd[2];
+        for (int64_t idx = threadIdx.x; idx < m; idx += blockDim.x) {
+            const int K = int(idx % p.cd[2]);
+            const int J = int((idx / p.cd[2]) % p.cd[1]);
+            const int I = int(idx / (int64_t(p.cd[2]) * p.cd[1]));
+            ch.dst[t][idx] = restrict_point(p, I, J, K, [&](int i, int j, int k) {
+                return fine[(size_t(i) * p.fd[1] + j) * p.fd[2] + k];
+            });
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(512) k_prolong_chain(XferChain ch, const ErrRec* err) {
+    if (failed(err)) return;
+    for (int t = 0; t < ch.n; ++t) {
+        const XferP& p = ch.x[t];
+        const int64_t m = int64_t(p.fd[0]) * p.fd[1] * p.fd[2];
+        for (int64_t idx = threadIdx.x; idx < m; idx += blockDim.x) prolong_point(p, ch.src[t], ch.dst[t], idx);
+        __syncthreads();
+    }
+}
+
+constexpr int64_t kChainMax = 6000; // transitions whose output has fewer points run in the chain kernel
+
+int launch_restrict_all(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err) {
+    int l = 0;
+    XferChain ch;
+    ch.n = 0;
+    for (int k = 0; k + 1 < g.levels; ++k) {
+        const int64_t mc = int64_t(g.lv[k + 1].size);
+        if (ch.n == 0 && mc >= kChainMax) {
+            const XferP p = make_xfer(g, k, L);
+            const int blocks = ((p.cd[0] + kRTx - 1) / kRTx) * ((p.cd[1] + kRTy - 1) / kRTy) *
+                               ((p.cd[2] + kRTz - 1) / kRTz);
+            k_restrict_tile<<<blocks, kRTx * kRTy * kRTz, 0, st>>>(p, L.charge + g.lv[k].offset,
+                                                                  L.charge + g.lv[k + 1].offset, err);
+            ++l;
+        } else {
+            ch.x[ch.n] = make_xfer(g, k, L);
+            ch.src[ch.n] = L.charge + g.lv[k].offset;
+            ch.dst[ch.n] = L.charge + g.lv[k + 1].offset;
+            ch.n++;
+        }
+    }
+    if (ch.n) {
+        k_restrict_chain<<<1, 512, 0, st>>>(ch, err);
+        ++l;
+    }
+    return l;
+}
+
+int launch_prolong_all(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err) {
+    int l = 0;
+    XferChain ch;
+    ch.n = 0;
+    // top-down: small transitions first (chain), then the large ones
+    for (int k = g.levels - 2; k >= 0; --k) {
+        const int64_t mf = int64_t(g.lv[k].size);
+        if (mf < kChainMax) {
+            ch.x[ch.n] = make_xfer(g, k, L);
+            ch.src[ch.n] = L.pot + g.lv[k + 1].offset;
+            ch.dst[ch.n] = L.pot + g.lv[k].offset;
+            ch.n++;
+            continue;
+        }
+        if (ch.n) {
+            k_prolong_chain<<<1, 512, 0, st>>>(ch, err);
+            ++l;
+            ch.n = 0;
+        }
+        k_prolong<<<int((mf + 127) / 128), 128, 0, st>>>(make_xfer(g, k, L), L.pot + g.lv[k + 1].offset,
+                                                         L.pot + g.lv[k].offset, err);
+        ++l;
+    }
+    if (ch.n) {
+        k_prolong_chain<<<1, 512, 0, st>>>(ch, err);
+        ++l;
+    }
+    return l;
+}
+
 int launch_restrict(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err) {
-    const int64_t m = int64_t(g.lv[k + 1].size);
-    k_restrict<<<int((m + 127) / 128), 128, 0, st>>>(make_xfer(g, k, L), L.charge + g.lv[k].offset,
-                                                     L.charge + g.lv[k + 1].offset, err);
+    const XferP p = make_xfer(g, k, L);
+    const int blocks = ((p.cd[0] + kRTx - 1) / kRTx) * ((p.cd[1] + kRTy - 1) / kRTy) * ((p.cd[2] + kRTz - 1) / kRTz);
+    k_restrict_tile<<<blocks, kRTx * kRTy * kRTz, 0, st>>>(p, L.charge + g.lv[k].offset,
+                                                          L.charge + g.lv[k + 1].offset, err);
     return 1;
 }
 
@@ -870,12 +1017,14 @@ __global__ void __launch_bounds__(32 * NWZ) k_conv(ConvJobs J, const ErrRec* err
         if (r0 == r1) continue;
         __syncthreads();
         const double* plane = jb.q + size_t(xs) * jb.d1 * jb.d2;
-        for (int idx = threadIdx.x; idx < jb.SY * jb.SZ; idx += blockDim.x) {
-            const int r = idx / jb.SZ, cc = idx - r * jb.SZ;
-            const int ys = y0 - jb.Ry + r, zs = z0 - jb.Rz + cc;
-            double v = 0.0;
-            if (ys >= 0 && ys < jb.d1 && zs >= 0 && zs < jb.d2) v = plane[size_t(ys) * jb.d2 + zs];
-            slab[r * jb.P + cc] = v;
+        for (int r = w; r < jb.SY; r += NWZ) { // warp per slab row, lanes along z (coalesced)
+            const int ys = y0 - jb.Ry + r;
+            const bool yok = ys >= 0 && ys < jb.d1;
+            const double* src = plane + size_t(yok ? ys : 0) * jb.d2;
+            for (int cc = lane; cc < jb.SZ; cc += 32) {
+                const int zs = z0 - jb.Rz + cc;
+                slab[r * jb.P + cc] = (yok && zs >= 0 && zs < jb.d2) ? src[zs] : 0.0;
+            }
         }
         __syncthreads();
         for (int r = r0; r < r1; ++r) {

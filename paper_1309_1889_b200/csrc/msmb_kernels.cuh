@@ -77,6 +77,8 @@ int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& 
 int launch_anterp(cudaStream_t st, const Geometry& g, DevAtoms& a, DevCells& c, DevLevels& L,
                   ErrRec* err);
 int launch_restrict(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err);
+int launch_restrict_all(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
+int launch_prolong_all(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
 int launch_lattice(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
 int launch_top(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
 int launch_prolong(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err);
