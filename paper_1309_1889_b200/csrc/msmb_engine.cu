@@ -208,6 +208,16 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
         L.taps[k] = wupload(*W, t.taps);
         smem = std::max(smem, conv_smem_bytes(t));
     }
+    if (g.levels >= 2) {
+        L.lat_rowidx = wupload(*W, g.lat.rowidx);
+        std::vector<int2> rc(g.lat.rowchunks.size());
+        for (size_t i = 0; i < rc.size(); ++i) rc[i] = make_int2(g.lat.rowchunks[i].x, g.lat.rowchunks[i].y);
+        L.lat_rowchunks = wupload(*W, rc);
+        L.lat_taps = wupload(*W, g.lat.taps);
+        L.lat_S = lattice_splits(g);
+        L.lat_partial = L.lat_S > 1 ? walloc<double>(*W, size_t(L.lat_S) * g.lattice_total) : nullptr;
+        ck(lattice_prepare(lattice_smem_bytes(g)), "cudaFuncSetAttribute");
+    }
     if (smem > 227 * 1024) {
         e.kind = MSMB_ERR_CONFIG;
         e.msg = "msm: top level of " + std::to_string(g.lv[g.levels - 1].size) +

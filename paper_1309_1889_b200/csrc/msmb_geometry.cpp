@@ -248,6 +248,24 @@ Error build_geometry(const msmb_msm_config& c, const msmb_units& u, const double
                 g.lattice_taps_clipped += ex * ey * ez;
             }
     }
+    // k_lattice table: level-0 stencil, absolute dz layout (levels k > 0 scale by 2^-k)
+    if (g.levels >= 2) {
+        const ConvTable& t0 = g.lattice[0];
+        LatticeTable& L = g.lat;
+        L.R = t0.Rx;
+        L.TW = (2 * L.R + 1 + 3) / 4 * 4;
+        const int W = 2 * L.R + 1;
+        L.rowidx.assign(size_t(W) * W, -1);
+        for (const auto& r : t0.rows) {
+            const int id = L.nrows++;
+            L.rowidx[size_t(r.dx + L.R) * W + (r.dy + L.R)] = id;
+            L.rowchunks.push_back(int2_{(L.R - r.m) / 4, (L.R + r.m) / 4});
+            for (int i = 0; i < L.TW; ++i) {
+                const int dz = i - L.R;
+                L.taps.push_back((dz >= -r.m && dz <= r.m) ? t0.taps[r.tap_off + dz + r.m] : 0.0);
+            }
+        }
+    }
     build_top_table(g, g.top);
     g.top_taps = int64_t(g.lv[g.levels - 1].size) * int64_t(g.lv[g.levels - 1].size);
 

@@ -64,6 +64,10 @@ struct TransferAxis {
     std::vector<double> rw;    // [d_coarse * kRestrictMax]
 };
 
+struct int2_ {
+    int x, y;
+};
+
 struct ConvRow { // one (dx, dy) row of a 3-D stencil: taps for dz = -m..m
     int dx, dy, m, tap_off;
 };
@@ -76,6 +80,17 @@ struct ConvTable {
     int64_t nonzero_taps = 0;         // nonzero taps in the stencil
 };
 
+// Level-0 lattice-cutoff stencil in the layout of k_lattice: for every (dx, dy)
+// row with a nonzero tap, the taps for dz = -R..R at index dz + R, zero padded to
+// a multiple of 4; level k uses 2^-k times these values (bit-identical to the
+// reference's per-level table, see msmb_geometry.cpp).
+struct LatticeTable {
+    int R = 0, TW = 0, nrows = 0;
+    std::vector<int> rowidx;   // [(2R+1)^2]: row id of (dx, dy) or -1
+    std::vector<int2_> rowchunks; // [nrows]: first / last 4-tap chunk holding nonzero taps
+    std::vector<double> taps;  // [nrows * TW]
+};
+
 struct Geometry {
     msmb_msm_config cfg{};
     msmb_units units{};
@@ -86,6 +101,7 @@ struct Geometry {
     TransferAxis tr[kMaxLevels][3];      // tr[k][axis], k = 0..levels-2
     ConvTable lattice[kMaxLevels];       // k = 0..levels-2
     ConvTable top;
+    LatticeTable lat;                    // shared level-0 stencil for k_lattice
     double inv_h0 = 0;                   // 1.0 / spacing of level 0
     double self_term = 0;                // smoothing_gamma(0)/a (src/msm.cpp:72)
     // pair-cell (column) decomposition over level-0 cells

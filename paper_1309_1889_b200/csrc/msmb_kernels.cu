@@ -668,18 +668,21 @@ __global__ void __launch_bounds__(128)
     if (failed(err)) return;
     const int d0 = p.d[0], d1 = p.d[1], d2 = p.d[2];
     const int nzq = (d2 + kAQ - 1) / kAQ;
-    const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= int64_t(d0) * d1 * nzq) return;
-    const int zq = int(idx % nzq);
-    const int y = int((idx / nzq) % d1);
-    const int x = int(idx / (int64_t(nzq) * d1));
+    // 4 lanes per quad of points, one cell column offset (ox) each; partial sums
+    // are combined by a fixed shuffle tree ((ox0 + ox1) + (ox2 + ox3))
+    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int ox = int(tid & 3);
+    const int64_t idx = tid >> 2;
+    const bool live = idx < int64_t(d0) * d1 * nzq;
+    const int zq = live ? int(idx % nzq) : 0;
+    const int y = live ? int((idx / nzq) % d1) : 0;
+    const int x = live ? int(idx / (int64_t(nzq) * d1)) : 0;
     const int z0 = zq * kAQ;
     double acc[kAQ];
 #pragma unroll
     for (int k = 0; k < kAQ; ++k) acc[k] = 0.0;
-    for (int ox = 0; ox < 4; ++ox) {
-        const int cx = x - 2 + ox;
-        if (cx < 1 || cx > d0 - 3) continue;
+    const int cx = x - 2 + ox;
+    if (live && cx >= 1 && cx <= d0 - 3) {
         const int dxw = 3 - ox; // weight index x - base = x - (cx - 1)
         for (int oy = 0; oy < 4; ++oy) {
             const int cy = y - 2 + oy;
@@ -697,8 +700,7 @@ __global__ void __launch_bounds__(128)
                     const double cxy = __dmul_rn(__ldg(w + dxw), __ldg(w + dyw));
                     const double2 wz01 = __ldg(reinterpret_cast<const double2*>(w + 8));
                     const double2 wz23 = __ldg(reinterpret_cast<const double2*>(w + 10));
-                    const double4 wz = make_double4(wz01.x, wz01.y, wz23.x, wz23.y);
-                    const double wzv[4] = {wz.x, wz.y, wz.z, wz.w};
+                    const double wzv[4] = {wz01.x, wz01.y, wz23.x, wz23.y};
 #pragma unroll
                     for (int k = 0; k < kAQ; ++k) {
                         const int dz = k - u + 3;
@@ -708,6 +710,12 @@ __global__ void __launch_bounds__(128)
             }
         }
     }
+#pragma unroll
+    for (int k = 0; k < kAQ; ++k) {
+        acc[k] += __shfl_xor_sync(FULLMASK, acc[k], 1);
+        acc[k] += __shfl_xor_sync(FULLMASK, acc[k], 2);
+    }
+    if (!live || ox != 0) return;
     double* out = q0 + (size_t(x) * d1 + y) * d2;
 #pragma unroll
     for (int k = 0; k < kAQ; ++k)
@@ -717,7 +725,7 @@ __global__ void __launch_bounds__(128)
 int launch_anterp(cudaStream_t st, const Geometry& g, DevAtoms& a, DevCells& c, DevLevels& L,
                   ErrRec* err) {
     const BinP p = make_binp(g);
-    const int64_t m = int64_t(p.d[0]) * p.d[1] * ((p.d[2] + kAQ - 1) / kAQ);
+    const int64_t m = 4 * int64_t(p.d[0]) * p.d[1] * ((p.d[2] + kAQ - 1) / kAQ);
     k_anterp<<<int((m + 127) / 128), 128, 0, st>>>(p, c.nat, a.aw, L.charge + g.lv[0].offset, err);
     return 1;
 }
@@ -1126,21 +1134,216 @@ static int launch_conv_jobs(cudaStream_t st, ConvJobs& J, int blocks, bool big, 
     return 1;
 }
 
-int launch_lattice(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err) {
+// ----------------------------------------------------------------------------
+// K5 (lattice cutoff, levels 0..l-2): one warp per tile of 4 x-planes x 32 y-rows
+// (a lane each) x 8 consecutive z.  For every source x-plane the warp stages a
+// zero-padded (y, z) slab in shared memory (odd pitch: the lane-per-row loads are
+// conflict-free) and, for every dy, slides a register window along z in 4-tap
+// chunks; each window chunk feeds all 4 output planes (their own dx rows of the
+// stencil), so one shared-memory load serves up to 4 x 8 x 4 = 128 FMAs.  Chunks
+// where no plane has a nonzero tap are skipped.  The stencil is the level-0 table
+// in absolute-dz layout; level k is scaled by 2^-k, which is exact (see
+// msmb_geometry.cpp).  Large grids run one warp per tile; small ones split the
+// source planes over S warps and a second kernel adds the S partial lattices in
+// fixed order (deterministic).
+// ----------------------------------------------------------------------------
+constexpr int kLB = 8, kLP = 4, kLC = 4;
+
+struct LatJob {
+    const double* q;
+    double* out;
+    int d0, d1, d2;
+    int tzn, tyn;
+    int blk0;      // first tile index of this job
+    double scale;  // 2^-k
+    size_t off;    // lattice offset (partials)
+};
+
+struct LatJobs {
+    LatJob j[kMaxLevels];
+    int n, S, R, TW, SZ, P;
+    const int* rowidx;
+    const int2* rowchunks;
+    const double* taps;
+    double* partial;     // S * lattice_total (S > 1)
+    size_t pstride;      // lattice_total
+};
+
+__global__ void __launch_bounds__(32) k_lattice(LatJobs J, const ErrRec* err) {
+    extern __shared__ double slab[];
+    if (failed(err)) return;
+    const int lane = threadIdx.x;
+    const int split = blockIdx.x % J.S;
+    int t = blockIdx.x / J.S;
+    int jj = 0;
+    while (jj + 1 < J.n && t >= J.j[jj + 1].blk0) ++jj;
+    const LatJob jb = J.j[jj];
+    t -= jb.blk0;
+    const int tz = t % jb.tzn, rest = t / jb.tzn;
+    const int ty = rest % jb.tyn, tx = rest / jb.tyn;
+    const int x0 = tx * kLP, y0 = ty * 32, z0 = tz * kLB;
+    const int R = J.R, W = 2 * J.R + 1, SY = 32 + 2 * J.R;
+    int xs_lo = max(0, x0 - R), xs_hi = min(jb.d0 - 1, x0 + kLP - 1 + R);
+    {
+        const int cnt = xs_hi - xs_lo + 1, per = (cnt + J.S - 1) / J.S;
+        xs_lo += split * per;
+        xs_hi = min(xs_hi, xs_lo + per - 1);
+    }
+    double acc[kLP][kLB];
+#pragma unroll
+    for (int p = 0; p < kLP; ++p)
+#pragma unroll
+        for (int b = 0; b < kLB; ++b) acc[p][b] = 0.0;
+    for (int xs = xs_lo; xs <= xs_hi; ++xs) {
+        __syncwarp();
+        const double* plane = jb.q + size_t(xs) * jb.d1 * jb.d2;
+        for (int r = 0; r < SY; ++r) {
+            const int ys = y0 - R + r;
+            const bool yok = ys >= 0 && ys < jb.d1;
+            for (int cc = lane; cc < J.SZ; cc += 32) {
+                const int zs = z0 - R + cc;
+                slab[r * J.P + cc] = (yok && zs >= 0 && zs < jb.d2) ? plane[size_t(ys) * jb.d2 + zs] : 0.0;
+            }
+        }
+        __syncwarp();
+        for (int dy = -R; dy <= R; ++dy) {
+            int rp[kLP], cl[kLP], ch[kLP];
+            int cmin = 1 << 30, cmax = -1;
+#pragma unroll
+            for (int p = 0; p < kLP; ++p) {
+                const int dxp = x0 + p - xs;
+                rp[p] = (dxp >= -R && dxp <= R) ? __ldg(J.rowidx + (dxp + R) * W + (dy + R)) : -1;
+                cl[p] = 1 << 30;
+                ch[p] = -1;
+                if (rp[p] >= 0) {
+                    const int2 c2 = __ldg(J.rowchunks + rp[p]);
+                    cl[p] = c2.x;
+                    ch[p] = c2.y;
+                    cmin = min(cmin, c2.x);
+                    cmax = max(cmax, c2.y);
+                }
+            }
+            if (cmax < 0) continue;
+            // lane's source row y - dy sits at slab row lane - dy + R; sources z0 + b + dz
+            // (dz = -R + 4c + j) at slab column b + 4c + j
+            const double* srow = slab + (lane - dy + R) * J.P;
+            double win[kLB + kLC - 1];
+#pragma unroll
+            for (int i = 0; i < kLB + kLC - 1; ++i) win[i] = srow[kLC * cmin + i];
+            for (int c = cmin; c <= cmax; ++c) {
+#pragma unroll
+                for (int p = 0; p < kLP; ++p) {
+                    if (c < cl[p] || c > ch[p]) continue;
+                    const double2 t01 = __ldg(reinterpret_cast<const double2*>(J.taps + size_t(rp[p]) * J.TW + kLC * c));
+                    const double2 t23 = __ldg(reinterpret_cast<const double2*>(J.taps + size_t(rp[p]) * J.TW + kLC * c + 2));
+                    const double tv[kLC] = {t01.x, t01.y, t23.x, t23.y};
+#pragma unroll
+                    for (int j = 0; j < kLC; ++j)
+#pragma unroll
+                        for (int b = 0; b < kLB; ++b) acc[p][b] = fma(tv[j], win[j + b], acc[p][b]);
+                }
+                if (c < cmax) {
+#pragma unroll
+                    for (int i = 0; i < kLB - 1; ++i) win[i] = win[i + kLC];
+#pragma unroll
+                    for (int i = kLB - 1; i < kLB + kLC - 1; ++i) win[i] = srow[kLC * (c + 1) + i];
+                }
+            }
+        }
+    }
+    const int y = y0 + lane;
+    if (y >= jb.d1) return;
+#pragma unroll
+    for (int p = 0; p < kLP; ++p) {
+        const int x = x0 + p;
+        if (x >= jb.d0) break;
+        const size_t rowoff = (size_t(x) * jb.d1 + y) * jb.d2;
+#pragma unroll
+        for (int b = 0; b < kLB; ++b) {
+            const int z = z0 + b;
+            if (z >= jb.d2) break;
+            if (J.S == 1)
+                jb.out[rowoff + z] = acc[p][b] * jb.scale;
+            else
+                J.partial[split * J.pstride + jb.off + rowoff + z] = acc[p][b];
+        }
+    }
+}
+
+// u = 2^-k * (((p_0 + p_1) + p_2) + ...) over the S partial lattices (fixed order)
+__global__ void k_lattice_reduce(LatJobs J, int64_t total, const ErrRec* err) {
+    if (failed(err)) return;
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    int jj = 0;
+    while (jj + 1 < J.n && size_t(i) >= J.j[jj + 1].off) ++jj;
+    const LatJob& jb = J.j[jj];
+    const size_t local = size_t(i) - jb.off;
+    double s = J.partial[jb.off + local];
+    for (int k = 1; k < J.S; ++k) s += J.partial[k * J.pstride + jb.off + local];
+    jb.out[local] = s * jb.scale;
+}
+
+size_t lattice_smem_bytes(const Geometry& g) {
     if (g.levels < 2) return 0;
-    const bool big = int64_t(g.lv[0].size) > kConvBigPoints;
-    const int Z = big ? kConvZ : kConvZSmall;
-    ConvJobs J;
-    J.njobs = 0;
-    int blocks = 0;
+    const int SY = 32 + 2 * g.lat.R, SZ = g.lat.TW + kLB - 1;
+    return size_t(SY) * size_t(SZ | 1) * sizeof(double);
+}
+
+cudaError_t lattice_prepare(size_t bytes) {
+    return cudaFuncSetAttribute(k_lattice, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(std::max<size_t>(bytes, 48 * 1024)));
+}
+
+int lattice_splits(const Geometry& g) {
+    if (g.levels < 2) return 1;
+    int64_t tiles = 0;
     for (int k = 0; k + 1 < g.levels; ++k) {
         const LevelGeom& lv = g.lv[k];
-        ConvJob j = make_job(g.lattice[k], lv, L.charge + lv.offset, L.pot + lv.offset, L.rows[k],
-                             L.dxb[k], L.taps[k], blocks, Z);
-        blocks += j.d0 * j.ty * j.tz;
-        J.j[J.njobs++] = j;
+        tiles += int64_t((lv.dims[0] + kLP - 1) / kLP) * ((lv.dims[1] + 31) / 32) * ((lv.dims[2] + kLB - 1) / kLB);
     }
-    return launch_conv_jobs(st, J, blocks, big, err);
+    const int64_t target = 148 * 16; // ~16 warps per SM
+    return int(std::max<int64_t>(1, std::min<int64_t>(8, (target + tiles - 1) / tiles)));
+}
+
+int launch_lattice(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err) {
+    if (g.levels < 2) return 0;
+    LatJobs J;
+    J.n = 0;
+    J.S = L.lat_S;
+    J.R = g.lat.R;
+    J.TW = g.lat.TW;
+    J.SZ = g.lat.TW + kLB - 1;
+    J.P = J.SZ | 1;
+    J.rowidx = L.lat_rowidx;
+    J.rowchunks = L.lat_rowchunks;
+    J.taps = L.lat_taps;
+    J.partial = L.lat_partial;
+    J.pstride = g.lattice_total;
+    int tiles = 0;
+    int64_t total = 0;
+    for (int k = 0; k + 1 < g.levels; ++k) {
+        const LevelGeom& lv = g.lv[k];
+        LatJob j;
+        j.q = L.charge + lv.offset;
+        j.out = L.pot + lv.offset;
+        j.d0 = lv.dims[0];
+        j.d1 = lv.dims[1];
+        j.d2 = lv.dims[2];
+        j.tzn = (j.d2 + kLB - 1) / kLB;
+        j.tyn = (j.d1 + 31) / 32;
+        j.blk0 = tiles;
+        j.scale = std::ldexp(1.0, -k);
+        j.off = lv.offset;
+        tiles += ((j.d0 + kLP - 1) / kLP) * j.tyn * j.tzn;
+        total = int64_t(lv.offset + lv.size);
+        J.j[J.n++] = j;
+    }
+    const size_t smem = lattice_smem_bytes(g);
+    k_lattice<<<tiles * J.S, 32, smem, st>>>(J, err);
+    if (J.S == 1) return 1;
+    k_lattice_reduce<<<int((total + 255) / 256), 256, 0, st>>>(J, total, err);
+    return 2;
 }
 
 // Small top levels: one thread per target point, a dense sum over every source

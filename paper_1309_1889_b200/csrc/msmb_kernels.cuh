@@ -43,6 +43,12 @@ struct DevLevels {      // concatenated lattices + tables
     int* tr_rcnt[kMaxLevels][3];
     int* tr_ridx[kMaxLevels][3];
     double* tr_rw[kMaxLevels][3];
+    // k_lattice: shared level-0 stencil + split partial lattices
+    int* lat_rowidx;
+    int2* lat_rowchunks;
+    double* lat_taps;
+    double* lat_partial;
+    int lat_S;
     // stencil tables: lattice levels then top (index levels-1)
     int4* rows[kMaxLevels];
     int* dxb[kMaxLevels];
@@ -80,6 +86,9 @@ int launch_restrict(cudaStream_t st, const Geometry& g, int k, DevLevels& L, Err
 int launch_restrict_all(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
 int launch_prolong_all(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
 int launch_lattice(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
+size_t lattice_smem_bytes(const Geometry& g);
+cudaError_t lattice_prepare(size_t bytes);
+int lattice_splits(const Geometry& g);
 int launch_top(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
 int launch_prolong(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err);
 int launch_interp(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c,
