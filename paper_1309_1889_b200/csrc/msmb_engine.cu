@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -147,9 +148,25 @@ static void alloc_plist(Workspace& W, int cap) {
     W.c.plist = W.plist_buf.as<int>();
 }
 
+static std::atomic<uint64_t> g_ws_uid{1};
+static std::mutex g_const_mu;
+static uint64_t g_const_owner[64] = {0}; // per device: uid of the workspace whose stencil is in c_lat_*
+
+// k_lattice<true> reads the level-0 stencil from constant memory, which is shared by
+// every field of the process on a device: make sure it holds this workspace's table.
+static void ensure_const_table(msmb_field* f, Workspace& W) {
+    if (!W.L.lat_const) return;
+    std::lock_guard<std::mutex> lk(g_const_mu);
+    const int d = f->device & 63;
+    if (g_const_owner[d] == W.uid) return;
+    ck(lattice_upload_const(W.g, f->stream), "cudaMemcpyToSymbol");
+    g_const_owner[d] = W.uid;
+}
+
 static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const double* box,
                                                  Error& e) {
     auto W = std::make_unique<Workspace>();
+    W->uid = g_ws_uid++;
     e = build_geometry(f->cfg, f->units, box, n, W->g);
     if (e.kind) return nullptr;
     Geometry& g = W->g;
@@ -215,6 +232,7 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
         L.lat_rowchunks = wupload(*W, rc);
         L.lat_taps = wupload(*W, g.lat.taps);
         L.lat_S = lattice_splits(g);
+        L.lat_const = lattice_const_fits(g) ? 1 : 0;
         L.lat_partial = L.lat_S > 1 ? walloc<double>(*W, size_t(L.lat_S) * g.lattice_total) : nullptr;
         ck(lattice_prepare(lattice_smem_bytes(g)), "cudaFuncSetAttribute");
     }
@@ -343,6 +361,7 @@ static int eval_device(msmb_field* f, StateBuf& sb, bool outputs) {
     Workspace& W = *f->ws;
     DevState s = sb.dev();
     for (int attempt = 0; attempt < 8; ++attempt) {
+        ensure_const_table(f, W);
         f->launches += launch_reset_err(f->stream, W.err, 0);
         W.launches_eval = enqueue_eval(f, W, s, outputs);
         ck(cudaGetLastError(), "kernel launch");
@@ -393,6 +412,7 @@ int engine_propagate(msmb_field* f, StateBuf& sb, double dt, int steps, double c
     // keep the input state: restored on error and on pair-list retries
     ck(cudaMemcpyAsync(bk, s.x, sizeof(double) * 6 * N, cudaMemcpyDeviceToDevice, f->stream), "backup");
     for (int attempt = 0; attempt < 8; ++attempt) {
+        ensure_const_table(f, W);
         const bool graphs = !f->timer.on;
         if (graphs && (W.graph_key != s.x || W.graph_dt != dt || W.graph_cap != W.cap || W.graph_bench)) {
             destroy_graphs(W);
@@ -878,6 +898,7 @@ int msmb_bench_propagate(msmb_field* f, msmb_system* sys, double dt, int steps, 
         (void)stages;
         return double(ms);
     };
+    ensure_const_table(f, W);
     f->launches += launch_reset_err(f->stream, W.err, 0);
     step_ms[0] = timed([&] {
         ck(cudaGraphLaunch(W.gx_eval, f->stream), "GraphLaunch");
@@ -1037,6 +1058,7 @@ int msmb_debug_stage(msmb_field* f, int stage, int k, const double box[3], const
     if (e.kind) return engine_set_error(f, e);
     Workspace& W = *f->ws;
     const Geometry& g = W.g;
+    ensure_const_table(f, W);
     f->launches += launch_reset_err(f->stream, W.err, 0);
     auto up = [&](double* d, const double* h, size_t cnt) {
         ck(cudaMemcpy(d, h, sizeof(double) * cnt, cudaMemcpyHostToDevice), "H2D");

@@ -86,6 +86,7 @@ struct Workspace {
     std::vector<std::string> stage_names;
     std::vector<cudaEvent_t> stage_ev;   // 2 per stage (begin, end)
     DBuf flush;                          // > L2, written between timed steps
+    uint64_t uid = 0;                    // identifies whose stencil is in constant memory
     ~Workspace();
 };
 

@@ -869,6 +869,39 @@ struct XferChain {
     int n;
 };
 
+// Production restriction: the same stencil applied as nested partial sums
+// sum_a wx[a] (sum_b wy[b] (sum_c wz[c] q)) with FMA -- exact in exact arithmetic,
+// ~1e-16 relative from the reference's scatter order (tolerance-tested; the
+// bit-exact variant k_restrict_tile backs msmb_debug_stage).
+__device__ __forceinline__ double restrict_point_fast(const XferP& p, const double* __restrict__ fine,
+                                                      int I, int J, int K) {
+    const int ni = p.rcnt[0][I], nj = p.rcnt[1][J], nk = p.rcnt[2][K];
+    double acc = 0.0;
+    for (int a = 0; a < ni; ++a) {
+        const int ix = p.ridx[0][I * kRestrictMax + a];
+        double accb = 0.0;
+        for (int b = 0; b < nj; ++b) {
+            const double* row = fine + (size_t(ix) * p.fd[1] + p.ridx[1][J * kRestrictMax + b]) * p.fd[2];
+            double accc = 0.0;
+            for (int c = 0; c < nk; ++c) accc = fma(p.rw[2][K * kRestrictMax + c], __ldg(row + p.ridx[2][K * kRestrictMax + c]), accc);
+            accb = fma(p.rw[1][J * kRestrictMax + b], accc, accb);
+        }
+        acc = fma(p.rw[0][I * kRestrictMax + a], accb, acc);
+    }
+    return acc;
+}
+
+__global__ void __launch_bounds__(128) k_restrict_fast(XferP p, const double* __restrict__ fine,
+                                                       double* coarse, const ErrRec* err) {
+    const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t m = int64_t(p.cd[0]) * p.cd[1] * p.cd[2];
+    if (idx >= m || failed(err)) return;
+    const int K = int(idx % p.cd[2]);
+    const int J = int((idx / p.cd[2]) % p.cd[1]);
+    const int I = int(idx / (int64_t(p.cd[2]) * p.cd[1]));
+    coarse[idx] = restrict_point_fast(p, fine, I, J, K);
+}
+
 __global__ void __launch_bounds__(512) k_restrict_chain(XferChain ch, const ErrRec* err) {
     if (failed(err)) return;
     for (int t = 0; t < ch.n; ++t) {
@@ -879,9 +912,7 @@ __global__ void __launch_bounds__(512) k_restrict_chain(XferChain ch, const ErrR
             const int K = int(idx % p.cd[2]);
             const int J = int((idx / p.cd[2]) % p.cd[1]);
             const int I = int(idx / (int64_t(p.cd[2]) * p.cd[1]));
-            ch.dst[t][idx] = restrict_point(p, I, J, K, [&](int i, int j, int k) {
-                return fine[(size_t(i) * p.fd[1] + j) * p.fd[2] + k];
-            });
+            ch.dst[t][idx] = restrict_point_fast(p, fine, I, J, K);
         }
         __syncthreads();
     }
@@ -906,11 +937,8 @@ int launch_restrict_all(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec
     for (int k = 0; k + 1 < g.levels; ++k) {
         const int64_t mc = int64_t(g.lv[k + 1].size);
         if (ch.n == 0 && mc >= kChainMax) {
-            const XferP p = make_xfer(g, k, L);
-            const int blocks = ((p.cd[0] + kRTx - 1) / kRTx) * ((p.cd[1] + kRTy - 1) / kRTy) *
-                               ((p.cd[2] + kRTz - 1) / kRTz);
-            k_restrict_tile<<<blocks, kRTx * kRTy * kRTz, 0, st>>>(p, L.charge + g.lv[k].offset,
-                                                                  L.charge + g.lv[k + 1].offset, err);
+            k_restrict_fast<<<int((mc + 127) / 128), 128, 0, st>>>(make_xfer(g, k, L), L.charge + g.lv[k].offset,
+                                                                   L.charge + g.lv[k + 1].offset, err);
             ++l;
         } else {
             ch.x[ch.n] = make_xfer(g, k, L);
@@ -1148,6 +1176,9 @@ static int launch_conv_jobs(cudaStream_t st, ConvJobs& J, int blocks, bool big, 
 // fixed order (deterministic).
 // ----------------------------------------------------------------------------
 constexpr int kLB = 8, kLP = 4, kLC = 4;
+constexpr int kLatConstRows = 320, kLatConstTW = 24; // constant-memory capacity (R <= 10)
+__constant__ double c_lat_taps[kLatConstRows * kLatConstTW];
+__constant__ int2 c_lat_chunks[kLatConstRows];
 
 struct LatJob {
     const double* q;
@@ -1169,6 +1200,7 @@ struct LatJobs {
     size_t pstride;      // lattice_total
 };
 
+template <bool CONST_TABLE>
 __global__ void __launch_bounds__(32) k_lattice(LatJobs J, const ErrRec* err) {
     extern __shared__ double slab[];
     if (failed(err)) return;
@@ -1195,6 +1227,19 @@ __global__ void __launch_bounds__(32) k_lattice(LatJobs J, const ErrRec* err) {
 #pragma unroll
         for (int b = 0; b < kLB; ++b) acc[p][b] = 0.0;
     for (int xs = xs_lo; xs <= xs_hi; ++xs) {
+        // row ids of the 4 planes for every dy: lane (dy + R) fetches, shuffles broadcast
+        int rid[kLP], rlo[kLP], rhi[kLP];
+#pragma unroll
+        for (int p = 0; p < kLP; ++p) {
+            const int dxp = x0 + p - xs;
+            int r = -1;
+            if (lane < W && dxp >= -R && dxp <= R) r = __ldg(J.rowidx + (dxp + R) * W + lane);
+            int2 ch = make_int2(1 << 30, -1);
+            if (r >= 0) ch = CONST_TABLE ? c_lat_chunks[r] : __ldg(J.rowchunks + r);
+            rid[p] = r;
+            rlo[p] = ch.x;
+            rhi[p] = ch.y;
+        }
         __syncwarp();
         const double* plane = jb.q + size_t(xs) * jb.d1 * jb.d2;
         for (int r = 0; r < SY; ++r) {
@@ -1211,17 +1256,11 @@ __global__ void __launch_bounds__(32) k_lattice(LatJobs J, const ErrRec* err) {
             int cmin = 1 << 30, cmax = -1;
 #pragma unroll
             for (int p = 0; p < kLP; ++p) {
-                const int dxp = x0 + p - xs;
-                rp[p] = (dxp >= -R && dxp <= R) ? __ldg(J.rowidx + (dxp + R) * W + (dy + R)) : -1;
-                cl[p] = 1 << 30;
-                ch[p] = -1;
-                if (rp[p] >= 0) {
-                    const int2 c2 = __ldg(J.rowchunks + rp[p]);
-                    cl[p] = c2.x;
-                    ch[p] = c2.y;
-                    cmin = min(cmin, c2.x);
-                    cmax = max(cmax, c2.y);
-                }
+                rp[p] = __shfl_sync(FULLMASK, rid[p], dy + R);
+                cl[p] = __shfl_sync(FULLMASK, rlo[p], dy + R);
+                ch[p] = __shfl_sync(FULLMASK, rhi[p], dy + R);
+                cmin = min(cmin, cl[p]);
+                cmax = max(cmax, ch[p]);
             }
             if (cmax < 0) continue;
             // lane's source row y - dy sits at slab row lane - dy + R; sources z0 + b + dz
@@ -1234,9 +1273,18 @@ __global__ void __launch_bounds__(32) k_lattice(LatJobs J, const ErrRec* err) {
 #pragma unroll
                 for (int p = 0; p < kLP; ++p) {
                     if (c < cl[p] || c > ch[p]) continue;
-                    const double2 t01 = __ldg(reinterpret_cast<const double2*>(J.taps + size_t(rp[p]) * J.TW + kLC * c));
-                    const double2 t23 = __ldg(reinterpret_cast<const double2*>(J.taps + size_t(rp[p]) * J.TW + kLC * c + 2));
-                    const double tv[kLC] = {t01.x, t01.y, t23.x, t23.y};
+                    double tv[kLC];
+                    if (CONST_TABLE) {
+#pragma unroll
+                        for (int j = 0; j < kLC; ++j) tv[j] = c_lat_taps[rp[p] * kLatConstTW + kLC * c + j];
+                    } else {
+                        const double2 t01 = __ldg(reinterpret_cast<const double2*>(J.taps + size_t(rp[p]) * J.TW + kLC * c));
+                        const double2 t23 = __ldg(reinterpret_cast<const double2*>(J.taps + size_t(rp[p]) * J.TW + kLC * c + 2));
+                        tv[0] = t01.x;
+                        tv[1] = t01.y;
+                        tv[2] = t23.x;
+                        tv[3] = t23.y;
+                    }
 #pragma unroll
                     for (int j = 0; j < kLC; ++j)
 #pragma unroll
@@ -1291,8 +1339,33 @@ size_t lattice_smem_bytes(const Geometry& g) {
 }
 
 cudaError_t lattice_prepare(size_t bytes) {
-    return cudaFuncSetAttribute(k_lattice, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_lattice<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(std::max<size_t>(bytes, 48 * 1024)));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_lattice<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(std::max<size_t>(bytes, 48 * 1024)));
+}
+
+bool lattice_const_fits(const Geometry& g) {
+    return g.levels >= 2 && g.lat.nrows <= kLatConstRows && g.lat.TW <= kLatConstTW;
+}
+
+// Copies the level-0 stencil into constant memory (the constant bank is global to
+// the module: the last field that uploads wins; engine.cu re-uploads per evaluation
+// when fields with different stencils share a process -- see Workspace::lat_key).
+cudaError_t lattice_upload_const(const Geometry& g, cudaStream_t st) {
+    if (!lattice_const_fits(g)) return cudaSuccess;
+    std::vector<double> taps(size_t(kLatConstRows) * kLatConstTW, 0.0);
+    for (int r = 0; r < g.lat.nrows; ++r)
+        for (int i = 0; i < g.lat.TW; ++i) taps[size_t(r) * kLatConstTW + i] = g.lat.taps[size_t(r) * g.lat.TW + i];
+    std::vector<int2> ch(kLatConstRows, make_int2(0, -1));
+    for (int r = 0; r < g.lat.nrows; ++r) ch[r] = make_int2(g.lat.rowchunks[r].x, g.lat.rowchunks[r].y);
+    cudaError_t e = cudaMemcpyToSymbolAsync(c_lat_taps, taps.data(), taps.size() * sizeof(double), 0,
+                                            cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpyToSymbolAsync(c_lat_chunks, ch.data(), ch.size() * sizeof(int2), 0, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return e;
+    return cudaStreamSynchronize(st);
 }
 
 int lattice_splits(const Geometry& g) {
@@ -1340,7 +1413,10 @@ int launch_lattice(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err
         J.j[J.n++] = j;
     }
     const size_t smem = lattice_smem_bytes(g);
-    k_lattice<<<tiles * J.S, 32, smem, st>>>(J, err);
+    if (L.lat_const)
+        k_lattice<true><<<tiles * J.S, 32, smem, st>>>(J, err);
+    else
+        k_lattice<false><<<tiles * J.S, 32, smem, st>>>(J, err);
     if (J.S == 1) return 1;
     k_lattice_reduce<<<int((total + 255) / 256), 256, 0, st>>>(J, total, err);
     return 2;

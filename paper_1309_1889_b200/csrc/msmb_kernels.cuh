@@ -49,6 +49,7 @@ struct DevLevels {      // concatenated lattices + tables
     double* lat_taps;
     double* lat_partial;
     int lat_S;
+    int lat_const;      // stencil lives in constant memory (k_lattice<true>)
     // stencil tables: lattice levels then top (index levels-1)
     int4* rows[kMaxLevels];
     int* dxb[kMaxLevels];
@@ -89,6 +90,8 @@ int launch_lattice(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err
 size_t lattice_smem_bytes(const Geometry& g);
 cudaError_t lattice_prepare(size_t bytes);
 int lattice_splits(const Geometry& g);
+bool lattice_const_fits(const Geometry& g);
+cudaError_t lattice_upload_const(const Geometry& g, cudaStream_t st);
 int launch_top(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
 int launch_prolong(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err);
 int launch_interp(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c,
