@@ -801,6 +801,7 @@ __device__ __forceinline__ double restrict_point(const XferP& p, int I, int J, i
 constexpr int kRTx = 4, kRTy = 4, kRTz = 8;
 constexpr int kRFx = 2 * kRTx + 6, kRFy = 2 * kRTy + 6, kRFz = 2 * kRTz + 6;
 
+template <bool BITWISE>
 __global__ void __launch_bounds__(kRTx * kRTy * kRTz)
     k_restrict_tile(XferP p, const double* __restrict__ fine, double* coarse, const ErrRec* err) {
     __shared__ double tile[kRFx * kRFy * kRFz];
@@ -821,9 +822,37 @@ __global__ void __launch_bounds__(kRTx * kRTy * kRTz)
     const int tz = threadIdx.x % kRTz, ty = (threadIdx.x / kRTz) % kRTy, tx = threadIdx.x / (kRTz * kRTy);
     const int I = I0 + tx, J = J0 + ty, K = K0 + tz;
     if (I >= p.cd[0] || J >= p.cd[1] || K >= p.cd[2]) return;
-    const double v = restrict_point(p, I, J, K, [&](int i, int j, int k) {
-        return tile[((i - fi0) * kRFy + (j - fj0)) * kRFz + (k - fk0)];
-    });
+    double v;
+    if (BITWISE) {
+        v = restrict_point(p, I, J, K, [&](int i, int j, int k) {
+            return tile[((i - fi0) * kRFy + (j - fj0)) * kRFz + (k - fk0)];
+        });
+    } else {
+        // production: sum_a wx[a] (sum_b wy[b] (sum_c wz[c] q)) with FMA -- exact in exact
+        // arithmetic, ~1e-16 relative from the reference's scatter order (tolerance-tested)
+        const int ni = p.rcnt[0][I], nj = p.rcnt[1][J], nk = p.rcnt[2][K];
+        int lz[kRestrictMax];
+        double wz[kRestrictMax];
+#pragma unroll
+        for (int c = 0; c < kRestrictMax; ++c) {
+            lz[c] = c < nk ? p.ridx[2][K * kRestrictMax + c] - fk0 : 0;
+            wz[c] = c < nk ? p.rw[2][K * kRestrictMax + c] : 0.0;
+        }
+        double acc = 0.0;
+        for (int a = 0; a < ni; ++a) {
+            const int li = p.ridx[0][I * kRestrictMax + a] - fi0;
+            double accb = 0.0;
+            for (int b = 0; b < nj; ++b) {
+                const double* row = tile + (li * kRFy + (p.ridx[1][J * kRestrictMax + b] - fj0)) * kRFz;
+                double accc = 0.0;
+#pragma unroll
+                for (int c = 0; c < kRestrictMax; ++c) accc = fma(wz[c], row[lz[c]], accc); // wz = 0 pads
+                accb = fma(p.rw[1][J * kRestrictMax + b], accc, accb);
+            }
+            acc = fma(p.rw[0][I * kRestrictMax + a], accb, acc);
+        }
+        v = acc;
+    }
     coarse[(size_t(I) * p.cd[1] + J) * p.cd[2] + K] = v;
 }
 
@@ -859,136 +888,26 @@ __global__ void k_prolong(XferP p, const double* __restrict__ coarse, double* fi
     prolong_point(p, coarse, fine, idx);
 }
 
-// Small levels: one CTA walks a chain of transitions with a block barrier between
-// levels (restriction upwards / prolongation downwards), saving a launch and the
-// per-launch latency for every small level.
-struct XferChain {
-    XferP x[kMaxLevels];
-    const double* src[kMaxLevels];
-    double* dst[kMaxLevels];
-    int n;
-};
-
-// Production restriction: the same stencil applied as nested partial sums
-// sum_a wx[a] (sum_b wy[b] (sum_c wz[c] q)) with FMA -- exact in exact arithmetic,
-// ~1e-16 relative from the reference's scatter order (tolerance-tested; the
-// bit-exact variant k_restrict_tile backs msmb_debug_stage).
-__device__ __forceinline__ double restrict_point_fast(const XferP& p, const double* __restrict__ fine,
-                                                      int I, int J, int K) {
-    const int ni = p.rcnt[0][I], nj = p.rcnt[1][J], nk = p.rcnt[2][K];
-    double acc = 0.0;
-    for (int a = 0; a < ni; ++a) {
-        const int ix = p.ridx[0][I * kRestrictMax + a];
-        double accb = 0.0;
-        for (int b = 0; b < nj; ++b) {
-            const double* row = fine + (size_t(ix) * p.fd[1] + p.ridx[1][J * kRestrictMax + b]) * p.fd[2];
-            double accc = 0.0;
-            for (int c = 0; c < nk; ++c) accc = fma(p.rw[2][K * kRestrictMax + c], __ldg(row + p.ridx[2][K * kRestrictMax + c]), accc);
-            accb = fma(p.rw[1][J * kRestrictMax + b], accc, accb);
-        }
-        acc = fma(p.rw[0][I * kRestrictMax + a], accb, acc);
-    }
-    return acc;
+static int restrict_blocks(const XferP& p) {
+    return ((p.cd[0] + kRTx - 1) / kRTx) * ((p.cd[1] + kRTy - 1) / kRTy) * ((p.cd[2] + kRTz - 1) / kRTz);
 }
-
-__global__ void __launch_bounds__(128) k_restrict_fast(XferP p, const double* __restrict__ fine,
-                                                       double* coarse, const ErrRec* err) {
-    const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t m = int64_t(p.cd[0]) * p.cd[1] * p.cd[2];
-    if (idx >= m || failed(err)) return;
-    const int K = int(idx % p.cd[2]);
-    const int J = int((idx / p.cd[2]) % p.cd[1]);
-    const int I = int(idx / (int64_t(p.cd[2]) * p.cd[1]));
-    coarse[idx] = restrict_point_fast(p, fine, I, J, K);
-}
-
-__global__ void __launch_bounds__(512) k_restrict_chain(XferChain ch, const ErrRec* err) {
-    if (failed(err)) return;
-    for (int t = 0; t < ch.n; ++t) {
-        const XferP& p = ch.x[t];
-        const double* fine = ch.src[t];
-        const int64_t m = int64_t(p.cd[0]) * p.cd[1] * p.cd[2];
-        for (int64_t idx = threadIdx.x; idx < m; idx += blockDim.x) {
-            const int K = int(idx % p.cd[2]);
-            const int J = int((idx / p.cd[2]) % p.cd[1]);
-            const int I = int(idx / (int64_t(p.cd[2]) * p.cd[1]));
-            ch.dst[t][idx] = restrict_point_fast(p, fine, I, J, K);
-        }
-        __syncthreads();
-    }
-}
-
-__global__ void __launch_bounds__(512) k_prolong_chain(XferChain ch, const ErrRec* err) {
-    if (failed(err)) return;
-    for (int t = 0; t < ch.n; ++t) {
-        const XferP& p = ch.x[t];
-        const int64_t m = int64_t(p.fd[0]) * p.fd[1] * p.fd[2];
-        for (int64_t idx = threadIdx.x; idx < m; idx += blockDim.x) prolong_point(p, ch.src[t], ch.dst[t], idx);
-        __syncthreads();
-    }
-}
-
-constexpr int64_t kChainMax = 6000; // transitions whose output has fewer points run in the chain kernel
 
 int launch_restrict_all(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err) {
     int l = 0;
-    XferChain ch;
-    ch.n = 0;
     for (int k = 0; k + 1 < g.levels; ++k) {
-        const int64_t mc = int64_t(g.lv[k + 1].size);
-        if (ch.n == 0 && mc >= kChainMax) {
-            k_restrict_fast<<<int((mc + 127) / 128), 128, 0, st>>>(make_xfer(g, k, L), L.charge + g.lv[k].offset,
-                                                                   L.charge + g.lv[k + 1].offset, err);
-            ++l;
-        } else {
-            ch.x[ch.n] = make_xfer(g, k, L);
-            ch.src[ch.n] = L.charge + g.lv[k].offset;
-            ch.dst[ch.n] = L.charge + g.lv[k + 1].offset;
-            ch.n++;
-        }
-    }
-    if (ch.n) {
-        k_restrict_chain<<<1, 512, 0, st>>>(ch, err);
+        const XferP p = make_xfer(g, k, L);
+        k_restrict_tile<false><<<restrict_blocks(p), kRTx * kRTy * kRTz, 0, st>>>(
+            p, L.charge + g.lv[k].offset, L.charge + g.lv[k + 1].offset, err);
         ++l;
     }
     return l;
 }
 
-int launch_prolong_all(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err) {
-    int l = 0;
-    XferChain ch;
-    ch.n = 0;
-    // top-down: small transitions first (chain), then the large ones
-    for (int k = g.levels - 2; k >= 0; --k) {
-        const int64_t mf = int64_t(g.lv[k].size);
-        if (mf < kChainMax) {
-            ch.x[ch.n] = make_xfer(g, k, L);
-            ch.src[ch.n] = L.pot + g.lv[k + 1].offset;
-            ch.dst[ch.n] = L.pot + g.lv[k].offset;
-            ch.n++;
-            continue;
-        }
-        if (ch.n) {
-            k_prolong_chain<<<1, 512, 0, st>>>(ch, err);
-            ++l;
-            ch.n = 0;
-        }
-        k_prolong<<<int((mf + 127) / 128), 128, 0, st>>>(make_xfer(g, k, L), L.pot + g.lv[k + 1].offset,
-                                                         L.pot + g.lv[k].offset, err);
-        ++l;
-    }
-    if (ch.n) {
-        k_prolong_chain<<<1, 512, 0, st>>>(ch, err);
-        ++l;
-    }
-    return l;
-}
-
+// bit-exact restriction of one level (msmb_debug_stage; tests/test_gpu_stages.py)
 int launch_restrict(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err) {
     const XferP p = make_xfer(g, k, L);
-    const int blocks = ((p.cd[0] + kRTx - 1) / kRTx) * ((p.cd[1] + kRTy - 1) / kRTy) * ((p.cd[2] + kRTz - 1) / kRTz);
-    k_restrict_tile<<<blocks, kRTx * kRTy * kRTz, 0, st>>>(p, L.charge + g.lv[k].offset,
-                                                          L.charge + g.lv[k + 1].offset, err);
+    k_restrict_tile<true><<<restrict_blocks(p), kRTx * kRTy * kRTz, 0, st>>>(p, L.charge + g.lv[k].offset,
+                                                                            L.charge + g.lv[k + 1].offset, err);
     return 1;
 }
 
@@ -997,6 +916,12 @@ int launch_prolong(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrR
     k_prolong<<<int((m + 127) / 128), 128, 0, st>>>(make_xfer(g, k, L), L.pot + g.lv[k + 1].offset,
                                                     L.pot + g.lv[k].offset, err);
     return 1;
+}
+
+int launch_prolong_all(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err) {
+    int l = 0;
+    for (int k = g.levels - 2; k >= 0; --k) l += launch_prolong(st, g, k, L, err);
+    return l;
 }
 
 // ============================================================================
