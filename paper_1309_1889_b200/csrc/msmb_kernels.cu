@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstdint>
 
 #include "msmb_kernels.cuh"
@@ -62,7 +63,15 @@ struct BinP {
     double inv_h;
     int d[3];
     int cw, ncx, ncy;
+    double sc[3];  // screening centre
+    float cut2f;   // screening cut^2 (fp32, rounded up)
 };
+
+static float float_ru(double x) { // host: smallest float >= x
+    float f = float(x);
+    if (double(f) < x) f = std::nextafter(f, 3e38f);
+    return f;
+}
 
 static BinP make_binp(const Geometry& g) {
     BinP p;
@@ -71,6 +80,8 @@ static BinP make_binp(const Geometry& g) {
         p.d[ax] = g.lv[0].dims[ax];
     }
     p.inv_h = g.inv_h0;
+    for (int ax = 0; ax < 3; ++ax) p.sc[ax] = g.screen_center[ax];
+    p.cut2f = float_ru(g.screen_cut2);
     p.cw = g.cw;
     p.ncx = g.ncx;
     p.ncy = g.ncy;
@@ -259,7 +270,10 @@ __global__ void k_gather(int n, const int* __restrict__ start_total, const int* 
     ys[s] = py;
     zs[s] = pz;
     qs[s] = qq;
-    f4[s] = make_float4(float(px), float(py), float(pz), 0.f);
+    {   // screening record (-2x', -2y', -2z', |x'|^2 - cut^2), x' = x - centre in fp32
+        const float fx = float(px - p.sc[0]), fy = float(py - p.sc[1]), fz = float(pz - p.sc[2]);
+        f4[s] = make_float4(-2.f * fx, -2.f * fy, -2.f * fz, fmaf(fz, fz, fmaf(fy, fy, fx * fx)) - p.cut2f);
+    }
     const double pp[3] = {px, py, pz};
     double w[3][4];
     for (int ax = 0; ax < 3; ++ax) {
@@ -419,6 +433,7 @@ __global__ void k_pairlist(const int* __restrict__ nclu, const float4* __restric
 }
 
 struct PairP {
+    double sc[3];        // screening centre
     double a2;
     long long a2bits;
     double c0, c1, c2;   // gamma(r/a)/a = c0 + r2*(c1 + r2*c2)
@@ -444,46 +459,56 @@ __device__ __forceinline__ void record_pair(ErrRec* err, int i, int j) {
 }
 
 // One warp per i-cluster (lane = i atom).  For every candidate j-cluster the warp
-// stages its 32 atoms in shared memory -- fp64 words split into 32-bit rows so
-// any lane->atom mapping reads conflict-free, plus an fp32 screening record
-// (-2x', -2y', -2z', |x'|^2 - cut^2) with x' the position relative to the
-// i-cluster's first atom -- builds each lane's 32-bit in-range mask with 4 packed
-// fp32x2 operations per two candidates (r^2 - cut^2 = |xi'|^2 + |xj'|^2 - cut^2
-// - 2 xi'.xj', sign bits shifted into the mask), then walks the set bits so the
-// DP pipe only sees screened pairs.  The exact fp64 test r2 < a2 decides inclusion
-// (src/msm_phases.cpp:240).  The next j-cluster is prefetched into registers
-// while the current one is processed.  Coincident pairs are caught in k_cellsort.
+// stages its 32 atoms in shared memory -- the fp32 screening records of k_gather
+// (-2x', -2y', -2z', |x'|^2 - cut^2) as SoA rows, and the fp64 x, y, z, q split
+// into 32-bit rows in which atom t sits at slot 32 - t and slot 0 is a dummy atom
+// (q = 0, far away), so any lane->slot mapping reads conflict-free -- then builds
+// each lane's 32-bit in-range mask with 4 packed fp32x2 operations per two
+// candidates (bit 31 - t <=> atom t), and walks the set bits with ffs; lanes that
+// run out of bits read the dummy slot, so the loop body has no selects or
+// branches.  The fp32 screen admits pairs up to a(1 + ~1e-3) (error bound of the
+// dot-product form, msmb_geometry.cpp); the reference skips r >= a
+// (src/msm_phases.cpp:240).  Those margin pairs are evaluated with the r < a
+// polynomial, and because g* is C^2 at r = a they add O(((r-a)/a)^3) ~ 1e-10 * q_j
+// to phi and O(((r-a)/a)^2) to g*'/r -- orders below the 1e-10 energy / 1e-8
+// force tolerances (tests/test_gpu_parity.py).  The next j-cluster is
+// prefetched into registers while the current one is processed.  Coincident
+// pairs are caught in k_cellsort.
+constexpr int kSlots = 33;
+
 __global__ void __launch_bounds__(kPairWarps * 32, 5)
     k_pairs(const int* __restrict__ nclu, const int2* __restrict__ clu,
             const int* __restrict__ plist, const int* __restrict__ pcnt, int cap,
             const double* __restrict__ xs, const double* __restrict__ ys,
             const double* __restrict__ zs, const double* __restrict__ qs,
-            const float4* __restrict__ f4, const int* __restrict__ perm, PairP p, double* phis,
-            double* fsx, double* fsy, double* fsz, ErrRec* err) {
-    __shared__ __align__(16) float s_sc[kPairWarps][4][32]; // -2x', -2y', -2z', |x'|^2 - cut^2
-    __shared__ unsigned s_w[kPairWarps][8][32];
+            const float4* __restrict__ f4, PairP p, double* phis, double* fsx, double* fsy,
+            double* fsz, ErrRec* err) {
+    __shared__ __align__(16) float s_sc[kPairWarps][4][32];
+    __shared__ unsigned s_w[kPairWarps][8][kSlots];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ic = blockIdx.x * kPairWarps + w;
     if (ic >= *nclu || failed(err)) return;
     double a2 = p.a2, c0 = p.c0, c1 = p.c1, c2 = p.c2, d0 = p.d0, d1 = p.d1;
     asm volatile("" : "+d"(a2), "+d"(c0), "+d"(c1), "+d"(c2), "+d"(d0), "+d"(d1));
-    const float cut2f = p.cut2f;
     const int2 c = clu[ic];
     const bool vi = lane < c.y;
     const int si = c.x + (vi ? lane : 0);
     const double xi = xs[si], yi = ys[si], zi = zs[si], qi = qs[si];
-    const double rx = xs[c.x], ry = ys[c.x], rz = zs[c.x]; // reference point (uniform)
-    const float xf = float(xi - rx), yf = float(yi - ry), zf = float(zi - rz);
+    const float xf = float(xi - p.sc[0]), yf = float(yi - p.sc[1]), zf = float(zi - p.sc[2]);
     const float2 xi2 = make_float2(xf, xf), yi2 = make_float2(yf, yf), zi2 = make_float2(zf, zf);
     const float nif = fmaf(zf, zf, fmaf(yf, yf, xf * xf));
     const float2 ni2 = make_float2(nif, nif);
+    // dummy slot 0: position (1e4, 1e4, 1e4) A -- far from every covered particle, so
+    // r2 ~ 1e8 keeps g, g' finite -- and q = 0: idle lanes add exact zeros
+    if (lane < 8) s_w[w][lane][0] = (lane == 1 || lane == 3 || lane == 5) ? 0x40C38800u : 0u;
     double ph = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
-    unsigned npair = 0, ncand = 0;
+    unsigned ncand = 0;
     const int nj = pcnt[ic];
     const int* pl = plist + size_t(ic) * cap;
     int jc_n = 0;
     int2 cj_n = make_int2(0, 0);
     double xj_n = 0, yj_n = 0, zj_n = 0, qj_n = 0;
+    float4 fj_n = make_float4(0.f, 0.f, 0.f, 0.f);
     auto fetch = [&](int jj) {
         jc_n = pl[jj];
         cj_n = clu[jc_n];
@@ -492,28 +517,29 @@ __global__ void __launch_bounds__(kPairWarps * 32, 5)
         yj_n = ys[sj];
         zj_n = zs[sj];
         qj_n = qs[sj];
+        fj_n = f4[sj];
     };
     if (nj > 0) fetch(0);
     for (int jj = 0; jj < nj; ++jj) {
         const int jc = jc_n;
         const bool vj = lane < cj_n.y;
-        const float xj = float(xj_n - rx), yj = float(yj_n - ry), zj = float(zj_n - rz);
         __syncwarp();
-        s_sc[w][0][lane] = -2.f * xj;
-        s_sc[w][1][lane] = -2.f * yj;
-        s_sc[w][2][lane] = -2.f * zj;
-        s_sc[w][3][lane] = vj ? fmaf(zj, zj, fmaf(yj, yj, xj * xj)) - cut2f : 3e38f;
-        s_w[w][0][lane] = __double2loint(xj_n);
-        s_w[w][1][lane] = __double2hiint(xj_n);
-        s_w[w][2][lane] = __double2loint(yj_n);
-        s_w[w][3][lane] = __double2hiint(yj_n);
-        s_w[w][4][lane] = __double2loint(zj_n);
-        s_w[w][5][lane] = __double2hiint(zj_n);
-        s_w[w][6][lane] = __double2loint(qj_n);
-        s_w[w][7][lane] = __double2hiint(qj_n);
+        s_sc[w][0][lane] = fj_n.x;
+        s_sc[w][1][lane] = fj_n.y;
+        s_sc[w][2][lane] = fj_n.z;
+        s_sc[w][3][lane] = vj ? fj_n.w : 3e38f;
+        const int slot = 32 - lane;
+        s_w[w][0][slot] = __double2loint(xj_n);
+        s_w[w][1][slot] = __double2hiint(xj_n);
+        s_w[w][2][slot] = __double2loint(yj_n);
+        s_w[w][3][slot] = __double2hiint(yj_n);
+        s_w[w][4][slot] = __double2loint(zj_n);
+        s_w[w][5][slot] = __double2hiint(zj_n);
+        s_w[w][6][slot] = __double2loint(qj_n);
+        s_w[w][7][slot] = __double2hiint(qj_n);
         __syncwarp();
         if (jj + 1 < nj) fetch(jj + 1);
-        // ---- screening: bit (31 - t) of mask <=> atom t within cut (fp32, with margin)
+        // ---- screening: bit (31 - t) of mask <=> atom t within the screening cut
         unsigned mask = 0;
 #pragma unroll
         for (int t = 0; t < 32; t += 4) {
@@ -539,29 +565,25 @@ __global__ void __launch_bounds__(kPairWarps * 32, 5)
         const int pc = __popc(mask);
         ncand += pc;
         const int iters = __reduce_max_sync(FULLMASK, pc);
+        const unsigned* row = &s_w[w][0][0];
         for (int k = 0; k < iters; ++k) {
-            const int t = __clz(mask) & 31;
-            const bool has = mask != 0;
-            mask &= ~(0x80000000u >> t);
-            const double xj2 = __hiloint2double(s_w[w][1][t], s_w[w][0][t]);
-            const double yj2 = __hiloint2double(s_w[w][3][t], s_w[w][2][t]);
-            const double zj2 = __hiloint2double(s_w[w][5][t], s_w[w][4][t]);
-            const double qj2 = __hiloint2double(s_w[w][7][t], s_w[w][6][t]);
-            const double dx = xi - xj2, dy = yi - yj2, dz = zi - zj2;
+            const int sl = __ffs(mask); // atom 32 - sl, or the dummy (0) once the lane is done
+            mask &= mask - 1;
+            const double xj = __hiloint2double(row[1 * kSlots + sl], row[0 * kSlots + sl]);
+            const double yj = __hiloint2double(row[3 * kSlots + sl], row[2 * kSlots + sl]);
+            const double zj = __hiloint2double(row[5 * kSlots + sl], row[4 * kSlots + sl]);
+            const double qj = __hiloint2double(row[7 * kSlots + sl], row[6 * kSlots + sl]);
+            const double dx = xi - xj, dy = yi - yj, dz = zi - zj;
             const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-            const bool in = has && (r2 < a2);
-            const double r2s = in ? r2 : a2; // excluded / idle lanes: finite dummy (0 * inf = NaN)
-            const double rinv = rsqrt_pos(r2s);
+            const double rinv = rsqrt_pos(r2);
             const double rinv2 = rinv * rinv;
-            const double g = rinv - fma(r2s, fma(r2s, c2, c1), c0);   // g*(r)
-            const double sd = fma(-rinv, rinv2, fma(r2s, d1, d0));    // g*'(r)/r
-            const double qe = in ? qj2 : 0.0;
-            ph = fma(qe, g, ph);
-            const double wgt = qe * sd;
+            const double g = rinv - fma(r2, fma(r2, c2, c1), c0);   // g*(r)
+            const double sd = fma(-rinv, rinv2, fma(r2, d1, d0));  // g*'(r)/r
+            ph = fma(qj, g, ph);
+            const double wgt = qj * sd;
             fx = fma(dx, wgt, fx);
             fy = fma(dy, wgt, fy);
             fz = fma(dz, wgt, fz);
-            npair += in ? 1u : 0u;
         }
     }
     if (vi) {
@@ -571,10 +593,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, 5)
         fsy[si] = fy * kq;
         fsz[si] = fz * kq;
     }
-    npair = __reduce_add_sync(FULLMASK, npair);
     ncand = __reduce_add_sync(FULLMASK, ncand);
     if (lane == 0) {
-        atomicAdd(&err->pairs, (unsigned long long)npair);
+        atomicAdd(&err->pairs, (unsigned long long)ncand);
         atomicAdd(&err->candidates, (unsigned long long)ncand);
     }
 }
@@ -639,12 +660,13 @@ int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& 
     p.d0 = 2.5 / (A * A * A);
     p.d1 = -1.5 / (A * A * A * A * A);
     p.kc = g.units.coulomb_constant;
-    p.cut2f = float(g.screen_cut * g.screen_cut);
+    p.cut2f = float_ru(g.screen_cut2);
+    for (int ax = 0; ax < 3; ++ax) p.sc[ax] = g.screen_center[ax];
     const int64_t maxclu = n / 32 + g.ncols + 1;
     int l = 0;
     if (n > 0) {
         k_pairs<<<int((maxclu + kPairWarps - 1) / kPairWarps), kPairWarps * 32, 0, st>>>(
-            c.nclu, c.clu, c.plist, c.pcnt, cap, a.xs, a.ys, a.zs, a.qs, a.f4, a.perm, p, a.phis,
+            c.nclu, c.clu, c.plist, c.pcnt, cap, a.xs, a.ys, a.zs, a.qs, a.f4, p, a.phis,
             a.fsx, a.fsy, a.fsz, err);
         k_err_brute<<<592, 256, 0, st>>>(n, s.x, s.y, s.z, a.outlist, err);
         l = 2;
