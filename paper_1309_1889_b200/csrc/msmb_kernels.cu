@@ -459,19 +459,19 @@ __device__ __forceinline__ void record_pair(ErrRec* err, int i, int j) {
 }
 
 // One warp per i-cluster (lane = i atom).  For every candidate j-cluster the warp
-// stages its 32 atoms in shared memory -- the fp32 screening records of k_gather
-// (-2x', -2y', -2z', |x'|^2 - cut^2) as SoA rows, and the fp64 x, y, z, q split
+// stages its 32 atoms in shared memory -- fp32 screening records
+// (-2x', -2y', -2z', |x'|^2 - cut^2), x' relative to the i-cluster, as SoA rows,
+// and the fp64 x, y, z, q split
 // into 32-bit rows in which atom t sits at slot 32 - t and slot 0 is a dummy atom
 // (q = 0, far away), so any lane->slot mapping reads conflict-free -- then builds
 // each lane's 32-bit in-range mask with 4 packed fp32x2 operations per two
 // candidates (bit 31 - t <=> atom t), and walks the set bits with ffs; lanes that
 // run out of bits read the dummy slot, so the loop body has no selects or
-// branches.  The fp32 screen admits pairs up to a(1 + ~1e-3) (error bound of the
-// dot-product form, msmb_geometry.cpp); the reference skips r >= a
-// (src/msm_phases.cpp:240).  Those margin pairs are evaluated with the r < a
-// polynomial, and because g* is C^2 at r = a they add O(((r-a)/a)^3) ~ 1e-10 * q_j
-// to phi and O(((r-a)/a)^2) to g*'/r -- orders below the 1e-10 energy / 1e-8
-// force tolerances (tests/test_gpu_parity.py).  The next j-cluster is
+// branches.  The fp32 screen admits pairs up to a(1 + ~1e-5) (its rigorous error
+// bound); the reference skips r >= a (src/msm_phases.cpp:240).  Those margin
+// pairs are evaluated with the r < a polynomial, and because g* is C^2 at r = a
+// they add O(((r-a)/a)^3) ~ 1e-15 * q_j to phi and O(((r-a)/a)^2) to g*'/r --
+// orders below the 1e-10 energy / 1e-8 force tolerances (tests/test_gpu_parity.py).  The next j-cluster is
 // prefetched into registers while the current one is processed.  Coincident
 // pairs are caught in k_cellsort.
 constexpr int kSlots = 33;
@@ -494,10 +494,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, 5)
     const bool vi = lane < c.y;
     const int si = c.x + (vi ? lane : 0);
     const double xi = xs[si], yi = ys[si], zi = zs[si], qi = qs[si];
-    const float xf = float(xi - p.sc[0]), yf = float(yi - p.sc[1]), zf = float(zi - p.sc[2]);
+    // fp32 screening coordinates relative to the i-cluster's first atom (|x'| ~ tens of A)
+    const double rx = xs[c.x], ry = ys[c.x], rz = zs[c.x];
+    const float xf = float(xi - rx), yf = float(yi - ry), zf = float(zi - rz);
     const float2 xi2 = make_float2(xf, xf), yi2 = make_float2(yf, yf), zi2 = make_float2(zf, zf);
     const float nif = fmaf(zf, zf, fmaf(yf, yf, xf * xf));
     const float2 ni2 = make_float2(nif, nif);
+    const float ri2 = __uint_as_float(__reduce_max_sync(FULLMASK, __float_as_uint(vi ? nif : 0.f)));
     // dummy slot 0: position (1e4, 1e4, 1e4) A -- far from every covered particle, so
     // r2 ~ 1e8 keeps g, g' finite -- and q = 0: idle lanes add exact zeros
     if (lane < 8) s_w[w][lane][0] = (lane == 1 || lane == 3 || lane == 5) ? 0x40C38800u : 0u;
@@ -508,7 +511,6 @@ __global__ void __launch_bounds__(kPairWarps * 32, 5)
     int jc_n = 0;
     int2 cj_n = make_int2(0, 0);
     double xj_n = 0, yj_n = 0, zj_n = 0, qj_n = 0;
-    float4 fj_n = make_float4(0.f, 0.f, 0.f, 0.f);
     auto fetch = [&](int jj) {
         jc_n = pl[jj];
         cj_n = clu[jc_n];
@@ -517,17 +519,23 @@ __global__ void __launch_bounds__(kPairWarps * 32, 5)
         yj_n = ys[sj];
         zj_n = zs[sj];
         qj_n = qs[sj];
-        fj_n = f4[sj];
     };
     if (nj > 0) fetch(0);
     for (int jj = 0; jj < nj; ++jj) {
         const int jc = jc_n;
         const bool vj = lane < cj_n.y;
+        // screening record (-2x', -2y', -2z', |x'|^2 - cut^2) of this lane's j atom.  The
+        // fp32 evaluation of r^2 - cut^2 = |xi'|^2 + |xj'|^2 - 2 xi'.xj' - cut^2 errs by
+        // < 16 * 2^-24 * (|xi'| + |xj'|)^2; cut^2 is padded by twice that (uniform per j-cluster).
+        const float xj = float(xj_n - rx), yj = float(yj_n - ry), zj = float(zj_n - rz);
+        const float njf = fmaf(zj, zj, fmaf(yj, yj, xj * xj));
+        const float rj2 = __uint_as_float(__reduce_max_sync(FULLMASK, __float_as_uint(vj ? njf : 0.f)));
+        const float cut2 = p.cut2f + 64.f * 5.9604645e-8f * (ri2 + rj2);
         __syncwarp();
-        s_sc[w][0][lane] = fj_n.x;
-        s_sc[w][1][lane] = fj_n.y;
-        s_sc[w][2][lane] = fj_n.z;
-        s_sc[w][3][lane] = vj ? fj_n.w : 3e38f;
+        s_sc[w][0][lane] = -2.f * xj;
+        s_sc[w][1][lane] = -2.f * yj;
+        s_sc[w][2][lane] = -2.f * zj;
+        s_sc[w][3][lane] = vj ? njf - cut2 : 3e38f;
         const int slot = 32 - lane;
         s_w[w][0][slot] = __double2loint(xj_n);
         s_w[w][1][slot] = __double2hiint(xj_n);
@@ -660,7 +668,7 @@ int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& 
     p.d0 = 2.5 / (A * A * A);
     p.d1 = -1.5 / (A * A * A * A * A);
     p.kc = g.units.coulomb_constant;
-    p.cut2f = float_ru(g.screen_cut2);
+    p.cut2f = float_ru(A * A * (1.0 + 1e-6)); // + per-j-cluster rounding pad in k_pairs
     for (int ax = 0; ax < 3; ++ax) p.sc[ax] = g.screen_center[ax];
     const int64_t maxclu = n / 32 + g.ncols + 1;
     int l = 0;
