@@ -8,7 +8,10 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libmsmb.so"
+import os
+
+# MSMB_LIB overrides the library path (used only by tools/ to compare kernel variants)
+LIB_PATH = Path(os.environ.get("MSMB_LIB", Path(__file__).resolve().parent / "lib" / "libmsmb.so"))
 
 _D = C.POINTER(C.c_double)
 _L = C.POINTER(C.c_int64)

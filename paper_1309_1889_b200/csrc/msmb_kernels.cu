@@ -475,8 +475,11 @@ __device__ __forceinline__ void record_pair(ErrRec* err, int i, int j) {
 // prefetched into registers while the current one is processed.  Coincident
 // pairs are caught in k_cellsort.
 constexpr int kSlots = 33;
+#ifndef MSMB_PAIR_MINB
+#define MSMB_PAIR_MINB 5
+#endif
 
-__global__ void __launch_bounds__(kPairWarps * 32, 5)
+__global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     k_pairs(const int* __restrict__ nclu, const int2* __restrict__ clu,
             const int* __restrict__ plist, const int* __restrict__ pcnt, int cap,
             const double* __restrict__ xs, const double* __restrict__ ys,
