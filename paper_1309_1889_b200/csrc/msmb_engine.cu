@@ -36,7 +36,6 @@ static void ck(cudaError_t e, const char* where) {
 }
 
 Workspace::~Workspace() {
-    for (auto e : stage_ev) cudaEventDestroy(e);
     if (gx_eval) cudaGraphExecDestroy(gx_eval);
     if (gx_step1) cudaGraphExecDestroy(gx_step1);
     if (gx_step2) cudaGraphExecDestroy(gx_step2);
@@ -300,28 +299,41 @@ static int stage_id(const char* name) {
     return -1;
 }
 
+// The long-range chain (anterpolation .. prolongation) depends only on the binned,
+// sorted atoms, and the short-range pair sum only on the cluster lists, so after
+// the sort the chain is forked onto the field's high-priority side stream and
+// joined before interpolation, which consumes both (a fork/join in the captured
+// graphs).  The two branches write disjoint buffers; every reduction keeps its
+// fixed order, so results do not depend on how the branches interleave.  With
+// per-stage timing on, everything runs on one stream so the stage events are
+// exclusive.
 static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs) {
     cudaStream_t st = f->stream;
+    const bool fork = !f->timer.on;
+    cudaStream_t lr = fork ? f->side : st;
     const Geometry& g = W.g;
     int total = 0;
     auto run = [&](const char* name, auto&& fn) {
         StageScope sc(f, name);
-        const int id = stage_id(name);
-        if (W.capture_events && id >= 0) cudaEventRecord(W.stage_ev[2 * id], st);
         const int nl = fn();
-        if (W.capture_events && id >= 0) cudaEventRecord(W.stage_ev[2 * id + 1], st);
         sc.done(nl);
         total += nl;
     };
     run("bin", [&] { return launch_bin(st, g, s, W.a, W.c, W.err); });
     run("sort", [&] { return launch_sort(st, g, s, W.a, W.c, W.err); });
+    if (fork) {
+        ck(cudaEventRecord(f->fork_ev, st), "fork");
+        ck(cudaStreamWaitEvent(lr, f->fork_ev, 0), "fork");
+    }
+    run("anterp", [&] { return launch_anterp(lr, g, W.a, W.c, W.L, W.err); });
+    run("restrict", [&] { return launch_restrict_all(lr, g, W.L, W.err); });
+    run("lattice", [&] { return launch_lattice(lr, g, W.L, W.err); });
+    run("top", [&] { return launch_top(lr, g, W.L, W.err); });
+    run("prolong", [&] { return launch_prolong_all(lr, g, W.L, W.err); });
+    if (fork) ck(cudaEventRecord(f->join_ev, lr), "join");
     run("clusters", [&] { return launch_clusters(st, g, s.n, W.a, W.c, W.err, W.cap); });
     run("pairs", [&] { return launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap); });
-    run("anterp", [&] { return launch_anterp(st, g, W.a, W.c, W.L, W.err); });
-    run("restrict", [&] { return launch_restrict_all(st, g, W.L, W.err); });
-    run("lattice", [&] { return launch_lattice(st, g, W.L, W.err); });
-    run("top", [&] { return launch_top(st, g, W.L, W.err); });
-    run("prolong", [&] { return launch_prolong_all(st, g, W.L, W.err); });
+    if (fork) ck(cudaStreamWaitEvent(st, f->join_ev, 0), "join");
     DevOut o = W.o;
     if (!outputs) o.phi = o.phis = o.phil = o.e = nullptr;
     run("interp", [&] { return launch_interp(st, g, s.n, W.a, W.c, W.L, o, W.err, outputs ? 1 : 0); });
@@ -386,13 +398,41 @@ static void destroy_graphs(Workspace& W) {
 }
 
 template <class Fn>
+static cudaGraphExec_t capture(msmb_field* f, Fn&& fn);
+
+// The three step graphs of a propagate call (cached per state buffer, dt and
+// pair-list capacity): evaluation, first step (kick + drift + evaluation), and
+// later steps (fused kick + kick + drift + evaluation).
+static void ensure_graphs(msmb_field* f, Workspace& W, DevState& s, double dt, double conv) {
+    if (W.graph_key == s.x && W.graph_dt == dt && W.graph_cap == W.cap) return;
+    destroy_graphs(W);
+    int nl = 0;
+    W.gx_eval = capture(f, [&] { nl = enqueue_eval(f, W, s, false); });
+    W.launches_eval = nl;
+    W.gx_step1 = capture(f, [&] {
+        nl = launch_kick_drift(f->stream, s, W.o, dt, conv, 1, W.err);
+        nl += enqueue_eval(f, W, s, false);
+    });
+    W.gx_step2 = capture(f, [&] {
+        nl = launch_kick_drift(f->stream, s, W.o, dt, conv, 2, W.err);
+        nl += enqueue_eval(f, W, s, false);
+    });
+    W.launches_step = nl;
+    f->launches -= 3 * int64_t(W.launches_eval); // captures are not launches
+    W.graph_key = s.x;
+    W.graph_dt = dt;
+    W.graph_cap = W.cap;
+}
+
+template <class Fn>
 static cudaGraphExec_t capture(msmb_field* f, Fn&& fn) {
     cudaGraph_t graph;
     ck(cudaStreamBeginCapture(f->stream, cudaStreamCaptureModeThreadLocal), "BeginCapture");
     fn();
     ck(cudaStreamEndCapture(f->stream, &graph), "EndCapture");
     cudaGraphExec_t ex;
-    ck(cudaGraphInstantiate(&ex, graph, 0), "GraphInstantiate");
+    ck(cudaGraphInstantiateWithFlags(&ex, graph, cudaGraphInstantiateFlagUseNodePriority),
+       "GraphInstantiate");
     cudaGraphDestroy(graph);
     return ex;
 }
@@ -414,26 +454,7 @@ int engine_propagate(msmb_field* f, StateBuf& sb, double dt, int steps, double c
     for (int attempt = 0; attempt < 8; ++attempt) {
         ensure_const_table(f, W);
         const bool graphs = !f->timer.on;
-        if (graphs && (W.graph_key != s.x || W.graph_dt != dt || W.graph_cap != W.cap || W.graph_bench)) {
-            destroy_graphs(W);
-            int nl = 0;
-            W.gx_eval = capture(f, [&] { nl = enqueue_eval(f, W, s, false); });
-            W.launches_eval = nl;
-            W.gx_step1 = capture(f, [&] {
-                nl = launch_kick_drift(f->stream, s, W.o, dt, conv, 1, W.err);
-                nl += enqueue_eval(f, W, s, false);
-            });
-            W.gx_step2 = capture(f, [&] {
-                nl = launch_kick_drift(f->stream, s, W.o, dt, conv, 2, W.err);
-                nl += enqueue_eval(f, W, s, false);
-            });
-            W.launches_step = nl;
-            f->launches -= 3 * int64_t(W.launches_eval); // captures are not launches
-            W.graph_key = s.x;
-            W.graph_dt = dt;
-            W.graph_cap = W.cap;
-            W.graph_bench = false;
-        }
+        if (graphs) ensure_graphs(f, W, s, dt, conv);
         f->launches += launch_reset_err(f->stream, W.err, 0);
         if (graphs) {
             ck(cudaGraphLaunch(W.gx_eval, f->stream), "GraphLaunch");
@@ -617,7 +638,16 @@ int msmb_create(const msmb_msm_config* cfg, const msmb_units* units, int device,
     f->units = *units;
     f->device = device;
     cudaSetDevice(device);
-    if (cudaStreamCreateWithFlags(&f->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    if (cudaStreamCreateWithPriority(&f->stream, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&f->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f->join_ev, cudaEventDisableTiming) != cudaSuccess) {
+        if (f->stream) cudaStreamDestroy(f->stream);
+        if (f->side) cudaStreamDestroy(f->side);
+        if (f->fork_ev) cudaEventDestroy(f->fork_ev);
+        if (f->join_ev) cudaEventDestroy(f->join_ev);
         delete f;
         g_create_error = Error{MSMB_ERR_CUDA, -1, -1, -1, "cudaStreamCreate failed"};
         return MSMB_ERR_CUDA;
@@ -632,6 +662,9 @@ static void field_free(msmb_field* f) {
     f->ws.reset();
     f->scratch.buf.reset();
     cudaStreamDestroy(f->stream);
+    cudaStreamDestroy(f->side);
+    cudaEventDestroy(f->fork_ev);
+    cudaEventDestroy(f->join_ev);
     delete f;
 }
 
@@ -852,33 +885,10 @@ int msmb_bench_propagate(msmb_field* f, msmb_system* sys, double dt, int steps, 
     DevState s = sb.dev();
     const size_t N = size_t(sb.n > 0 ? sb.n : 1);
     const double conv = f->units.energy_to_native;
-    if (W.stage_ev.empty()) {
-        W.stage_ev.resize(2 * kNumStages);
-        for (auto& ev : W.stage_ev) ck(cudaEventCreate(&ev), "cudaEventCreate");
-    }
     const size_t flush_bytes = size_t(256) << 20; // 2x the 126 MB L2
     if (flush_l2 && W.flush.bytes < flush_bytes) ck(W.flush.alloc(flush_bytes), "cudaMalloc flush");
     if (f->timer.on) f->timer.on = false;
-    if (!(W.graph_key == s.x && W.graph_dt == dt && W.graph_cap == W.cap && W.graph_bench)) {
-        destroy_graphs(W);
-        int nl = 0;
-        W.gx_eval = capture(f, [&] { nl = enqueue_eval(f, W, s, false); });
-        W.launches_eval = nl;
-        W.gx_step1 = capture(f, [&] {
-            nl = launch_kick_drift(f->stream, s, W.o, dt, conv, 1, W.err);
-            nl += enqueue_eval(f, W, s, false);
-        });
-        W.gx_step2 = capture(f, [&] {
-            nl = launch_kick_drift(f->stream, s, W.o, dt, conv, 2, W.err);
-            nl += enqueue_eval(f, W, s, false);
-        });
-        W.launches_step = nl;
-        f->launches -= 3 * int64_t(W.launches_eval);
-        W.graph_key = s.x;
-        W.graph_dt = dt;
-        W.graph_cap = W.cap;
-        W.graph_bench = true;
-    }
+    ensure_graphs(f, W, s, dt, conv);
     double* bk = W.backup.as<double>();
     ck(cudaMemcpyAsync(bk, s.x, sizeof(double) * 6 * N, cudaMemcpyDeviceToDevice, f->stream), "backup");
     cudaEvent_t ea, eb;

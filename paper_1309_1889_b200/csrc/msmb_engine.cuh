@@ -81,10 +81,7 @@ struct Workspace {
     double graph_dt = 0;
     int graph_cap = 0;
     int launches_eval = 0, launches_step = 0;
-    bool graph_bench = false;            // graphs carry per-stage event nodes
-    bool capture_events = false;         // enqueue_eval records stage events
     std::vector<std::string> stage_names;
-    std::vector<cudaEvent_t> stage_ev;   // 2 per stage (begin, end)
     DBuf flush;                          // > L2, written between timed steps
     uint64_t uid = 0;                    // identifies whose stencil is in constant memory
     ~Workspace();
@@ -115,6 +112,8 @@ struct msmb_field {
     msmb_units units{};
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;             // long-range chain, forked from `stream` (higher priority)
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     std::recursive_mutex mu;
     std::unique_ptr<msmb::Workspace> ws;
     msmb::Error last;

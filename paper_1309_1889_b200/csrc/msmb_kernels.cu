@@ -478,6 +478,9 @@ constexpr int kSlots = 33;
 #ifndef MSMB_PAIR_MINB
 #define MSMB_PAIR_MINB 5
 #endif
+#ifndef MSMB_PAIR_UNROLL
+#define MSMB_PAIR_UNROLL 1
+#endif
 
 __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     k_pairs(const int* __restrict__ nclu, const int2* __restrict__ clu,
@@ -508,6 +511,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     // r2 ~ 1e8 keeps g, g' finite -- and q = 0: idle lanes add exact zeros
     if (lane < 8) s_w[w][lane][0] = (lane == 1 || lane == 3 || lane == 5) ? 0x40C38800u : 0u;
     double ph = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
+#if MSMB_PAIR_UNROLL == 2
+    double ph2 = 0.0, fx2 = 0.0, fy2 = 0.0, fz2 = 0.0;
+#endif
     unsigned ncand = 0;
     const int nj = pcnt[ic];
     const int* pl = plist + size_t(ic) * cap;
@@ -577,9 +583,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         ncand += pc;
         const int iters = __reduce_max_sync(FULLMASK, pc);
         const unsigned* row = &s_w[w][0][0];
-        for (int k = 0; k < iters; ++k) {
-            const int sl = __ffs(mask); // atom 32 - sl, or the dummy (0) once the lane is done
-            mask &= mask - 1;
+        auto pair = [&](int sl, double& ph_, double& fx_, double& fy_, double& fz_) {
             const double xj = __hiloint2double(row[1 * kSlots + sl], row[0 * kSlots + sl]);
             const double yj = __hiloint2double(row[3 * kSlots + sl], row[2 * kSlots + sl]);
             const double zj = __hiloint2double(row[5 * kSlots + sl], row[4 * kSlots + sl]);
@@ -590,13 +594,36 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
             const double rinv2 = rinv * rinv;
             const double g = rinv - fma(r2, fma(r2, c2, c1), c0);   // g*(r)
             const double sd = fma(-rinv, rinv2, fma(r2, d1, d0));  // g*'(r)/r
-            ph = fma(qj, g, ph);
+            ph_ = fma(qj, g, ph_);
             const double wgt = qj * sd;
-            fx = fma(dx, wgt, fx);
-            fy = fma(dy, wgt, fy);
-            fz = fma(dz, wgt, fz);
+            fx_ = fma(dx, wgt, fx_);
+            fy_ = fma(dy, wgt, fy_);
+            fz_ = fma(dz, wgt, fz_);
+        };
+#if MSMB_PAIR_UNROLL == 2
+        // two independent chains per iteration; the odd tail reads the dummy slot (ffs(0) = 0)
+        for (int k = 0; k < iters; k += 2) {
+            const int s0 = __ffs(mask);
+            mask &= mask - 1;
+            const int s1 = __ffs(mask);
+            mask &= mask - 1;
+            pair(s0, ph, fx, fy, fz);
+            pair(s1, ph2, fx2, fy2, fz2);
         }
+#else
+        for (int k = 0; k < iters; ++k) {
+            const int sl = __ffs(mask); // atom 32 - sl, or the dummy (0) once the lane is done
+            mask &= mask - 1;
+            pair(sl, ph, fx, fy, fz);
+        }
+#endif
     }
+#if MSMB_PAIR_UNROLL == 2
+    ph += ph2;
+    fx += fx2;
+    fy += fy2;
+    fz += fz2;
+#endif
     if (vi) {
         const double kq = -p.kc * qi; // f = d * (-k_C q_i q_j g*'/r)  (msm_phases.cpp:246)
         phis[si] = ph;
