@@ -6,9 +6,9 @@
 //   K2  short-range pairs            src/msm_phases.cpp:224-252, msm_kernels.hpp:30-42
 //                                    -> k_columns, k_clusters, k_bbox, k_pairlist, k_pairs, k_err_brute
 //   K3  anterpolation                src/msm_phases.cpp:39-61      -> k_anterp
-//   K4  restriction                  src/msm_phases.cpp:63-91      -> k_restrict
-//   K5  lattice cutoff               src/msm_phases.cpp:93-134     -> k_conv (lattice jobs)
-//   K6  top level                    src/msm_phases.cpp:136-162    -> k_conv (top job)
+//   K4  restriction                  src/msm_phases.cpp:63-91      -> k_restrict_tile
+//   K5  lattice cutoff               src/msm_phases.cpp:93-134     -> k_lattice, k_lattice_reduce
+//   K6  top level                    src/msm_phases.cpp:136-162    -> k_top_direct (k_conv above 8192 points)
 //   K7  prolongation                 src/msm_phases.cpp:164-193    -> k_prolong
 //   K8  interpolation + forces + E   src/msm_phases.cpp:195-222, src/msm.cpp:16-48,69-86
 //                                    -> k_interp, k_energy1/2
