@@ -127,6 +127,9 @@ int msmb_system_download(const msmb_system* s, double* pos_xyz, double* vel_xyz)
 int msmb_system_copy(msmb_system* dst, const msmb_system* src);
 /* In-place device-resident propagate (same semantics as msmb_propagate). */
 int msmb_system_propagate(msmb_field* f, msmb_system* s, double dt, int steps);
+/* ... with an explicit UnitsConfig (as msmb_propagate_ex; NULL = the field's). */
+int msmb_system_propagate_ex(msmb_field* f, msmb_system* s, double dt, int steps,
+                             const msmb_units* units);
 /* Device-resident evaluate; outputs copied to the (optional) host arrays. */
 int msmb_system_evaluate(msmb_field* f, msmb_system* s, double* phi, double* phi_short,
                          double* phi_long, double* force_xyz, double* energy);
@@ -167,6 +170,28 @@ int msmb_parareal_run(const msmb_parareal_config* cfg, int64_t n, const double* 
                       const double* vel_xyz, const double* q, const double* mass,
                       const double box[3], int total_points, double* traj_pos,
                       double* traj_vel, int64_t* report);
+
+/* ---- raw device states, for multi-process (one process per GPU) drivers -----
+ * A "state" is 6*n doubles in device memory of the field's GPU, SoA:
+ * x[n] y[n] z[n] vx[n] vy[n] vz[n] (the first six arrays of a msmb_system).
+ * A "delta" is the reference's StateDelta (include/paramd/parareal.hpp:53-59):
+ * dpos as n interleaved Vec3, then dvel, 6*n doubles.  Each call runs on the
+ * field's stream and returns after the stream is synchronised, so the buffers
+ * may be handed to a communication library (e.g. NCCL) right away.  The
+ * arithmetic and reduction order are those of msmb_parareal_run, so a
+ * multi-process parareal built on these calls reproduces it bit for bit. */
+/* state_sub(a, b)  src/parareal.cpp:58-73; *rms_pos = sqrt(sum |dpos|^2 / 3n). */
+int msmb_state_sub_device(msmb_field* f, int64_t n, const double* a, const double* b,
+                          double* delta, double* rms_pos);
+/* state_add(base, d)  src/parareal.cpp:75-82. */
+int msmb_state_add_device(msmb_field* f, int64_t n, const double* base, const double* delta,
+                          double* out);
+/* rms_pos_change(a, b)  src/parareal.cpp:86-90. */
+int msmb_state_rms_change_device(msmb_field* f, int64_t n, const double* a, const double* b,
+                                 double* rms);
+/* Copy a device state into / out of a msmb_system (device to device). */
+int msmb_system_set_state_device(msmb_system* s, const double* state);
+int msmb_system_get_state_device(const msmb_system* s, double* state);
 
 /* ---- measurement ------------------------------------------------------------ */
 /* When enabled, every evaluation records CUDA events around each stage on the

@@ -210,6 +210,7 @@ class MsmField(ForceField):
     def __init__(self, config: MsmConfig, units: UnitsConfig = None, device: int = 0):
         units = units or UnitsConfig.physical()
         self._config, self._units = config, units
+        self._device = device
         self._h = C.c_void_p()
         cfg, u = config._c(), units._c()
         rc = _native.lib().msmb_create(C.byref(cfg), C.byref(u), device, C.byref(self._h))

@@ -58,6 +58,12 @@ SIGNATURES = {
     "msmb_system_upload": (C.c_int, [_VP, _D, _D]),
     "msmb_system_download": (C.c_int, [_VP, _D, _D]),
     "msmb_system_copy": (C.c_int, [_VP, _VP]),
+    "msmb_system_propagate_ex": (C.c_int, [_VP, _VP, C.c_double, C.c_int, C.POINTER(UnitsC)]),
+    "msmb_state_sub_device": (C.c_int, [_VP, C.c_int64, _VP, _VP, _VP, _D]),
+    "msmb_state_add_device": (C.c_int, [_VP, C.c_int64, _VP, _VP, _VP]),
+    "msmb_state_rms_change_device": (C.c_int, [_VP, C.c_int64, _VP, _VP, _D]),
+    "msmb_system_set_state_device": (C.c_int, [_VP, _VP]),
+    "msmb_system_get_state_device": (C.c_int, [_VP, _VP]),
     "msmb_system_propagate": (C.c_int, [_VP, _VP, C.c_double, C.c_int]),
     "msmb_system_evaluate": (C.c_int, [_VP, _VP, _D, _D, _D, _D, _D]),
     "msmb_parareal_window": (C.c_int, [C.POINTER(PararealC), C.c_int64, _D, _D, _D, _D, _D, C.c_int,

@@ -855,6 +855,18 @@ int msmb_system_propagate(msmb_field* f, msmb_system* s, double dt, int steps) {
     GUARD_END(f)
 }
 
+int msmb_system_propagate_ex(msmb_field* f, msmb_system* s, double dt, int steps, const msmb_units* units) {
+    if (!units) return msmb_system_propagate(f, s, dt, steps);
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    GUARD_BEGIN
+    f->last = Error{};
+    Error e = validate_units(*units);
+    if (e.kind) return engine_set_error(f, e);
+    cudaSetDevice(f->device);
+    return engine_propagate(f, s->st, dt, steps, units->energy_to_native);
+    GUARD_END(f)
+}
+
 int msmb_system_evaluate(msmb_field* f, msmb_system* s, double* phi, double* phi_short,
                          double* phi_long, double* force_xyz, double* energy) {
     std::lock_guard<std::recursive_mutex> lk(f->mu);

@@ -10,7 +10,8 @@
 // The Executor of the reference (src/parareal.cpp:11-36) only changes where fine
 // slices run; results are independent of it (pure propagators).  On one GPU the
 // fine slices run back to back on the fine field's stream; the multi-GPU split of
-// the fine sweep is in paper_1309_1889_b200/parallel.py (one process per GPU).
+// the fine sweep is paper_1309_1889_b200/parallel.py (one process per GPU) over the
+// raw device-state entry points at the end of this file.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -367,4 +368,102 @@ extern "C" int msmb_parareal_run(const msmb_parareal_config* cfg, int64_t n, con
     } catch (const std::exception& ex) {
         return pr_fail(cfg, Error{MSMB_ERR_CUDA, -1, -1, -1, ex.what()});
     }
+}
+
+// ---- raw device states (multi-process drivers, paper_1309_1889_b200/parallel.py) ----
+namespace {
+
+DevState raw_state(const double* p, int64_t n) {
+    DevState s{};
+    s.n = n;
+    double* b = const_cast<double*>(p);
+    s.x = b;
+    s.y = b + n;
+    s.z = b + 2 * n;
+    s.vx = b + 3 * n;
+    s.vy = b + 4 * n;
+    s.vz = b + 5 * n;
+    s.q = s.m = nullptr;
+    return s;
+}
+
+// the block partials summed on the host in block order (host_sum above)
+double partial_sum(msmb_field* f, int nblk) {
+    std::vector<double> h(static_cast<size_t>(nblk), 0.0);
+    ckp(cudaMemcpyAsync(h.data(), f->reduce.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, f->stream),
+        "D2H");
+    ckp(cudaStreamSynchronize(f->stream), "sync");
+    double s = 0.0;
+    for (double v : h) s += v;
+    return s;
+}
+
+template <class Fn>
+int raw_call(msmb_field* f, int64_t n, Fn&& fn) {
+    if (!f) return MSMB_ERR_CONFIG;
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    try {
+        cudaSetDevice(f->device);
+        const int nblk = reduce_blocks(n);
+        if (f->reduce.bytes < sizeof(double) * size_t(nblk)) ckp(f->reduce.alloc(sizeof(double) * size_t(nblk)), "alloc");
+        fn(nblk);
+        ckp(cudaGetLastError(), "kernel launch");
+        ckp(cudaStreamSynchronize(f->stream), "sync");
+        f->last = Error{};
+        return MSMB_OK;
+    } catch (const std::exception& ex) {
+        f->last = Error{MSMB_ERR_CUDA, -1, -1, -1, ex.what()};
+        return MSMB_ERR_CUDA;
+    }
+}
+
+} // namespace
+
+extern "C" int msmb_state_sub_device(msmb_field* f, int64_t n, const double* a, const double* b,
+                                     double* delta, double* rms_pos) {
+    return raw_call(f, n, [&](int nblk) {
+        if (n > 0) {
+            f->launches += launch_state_sub(f->stream, n, raw_state(a, n), raw_state(b, n), delta, delta + 3 * n,
+                                            f->reduce.as<double>(), nblk);
+        }
+        const double s = n > 0 ? partial_sum(f, nblk) : 0.0;
+        if (rms_pos) *rms_pos = std::sqrt(s / (3.0 * double(n)));
+    });
+}
+
+extern "C" int msmb_state_add_device(msmb_field* f, int64_t n, const double* base, const double* delta,
+                                     double* out) {
+    return raw_call(f, n, [&](int) {
+        if (n == 0) return;
+        DevState o = raw_state(out, n);
+        f->launches += launch_state_add(f->stream, n, raw_state(base, n), delta, delta + 3 * n, o);
+    });
+}
+
+extern "C" int msmb_state_rms_change_device(msmb_field* f, int64_t n, const double* a, const double* b,
+                                            double* rms) {
+    return raw_call(f, n, [&](int nblk) {
+        if (n > 0) f->launches += launch_rms_change(f->stream, n, raw_state(a, n), raw_state(b, n),
+                                                    f->reduce.as<double>(), nblk);
+        const double s = n > 0 ? partial_sum(f, nblk) : 0.0;
+        if (rms) *rms = std::sqrt(s / (3.0 * double(n)));
+    });
+}
+
+extern "C" int msmb_system_set_state_device(msmb_system* s, const double* state) {
+    if (!s) return MSMB_ERR_CONFIG;
+    return raw_call(s->f, s->st.n, [&](int) {
+        if (s->st.n > 0)
+            ckp(cudaMemcpyAsync(s->st.buf.p, state, sizeof(double) * 6 * size_t(s->st.n), cudaMemcpyDeviceToDevice,
+                                s->f->stream), "D2D");
+    });
+}
+
+extern "C" int msmb_system_get_state_device(const msmb_system* s, double* state) {
+    if (!s) return MSMB_ERR_CONFIG;
+    return raw_call(s->f, s->st.n, [&](int) {
+        if (s->st.n > 0)
+            ckp(cudaMemcpyAsync(state, s->st.buf.p, sizeof(double) * 6 * size_t(s->st.n), cudaMemcpyDeviceToDevice,
+                                s->f->stream), "D2D");
+    });
 }
