@@ -256,6 +256,9 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
     ck(W->staging.alloc(sizeof(double) * 3 * N), "cudaMalloc staging");
     ck(cudaMalloc(&W->err, sizeof(ErrRec)), "cudaMalloc err");
     ck(cudaMallocHost(&W->err_host, sizeof(ErrRec)), "cudaMallocHost err");
+    // wupload's pageable cudaMemcpy may return before its DMA lands, and the
+    // field's streams are non-blocking (not ordered after the legacy stream)
+    ck(cudaDeviceSynchronize(), "sync uploads");
     return W;
 }
 
@@ -1043,6 +1046,7 @@ int msmb_debug_levels(msmb_field* f, double* level_charge, double* level_potenti
     if (!f->ws) return MSMB_ERR_INTERNAL;
     cudaSetDevice(f->device);
     const size_t bytes = sizeof(double) * f->ws->g.lattice_total;
+    ck(cudaStreamSynchronize(f->stream), "sync");
     if (level_charge) ck(cudaMemcpy(level_charge, f->ws->L.charge, bytes, cudaMemcpyDeviceToHost), "D2H");
     if (level_potential) ck(cudaMemcpy(level_potential, f->ws->L.pot, bytes, cudaMemcpyDeviceToHost), "D2H");
     return MSMB_OK;
@@ -1082,8 +1086,9 @@ int msmb_debug_stage(msmb_field* f, int stage, int k, const double box[3], const
     const Geometry& g = W.g;
     ensure_const_table(f, W);
     f->launches += launch_reset_err(f->stream, W.err, 0);
-    auto up = [&](double* d, const double* h, size_t cnt) {
-        ck(cudaMemcpy(d, h, sizeof(double) * cnt, cudaMemcpyHostToDevice), "H2D");
+    auto up = [&](double* d, const double* h, size_t cnt) { // stream-ordered before the stage kernel
+        ck(cudaMemcpyAsync(d, h, sizeof(double) * cnt, cudaMemcpyHostToDevice, f->stream), "H2D");
+        ck(cudaStreamSynchronize(f->stream), "sync");
     };
     auto down = [&](double* h, const double* d, size_t cnt) {
         ck(cudaStreamSynchronize(f->stream), "sync");

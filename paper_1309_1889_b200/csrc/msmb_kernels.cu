@@ -381,11 +381,23 @@ __device__ __forceinline__ float gapf(float alo, float ahi, float blo, float bhi
     return fmaxf(0.f, fmaxf(blo - ahi, alo - bhi));
 }
 
-__global__ void k_pairlist(const int* __restrict__ nclu, const float4* __restrict__ blo,
-                           const float4* __restrict__ bhi, const int* __restrict__ col_off, ListP p,
-                           int* plist, int* pcnt, int cap, ErrRec* err) {
+// Pair list of one i-cluster (one warp): every j-cluster whose fp32 bounding box
+// is within the screening cut.  The order is chosen for k_pairs' lane balance:
+// columns are visited in mirror groups (|dx|, |dy|) around the i-cluster's
+// column, and the (up to 4) columns of a group are interleaved cluster by
+// cluster, every other column in reverse z order.  A j-cluster above-left of the
+// i-cluster (busy for its upper-left lanes) is thereby followed by one
+// below-right (busy for the other lanes), so k_pairs' two-cluster ring keeps
+// most lanes busy.  Order only affects speed: the list is complete either way.
+constexpr int kListSeg = 128; // group segments longer than this keep column order
+
+__global__ void __launch_bounds__(256)
+    k_pairlist(const int* __restrict__ nclu, const float4* __restrict__ blo,
+               const float4* __restrict__ bhi, const int* __restrict__ col_off, ListP p, int* plist,
+               int* pcnt, int cap, ErrRec* err) {
+    __shared__ int s_seg[8][kListSeg];
     const int ic = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     if (ic >= *nclu || failed(err)) return;
     const float4 lo = blo[ic], hi = bhi[ic];
     const double cutd = double(p.cut);
@@ -397,35 +409,68 @@ __global__ void k_pairlist(const int* __restrict__ nclu, const float4* __restric
     cy0 = max(cy0, 0);
     cx1 = min(cx1, p.ncx - 1);
     cy1 = min(cy1, p.ncy - 1);
+    const int cxi = min(max(int(floor((0.5 * (double(lo.x) + double(hi.x)) - p.ox) / p.colw)), 0), p.ncx - 1);
+    const int cyi = min(max(int(floor((0.5 * (double(lo.y) + double(hi.y)) - p.oy) / p.colw)), 0), p.ncy - 1);
+    const int DX = max(cxi - cx0, cx1 - cxi), DY = max(cyi - cy0, cy1 - cyi);
     int count = 0;
     int* out = plist + size_t(ic) * cap;
-    for (int cx = cx0; cx <= cx1; ++cx) {
-        const float xlo = float(p.ox + cx * p.colw) - 1e-3f, xhi = float(p.ox + (cx + 1) * p.colw) + 1e-3f;
-        const float gx = gapf(lo.x, hi.x, xlo, xhi);
-        if (gx >= p.cut) continue;
-        for (int cy = cy0; cy <= cy1; ++cy) {
-            const float ylo = float(p.oy + cy * p.colw) - 1e-3f, yhi = float(p.oy + (cy + 1) * p.colw) + 1e-3f;
-            const float gy = gapf(lo.y, hi.y, ylo, yhi);
-            if (gx * gx + gy * gy >= p.cut2) continue;
-            const int col = cx * p.ncy + cy;
-            const int j0 = col_off[col], j1 = col_off[col + 1];
-            for (int jb = j0; jb < j1; jb += 32) {
-                const int jc = jb + lane;
-                bool ok = false;
-                if (jc < j1) {
-                    const float4 l2 = blo[jc], h2 = bhi[jc];
-                    const float dx = gapf(lo.x, hi.x, l2.x, h2.x);
-                    const float dy = gapf(lo.y, hi.y, l2.y, h2.y);
-                    const float dz = gapf(lo.z, hi.z, l2.z, h2.z);
-                    ok = dx * dx + dy * dy + dz * dz < p.cut2;
+    for (int dx = 0; dx <= DX; ++dx)
+        for (int dy = 0; dy <= DY; ++dy) {
+            const int gstart = count;
+            int nseg[4] = {0, 0, 0, 0};
+            int ncol = 0;
+            // (-dx,-dy), (+dx,+dy), (-dx,+dy), (+dx,-dy); duplicates dropped when dx or dy is 0
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int sx = (v == 0 || v == 2) ? -1 : 1, sy = (v == 0 || v == 3) ? -1 : 1;
+                if ((dx == 0 && sx > 0) || (dy == 0 && sy > 0)) continue;
+                const int cx = cxi + sx * dx, cy = cyi + sy * dy;
+                int emitted = 0;
+                if (cx >= cx0 && cx <= cx1 && cy >= cy0 && cy <= cy1) {
+                    const float xlo = float(p.ox + cx * p.colw) - 1e-3f, xhi = float(p.ox + (cx + 1) * p.colw) + 1e-3f;
+                    const float ylo = float(p.oy + cy * p.colw) - 1e-3f, yhi = float(p.oy + (cy + 1) * p.colw) + 1e-3f;
+                    const float gx = gapf(lo.x, hi.x, xlo, xhi), gy = gapf(lo.y, hi.y, ylo, yhi);
+                    if (gx * gx + gy * gy < p.cut2) {
+                        const int col = cx * p.ncy + cy;
+                        const int j0 = col_off[col], j1 = col_off[col + 1];
+                        for (int jb = j0; jb < j1; jb += 32) {
+                            const int jc = jb + lane;
+                            bool ok = false;
+                            if (jc < j1) {
+                                const float4 l2 = blo[jc], h2 = bhi[jc];
+                                const float ex = gapf(lo.x, hi.x, l2.x, h2.x);
+                                const float ey = gapf(lo.y, hi.y, l2.y, h2.y);
+                                const float ez = gapf(lo.z, hi.z, l2.z, h2.z);
+                                ok = ex * ex + ey * ey + ez * ez < p.cut2;
+                            }
+                            const unsigned b = __ballot_sync(FULLMASK, ok);
+                            const int pos = count + __popc(b & ((1u << lane) - 1u));
+                            if (ok && pos < cap) out[pos] = jc;
+                            count += __popc(b);
+                            emitted += __popc(b);
+                        }
+                    }
                 }
-                const unsigned b = __ballot_sync(FULLMASK, ok);
-                const int pos = count + __popc(b & ((1u << lane) - 1u));
-                if (ok && pos < cap) out[pos] = jc;
-                count += __popc(b);
+                nseg[ncol++] = emitted;
+            }
+            // interleave the group's columns: rank r of column c (odd c reversed) goes to
+            // sum_c' min(n_c', r) + #{c' < c : n_c' > r}
+            const int total = count - gstart;
+            if (ncol > 1 && total > 1 && total <= kListSeg && count <= cap) {
+                __syncwarp();
+                for (int e = lane; e < total; e += 32) s_seg[wl][e] = out[gstart + e];
+                __syncwarp();
+                for (int e = lane; e < total; e += 32) {
+                    int c = 0, i = e;
+                    while (i >= nseg[c]) i -= nseg[c++];
+                    const int r = (c & 1) ? nseg[c] - 1 - i : i;
+                    int dest = 0;
+                    for (int c2 = 0; c2 < ncol; ++c2) dest += min(nseg[c2], r) + ((c2 < c && nseg[c2] > r) ? 1 : 0);
+                    out[gstart + dest] = s_seg[wl][e];
+                }
+                __syncwarp();
             }
         }
-    }
     if (lane == 0) {
         pcnt[ic] = min(count, cap);
         if (count > cap) atomicMax(&err->overflow, count);
@@ -458,28 +503,30 @@ __device__ __forceinline__ void record_pair(ErrRec* err, int i, int j) {
     atomicMin(&err->pair_key, (lo << 32) | hi);
 }
 
-// One warp per i-cluster (lane = i atom).  For every candidate j-cluster the warp
-// stages its 32 atoms in shared memory -- fp32 screening records
-// (-2x', -2y', -2z', |x'|^2 - cut^2), x' relative to the i-cluster, as SoA rows,
-// and the fp64 x, y, z, q split
-// into 32-bit rows in which atom t sits at slot 32 - t and slot 0 is a dummy atom
-// (q = 0, far away), so any lane->slot mapping reads conflict-free -- then builds
-// each lane's 32-bit in-range mask with 4 packed fp32x2 operations per two
-// candidates (bit 31 - t <=> atom t), and walks the set bits with ffs; lanes that
-// run out of bits read the dummy slot, so the loop body has no selects or
-// branches.  The fp32 screen admits pairs up to a(1 + ~1e-5) (its rigorous error
-// bound); the reference skips r >= a (src/msm_phases.cpp:240).  Those margin
-// pairs are evaluated with the r < a polynomial, and because g* is C^2 at r = a
-// they add O(((r-a)/a)^3) ~ 1e-15 * q_j to phi and O(((r-a)/a)^2) to g*'/r --
-// orders below the 1e-10 energy / 1e-8 force tolerances (tests/test_gpu_parity.py).  The next j-cluster is
-// prefetched into registers while the current one is processed.  Coincident
-// pairs are caught in k_cellsort.
-constexpr int kSlots = 33;
+// One warp per i-cluster (lane = i atom).  The warp walks the i-cluster's j-cluster
+// list (k_pairlist order) through a two-cluster ring in shared memory.  Staging a
+// j-cluster writes its fp32 screening records (-2x', -2y', -2z', |x'|^2 - cut^2;
+// x' relative to the i-cluster) and its fp64 x, y, z, q split into 32-bit rows;
+// ring slot p holds atom t at position 33p + 32 - t and a dummy atom (q = 0, far
+// away) at 33p, so any lane -> position mapping reads a valid record.  Each lane
+// builds a 32-bit in-range mask per staged cluster with packed fp32x2 operations
+// (bit 31 - t <=> atom t).  A pair step takes the lowest set bit of the lane's
+// OLDER cluster mask, or of the newer one once the older is exhausted, or the
+// dummy once both are: no branches, no selects in the fp64 math.  Before a new
+// cluster is staged the older slot is drained -- max over lanes of its popcount
+// steps, during which lanes with nothing left in it already work on the newer
+// cluster -- so lanes stay busy across clusters (k_pairlist puts complementary
+// clusters next to each other).  The fp32 screen admits pairs up to a(1 + ~1e-5)
+// (its rigorous error bound); the reference skips r >= a (src/msm_phases.cpp:240).
+// Those margin pairs are evaluated with the r < a polynomial, and because g* is
+// C^2 at r = a they add O(((r-a)/a)^3) ~ 1e-15 * q_j to phi and O(((r-a)/a)^2) to
+// g*'/r -- orders below the 1e-10 energy / 1e-8 force tolerances
+// (tests/test_gpu_parity.py).  The next j-cluster is prefetched into registers
+// while the current one is processed.  Coincident pairs are caught in k_cellsort.
+constexpr int kSlots = 33;            // one ring slot: dummy + 32 atoms
+constexpr int kRow = 2 * kSlots;      // two ring slots per 32-bit row
 #ifndef MSMB_PAIR_MINB
 #define MSMB_PAIR_MINB 5
-#endif
-#ifndef MSMB_PAIR_UNROLL
-#define MSMB_PAIR_UNROLL 1
 #endif
 
 __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
@@ -490,7 +537,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
             const float4* __restrict__ f4, PairP p, double* phis, double* fsx, double* fsy,
             double* fsz, ErrRec* err) {
     __shared__ __align__(16) float s_sc[kPairWarps][4][32];
-    __shared__ unsigned s_w[kPairWarps][8][kSlots];
+    __shared__ unsigned s_w[kPairWarps][8][kRow];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ic = blockIdx.x * kPairWarps + w;
     if (ic >= *nclu || failed(err)) return;
@@ -507,13 +554,10 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     const float nif = fmaf(zf, zf, fmaf(yf, yf, xf * xf));
     const float2 ni2 = make_float2(nif, nif);
     const float ri2 = __uint_as_float(__reduce_max_sync(FULLMASK, __float_as_uint(vi ? nif : 0.f)));
-    // dummy slot 0: position (1e4, 1e4, 1e4) A -- far from every covered particle, so
-    // r2 ~ 1e8 keeps g, g' finite -- and q = 0: idle lanes add exact zeros
-    if (lane < 8) s_w[w][lane][0] = (lane == 1 || lane == 3 || lane == 5) ? 0x40C38800u : 0u;
+    // dummies at positions 0 and 33: (1e4, 1e4, 1e4) A -- far from every covered
+    // particle, so r2 ~ 1e8 keeps g, g' finite -- with q = 0: idle steps add exact zeros
+    if (lane < 16) s_w[w][lane & 7][(lane >> 3) * kSlots] = ((lane & 7) == 1 || (lane & 7) == 3 || (lane & 7) == 5) ? 0x40C38800u : 0u;
     double ph = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
-#if MSMB_PAIR_UNROLL == 2
-    double ph2 = 0.0, fx2 = 0.0, fy2 = 0.0, fz2 = 0.0;
-#endif
     unsigned ncand = 0;
     const int nj = pcnt[ic];
     const int* pl = plist + size_t(ic) * cap;
@@ -529,12 +573,43 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         zj_n = zs[sj];
         qj_n = qs[sj];
     };
+    const unsigned* row = &s_w[w][0][0];
+    unsigned mA = 0, mB = 0; // lane masks of the older / newer staged cluster
+    int pA = 1;              // ring slot of the older cluster (warp-uniform)
+    auto step = [&]() {
+        const bool useA = mA != 0;
+        const int sl = (useA ? pA : pA ^ 1) * kSlots + __ffs(useA ? mA : mB);
+        mA = useA ? (mA & (mA - 1)) : mA;
+        mB = useA ? mB : (mB & (mB - 1));
+        const double xj = __hiloint2double(row[1 * kRow + sl], row[0 * kRow + sl]);
+        const double yj = __hiloint2double(row[3 * kRow + sl], row[2 * kRow + sl]);
+        const double zj = __hiloint2double(row[5 * kRow + sl], row[4 * kRow + sl]);
+        const double qj = __hiloint2double(row[7 * kRow + sl], row[6 * kRow + sl]);
+        const double dx = xi - xj, dy = yi - yj, dz = zi - zj;
+        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        const double rinv = rsqrt_pos(r2);
+        const double rinv2 = rinv * rinv;
+        const double g = rinv - fma(r2, fma(r2, c2, c1), c0);   // g*(r)
+        const double sd = fma(-rinv, rinv2, fma(r2, d1, d0));  // g*'(r)/r
+        ph = fma(qj, g, ph);
+        const double wgt = qj * sd;
+        fx = fma(dx, wgt, fx);
+        fy = fma(dy, wgt, fy);
+        fz = fma(dz, wgt, fz);
+    };
     if (nj > 0) fetch(0);
     for (int jj = 0; jj < nj; ++jj) {
+        // drain the older cluster; lanes done with it already consume the newer one
+        const int dA = __reduce_max_sync(FULLMASK, __popc(mA));
+        for (int k = 0; k < dA; ++k) step();
+        mA = mB;
+        mB = 0;
+        pA ^= 1;
+        const int pB = pA ^ 1; // the freed slot receives cluster jj
         const int jc = jc_n;
         const bool vj = lane < cj_n.y;
-        // screening record (-2x', -2y', -2z', |x'|^2 - cut^2) of this lane's j atom.  The
-        // fp32 evaluation of r^2 - cut^2 = |xi'|^2 + |xj'|^2 - 2 xi'.xj' - cut^2 errs by
+        // screening record of this lane's j atom.  The fp32 evaluation of
+        // r^2 - cut^2 = |xi'|^2 + |xj'|^2 - 2 xi'.xj' - cut^2 errs by
         // < 16 * 2^-24 * (|xi'| + |xj'|)^2; cut^2 is padded by twice that (uniform per j-cluster).
         const float xj = float(xj_n - rx), yj = float(yj_n - ry), zj = float(zj_n - rz);
         const float njf = fmaf(zj, zj, fmaf(yj, yj, xj * xj));
@@ -545,7 +620,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         s_sc[w][1][lane] = -2.f * yj;
         s_sc[w][2][lane] = -2.f * zj;
         s_sc[w][3][lane] = vj ? njf - cut2 : 3e38f;
-        const int slot = 32 - lane;
+        const int slot = pB * kSlots + 32 - lane;
         s_w[w][0][slot] = __double2loint(xj_n);
         s_w[w][1][slot] = __double2hiint(xj_n);
         s_w[w][2][slot] = __double2loint(yj_n);
@@ -579,51 +654,11 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         }
         if (!vi) mask = 0;
         if (jc == ic) mask &= ~(0x80000000u >> lane);
-        const int pc = __popc(mask);
-        ncand += pc;
-        const int iters = __reduce_max_sync(FULLMASK, pc);
-        const unsigned* row = &s_w[w][0][0];
-        auto pair = [&](int sl, double& ph_, double& fx_, double& fy_, double& fz_) {
-            const double xj = __hiloint2double(row[1 * kSlots + sl], row[0 * kSlots + sl]);
-            const double yj = __hiloint2double(row[3 * kSlots + sl], row[2 * kSlots + sl]);
-            const double zj = __hiloint2double(row[5 * kSlots + sl], row[4 * kSlots + sl]);
-            const double qj = __hiloint2double(row[7 * kSlots + sl], row[6 * kSlots + sl]);
-            const double dx = xi - xj, dy = yi - yj, dz = zi - zj;
-            const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-            const double rinv = rsqrt_pos(r2);
-            const double rinv2 = rinv * rinv;
-            const double g = rinv - fma(r2, fma(r2, c2, c1), c0);   // g*(r)
-            const double sd = fma(-rinv, rinv2, fma(r2, d1, d0));  // g*'(r)/r
-            ph_ = fma(qj, g, ph_);
-            const double wgt = qj * sd;
-            fx_ = fma(dx, wgt, fx_);
-            fy_ = fma(dy, wgt, fy_);
-            fz_ = fma(dz, wgt, fz_);
-        };
-#if MSMB_PAIR_UNROLL == 2
-        // two independent chains per iteration; the odd tail reads the dummy slot (ffs(0) = 0)
-        for (int k = 0; k < iters; k += 2) {
-            const int s0 = __ffs(mask);
-            mask &= mask - 1;
-            const int s1 = __ffs(mask);
-            mask &= mask - 1;
-            pair(s0, ph, fx, fy, fz);
-            pair(s1, ph2, fx2, fy2, fz2);
-        }
-#else
-        for (int k = 0; k < iters; ++k) {
-            const int sl = __ffs(mask); // atom 32 - sl, or the dummy (0) once the lane is done
-            mask &= mask - 1;
-            pair(sl, ph, fx, fy, fz);
-        }
-#endif
+        ncand += __popc(mask);
+        mB = mask;
     }
-#if MSMB_PAIR_UNROLL == 2
-    ph += ph2;
-    fx += fx2;
-    fy += fy2;
-    fz += fz2;
-#endif
+    const int dAll = __reduce_max_sync(FULLMASK, __popc(mA) + __popc(mB));
+    for (int k = 0; k < dAll; ++k) step();
     if (vi) {
         const double kq = -p.kc * qi; // f = d * (-k_C q_i q_j g*'/r)  (msm_phases.cpp:246)
         phis[si] = ph;

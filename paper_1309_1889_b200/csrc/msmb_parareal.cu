@@ -235,7 +235,9 @@ static int setup(PR& P, const msmb_parareal_config* cfg, int64_t n, const double
         soa[size_t(6) * n + i] = q[i];
         soa[size_t(7) * n + i] = mass[i];
     }
-    ckp(cudaMemcpy(P.proto.buf.p, soa.data(), sizeof(double) * soa.size(), cudaMemcpyHostToDevice), "H2D");
+    ckp(cudaMemcpyAsync(P.proto.buf.p, soa.data(), sizeof(double) * soa.size(), cudaMemcpyHostToDevice, P.st),
+        "H2D");
+    ckp(cudaStreamSynchronize(P.st), "sync"); // before other fields' streams read proto
     return MSMB_OK;
 }
 

@@ -47,7 +47,10 @@ def test_prolongation_bitwise(port, name, n):
         fine_in = port.lattice_cutoff(w.box, w.a, w.h, w.levels, k, o["level_charge"][sl[k]])
         coarse = o["level_potential"][sl[k + 1]]
         got = f.debug_stage(3, k, w.box, coarse, out=fine_in)
-        assert np.array_equal(got, port.prolongate(w.box, w.a, w.h, w.levels, k, coarse, fine_in))
+        exp = port.prolongate(w.box, w.a, w.h, w.levels, k, coarse, fine_in)
+        bad = np.flatnonzero(got != exp)
+        assert bad.size == 0, (f"level {k}: {bad.size}/{got.size} differ, first {bad[:5]}, "
+                               f"unchanged={np.array_equal(got, fine_in)}, maxdiff={np.max(np.abs(got - exp))}")
         assert np.array_equal(got, o["level_potential"][sl[k]])
 
 
