@@ -193,6 +193,35 @@ int msmb_state_rms_change_device(msmb_field* f, int64_t n, const double* a, cons
 int msmb_system_set_state_device(msmb_system* s, const double* state);
 int msmb_system_get_state_device(const msmb_system* s, double* state);
 
+/* ---- spatial decomposition: one part per GPU -------------
+ * Every part holds the whole particle state (a msmb_system).  A part owns an
+ * x-range of pair columns (pair sum, interpolation, forces and Verlet update of
+ * the atoms binned there) and an x-range of output planes on every grid level
+ * (anterpolation, lattice cutoff).  A step is four phases, with an exchange of the
+ * phase's buffer between consecutive phases:
+ *   phase 0  binning, owned pair sum + anterpolation   -> xbuf: level-0 charges
+ *   phase 1  restriction, owned lattice cutoff         -> xbuf: level potentials
+ *   phase 2  top level, prolongation, owned interpolation, forces, energy share
+ *            (*energy), owned Verlet update (`kicks` half-kicks, then a drift
+ *            if `drift`)                               -> xbuf: particle state
+ *   phase 3  import the exchanged state.
+ * xbuf is device memory of the field's GPU holding doubles as int64 bit patterns;
+ * entries a part does not own are INT64_MIN, so an element-wise int64 MAX
+ * all-reduce of the buffers (e.g. NCCL) gives every part the owners' exact
+ * values.  Sizes (msmb_dd_sizes) are [level-0 points, all level points, 6 n]
+ * int64 for the three exchanges.  The decomposed trajectory is bit-identical to
+ * msmb_system_propagate's.  Binning errors are detected identically on every
+ * part (phase 0 returns the reference's error everywhere).  The driver is
+ * paper_1309_1889_b200/parallel.py. */
+/* Work plan of `part` (no GPU needed): out = [ncx, cx0, cx1, levels,
+ * (d0_k, plane0_k, plane1_k) per level]; cap >= 4 + 3 * levels. */
+int msmb_dd_plan(const msmb_msm_config* cfg, const msmb_units* units, const double box[3], int64_t n,
+                 int nparts, int part, int* out, int cap);
+int msmb_dd_set_part(msmb_field* f, int nparts, int part);
+int msmb_dd_sizes(msmb_field* f, msmb_system* s, int64_t* out3);
+int msmb_dd_phase(msmb_field* f, msmb_system* s, int phase, double dt, int kicks, int drift,
+                  const msmb_units* units, const void* xin, void* xout, double* energy);
+
 /* ---- measurement ------------------------------------------------------------ */
 /* When enabled, every evaluation records CUDA events around each stage on the
  * handle's stream (eager launches, no graph) and accumulates durations. */

@@ -98,7 +98,7 @@ int cuda_fail(msmb_field* f, cudaError_t e, const char* where) {
     return MSMB_ERR_CUDA;
 }
 
-static Error error_from_rec(const ErrRec& r) {
+Error error_from_rec(const ErrRec& r) {
     Error e;
     e.kind = r.kind;
     e.step = r.step;
@@ -153,7 +153,7 @@ static uint64_t g_const_owner[64] = {0}; // per device: uid of the workspace who
 
 // k_lattice<true> reads the level-0 stencil from constant memory, which is shared by
 // every field of the process on a device: make sure it holds this workspace's table.
-static void ensure_const_table(msmb_field* f, Workspace& W) {
+void ensure_const_table(msmb_field* f, Workspace& W) {
     if (!W.L.lat_const) return;
     std::lock_guard<std::mutex> lk(g_const_mu);
     const int d = f->device & 63;
@@ -170,6 +170,8 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
     if (e.kind) return nullptr;
     Geometry& g = W->g;
     W->n = n;
+    W->whole = make_part(g, 1, 0);
+    W->part = make_part(g, f->dd_nparts, f->dd_part);
     const size_t N = size_t(n > 0 ? n : 1);
     DevAtoms& a = W->a;
     a.key = walloc<int>(*W, N);
@@ -262,7 +264,7 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
     return W;
 }
 
-static Error ensure_workspace(msmb_field* f, int64_t n, const double* box) {
+Error ensure_workspace(msmb_field* f, int64_t n, const double* box) {
     Error e;
     if (f->ws && f->ws->n == n && f->ws->g.box[0] == box[0] && f->ws->g.box[1] == box[1] &&
         f->ws->g.box[2] == box[2])
@@ -328,23 +330,23 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs) 
         ck(cudaEventRecord(f->fork_ev, st), "fork");
         ck(cudaStreamWaitEvent(lr, f->fork_ev, 0), "fork");
     }
-    run("anterp", [&] { return launch_anterp(lr, g, W.a, W.c, W.L, W.err); });
+    run("anterp", [&] { return launch_anterp(lr, g, W.a, W.c, W.L, W.err, W.whole); });
     run("restrict", [&] { return launch_restrict_all(lr, g, W.L, W.err); });
-    run("lattice", [&] { return launch_lattice(lr, g, W.L, W.err); });
+    run("lattice", [&] { return launch_lattice(lr, g, W.L, W.err, W.whole); });
     run("top", [&] { return launch_top(lr, g, W.L, W.err); });
     run("prolong", [&] { return launch_prolong_all(lr, g, W.L, W.err); });
     if (fork) ck(cudaEventRecord(f->join_ev, lr), "join");
-    run("clusters", [&] { return launch_clusters(st, g, s.n, W.a, W.c, W.err, W.cap); });
-    run("pairs", [&] { return launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap); });
+    run("clusters", [&] { return launch_clusters(st, g, s.n, W.a, W.c, W.err, W.cap, W.whole); });
+    run("pairs", [&] { return launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole); });
     if (fork) ck(cudaStreamWaitEvent(st, f->join_ev, 0), "join");
     DevOut o = W.o;
     if (!outputs) o.phi = o.phis = o.phil = o.e = nullptr;
-    run("interp", [&] { return launch_interp(st, g, s.n, W.a, W.c, W.L, o, W.err, outputs ? 1 : 0); });
+    run("interp", [&] { return launch_interp(st, g, s.n, W.a, W.c, W.L, o, W.err, outputs ? 1 : 0, W.whole); });
     run("finalize", [&] { return launch_finalize(st, s, W.err); });
     return total;
 }
 
-static ErrRec read_err(msmb_field* f, Workspace& W) {
+ErrRec read_err(msmb_field* f, Workspace& W) {
     ck(cudaMemcpyAsync(W.err_host, W.err, sizeof(ErrRec), cudaMemcpyDeviceToHost, f->stream),
        "read err");
     ck(cudaStreamSynchronize(f->stream), "cudaStreamSynchronize");
@@ -352,7 +354,7 @@ static ErrRec read_err(msmb_field* f, Workspace& W) {
     return *W.err_host;
 }
 
-static void record_counters(msmb_field* f, const Workspace& W, const ErrRec& r) {
+void record_counters(msmb_field* f, const Workspace& W, const ErrRec& r) {
     f->counters[0] = int64_t(r.pairs / 2);
     f->counters[1] = int64_t(r.candidates);
     int nclu = 0;
@@ -363,7 +365,7 @@ static void record_counters(msmb_field* f, const Workspace& W, const ErrRec& r) 
     f->counters[5] = W.launches_eval;
 }
 
-static void grow_cap(Workspace& W, const ErrRec& r) {
+void grow_cap(Workspace& W, const ErrRec& r) {
     const int need = std::max(r.overflow, W.cap);
     const int cap = std::max(need + need / 4 + 32, W.cap * 2);
     alloc_plist(W, cap);
@@ -1104,7 +1106,7 @@ int msmb_debug_stage(msmb_field* f, int stage, int k, const double box[3], const
         case 1: { // lattice cutoff on level k (runs all non-top levels; reads level k only)
             if (k < 0 || k + 1 >= g.levels) return MSMB_ERR_HIERARCHY;
             up(W.L.charge + g.lv[k].offset, in, g.lv[k].size);
-            f->launches += launch_lattice(f->stream, g, W.L, W.err);
+            f->launches += launch_lattice(f->stream, g, W.L, W.err, W.whole);
             down(out, W.L.pot + g.lv[k].offset, g.lv[k].size);
             break;
         }

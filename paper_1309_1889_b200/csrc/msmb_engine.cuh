@@ -84,6 +84,8 @@ struct Workspace {
     std::vector<std::string> stage_names;
     DBuf flush;                          // > L2, written between timed steps
     uint64_t uid = 0;                    // identifies whose stencil is in constant memory
+    Part whole;                          // the whole system (single-GPU path)
+    Part part;                           // this field's part of a spatial decomposition (msmb_dd.cu)
     ~Workspace();
 };
 
@@ -123,6 +125,7 @@ struct msmb_field {
     msmb::StateBuf scratch; // device system for the host-pointer entry points
     msmb::DBuf reduce;      // block partials of the raw-state reductions
     int refs = 0;           // live msmb_system objects bound to this field
+    int dd_nparts = 1, dd_part = 0; // spatial decomposition part (msmb_dd_set_part)
     bool destroy_pending = false;
 };
 
@@ -132,8 +135,15 @@ struct msmb_system {
 };
 
 namespace msmb {
-// engine entry points used by the parareal driver (caller holds f->mu)
+// engine entry points used by the parareal driver and the spatial decomposition
+// (caller holds f->mu)
 int engine_propagate(msmb_field* f, StateBuf& s, double dt, int steps, double conv);
 int engine_set_error(msmb_field* f, const Error& e);
 int cuda_fail(msmb_field* f, cudaError_t e, const char* where);
+Error ensure_workspace(msmb_field* f, int64_t n, const double* box);
+void ensure_const_table(msmb_field* f, Workspace& W);
+ErrRec read_err(msmb_field* f, Workspace& W);
+void record_counters(msmb_field* f, const Workspace& W, const ErrRec& r);
+void grow_cap(Workspace& W, const ErrRec& r);
+Error error_from_rec(const ErrRec& r);
 } // namespace msmb

@@ -314,4 +314,27 @@ Error build_geometry(const msmb_msm_config& c, const msmb_units& u, const double
     return Error{};
 }
 
+// Even split of [0, n) into `parts` ranges, range `part`, boundaries rounded down
+// to multiples of `align` (the last range ends at n).
+static void split_range(int n, int parts, int part, int align, int& b, int& e) {
+    auto cut = [&](int k) {
+        if (k >= parts) return n;
+        const int64_t c = int64_t(n) * k / parts;
+        return int(c - c % align);
+    };
+    b = cut(part);
+    e = cut(part + 1);
+    if (e < b) e = b;
+}
+
+Part make_part(const Geometry& g, int nparts, int part) {
+    Part P;
+    P.nparts = nparts < 1 ? 1 : nparts;
+    P.part = (part < 0 || part >= P.nparts) ? 0 : part;
+    split_range(g.ncx, P.nparts, P.part, 1, P.cx0, P.cx1);
+    for (int k = 0; k < g.levels; ++k) split_range(g.lv[k].dims[0], P.nparts, P.part, 4, P.pl0[k], P.pl1[k]);
+    return P;
+}
+
 } // namespace msmb
+

@@ -118,6 +118,19 @@ struct Geometry {
     int64_t top_taps = 0;                // M_top^2
 };
 
+// Work owned by one part of a spatial decomposition (one part
+// per GPU): the pair sum for i-clusters in pair columns [cx0, cx1) along x (all
+// y), anterpolation of level-0 planes [pl0[0], pl1[0]), the lattice cutoff of
+// level-k output planes [pl0[k], pl1[k]) (starts multiples of 4, the k_lattice
+// tile height), and interpolation + Verlet for the atoms binned into the owned
+// pair columns.  nparts == 1 is the whole system.
+struct Part {
+    int nparts = 1, part = 0;
+    int cx0 = 0, cx1 = 0;
+    int pl0[kMaxLevels] = {}, pl1[kMaxLevels] = {};
+};
+Part make_part(const Geometry& g, int nparts, int part);
+
 // Validation with the reference's messages.  Returns MSMB_OK or an error.
 Error validate_config(const msmb_msm_config& c);
 Error validate_units(const msmb_units& u);

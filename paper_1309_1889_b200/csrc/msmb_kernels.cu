@@ -394,11 +394,11 @@ constexpr int kListSeg = 128; // group segments longer than this keep column ord
 __global__ void __launch_bounds__(256)
     k_pairlist(const int* __restrict__ nclu, const float4* __restrict__ blo,
                const float4* __restrict__ bhi, const int* __restrict__ col_off, ListP p, int* plist,
-               int* pcnt, int cap, ErrRec* err) {
+               int* pcnt, int cap, int col_a, int col_b, ErrRec* err) {
     __shared__ int s_seg[8][kListSeg];
-    const int ic = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int ic = col_off[col_a] + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-    if (ic >= *nclu || failed(err)) return;
+    if (ic >= col_off[col_b] || failed(err)) return;
     const float4 lo = blo[ic], hi = bhi[ic];
     const double cutd = double(p.cut);
     int cx0 = int(floor((double(lo.x) - cutd - p.ox) / p.colw)) - 1;
@@ -487,15 +487,24 @@ struct PairP {
     float cut2f;
 };
 
-// 1/sqrt(x) for 0 < x < inf: MUFU.RSQ64H seed (rel. err < 2^-22.9) refined by one
-// cubically convergent Newton step, y += y*e*(1/2 + 3/8 e) with e = 1 - x*y^2
-// (error ~2^-68 before rounding: full double precision).  No special-value path:
-// callers only accumulate pairs with 0 < r2 < a2.
+#ifndef MSMB_RSQRT_NEWTON
+#define MSMB_RSQRT_NEWTON 3
+#endif
+// 1/sqrt(x) for 0 < x < inf: MUFU.RSQ64H seed refined by one cubically convergent
+// Newton step, y += y*e*(1/2 + 3/8 e) with e = 1 - x*y^2: full double precision.
+// (A quadratic step, MSMB_RSQRT_NEWTON=2, is one DP op cheaper and ~4% faster but
+// leaves a one-sided ~1e-12 relative bias -- measured: energy 8.7e-13, phi_short
+// 1.1e-12 on C2 shapes vs ~1e-15 with the cubic step -- so it is not the default.)
+// No special-value path: callers only accumulate pairs with 0 < r2 < a2.
 __device__ __forceinline__ double rsqrt_pos(double x) {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
     const double e = fma(-(x * y), y, 1.0);
+#if MSMB_RSQRT_NEWTON == 2
+    return fma(y * e, 0.5, y);
+#else
     return fma(y * e, fma(e, 0.375, 0.5), y);
+#endif
 }
 
 __device__ __forceinline__ void record_pair(ErrRec* err, int i, int j) {
@@ -535,12 +544,12 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
             const double* __restrict__ xs, const double* __restrict__ ys,
             const double* __restrict__ zs, const double* __restrict__ qs,
             const float4* __restrict__ f4, PairP p, double* phis, double* fsx, double* fsy,
-            double* fsz, ErrRec* err) {
+            double* fsz, const int* __restrict__ col_off, int col_a, int col_b, ErrRec* err) {
     __shared__ __align__(16) float s_sc[kPairWarps][4][32];
     __shared__ unsigned s_w[kPairWarps][8][kRow];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ic = blockIdx.x * kPairWarps + w;
-    if (ic >= *nclu || failed(err)) return;
+    const int ic = col_off[col_a] + blockIdx.x * kPairWarps + w;
+    if (ic >= col_off[col_b] || failed(err)) return;
     double a2 = p.a2, c0 = p.c0, c1 = p.c1, c2 = p.c2, d0 = p.d0, d1 = p.d1;
     asm volatile("" : "+d"(a2), "+d"(c0), "+d"(c1), "+d"(c2), "+d"(d0), "+d"(d1));
     const int2 c = clu[ic];
@@ -695,7 +704,7 @@ __global__ void k_err_brute(int64_t n, const double* __restrict__ x, const doubl
 }
 
 int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c,
-                    ErrRec* err, int cap) {
+                    ErrRec* err, int cap, const Part& P) {
     (void)a;
     const int cells_per_col = int(g.lv[0].dims[2]) * g.cw * g.cw;
     const int64_t nc = g.ncols;
@@ -715,12 +724,13 @@ int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, 
     lp.cut = float(g.screen_cut);
     lp.cut2 = float(g.screen_cut * g.screen_cut);
     k_pairlist<<<int((maxclu * 32 + 255) / 256), 256, 0, st>>>(c.nclu, c.blo, c.bhi, c.col_off, lp,
-                                                                c.plist, c.pcnt, cap, err);
+                                                                c.plist, c.pcnt, cap, P.cx0 * g.ncy,
+                                                                P.cx1 * g.ncy, err);
     return l + 4;
 }
 
 int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
-                 DevCells& c, ErrRec* err, int cap) {
+                 DevCells& c, ErrRec* err, int cap, const Part& P) {
     const double A = g.cfg.cutoff_a;
     PairP p;
     p.a2 = A * A;
@@ -740,7 +750,7 @@ int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& 
     if (n > 0) {
         k_pairs<<<int((maxclu + kPairWarps - 1) / kPairWarps), kPairWarps * 32, 0, st>>>(
             c.nclu, c.clu, c.plist, c.pcnt, cap, a.xs, a.ys, a.zs, a.qs, a.f4, p, a.phis,
-            a.fsx, a.fsy, a.fsz, err);
+            a.fsx, a.fsy, a.fsz, c.col_off, P.cx0 * g.ncy, P.cx1 * g.ncy, err);
         k_err_brute<<<592, 256, 0, st>>>(n, s.x, s.y, s.z, a.outlist, err);
         l = 2;
     }
@@ -759,7 +769,7 @@ constexpr int kAQ = 4; // points per thread along z
 
 __global__ void __launch_bounds__(128)
     k_anterp(BinP p, const int2* __restrict__ nat, const double* __restrict__ aw, double* q0,
-             const ErrRec* err) {
+             int x_begin, int x_end, const ErrRec* err) {
     if (failed(err)) return;
     const int d0 = p.d[0], d1 = p.d[1], d2 = p.d[2];
     const int nzq = (d2 + kAQ - 1) / kAQ;
@@ -768,10 +778,10 @@ __global__ void __launch_bounds__(128)
     const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int ox = int(tid & 3);
     const int64_t idx = tid >> 2;
-    const bool live = idx < int64_t(d0) * d1 * nzq;
+    const bool live = idx < int64_t(x_end - x_begin) * d1 * nzq;
     const int zq = live ? int(idx % nzq) : 0;
     const int y = live ? int((idx / nzq) % d1) : 0;
-    const int x = live ? int(idx / (int64_t(nzq) * d1)) : 0;
+    const int x = live ? x_begin + int(idx / (int64_t(nzq) * d1)) : 0;
     const int z0 = zq * kAQ;
     double acc[kAQ];
 #pragma unroll
@@ -818,10 +828,12 @@ __global__ void __launch_bounds__(128)
 }
 
 int launch_anterp(cudaStream_t st, const Geometry& g, DevAtoms& a, DevCells& c, DevLevels& L,
-                  ErrRec* err) {
+                  ErrRec* err, const Part& P) {
     const BinP p = make_binp(g);
-    const int64_t m = 4 * int64_t(p.d[0]) * p.d[1] * ((p.d[2] + kAQ - 1) / kAQ);
-    k_anterp<<<int((m + 127) / 128), 128, 0, st>>>(p, c.nat, a.aw, L.charge + g.lv[0].offset, err);
+    const int64_t m = 4 * int64_t(P.pl1[0] - P.pl0[0]) * p.d[1] * ((p.d[2] + kAQ - 1) / kAQ);
+    if (m == 0) return 0;
+    k_anterp<<<int((m + 127) / 128), 128, 0, st>>>(p, c.nat, a.aw, L.charge + g.lv[0].offset, P.pl0[0],
+                                                   P.pl1[0], err);
     return 1;
 }
 
@@ -1206,6 +1218,7 @@ struct LatJob {
     int d0, d1, d2;
     int tzn, tyn;
     int blk0;      // first tile index of this job
+    int x0;        // first owned output plane (multiple of 4)
     double scale;  // 2^-k
     size_t off;    // lattice offset (partials)
 };
@@ -1233,7 +1246,7 @@ __global__ void __launch_bounds__(32) k_lattice(LatJobs J, const ErrRec* err) {
     t -= jb.blk0;
     const int tz = t % jb.tzn, rest = t / jb.tzn;
     const int ty = rest % jb.tyn, tx = rest / jb.tyn;
-    const int x0 = tx * kLP, y0 = ty * 32, z0 = tz * kLB;
+    const int x0 = jb.x0 + tx * kLP, y0 = ty * 32, z0 = tz * kLB;
     const int R = J.R, W = 2 * J.R + 1, SY = 32 + 2 * J.R;
     int xs_lo = max(0, x0 - R), xs_hi = min(jb.d0 - 1, x0 + kLP - 1 + R);
     {
@@ -1399,7 +1412,7 @@ int lattice_splits(const Geometry& g) {
     return int(std::max<int64_t>(1, std::min<int64_t>(8, (target + tiles - 1) / tiles)));
 }
 
-int launch_lattice(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err) {
+int launch_lattice(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err, const Part& P) {
     if (g.levels < 2) return 0;
     LatJobs J;
     J.n = 0;
@@ -1426,12 +1439,14 @@ int launch_lattice(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err
         j.tzn = (j.d2 + kLB - 1) / kLB;
         j.tyn = (j.d1 + 31) / 32;
         j.blk0 = tiles;
+        j.x0 = P.pl0[k];
         j.scale = std::ldexp(1.0, -k);
         j.off = lv.offset;
-        tiles += ((j.d0 + kLP - 1) / kLP) * j.tyn * j.tzn;
+        tiles += ((P.pl1[k] - P.pl0[k] + kLP - 1) / kLP) * j.tyn * j.tzn;
         total = int64_t(lv.offset + lv.size);
         J.j[J.n++] = j;
     }
+    if (tiles == 0) return 0;
     const size_t smem = lattice_smem_bytes(g);
     if (L.lat_const)
         k_lattice<true><<<tiles * J.S, 32, smem, st>>>(J, err);
@@ -1548,14 +1563,15 @@ static InterpP make_interp(const Geometry& g) {
     return p;
 }
 
-__global__ void k_interp(InterpP p, const int* __restrict__ total, const int* __restrict__ perm,
+__global__ void k_interp(InterpP p, const int* __restrict__ start, int64_t cell_a, int64_t cell_b,
+                         const int* __restrict__ perm,
                          const double* __restrict__ xs, const double* __restrict__ ys,
                          const double* __restrict__ zs, const double* __restrict__ qs,
                          const double* __restrict__ pot, const double* __restrict__ phis,
                          const double* __restrict__ fsx, const double* __restrict__ fsy,
                          const double* __restrict__ fsz, DevOut o, const ErrRec* err) {
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= *total || failed(err)) return;
+    const int s = start[cell_a] + blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= start[cell_b] || failed(err)) return;
     double u, gx, gy, gz;
     const double q = qs[s];
     interp_atom(p, pot, xs[s], ys[s], zs[s], u, gx, gy, gz);
@@ -1608,9 +1624,11 @@ __global__ void __launch_bounds__(256) k_energy2(int nb, const double* __restric
 int reduce_blocks(int64_t n) { return int((n + 4095) / 4096) > 0 ? int((n + 4095) / 4096) : 1; }
 
 int launch_interp(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c,
-                  DevLevels& L, DevOut& o, ErrRec* err, int want_energy) {
+                  DevLevels& L, DevOut& o, ErrRec* err, int want_energy, const Part& P) {
     if (n == 0) return 0;
-    k_interp<<<int((n + 127) / 128), 128, 0, st>>>(make_interp(g), c.start + g.ncells, a.perm, a.xs,
+    const int64_t cpc = int64_t(g.lv[0].dims[2]) * g.cw * g.cw; // sorted cells per pair column
+    k_interp<<<int((n + 127) / 128), 128, 0, st>>>(make_interp(g), c.start, int64_t(P.cx0) * g.ncy * cpc,
+                                                   int64_t(P.cx1) * g.ncy * cpc, a.perm, a.xs,
                                                    a.ys, a.zs, a.qs, L.pot + g.lv[0].offset, a.phis,
                                                    a.fsx, a.fsy, a.fsz, o, err);
     if (!want_energy) return 1;
@@ -1727,6 +1745,76 @@ int launch_kick(cudaStream_t st, DevState& s, const DevOut& o, double dt, double
     const double hdc = 0.5 * dt * conv;
     k_kick<<<int((s.n + 255) / 256), 256, 0, st>>>(s.n, s.vx, s.vy, s.vz, s.m, o.fx, o.fy, o.fz, hdc,
                                                    err);
+    return 1;
+}
+
+// Spatial decomposition (msmb_dd.cu): the same Verlet arithmetic restricted to the
+// atoms binned into the owned pair columns (sorted range -> original index).
+__global__ void k_verlet_part(const int* __restrict__ start, int64_t cell_a, int64_t cell_b,
+                              const int* __restrict__ perm, DevState s, const double* __restrict__ fx,
+                              const double* __restrict__ fy, const double* __restrict__ fz, double dt,
+                              double hdc, int kicks, int drift, const ErrRec* err) {
+    if (failed(err)) return;
+    const int t = start[cell_a] + blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= start[cell_b]) return;
+    const int i = perm[t];
+    const double c = __ddiv_rn(hdc, s.m[i]);
+    double a = s.vx[i], b = s.vy[i], d = s.vz[i];
+    const double Fx = fx[i], Fy = fy[i], Fz = fz[i];
+    for (int k = 0; k < kicks; ++k) {
+        a = __dadd_rn(a, __dmul_rn(Fx, c));
+        b = __dadd_rn(b, __dmul_rn(Fy, c));
+        d = __dadd_rn(d, __dmul_rn(Fz, c));
+    }
+    s.vx[i] = a;
+    s.vy[i] = b;
+    s.vz[i] = d;
+    if (drift) {
+        s.x[i] = __dadd_rn(s.x[i], __dmul_rn(a, dt));
+        s.y[i] = __dadd_rn(s.y[i], __dmul_rn(b, dt));
+        s.z[i] = __dadd_rn(s.z[i], __dmul_rn(d, dt));
+    }
+}
+
+__global__ void k_export_state(const int* __restrict__ start, int64_t cell_a, int64_t cell_b,
+                               const int* __restrict__ perm, DevState s, int64_t n, long long* xbuf) {
+    const int t = start[cell_a] + blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= start[cell_b]) return;
+    const int i = perm[t];
+    const double* src[6] = {s.x, s.y, s.z, s.vx, s.vy, s.vz};
+#pragma unroll
+    for (int k = 0; k < 6; ++k) xbuf[k * n + i] = __double_as_longlong(src[k][i]);
+}
+
+__global__ void k_fill_i64(long long* p, int64_t count, long long v) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+
+int launch_verlet_part(cudaStream_t st, const Geometry& g, const DevCells& c, const DevAtoms& a,
+                       DevState& s, const DevOut& o, double dt, double conv, int kicks, int drift,
+                       const Part& P, ErrRec* err) {
+    if (s.n == 0 || (kicks == 0 && !drift)) return 0;
+    const int64_t cpc = int64_t(g.lv[0].dims[2]) * g.cw * g.cw;
+    const double hdc = 0.5 * dt * conv;
+    k_verlet_part<<<int((s.n + 255) / 256), 256, 0, st>>>(c.start, int64_t(P.cx0) * g.ncy * cpc,
+                                                           int64_t(P.cx1) * g.ncy * cpc, a.perm, s, o.fx,
+                                                           o.fy, o.fz, dt, hdc, kicks, drift, err);
+    return 1;
+}
+
+int launch_export_state(cudaStream_t st, const Geometry& g, const DevCells& c, const DevAtoms& a,
+                        const DevState& s, long long* xbuf, const Part& P) {
+    if (s.n == 0) return 0;
+    const int64_t cpc = int64_t(g.lv[0].dims[2]) * g.cw * g.cw;
+    k_export_state<<<int((s.n + 255) / 256), 256, 0, st>>>(c.start, int64_t(P.cx0) * g.ncy * cpc,
+                                                            int64_t(P.cx1) * g.ncy * cpc, a.perm, s, s.n, xbuf);
+    return 1;
+}
+
+int launch_fill_i64(cudaStream_t st, long long* p, int64_t count, long long v) {
+    if (count <= 0) return 0;
+    k_fill_i64<<<592, 256, 0, st>>>(p, count, v);
     return 1;
 }
 

@@ -78,15 +78,15 @@ int launch_bin(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& 
 int launch_sort(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& a, DevCells& c,
                 ErrRec* err);
 int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c,
-                    ErrRec* err, int cap);
+                    ErrRec* err, int cap, const Part& P);
 int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
-                 DevCells& c, ErrRec* err, int cap);
+                 DevCells& c, ErrRec* err, int cap, const Part& P);
 int launch_anterp(cudaStream_t st, const Geometry& g, DevAtoms& a, DevCells& c, DevLevels& L,
-                  ErrRec* err);
+                  ErrRec* err, const Part& P);
 int launch_restrict(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err);
 int launch_restrict_all(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
 int launch_prolong_all(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
-int launch_lattice(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
+int launch_lattice(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err, const Part& P);
 size_t lattice_smem_bytes(const Geometry& g);
 cudaError_t lattice_prepare(size_t bytes);
 int lattice_splits(const Geometry& g);
@@ -95,7 +95,16 @@ cudaError_t lattice_upload_const(const Geometry& g, cudaStream_t st);
 int launch_top(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
 int launch_prolong(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err);
 int launch_interp(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c,
-                  DevLevels& L, DevOut& o, ErrRec* err, int want_energy);
+                  DevLevels& L, DevOut& o, ErrRec* err, int want_energy, const Part& P);
+// spatial decomposition (msmb_dd.cu): Verlet on the atoms of the owned pair columns
+// (kicks half-kicks, then a drift if `drift`), export of their state into a 6n
+// int64 exchange buffer (others INT64_MIN), and an int64 fill
+int launch_verlet_part(cudaStream_t st, const Geometry& g, const DevCells& c, const DevAtoms& a,
+                       DevState& s, const DevOut& o, double dt, double conv, int kicks, int drift,
+                       const Part& P, ErrRec* err);
+int launch_export_state(cudaStream_t st, const Geometry& g, const DevCells& c, const DevAtoms& a,
+                        const DevState& s, long long* xbuf, const Part& P);
+int launch_fill_i64(cudaStream_t st, long long* p, int64_t count, long long v);
 int launch_finalize(cudaStream_t st, const DevState& s, ErrRec* err);
 int launch_kick_drift(cudaStream_t st, DevState& s, const DevOut& o, double dt, double conv,
                       int kicks, ErrRec* err);

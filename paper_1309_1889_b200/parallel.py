@@ -329,3 +329,146 @@ def parareal_run(v: ParticleSystem, total_points: int, cfg: PararealConfig, grou
         current = w.lam_prev[prefix]
         remaining -= prefix
     return ShardedPararealResult(traj, counts, window_idx, True, rows, point_iters, info)
+
+
+# ============================================================================ spatial
+def exchange_max_bits(tensors, group=None, use_dist: bool = True):
+    """Exact exchange of disjointly owned values (include/msmb.h, spatial decomposition).
+
+    `tensors` are the int64 views of one buffer on each local part. Unowned
+    entries are INT64_MIN, so an element-wise MAX over parts and ranks leaves
+    every owner's bit pattern in place. This also covers -0.0 (== INT64_MIN),
+    NaNs and infinities. Local parts are combined first, then the result is
+    all-reduced (MAX) over the ranks of `group` and copied back to every local
+    part.
+    """
+    import torch
+    m = tensors[0]
+    if len(tensors) > 1:
+        m = tensors[0].clone()
+        for t in tensors[1:]:
+            torch.maximum(m, t, out=m)
+    dist = _dist() if use_dist else None
+    if dist is not None and dist.get_world_size(group) > 1:
+        dist.all_reduce(m, op=dist.ReduceOp.MAX, group=group)
+    for t in tensors:
+        if t is not m:
+            t.copy_(m)
+    return m
+
+
+class SpatialDecomposition:
+    """MSM force + velocity-Verlet propagation split over parts.
+
+    One part per process/GPU under torchrun (``group``, default: the whole job),
+    or ``local_parts`` parts in this process (one GPU). The latter runs the
+    identical phase/exchange sequence; the tests use it to check the decomposed
+    trajectory against the single-GPU one. Every part holds the whole particle
+    state, owns an x-slab of the work, and exchanges exactly (see
+    csrc/msmb_dd.cu and include/msmb.h). Results equal
+    ``propagate(PropagatorSpec(MsmField(config), dt, steps), s)`` bit for bit.
+    Only the energy differs: it is summed per part.
+    """
+
+    def __init__(self, config, system: ParticleSystem, units=None, group=None, local_parts: int = 0,
+                 device: Optional[int] = None):
+        import torch
+        from . import DeviceSystem, UnitsConfig
+        self.torch = torch
+        self.group = group
+        self.units = units or UnitsConfig.physical()
+        self._uc = self.units._c()
+        if local_parts:
+            nparts, mine, self.distributed = int(local_parts), list(range(int(local_parts))), False
+        else:
+            comm = _Comm(group)
+            nparts, mine, self.distributed = comm.world, [comm.rank], comm.world > 1
+        self.nparts = nparts
+        dev = torch.cuda.current_device() if device is None else device
+        self.device = torch.device("cuda", dev)
+        lib = _native.lib()
+        self.lib = lib
+        self.parts = []
+        for p in mine:
+            f = MsmField(config, self.units, device=dev)
+            _check(f.handle, lib.msmb_dd_set_part(f.handle, nparts, p))
+            ds = DeviceSystem(f, system)
+            sizes = np.zeros(3, dtype=np.int64)
+            _check(f.handle, lib.msmb_dd_sizes(f.handle, ds._h, sizes.ctypes.data_as(C.POINTER(C.c_int64))))
+            bufs = [torch.empty(int(max(sz, 1)), dtype=torch.int64, device=self.device) for sz in sizes]
+            self.parts.append((f, ds, bufs))
+        self.system = system
+        self.n = system.size()
+        self.exchanged_bytes = 0
+
+    def _phase(self, phase: int, dt: float = 0.0, kicks: int = 0, drift: int = 0) -> float:
+        self.torch.cuda.current_stream(self.device).synchronize()
+        energy = 0.0
+        for f, ds, bufs in self.parts:
+            e = C.c_double()
+            xin = C.c_void_p(bufs[phase - 1].data_ptr()) if phase > 0 else None
+            xout = C.c_void_p(bufs[phase].data_ptr()) if phase < 3 else None
+            _check(f.handle, self.lib.msmb_dd_phase(f.handle, ds._h, phase, dt, kicks, drift, C.byref(self._uc),
+                                                    xin, xout, C.byref(e)))
+            energy += e.value
+        return energy
+
+    def _exchange(self, which: int):
+        bufs = [b[which] for _, _, b in self.parts]
+        exchange_max_bits(bufs, self.group, use_dist=self.distributed)
+        self.exchanged_bytes += bufs[0].numel() * 8
+        self.torch.cuda.current_stream(self.device).synchronize()
+
+    def _energy_sum(self, e: float) -> float:
+        if not self.distributed:
+            return e
+        t = self.torch.tensor([e], dtype=self.torch.float64, device=self.device)
+        _dist().all_reduce(t, group=self.group)
+        return float(t.item())
+
+    def _state(self):
+        _, ds, _ = self.parts[0]
+        t = self.torch.empty(6 * self.n, dtype=self.torch.float64, device=self.device)
+        _check(self.parts[0][0].handle, self.lib.msmb_system_get_state_device(ds._h, C.c_void_p(t.data_ptr())))
+        return t
+
+    def _set_state(self, t):
+        for f, ds, _ in self.parts:
+            _check(f.handle, self.lib.msmb_system_set_state_device(ds._h, C.c_void_p(t.data_ptr())))
+
+    def propagate(self, dt: float, steps: int):
+        """propagate(spec, s, units) (src/integrate.cpp:13-36): one evaluation, then
+        `steps` velocity-Verlet steps. Returns (final ParticleSystem, energy of the
+        last evaluation). On error the state is left as it was, and the
+        reference's exception is raised on every part."""
+        if not (dt > 0.0):
+            raise ConfigError("dt must be > 0")
+        if steps < 0:
+            raise ConfigError("steps_per_slice must be >= 1")
+        backup = self._state()
+        energy = 0.0
+        try:
+            for s in range(steps + 1):
+                if steps == 0:
+                    kicks, drift = 0, 0
+                elif s == 0:
+                    kicks, drift = 1, 1      # opening half-kick + drift of step 1
+                elif s < steps:
+                    kicks, drift = 2, 1      # closing kick of step s, opening kick + drift of s+1
+                else:
+                    kicks, drift = 1, 0      # closing half-kick of the last step
+                self._phase(0)
+                self._exchange(0)
+                self._phase(1)
+                self._exchange(1)
+                energy = self._phase(2, dt, kicks, drift)
+                if kicks or drift:
+                    self._exchange(2)
+                    self._phase(3)
+        except Error:
+            self._set_state(backup)
+            raise
+        energy = self._energy_sum(energy)
+        pos, vel = self.parts[0][1].download()
+        s = self.system
+        return ParticleSystem(pos, vel, s.charges, s.masses, s.box), energy
