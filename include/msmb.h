@@ -247,6 +247,10 @@ int msmb_bench_propagate(msmb_field* f, msmb_system* s, double dt, int steps, in
 /* Sustained FP64 FMA throughput of `device` (TFLOP/s, FMA = 2 flops), measured
  * with an FMA-chain microbenchmark for about `seconds`. */
 int msmb_measure_fp64_peak(int device, double seconds, double* tflops);
+/* Lattice-cutoff method for levels 0..l-2: 0 (default) = zero-padded FFT
+ * convolution, 1 = direct stencil sum as the reference (src/msm_phases.cpp:93-134).
+ * Both agree to rounding; the direct sum is kept for comparison and tests. */
+int msmb_set_lattice_method(msmb_field* f, int direct);
 /* Kernel launches issued by this handle since creation. */
 int64_t msmb_kernel_launches(const msmb_field* f);
 

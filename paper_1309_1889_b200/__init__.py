@@ -245,6 +245,11 @@ class MsmField(ForceField):
         return PotentialResult(phi, f, float(e[0]), ps, pl)
 
     # -- measurement / diagnostics
+    def set_lattice_method(self, direct: bool):
+        """Lattice cutoff by zero-padded FFT convolution (default) or by the direct
+        stencil sum of the reference (src/msm_phases.cpp:93-134)."""
+        _check(self._h, _native.lib().msmb_set_lattice_method(self._h, int(bool(direct))))
+
     def set_stage_timing(self, on: bool):
         _native.lib().msmb_set_stage_timing(self._h, int(on))
 

@@ -92,7 +92,8 @@ int phase1(msmb_field* f, Workspace& W, const long long* xin, long long* xbuf) {
     ckd(cudaMemcpyAsync(W.L.charge, xin, sizeof(double) * g.lv[0].size, cudaMemcpyDeviceToDevice, st), "D2D");
     ensure_const_table(f, W);
     f->launches += launch_restrict_all(st, g, W.L, W.err);
-    f->launches += launch_lattice(st, g, W.L, W.err, W.part);
+    // the FFT path transforms whole levels (replicated); the direct path only owned planes
+    f->launches += W.lattice_fft ? launch_lattice_fft(st, W.fft, W.err) : launch_lattice(st, g, W.L, W.err, W.part);
     f->launches += launch_fill_i64(st, xbuf, int64_t(g.lattice_total), LLONG_MIN);
     for (int k = 0; k + 1 < g.levels; ++k) export_planes(st, g, W.part, k, W.L.pot, xbuf);
     ckd(cudaGetLastError(), "kernel launch");
@@ -162,6 +163,14 @@ extern "C" int msmb_dd_set_part(msmb_field* f, int nparts, int part) {
     f->dd_nparts = nparts;
     f->dd_part = part;
     if (f->ws) f->ws->part = make_part(f->ws->g, nparts, part);
+    return MSMB_OK;
+}
+
+extern "C" int msmb_set_lattice_method(msmb_field* f, int direct) {
+    if (!f) return MSMB_ERR_CONFIG;
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    f->lattice_direct = direct ? 1 : 0;
+    f->ws.reset(); // rebuilt on the next call with the chosen method
     return MSMB_OK;
 }
 

@@ -237,6 +237,48 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
         L.lat_partial = L.lat_S > 1 ? walloc<double>(*W, size_t(L.lat_S) * g.lattice_total) : nullptr;
         ck(lattice_prepare(lattice_smem_bytes(g)), "cudaFuncSetAttribute");
     }
+    // FFT lattice cutoff: plan, twiddles, per-level kernel spectra (msmb_fft.cu)
+    W->lattice_fft = !f->lattice_direct && g.levels >= 2;
+    if (g.levels >= 2 && W->lattice_fft) {
+        FftJobs& J = W->fft;
+        J = FftJobs{};
+        J.n = g.levels - 1;
+        std::vector<int> Ms;
+        std::vector<double2> tw;
+        auto tw_of = [&](int M) {
+            for (size_t i = 0, off = 0; i < Ms.size(); off += size_t(Ms[i]), ++i)
+                if (Ms[i] == M) return int(off);
+            const int off = int(tw.size());
+            Ms.push_back(M);
+            for (int m = 0; m < M; ++m) {
+                const long double ang = -2.0L * 3.141592653589793238462643383279502884L * m / M;
+                tw.push_back(make_double2(double(cosl(ang)), double(sinl(ang))));
+            }
+            return off;
+        };
+        size_t boff = 0;
+        for (int k = 0; k < J.n; ++k) {
+            FftLevel& lv = J.lv[k];
+            for (int ax = 0; ax < 3; ++ax) {
+                lv.d[ax] = g.lv[k].dims[ax];
+                const int M = fft_len(lv.d[ax] + g.lat.R);
+                lv.ax[ax] = fft_axis(M, tw_of(M));
+                J.maxM = std::max(J.maxM, M);
+            }
+            lv.boff = lv.soff = boff;
+            boff += size_t(lv.ax[0].M) * lv.ax[1].M * lv.ax[2].M;
+            lv.q = L.charge + g.lv[k].offset;
+            lv.u = L.pot + g.lv[k].offset;
+        }
+        J.L = std::max(1, std::min(16, 2048 / J.maxM));
+        J.buf = walloc<double2>(*W, boff);
+        J.spec = walloc<double>(*W, boff);
+        J.tw = wupload(*W, tw);
+        ck(cudaDeviceSynchronize(), "sync uploads");
+        ck(fft_prepare(size_t(2) * J.L * J.maxM * sizeof(double2)), "cudaFuncSetAttribute");
+        launch_fft_spectrum(f->stream, J, L, g.lat.R, g.lat.TW);
+        ck(cudaGetLastError(), "fft spectrum");
+    }
     if (smem > 227 * 1024) {
         e.kind = MSMB_ERR_CONFIG;
         e.msg = "msm: top level of " + std::to_string(g.lv[g.levels - 1].size) +
@@ -332,7 +374,9 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs) 
     }
     run("anterp", [&] { return launch_anterp(lr, g, W.a, W.c, W.L, W.err, W.whole); });
     run("restrict", [&] { return launch_restrict_all(lr, g, W.L, W.err); });
-    run("lattice", [&] { return launch_lattice(lr, g, W.L, W.err, W.whole); });
+    run("lattice", [&] {
+        return W.lattice_fft ? launch_lattice_fft(lr, W.fft, W.err) : launch_lattice(lr, g, W.L, W.err, W.whole);
+    });
     run("top", [&] { return launch_top(lr, g, W.L, W.err); });
     run("prolong", [&] { return launch_prolong_all(lr, g, W.L, W.err); });
     if (fork) ck(cudaEventRecord(f->join_ev, lr), "join");
@@ -1106,7 +1150,8 @@ int msmb_debug_stage(msmb_field* f, int stage, int k, const double box[3], const
         case 1: { // lattice cutoff on level k (runs all non-top levels; reads level k only)
             if (k < 0 || k + 1 >= g.levels) return MSMB_ERR_HIERARCHY;
             up(W.L.charge + g.lv[k].offset, in, g.lv[k].size);
-            f->launches += launch_lattice(f->stream, g, W.L, W.err, W.whole);
+            f->launches += W.lattice_fft ? launch_lattice_fft(f->stream, W.fft, W.err)
+                                         : launch_lattice(f->stream, g, W.L, W.err, W.whole);
             down(out, W.L.pot + g.lv[k].offset, g.lv[k].size);
             break;
         }

@@ -84,6 +84,8 @@ struct Workspace {
     std::vector<std::string> stage_names;
     DBuf flush;                          // > L2, written between timed steps
     uint64_t uid = 0;                    // identifies whose stencil is in constant memory
+    FftJobs fft{};                       // FFT lattice cutoff plan (msmb_fft.cu)
+    bool lattice_fft = true;             // false: direct stencil (k_lattice)
     Part whole;                          // the whole system (single-GPU path)
     Part part;                           // this field's part of a spatial decomposition (msmb_dd.cu)
     ~Workspace();
@@ -126,6 +128,7 @@ struct msmb_field {
     msmb::DBuf reduce;      // block partials of the raw-state reductions
     int refs = 0;           // live msmb_system objects bound to this field
     int dd_nparts = 1, dd_part = 0; // spatial decomposition part (msmb_dd_set_part)
+    int lattice_direct = 0;         // msmb_set_lattice_method: 1 = direct stencil sum
     bool destroy_pending = false;
 };
 

@@ -56,6 +56,34 @@ struct DevLevels {      // concatenated lattices + tables
     double* taps[kMaxLevels];
 };
 
+// FFT lattice cutoff (msmb_fft.cu): per level and axis a padded length M = 2^a 3^b
+// >= d + R, its radix list and the offset of its twiddle table exp(-2 pi i m / M)
+constexpr int kFftMaxF = 20;
+struct FftAxis {
+    int M, nf, tw;
+    int fac[kFftMaxF];
+};
+struct FftLevel {
+    int d[3];
+    FftAxis ax[3];
+    size_t boff, soff;  // complex work buffer / spectrum offsets
+    const double* q;    // level charges
+    double* u;          // level potentials
+    int blk0;           // first block of this level in the current pass
+};
+struct FftJobs {
+    FftLevel lv[kMaxLevels];
+    int n, L, maxM;     // levels, lines per tile, max M
+    double2* buf;
+    double* spec;
+    const double2* tw;
+};
+int fft_len(int need);
+FftAxis fft_axis(int M, int tw_off);
+cudaError_t fft_prepare(size_t smem);
+int launch_fft_spectrum(cudaStream_t st, FftJobs J, const DevLevels& L, int R, int TW);
+int launch_lattice_fft(cudaStream_t st, FftJobs J, const ErrRec* err);
+
 struct DevState {       // a device-resident ParticleSystem (SoA)
     int64_t n;
     double* x; double* y; double* z;

@@ -140,3 +140,32 @@ def test_msm_potential_free_function(port):
     g = golden("spec500")
     r = pkg.msm_potential(pkg.ParticleSystem(g["pos"], None, g["q"], None, g["box"]), pkg.MsmConfig(8.0, 2.0, 3))
     assert rel_e(r.total_energy, float(g["energy"])) <= E_TOL
+
+
+@pytest.mark.parametrize("name,n", [("c2s", 30000), ("c4", 45000), ("c5", 40000)])
+def test_fft_and_direct_lattice_agree(name, n):
+    w = fx.config(name, n_override=n)
+    a = field(w)
+    b = field(w)
+    b.set_lattice_method(direct=True)
+    ra, rb = a.evaluate(system(w)), b.evaluate(system(w))
+    assert rel_e(ra.total_energy, rb.total_energy) <= 1e-13
+    assert rel_rms(ra.long_part, rb.long_part) <= 1e-13
+    assert np.array_equal(ra.short_part, rb.short_part)
+
+
+def test_propagate_bitwise_across_fresh_fields():
+    # two independently built fields (own spectra, own workspaces) and the graph vs
+    # eager paths give bit-identical trajectories (C2 shape with small levels where
+    # the FFT padding M < 2R + 1)
+    w = fx.config("c2s", n_override=30000)
+    out = []
+    for eager in (False, False, True):
+        f = field(w)
+        ds = pkg.DeviceSystem(f, system(w))
+        if eager:
+            f.set_stage_timing(True)
+        ds.propagate(w.dt, 2)
+        out.append(ds.download())
+    for p, v in out[1:]:
+        assert np.array_equal(p, out[0][0]) and np.array_equal(v, out[0][1])

@@ -63,10 +63,13 @@ def test_interpolation_bitwise(port, name, n):
     assert np.array_equal(got, port.interpolate(w.pos, w.box, w.a, w.h, w.levels, pot0))
 
 
+@pytest.mark.parametrize("method", ["fft", "direct"])
 @pytest.mark.parametrize("name,n", CASES)
-def test_lattice_cutoff(port, name, n):
+def test_lattice_cutoff(port, name, n, method):
+    # fft: zero-padded FFT convolution (default); direct: the stencil sum (k_lattice)
     w, cfg, o, sl = _setup(port, name, n)
     f = pkg.MsmField(cfg)
+    f.set_lattice_method(direct=method == "direct")
     for k in range(w.levels - 1):
         q = o["level_charge"][sl[k]]
         got = f.debug_stage(1, k, w.box, q)
