@@ -106,7 +106,7 @@ int phase2(msmb_field* f, Workspace& W, DevState& s, const long long* xin, long 
     const Geometry& g = W.g;
     cudaStream_t st = f->stream;
     ckd(cudaMemcpyAsync(W.L.pot, xin, sizeof(double) * g.lattice_total, cudaMemcpyDeviceToDevice, st), "D2D");
-    f->launches += launch_top(st, g, W.L, W.err);
+    f->launches += W.fft_top.n ? launch_lattice_fft(st, W.fft_top, W.err) : launch_top(st, g, W.L, W.err);
     f->launches += launch_prolong_all(st, g, W.L, W.err);
     DevOut o = W.o;
     o.phi = o.phis = o.phil = nullptr;

@@ -237,46 +237,66 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
         L.lat_partial = L.lat_S > 1 ? walloc<double>(*W, size_t(L.lat_S) * g.lattice_total) : nullptr;
         ck(lattice_prepare(lattice_smem_bytes(g)), "cudaFuncSetAttribute");
     }
-    // FFT lattice cutoff: plan, twiddles, per-level kernel spectra (msmb_fft.cu)
+    // FFT lattice cutoff + large top level: plans, twiddles, kernel spectra (msmb_fft.cu)
     W->lattice_fft = !f->lattice_direct && g.levels >= 2;
-    if (g.levels >= 2 && W->lattice_fft) {
-        FftJobs& J = W->fft;
-        J = FftJobs{};
-        J.n = g.levels - 1;
+    if (W->lattice_fft) {
         std::vector<int> Ms;
         std::vector<double2> tw;
         auto tw_of = [&](int M) {
-            for (size_t i = 0, off = 0; i < Ms.size(); off += size_t(Ms[i]), ++i)
+            size_t off = 0;
+            for (size_t i = 0; i < Ms.size(); off += size_t(Ms[i]), ++i)
                 if (Ms[i] == M) return int(off);
-            const int off = int(tw.size());
             Ms.push_back(M);
             for (int m = 0; m < M; ++m) {
                 const long double ang = -2.0L * 3.141592653589793238462643383279502884L * m / M;
                 tw.push_back(make_double2(double(cosl(ang)), double(sinl(ang))));
             }
-            return off;
+            return int(off);
         };
-        size_t boff = 0;
-        for (int k = 0; k < J.n; ++k) {
-            FftLevel& lv = J.lv[k];
-            for (int ax = 0; ax < 3; ++ax) {
-                lv.d[ax] = g.lv[k].dims[ax];
-                const int M = fft_len(lv.d[ax] + g.lat.R);
-                lv.ax[ax] = fft_axis(M, tw_of(M));
-                J.maxM = std::max(J.maxM, M);
+        // job lists: cutoff levels 0..l-2 (pad d + R) and, if large, the top (pad 2d - 1)
+        auto plan = [&](FftJobs& J, int k0, int k1, bool top) {
+            J = FftJobs{};
+            J.n = k1 - k0;
+            size_t boff = 0;
+            for (int k = k0; k < k1; ++k) {
+                FftLevel& lv = J.lv[k - k0];
+                for (int ax = 0; ax < 3; ++ax) {
+                    lv.d[ax] = g.lv[k].dims[ax];
+                    const int M = fft_len(top ? 2 * lv.d[ax] - 1 : lv.d[ax] + g.lat.R);
+                    lv.ax[ax] = fft_axis(M, tw_of(M));
+                    J.maxM = std::max(J.maxM, M);
+                }
+                lv.boff = lv.soff = boff;
+                boff += size_t(lv.ax[0].M) * lv.ax[1].M * lv.ax[2].M;
+                lv.q = L.charge + g.lv[k].offset;
+                lv.u = L.pot + g.lv[k].offset;
             }
-            lv.boff = lv.soff = boff;
-            boff += size_t(lv.ax[0].M) * lv.ax[1].M * lv.ax[2].M;
-            lv.q = L.charge + g.lv[k].offset;
-            lv.u = L.pot + g.lv[k].offset;
-        }
-        J.L = std::max(1, std::min(16, 2048 / J.maxM));
-        J.buf = walloc<double2>(*W, boff);
-        J.spec = walloc<double>(*W, boff);
-        J.tw = wupload(*W, tw);
+            J.L = std::max(1, std::min(16, 2048 / std::max(J.maxM, 1)));
+            J.buf = walloc<double2>(*W, boff);
+            J.spec = walloc<double>(*W, boff);
+            return boff;
+        };
+        const int lt = g.levels - 1;
+        plan(W->fft, 0, lt, false);
+        const bool big_top = int64_t(g.lv[lt].size) > kTopFftMin;
+        if (big_top) plan(W->fft_top, lt, lt + 1, true);
+        const double2* twd = wupload(*W, tw);
+        W->fft.tw = twd;
+        W->fft_top.tw = twd;
         ck(cudaDeviceSynchronize(), "sync uploads");
-        ck(fft_prepare(size_t(2) * J.L * J.maxM * sizeof(double2)), "cudaFuncSetAttribute");
-        launch_fft_spectrum(f->stream, J, L, g.lat.R, g.lat.TW);
+        ck(fft_prepare(size_t(2) * std::max(W->fft.L * W->fft.maxM, W->fft_top.L * W->fft_top.maxM) *
+                       sizeof(double2)),
+           "cudaFuncSetAttribute");
+        std::vector<FftKernel> K(size_t(W->fft.n));
+        for (int k = 0; k < W->fft.n; ++k)
+            K[k] = FftKernel{0, L.lat_rowidx, L.lat_taps, {g.lat.R, g.lat.R, g.lat.R}, g.lat.TW, std::ldexp(1.0, -k)};
+        launch_fft_spectrum(f->stream, W->fft, K.data());
+        if (big_top) {
+            const ConvTable& t = g.top;
+            const FftKernel KT{1, nullptr, L.taps[lt], {t.Rx, t.Ry, t.Rz}, (2 * t.Rz + 1 + kConvL - 1) / kConvL * kConvL,
+                               1.0};
+            launch_fft_spectrum(f->stream, W->fft_top, &KT);
+        }
         ck(cudaGetLastError(), "fft spectrum");
     }
     if (smem > 227 * 1024) {
@@ -377,7 +397,9 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs) 
     run("lattice", [&] {
         return W.lattice_fft ? launch_lattice_fft(lr, W.fft, W.err) : launch_lattice(lr, g, W.L, W.err, W.whole);
     });
-    run("top", [&] { return launch_top(lr, g, W.L, W.err); });
+    run("top", [&] {
+        return W.fft_top.n ? launch_lattice_fft(lr, W.fft_top, W.err) : launch_top(lr, g, W.L, W.err);
+    });
     run("prolong", [&] { return launch_prolong_all(lr, g, W.L, W.err); });
     if (fork) ck(cudaEventRecord(f->join_ev, lr), "join");
     run("clusters", [&] { return launch_clusters(st, g, s.n, W.a, W.c, W.err, W.cap, W.whole); });
@@ -1158,7 +1180,8 @@ int msmb_debug_stage(msmb_field* f, int stage, int k, const double box[3], const
         case 2: { // top level
             const int t = g.levels - 1;
             up(W.L.charge + g.lv[t].offset, in, g.lv[t].size);
-            f->launches += launch_top(f->stream, g, W.L, W.err);
+            f->launches += W.fft_top.n ? launch_lattice_fft(f->stream, W.fft_top, W.err)
+                                       : launch_top(f->stream, g, W.L, W.err);
             down(out, W.L.pot + g.lv[t].offset, g.lv[t].size);
             break;
         }

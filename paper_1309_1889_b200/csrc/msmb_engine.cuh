@@ -85,6 +85,7 @@ struct Workspace {
     DBuf flush;                          // > L2, written between timed steps
     uint64_t uid = 0;                    // identifies whose stencil is in constant memory
     FftJobs fft{};                       // FFT lattice cutoff plan (msmb_fft.cu)
+    FftJobs fft_top{};                   // FFT top level (n = 0: k_top_direct / k_conv)
     bool lattice_fft = true;             // false: direct stencil (k_lattice)
     Part whole;                          // the whole system (single-GPU path)
     Part part;                           // this field's part of a spatial decomposition (msmb_dd.cu)

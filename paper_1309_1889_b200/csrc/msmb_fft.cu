@@ -222,24 +222,30 @@ __global__ void __launch_bounds__(256) k_fft_z(FftJobs J, int mode, const ErrRec
     }
 }
 
-// the level-k stencil wrapped into B (spectrum precompute): B[dx mod M0][dy mod M1][dz mod M2] = 2^-k K0(dx,dy,dz)
-__global__ void k_fft_stencil(FftJobs J, const int* __restrict__ rowidx, const double* __restrict__ taps, int R,
-                              int TW, int k) {
+// The kernel of job k wrapped into B (spectrum precompute):
+// B[dx mod M0][dy mod M1][dz mod M2] = K(dx, dy, dz) for the offsets a pair of
+// lattice points can have (|d| < dims).  Those wrap to distinct slots: M >= d + R
+// for the cutoff levels, M >= 2d - 1 for the dense top level.  The other offsets
+// would alias (M < 2R + 1 on small levels) and only feed discarded outputs.
+//   cutoff levels: K = 2^-k * level-0 stencil (rowidx / taps, half-width R)
+//   top level:     dense offset table [2d0-1][2d1-1][rowlen] of k_top_direct
+__global__ void k_fft_stencil(FftJobs J, int k, FftKernel K) {
     const FftLevel& lv = J.lv[k];
-    const int W = 2 * R + 1;
-    const int64_t tot = int64_t(W) * W * W;
-    const double sc = ldexp(1.0, -k);
+    const int W0 = 2 * K.R[0] + 1, W1 = 2 * K.R[1] + 1, W2 = 2 * K.R[2] + 1;
+    const int64_t tot = int64_t(W0) * W1 * W2;
     const int M0 = lv.ax[0].M, M1 = lv.ax[1].M, M2 = lv.ax[2].M;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < tot; i += int64_t(gridDim.x) * blockDim.x) {
-        const int dz = int(i % W) - R, dy = int((i / W) % W) - R, dx = int(i / (int64_t(W) * W)) - R;
-        // only offsets a pair of lattice points can have (|d| < dims): those wrap to
-        // distinct slots (M >= d + R), the rest would alias (M < 2R + 1 on small
-        // levels) and only feed discarded outputs
+        const int dz = int(i % W2) - K.R[2], dy = int((i / W2) % W1) - K.R[1], dx = int(i / (int64_t(W2) * W1)) - K.R[0];
         if (abs(dx) >= lv.d[0] || abs(dy) >= lv.d[1] || abs(dz) >= lv.d[2]) continue;
-        const int r = rowidx[(dx + R) * W + (dy + R)];
-        const double v = r >= 0 ? taps[size_t(r) * TW + dz + R] * sc : 0.0;
+        double v;
+        if (K.dense) {
+            v = K.taps[(size_t(dx + K.R[0]) * W1 + (dy + K.R[1])) * K.rowlen + (dz + K.R[2])];
+        } else {
+            const int r = K.rowidx[(dx + K.R[0]) * W1 + (dy + K.R[1])];
+            v = r >= 0 ? K.taps[size_t(r) * K.rowlen + dz + K.R[2]] : 0.0;
+        }
         const int x = (dx + M0) % M0, y = (dy + M1) % M1, z = (dz + M2) % M2;
-        J.buf[lv.boff + (size_t(x) * M1 + y) * M2 + z] = make_double2(v, 0.0);
+        J.buf[lv.boff + (size_t(x) * M1 + y) * M2 + z] = make_double2(v * K.scale, 0.0);
     }
 }
 
@@ -307,12 +313,12 @@ cudaError_t fft_prepare(size_t smem) {
     return e;
 }
 
-int launch_fft_spectrum(cudaStream_t st, FftJobs J, const DevLevels& L, int R, int TW) {
+int launch_fft_spectrum(cudaStream_t st, FftJobs J, const FftKernel* K) {
     int nl = 0;
     for (int k = 0; k < J.n; ++k) {
         const FftLevel& lv = J.lv[k];
         cudaMemsetAsync(J.buf + lv.boff, 0, sizeof(double2) * size_t(lv.ax[0].M) * lv.ax[1].M * lv.ax[2].M, st);
-        k_fft_stencil<<<148, 256, 0, st>>>(J, L.lat_rowidx, L.lat_taps, R, TW, k);
+        k_fft_stencil<<<148, 256, 0, st>>>(J, k, K[k]);
         ++nl;
     }
     const size_t sm = fft_smem(J);

@@ -78,10 +78,18 @@ struct FftJobs {
     double* spec;
     const double2* tw;
 };
+struct FftKernel {       // where the spectrum precompute reads a job's kernel
+    int dense;          // 0: cutoff stencil (rowidx/taps rows), 1: dense top table
+    const int* rowidx;
+    const double* taps;
+    int R[3];           // half-widths of the table
+    int rowlen;         // taps per (dx, dy) row
+    double scale;       // 2^-k for cutoff levels, 1 for the top
+};
 int fft_len(int need);
 FftAxis fft_axis(int M, int tw_off);
 cudaError_t fft_prepare(size_t smem);
-int launch_fft_spectrum(cudaStream_t st, FftJobs J, const DevLevels& L, int R, int TW);
+int launch_fft_spectrum(cudaStream_t st, FftJobs J, const FftKernel* K);
 int launch_lattice_fft(cudaStream_t st, FftJobs J, const ErrRec* err);
 
 struct DevState {       // a device-resident ParticleSystem (SoA)
@@ -121,6 +129,7 @@ int lattice_splits(const Geometry& g);
 bool lattice_const_fits(const Geometry& g);
 cudaError_t lattice_upload_const(const Geometry& g, cudaStream_t st);
 int launch_top(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
+constexpr int64_t kTopFftMin = 4096; // FFT lattice mode: top levels above this many points use an FFT job
 int launch_prolong(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err);
 int launch_interp(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c,
                   DevLevels& L, DevOut& o, ErrRec* err, int want_energy, const Part& P);

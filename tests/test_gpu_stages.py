@@ -124,3 +124,19 @@ def test_cells_bit_exact_including_grid_lines():
     exp_cov = np.all((np.floor(t) >= 1) & (np.floor(t) <= dims[0] - 3), axis=1)
     assert np.array_equal(cov, exp_cov)
     assert cov[100] and cov[101] and not cov[102] and not cov[103]
+
+
+@pytest.mark.parametrize("box,levels", [((219.0, 219.0, 219.0), 4),      # C5 fine: top 17^3 = 4913
+                                        ((120.0, 180.0, 150.0), 3)])     # ragged top
+def test_top_level_fft_large(port, box, levels):
+    # top levels above kTopFftMin points run as a dense FFT convolution (M >= 2d - 1)
+    cfg = pkg.MsmConfig(12.0, 2.5, levels)
+    box = np.array(box)
+    _, dims = level_slices(cfg, box)
+    t = levels - 1
+    m = int(np.prod(dims[t]))
+    assert m > 4096
+    q = np.random.default_rng(3).standard_normal(m)
+    got = pkg.MsmField(cfg).debug_stage(2, t, box, q)
+    ref = port.top_level(box, 12.0, 2.5, levels, q)
+    assert _scale_err(got, ref) <= 1e-13
