@@ -306,6 +306,7 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
         return nullptr;
     }
     ck(conv_prepare(smem), "cudaFuncSetAttribute");
+    ck(top_prepare(g), "cudaFuncSetAttribute");
     DevOut& o = W->o;
     o.fx = walloc<double>(*W, N);
     o.fy = walloc<double>(*W, N);

@@ -375,6 +375,8 @@ struct ListP {
     double colw;     // column width (A)
     int ncx, ncy;
     float cut, cut2;
+    double oz, h;    // level-0 origin z, spacing: z-layer window of a column
+    int d2, cw;      // z-layers, level-0 cells per column side
 };
 
 __device__ __forceinline__ float gapf(float alo, float ahi, float blo, float bhi) {
@@ -393,8 +395,9 @@ constexpr int kListSeg = 128; // group segments longer than this keep column ord
 
 __global__ void __launch_bounds__(256)
     k_pairlist(const int* __restrict__ nclu, const float4* __restrict__ blo,
-               const float4* __restrict__ bhi, const int* __restrict__ col_off, ListP p, int* plist,
-               int* pcnt, int cap, int col_a, int col_b, ErrRec* err) {
+               const float4* __restrict__ bhi, const int* __restrict__ col_off,
+               const int* __restrict__ start, ListP p, int* plist, int* pcnt, int cap, int col_a, int col_b,
+               ErrRec* err) {
     __shared__ int s_seg[8][kListSeg];
     const int ic = col_off[col_a] + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -412,6 +415,13 @@ __global__ void __launch_bounds__(256)
     const int cxi = min(max(int(floor((0.5 * (double(lo.x) + double(hi.x)) - p.ox) / p.colw)), 0), p.ncx - 1);
     const int cyi = min(max(int(floor((0.5 * (double(lo.y) + double(hi.y)) - p.oy) / p.colw)), 0), p.ncy - 1);
     const int DX = max(cxi - cx0, cx1 - cxi), DY = max(cyi - cy0, cy1 - cyi);
+    // z-layers that can hold atoms within the cut (one extra layer each side):
+    // within a column the sorted atoms are ordered by z-layer, so the window is
+    // one atom range per column, i.e. one contiguous range of its clusters
+    const int czA = max(0, int(floor((double(lo.z) - cutd - p.oz) / p.h)) - 1);
+    const int czB = min(p.d2 - 1, int(floor((double(hi.z) + cutd - p.oz) / p.h)) + 1);
+    const int lay = p.cw * p.cw;
+    const int64_t cpc = int64_t(p.d2) * lay;
     int count = 0;
     int* out = plist + size_t(ic) * cap;
     for (int dx = 0; dx <= DX; ++dx)
@@ -432,7 +442,15 @@ __global__ void __launch_bounds__(256)
                     const float gx = gapf(lo.x, hi.x, xlo, xhi), gy = gapf(lo.y, hi.y, ylo, yhi);
                     if (gx * gx + gy * gy < p.cut2) {
                         const int col = cx * p.ncy + cy;
-                        const int j0 = col_off[col], j1 = col_off[col + 1];
+                        int j0 = col_off[col], j1 = col_off[col + 1];
+                        if (j1 - j0 > 64) { // tall column: only the clusters of the z-window
+                            const int a0 = start[int64_t(col) * cpc];
+                            const int aA = start[int64_t(col) * cpc + int64_t(czA) * lay];
+                            const int aB = start[int64_t(col) * cpc + int64_t(czB + 1) * lay];
+                            const int c0 = col_off[col];
+                            j0 = c0 + (aA - a0) / 32;
+                            j1 = aB > aA ? c0 + (aB - 1 - a0) / 32 + 1 : j0;
+                        }
                         for (int jb = j0; jb < j1; jb += 32) {
                             const int jc = jb + lane;
                             bool ok = false;
@@ -723,7 +741,11 @@ int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, 
     lp.ncy = g.ncy;
     lp.cut = float(g.screen_cut);
     lp.cut2 = float(g.screen_cut * g.screen_cut);
-    k_pairlist<<<int((maxclu * 32 + 255) / 256), 256, 0, st>>>(c.nclu, c.blo, c.bhi, c.col_off, lp,
+    lp.oz = g.lv[0].origin[2];
+    lp.h = g.lv[0].spacing;
+    lp.d2 = g.lv[0].dims[2];
+    lp.cw = g.cw;
+    k_pairlist<<<int((maxclu * 32 + 255) / 256), 256, 0, st>>>(c.nclu, c.blo, c.bhi, c.col_off, c.start, lp,
                                                                 c.plist, c.pcnt, cap, P.cx0 * g.ncy,
                                                                 P.cx1 * g.ncy, err);
     return l + 4;
@@ -917,13 +939,21 @@ __global__ void __launch_bounds__(kRTx * kRTy * kRTz)
     const int bz = blockIdx.x % tz_n, by = (blockIdx.x / tz_n) % ty_n, bx = blockIdx.x / (tz_n * ty_n);
     const int I0 = bx * kRTx, J0 = by * kRTy, K0 = bz * kRTz;
     const int fi0 = 2 * I0 - 5, fj0 = 2 * J0 - 5, fk0 = 2 * K0 - 5;
-    for (int e = threadIdx.x; e < kRFx * kRFy * kRFz; e += blockDim.x) {
-        const int kk = e % kRFz, jj = (e / kRFz) % kRFy, ii = e / (kRFz * kRFy);
-        const int i = fi0 + ii, j = fj0 + jj, k = fk0 + kk;
-        double v = 0.0;
-        if (i >= 0 && i < p.fd[0] && j >= 0 && j < p.fd[1] && k >= 0 && k < p.fd[2])
-            v = fine[(size_t(i) * p.fd[1] + j) * p.fd[2] + k];
-        tile[e] = v;
+    constexpr int kTile = kRFx * kRFy * kRFz;
+    for (int e0 = threadIdx.x; e0 < kTile; e0 += 8 * blockDim.x) { // 8 independent loads in flight
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * blockDim.x;
+            const int kk = e % kRFz, jj = (e / kRFz) % kRFy, ii = e / (kRFz * kRFy);
+            const int i = fi0 + ii, j = fj0 + jj, k = fk0 + kk;
+            v[u] = (e < kTile && i >= 0 && i < p.fd[0] && j >= 0 && j < p.fd[1] && k >= 0 && k < p.fd[2])
+                       ? fine[(size_t(i) * p.fd[1] + j) * p.fd[2] + k]
+                       : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (e0 + u * blockDim.x < kTile) tile[e0 + u * blockDim.x] = v[u];
     }
     __syncthreads();
     const int tz = threadIdx.x % kRTz, ty = (threadIdx.x / kRTz) % kRTy, tx = threadIdx.x / (kRTz * kRTy);
@@ -945,18 +975,31 @@ __global__ void __launch_bounds__(kRTx * kRTy * kRTz)
             lz[c] = c < nk ? p.ridx[2][K * kRestrictMax + c] - fk0 : 0;
             wz[c] = c < nk ? p.rw[2][K * kRestrictMax + c] : 0.0;
         }
-        double acc = 0.0;
-        for (int a = 0; a < ni; ++a) {
-            const int li = p.ridx[0][I * kRestrictMax + a] - fi0;
-            double accb = 0.0;
-            for (int b = 0; b < nj; ++b) {
-                const double* row = tile + (li * kRFy + (p.ridx[1][J * kRestrictMax + b] - fj0)) * kRFz;
-                double accc = 0.0;
+        // all table entries up front (independent loads), zero weights pad to kRestrictMax
+        int lx[kRestrictMax], ly[kRestrictMax];
+        double wx[kRestrictMax], wy[kRestrictMax];
 #pragma unroll
-                for (int c = 0; c < kRestrictMax; ++c) accc = fma(wz[c], row[lz[c]], accc); // wz = 0 pads
-                accb = fma(p.rw[1][J * kRestrictMax + b], accc, accb);
+        for (int c = 0; c < kRestrictMax; ++c) {
+            lx[c] = c < ni ? p.ridx[0][I * kRestrictMax + c] - fi0 : 0;
+            wx[c] = c < ni ? p.rw[0][I * kRestrictMax + c] : 0.0;
+            ly[c] = c < nj ? p.ridx[1][J * kRestrictMax + c] - fj0 : 0;
+            wy[c] = c < nj ? p.rw[1][J * kRestrictMax + c] : 0.0;
+        }
+        double acc = 0.0;
+#pragma unroll 1
+        for (int a = 0; a < ni; ++a) {
+            double accb = 0.0;
+#pragma unroll
+            for (int b = 0; b < kRestrictMax; ++b) {
+                if (b < nj) {
+                    const double* row = tile + (lx[a] * kRFy + ly[b]) * kRFz;
+                    double accc = 0.0;
+#pragma unroll
+                    for (int c = 0; c < kRestrictMax; ++c) accc = fma(wz[c], row[lz[c]], accc); // wz = 0 pads
+                    accb = fma(wy[b], accc, accb);
+                }
             }
-            acc = fma(p.rw[0][I * kRestrictMax + a], accb, acc);
+            acc = fma(wx[a], accb, acc);
         }
         v = acc;
     }
@@ -1018,10 +1061,65 @@ int launch_restrict(cudaStream_t st, const Geometry& g, int k, DevLevels& L, Err
     return 1;
 }
 
+// Prolongation by fine tiles of 4 x 8 x 8 points: the coarse window they read
+// (base .. base + 3 per axis, monotone in the fine index) is staged in shared
+// memory, then each point forms the reference's nested sums (prolong_point order).
+constexpr int kPx = 4, kPy = 8, kPz = 8;
+constexpr int kPCx = kPx / 2 + 5, kPCy = kPy / 2 + 5, kPCz = kPz / 2 + 5;
+
+__global__ void __launch_bounds__(kPx * kPy * kPz)
+    k_prolong_tile(XferP p, const double* __restrict__ coarse, double* fine, const ErrRec* err) {
+    __shared__ double ct[kPCx * kPCy * kPCz];
+    if (failed(err)) return;
+    const int tz_n = (p.fd[2] + kPz - 1) / kPz, ty_n = (p.fd[1] + kPy - 1) / kPy;
+    const int bz = blockIdx.x % tz_n, by = (blockIdx.x / tz_n) % ty_n, bx = blockIdx.x / (tz_n * ty_n);
+    const int I0 = bx * kPx, J0 = by * kPy, K0 = bz * kPz;
+    const int I1 = min(I0 + kPx, p.fd[0]) - 1, J1 = min(J0 + kPy, p.fd[1]) - 1, K1 = min(K0 + kPz, p.fd[2]) - 1;
+    const int cx0 = p.base[0][I0], cy0 = p.base[1][J0], cz0 = p.base[2][K0];
+    const int nx = p.base[0][I1] + 4 - cx0, ny = p.base[1][J1] + 4 - cy0, nz = p.base[2][K1] + 4 - cz0;
+    if (nx > kPCx || ny > kPCy || nz > kPCz) { // not expected (base ~ i/2); stay exact without staging
+        const int tz = threadIdx.x % kPz, ty = (threadIdx.x / kPz) % kPy, tx = threadIdx.x / (kPz * kPy);
+        if (I0 + tx <= I1 && J0 + ty <= J1 && K0 + tz <= K1)
+            prolong_point(p, coarse, fine, (int64_t(I0 + tx) * p.fd[1] + (J0 + ty)) * p.fd[2] + (K0 + tz));
+        return;
+    }
+    for (int e = threadIdx.x; e < nx * ny * nz; e += blockDim.x) {
+        const int c = e % nz, b = (e / nz) % ny, a = e / (nz * ny);
+        ct[e] = coarse[(size_t(cx0 + a) * p.cd[1] + (cy0 + b)) * p.cd[2] + (cz0 + c)];
+    }
+    __syncthreads();
+    const int tz = threadIdx.x % kPz, ty = (threadIdx.x / kPz) % kPy, tx = threadIdx.x / (kPz * kPy);
+    const int i = I0 + tx, j = J0 + ty, k = K0 + tz;
+    if (i > I1 || j > J1 || k > K1) return;
+    const int ox = p.base[0][i] - cx0, oy = p.base[1][j] - cy0, oz = p.base[2][k] - cz0;
+    const double* wx = p.w[0] + 4 * i;
+    const double* wy = p.w[1] + 4 * j;
+    const double* wz = p.w[2] + 4 * k;
+    double x4[4], y4[4], z4[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) x4[t] = wx[t], y4[t] = wy[t], z4[t] = wz[t];
+    double acc = 0.0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        double accb = 0.0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const double* row = ct + ((ox + a) * ny + (oy + b)) * nz + oz;
+            double accc = 0.0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) accc = __dadd_rn(accc, __dmul_rn(z4[c], row[c]));
+            accb = __dadd_rn(accb, __dmul_rn(y4[b], accc));
+        }
+        acc = __dadd_rn(acc, __dmul_rn(x4[a], accb));
+    }
+    const size_t idx = (size_t(i) * p.fd[1] + j) * p.fd[2] + k;
+    fine[idx] = __dadd_rn(fine[idx], acc);
+}
+
 int launch_prolong(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err) {
-    const int64_t m = int64_t(g.lv[k].size);
-    k_prolong<<<int((m + 127) / 128), 128, 0, st>>>(make_xfer(g, k, L), L.pot + g.lv[k + 1].offset,
-                                                    L.pot + g.lv[k].offset, err);
+    const XferP p = make_xfer(g, k, L);
+    const int blocks = ((p.fd[0] + kPx - 1) / kPx) * ((p.fd[1] + kPy - 1) / kPy) * ((p.fd[2] + kPz - 1) / kPz);
+    k_prolong_tile<<<blocks, kPx * kPy * kPz, 0, st>>>(p, L.pot + g.lv[k + 1].offset, L.pot + g.lv[k].offset, err);
     return 1;
 }
 
@@ -1485,11 +1583,70 @@ __global__ void __launch_bounds__(128)
 
 constexpr int64_t kTopDirectMax = 8192; // top levels up to this many points use k_top_direct
 
+// k_top_direct with the offset table and the charges staged in shared memory (when
+// they fit): the same sequential sum per point, without global-load latency in its
+// dependent chain.
+__global__ void __launch_bounds__(128)
+    k_top_direct_smem(const double* __restrict__ q, double* u, int d0, int d1, int d2,
+                      const double* __restrict__ taps, int rowlen, const ErrRec* err) {
+    extern __shared__ double sh[];
+    if (failed(err)) return;
+    const int m = d0 * d1 * d2;
+    const int ntab = (2 * d0 - 1) * (2 * d1 - 1) * rowlen;
+    double* st = sh;
+    double* sq = sh + ntab;
+    for (int i0 = threadIdx.x; i0 < ntab + m; i0 += 8 * blockDim.x) { // 8 independent loads in flight
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * blockDim.x;
+            v[u] = i < ntab ? taps[i] : (i < ntab + m ? q[i - ntab] : 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (i0 + u * blockDim.x < ntab + m) sh[i0 + u * blockDim.x] = v[u];
+    }
+    __syncthreads();
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= m) return;
+    const int z = idx % d2, y = (idx / d2) % d1, x = idx / (d2 * d1);
+    const int Rx = d0 - 1, Ry = d1 - 1, Rz = d2 - 1;
+    double acc = 0.0;
+    for (int xs = 0; xs < d0; ++xs)
+        for (int ys = 0; ys < d1; ++ys) {
+            const double* trow = st + ((x - xs + Rx) * (2 * Ry + 1) + (y - ys + Ry)) * rowlen + (z + Rz);
+            const double* qrow = sq + (xs * d1 + ys) * d2;
+#pragma unroll 8
+            for (int zs = 0; zs < d2; ++zs) acc = __dadd_rn(acc, __dmul_rn(trow[-zs], qrow[zs]));
+        }
+    u[idx] = acc;
+}
+
+size_t top_smem_bytes(const Geometry& g) {
+    const LevelGeom& lv = g.lv[g.levels - 1];
+    const int rowlen = (2 * g.top.Rz + 1 + kConvL - 1) / kConvL * kConvL;
+    return sizeof(double) * (size_t(2 * lv.dims[0] - 1) * (2 * lv.dims[1] - 1) * rowlen + lv.size);
+}
+
+cudaError_t top_prepare(const Geometry& g) {
+    const size_t b = top_smem_bytes(g);
+    if (b > 220 * 1024) return cudaSuccess;
+    return cudaFuncSetAttribute(k_top_direct_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(std::max<size_t>(b, 48 * 1024)));
+}
+
 int launch_top(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err) {
     const int k = g.levels - 1;
     const LevelGeom& lv = g.lv[k];
     if (int64_t(lv.size) <= kTopDirectMax) {
         const int rowlen = (2 * g.top.Rz + 1 + kConvL - 1) / kConvL * kConvL;
+        const size_t sb = top_smem_bytes(g);
+        if (sb <= 220 * 1024) {
+            k_top_direct_smem<<<int((lv.size + 127) / 128), 128, sb, st>>>(L.charge + lv.offset, L.pot + lv.offset,
+                                                                           lv.dims[0], lv.dims[1], lv.dims[2],
+                                                                           L.taps[k], rowlen, err);
+            return 1;
+        }
         k_top_direct<<<int((lv.size + 127) / 128), 128, 0, st>>>(L.charge + lv.offset, L.pot + lv.offset,
                                                                  lv.dims[0], lv.dims[1], lv.dims[2],
                                                                  L.taps[k], rowlen, err);

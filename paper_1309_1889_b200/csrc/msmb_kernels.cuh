@@ -129,6 +129,7 @@ int lattice_splits(const Geometry& g);
 bool lattice_const_fits(const Geometry& g);
 cudaError_t lattice_upload_const(const Geometry& g, cudaStream_t st);
 int launch_top(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
+cudaError_t top_prepare(const Geometry& g); // dynamic smem of the staged direct top kernel
 constexpr int64_t kTopFftMin = 4096; // FFT lattice mode: top levels above this many points use an FFT job
 int launch_prolong(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err);
 int launch_interp(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c,
