@@ -117,7 +117,7 @@ struct msmb_field {
     msmb_units units{};
     int device = 0;
     cudaStream_t stream = nullptr;
-    cudaStream_t side = nullptr;             // long-range chain, forked from `stream` (higher priority)
+    cudaStream_t side = nullptr;             // long-range chain, forked from `stream`
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     std::recursive_mutex mu;
     std::unique_ptr<msmb::Workspace> ws;

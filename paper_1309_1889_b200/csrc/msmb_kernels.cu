@@ -780,12 +780,13 @@ int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& 
 }
 
 // ============================================================================
-// K3: anterpolation as an owner-computes gather (no atomics): a thread owns 4
-// consecutive level-0 points along z and sums the contributions of the particles
-// in the cells whose stencils reach them, in a fixed order (cells in x, y, z
-// order, particles in sorted order), using the per-particle weights of k_gather:
+// K3: anterpolation as an owner-computes gather (no atomics).  16 lanes own a quad
+// of 4 consecutive level-0 points along z; lane (ox, oy) sums the contributions
+// of the particles in its cell column (cells along z in order, particles in
+// sorted order), using the per-particle weights of k_gather:
 // q_mu += ((q*wx[dx]) * wy[dy]) * wz[dz]  (the reference's qa/qab products,
-// src/msm_phases.cpp:52-57).  One weight fetch serves up to 4 points.
+// src/msm_phases.cpp:52-57), and a fixed xor-shuffle tree adds the 16 lanes.
+// One weight fetch serves up to 4 points; the 7 cell ranges are fetched up front.
 // ============================================================================
 constexpr int kAQ = 4; // points per thread along z
 
@@ -795,11 +796,11 @@ __global__ void __launch_bounds__(128)
     if (failed(err)) return;
     const int d0 = p.d[0], d1 = p.d[1], d2 = p.d[2];
     const int nzq = (d2 + kAQ - 1) / kAQ;
-    // 4 lanes per quad of points, one cell column offset (ox) each; partial sums
-    // are combined by a fixed shuffle tree ((ox0 + ox1) + (ox2 + ox3))
+    // 16 lanes per quad of points, one cell column (ox, oy) each; the partial sums
+    // are combined by a fixed xor-shuffle tree over the 16 lanes
     const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int ox = int(tid & 3);
-    const int64_t idx = tid >> 2;
+    const int ox = int(tid & 3), oy = int((tid >> 2) & 3);
+    const int64_t idx = tid >> 4;
     const bool live = idx < int64_t(x_end - x_begin) * d1 * nzq;
     const int zq = live ? int(idx % nzq) : 0;
     const int y = live ? int((idx / nzq) % d1) : 0;
@@ -808,31 +809,31 @@ __global__ void __launch_bounds__(128)
     double acc[kAQ];
 #pragma unroll
     for (int k = 0; k < kAQ; ++k) acc[k] = 0.0;
-    const int cx = x - 2 + ox;
-    if (live && cx >= 1 && cx <= d0 - 3) {
-        const int dxw = 3 - ox; // weight index x - base = x - (cx - 1)
-        for (int oy = 0; oy < 4; ++oy) {
-            const int cy = y - 2 + oy;
-            if (cy < 1 || cy > d1 - 3) continue;
-            const int dyw = 4 + 3 - oy;
-            const int2* row = nat + (size_t(cx) * d1 + cy) * d2;
-            // cells cz = z0 - 2 + u, u = 0 .. kAQ + 2, reach points z0 + k with dz = k - u + 3
+    const int cx = x - 2 + ox, cy = y - 2 + oy;
+    if (live && cx >= 1 && cx <= d0 - 3 && cy >= 1 && cy <= d1 - 3) {
+        const int dxw = 3 - ox;     // weight index x - base = x - (cx - 1)
+        const int dyw = 4 + 3 - oy;
+        const int2* row = nat + (size_t(cx) * d1 + cy) * d2;
+        // cells cz = z0 - 2 + u, u = 0 .. kAQ + 2, reach points z0 + k with dz = k - u + 3;
+        // all ranges fetched up front (independent loads)
+        int2 rg[kAQ + 3];
 #pragma unroll
-            for (int u = 0; u < kAQ + 3; ++u) {
-                const int cz = z0 - 2 + u;
-                if (cz < 1 || cz > d2 - 3) continue;
-                const int2 r = __ldg(row + cz);
-                for (int s = r.x; s < r.y; ++s) {
-                    const double* w = aw + size_t(s) * 12;
-                    const double cxy = __dmul_rn(__ldg(w + dxw), __ldg(w + dyw));
-                    const double2 wz01 = __ldg(reinterpret_cast<const double2*>(w + 8));
-                    const double2 wz23 = __ldg(reinterpret_cast<const double2*>(w + 10));
-                    const double wzv[4] = {wz01.x, wz01.y, wz23.x, wz23.y};
+        for (int u = 0; u < kAQ + 3; ++u) {
+            const int cz = z0 - 2 + u;
+            rg[u] = (cz >= 1 && cz <= d2 - 3) ? __ldg(row + cz) : make_int2(0, 0);
+        }
 #pragma unroll
-                    for (int k = 0; k < kAQ; ++k) {
-                        const int dz = k - u + 3;
-                        if (dz >= 0 && dz <= 3) acc[k] = fma(cxy, wzv[dz], acc[k]);
-                    }
+        for (int u = 0; u < kAQ + 3; ++u) {
+            for (int s = rg[u].x; s < rg[u].y; ++s) {
+                const double* w = aw + size_t(s) * 12;
+                const double cxy = __dmul_rn(__ldg(w + dxw), __ldg(w + dyw));
+                const double2 wz01 = __ldg(reinterpret_cast<const double2*>(w + 8));
+                const double2 wz23 = __ldg(reinterpret_cast<const double2*>(w + 10));
+                const double wzv[4] = {wz01.x, wz01.y, wz23.x, wz23.y};
+#pragma unroll
+                for (int k = 0; k < kAQ; ++k) {
+                    const int dz = k - u + 3;
+                    if (dz >= 0 && dz <= 3) acc[k] = fma(cxy, wzv[dz], acc[k]);
                 }
             }
         }
@@ -841,8 +842,10 @@ __global__ void __launch_bounds__(128)
     for (int k = 0; k < kAQ; ++k) {
         acc[k] += __shfl_xor_sync(FULLMASK, acc[k], 1);
         acc[k] += __shfl_xor_sync(FULLMASK, acc[k], 2);
+        acc[k] += __shfl_xor_sync(FULLMASK, acc[k], 4);
+        acc[k] += __shfl_xor_sync(FULLMASK, acc[k], 8);
     }
-    if (!live || ox != 0) return;
+    if (!live || (tid & 15) != 0) return;
     double* out = q0 + (size_t(x) * d1 + y) * d2;
 #pragma unroll
     for (int k = 0; k < kAQ; ++k)
@@ -852,7 +855,7 @@ __global__ void __launch_bounds__(128)
 int launch_anterp(cudaStream_t st, const Geometry& g, DevAtoms& a, DevCells& c, DevLevels& L,
                   ErrRec* err, const Part& P) {
     const BinP p = make_binp(g);
-    const int64_t m = 4 * int64_t(P.pl1[0] - P.pl0[0]) * p.d[1] * ((p.d[2] + kAQ - 1) / kAQ);
+    const int64_t m = 16 * int64_t(P.pl1[0] - P.pl0[0]) * p.d[1] * ((p.d[2] + kAQ - 1) / kAQ);
     if (m == 0) return 0;
     k_anterp<<<int((m + 127) / 128), 128, 0, st>>>(p, c.nat, a.aw, L.charge + g.lv[0].offset, P.pl0[0],
                                                    P.pl1[0], err);
