@@ -336,6 +336,7 @@ class DeviceSystem:
         self.field = field
         self.n = s.size()
         self.box = s.box.copy()
+        field._last_box = self.box  # debug_levels reads the lattices of this box
         self._h = C.c_void_p()
         rc = _native.lib().msmb_system_create(field.handle, self.n, _p(s.positions), _p(s.velocities),
                                               _p(s.charges), _p(s.masses), _p(s.box), C.byref(self._h))
