@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--workload", default="step", choices=["step", "spatial", "parareal"],
+                    help="step: the contract line (C2-S); spatial / parareal: the multi-GPU paths "
+                         "(tools/bench_paths.py)")
     return ap.parse_args()
 
 
@@ -204,6 +207,12 @@ def main():
     args = parse()
     D = Dist()
     from paper_1309_1889_b200 import fixtures as fx
+    if args.workload != "step" and args.impl == "ours":
+        sys.path.insert(0, str(ROOT / "tools"))
+        import bench_paths
+        bench_paths.run(args, D, METRIC, UNIT)
+        D.close()
+        return
 
     name = args.config
     wname = {"c5f": "c5"}.get(name, name)

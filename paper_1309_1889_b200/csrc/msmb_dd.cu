@@ -77,9 +77,11 @@ int phase0(msmb_field* f, Workspace& W, DevState& s, long long* xbuf) {
         record_counters(f, W, r);
         // binning, sorting and error detection are replicated: every part fails alike
         if (r.kind) return engine_set_error(f, error_from_rec(r));
-        const LevelGeom& l0 = g.lv[0];
-        f->launches += launch_fill_i64(st, xbuf, int64_t(l0.size), LLONG_MIN);
-        export_planes(st, g, W.part, 0, W.L.charge, xbuf);
+        if (W.part.nparts > 1) { // one part: the charges stay where phase 1 reads them
+            const LevelGeom& l0 = g.lv[0];
+            f->launches += launch_fill_i64(st, xbuf, int64_t(l0.size), LLONG_MIN);
+            export_planes(st, g, W.part, 0, W.L.charge, xbuf);
+        }
         ckd(cudaStreamSynchronize(st), "sync");
         return MSMB_OK;
     }
@@ -89,13 +91,16 @@ int phase0(msmb_field* f, Workspace& W, DevState& s, long long* xbuf) {
 int phase1(msmb_field* f, Workspace& W, const long long* xin, long long* xbuf) {
     const Geometry& g = W.g;
     cudaStream_t st = f->stream;
-    ckd(cudaMemcpyAsync(W.L.charge, xin, sizeof(double) * g.lv[0].size, cudaMemcpyDeviceToDevice, st), "D2D");
+    const bool x = W.part.nparts > 1;
+    if (x) ckd(cudaMemcpyAsync(W.L.charge, xin, sizeof(double) * g.lv[0].size, cudaMemcpyDeviceToDevice, st), "D2D");
     ensure_const_table(f, W);
     f->launches += launch_restrict_all(st, g, W.L, W.err);
     // the FFT path transforms whole levels (replicated); the direct path only owned planes
     f->launches += W.lattice_fft ? launch_lattice_fft(st, W.fft, W.err) : launch_lattice(st, g, W.L, W.err, W.part);
-    f->launches += launch_fill_i64(st, xbuf, int64_t(g.lattice_total), LLONG_MIN);
-    for (int k = 0; k + 1 < g.levels; ++k) export_planes(st, g, W.part, k, W.L.pot, xbuf);
+    if (x) {
+        f->launches += launch_fill_i64(st, xbuf, int64_t(g.lattice_total), LLONG_MIN);
+        for (int k = 0; k + 1 < g.levels; ++k) export_planes(st, g, W.part, k, W.L.pot, xbuf);
+    }
     ckd(cudaGetLastError(), "kernel launch");
     ckd(cudaStreamSynchronize(st), "sync");
     return MSMB_OK;
@@ -105,7 +110,8 @@ int phase2(msmb_field* f, Workspace& W, DevState& s, const long long* xin, long 
            int drift, double conv, double* energy) {
     const Geometry& g = W.g;
     cudaStream_t st = f->stream;
-    ckd(cudaMemcpyAsync(W.L.pot, xin, sizeof(double) * g.lattice_total, cudaMemcpyDeviceToDevice, st), "D2D");
+    const bool x = W.part.nparts > 1;
+    if (x) ckd(cudaMemcpyAsync(W.L.pot, xin, sizeof(double) * g.lattice_total, cudaMemcpyDeviceToDevice, st), "D2D");
     f->launches += W.fft_top.n ? launch_lattice_fft(st, W.fft_top, W.err) : launch_top(st, g, W.L, W.err);
     f->launches += launch_prolong_all(st, g, W.L, W.err);
     DevOut o = W.o;
@@ -113,8 +119,10 @@ int phase2(msmb_field* f, Workspace& W, DevState& s, const long long* xin, long 
     if (s.n) ckd(cudaMemsetAsync(o.e, 0, sizeof(double) * size_t(s.n), st), "memset"); // unowned e_i = 0
     f->launches += launch_interp(st, g, s.n, W.a, W.c, W.L, o, W.err, 1, W.part);
     f->launches += launch_verlet_part(st, g, W.c, W.a, s, o, dt, conv, kicks, drift, W.part, W.err);
-    f->launches += launch_fill_i64(st, xbuf, 6 * s.n, LLONG_MIN);
-    f->launches += launch_export_state(st, g, W.c, W.a, s, xbuf, W.part);
+    if (x) {
+        f->launches += launch_fill_i64(st, xbuf, 6 * s.n, LLONG_MIN);
+        f->launches += launch_export_state(st, g, W.c, W.a, s, xbuf, W.part);
+    }
     ckd(cudaGetLastError(), "kernel launch");
     double e = 0.0;
     if (s.n) ckd(cudaMemcpyAsync(&e, W.o.energy, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
@@ -123,8 +131,8 @@ int phase2(msmb_field* f, Workspace& W, DevState& s, const long long* xin, long 
     return MSMB_OK;
 }
 
-int phase3(msmb_field* f, DevState& s, const long long* xbuf) {
-    if (s.n)
+int phase3(msmb_field* f, Workspace& W, DevState& s, const long long* xbuf) {
+    if (s.n && W.part.nparts > 1)
         ckd(cudaMemcpyAsync(s.x, xbuf, sizeof(double) * 6 * size_t(s.n), cudaMemcpyDeviceToDevice, f->stream),
             "D2D");
     ckd(cudaStreamSynchronize(f->stream), "sync");
@@ -210,7 +218,7 @@ extern "C" int msmb_dd_phase(msmb_field* f, msmb_system* sys, int phase, double 
             case 0: return phase0(f, W, s, xo);
             case 1: return phase1(f, W, xi, xo);
             case 2: return phase2(f, W, s, xi, xo, dt, kicks, drift, u.energy_to_native, energy);
-            case 3: return phase3(f, s, xi);
+            case 3: return phase3(f, W, s, xi);
             default: return engine_set_error(f, Error{MSMB_ERR_CONFIG, -1, -1, -1, "invalid phase"});
         }
     } catch (const std::exception& ex) {

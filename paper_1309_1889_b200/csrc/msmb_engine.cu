@@ -501,9 +501,16 @@ static void ensure_graphs(msmb_field* f, Workspace& W, DevState& s, double dt, d
 
 template <class Fn>
 static cudaGraphExec_t capture(msmb_field* f, Fn&& fn) {
-    cudaGraph_t graph;
+    cudaGraph_t graph = nullptr;
     ck(cudaStreamBeginCapture(f->stream, cudaStreamCaptureModeThreadLocal), "BeginCapture");
-    fn();
+    try {
+        fn();
+    } catch (...) { // never leave the stream (and this thread) in capture mode
+        cudaStreamEndCapture(f->stream, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        throw;
+    }
     ck(cudaStreamEndCapture(f->stream, &graph), "EndCapture");
     cudaGraphExec_t ex;
     ck(cudaGraphInstantiateWithFlags(&ex, graph, cudaGraphInstantiateFlagUseNodePriority),

@@ -306,10 +306,9 @@ FftAxis fft_axis(int M, int tw_off) {
 }
 
 cudaError_t fft_prepare(size_t smem) {
-    const int b = int(std::max<size_t>(smem, 48 * 1024));
-    cudaError_t e = cudaFuncSetAttribute(k_fft_x, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fft_y, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fft_z, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaError_t e = smem_grow(reinterpret_cast<const void*>(k_fft_x), smem);
+    if (e == cudaSuccess) e = smem_grow(reinterpret_cast<const void*>(k_fft_y), smem);
+    if (e == cudaSuccess) e = smem_grow(reinterpret_cast<const void*>(k_fft_z), smem);
     return e;
 }
 

@@ -26,9 +26,27 @@
 #include <cmath>
 #include <cstdint>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "msmb_kernels.cuh"
 
 namespace msmb {
+
+cudaError_t smem_grow(const void* func, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> cur;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const size_t want = std::max<size_t>(bytes, 48 * 1024);
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& have = cur[{dev, func}];
+    if (want <= have) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, int(want));
+    if (e == cudaSuccess) have = want;
+    return e;
+}
 
 #define FULLMASK 0xffffffffu
 
@@ -1278,11 +1296,9 @@ size_t conv_smem_bytes(const ConvTable& t) {
 
 cudaError_t conv_prepare(size_t bytes) {
     const int b = int(std::max<size_t>(bytes, 48 * 1024));
-    cudaError_t e = cudaFuncSetAttribute(k_conv<kConvB, kConvL, kConvNWZ>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaError_t e = smem_grow(reinterpret_cast<const void*>(k_conv<kConvB, kConvL, kConvNWZ>), size_t(b));
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_conv<kConvBSmall, kConvL, kConvNWZ>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    return smem_grow(reinterpret_cast<const void*>(k_conv<kConvBSmall, kConvL, kConvNWZ>), size_t(b));
 }
 
 static int launch_conv_jobs(cudaStream_t st, ConvJobs& J, int blocks, bool big, const ErrRec* err) {
@@ -1473,11 +1489,9 @@ size_t lattice_smem_bytes(const Geometry& g) {
 }
 
 cudaError_t lattice_prepare(size_t bytes) {
-    cudaError_t e = cudaFuncSetAttribute(k_lattice<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(std::max<size_t>(bytes, 48 * 1024)));
+    cudaError_t e = smem_grow(reinterpret_cast<const void*>(k_lattice<true>), bytes);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_lattice<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(std::max<size_t>(bytes, 48 * 1024)));
+    return smem_grow(reinterpret_cast<const void*>(k_lattice<false>), bytes);
 }
 
 bool lattice_const_fits(const Geometry& g) {
@@ -1634,8 +1648,7 @@ size_t top_smem_bytes(const Geometry& g) {
 cudaError_t top_prepare(const Geometry& g) {
     const size_t b = top_smem_bytes(g);
     if (b > 220 * 1024) return cudaSuccess;
-    return cudaFuncSetAttribute(k_top_direct_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(std::max<size_t>(b, 48 * 1024)));
+    return smem_grow(reinterpret_cast<const void*>(k_top_direct_smem), b);
 }
 
 int launch_top(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err) {

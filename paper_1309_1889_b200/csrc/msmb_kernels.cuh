@@ -86,6 +86,10 @@ struct FftKernel {       // where the spectrum precompute reads a job's kernel
     int rowlen;         // taps per (dx, dy) row
     double scale;       // 2^-k for cutoff levels, 1 for the top
 };
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is process-wide per device:
+// fields with different geometries share the kernels, so the limit only ever grows
+// (a smaller workspace must not lower what a larger one's launches need).
+cudaError_t smem_grow(const void* func, size_t bytes);
 int fft_len(int need);
 FftAxis fft_axis(int M, int tw_off);
 cudaError_t fft_prepare(size_t smem);

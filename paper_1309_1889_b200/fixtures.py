@@ -108,9 +108,11 @@ def config(name: str, seed: int | None = None, n_override: int | None = None) ->
     c2    : configs[1] literal (100,000 waters in a 144 A cube, a=12 h=2.5 l=6, dt 1 fs x 100)
     c2s   : c2 survivable variant (O-O min-sep 2.5 A, dt 0.02 fs)
     c3    : configs[2] (2^24 atoms, 551 A, rebalanced +-1, a=12 h=2.5 l=4, dt 2 fs x 20)
+    c3s   : c3 survivable variant (RSA min-sep 1.5 A, dt 0.02 fs)
     c4    : configs[3] (water slab 300x650x650 A, a=12 h=2.5 l=5, dt 2 fs x 20)
     c5    : configs[4] (2^20 atoms, 219 A, random_neutral; F a=12 h=2.5 l=4 dt .5 x100,
             G a=8 h=5 l=3 dt 2 x25; 8 slices)
+    c5s   : c5 survivable parareal variant (RSA min-sep 1.5 A, F dt 0.005 x100, G dt 0.02 x25)
     n_override scales N down at fixed density (for parity tests at oracle-friendly sizes).
     """
     base = name.rstrip("s") if name.endswith("s") and name[:-1] in ("c1", "c2") else name
@@ -132,16 +134,18 @@ def config(name: str, seed: int | None = None, n_override: int | None = None) ->
         pos, q, mass = water(nm, box, 2.5 if surv else 0.0, seed)
         vel = maxwell_boltzmann(mass, 300.0, seed + 1)
         return Workload(name, pos, vel, q, mass, box, 12.0, 2.5, 6, 0.02 if surv else 1.0, 100)
-    if base == "c3":
+    if base in ("c3", "c3s"):
+        # c3s: survivable variant (RSA min-sep 1.5 A, dt 0.02 fs) for multi-step runs
+        surv = base == "c3s"
         seed = 3309 if seed is None else seed
         n = 1 << 24 if n_override is None else n_override
         L = 551.0 * (n / (1 << 24)) ** (1 / 3)
         box = np.array([L, L, L])
-        pos, _ = uniform(n, box, "all_plus_one", 0.0, seed)
+        pos, _ = uniform(n, box, "all_plus_one", 1.5 if surv else 0.0, seed)
         q = rebalanced_charges(n, seed + 2)
         mass = np.full(n, 18.0)
         vel = maxwell_boltzmann(mass, 300.0, seed + 1)
-        return Workload(name, pos, vel, q, mass, box, 12.0, 2.5, 4, 2.0, 20)
+        return Workload(name, pos, vel, q, mass, box, 12.0, 2.5, 4, 0.02 if surv else 2.0, 20)
     if base == "c4":
         seed = 4309 if seed is None else seed
         nm = 4_225_000 if n_override is None else max(1, n_override // 3)
@@ -150,15 +154,19 @@ def config(name: str, seed: int | None = None, n_override: int | None = None) ->
         pos, q, mass = water(nm, box, 0.0, seed)
         vel = maxwell_boltzmann(mass, 300.0, seed + 1)
         return Workload(name, pos, vel, q, mass, box, 12.0, 2.5, 5, 2.0, 20)
-    if base == "c5":
+    if base in ("c5", "c5s"):
+        # c5s: survivable variant for parareal runs: RSA min-sep 1.5 A,
+        # fine dt 0.005 fs x 100, coarse dt 0.02 fs x 25 (slice span 0.5 fs, 8 slices)
+        surv = base == "c5s"
         seed = 5309 if seed is None else seed
         n = 1 << 20 if n_override is None else n_override
         L = 219.0 * (n / (1 << 20)) ** (1 / 3)
         box = np.array([L, L, L])
-        pos, q = uniform(n, box, "random_neutral", 0.0, seed)
+        pos, q = uniform(n, box, "random_neutral", 1.5 if surv else 0.0, seed)
         mass = np.full(n, 18.0)
         vel = maxwell_boltzmann(mass, 300.0, seed + 1)
-        w = Workload(name, pos, vel, q, mass, box, 12.0, 2.5, 4, 0.5, 100)
-        w.extra = dict(coarse=(8.0, 5.0, 3, 2.0, 25), fine=(12.0, 2.5, 4, 0.5, 100), slices=8)
+        fdt, gdt = (0.005, 0.02) if surv else (0.5, 2.0)
+        w = Workload(name, pos, vel, q, mass, box, 12.0, 2.5, 4, fdt, 100)
+        w.extra = dict(coarse=(8.0, 5.0, 3, gdt, 25), fine=(12.0, 2.5, 4, fdt, 100), slices=8)
         return w
     raise ValueError(name)

@@ -436,11 +436,12 @@ class SpatialDecomposition:
         for f, ds, _ in self.parts:
             _check(f.handle, self.lib.msmb_system_set_state_device(ds._h, C.c_void_p(t.data_ptr())))
 
-    def propagate(self, dt: float, steps: int):
+    def propagate(self, dt: float, steps: int, download: bool = True):
         """propagate(spec, s, units) (src/integrate.cpp:13-36): one evaluation, then
         `steps` velocity-Verlet steps. Returns (final ParticleSystem, energy of the
-        last evaluation). On error the state is left as it was, and the
-        reference's exception is raised on every part."""
+        last evaluation), or (None, energy) with download=False (the state stays on
+        the devices). On error the state is left as it was, and the reference's
+        exception is raised on every part."""
         if not (dt > 0.0):
             raise ConfigError("dt must be > 0")
         if steps < 0:
@@ -469,6 +470,8 @@ class SpatialDecomposition:
             self._set_state(backup)
             raise
         energy = self._energy_sum(energy)
+        if not download:
+            return None, energy
         pos, vel = self.parts[0][1].download()
         s = self.system
         return ParticleSystem(pos, vel, s.charges, s.masses, s.box), energy

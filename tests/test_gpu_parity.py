@@ -169,3 +169,21 @@ def test_propagate_bitwise_across_fresh_fields():
         out.append(ds.download())
     for p, v in out[1:]:
         assert np.array_equal(p, out[0][0]) and np.array_equal(v, out[0][1])
+
+
+def test_fields_with_different_fft_sizes_coexist(port):
+    # the dynamic shared-memory limit of the FFT kernels is process-wide; a field with
+    # a small plan created after one with a large plan must not break the large one
+    box = np.array([219.0, 219.0, 219.0])
+    pos, q = fx.uniform(4000, box, "random_neutral", 1.5, 21)
+    s = pkg.ParticleSystem(pos, None, q, None, box)
+    big = pkg.MsmField(pkg.MsmConfig(12.0, 2.5, 4))
+    e1 = big.evaluate(s).total_energy
+    small = pkg.MsmField(pkg.MsmConfig(8.0, 5.0, 3))
+    small.evaluate(s)
+    r = big.evaluate(s)
+    assert r.total_energy == e1
+    ds = pkg.DeviceSystem(big, s)
+    ds.propagate(0.005, 2)  # graph capture path
+    o = port.msm_potential(pos, q, box, 12.0, 2.5, 4)
+    assert rel_e(e1, o["energy"]) <= 1e-10

@@ -113,7 +113,7 @@ def _single(w, steps):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name,n,parts,steps", [("c2s", 30000, 2, 3), ("c2s", 30000, 3, 2), ("c5", 20000, 4, 2),
+@pytest.mark.parametrize("name,n,parts,steps", [("c2s", 30000, 1, 2), ("c2s", 30000, 2, 3), ("c2s", 30000, 3, 2), ("c5", 20000, 4, 2),
                                                 ("c4", 30000, 3, 2), ("c1s", 2048, 7, 3)])
 def test_decomposed_trajectory_bitwise(name, n, parts, steps):
     w = fx.config(name, n_override=n)
