@@ -573,6 +573,10 @@ constexpr int kRow = 2 * kSlots;      // two ring slots per 32-bit row
 #ifndef MSMB_PAIR_MINB
 #define MSMB_PAIR_MINB 5
 #endif
+#ifndef MSMB_PAIR_LDS
+#define MSMB_PAIR_LDS 128 // j-data smem layout: 128 = (x,y),(z,q) double2 rows, 2 loads/pair (measured
+                         // 0.958 ms vs 1.013 for 32-bit rows / 8 loads, 0.963 for 4 double rows)
+#endif
 
 __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     k_pairs(const int* __restrict__ nclu, const int2* __restrict__ clu,
@@ -582,7 +586,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
             const float4* __restrict__ f4, PairP p, double* phis, double* fsx, double* fsy,
             double* fsz, const int* __restrict__ col_off, int col_a, int col_b, ErrRec* err) {
     __shared__ __align__(16) float s_sc[kPairWarps][4][32];
+#if MSMB_PAIR_LDS == 32
     __shared__ unsigned s_w[kPairWarps][8][kRow];
+#elif MSMB_PAIR_LDS == 64
+    __shared__ double s_d[kPairWarps][4][kRow];     // x, y, z, q rows
+#else
+    __shared__ double2 s_v[kPairWarps][2][kRow];    // (x, y), (z, q) rows
+#endif
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ic = col_off[col_a] + blockIdx.x * kPairWarps + w;
     if (ic >= col_off[col_b] || failed(err)) return;
@@ -601,7 +611,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     const float ri2 = __uint_as_float(__reduce_max_sync(FULLMASK, __float_as_uint(vi ? nif : 0.f)));
     // dummies at positions 0 and 33: (1e4, 1e4, 1e4) A -- far from every covered
     // particle, so r2 ~ 1e8 keeps g, g' finite -- with q = 0: idle steps add exact zeros
+#if MSMB_PAIR_LDS == 32
     if (lane < 16) s_w[w][lane & 7][(lane >> 3) * kSlots] = ((lane & 7) == 1 || (lane & 7) == 3 || (lane & 7) == 5) ? 0x40C38800u : 0u;
+#elif MSMB_PAIR_LDS == 64
+    if (lane < 8) s_d[w][lane & 3][(lane >> 2) * kSlots] = (lane & 3) == 3 ? 0.0 : 1e4;
+#else
+    if (lane < 4) s_v[w][lane & 1][(lane >> 1) * kSlots] = (lane & 1) ? make_double2(1e4, 0.0) : make_double2(1e4, 1e4);
+#endif
     double ph = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
     unsigned ncand = 0;
     const int nj = pcnt[ic];
@@ -618,7 +634,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         zj_n = zs[sj];
         qj_n = qs[sj];
     };
+#if MSMB_PAIR_LDS == 32
     const unsigned* row = &s_w[w][0][0];
+#elif MSMB_PAIR_LDS == 64
+    const double* row = &s_d[w][0][0];
+#else
+    const double2* row = &s_v[w][0][0];
+#endif
     unsigned mA = 0, mB = 0; // lane masks of the older / newer staged cluster
     int pA = 1;              // ring slot of the older cluster (warp-uniform)
     auto step = [&]() {
@@ -626,10 +648,17 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         const int sl = (useA ? pA : pA ^ 1) * kSlots + __ffs(useA ? mA : mB);
         mA = useA ? (mA & (mA - 1)) : mA;
         mB = useA ? mB : (mB & (mB - 1));
+#if MSMB_PAIR_LDS == 32
         const double xj = __hiloint2double(row[1 * kRow + sl], row[0 * kRow + sl]);
         const double yj = __hiloint2double(row[3 * kRow + sl], row[2 * kRow + sl]);
         const double zj = __hiloint2double(row[5 * kRow + sl], row[4 * kRow + sl]);
         const double qj = __hiloint2double(row[7 * kRow + sl], row[6 * kRow + sl]);
+#elif MSMB_PAIR_LDS == 64
+        const double xj = row[sl], yj = row[kRow + sl], zj = row[2 * kRow + sl], qj = row[3 * kRow + sl];
+#else
+        const double2 xy = row[sl], zq = row[kRow + sl];
+        const double xj = xy.x, yj = xy.y, zj = zq.x, qj = zq.y;
+#endif
         const double dx = xi - xj, dy = yi - yj, dz = zi - zj;
         const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
         const double rinv = rsqrt_pos(r2);
@@ -666,6 +695,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         s_sc[w][2][lane] = -2.f * zj;
         s_sc[w][3][lane] = vj ? njf - cut2 : 3e38f;
         const int slot = pB * kSlots + 32 - lane;
+#if MSMB_PAIR_LDS == 32
         s_w[w][0][slot] = __double2loint(xj_n);
         s_w[w][1][slot] = __double2hiint(xj_n);
         s_w[w][2][slot] = __double2loint(yj_n);
@@ -674,6 +704,15 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         s_w[w][5][slot] = __double2hiint(zj_n);
         s_w[w][6][slot] = __double2loint(qj_n);
         s_w[w][7][slot] = __double2hiint(qj_n);
+#elif MSMB_PAIR_LDS == 64
+        s_d[w][0][slot] = xj_n;
+        s_d[w][1][slot] = yj_n;
+        s_d[w][2][slot] = zj_n;
+        s_d[w][3][slot] = qj_n;
+#else
+        s_v[w][0][slot] = make_double2(xj_n, yj_n);
+        s_v[w][1][slot] = make_double2(zj_n, qj_n);
+#endif
         __syncwarp();
         if (jj + 1 < nj) fetch(jj + 1);
         // ---- screening: bit (31 - t) of mask <=> atom t within the screening cut
