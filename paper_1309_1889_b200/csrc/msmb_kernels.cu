@@ -573,6 +573,9 @@ constexpr int kRow = 2 * kSlots;      // two ring slots per 32-bit row
 #ifndef MSMB_PAIR_MINB
 #define MSMB_PAIR_MINB 5
 #endif
+#ifndef MSMB_PAIR_FLO
+#define MSMB_PAIR_FLO 1 // highest-bit walk with bfind (measured 0.940 vs 0.961 ms for ffs)
+#endif
 #ifndef MSMB_PAIR_LDS
 #define MSMB_PAIR_LDS 128 // j-data smem layout: 128 = (x,y),(z,q) double2 rows, 2 loads/pair (measured
                          // 0.958 ms vs 1.013 for 32-bit rows / 8 loads, 0.963 for 4 double rows)
@@ -643,11 +646,33 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
 #endif
     unsigned mA = 0, mB = 0; // lane masks of the older / newer staged cluster
     int pA = 1;              // ring slot of the older cluster (warp-uniform)
+#if MSMB_PAIR_LDS == 128
+    const double2* rowA = row + kSlots; // ring slot pA's rows
+    const double2* rowB = row;          // ring slot pA ^ 1's rows
+#endif
     auto step = [&]() {
         const bool useA = mA != 0;
+#if MSMB_PAIR_FLO
+        // highest set bit (bfind: 0xffffffff when none -> the slot's dummy at +0); clearing
+        // it with shl, which PTX clamps to 0 for shift amounts >= 32
+        const unsigned m = useA ? mA : mB;
+        int pos;
+        asm("bfind.u32 %0, %1;" : "=r"(pos) : "r"(m));
+        unsigned bit;
+        asm("shl.b32 %0, %1, %2;" : "=r"(bit) : "r"(1u), "r"(pos));
+        const unsigned mc = m & ~bit;
+        mA = useA ? mc : mA;
+        mB = useA ? mB : mc;
+#if MSMB_PAIR_LDS == 128
+        const double2* rs = (useA ? rowA : rowB) + (pos + 1);
+#else
+        const int sl = (useA ? pA : pA ^ 1) * kSlots + pos + 1;
+#endif
+#else
         const int sl = (useA ? pA : pA ^ 1) * kSlots + __ffs(useA ? mA : mB);
         mA = useA ? (mA & (mA - 1)) : mA;
         mB = useA ? mB : (mB & (mB - 1));
+#endif
 #if MSMB_PAIR_LDS == 32
         const double xj = __hiloint2double(row[1 * kRow + sl], row[0 * kRow + sl]);
         const double yj = __hiloint2double(row[3 * kRow + sl], row[2 * kRow + sl]);
@@ -655,6 +680,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         const double qj = __hiloint2double(row[7 * kRow + sl], row[6 * kRow + sl]);
 #elif MSMB_PAIR_LDS == 64
         const double xj = row[sl], yj = row[kRow + sl], zj = row[2 * kRow + sl], qj = row[3 * kRow + sl];
+#elif MSMB_PAIR_FLO
+        const double2 xy = rs[0], zq = rs[kRow];
+        const double xj = xy.x, yj = xy.y, zj = zq.x, qj = zq.y;
 #else
         const double2 xy = row[sl], zq = row[kRow + sl];
         const double xj = xy.x, yj = xy.y, zj = zq.x, qj = zq.y;
@@ -679,6 +707,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         mA = mB;
         mB = 0;
         pA ^= 1;
+#if MSMB_PAIR_LDS == 128
+        {
+            const double2* t = rowA;
+            rowA = rowB;
+            rowB = t;
+        }
+#endif
         const int pB = pA ^ 1; // the freed slot receives cluster jj
         const int jc = jc_n;
         const bool vj = lane < cj_n.y;
