@@ -440,6 +440,7 @@ __global__ void __launch_bounds__(256)
     const int czB = min(p.d2 - 1, int(floor((double(hi.z) + cutd - p.oz) / p.h)) + 1);
     const int lay = p.cw * p.cw;
     const int64_t cpc = int64_t(p.d2) * lay;
+    const float oxf = float(p.ox), oyf = float(p.oy), colwf = float(p.colw);
     int count = 0;
     int* out = plist + size_t(ic) * cap;
     for (int dx = 0; dx <= DX; ++dx)
@@ -455,8 +456,9 @@ __global__ void __launch_bounds__(256)
                 const int cx = cxi + sx * dx, cy = cyi + sy * dy;
                 int emitted = 0;
                 if (cx >= cx0 && cx <= cx1 && cy >= cy0 && cy <= cy1) {
-                    const float xlo = float(p.ox + cx * p.colw) - 1e-3f, xhi = float(p.ox + (cx + 1) * p.colw) + 1e-3f;
-                    const float ylo = float(p.oy + cy * p.colw) - 1e-3f, yhi = float(p.oy + (cy + 1) * p.colw) + 1e-3f;
+                    // column bounds in fp32 (error ~1e-5 A, inside the 1e-3 A margin)
+                    const float xlo = fmaf(float(cx), colwf, oxf) - 1e-3f, xhi = fmaf(float(cx + 1), colwf, oxf) + 1e-3f;
+                    const float ylo = fmaf(float(cy), colwf, oyf) - 1e-3f, yhi = fmaf(float(cy + 1), colwf, oyf) + 1e-3f;
                     const float gx = gapf(lo.x, hi.x, xlo, xhi), gy = gapf(lo.y, hi.y, ylo, yhi);
                     if (gx * gx + gy * gy < p.cut2) {
                         const int col = cx * p.ncy + cy;
@@ -480,8 +482,13 @@ __global__ void __launch_bounds__(256)
                                 ok = ex * ex + ey * ey + ez * ez < p.cut2;
                             }
                             const unsigned b = __ballot_sync(FULLMASK, ok);
-                            const int pos = count + __popc(b & ((1u << lane) - 1u));
-                            if (ok && pos < cap) out[pos] = jc;
+                            const int loc = count - gstart + __popc(b & ((1u << lane) - 1u));
+                            if (ok) { // staged in shared memory for the interleave; overflow straight out
+                                if (loc < kListSeg)
+                                    s_seg[wl][loc] = jc;
+                                else if (gstart + loc < cap)
+                                    out[gstart + loc] = jc;
+                            }
                             count += __popc(b);
                             emitted += __popc(b);
                         }
@@ -492,20 +499,21 @@ __global__ void __launch_bounds__(256)
             // interleave the group's columns: rank r of column c (odd c reversed) goes to
             // sum_c' min(n_c', r) + #{c' < c : n_c' > r}
             const int total = count - gstart;
-            if (ncol > 1 && total > 1 && total <= kListSeg && count <= cap) {
-                __syncwarp();
-                for (int e = lane; e < total; e += 32) s_seg[wl][e] = out[gstart + e];
-                __syncwarp();
+            __syncwarp();
+            if (ncol > 1 && total > 1 && total <= kListSeg) {
                 for (int e = lane; e < total; e += 32) {
                     int c = 0, i = e;
                     while (i >= nseg[c]) i -= nseg[c++];
                     const int r = (c & 1) ? nseg[c] - 1 - i : i;
                     int dest = 0;
                     for (int c2 = 0; c2 < ncol; ++c2) dest += min(nseg[c2], r) + ((c2 < c && nseg[c2] > r) ? 1 : 0);
-                    out[gstart + dest] = s_seg[wl][e];
+                    if (gstart + dest < cap) out[gstart + dest] = s_seg[wl][e];
                 }
-                __syncwarp();
+            } else { // column order
+                for (int e = lane; e < min(total, kListSeg); e += 32)
+                    if (gstart + e < cap) out[gstart + e] = s_seg[wl][e];
             }
+            __syncwarp();
         }
     if (lane == 0) {
         pcnt[ic] = min(count, cap);
@@ -573,6 +581,12 @@ constexpr int kRow = 2 * kSlots;      // two ring slots per 32-bit row
 #ifndef MSMB_PAIR_MINB
 #define MSMB_PAIR_MINB 5
 #endif
+#ifndef MSMB_PAIR_ILP2
+#define MSMB_PAIR_ILP2 0
+#endif
+#ifndef MSMB_PAIR_CONSTREG
+#define MSMB_PAIR_CONSTREG 1 // pin the kernel constants in registers
+#endif
 #ifndef MSMB_PAIR_FLO
 #define MSMB_PAIR_FLO 1 // highest-bit walk with bfind (measured 0.940 vs 0.961 ms for ffs)
 #endif
@@ -600,7 +614,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     const int ic = col_off[col_a] + blockIdx.x * kPairWarps + w;
     if (ic >= col_off[col_b] || failed(err)) return;
     double a2 = p.a2, c0 = p.c0, c1 = p.c1, c2 = p.c2, d0 = p.d0, d1 = p.d1;
+#if MSMB_PAIR_CONSTREG
     asm volatile("" : "+d"(a2), "+d"(c0), "+d"(c1), "+d"(c2), "+d"(d0), "+d"(d1));
+#endif
     const int2 c = clu[ic];
     const bool vi = lane < c.y;
     const int si = c.x + (vi ? lane : 0);
@@ -650,7 +666,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     const double2* rowA = row + kSlots; // ring slot pA's rows
     const double2* rowB = row;          // ring slot pA ^ 1's rows
 #endif
-    auto step = [&]() {
+    auto step_acc = [&](double& ph, double& fx, double& fy, double& fz) {
         const bool useA = mA != 0;
 #if MSMB_PAIR_FLO
         // highest set bit (bfind: 0xffffffff when none -> the slot's dummy at +0); clearing
@@ -699,11 +715,23 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         fy = fma(dy, wgt, fy);
         fz = fma(dz, wgt, fz);
     };
+    auto step = [&]() { step_acc(ph, fx, fy, fz); };
+#if MSMB_PAIR_ILP2
+    double ph2 = 0.0, fx2 = 0.0, fy2 = 0.0, fz2 = 0.0;
+    auto step2x = [&]() { // two independent chains; an odd count starts the newer cluster early
+        step_acc(ph, fx, fy, fz);
+        step_acc(ph2, fx2, fy2, fz2);
+    };
+#endif
     if (nj > 0) fetch(0);
     for (int jj = 0; jj < nj; ++jj) {
         // drain the older cluster; lanes done with it already consume the newer one
         const int dA = __reduce_max_sync(FULLMASK, __popc(mA));
+#if MSMB_PAIR_ILP2
+        for (int k = 0; k < dA; k += 2) step2x();
+#else
         for (int k = 0; k < dA; ++k) step();
+#endif
         mA = mB;
         mB = 0;
         pA ^= 1;
@@ -777,7 +805,15 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         mB = mask;
     }
     const int dAll = __reduce_max_sync(FULLMASK, __popc(mA) + __popc(mB));
+#if MSMB_PAIR_ILP2
+    for (int k = 0; k < dAll; k += 2) step2x();
+    ph += ph2;
+    fx += fx2;
+    fy += fy2;
+    fz += fz2;
+#else
     for (int k = 0; k < dAll; ++k) step();
+#endif
     if (vi) {
         const double kq = -p.kc * qi; // f = d * (-k_C q_i q_j g*'/r)  (msm_phases.cpp:246)
         phis[si] = ph;
