@@ -140,3 +140,17 @@ def test_top_level_fft_large(port, box, levels):
     got = pkg.MsmField(cfg).debug_stage(2, t, box, q)
     ref = port.top_level(box, 12.0, 2.5, levels, q)
     assert _scale_err(got, ref) <= 1e-13
+
+
+def test_anterpolation_streaming_kernel(port):
+    # the layer-streaming anterpolation runs for level-0 lattices above 4M points: a
+    # C3-sized box (226^3 points) with few atoms exercises it against the reference
+    box = np.array([551.0, 551.0, 551.0])
+    pos, q = fx.uniform(20000, box, "random_neutral", 1.5, 31)
+    cfg = pkg.MsmConfig(12.0, 2.5, 4)
+    f = pkg.MsmField(cfg)
+    f.evaluate(pkg.ParticleSystem(pos, None, q, None, box))
+    qc, _ = f.debug_levels()
+    o = port.msm_potential(pos, q, box, 12.0, 2.5, 4, diag=True)
+    sl, _ = level_slices(cfg, box)
+    assert _scale_err(qc[sl[0]], o["level_charge"][sl[0]]) <= 1e-14
