@@ -251,6 +251,14 @@ int msmb_measure_fp64_peak(int device, double seconds, double* tflops);
  * convolution, 1 = direct stencil sum as the reference (src/msm_phases.cpp:93-134).
  * Both agree to rounding; the direct sum is kept for comparison and tests. */
 int msmb_set_lattice_method(msmb_field* f, int direct);
+/* Pair-list skin (A, default 0.2): the cluster pair list of a propagate call is
+ * built at its first evaluation and rebuilt only once some atom moved more than
+ * skin/2; the pair kernel always screens with the exact cutoff, so the results are
+ * the reference's within rounding.  The summation order follows the list, so
+ * forces are bit-reproducible for a given call sequence but depend on when the
+ * list was built (last bits); skin = 0 rebuilds at every evaluation, making the
+ * forces a pure function of the positions. */
+int msmb_set_pair_skin(msmb_field* f, double skin);
 /* Kernel launches issued by this handle since creation. */
 int64_t msmb_kernel_launches(const msmb_field* f);
 

@@ -245,6 +245,11 @@ class MsmField(ForceField):
         return PotentialResult(phi, f, float(e[0]), ps, pl)
 
     # -- measurement / diagnostics
+    def set_pair_skin(self, skin: float):
+        """Pair-list skin in A (default 0.2; 0 = rebuild the list at every evaluation,
+        making forces a pure function of the positions).  See msmb_set_pair_skin."""
+        _check(self._h, _native.lib().msmb_set_pair_skin(self._h, float(skin)))
+
     def set_lattice_method(self, direct: bool):
         """Lattice cutoff by zero-padded FFT convolution (default) or by the direct
         stencil sum of the reference (src/msm_phases.cpp:93-134)."""

@@ -60,6 +60,7 @@ SIGNATURES = {
     "msmb_system_copy": (C.c_int, [_VP, _VP]),
     "msmb_system_propagate_ex": (C.c_int, [_VP, _VP, C.c_double, C.c_int, C.POINTER(UnitsC)]),
     "msmb_set_lattice_method": (C.c_int, [_VP, C.c_int]),
+    "msmb_set_pair_skin": (C.c_int, [_VP, C.c_double]),
     "msmb_dd_plan": (C.c_int, [C.POINTER(MsmConfigC), C.POINTER(UnitsC), _D, C.c_int64, C.c_int, C.c_int, _I,
                               C.c_int]),
     "msmb_dd_set_part": (C.c_int, [_VP, C.c_int, C.c_int]),

@@ -55,7 +55,7 @@ void export_planes(cudaStream_t st, const Geometry& g, const Part& P, int k, con
     if (cnt) ckd(cudaMemcpyAsync(x + off, src + off, cnt * sizeof(double), cudaMemcpyDeviceToDevice, st), "D2D");
 }
 
-int phase0(msmb_field* f, Workspace& W, DevState& s, long long* xbuf) {
+int phase0(msmb_field* f, Workspace& W, DevState& s, long long* xbuf, int rebuild) {
     const Geometry& g = W.g;
     cudaStream_t st = f->stream;
     for (int attempt = 0; attempt < 8; ++attempt) {
@@ -63,7 +63,7 @@ int phase0(msmb_field* f, Workspace& W, DevState& s, long long* xbuf) {
         int nl = launch_reset_err(st, W.err, 0);
         nl += launch_bin(st, g, s, W.a, W.c, W.err);
         nl += launch_sort(st, g, s, W.a, W.c, W.err);
-        nl += launch_clusters(st, g, s.n, W.a, W.c, W.err, W.cap, W.part);
+        nl += launch_clusters(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.part, attempt > 0 ? 1 : rebuild);
         nl += launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.part);
         nl += launch_anterp(st, g, W.a, W.c, W.L, W.err, W.part);
         nl += launch_finalize(st, s, W.err);
@@ -174,6 +174,14 @@ extern "C" int msmb_dd_set_part(msmb_field* f, int nparts, int part) {
     return MSMB_OK;
 }
 
+extern "C" int msmb_set_pair_skin(msmb_field* f, double skin) {
+    if (!f || !(skin >= 0.0)) return MSMB_ERR_CONFIG;
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    f->pair_skin = skin;
+    f->ws.reset(); // rebuilt on the next call
+    return MSMB_OK;
+}
+
 extern "C" int msmb_set_lattice_method(msmb_field* f, int direct) {
     if (!f) return MSMB_ERR_CONFIG;
     std::lock_guard<std::recursive_mutex> lk(f->mu);
@@ -215,7 +223,7 @@ extern "C" int msmb_dd_phase(msmb_field* f, msmb_system* sys, int phase, double 
         const long long* xi = static_cast<const long long*>(xin);
         long long* xo = static_cast<long long*>(xout);
         switch (phase) {
-            case 0: return phase0(f, W, s, xo);
+            case 0: return phase0(f, W, s, xo, kicks); // phase 0: `kicks` = force a pair-list rebuild
             case 1: return phase1(f, W, xi, xo);
             case 2: return phase2(f, W, s, xi, xo, dt, kicks, drift, u.energy_to_native, energy);
             case 3: return phase3(f, W, s, xi);

@@ -172,6 +172,7 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
     e = build_geometry(f->cfg, f->units, box, n, W->g);
     if (e.kind) return nullptr;
     Geometry& g = W->g;
+    if (f->pair_skin >= 0.0) g.skin = f->pair_skin;
     W->n = n;
     W->whole = make_part(g, 1, 0);
     W->part = make_part(g, f->dd_nparts, f->dd_part);
@@ -191,6 +192,12 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
     a.fsx = walloc<double>(*W, N);
     a.fsy = walloc<double>(*W, N);
     a.fsz = walloc<double>(*W, N);
+    a.cl_perm = walloc<int>(*W, N);
+    a.xc = walloc<double>(*W, N);
+    a.yc = walloc<double>(*W, N);
+    a.zc = walloc<double>(*W, N);
+    a.qc = walloc<double>(*W, N);
+    a.ref = walloc<double>(*W, 3 * N);
     DevCells& c = W->c;
     c.count = walloc<int>(*W, size_t(g.ncells + 1));
     c.start = walloc<int>(*W, size_t(g.ncells + 1));
@@ -204,7 +211,11 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
     c.nclu = walloc<int>(*W, 1);
     c.pcnt = walloc<int>(*W, size_t(W->maxclu));
     c.scan_tmp = walloc<int>(*W, size_t((std::max(g.ncells, g.ncols) + 1 + 4095) / 4096 + 8));
+    c.colstart = walloc<int>(*W, size_t(g.ncols + 1));
+    c.flag = walloc<int>(*W, 2);
     ck(cudaMemset(c.nclu, 0, sizeof(int)), "memset");
+    ck(cudaMemset(c.flag, 0, 2 * sizeof(int)), "memset");
+    ck(cudaMemset(c.colstart, 0, sizeof(int) * size_t(g.ncols + 1)), "memset");
     alloc_plist(*W, g.pair_cap);
     DevLevels& L = W->L;
     L.charge = walloc<double>(*W, g.lattice_total);
@@ -378,7 +389,9 @@ static int stage_id(const char* name) {
 // fixed order, so results do not depend on how the branches interleave.  With
 // per-stage timing on, everything runs on one stream so the stage events are
 // exclusive.
-static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs) {
+// `rebuild`: force a pair-list rebuild (the first evaluation of a call); otherwise
+// the list is rebuilt only once some atom moved more than skin/2 (launch_clusters).
+static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, bool rebuild = true) {
     cudaStream_t st = f->stream;
     const bool fork = !f->timer.on;
     cudaStream_t lr = fork ? f->side : st;
@@ -406,7 +419,7 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs) 
     });
     run("prolong", [&] { return launch_prolong_all(lr, g, W.L, W.err); });
     if (fork) ck(cudaEventRecord(f->join_ev, lr), "join");
-    run("clusters", [&] { return launch_clusters(st, g, s.n, W.a, W.c, W.err, W.cap, W.whole); });
+    run("clusters", [&] { return launch_clusters(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, rebuild ? 1 : 0); });
     run("pairs", [&] { return launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole); });
     if (fork) ck(cudaStreamWaitEvent(st, f->join_ev, 0), "join");
     DevOut o = W.o;
@@ -486,11 +499,11 @@ static void ensure_graphs(msmb_field* f, Workspace& W, DevState& s, double dt, d
     W.launches_eval = nl;
     W.gx_step1 = capture(f, [&] {
         nl = launch_kick_drift(f->stream, s, W.o, dt, conv, 1, W.err);
-        nl += enqueue_eval(f, W, s, false);
+        nl += enqueue_eval(f, W, s, false, false);
     });
     W.gx_step2 = capture(f, [&] {
         nl = launch_kick_drift(f->stream, s, W.o, dt, conv, 2, W.err);
-        nl += enqueue_eval(f, W, s, false);
+        nl += enqueue_eval(f, W, s, false, false);
     });
     W.launches_step = nl;
     f->launches -= 3 * int64_t(W.launches_eval); // captures are not launches
@@ -546,11 +559,11 @@ int engine_propagate(msmb_field* f, StateBuf& sb, double dt, int steps, double c
                 f->launches += W.launches_step;
             }
         } else {
-            enqueue_eval(f, W, s, false);
+            enqueue_eval(f, W, s, false, true);
             for (int st = 1; st <= steps; ++st) {
                 StageScope sc(f, "verlet");
                 sc.done(launch_kick_drift(f->stream, s, W.o, dt, conv, st == 1 ? 1 : 2, W.err));
-                enqueue_eval(f, W, s, false);
+                enqueue_eval(f, W, s, false, false);
             }
         }
         {

@@ -130,6 +130,7 @@ struct msmb_field {
     int refs = 0;           // live msmb_system objects bound to this field
     int dd_nparts = 1, dd_part = 0; // spatial decomposition part (msmb_dd_set_part)
     int lattice_direct = 0;         // msmb_set_lattice_method: 1 = direct stencil sum
+    double pair_skin = -1.0;        // msmb_set_pair_skin (A); < 0 = default
     bool destroy_pending = false;
 };
 

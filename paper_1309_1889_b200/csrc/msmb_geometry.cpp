@@ -11,6 +11,7 @@
 //  * top-level kernel table: src/msm_phases.cpp:136-162
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <string>
 
@@ -301,10 +302,15 @@ Error build_geometry(const msmb_msm_config& c, const msmb_units& u, const double
         }
         g.screen_cut2 = c.cutoff_a * c.cutoff_a * (1.0 + 1e-6) + 64.0 * std::ldexp(1.0, -24) * 3.0 * rc2;
     }
+    // pair-list skin: the cluster pair list is rebuilt only once some atom moved more
+    // than skin/2 since the last build (MSMB_SKIN overrides, 0 = rebuild every evaluation)
+    g.skin = 0.2;
+    if (const char* e = std::getenv("MSMB_SKIN")) g.skin = std::max(0.0, std::atof(e));
     {
         const double zext = 32.0 / (rho * g.colw * g.colw);
-        const double ext_xy = 2.0 * (g.colw + c.cutoff_a);
-        const double ext_z = 2.0 * (std::min(zext, box[2] + 4 * L0.spacing) + c.cutoff_a);
+        const double lc = c.cutoff_a + g.skin;
+        const double ext_xy = 2.0 * (g.colw + lc);
+        const double ext_z = 2.0 * (std::min(zext, box[2] + 4 * L0.spacing) + lc);
         const double ncand = 1.5 * rho * ext_xy * ext_xy * ext_z / 32.0;
         const double ncol_range = (ext_xy / g.colw + 1) * (ext_xy / g.colw + 1);
         double cap = ncand + 2.0 * ncol_range + 32.0;

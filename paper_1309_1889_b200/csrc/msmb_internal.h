@@ -113,6 +113,7 @@ struct Geometry {
     double screen_cut = 0;               // fp32 bounding-box cutoff (a + margin)
     double screen_center[3] = {0, 0, 0}; // fp32 screening coordinates are relative to this point
     double screen_cut2 = 0;              // a^2 + bound on the fp32 dot-product-form error
+    double skin = 0;                     // pair-list skin (A): rebuilt once an atom moved > skin/2
     int pair_cap = 0;                    // initial pair-list capacity per cluster
     int64_t lattice_taps_clipped = 0;    // sum over levels 0..l-2 of clipped nonzero taps
     int64_t top_taps = 0;                // M_top^2

@@ -288,10 +288,6 @@ __global__ void k_gather(int n, const int* __restrict__ start_total, const int* 
     ys[s] = py;
     zs[s] = pz;
     qs[s] = qq;
-    {   // screening record (-2x', -2y', -2z', |x'|^2 - cut^2), x' = x - centre in fp32
-        const float fx = float(px - p.sc[0]), fy = float(py - p.sc[1]), fz = float(pz - p.sc[2]);
-        f4[s] = make_float4(-2.f * fx, -2.f * fy, -2.f * fz, fmaf(fz, fz, fmaf(fy, fy, fx * fx)) - p.cut2f);
-    }
     const double pp[3] = {px, py, pz};
     double w[3][4];
     for (int ax = 0; ax < 3; ++ax) {
@@ -337,10 +333,54 @@ int launch_sort(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms&
 // sorted atoms of a column form a cluster; one warp per i-cluster walks the
 // list of j-clusters whose bounding boxes are within the cutoff.
 // ============================================================================
+// ---- pair-list (Verlet skin) bookkeeping.  flag[0]: rebuild the cluster pair list
+// in this evaluation (forced, or some atom moved more than skin/2 since the last
+// rebuild); flag[1]: atoms in the cluster order.  Between rebuilds the clusters keep
+// their atoms (cl_perm) and only the positions are gathered anew; the pair kernel
+// screens with the exact cutoff, so the frozen list only has to be a superset.
+__global__ void k_flag_reset(int* flag, int force) { flag[0] = force; }
+
+__global__ void k_disp(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
+                       const double* __restrict__ z, const double* __restrict__ ref, double half_skin2,
+                       int* flag) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double dx = x[i] - ref[i], dy = y[i] - ref[n + i], dz = z[i] - ref[2 * n + i];
+    if (!(dx * dx + dy * dy + dz * dz <= half_skin2)) flag[0] = 1; // same value from every writer
+}
+
+__global__ void k_cl_perm(int64_t n, const int* __restrict__ start_total, const int* __restrict__ perm,
+                          const double* __restrict__ x, const double* __restrict__ y,
+                          const double* __restrict__ z, int* cl_perm, double* ref, int* flag) {
+    if (!flag[0]) return;
+    const int tot = *start_total;
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s == 0) flag[1] = tot;
+    if (s >= tot) return;
+    const int i = perm[s];
+    cl_perm[s] = i;
+    ref[i] = x[i];
+    ref[n + i] = y[i];
+    ref[2 * n + i] = z[i];
+}
+
+__global__ void k_gather_cl(const int* __restrict__ flag, const int* __restrict__ cl_perm,
+                            const double* __restrict__ x, const double* __restrict__ y,
+                            const double* __restrict__ z, const double* __restrict__ q, double* xc,
+                            double* yc, double* zc, double* qc, const ErrRec* err) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= flag[1] || failed(err)) return;
+    const int i = cl_perm[k];
+    xc[k] = x[i];
+    yc[k] = y[i];
+    zc[k] = z[i];
+    qc[k] = q[i];
+}
+
 __global__ void k_columns(int64_t ncols, int cells_per_col, const int* __restrict__ start,
-                          int* col_cnt, const ErrRec* err) {
+                          int* col_cnt, const int* __restrict__ flag, const ErrRec* err) {
     const int64_t col = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (col > ncols || failed(err)) return;
+    if (col > ncols || failed(err) || !flag[0]) return;
     if (col == ncols) {
         col_cnt[col] = 0;
         return;
@@ -350,12 +390,16 @@ __global__ void k_columns(int64_t ncols, int cells_per_col, const int* __restric
 }
 
 __global__ void k_clusters(int64_t ncols, int cells_per_col, const int* __restrict__ start,
-                           const int* __restrict__ col_off, int2* clu, int* nclu,
-                           const ErrRec* err) {
+                           const int* __restrict__ col_off, int2* clu, int* nclu, int* colstart,
+                           const int* __restrict__ flag, const ErrRec* err) {
     const int64_t col = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (col >= ncols || failed(err)) return;
-    if (col == ncols - 1) *nclu = col_off[ncols];
+    if (col >= ncols || failed(err) || !flag[0]) return;
+    if (col == ncols - 1) {
+        *nclu = col_off[ncols];
+        colstart[ncols] = start[ncols * cells_per_col];
+    }
     const int s0 = start[col * cells_per_col];
+    colstart[col] = s0;
     const int cnt = start[(col + 1) * cells_per_col] - s0;
     const int off = col_off[col];
     for (int k = 0; 32 * k < cnt; ++k) clu[off + k] = make_int2(s0 + 32 * k, min(32, cnt - 32 * k));
@@ -364,10 +408,10 @@ __global__ void k_clusters(int64_t ncols, int cells_per_col, const int* __restri
 __global__ void k_bbox(const int* __restrict__ nclu, const int2* __restrict__ clu,
                        const double* __restrict__ xs, const double* __restrict__ ys,
                        const double* __restrict__ zs, float4* blo, float4* bhi,
-                       const ErrRec* err) {
+                       const int* __restrict__ flag, const ErrRec* err) {
     const int ic = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (ic >= *nclu || failed(err)) return;
+    if (ic >= *nclu || failed(err) || !flag[0]) return;
     const int2 c = clu[ic];
     float lo[3] = {3e38f, 3e38f, 3e38f}, hi[3] = {-3e38f, -3e38f, -3e38f};
     if (lane < c.y) {
@@ -415,11 +459,11 @@ __global__ void __launch_bounds__(256)
     k_pairlist(const int* __restrict__ nclu, const float4* __restrict__ blo,
                const float4* __restrict__ bhi, const int* __restrict__ col_off,
                const int* __restrict__ start, ListP p, int* plist, int* pcnt, int cap, int col_a, int col_b,
-               ErrRec* err) {
+               const int* __restrict__ flag, ErrRec* err) {
     __shared__ int s_seg[8][kListSeg];
     const int ic = col_off[col_a] + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-    if (ic >= col_off[col_b] || failed(err)) return;
+    if (ic >= col_off[col_b] || failed(err) || !flag[0]) return;
     const float4 lo = blo[ic], hi = bhi[ic];
     const double cutd = double(p.cut);
     int cx0 = int(floor((double(lo.x) - cutd - p.ox) / p.colw)) - 1;
@@ -849,34 +893,42 @@ __global__ void k_err_brute(int64_t n, const double* __restrict__ x, const doubl
     }
 }
 
-int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c,
-                    ErrRec* err, int cap, const Part& P) {
-    (void)a;
+int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
+                    DevCells& c, ErrRec* err, int cap, const Part& P, int force_rebuild) {
     const int cells_per_col = int(g.lv[0].dims[2]) * g.cw * g.cw;
     const int64_t nc = g.ncols;
-    k_columns<<<int((nc + 1 + 255) / 256), 256, 0, st>>>(nc, cells_per_col, c.start, c.col_cnt, err);
-    int l = 1 + scan_exclusive(st, c.col_cnt, c.col_off, c.scan_tmp, nc + 1);
+    const int nb = int((n + 255) / 256) > 0 ? int((n + 255) / 256) : 1;
+    // rebuild decision, frozen cluster order, current positions in it
+    k_flag_reset<<<1, 1, 0, st>>>(c.flag, force_rebuild || !(g.skin > 0.0) ? 1 : 0);
+    const double hs = 0.5 * g.skin;
+    k_disp<<<nb, 256, 0, st>>>(n, s.x, s.y, s.z, a.ref, hs * hs, c.flag);
+    k_cl_perm<<<nb, 256, 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, a.cl_perm, a.ref, c.flag);
+    k_gather_cl<<<nb, 256, 0, st>>>(c.flag, a.cl_perm, s.x, s.y, s.z, s.q, a.xc, a.yc, a.zc, a.qc, err);
+    // cluster pair list (rebuild evaluations only)
+    k_columns<<<int((nc + 1 + 255) / 256), 256, 0, st>>>(nc, cells_per_col, c.start, c.col_cnt, c.flag, err);
+    int l = 5 + scan_exclusive(st, c.col_cnt, c.col_off, c.scan_tmp, nc + 1);
     k_clusters<<<int((nc + 255) / 256), 256, 0, st>>>(nc, cells_per_col, c.start, c.col_off, c.clu,
-                                                      c.nclu, err);
+                                                      c.nclu, c.colstart, c.flag, err);
     const int64_t maxclu = n / 32 + nc + 1;
-    k_bbox<<<int((maxclu * 32 + 255) / 256), 256, 0, st>>>(c.nclu, c.clu, a.xs, a.ys, a.zs, c.blo,
-                                                            c.bhi, err);
+    k_bbox<<<int((maxclu * 32 + 255) / 256), 256, 0, st>>>(c.nclu, c.clu, a.xc, a.yc, a.zc, c.blo,
+                                                            c.bhi, c.flag, err);
     ListP lp;
     lp.ox = g.lv[0].origin[0];
     lp.oy = g.lv[0].origin[1];
     lp.colw = g.colw;
     lp.ncx = g.ncx;
     lp.ncy = g.ncy;
-    lp.cut = float(g.screen_cut);
-    lp.cut2 = float(g.screen_cut * g.screen_cut);
+    const double lc = g.screen_cut + g.skin; // list cutoff: screening cut + skin
+    lp.cut = float(lc);
+    lp.cut2 = float(lc * lc);
     lp.oz = g.lv[0].origin[2];
     lp.h = g.lv[0].spacing;
     lp.d2 = g.lv[0].dims[2];
     lp.cw = g.cw;
     k_pairlist<<<int((maxclu * 32 + 255) / 256), 256, 0, st>>>(c.nclu, c.blo, c.bhi, c.col_off, c.start, lp,
                                                                 c.plist, c.pcnt, cap, P.cx0 * g.ncy,
-                                                                P.cx1 * g.ncy, err);
-    return l + 4;
+                                                                P.cx1 * g.ncy, c.flag, err);
+    return l + 3;
 }
 
 int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
@@ -899,7 +951,7 @@ int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& 
     int l = 0;
     if (n > 0) {
         k_pairs<<<int((maxclu + kPairWarps - 1) / kPairWarps), kPairWarps * 32, 0, st>>>(
-            c.nclu, c.clu, c.plist, c.pcnt, cap, a.xs, a.ys, a.zs, a.qs, a.f4, p, a.phis,
+            c.nclu, c.clu, c.plist, c.pcnt, cap, a.xc, a.yc, a.zc, a.qc, a.f4, p, a.phis,
             a.fsx, a.fsy, a.fsz, c.col_off, P.cx0 * g.ncy, P.cx1 * g.ncy, err);
         k_err_brute<<<592, 256, 0, st>>>(n, s.x, s.y, s.z, a.outlist, err);
         l = 2;
@@ -2011,15 +2063,16 @@ static InterpP make_interp(const Geometry& g) {
     return p;
 }
 
-__global__ void k_interp(InterpP p, const int* __restrict__ start, int64_t cell_a, int64_t cell_b,
+// one thread per atom in cluster order (the short-range results are in that order)
+__global__ void k_interp(InterpP p, const int* __restrict__ colstart, int col_a, int col_b,
                          const int* __restrict__ perm,
                          const double* __restrict__ xs, const double* __restrict__ ys,
                          const double* __restrict__ zs, const double* __restrict__ qs,
                          const double* __restrict__ pot, const double* __restrict__ phis,
                          const double* __restrict__ fsx, const double* __restrict__ fsy,
                          const double* __restrict__ fsz, DevOut o, const ErrRec* err) {
-    const int s = start[cell_a] + blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= start[cell_b] || failed(err)) return;
+    const int s = colstart[col_a] + blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= colstart[col_b] || failed(err)) return;
     double u, gx, gy, gz;
     const double q = qs[s];
     interp_atom(p, pot, xs[s], ys[s], zs[s], u, gx, gy, gz);
@@ -2074,10 +2127,8 @@ int reduce_blocks(int64_t n) { return int((n + 4095) / 4096) > 0 ? int((n + 4095
 int launch_interp(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c,
                   DevLevels& L, DevOut& o, ErrRec* err, int want_energy, const Part& P) {
     if (n == 0) return 0;
-    const int64_t cpc = int64_t(g.lv[0].dims[2]) * g.cw * g.cw; // sorted cells per pair column
-    k_interp<<<int((n + 127) / 128), 128, 0, st>>>(make_interp(g), c.start, int64_t(P.cx0) * g.ncy * cpc,
-                                                   int64_t(P.cx1) * g.ncy * cpc, a.perm, a.xs,
-                                                   a.ys, a.zs, a.qs, L.pot + g.lv[0].offset, a.phis,
+    k_interp<<<int((n + 127) / 128), 128, 0, st>>>(make_interp(g), c.colstart, P.cx0 * g.ncy, P.cx1 * g.ncy,
+                                                   a.cl_perm, a.xc, a.yc, a.zc, a.qc, L.pot + g.lv[0].offset, a.phis,
                                                    a.fsx, a.fsy, a.fsz, o, err);
     if (!want_energy) return 1;
     const int nb = reduce_blocks(n);
@@ -2198,13 +2249,13 @@ int launch_kick(cudaStream_t st, DevState& s, const DevOut& o, double dt, double
 
 // Spatial decomposition (msmb_dd.cu): the same Verlet arithmetic restricted to the
 // atoms binned into the owned pair columns (sorted range -> original index).
-__global__ void k_verlet_part(const int* __restrict__ start, int64_t cell_a, int64_t cell_b,
+__global__ void k_verlet_part(const int* __restrict__ colstart, int col_a, int col_b,
                               const int* __restrict__ perm, DevState s, const double* __restrict__ fx,
                               const double* __restrict__ fy, const double* __restrict__ fz, double dt,
                               double hdc, int kicks, int drift, const ErrRec* err) {
     if (failed(err)) return;
-    const int t = start[cell_a] + blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= start[cell_b]) return;
+    const int t = colstart[col_a] + blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= colstart[col_b]) return;
     const int i = perm[t];
     const double c = __ddiv_rn(hdc, s.m[i]);
     double a = s.vx[i], b = s.vy[i], d = s.vz[i];
@@ -2224,10 +2275,10 @@ __global__ void k_verlet_part(const int* __restrict__ start, int64_t cell_a, int
     }
 }
 
-__global__ void k_export_state(const int* __restrict__ start, int64_t cell_a, int64_t cell_b,
+__global__ void k_export_state(const int* __restrict__ colstart, int col_a, int col_b,
                                const int* __restrict__ perm, DevState s, int64_t n, long long* xbuf) {
-    const int t = start[cell_a] + blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= start[cell_b]) return;
+    const int t = colstart[col_a] + blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= colstart[col_b]) return;
     const int i = perm[t];
     const double* src[6] = {s.x, s.y, s.z, s.vx, s.vy, s.vz};
 #pragma unroll
@@ -2243,20 +2294,17 @@ int launch_verlet_part(cudaStream_t st, const Geometry& g, const DevCells& c, co
                        DevState& s, const DevOut& o, double dt, double conv, int kicks, int drift,
                        const Part& P, ErrRec* err) {
     if (s.n == 0 || (kicks == 0 && !drift)) return 0;
-    const int64_t cpc = int64_t(g.lv[0].dims[2]) * g.cw * g.cw;
     const double hdc = 0.5 * dt * conv;
-    k_verlet_part<<<int((s.n + 255) / 256), 256, 0, st>>>(c.start, int64_t(P.cx0) * g.ncy * cpc,
-                                                           int64_t(P.cx1) * g.ncy * cpc, a.perm, s, o.fx,
-                                                           o.fy, o.fz, dt, hdc, kicks, drift, err);
+    k_verlet_part<<<int((s.n + 255) / 256), 256, 0, st>>>(c.colstart, P.cx0 * g.ncy, P.cx1 * g.ncy, a.cl_perm,
+                                                           s, o.fx, o.fy, o.fz, dt, hdc, kicks, drift, err);
     return 1;
 }
 
 int launch_export_state(cudaStream_t st, const Geometry& g, const DevCells& c, const DevAtoms& a,
                         const DevState& s, long long* xbuf, const Part& P) {
     if (s.n == 0) return 0;
-    const int64_t cpc = int64_t(g.lv[0].dims[2]) * g.cw * g.cw;
-    k_export_state<<<int((s.n + 255) / 256), 256, 0, st>>>(c.start, int64_t(P.cx0) * g.ncy * cpc,
-                                                            int64_t(P.cx1) * g.ncy * cpc, a.perm, s, s.n, xbuf);
+    k_export_state<<<int((s.n + 255) / 256), 256, 0, st>>>(c.colstart, P.cx0 * g.ncy, P.cx1 * g.ncy, a.cl_perm,
+                                                            s, s.n, xbuf);
     return 1;
 }
 

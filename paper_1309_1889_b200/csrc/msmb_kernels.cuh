@@ -16,8 +16,13 @@ struct DevAtoms {       // sorted-order working set, capacity n
     double* xs; double* ys; double* zs; double* qs;  // sorted positions / charges
     float4* f4;         // sorted fp32 copies (screening)
     double* aw;         // [n*12] anterpolation weights: q*wx[4], wy[4], wz[4]
-    double* phis;       // [n] short-range potential (per unit charge), sorted order
-    double* fsx; double* fsy; double* fsz; // short-range forces (with k_C), sorted order
+    double* phis;       // [n] short-range potential (per unit charge), cluster order
+    double* fsx; double* fsy; double* fsz; // short-range forces (with k_C), cluster order
+    // pair-list (Verlet skin) state: the cluster order is the sorted order of the
+    // last list rebuild; positions are gathered into it every evaluation
+    int* cl_perm;       // [n] cluster slot -> original index
+    double* xc; double* yc; double* zc; double* qc; // [n] positions / charges, cluster order
+    double* ref;        // [3n] positions (original order) at the last rebuild
 };
 
 struct DevCells {
@@ -32,6 +37,8 @@ struct DevCells {
     int* plist;         // [max_clusters * cap]
     int* pcnt;          // [max_clusters]
     int* scan_tmp;      // scratch for the multi-block scan
+    int* colstart;      // [ncols+1] first cluster slot of each pair column (frozen at rebuild)
+    int* flag;          // [2] [0] rebuild the pair list this evaluation, [1] clustered atoms
 };
 
 struct DevLevels {      // concatenated lattices + tables
@@ -117,8 +124,8 @@ int launch_bin(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& 
                ErrRec* err);
 int launch_sort(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& a, DevCells& c,
                 ErrRec* err);
-int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c,
-                    ErrRec* err, int cap, const Part& P);
+int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
+                    DevCells& c, ErrRec* err, int cap, const Part& P, int force_rebuild);
 int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
                  DevCells& c, ErrRec* err, int cap, const Part& P);
 int launch_anterp(cudaStream_t st, const Geometry& g, DevAtoms& a, DevCells& c, DevLevels& L,

@@ -458,7 +458,7 @@ class SpatialDecomposition:
                     kicks, drift = 2, 1      # closing kick of step s, opening kick + drift of s+1
                 else:
                     kicks, drift = 1, 0      # closing half-kick of the last step
-                self._phase(0)
+                self._phase(0, kicks=1 if s == 0 else 0)  # phase 0: kicks = force a pair-list rebuild
                 self._exchange(0)
                 self._phase(1)
                 self._exchange(1)
