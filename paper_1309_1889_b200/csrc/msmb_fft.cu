@@ -115,7 +115,7 @@ __device__ __forceinline__ int find_level(const FftJobs& J, int blk) {
 // 2: forward from B over every line (spectrum precompute).
 __global__ void __launch_bounds__(256) k_fft_x(FftJobs J, int mode, const ErrRec* err) {
     extern __shared__ double2 sm[];
-    if (err && *(volatile const int*)&err->kind) return;
+    if (err && __ldcg(&err->kind)) return;
     const int k = find_level(J, blockIdx.x);
     const FftLevel& lv = J.lv[k];
     const int M0 = lv.ax[0].M, M1 = lv.ax[1].M, M2 = lv.ax[2].M;
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(256) k_fft_x(FftJobs J, int mode, const ErrRec
 // 1: inverse (output y < d1); 2: forward over every line.
 __global__ void __launch_bounds__(256) k_fft_y(FftJobs J, int mode, const ErrRec* err) {
     extern __shared__ double2 sm[];
-    if (err && *(volatile const int*)&err->kind) return;
+    if (err && __ldcg(&err->kind)) return;
     const int k = find_level(J, blockIdx.x);
     const FftLevel& lv = J.lv[k];
     const int M1 = lv.ax[1].M, M2 = lv.ax[2].M;
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(256) k_fft_y(FftJobs J, int mode, const ErrRec
 // inverse, output z < d2; 2: forward over every line, Khat = Re / (M0 M1 M2).
 __global__ void __launch_bounds__(256) k_fft_z(FftJobs J, int mode, const ErrRec* err) {
     extern __shared__ double2 sm[];
-    if (err && *(volatile const int*)&err->kind) return;
+    if (err && __ldcg(&err->kind)) return;
     const int k = find_level(J, blockIdx.x);
     const FftLevel& lv = J.lv[k];
     const int M0 = lv.ax[0].M, M1 = lv.ax[1].M, M2 = lv.ax[2].M;

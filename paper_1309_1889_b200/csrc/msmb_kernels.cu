@@ -51,7 +51,10 @@ cudaError_t smem_grow(const void* func, size_t bytes) {
 #define FULLMASK 0xffffffffu
 
 __device__ __forceinline__ bool failed(const ErrRec* e) {
-    return *(volatile const int*)&e->kind != 0;
+    // L2 (GPU-coherent) load: kernel boundaries order it after earlier kernels'
+    // writes; a stale value inside a kernel only delays an early exit.  (A volatile
+    // read compiles to a system-scope LDG.STRONG.SYS, which every thread would pay.)
+    return __ldcg(&e->kind) != 0;
 }
 
 // basis_phi / basis_phi_deriv (include/paramd/msm_kernels.hpp:71-92), reference op order.
@@ -878,7 +881,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
 __global__ void k_err_brute(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
                             const double* __restrict__ z, const int* __restrict__ outlist,
                             ErrRec* err) {
-    const int cnt = *(volatile int*)&err->cov_count;
+    const int cnt = __ldcg(&err->cov_count);
     if (cnt == 0 || failed(err)) return;
     const int64_t total = int64_t(cnt) * n;
     for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
