@@ -186,7 +186,6 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
     a.ys = walloc<double>(*W, N);
     a.zs = walloc<double>(*W, N);
     a.qs = walloc<double>(*W, N);
-    a.f4 = walloc<float4>(*W, N);
     a.aw = walloc<double>(*W, N * 12);
     a.phis = walloc<double>(*W, N);
     a.fsx = walloc<double>(*W, N);

@@ -287,21 +287,6 @@ Error build_geometry(const msmb_msm_config& c, const msmb_units& u, const double
         maxabs = std::max(maxabs, std::fabs(L0.origin[ax]) + L0.dims[ax] * L0.spacing);
     const double margin = 8.0 * std::ldexp(1.0, -24) * (2.0 * maxabs + c.cutoff_a) + 1e-6 * c.cutoff_a;
     g.screen_cut = c.cutoff_a + margin;
-    {
-        // k_pairs screens with r^2 - cut^2 = |xi'|^2 + (|xj'|^2 - cut^2) - 2 xi'.xj' in fp32,
-        // x' relative to the box centre; |x'| <= rc over the coverage region.  Each of the
-        // ~10 fp32 operations errs by <= 2^-24 of a term bounded by 3 rc^2: pad cut^2 by
-        // 64 * 2^-24 * 3 rc^2 so no pair with r < a is ever screened out.
-        double rc2 = 0;
-        for (int ax = 0; ax < 3; ++ax) {
-            g.screen_center[ax] = 0.5 * box[ax];
-            const double lo = L0.origin[ax] - g.screen_center[ax];
-            const double hi = L0.origin[ax] + L0.dims[ax] * L0.spacing - g.screen_center[ax];
-            const double m = std::max(std::fabs(lo), std::fabs(hi));
-            rc2 += m * m;
-        }
-        g.screen_cut2 = c.cutoff_a * c.cutoff_a * (1.0 + 1e-6) + 64.0 * std::ldexp(1.0, -24) * 3.0 * rc2;
-    }
     // pair-list skin: the cluster pair list is rebuilt only once some atom moved more
     // than skin/2 since the last build (MSMB_SKIN overrides, 0 = rebuild every evaluation)
     g.skin = 0.2;

@@ -16,7 +16,6 @@ constexpr int kConvB = 16;         // outputs per thread along z in the stencil 
 constexpr int kConvL = 8;          // taps per chunk in the stencil kernel
 constexpr int kConvNWZ = 2;        // warps along z per stencil CTA
 constexpr int kConvZ = kConvB * kConvNWZ;
-constexpr int kAnterpSeg = 16;     // z points per anterpolation thread
 constexpr int kRestrictMax = 8;    // fine indices feeding one coarse index per axis
 constexpr int kOverflowKind = 100; // internal: pair-list capacity exceeded, retry
 
@@ -110,9 +109,8 @@ struct Geometry {
     int64_t ncells = 0;                  // sorted-cell index space
     int64_t ncols = 0;
     double colw = 0;                     // column width in Angstrom
-    double screen_cut = 0;               // fp32 bounding-box cutoff (a + margin)
-    double screen_center[3] = {0, 0, 0}; // fp32 screening coordinates are relative to this point
-    double screen_cut2 = 0;              // a^2 + bound on the fp32 dot-product-form error
+    double screen_cut = 0;               // fp32 bounding-box cutoff (a + margin); the per-atom
+                                         // screen in k_pairs pads its own rounding bound
     double skin = 0;                     // pair-list skin (A): rebuilt once an atom moved > skin/2
     int pair_cap = 0;                    // initial pair-list capacity per cluster
     int64_t lattice_taps_clipped = 0;    // sum over levels 0..l-2 of clipped nonzero taps

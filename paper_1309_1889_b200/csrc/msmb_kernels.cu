@@ -84,8 +84,6 @@ struct BinP {
     double inv_h;
     int d[3];
     int cw, ncx, ncy;
-    double sc[3];  // screening centre
-    float cut2f;   // screening cut^2 (fp32, rounded up)
 };
 
 static float float_ru(double x) { // host: smallest float >= x
@@ -101,8 +99,6 @@ static BinP make_binp(const Geometry& g) {
         p.d[ax] = g.lv[0].dims[ax];
     }
     p.inv_h = g.inv_h0;
-    for (int ax = 0; ax < 3; ++ax) p.sc[ax] = g.screen_center[ax];
-    p.cut2f = float_ru(g.screen_cut2);
     p.cw = g.cw;
     p.ncx = g.ncx;
     p.ncy = g.ncy;
@@ -281,7 +277,7 @@ __global__ void k_cellsort(int64_t ncells, BinP p, const int* __restrict__ start
 __global__ void k_gather(int n, const int* __restrict__ start_total, const int* __restrict__ perm,
                          const double* __restrict__ x, const double* __restrict__ y,
                          const double* __restrict__ z, const double* __restrict__ q, BinP p,
-                         double* xs, double* ys, double* zs, double* qs, float4* f4, double* aw,
+                         double* xs, double* ys, double* zs, double* qs, double* aw,
                          const ErrRec* err) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= *start_total || failed(err)) return;
@@ -326,7 +322,7 @@ int launch_sort(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms&
                                                             c.nat, s.x, s.y, s.z, err);
     if (n == 0) return l + 1;
     k_gather<<<(n + 255) / 256, 256, 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, s.q,
-                                              make_binp(g), a.xs, a.ys, a.zs, a.qs, a.f4, a.aw,
+                                              make_binp(g), a.xs, a.ys, a.zs, a.qs, a.aw,
                                               err);
     return l + 3;
 }
@@ -569,9 +565,6 @@ __global__ void __launch_bounds__(256)
 }
 
 struct PairP {
-    double sc[3];        // screening centre
-    double a2;
-    long long a2bits;
     double c0, c1, c2;   // gamma(r/a)/a = c0 + r2*(c1 + r2*c2)
     double d0, d1;       // g*'(r)/r + 1/r^3 = d0 + r2*d1
     double kc;
@@ -606,64 +599,43 @@ __device__ __forceinline__ void record_pair(ErrRec* err, int i, int j) {
 // One warp per i-cluster (lane = i atom).  The warp walks the i-cluster's j-cluster
 // list (k_pairlist order) through a two-cluster ring in shared memory.  Staging a
 // j-cluster writes its fp32 screening records (-2x', -2y', -2z', |x'|^2 - cut^2;
-// x' relative to the i-cluster) and its fp64 x, y, z, q split into 32-bit rows;
-// ring slot p holds atom t at position 33p + 32 - t and a dummy atom (q = 0, far
-// away) at 33p, so any lane -> position mapping reads a valid record.  Each lane
-// builds a 32-bit in-range mask per staged cluster with packed fp32x2 operations
-// (bit 31 - t <=> atom t).  A pair step takes the lowest set bit of the lane's
-// OLDER cluster mask, or of the newer one once the older is exhausted, or the
-// dummy once both are: no branches, no selects in the fp64 math.  Before a new
-// cluster is staged the older slot is drained -- max over lanes of its popcount
-// steps, during which lanes with nothing left in it already work on the newer
-// cluster -- so lanes stay busy across clusters (k_pairlist puts complementary
-// clusters next to each other).  The fp32 screen admits pairs up to a(1 + ~1e-5)
-// (its rigorous error bound); the reference skips r >= a (src/msm_phases.cpp:240).
-// Those margin pairs are evaluated with the r < a polynomial, and because g* is
-// C^2 at r = a they add O(((r-a)/a)^3) ~ 1e-15 * q_j to phi and O(((r-a)/a)^2) to
-// g*'/r -- orders below the 1e-10 energy / 1e-8 force tolerances
-// (tests/test_gpu_parity.py).  The next j-cluster is prefetched into registers
-// while the current one is processed.  Coincident pairs are caught in k_cellsort.
+// x' relative to the i-cluster) and its fp64 (x, y), (z, q) as double2 rows; ring
+// slot p holds atom t at position 33p + 32 - t and a dummy atom (q = 0, far away)
+// at 33p, so any lane -> position mapping reads a valid record.  Each lane builds a
+// 32-bit in-range mask per staged cluster with packed fp32x2 operations (bit 31 - t
+// <=> atom t).  A pair step takes the highest set bit of the lane's OLDER cluster
+// mask (bfind), or of the newer one once the older is exhausted, or the dummy once
+// both are (bfind of 0 = -1 -> position +0): no branches, no selects in the fp64
+// math, 2 LDS.128 per pair.  Before a new cluster is staged the older slot is
+// drained -- max over lanes of its popcount steps, during which lanes with nothing
+// left in it already work on the newer cluster -- so lanes stay busy across
+// clusters (k_pairlist puts complementary clusters next to each other).  The fp32
+// screen admits pairs up to a(1 + ~1e-5) (its rigorous error bound); the reference
+// skips r >= a (src/msm_phases.cpp:240).  Those margin pairs are evaluated with the
+// r < a polynomial, and because g* is C^2 at r = a they add O(((r-a)/a)^3) ~ 1e-15
+// * q_j to phi and O(((r-a)/a)^2) to g*'/r -- orders below the 1e-10 energy / 1e-8
+// force tolerances (tests/test_gpu_parity.py).  The next j-cluster is prefetched
+// into registers while the current one is processed.  Coincident pairs are caught
+// in k_cellsort.  Measured alternatives on C2-S (ms): 8 LDS.32 per pair 1.013, 4
+// LDS.64 0.963, ffs walk 0.961 (this kernel 0.92); two independent accumulator
+// chains 0.94; 80 / 72 registers (6 / 7 blocks per SM) 0.974 / 0.999.
 constexpr int kSlots = 33;            // one ring slot: dummy + 32 atoms
-constexpr int kRow = 2 * kSlots;      // two ring slots per 32-bit row
+constexpr int kRow = 2 * kSlots;      // two ring slots per double2 row
 #ifndef MSMB_PAIR_MINB
 #define MSMB_PAIR_MINB 5
 #endif
-#ifndef MSMB_PAIR_ILP2
-#define MSMB_PAIR_ILP2 0
-#endif
-#ifndef MSMB_PAIR_CONSTREG
-#define MSMB_PAIR_CONSTREG 1 // pin the kernel constants in registers
-#endif
-#ifndef MSMB_PAIR_FLO
-#define MSMB_PAIR_FLO 1 // highest-bit walk with bfind (measured 0.940 vs 0.961 ms for ffs)
-#endif
-#ifndef MSMB_PAIR_LDS
-#define MSMB_PAIR_LDS 128 // j-data smem layout: 128 = (x,y),(z,q) double2 rows, 2 loads/pair (measured
-                         // 0.958 ms vs 1.013 for 32-bit rows / 8 loads, 0.963 for 4 double rows)
-#endif
 
 __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
-    k_pairs(const int* __restrict__ nclu, const int2* __restrict__ clu,
-            const int* __restrict__ plist, const int* __restrict__ pcnt, int cap,
-            const double* __restrict__ xs, const double* __restrict__ ys,
-            const double* __restrict__ zs, const double* __restrict__ qs,
-            const float4* __restrict__ f4, PairP p, double* phis, double* fsx, double* fsy,
-            double* fsz, const int* __restrict__ col_off, int col_a, int col_b, ErrRec* err) {
+    k_pairs(const int2* __restrict__ clu, const int* __restrict__ plist, const int* __restrict__ pcnt, int cap,
+            const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
+            const double* __restrict__ qs, PairP p, double* phis, double* fsx, double* fsy, double* fsz,
+            const int* __restrict__ col_off, int col_a, int col_b, ErrRec* err) {
     __shared__ __align__(16) float s_sc[kPairWarps][4][32];
-#if MSMB_PAIR_LDS == 32
-    __shared__ unsigned s_w[kPairWarps][8][kRow];
-#elif MSMB_PAIR_LDS == 64
-    __shared__ double s_d[kPairWarps][4][kRow];     // x, y, z, q rows
-#else
-    __shared__ double2 s_v[kPairWarps][2][kRow];    // (x, y), (z, q) rows
-#endif
+    __shared__ double2 s_v[kPairWarps][2][kRow]; // (x, y), (z, q) rows
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ic = col_off[col_a] + blockIdx.x * kPairWarps + w;
     if (ic >= col_off[col_b] || failed(err)) return;
-    double a2 = p.a2, c0 = p.c0, c1 = p.c1, c2 = p.c2, d0 = p.d0, d1 = p.d1;
-#if MSMB_PAIR_CONSTREG
-    asm volatile("" : "+d"(a2), "+d"(c0), "+d"(c1), "+d"(c2), "+d"(d0), "+d"(d1));
-#endif
+    const double c0 = p.c0, c1 = p.c1, c2 = p.c2, d0 = p.d0, d1 = p.d1;
     const int2 c = clu[ic];
     const bool vi = lane < c.y;
     const int si = c.x + (vi ? lane : 0);
@@ -677,13 +649,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     const float ri2 = __uint_as_float(__reduce_max_sync(FULLMASK, __float_as_uint(vi ? nif : 0.f)));
     // dummies at positions 0 and 33: (1e4, 1e4, 1e4) A -- far from every covered
     // particle, so r2 ~ 1e8 keeps g, g' finite -- with q = 0: idle steps add exact zeros
-#if MSMB_PAIR_LDS == 32
-    if (lane < 16) s_w[w][lane & 7][(lane >> 3) * kSlots] = ((lane & 7) == 1 || (lane & 7) == 3 || (lane & 7) == 5) ? 0x40C38800u : 0u;
-#elif MSMB_PAIR_LDS == 64
-    if (lane < 8) s_d[w][lane & 3][(lane >> 2) * kSlots] = (lane & 3) == 3 ? 0.0 : 1e4;
-#else
     if (lane < 4) s_v[w][lane & 1][(lane >> 1) * kSlots] = (lane & 1) ? make_double2(1e4, 0.0) : make_double2(1e4, 1e4);
-#endif
     double ph = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
     unsigned ncand = 0;
     const int nj = pcnt[ic];
@@ -700,22 +666,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         zj_n = zs[sj];
         qj_n = qs[sj];
     };
-#if MSMB_PAIR_LDS == 32
-    const unsigned* row = &s_w[w][0][0];
-#elif MSMB_PAIR_LDS == 64
-    const double* row = &s_d[w][0][0];
-#else
     const double2* row = &s_v[w][0][0];
-#endif
-    unsigned mA = 0, mB = 0; // lane masks of the older / newer staged cluster
-    int pA = 1;              // ring slot of the older cluster (warp-uniform)
-#if MSMB_PAIR_LDS == 128
+    unsigned mA = 0, mB = 0;            // lane masks of the older / newer staged cluster
+    int pA = 1;                         // ring slot of the older cluster (warp-uniform)
     const double2* rowA = row + kSlots; // ring slot pA's rows
     const double2* rowB = row;          // ring slot pA ^ 1's rows
-#endif
-    auto step_acc = [&](double& ph, double& fx, double& fy, double& fz) {
+    auto step = [&]() {
         const bool useA = mA != 0;
-#if MSMB_PAIR_FLO
         // highest set bit (bfind: 0xffffffff when none -> the slot's dummy at +0); clearing
         // it with shl, which PTX clamps to 0 for shift amounts >= 32
         const unsigned m = useA ? mA : mB;
@@ -726,30 +683,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         const unsigned mc = m & ~bit;
         mA = useA ? mc : mA;
         mB = useA ? mB : mc;
-#if MSMB_PAIR_LDS == 128
         const double2* rs = (useA ? rowA : rowB) + (pos + 1);
-#else
-        const int sl = (useA ? pA : pA ^ 1) * kSlots + pos + 1;
-#endif
-#else
-        const int sl = (useA ? pA : pA ^ 1) * kSlots + __ffs(useA ? mA : mB);
-        mA = useA ? (mA & (mA - 1)) : mA;
-        mB = useA ? mB : (mB & (mB - 1));
-#endif
-#if MSMB_PAIR_LDS == 32
-        const double xj = __hiloint2double(row[1 * kRow + sl], row[0 * kRow + sl]);
-        const double yj = __hiloint2double(row[3 * kRow + sl], row[2 * kRow + sl]);
-        const double zj = __hiloint2double(row[5 * kRow + sl], row[4 * kRow + sl]);
-        const double qj = __hiloint2double(row[7 * kRow + sl], row[6 * kRow + sl]);
-#elif MSMB_PAIR_LDS == 64
-        const double xj = row[sl], yj = row[kRow + sl], zj = row[2 * kRow + sl], qj = row[3 * kRow + sl];
-#elif MSMB_PAIR_FLO
         const double2 xy = rs[0], zq = rs[kRow];
         const double xj = xy.x, yj = xy.y, zj = zq.x, qj = zq.y;
-#else
-        const double2 xy = row[sl], zq = row[kRow + sl];
-        const double xj = xy.x, yj = xy.y, zj = zq.x, qj = zq.y;
-#endif
         const double dx = xi - xj, dy = yi - yj, dz = zi - zj;
         const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
         const double rinv = rsqrt_pos(r2);
@@ -762,33 +698,19 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         fy = fma(dy, wgt, fy);
         fz = fma(dz, wgt, fz);
     };
-    auto step = [&]() { step_acc(ph, fx, fy, fz); };
-#if MSMB_PAIR_ILP2
-    double ph2 = 0.0, fx2 = 0.0, fy2 = 0.0, fz2 = 0.0;
-    auto step2x = [&]() { // two independent chains; an odd count starts the newer cluster early
-        step_acc(ph, fx, fy, fz);
-        step_acc(ph2, fx2, fy2, fz2);
-    };
-#endif
     if (nj > 0) fetch(0);
     for (int jj = 0; jj < nj; ++jj) {
         // drain the older cluster; lanes done with it already consume the newer one
         const int dA = __reduce_max_sync(FULLMASK, __popc(mA));
-#if MSMB_PAIR_ILP2
-        for (int k = 0; k < dA; k += 2) step2x();
-#else
         for (int k = 0; k < dA; ++k) step();
-#endif
         mA = mB;
         mB = 0;
         pA ^= 1;
-#if MSMB_PAIR_LDS == 128
         {
             const double2* t = rowA;
             rowA = rowB;
             rowB = t;
         }
-#endif
         const int pB = pA ^ 1; // the freed slot receives cluster jj
         const int jc = jc_n;
         const bool vj = lane < cj_n.y;
@@ -805,24 +727,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         s_sc[w][2][lane] = -2.f * zj;
         s_sc[w][3][lane] = vj ? njf - cut2 : 3e38f;
         const int slot = pB * kSlots + 32 - lane;
-#if MSMB_PAIR_LDS == 32
-        s_w[w][0][slot] = __double2loint(xj_n);
-        s_w[w][1][slot] = __double2hiint(xj_n);
-        s_w[w][2][slot] = __double2loint(yj_n);
-        s_w[w][3][slot] = __double2hiint(yj_n);
-        s_w[w][4][slot] = __double2loint(zj_n);
-        s_w[w][5][slot] = __double2hiint(zj_n);
-        s_w[w][6][slot] = __double2loint(qj_n);
-        s_w[w][7][slot] = __double2hiint(qj_n);
-#elif MSMB_PAIR_LDS == 64
-        s_d[w][0][slot] = xj_n;
-        s_d[w][1][slot] = yj_n;
-        s_d[w][2][slot] = zj_n;
-        s_d[w][3][slot] = qj_n;
-#else
         s_v[w][0][slot] = make_double2(xj_n, yj_n);
         s_v[w][1][slot] = make_double2(zj_n, qj_n);
-#endif
         __syncwarp();
         if (jj + 1 < nj) fetch(jj + 1);
         // ---- screening: bit (31 - t) of mask <=> atom t within the screening cut
@@ -852,15 +758,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         mB = mask;
     }
     const int dAll = __reduce_max_sync(FULLMASK, __popc(mA) + __popc(mB));
-#if MSMB_PAIR_ILP2
-    for (int k = 0; k < dAll; k += 2) step2x();
-    ph += ph2;
-    fx += fx2;
-    fy += fy2;
-    fz += fz2;
-#else
     for (int k = 0; k < dAll; ++k) step();
-#endif
     if (vi) {
         const double kq = -p.kc * qi; // f = d * (-k_C q_i q_j g*'/r)  (msm_phases.cpp:246)
         phis[si] = ph;
@@ -938,8 +836,6 @@ int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& 
                  DevCells& c, ErrRec* err, int cap, const Part& P) {
     const double A = g.cfg.cutoff_a;
     PairP p;
-    p.a2 = A * A;
-    p.a2bits = *reinterpret_cast<const long long*>(&p.a2);
     // gamma(rho)/a = 15/(8a) - 5 r^2/(4a^3) + 3 r^4/(8a^5)          (msm_kernels.hpp:14-20,30-35)
     p.c0 = 15.0 / (8.0 * A);
     p.c1 = -5.0 / (4.0 * A * A * A);
@@ -949,13 +845,12 @@ int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& 
     p.d1 = -1.5 / (A * A * A * A * A);
     p.kc = g.units.coulomb_constant;
     p.cut2f = float_ru(A * A * (1.0 + 1e-6)); // + per-j-cluster rounding pad in k_pairs
-    for (int ax = 0; ax < 3; ++ax) p.sc[ax] = g.screen_center[ax];
     const int64_t maxclu = n / 32 + g.ncols + 1;
     int l = 0;
     if (n > 0) {
         k_pairs<<<int((maxclu + kPairWarps - 1) / kPairWarps), kPairWarps * 32, 0, st>>>(
-            c.nclu, c.clu, c.plist, c.pcnt, cap, a.xc, a.yc, a.zc, a.qc, a.f4, p, a.phis,
-            a.fsx, a.fsy, a.fsz, c.col_off, P.cx0 * g.ncy, P.cx1 * g.ncy, err);
+            c.clu, c.plist, c.pcnt, cap, a.xc, a.yc, a.zc, a.qc, p, a.phis, a.fsx, a.fsy, a.fsz, c.col_off,
+            P.cx0 * g.ncy, P.cx1 * g.ncy, err);
         k_err_brute<<<592, 256, 0, st>>>(n, s.x, s.y, s.z, a.outlist, err);
         l = 2;
     }
@@ -1615,8 +1510,6 @@ static ConvJob make_job(const ConvTable& t, const LevelGeom& lv, const double* q
 // Two stencil variants: 16 outputs per thread (large lattices: fewest loads per
 // FMA) and 8 outputs per thread (small lattices: twice the CTAs).
 constexpr int kConvBSmall = 8;
-constexpr int kConvZSmall = kConvBSmall * kConvNWZ;
-constexpr int64_t kConvBigPoints = 1500000; // level-0 points above which the 16-wide variant is used
 
 size_t conv_smem_bytes(const ConvTable& t) {
     const int SY = 32 + 2 * t.Ry;

@@ -14,7 +14,6 @@ struct DevAtoms {       // sorted-order working set, capacity n
     int* perm;          // [n] sorted slot -> original index
     int* outlist;       // [n] out-of-coverage atoms
     double* xs; double* ys; double* zs; double* qs;  // sorted positions / charges
-    float4* f4;         // sorted fp32 copies (screening)
     double* aw;         // [n*12] anterpolation weights: q*wx[4], wy[4], wz[4]
     double* phis;       // [n] short-range potential (per unit charge), cluster order
     double* fsx; double* fsy; double* fsz; // short-range forces (with k_C), cluster order
