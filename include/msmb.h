@@ -233,7 +233,7 @@ void msmb_reset_stage_times(msmb_field* f);
 /* Work counters of the most recent evaluation: [0] in-cutoff unordered pairs
  * P_u, [1] candidate pair tests, [2] clusters, [3] clipped lattice taps
  * (all levels except the top), [4] top-level taps, [5] kernel launches per
- * evaluation. */
+ * evaluation, [6] pair-list rebuilds since the workspace was created. */
 int msmb_work_counters(msmb_field* f, int64_t* out, int cap);
 /* Device-timed propagate for benchmarking: the same computation as
  * msmb_system_propagate, with CUDA events on the field's stream around the

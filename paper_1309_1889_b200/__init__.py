@@ -270,9 +270,10 @@ class MsmField(ForceField):
         _native.lib().msmb_reset_stage_times(self._h)
 
     def work_counters(self):
-        out = np.zeros(6, dtype=np.int64)
-        _native.lib().msmb_work_counters(self._h, out.ctypes.data_as(C.POINTER(C.c_int64)), 6)
-        keys = ["pairs", "candidates", "clusters", "lattice_taps", "top_taps", "launches_per_eval"]
+        out = np.zeros(7, dtype=np.int64)
+        _native.lib().msmb_work_counters(self._h, out.ctypes.data_as(C.POINTER(C.c_int64)), 7)
+        keys = ["pairs", "candidates", "clusters", "lattice_taps", "top_taps", "launches_per_eval",
+                "list_rebuilds"]
         return dict(zip(keys, map(int, out)))
 
     def kernel_launches(self) -> int:

@@ -211,9 +211,9 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
     c.pcnt = walloc<int>(*W, size_t(W->maxclu));
     c.scan_tmp = walloc<int>(*W, size_t((std::max(g.ncells, g.ncols) + 1 + 4095) / 4096 + 8));
     c.colstart = walloc<int>(*W, size_t(g.ncols + 1));
-    c.flag = walloc<int>(*W, 2);
+    c.flag = walloc<int>(*W, 3);
     ck(cudaMemset(c.nclu, 0, sizeof(int)), "memset");
-    ck(cudaMemset(c.flag, 0, 2 * sizeof(int)), "memset");
+    ck(cudaMemset(c.flag, 0, 3 * sizeof(int)), "memset");
     ck(cudaMemset(c.colstart, 0, sizeof(int) * size_t(g.ncols + 1)), "memset");
     alloc_plist(*W, g.pair_cap);
     DevLevels& L = W->L;
@@ -445,6 +445,9 @@ void record_counters(msmb_field* f, const Workspace& W, const ErrRec& r) {
     f->counters[3] = W.g.lattice_taps_clipped;
     f->counters[4] = W.g.top_taps;
     f->counters[5] = W.launches_eval;
+    int rebuilds = 0;
+    cudaMemcpy(&rebuilds, W.c.flag + 2, sizeof(int), cudaMemcpyDeviceToHost);
+    f->counters[6] = rebuilds;
 }
 
 void grow_cap(Workspace& W, const ErrRec& r) {
@@ -1113,7 +1116,7 @@ void msmb_reset_stage_times(msmb_field* f) {
 }
 
 int msmb_work_counters(msmb_field* f, int64_t* out, int cap) {
-    const int n = std::min(cap, 6);
+    const int n = std::min(cap, 7);
     for (int i = 0; i < n; ++i) out[i] = f->counters[i];
     return n;
 }

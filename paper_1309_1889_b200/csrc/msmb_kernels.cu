@@ -354,7 +354,10 @@ __global__ void k_cl_perm(int64_t n, const int* __restrict__ start_total, const 
     if (!flag[0]) return;
     const int tot = *start_total;
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s == 0) flag[1] = tot;
+    if (s == 0) {
+        flag[1] = tot;
+        flag[2] += 1; // rebuilds since the workspace was created (diagnostics)
+    }
     if (s >= tot) return;
     const int i = perm[s];
     cl_perm[s] = i;

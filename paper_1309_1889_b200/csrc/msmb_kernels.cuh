@@ -37,7 +37,8 @@ struct DevCells {
     int* pcnt;          // [max_clusters]
     int* scan_tmp;      // scratch for the multi-block scan
     int* colstart;      // [ncols+1] first cluster slot of each pair column (frozen at rebuild)
-    int* flag;          // [2] [0] rebuild the pair list this evaluation, [1] clustered atoms
+    int* flag;          // [3] [0] rebuild the pair list this evaluation, [1] clustered atoms,
+                        //     [2] rebuild count (diagnostics)
 };
 
 struct DevLevels {      // concatenated lattices + tables

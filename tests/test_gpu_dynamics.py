@@ -141,3 +141,27 @@ def test_parareal_config_validation():
     cfg = pkg.PararealConfig(2, 1, 1e-6, pkg.PropagatorSpec(F, 0.5, 4), pkg.PropagatorSpec(F, 1.0, 3))
     with pytest.raises(pkg.ConfigError, match="span different slice lengths"):
         pkg.parareal_window(s, cfg, 2, 1)
+
+
+def test_pair_list_rebuilds_mid_trajectory(port):
+    # a tiny skin makes the displacement check trigger several rebuilds inside one
+    # propagate (graph-captured steps); the trajectory must still match the oracle,
+    # and a skin-0 run (rebuild every evaluation) to rounding
+    w = fx.config("c1s", n_override=2000)
+    dt, steps = 0.05, 40
+    s = pkg.ParticleSystem(w.pos, w.vel, w.q, w.mass, w.box)
+    runs = {}
+    for skin in (0.002, 0.0):
+        f = pkg.MsmField(pkg.MsmConfig(w.a, w.h, w.levels))
+        f.set_pair_skin(skin)
+        ds = pkg.DeviceSystem(f, s)
+        ds.propagate(dt, steps)
+        runs[skin] = (ds.download(), f.work_counters()["list_rebuilds"])
+    (p1, v1), nreb = runs[0.002]
+    (p0, v0), nreb0 = runs[0.0]
+    assert 2 < nreb < steps + 1       # rebuilt more than once, but not at every evaluation
+    assert nreb0 == steps + 1         # skin 0: every evaluation
+    assert rel_rms(p1, p0) <= 1e-13 and rel_rms(v1, v0) <= 1e-11
+    pp, vv, done, err = port.propagate(w.pos, w.vel, w.q, w.mass, w.box, w.a, w.h, w.levels, dt, steps)
+    assert err is None and done == steps
+    assert rel_rms(p1, pp) <= 1e-8 and rel_rms(v1, vv) <= 1e-8
