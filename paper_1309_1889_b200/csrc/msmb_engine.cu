@@ -148,6 +148,8 @@ static void alloc_plist(Workspace& W, int cap) {
     W.cap = cap;
     ck(W.plist_buf.alloc(sizeof(int) * size_t(W.maxclu) * size_t(cap)), "cudaMalloc plist");
     W.c.plist = W.plist_buf.as<int>();
+    ck(W.pmask_buf.alloc(sizeof(unsigned) * 32 * size_t(W.maxclu) * size_t(cap)), "cudaMalloc pmask");
+    W.c.pmask = W.pmask_buf.as<unsigned>();
 }
 
 static std::atomic<uint64_t> g_ws_uid{1};

@@ -71,6 +71,7 @@ struct Workspace {
     DevOut o{};
     std::vector<std::unique_ptr<DBuf>> bufs; // owns everything above
     DBuf plist_buf;
+    DBuf pmask_buf;
     DBuf backup;   // 6n doubles: initial x,y,z,vx,vy,vz of a propagate call
     DBuf staging;  // 3n doubles: AoS transfers
     ErrRec* err = nullptr;

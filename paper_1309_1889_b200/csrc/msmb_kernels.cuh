@@ -35,6 +35,7 @@ struct DevCells {
     int* nclu;          // [1]
     int* plist;         // [max_clusters * cap]
     int* pcnt;          // [max_clusters]
+    unsigned* pmask;    // [max_clusters * cap * 32] per-lane j-atom masks (k_pairmask)
     int* scan_tmp;      // scratch for the multi-block scan
     int* colstart;      // [ncols+1] first cluster slot of each pair column (frozen at rebuild)
     int* flag;          // [3] [0] rebuild the pair list this evaluation, [1] clustered atoms,
