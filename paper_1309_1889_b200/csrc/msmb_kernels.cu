@@ -599,195 +599,15 @@ __device__ __forceinline__ void record_pair(ErrRec* err, int i, int j) {
     atomicMin(&err->pair_key, (lo << 32) | hi);
 }
 
-// One warp per i-cluster (lane = i atom).  The warp walks the i-cluster's j-cluster
-// list (k_pairlist order) through a two-cluster ring in shared memory.  Staging a
-// j-cluster writes its fp32 screening records (-2x', -2y', -2z', |x'|^2 - cut^2;
-// x' relative to the i-cluster) and its fp64 (x, y), (z, q) as double2 rows; ring
-// slot p holds atom t at position 33p + 32 - t and a dummy atom (q = 0, far away)
-// at 33p, so any lane -> position mapping reads a valid record.  Each lane builds a
-// 32-bit in-range mask per staged cluster with packed fp32x2 operations (bit 31 - t
-// <=> atom t).  A pair step takes the highest set bit of the lane's OLDER cluster
-// mask (bfind), or of the newer one once the older is exhausted, or the dummy once
-// both are (bfind of 0 = -1 -> position +0): no branches, no selects in the fp64
-// math, 2 LDS.128 per pair.  Before a new cluster is staged the older slot is
-// drained -- max over lanes of its popcount steps, during which lanes with nothing
-// left in it already work on the newer cluster -- so lanes stay busy across
-// clusters (k_pairlist puts complementary clusters next to each other).  The fp32
-// screen admits pairs up to a(1 + ~1e-5) (its rigorous error bound); the reference
-// skips r >= a (src/msm_phases.cpp:240).  Those margin pairs are evaluated with the
-// r < a polynomial, and because g* is C^2 at r = a they add O(((r-a)/a)^3) ~ 1e-15
-// * q_j to phi and O(((r-a)/a)^2) to g*'/r -- orders below the 1e-10 energy / 1e-8
-// force tolerances (tests/test_gpu_parity.py).  The next j-cluster is prefetched
-// into registers while the current one is processed.  Coincident pairs are caught
-// in k_cellsort.  Measured alternatives on C2-S (ms): 8 LDS.32 per pair 1.013, 4
-// LDS.64 0.963, ffs walk 0.961 (this kernel 0.92); two independent accumulator
-// chains 0.94; 80 / 72 registers (6 / 7 blocks per SM) 0.974 / 0.999.
+// Short-range pair sum in two kernels over the cluster pair list of
+// k_pairlist: k_pairmask (list rebuilds only) turns every entry into per-lane
+// 32-bit masks of the j-cluster atoms within a + skin; k_pairs_mw (every
+// evaluation) walks them.  Measured history on C2-S (pairs, ms): two-slot drain
+// ring with in-kernel fp32 screening 0.92; per-lane walk with in-kernel
+// screening 0.92 (screening was 36% of the instructions); masks + walk 0.64.
 constexpr int kSlots = 33;            // one ring slot: dummy + 32 atoms
-constexpr int kRow = 2 * kSlots;      // two ring slots per double2 row
 #ifndef MSMB_PAIR_MINB
 #define MSMB_PAIR_MINB 5
-#endif
-
-__global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
-    k_pairs(const int2* __restrict__ clu, const int* __restrict__ plist, const int* __restrict__ pcnt, int cap,
-            const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
-            const double* __restrict__ qs, PairP p, double* phis, double* fsx, double* fsy, double* fsz,
-            const int* __restrict__ col_off, int col_a, int col_b, ErrRec* err) {
-    __shared__ __align__(16) float s_sc[kPairWarps][4][32];
-    __shared__ double2 s_v[kPairWarps][2][kRow]; // (x, y), (z, q) rows
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ic = col_off[col_a] + blockIdx.x * kPairWarps + w;
-    if (ic >= col_off[col_b] || failed(err)) return;
-    const double c0 = p.c0, c1 = p.c1, c2 = p.c2, d0 = p.d0, d1 = p.d1;
-    const int2 c = clu[ic];
-    const bool vi = lane < c.y;
-    const int si = c.x + (vi ? lane : 0);
-    const double xi = xs[si], yi = ys[si], zi = zs[si], qi = qs[si];
-    // fp32 screening coordinates relative to the i-cluster's first atom (|x'| ~ tens of A)
-    const double rx = xs[c.x], ry = ys[c.x], rz = zs[c.x];
-    const float xf = float(xi - rx), yf = float(yi - ry), zf = float(zi - rz);
-    const float2 xi2 = make_float2(xf, xf), yi2 = make_float2(yf, yf), zi2 = make_float2(zf, zf);
-    const float nif = fmaf(zf, zf, fmaf(yf, yf, xf * xf));
-    const float2 ni2 = make_float2(nif, nif);
-    const float ri2 = __uint_as_float(__reduce_max_sync(FULLMASK, __float_as_uint(vi ? nif : 0.f)));
-    // dummies at positions 0 and 33: (1e4, 1e4, 1e4) A -- far from every covered
-    // particle, so r2 ~ 1e8 keeps g, g' finite -- with q = 0: idle steps add exact zeros
-    if (lane < 4) s_v[w][lane & 1][(lane >> 1) * kSlots] = (lane & 1) ? make_double2(1e4, 0.0) : make_double2(1e4, 1e4);
-    double ph = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
-    unsigned ncand = 0;
-    const int nj = pcnt[ic];
-    const int* pl = plist + size_t(ic) * cap;
-    int jc_n = 0;
-    int2 cj_n = make_int2(0, 0);
-    double xj_n = 0, yj_n = 0, zj_n = 0, qj_n = 0;
-    auto fetch = [&](int jj) {
-        jc_n = pl[jj];
-        cj_n = clu[jc_n];
-        const int sj = cj_n.x + (lane < cj_n.y ? lane : 0);
-        xj_n = xs[sj];
-        yj_n = ys[sj];
-        zj_n = zs[sj];
-        qj_n = qs[sj];
-    };
-    const double2* row = &s_v[w][0][0];
-    unsigned mA = 0, mB = 0;            // lane masks of the older / newer staged cluster
-    int pA = 1;                         // ring slot of the older cluster (warp-uniform)
-    const double2* rowA = row + kSlots; // ring slot pA's rows
-    const double2* rowB = row;          // ring slot pA ^ 1's rows
-    auto step = [&]() {
-        const bool useA = mA != 0;
-        // highest set bit (bfind: 0xffffffff when none -> the slot's dummy at +0); clearing
-        // it with shl, which PTX clamps to 0 for shift amounts >= 32
-        const unsigned m = useA ? mA : mB;
-        int pos;
-        asm("bfind.u32 %0, %1;" : "=r"(pos) : "r"(m));
-        unsigned bit;
-        asm("shl.b32 %0, %1, %2;" : "=r"(bit) : "r"(1u), "r"(pos));
-        const unsigned mc = m & ~bit;
-        mA = useA ? mc : mA;
-        mB = useA ? mB : mc;
-        const double2* rs = (useA ? rowA : rowB) + (pos + 1);
-        const double2 xy = rs[0], zq = rs[kRow];
-        const double xj = xy.x, yj = xy.y, zj = zq.x, qj = zq.y;
-        const double dx = xi - xj, dy = yi - yj, dz = zi - zj;
-        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-        const double rinv = rsqrt_pos(r2);
-        const double rinv2 = rinv * rinv;
-        const double g = rinv - fma(r2, fma(r2, c2, c1), c0);   // g*(r)
-        const double sd = fma(-rinv, rinv2, fma(r2, d1, d0));  // g*'(r)/r
-        ph = fma(qj, g, ph);
-        const double wgt = qj * sd;
-        fx = fma(dx, wgt, fx);
-        fy = fma(dy, wgt, fy);
-        fz = fma(dz, wgt, fz);
-    };
-    if (nj > 0) fetch(0);
-    for (int jj = 0; jj < nj; ++jj) {
-        // drain the older cluster; lanes done with it already consume the newer one
-        const int dA = __reduce_max_sync(FULLMASK, __popc(mA));
-        for (int k = 0; k < dA; ++k) step();
-        mA = mB;
-        mB = 0;
-        pA ^= 1;
-        {
-            const double2* t = rowA;
-            rowA = rowB;
-            rowB = t;
-        }
-        const int pB = pA ^ 1; // the freed slot receives cluster jj
-        const int jc = jc_n;
-        const bool vj = lane < cj_n.y;
-        // screening record of this lane's j atom.  The fp32 evaluation of
-        // r^2 - cut^2 = |xi'|^2 + |xj'|^2 - 2 xi'.xj' - cut^2 errs by
-        // < 16 * 2^-24 * (|xi'| + |xj'|)^2; cut^2 is padded by twice that (uniform per j-cluster).
-        const float xj = float(xj_n - rx), yj = float(yj_n - ry), zj = float(zj_n - rz);
-        const float njf = fmaf(zj, zj, fmaf(yj, yj, xj * xj));
-        const float rj2 = __uint_as_float(__reduce_max_sync(FULLMASK, __float_as_uint(vj ? njf : 0.f)));
-        const float cut2 = p.cut2f + 64.f * 5.9604645e-8f * (ri2 + rj2);
-        __syncwarp();
-        s_sc[w][0][lane] = -2.f * xj;
-        s_sc[w][1][lane] = -2.f * yj;
-        s_sc[w][2][lane] = -2.f * zj;
-        s_sc[w][3][lane] = vj ? njf - cut2 : 3e38f;
-        const int slot = pB * kSlots + 32 - lane;
-        s_v[w][0][slot] = make_double2(xj_n, yj_n);
-        s_v[w][1][slot] = make_double2(zj_n, qj_n);
-        __syncwarp();
-        if (jj + 1 < nj) fetch(jj + 1);
-        // ---- screening: bit (31 - t) of mask <=> atom t within the screening cut
-        unsigned mask = 0;
-#pragma unroll
-        for (int t = 0; t < 32; t += 4) {
-            const float4 mx = *reinterpret_cast<const float4*>(&s_sc[w][0][t]);
-            const float4 my = *reinterpret_cast<const float4*>(&s_sc[w][1][t]);
-            const float4 mz = *reinterpret_cast<const float4*>(&s_sc[w][2][t]);
-            const float4 cc = *reinterpret_cast<const float4*>(&s_sc[w][3][t]);
-            float2 sa = __fadd2_rn(ni2, make_float2(cc.x, cc.y));
-            float2 sb = __fadd2_rn(ni2, make_float2(cc.z, cc.w));
-            sa = __ffma2_rn(make_float2(mx.x, mx.y), xi2, sa);
-            sb = __ffma2_rn(make_float2(mx.z, mx.w), xi2, sb);
-            sa = __ffma2_rn(make_float2(my.x, my.y), yi2, sa);
-            sb = __ffma2_rn(make_float2(my.z, my.w), yi2, sb);
-            sa = __ffma2_rn(make_float2(mz.x, mz.y), zi2, sa);
-            sb = __ffma2_rn(make_float2(mz.z, mz.w), zi2, sb);
-            mask = (mask << 1) | (__float_as_uint(sa.x) >> 31);
-            mask = (mask << 1) | (__float_as_uint(sa.y) >> 31);
-            mask = (mask << 1) | (__float_as_uint(sb.x) >> 31);
-            mask = (mask << 1) | (__float_as_uint(sb.y) >> 31);
-        }
-        if (!vi) mask = 0;
-        if (jc == ic) mask &= ~(0x80000000u >> lane);
-        ncand += __popc(mask);
-        mB = mask;
-    }
-    const int dAll = __reduce_max_sync(FULLMASK, __popc(mA) + __popc(mB));
-    for (int k = 0; k < dAll; ++k) step();
-    if (vi) {
-        const double kq = -p.kc * qi; // f = d * (-k_C q_i q_j g*'/r)  (msm_phases.cpp:246)
-        phis[si] = ph;
-        fsx[si] = fx * kq;
-        fsy[si] = fy * kq;
-        fsz[si] = fz * kq;
-    }
-    ncand = __reduce_add_sync(FULLMASK, ncand);
-    if (lane == 0) {
-        atomicAdd(&err->pairs, (unsigned long long)ncand);
-        atomicAdd(&err->candidates, (unsigned long long)ncand);
-    }
-}
-
-// Per-lane walk over a ring of kRing staged j-clusters.  Same screening, ring-slot
-// layout and pair arithmetic as k_pairs, but each lane walks the whole list on its
-// own: it holds a cursor c (list position of the cluster it consumes) and that
-// cluster's remaining mask; when the mask empties it moves to the next staged
-// cluster (masks kept per (slot, lane) in shared memory).  The warp stages a new
-// cluster whenever the slowest lane's cluster is less than kRing behind the staging
-// frontier, so a lane only idles when it is kRing clusters ahead of the slowest
-// one or at the end of the list -- instead of at every drain of the two-slot ring.
-// Per lane, pairs are still accumulated in list order, atoms of a cluster in
-// ascending order: the result is bit-identical to k_pairs.
-#ifndef MSMB_PAIR_MASK
-#define MSMB_PAIR_MASK 1
 #endif
 #ifndef MSMB_PAIR_RING
 #define MSMB_PAIR_RING 8
@@ -797,162 +617,6 @@ static_assert((kRing & (kRing - 1)) == 0, "ring size must be a power of two");
 #ifndef MSMB_PAIR_UNROLL
 #define MSMB_PAIR_UNROLL 4
 #endif
-
-__global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
-    k_pairs_walk(const int2* __restrict__ clu, const int* __restrict__ plist, const int* __restrict__ pcnt, int cap,
-                 const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
-                 const double* __restrict__ qs, PairP p, double* phis, double* fsx, double* fsy, double* fsz,
-                 const int* __restrict__ col_off, int col_a, int col_b, ErrRec* err) {
-    __shared__ __align__(16) float s_sc[kPairWarps][4][32];
-    __shared__ unsigned s_mask[kPairWarps][kRing][32];
-    __shared__ double2 s_v[kPairWarps][2][kRing * kSlots]; // (x, y), (z, q) rows
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ic = col_off[col_a] + blockIdx.x * kPairWarps + w;
-    if (ic >= col_off[col_b] || failed(err)) return;
-    const double c0 = p.c0, c1 = p.c1, c2 = p.c2, d0 = p.d0, d1 = p.d1;
-    const int2 c = clu[ic];
-    const bool vi = lane < c.y;
-    const int si = c.x + (vi ? lane : 0);
-    const double xi = xs[si], yi = ys[si], zi = zs[si], qi = qs[si];
-    const double rx = xs[c.x], ry = ys[c.x], rz = zs[c.x];
-    const float xf = float(xi - rx), yf = float(yi - ry), zf = float(zi - rz);
-    const float2 xi2 = make_float2(xf, xf), yi2 = make_float2(yf, yf), zi2 = make_float2(zf, zf);
-    const float nif = fmaf(zf, zf, fmaf(yf, yf, xf * xf));
-    const float2 ni2 = make_float2(nif, nif);
-    const float ri2 = __uint_as_float(__reduce_max_sync(FULLMASK, __float_as_uint(vi ? nif : 0.f)));
-    for (int s = lane; s < 2 * kRing; s += 32) // dummies (q = 0, far away) at each slot's position 0
-        s_v[w][s & 1][(s >> 1) * kSlots] = (s & 1) ? make_double2(1e4, 0.0) : make_double2(1e4, 1e4);
-    double ph = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
-    unsigned ncand = 0;
-    const int nj = pcnt[ic];
-    const int* pl = plist + size_t(ic) * cap;
-    int jc_n = 0;
-    int2 cj_n = make_int2(0, 0);
-    double xj_n = 0, yj_n = 0, zj_n = 0, qj_n = 0;
-    auto fetch = [&](int jj) {
-        jc_n = pl[jj];
-        cj_n = clu[jc_n];
-        const int sj = cj_n.x + (lane < cj_n.y ? lane : 0);
-        xj_n = xs[sj];
-        yj_n = ys[sj];
-        zj_n = zs[sj];
-        qj_n = qs[sj];
-    };
-    // stage list entry jj (already fetched) into ring slot jj % kRing, prefetch jj + 1
-    auto stage = [&](int jj) {
-        const int slot = jj & (kRing - 1);
-        const int jc = jc_n;
-        const bool vj = lane < cj_n.y;
-        const float xj = float(xj_n - rx), yj = float(yj_n - ry), zj = float(zj_n - rz);
-        const float njf = fmaf(zj, zj, fmaf(yj, yj, xj * xj));
-        const float rj2 = __uint_as_float(__reduce_max_sync(FULLMASK, __float_as_uint(vj ? njf : 0.f)));
-        const float cut2 = p.cut2f + 64.f * 5.9604645e-8f * (ri2 + rj2);
-        __syncwarp();
-        s_sc[w][0][lane] = -2.f * xj;
-        s_sc[w][1][lane] = -2.f * yj;
-        s_sc[w][2][lane] = -2.f * zj;
-        s_sc[w][3][lane] = vj ? njf - cut2 : 3e38f;
-        const int pos = slot * kSlots + 32 - lane;
-        s_v[w][0][pos] = make_double2(xj_n, yj_n);
-        s_v[w][1][pos] = make_double2(zj_n, qj_n);
-        __syncwarp();
-        if (jj + 1 < nj) fetch(jj + 1);
-        unsigned mask = 0;
-#pragma unroll
-        for (int t = 0; t < 32; t += 4) {
-            const float4 mx = *reinterpret_cast<const float4*>(&s_sc[w][0][t]);
-            const float4 my = *reinterpret_cast<const float4*>(&s_sc[w][1][t]);
-            const float4 mz = *reinterpret_cast<const float4*>(&s_sc[w][2][t]);
-            const float4 cc = *reinterpret_cast<const float4*>(&s_sc[w][3][t]);
-            float2 sa = __fadd2_rn(ni2, make_float2(cc.x, cc.y));
-            float2 sb = __fadd2_rn(ni2, make_float2(cc.z, cc.w));
-            sa = __ffma2_rn(make_float2(mx.x, mx.y), xi2, sa);
-            sb = __ffma2_rn(make_float2(mx.z, mx.w), xi2, sb);
-            sa = __ffma2_rn(make_float2(my.x, my.y), yi2, sa);
-            sb = __ffma2_rn(make_float2(my.z, my.w), yi2, sb);
-            sa = __ffma2_rn(make_float2(mz.x, mz.y), zi2, sa);
-            sb = __ffma2_rn(make_float2(mz.z, mz.w), zi2, sb);
-            mask = (mask << 1) | (__float_as_uint(sa.x) >> 31);
-            mask = (mask << 1) | (__float_as_uint(sa.y) >> 31);
-            mask = (mask << 1) | (__float_as_uint(sb.x) >> 31);
-            mask = (mask << 1) | (__float_as_uint(sb.y) >> 31);
-        }
-        if (!vi) mask = 0;
-        if (jc == ic) mask &= ~(0x80000000u >> lane);
-        ncand += __popc(mask);
-        s_mask[w][slot][lane] = mask;
-    };
-    const double2* rows = &s_v[w][0][0];
-    int hi = 0;          // clusters staged so far (warp-uniform)
-    int cur = 0;         // this lane's list position
-    unsigned m = 0;      // this lane's remaining mask of cluster `cur`
-    unsigned mnext = 0;  // mask of cluster cur + 1 (valid while cur + 1 < hi)
-    const double2* row = rows;
-    // branch-free: an exhausted lane moves to the next staged cluster (a cluster
-    // without in-range atoms for the lane costs it one idle step)
-    auto advance = [&]() {
-        const bool adv = (m == 0) & (cur + 1 < hi);
-        cur += adv ? 1 : 0;
-        m = adv ? mnext : m;
-        row = rows + (cur & (kRing - 1)) * kSlots;
-        mnext = s_mask[w][(cur + 1) & (kRing - 1)][lane];
-    };
-    auto step = [&]() {
-        int pos;
-        asm("bfind.u32 %0, %1;" : "=r"(pos) : "r"(m));
-        unsigned bit;
-        asm("shl.b32 %0, %1, %2;" : "=r"(bit) : "r"(1u), "r"(pos));
-        m &= ~bit;
-        const double2* rs = row + (pos + 1);
-        const double2 xy = rs[0], zq = rs[kRing * kSlots];
-        advance();
-        const double xj = xy.x, yj = xy.y, zj = zq.x, qj = zq.y;
-        const double dx = xi - xj, dy = yi - yj, dz = zi - zj;
-        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-        const double rinv = rsqrt_pos(r2);
-        const double rinv2 = rinv * rinv;
-        const double g = rinv - fma(r2, fma(r2, c2, c1), c0);   // g*(r)
-        const double sd = fma(-rinv, rinv2, fma(r2, d1, d0));  // g*'(r)/r
-        ph = fma(qj, g, ph);
-        const double wgt = qj * sd;
-        fx = fma(dx, wgt, fx);
-        fy = fma(dy, wgt, fy);
-        fz = fma(dz, wgt, fz);
-    };
-    if (nj > 0) {
-        fetch(0);
-        while (hi < nj && hi < kRing) stage(hi++);
-        __syncwarp();
-        m = s_mask[w][0][lane];
-        mnext = s_mask[w][1][lane];
-        for (;;) {
-#pragma unroll
-            for (int u = 0; u < MSMB_PAIR_UNROLL; ++u) step();
-            const int lo = __reduce_min_sync(FULLMASK, cur);
-            if (hi < nj && hi - lo < kRing) {
-                do stage(hi++);
-                while (hi < nj && hi - lo < kRing);
-                __syncwarp();
-                mnext = s_mask[w][(cur + 1) & (kRing - 1)][lane];
-                advance();
-            }
-            // every lane idle at the staging frontier and the whole list staged
-            if (hi >= nj && __all_sync(FULLMASK, m == 0 && cur + 1 >= hi)) break;
-        }
-    }
-    if (vi) {
-        const double kq = -p.kc * qi; // f = d * (-k_C q_i q_j g*'/r)  (msm_phases.cpp:246)
-        phis[si] = ph;
-        fsx[si] = fx * kq;
-        fsy[si] = fy * kq;
-        fsz[si] = fz * kq;
-    }
-    ncand = __reduce_add_sync(FULLMASK, ncand);
-    if (lane == 0) {
-        atomicAdd(&err->pairs, (unsigned long long)ncand);
-        atomicAdd(&err->candidates, (unsigned long long)ncand);
-    }
-}
 
 // Per-lane pair masks, built once per pair-list rebuild (flag[0]): for every list
 // entry of an i-cluster, lane i's 32-bit mask of the j-cluster atoms within the
@@ -1033,14 +697,22 @@ __global__ void __launch_bounds__(kMaskWarps * 32)
     if (lane == 0) pcnt[ic] = out;
 }
 
-// k_pairs_walk over the masks of k_pairmask: staging a j-cluster is a copy of its
-// atoms and of the lane masks into the ring (no screening), and each pair step
-// applies the exact cutoff r^2 < a^2 in fp64 (pairs in the skin shell add exact
-// zeros, as the reference skips r >= a, src/msm_phases.cpp:240).  Per lane the
-// pairs are accumulated in list order, atoms of a cluster in ascending order.
-#ifndef MSMB_PAIR_COUNT
-#define MSMB_PAIR_COUNT 1
-#endif
+// One warp per i-cluster (lane = i atom) walks the i-cluster's mask list.  The warp
+// stages j-clusters into a ring of kRing slots in shared memory: fp64 (x, y) and
+// (z, q) as double2 rows, atom t at slot position 32 - t and a dummy atom (q = 0,
+// far away) at position 0, plus each lane's mask.  Every lane walks the list on
+// its own: it holds the list position `cur` of the cluster it consumes and that
+// cluster's remaining mask; a pair step takes the highest set bit (bfind; bit
+// 31 - t <=> atom t), or the dummy once the mask is empty (bfind(0) = -1), and an
+// exhausted lane moves to the next staged cluster (branch-free; a cluster without
+// atoms for the lane costs it one idle step).  The warp stages more clusters once
+// the slowest lane is less than kRing clusters behind the staging frontier, so
+// lanes only idle at the end of the list.  Each pair step applies the exact cutoff
+// r^2 < a^2 in fp64 as a predicate on the accumulation: skin-shell pairs and the
+// dummy add nothing, as the reference skips r >= a (src/msm_phases.cpp:240).  Per
+// lane the pairs are accumulated in list order, atoms of a cluster in ascending
+// order: the sums are deterministic.  rsqrt is MUFU.RSQ64H + one cubic Newton step
+// (rsqrt_pos); 22 DP instructions + 1 DSETP per pair step.
 __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     k_pairs_mw(const int2* __restrict__ clu, const int* __restrict__ plist, const int* __restrict__ pcnt,
                const unsigned* __restrict__ pmask, int cap, const double* __restrict__ xs,
@@ -1101,21 +773,19 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         asm("bfind.u32 %0, %1;" : "=r"(pos) : "r"(m));
         unsigned bit;
         asm("shl.b32 %0, %1, %2;" : "=r"(bit) : "r"(1u), "r"(pos));
-        m &= ~bit;
+        m ^= bit; // bit = 0 when m == 0 (shl clamps): the dummy step leaves m at 0
         const double2* rs = row + (pos + 1);
         const double2 xy = rs[0], zq = rs[kRing * kSlots];
         advance();
         const double dx = xi - xy.x, dy = yi - xy.y, dz = zi - zq.x;
         const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-        const bool in = r2 < a2;
-#if MSMB_PAIR_COUNT
-        npair += in ? 1u : 0u;
-#endif
-        const double qj = in ? zq.y : 0.0;
         const double rinv = rsqrt_pos(r2);
         const double rinv2 = rinv * rinv;
         const double g = rinv - fma(r2, fma(r2, c2, c1), c0);   // g*(r)
         const double sd = fma(-rinv, rinv2, fma(r2, d1, d0));  // g*'(r)/r
+        const bool in = r2 < a2;
+        npair += in ? 1u : 0u;
+        const double qj = in ? zq.y : 0.0; // two FSELs (a predicated accumulation costs 8)
         ph = fma(qj, g, ph);
         const double wgt = qj * sd;
         fx = fma(dx, wgt, fx);
@@ -1215,7 +885,6 @@ int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevStat
     k_pairlist<<<int((maxclu * 32 + 255) / 256), 256, 0, st>>>(c.nclu, c.blo, c.bhi, c.col_off, c.start, lp,
                                                                 c.plist, c.pcnt, cap, P.cx0 * g.ncy,
                                                                 P.cx1 * g.ncy, c.flag, err);
-#if MSMB_PAIR_MASK
     {
         const double lm = g.cfg.cutoff_a + g.skin; // mask cut: a + skin (+ the fp32 pad in k_pairmask)
         k_pairmask<<<int((maxclu + kMaskWarps - 1) / kMaskWarps), kMaskWarps * 32, 0, st>>>(
@@ -1223,7 +892,6 @@ int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevStat
             P.cx0 * g.ncy, P.cx1 * g.ncy, c.flag, err);
         ++l;
     }
-#endif
     return l + 3;
 }
 
@@ -1243,15 +911,9 @@ int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& 
     const int64_t maxclu = n / 32 + g.ncols + 1;
     int l = 0;
     if (n > 0) {
-#if MSMB_PAIR_MASK
         k_pairs_mw<<<int((maxclu + kPairWarps - 1) / kPairWarps), kPairWarps * 32, 0, st>>>(
             c.clu, c.plist, c.pcnt, c.pmask, cap, a.xc, a.yc, a.zc, a.qc, p, A * A, a.phis, a.fsx, a.fsy, a.fsz,
             c.col_off, P.cx0 * g.ncy, P.cx1 * g.ncy, n, err);
-#else
-        (kRing > 2 ? k_pairs_walk : k_pairs)<<<int((maxclu + kPairWarps - 1) / kPairWarps), kPairWarps * 32, 0, st>>>(
-            c.clu, c.plist, c.pcnt, cap, a.xc, a.yc, a.zc, a.qc, p, a.phis, a.fsx, a.fsy, a.fsz, c.col_off,
-            P.cx0 * g.ncy, P.cx1 * g.ncy, err);
-#endif
         k_err_brute<<<592, 256, 0, st>>>(n, s.x, s.y, s.z, a.outlist, err);
         l = 2;
     }
