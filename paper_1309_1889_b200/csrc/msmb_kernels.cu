@@ -618,14 +618,14 @@ static_assert((kRing & (kRing - 1)) == 0, "ring size must be a power of two");
 #define MSMB_PAIR_UNROLL 4
 #endif
 
-// Per-lane pair masks, built once per pair-list rebuild (flag[0]): for every list
-// entry of an i-cluster, lane i's 32-bit mask of the j-cluster atoms within the
-// list cut a + skin (fp32 screen with the rigorous rounding pad of k_pairs).  A
-// pair within a at any evaluation before the next rebuild is within a + skin at
-// the build (the rebuild trigger is a move of skin/2), so the masks stay complete
-// until then; k_pairs_mw applies the exact r < a test in fp64.  Entries whose
-// masks are empty for every lane are dropped (in-place compaction), and each entry
-// becomes the j-cluster's first sorted slot (the atoms k_pairs_mw stages).
+// Pair masks, built once per pair-list rebuild (flag[0]): for every list entry of
+// an i-cluster, each lane's 32-bit mask of the j-cluster atoms within the list cut
+// a + skin (fp32 screen with the rigorous rounding pad).  A pair within a at any
+// evaluation before the next rebuild is within a + skin at the build (the rebuild
+// trigger is a move of skin/2), so the masks stay complete until then; k_pairs_mw
+// applies the exact r < a test in fp64.  Entries whose masks are empty for every
+// lane are dropped (in-place compaction), as is the i-cluster's own entry (summed
+// densely by k_pairs_mw), and each entry becomes the j-cluster's first sorted slot.
 constexpr int kMaskWarps = 8;
 __global__ void __launch_bounds__(kMaskWarps * 32)
     k_pairmask(const int2* __restrict__ clu, int* plist, int* pcnt, unsigned* __restrict__ pmask, int cap,
@@ -686,8 +686,7 @@ __global__ void __launch_bounds__(kMaskWarps * 32)
             mask = (mask << 1) | (__float_as_uint(sb.x) >> 31);
             mask = (mask << 1) | (__float_as_uint(sb.y) >> 31);
         }
-        if (!vi) mask = 0;
-        if (jc == ic) mask &= ~(0x80000000u >> lane);
+        if (!vi || jc == ic) mask = 0; // the own cluster is summed densely by k_pairs_mw
         if (__any_sync(FULLMASK, mask != 0)) {
             pm[size_t(out) * 32 + lane] = mask;
             if (lane == 0) pl[out] = cj.x;
@@ -708,11 +707,15 @@ __global__ void __launch_bounds__(kMaskWarps * 32)
 // atoms for the lane costs it one idle step).  The warp stages more clusters once
 // the slowest lane is less than kRing clusters behind the staging frontier, so
 // lanes only idle at the end of the list.  Each pair step applies the exact cutoff
-// r^2 < a^2 in fp64 as a predicate on the accumulation: skin-shell pairs and the
-// dummy add nothing, as the reference skips r >= a (src/msm_phases.cpp:240).  Per
-// lane the pairs are accumulated in list order, atoms of a cluster in ascending
-// order: the sums are deterministic.  rsqrt is MUFU.RSQ64H + one cubic Newton step
-// (rsqrt_pos); 22 DP instructions + 1 DSETP per pair step.
+// r^2 < a^2 in fp64: skin-shell pairs and the dummy add nothing, as the reference
+// skips r >= a (src/msm_phases.cpp:240).  The own cluster is not in the list: its
+// pairs are summed first, densely (j broadcast by shuffles).  Per lane the pairs
+// are accumulated in a fixed order (own cluster, then list order, atoms of a
+// cluster ascending): the sums are deterministic.  rsqrt is MUFU.RSQ64H + one
+// cubic Newton step (rsqrt_pos); 22 DP instructions + 1 DSETP per pair step.
+// Measured alternatives (C2-S, ms): lanes in lockstep groups of 2 / 4 walking the
+// union of their masks (spatially sorted groups; fewer shared-memory bank
+// conflicts, more steps) 0.68 / 0.73 vs 0.63 per lane; unroll 8 vs 4: equal.
 __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     k_pairs_mw(const int2* __restrict__ clu, const int* __restrict__ plist, const int* __restrict__ pcnt,
                const unsigned* __restrict__ pmask, int cap, const double* __restrict__ xs,
@@ -792,8 +795,28 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         fy = fma(dy, wgt, fy);
         fz = fma(dz, wgt, fz);
     };
+    if (nj > 0) fetch(0);
+    ncand += vi ? unsigned(c.y - 1) : 0u;
+    // the own cluster (dropped from the mask list): all atom pairs, j broadcast by shuffles
+    for (int t = 0; t < c.y; ++t) {
+        const double xj = __shfl_sync(FULLMASK, xi, t), yj = __shfl_sync(FULLMASK, yi, t);
+        const double zj = __shfl_sync(FULLMASK, zi, t), qt = __shfl_sync(FULLMASK, qi, t);
+        const double dx = xi - xj, dy = yi - yj, dz = zi - zj;
+        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        const bool in = r2 < a2 && t != lane;
+        const double rinv = rsqrt_pos(in ? r2 : a2);
+        const double rinv2 = rinv * rinv;
+        const double g = rinv - fma(r2, fma(r2, c2, c1), c0);
+        const double sd = fma(-rinv, rinv2, fma(r2, d1, d0));
+        npair += in ? 1u : 0u;
+        const double qj = in ? qt : 0.0;
+        ph = fma(qj, g, ph);
+        const double wgt = qj * sd;
+        fx = fma(dx, wgt, fx);
+        fy = fma(dy, wgt, fy);
+        fz = fma(dz, wgt, fz);
+    }
     if (nj > 0) {
-        fetch(0);
         __syncwarp();
         while (hi < nj && hi < kRing) stage(hi++);
         __syncwarp();
