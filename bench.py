@@ -305,7 +305,7 @@ def main():
     tr_file = ROOT / "profiles" / "ncu_traffic.json"
     if tr_file.exists():
         try:
-            traffic = json.loads(tr_file.read_text()).get(name, {}).get("k_pairs_dram_bytes")
+            traffic = json.loads(tr_file.read_text()).get(name, {}).get("k_pairs_mw_dram_bytes")
         except Exception:
             traffic = None
 
@@ -357,9 +357,12 @@ def main():
             "value": value, "ms_per_step": total_max / K,
             "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.result(),
-            "roofline": {"bound": "fp64", "kernel": "k_pairs (short-range pair sum, SURVEY S2)",
+            "roofline": {"bound": "fp64", "kernel": "k_pairs_mw (short-range pair sum, SURVEY S2)",
                          "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
                          "slot_frac": slot_frac, "traffic": traffic,
+                         "traffic_note": "DRAM bytes per launch from profiles/r01c_k_pairs_mw_full.md: mostly the "
+                                         "per-lane pair masks (k_pairmask, 128 B per list entry, read once per "
+                                         "evaluation; L2-flushed between timed steps), not atom data",
                          "work_per_launch": f"{pairs_u} in-cutoff unordered pairs x {roofline.PAIR_FLOPS} flops "
                                             f"({roofline.PAIR_SLOTS} FP64 issue slots)",
                          "avg_launch_ms": pair_ms,

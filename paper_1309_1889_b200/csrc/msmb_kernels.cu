@@ -633,6 +633,7 @@ __global__ void __launch_bounds__(kMaskWarps * 32)
                float cut2f, const int* __restrict__ col_off, int col_a, int col_b, const int* __restrict__ flag,
                ErrRec* err) {
     __shared__ __align__(16) float s_sc[kMaskWarps][4][32];
+    __shared__ __align__(16) int s_sh[kMaskWarps][32];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ic = col_off[col_a] + blockIdx.x * kMaskWarps + w;
     if (ic >= col_off[col_b] || failed(err) || !flag[0]) return;
@@ -645,34 +646,96 @@ __global__ void __launch_bounds__(kMaskWarps * 32)
     const float nif = fmaf(zf, zf, fmaf(yf, yf, xf * xf));
     const float2 ni2 = make_float2(nif, nif);
     const float ri2 = __uint_as_float(__reduce_max_sync(FULLMASK, __float_as_uint(vi ? nif : 0.f)));
+    // the i-cluster's box in the same relative fp32 coordinates
+    float blo[3] = {vi ? xf : 3e38f, vi ? yf : 3e38f, vi ? zf : 3e38f};
+    float bhi[3] = {vi ? xf : -3e38f, vi ? yf : -3e38f, vi ? zf : -3e38f};
+#pragma unroll
+    for (int o = 16; o; o >>= 1)
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            blo[ax] = fminf(blo[ax], __shfl_xor_sync(FULLMASK, blo[ax], o));
+            bhi[ax] = fmaxf(bhi[ax], __shfl_xor_sync(FULLMASK, bhi[ax], o));
+        }
     const int nj = pcnt[ic];
     int* pl = plist + size_t(ic) * cap;
     unsigned* pm = pmask + size_t(ic) * cap * 32;
     int out = 0;
-    int jc_n = nj > 0 ? pl[0] : 0;
+    // list entries and their clusters in two register windows of 32 (lane l holds
+    // entry 32w + l), refilled one window ahead; the j atoms of entry jj + 1 are
+    // loaded while entry jj is screened (the dependent loads stay off the chain)
+    int jcw[2];
+    int2 cjw[2];
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+        jcw[b] = 32 * b + lane < nj ? pl[32 * b + lane] : ic;
+        cjw[b] = clu[jcw[b]];
+    }
+    auto entry = [&](int jj, int& jc, int2& cj) {
+        const int b = (jj >> 5) & 1, src = jj & 31;
+        jc = __shfl_sync(FULLMASK, b ? jcw[1] : jcw[0], src);
+        cj.x = __shfl_sync(FULLMASK, b ? cjw[1].x : cjw[0].x, src);
+        cj.y = __shfl_sync(FULLMASK, b ? cjw[1].y : cjw[0].y, src);
+    };
+    int jc_n = ic;
+    int2 cj_n = make_int2(0, 0);
+    double xn = 0, yn = 0, zn = 0;
+    auto fetch = [&](int jj) {
+        entry(jj, jc_n, cj_n);
+        const int sj = cj_n.x + (lane < cj_n.y ? lane : 0);
+        xn = xs[sj];
+        yn = ys[sj];
+        zn = zs[sj];
+    };
+    if (nj > 0) fetch(0);
     for (int jj = 0; jj < nj; ++jj) {
         const int jc = jc_n;
-        const int2 cj = clu[jc];
-        if (jj + 1 < nj) jc_n = pl[jj + 1];
+        const int2 cj = cj_n;
+        const double xd = xn, yd = yn, zd = zn;
+        if ((jj & 31) == 0 && jj > 0) { // window jj/32 is in use: refill the other one with the next
+            const int b = ((jj >> 5) + 1) & 1, e = jj + 32 + lane;
+            const int v = e < nj ? pl[e] : ic;
+            const int2 cv = clu[v];
+            if (b) { jcw[1] = v; cjw[1] = cv; } else { jcw[0] = v; cjw[0] = cv; }
+        }
+        if (jj + 1 < nj) fetch(jj + 1);
         const bool vj = lane < cj.y;
-        const int sj = cj.x + (vj ? lane : 0);
-        const float xj = float(xs[sj] - rx), yj = float(ys[sj] - ry), zj = float(zs[sj] - rz);
+        const float xj = float(xd - rx), yj = float(yd - ry), zj = float(zd - rz);
         const float njf = fmaf(zj, zj, fmaf(yj, yj, xj * xj));
         const float rj2 = __uint_as_float(__reduce_max_sync(FULLMASK, __float_as_uint(vj ? njf : 0.f)));
         const float cut2 = cut2f + 64.f * 5.9604645e-8f * (ri2 + rj2);
+        // atoms beyond the cut from the whole i-box cannot be in any lane's mask: only the
+        // others are screened, compacted into chunks of 4 (bit position kept per slot)
+        const float ex = fmaxf(0.f, fmaxf(blo[0] - xj, xj - bhi[0]));
+        const float ey = fmaxf(0.f, fmaxf(blo[1] - yj, yj - bhi[1]));
+        const float ez = fmaxf(0.f, fmaxf(blo[2] - zj, zj - bhi[2]));
+        const bool rel = vj && fmaf(ez, ez, fmaf(ey, ey, ex * ex)) <= cut2 * 1.00001f;
+        const unsigned R = __ballot_sync(FULLMASK, rel);
+        if (R == 0u) continue;
+        const int k = __popc(R & ((1u << lane) - 1u)), nr = __popc(R), nr4 = (nr + 3) & ~3;
         __syncwarp();
-        s_sc[w][0][lane] = -2.f * xj;
-        s_sc[w][1][lane] = -2.f * yj;
-        s_sc[w][2][lane] = -2.f * zj;
-        s_sc[w][3][lane] = vj ? njf - cut2 : 3e38f;
+        if (rel) {
+            s_sc[w][0][k] = -2.f * xj;
+            s_sc[w][1][k] = -2.f * yj;
+            s_sc[w][2][k] = -2.f * zj;
+            s_sc[w][3][k] = njf - cut2;
+            s_sh[w][k] = 31 - lane;
+        }
+        if (lane >= nr && lane < nr4) { // padding slots: never in range
+            s_sc[w][0][lane] = 0.f;
+            s_sc[w][1][lane] = 0.f;
+            s_sc[w][2][lane] = 0.f;
+            s_sc[w][3][lane] = 3e38f;
+            s_sh[w][lane] = 0;
+        }
         __syncwarp();
         unsigned mask = 0;
-#pragma unroll
-        for (int t = 0; t < 32; t += 4) {
+#pragma unroll 2
+        for (int t = 0; t < nr4; t += 4) {
             const float4 mx = *reinterpret_cast<const float4*>(&s_sc[w][0][t]);
             const float4 my = *reinterpret_cast<const float4*>(&s_sc[w][1][t]);
             const float4 mz = *reinterpret_cast<const float4*>(&s_sc[w][2][t]);
             const float4 cc = *reinterpret_cast<const float4*>(&s_sc[w][3][t]);
+            const int4 sh = *reinterpret_cast<const int4*>(&s_sh[w][t]);
             float2 sa = __fadd2_rn(ni2, make_float2(cc.x, cc.y));
             float2 sb = __fadd2_rn(ni2, make_float2(cc.z, cc.w));
             sa = __ffma2_rn(make_float2(mx.x, mx.y), xi2, sa);
@@ -681,12 +744,11 @@ __global__ void __launch_bounds__(kMaskWarps * 32)
             sb = __ffma2_rn(make_float2(my.z, my.w), yi2, sb);
             sa = __ffma2_rn(make_float2(mz.x, mz.y), zi2, sa);
             sb = __ffma2_rn(make_float2(mz.z, mz.w), zi2, sb);
-            mask = (mask << 1) | (__float_as_uint(sa.x) >> 31);
-            mask = (mask << 1) | (__float_as_uint(sa.y) >> 31);
-            mask = (mask << 1) | (__float_as_uint(sb.x) >> 31);
-            mask = (mask << 1) | (__float_as_uint(sb.y) >> 31);
+            mask |= ((__float_as_uint(sa.x) >> 31) << sh.x) | ((__float_as_uint(sa.y) >> 31) << sh.y) |
+                    ((__float_as_uint(sb.x) >> 31) << sh.z) | ((__float_as_uint(sb.y) >> 31) << sh.w);
         }
         if (!vi || jc == ic) mask = 0; // the own cluster is summed densely by k_pairs_mw
+        mask &= ~(0xffffffffu >> cj.y); // bits 31 .. 32 - cj.y: the cluster's atoms only
         if (__any_sync(FULLMASK, mask != 0)) {
             pm[size_t(out) * 32 + lane] = mask;
             if (lane == 0) pl[out] = cj.x;

@@ -23,7 +23,7 @@ ROOT = Path(__file__).resolve().parent.parent
 
 def _short(name: str) -> str:
     name = re.sub(r"\(.*", "", name)
-    return name.replace("void ", "").strip()
+    return name.replace("void ", "").replace("msmb::", "").strip()
 
 
 def launches(csv_path: str, out: str) -> None:
@@ -72,6 +72,7 @@ WANT = [
     ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "LSU pipe"),
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "shared-memory wavefronts"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "shared-memory bank conflicts"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "shared-memory pipe busy"),
     ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1/TEX throughput"),
     ("lts__t_sector_hit_rate.pct", "L2 hit rate"),
     ("dram__bytes_read.sum", "DRAM read"),

@@ -10,4 +10,4 @@ dev.propagate(w.dt, 2)
 f.set_stage_timing(True); f.reset_stage_times()
 dev.propagate(w.dt, 10)
 st = f.stage_times()
-print(os.environ.get("MSMB_LIB", "default"), " ".join(f"{k}={v[0]/11:.4f}" for k, v in st.items() if k in ("pairs", "lattice", "anterp", "restrict", "top", "prolong")))
+print(os.environ.get("MSMB_LIB", "default"), " ".join(f"{k}={v[0]/11:.4f}" for k, v in st.items() if k in ("pairs", "clusters", "lattice", "anterp", "restrict", "top", "prolong", "sort", "interp")))
