@@ -392,6 +392,11 @@ static int stage_id(const char* name) {
 // exclusive.
 // `rebuild`: force a pair-list rebuild (the first evaluation of a call); otherwise
 // the list is rebuilt only once some atom moved more than skin/2 (launch_clusters).
+// MSMB_TIMELINE=1: globaltimer stamps at the fork/join points of every evaluation
+// (diagnostic only; msmb_bench_propagate prints the per-step averages to stderr)
+void launch_stamp(cudaStream_t st, int idx);
+void read_stamps(unsigned long long* h);
+static const bool g_exp_stamps = std::getenv("MSMB_TIMELINE") != nullptr;
 static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, bool rebuild = true) {
     cudaStream_t st = f->stream;
     const bool fork = !f->timer.on;
@@ -404,29 +409,39 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, 
         sc.done(nl);
         total += nl;
     };
+    if (g_exp_stamps) launch_stamp(st, 0);
     run("bin", [&] { return launch_bin(st, g, s, W.a, W.c, W.err); });
     run("sort", [&] { return launch_sort(st, g, s, W.a, W.c, W.err); });
     if (fork) {
         ck(cudaEventRecord(f->fork_ev, st), "fork");
         ck(cudaStreamWaitEvent(lr, f->fork_ev, 0), "fork");
     }
+    if (g_exp_stamps) { launch_stamp(st, 1); launch_stamp(lr, 2); }
     run("anterp", [&] { return launch_anterp(lr, g, W.a, W.c, W.L, W.err, W.whole); });
+    if (g_exp_stamps) launch_stamp(lr, 7);
     run("restrict", [&] { return launch_restrict_all(lr, g, W.L, W.err); });
+    if (g_exp_stamps) launch_stamp(lr, 8);
     run("lattice", [&] {
         return W.lattice_fft ? launch_lattice_fft(lr, W.fft, W.err) : launch_lattice(lr, g, W.L, W.err, W.whole);
     });
+    if (g_exp_stamps) launch_stamp(lr, 9);
     run("top", [&] {
         return W.fft_top.n ? launch_lattice_fft(lr, W.fft_top, W.err) : launch_top(lr, g, W.L, W.err);
     });
+    if (g_exp_stamps) launch_stamp(lr, 10);
     run("prolong", [&] { return launch_prolong_all(lr, g, W.L, W.err); });
+    if (g_exp_stamps) launch_stamp(lr, 3);
     if (fork) ck(cudaEventRecord(f->join_ev, lr), "join");
     run("clusters", [&] { return launch_clusters(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, rebuild ? 1 : 0); });
+    if (g_exp_stamps) launch_stamp(st, 4);
     run("pairs", [&] { return launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole); });
+    if (g_exp_stamps) launch_stamp(st, 5);
     if (fork) ck(cudaStreamWaitEvent(st, f->join_ev, 0), "join");
     DevOut o = W.o;
     if (!outputs) o.phi = o.phis = o.phil = o.e = nullptr;
     run("interp", [&] { return launch_interp(st, g, s.n, W.a, W.c, W.L, o, W.err, outputs ? 1 : 0, W.whole); });
     run("finalize", [&] { return launch_finalize(st, s, W.err); });
+    if (g_exp_stamps) launch_stamp(st, 6);
     return total;
 }
 
@@ -1033,11 +1048,24 @@ int msmb_bench_propagate(msmb_field* f, msmb_system* sys, double dt, int steps, 
         ck(cudaGraphLaunch(W.gx_eval, f->stream), "GraphLaunch");
         f->launches += W.launches_eval;
     }, true);
-    for (int st = 1; st <= steps; ++st)
+    double stamp_acc[16] = {0};
+    for (int st = 1; st <= steps; ++st) {
         step_ms[st] = timed([&] {
             ck(cudaGraphLaunch(st == 1 ? W.gx_step1 : W.gx_step2, f->stream), "GraphLaunch");
             f->launches += W.launches_step;
         }, true);
+        if (g_exp_stamps) {
+            unsigned long long h[16];
+            read_stamps(h);
+            for (int k = 1; k <= 10; ++k) stamp_acc[k] += double(h[k] - h[0]) * 1e-3;
+        }
+    }
+    if (g_exp_stamps && steps > 0)
+        fprintf(stderr, "timeline (us from evaluation start): sort_end %.1f chain_start %.1f chain_end %.1f clusters_end %.1f pairs_end %.1f eval_end %.1f\n",
+                stamp_acc[1] / steps, stamp_acc[2] / steps, stamp_acc[3] / steps, stamp_acc[4] / steps, stamp_acc[5] / steps, stamp_acc[6] / steps);
+    if (g_exp_stamps && steps > 0)
+        fprintf(stderr, "chain: anterp_end %.1f restrict_end %.1f lattice_end %.1f top_end %.1f\n", stamp_acc[7] / steps,
+                stamp_acc[8] / steps, stamp_acc[9] / steps, stamp_acc[10] / steps);
     step_ms[steps + 1] = timed([&] { f->launches += launch_kick(f->stream, s, W.o, dt, conv, W.err); }, false);
     cudaEventDestroy(ea);
     cudaEventDestroy(eb);

@@ -25,6 +25,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include <map>
 #include <mutex>
@@ -1052,19 +1053,37 @@ __global__ void __launch_bounds__(128)
             const int cz = z0 - 2 + u;
             rg[u] = (cz >= 1 && cz <= d2 - 3) ? __ldg(row + cz) : make_int2(0, 0);
         }
+        // the first atom of every cell is fetched up front (one batch of independent
+        // loads: ~1.2 atoms per cell, so most atoms), the rest as the cells are summed
+        double fx_[kAQ + 3], fy_[kAQ + 3];
+        double2 f01[kAQ + 3], f23[kAQ + 3];
 #pragma unroll
         for (int u = 0; u < kAQ + 3; ++u) {
-            for (int s = rg[u].x; s < rg[u].y; ++s) {
-                const double* w = aw + size_t(s) * 12;
-                const double cxy = __dmul_rn(__ldg(w + dxw), __ldg(w + dyw));
-                const double2 wz01 = __ldg(reinterpret_cast<const double2*>(w + 8));
-                const double2 wz23 = __ldg(reinterpret_cast<const double2*>(w + 10));
+            const double* w = aw + size_t(rg[u].x < rg[u].y ? rg[u].x : 0) * 12;
+            fx_[u] = __ldg(w + dxw);
+            fy_[u] = __ldg(w + dyw);
+            f01[u] = __ldg(reinterpret_cast<const double2*>(w + 8));
+            f23[u] = __ldg(reinterpret_cast<const double2*>(w + 10));
+        }
+#pragma unroll
+        for (int u = 0; u < kAQ + 3; ++u) {
+            if (rg[u].x >= rg[u].y) continue;
+            double wxv = fx_[u], wyv = fy_[u];
+            double2 wz01 = f01[u], wz23 = f23[u];
+            for (int s = rg[u].x;;) {
+                const double cxy = __dmul_rn(wxv, wyv);
                 const double wzv[4] = {wz01.x, wz01.y, wz23.x, wz23.y};
 #pragma unroll
                 for (int k = 0; k < kAQ; ++k) {
                     const int dz = k - u + 3;
                     if (dz >= 0 && dz <= 3) acc[k] = fma(cxy, wzv[dz], acc[k]);
                 }
+                if (++s >= rg[u].y) break;
+                const double* w = aw + size_t(s) * 12;
+                wxv = __ldg(w + dxw);
+                wyv = __ldg(w + dyw);
+                wz01 = __ldg(reinterpret_cast<const double2*>(w + 8));
+                wz23 = __ldg(reinterpret_cast<const double2*>(w + 10));
             }
         }
     }
@@ -2095,6 +2114,54 @@ __device__ __forceinline__ void interp_atom(const InterpP& p, const double* __re
     u = acc;
 }
 
+// Production interpolation: the same tensor-product sums factored separably with
+// FMAs -- per (a, b) row S = sum_c wz[c] u, Sd = sum_c dwz[c] u, then the y and x
+// sums -- 192 DP ops per atom instead of ~750 for the reference's per-point
+// products (interp_atom, kept bit-exact for the stage tests: msmb_debug_stage 4).
+// Reassociation moves phi_long and the long-range force by ~1e-16 relative.
+__device__ __forceinline__ void interp_atom_fast(const InterpP& p, const double* __restrict__ pot,
+                                                 double px, double py, double pz, double& u,
+                                                 double& gx, double& gy, double& gz) {
+    const double pp[3] = {px, py, pz};
+    double w[3][4], dw[3][4];
+    int base[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        const double t = __dmul_rn(__dsub_rn(pp[ax], p.o[ax]), p.inv_h);
+        base[ax] = int(floor(t)) - 1;
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            const double xi = __dsub_rn(t, double(base[ax] + d));
+            w[ax][d] = phi_rn(xi);
+            dw[ax][d] = __dmul_rn(dphi_rn(xi), p.inv_h);
+        }
+    }
+    const double* r0 = pot + (size_t(base[0]) * p.d[1] + base[1]) * p.d[2] + base[2];
+    double uu = 0.0, ax_ = 0.0, ay_ = 0.0, az_ = 0.0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        double T = 0.0, Td = 0.0, Tz = 0.0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const double* row = r0 + (size_t(a) * p.d[1] + b) * p.d[2];
+            const double u0 = __ldg(row), u1 = __ldg(row + 1), u2 = __ldg(row + 2), u3 = __ldg(row + 3);
+            const double S = fma(w[2][3], u3, fma(w[2][2], u2, fma(w[2][1], u1, w[2][0] * u0)));
+            const double Sd = fma(dw[2][3], u3, fma(dw[2][2], u2, fma(dw[2][1], u1, dw[2][0] * u0)));
+            T = fma(w[1][b], S, T);
+            Td = fma(dw[1][b], S, Td);
+            Tz = fma(w[1][b], Sd, Tz);
+        }
+        uu = fma(w[0][a], T, uu);
+        ax_ = fma(dw[0][a], T, ax_);
+        ay_ = fma(w[0][a], Td, ay_);
+        az_ = fma(w[0][a], Tz, az_);
+    }
+    u = uu;
+    gx = ax_;
+    gy = ay_;
+    gz = az_;
+}
+
 static InterpP make_interp(const Geometry& g) {
     InterpP p;
     for (int ax = 0; ax < 3; ++ax) {
@@ -2119,7 +2186,7 @@ __global__ void k_interp(InterpP p, const int* __restrict__ colstart, int col_a,
     if (s >= colstart[col_b] || failed(err)) return;
     double u, gx, gy, gz;
     const double q = qs[s];
-    interp_atom(p, pot, xs[s], ys[s], zs[s], u, gx, gy, gz);
+    interp_atom_fast(p, pot, xs[s], ys[s], zs[s], u, gx, gy, gz);
     const double ul = __dsub_rn(u, __dmul_rn(q, p.self_term));  // msm.cpp:73
     const double kq = __dmul_rn(p.kc, q);                          // msm.cpp:47
     const int i = perm[s];
@@ -2505,4 +2572,16 @@ int launch_debug_interp(cudaStream_t st, const Geometry& g, const DevState& s, c
     return 1;
 }
 
+} // namespace msmb
+
+// ---- diagnostic: globaltimer stamps for a step timeline (MSMB_TIMELINE, msmb_engine.cu) ----
+namespace msmb {
+__device__ unsigned long long g_stamps[16];
+__global__ void k_stamp(int idx) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_stamps[idx] = t;
+}
+void launch_stamp(cudaStream_t st, int idx) { k_stamp<<<1, 1, 0, st>>>(idx); }
+void read_stamps(unsigned long long* h) { cudaMemcpyFromSymbol(h, g_stamps, sizeof(unsigned long long) * 16); }
 } // namespace msmb
