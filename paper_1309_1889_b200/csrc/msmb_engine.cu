@@ -90,6 +90,8 @@ StageTimer::~StageTimer() {
 // ---- errors -----------------------------------------------------------------------
 int engine_set_error(msmb_field* f, const Error& e) {
     f->last = e;
+    // a failed evaluation may have left a partial pair list: rebuild at the next one
+    if (f->ws && f->ws->c.flag) cudaMemsetAsync(f->ws->c.flag + 3, 0, sizeof(int), f->stream);
     return e.kind;
 }
 
@@ -213,9 +215,9 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
     c.pcnt = walloc<int>(*W, size_t(W->maxclu));
     c.scan_tmp = walloc<int>(*W, size_t((std::max(g.ncells, g.ncols) + 1 + 4095) / 4096 + 8));
     c.colstart = walloc<int>(*W, size_t(g.ncols + 1));
-    c.flag = walloc<int>(*W, 3);
+    c.flag = walloc<int>(*W, 5);
     ck(cudaMemset(c.nclu, 0, sizeof(int)), "memset");
-    ck(cudaMemset(c.flag, 0, 3 * sizeof(int)), "memset");
+    ck(cudaMemset(c.flag, 0, 5 * sizeof(int)), "memset");
     ck(cudaMemset(c.colstart, 0, sizeof(int) * size_t(g.ncols + 1)), "memset");
     alloc_plist(*W, g.pair_cap);
     DevLevels& L = W->L;
@@ -390,14 +392,17 @@ static int stage_id(const char* name) {
 // fixed order, so results do not depend on how the branches interleave.  With
 // per-stage timing on, everything runs on one stream so the stage events are
 // exclusive.
-// `rebuild`: force a pair-list rebuild (the first evaluation of a call); otherwise
-// the list is rebuilt only once some atom moved more than skin/2 (launch_clusters).
+// `rebuild`: force a pair-list rebuild; otherwise the list is rebuilt only when it
+// is not valid (never built, capacity grown, a failed evaluation, another part's
+// columns) or once some atom moved more than skin/2 since it was built
+// (launch_clusters) -- also across calls: a call that starts within skin/2 of the
+// last build reuses its list.
 // MSMB_TIMELINE=1: globaltimer stamps at the fork/join points of every evaluation
 // (diagnostic only; msmb_bench_propagate prints the per-step averages to stderr)
 void launch_stamp(cudaStream_t st, int idx);
 void read_stamps(unsigned long long* h);
 static const bool g_exp_stamps = std::getenv("MSMB_TIMELINE") != nullptr;
-static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, bool rebuild = true) {
+static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, bool rebuild = false) {
     cudaStream_t st = f->stream;
     const bool fork = !f->timer.on;
     cudaStream_t lr = fork ? f->side : st;
@@ -471,6 +476,8 @@ void grow_cap(Workspace& W, const ErrRec& r) {
     const int need = std::max(r.overflow, W.cap);
     const int cap = std::max(need + need / 4 + 32, W.cap * 2);
     alloc_plist(W, cap);
+    ck(cudaMemset(W.c.flag + 3, 0, sizeof(int)), "memset"); // the list must be rebuilt
+    ck(cudaDeviceSynchronize(), "sync");
 }
 
 // Evaluate the system in `s` (device), outputs left in W.o.
@@ -578,7 +585,7 @@ int engine_propagate(msmb_field* f, StateBuf& sb, double dt, int steps, double c
                 f->launches += W.launches_step;
             }
         } else {
-            enqueue_eval(f, W, s, false, true);
+            enqueue_eval(f, W, s, false);
             for (int st = 1; st <= steps; ++st) {
                 StageScope sc(f, "verlet");
                 sc.done(launch_kick_drift(f->stream, s, W.o, dt, conv, st == 1 ? 1 : 2, W.err));

@@ -338,7 +338,12 @@ int launch_sort(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms&
 // rebuild); flag[1]: atoms in the cluster order.  Between rebuilds the clusters keep
 // their atoms (cl_perm) and only the positions are gathered anew; the pair kernel
 // screens with the exact cutoff, so the frozen list only has to be a superset.
-__global__ void k_flag_reset(int* flag, int force) { flag[0] = force; }
+// flag[0] = rebuild the pair list in this evaluation: forced, or no valid list
+// (flag[3] == 0: never built, capacity grown, an evaluation failed), or the list was
+// built for another ownership range (flag[4]: the part's pair-column key)
+__global__ void k_flag_reset(int* flag, int force, int key) {
+    flag[0] = (force || flag[3] == 0 || flag[4] != key) ? 1 : 0;
+}
 
 __global__ void k_disp(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
                        const double* __restrict__ z, const double* __restrict__ ref, double half_skin2,
@@ -351,13 +356,15 @@ __global__ void k_disp(int64_t n, const double* __restrict__ x, const double* __
 
 __global__ void k_cl_perm(int64_t n, const int* __restrict__ start_total, const int* __restrict__ perm,
                           const double* __restrict__ x, const double* __restrict__ y,
-                          const double* __restrict__ z, int* cl_perm, double* ref, int* flag) {
+                          const double* __restrict__ z, int* cl_perm, double* ref, int* flag, int key) {
     if (!flag[0]) return;
     const int tot = *start_total;
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s == 0) {
         flag[1] = tot;
         flag[2] += 1; // rebuilds since the workspace was created (diagnostics)
+        flag[3] = 1;  // valid until the host invalidates it (capacity growth, errors)
+        flag[4] = key;
     }
     if (s >= tot) return;
     const int i = perm[s];
@@ -942,10 +949,11 @@ int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevStat
     const int64_t nc = g.ncols;
     const int nb = int((n + 255) / 256) > 0 ? int((n + 255) / 256) : 1;
     // rebuild decision, frozen cluster order, current positions in it
-    k_flag_reset<<<1, 1, 0, st>>>(c.flag, force_rebuild || !(g.skin > 0.0) ? 1 : 0);
+    const int key = P.cx0 * 65536 + P.cx1;
+    k_flag_reset<<<1, 1, 0, st>>>(c.flag, force_rebuild || !(g.skin > 0.0) ? 1 : 0, key);
     const double hs = 0.5 * g.skin;
     k_disp<<<nb, 256, 0, st>>>(n, s.x, s.y, s.z, a.ref, hs * hs, c.flag);
-    k_cl_perm<<<nb, 256, 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, a.cl_perm, a.ref, c.flag);
+    k_cl_perm<<<nb, 256, 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, a.cl_perm, a.ref, c.flag, key);
     k_gather_cl<<<nb, 256, 0, st>>>(c.flag, a.cl_perm, s.x, s.y, s.z, s.q, a.xc, a.yc, a.zc, a.qc, err);
     // cluster pair list (rebuild evaluations only)
     k_columns<<<int((nc + 1 + 255) / 256), 256, 0, st>>>(nc, cells_per_col, c.start, c.col_cnt, c.flag, err);
