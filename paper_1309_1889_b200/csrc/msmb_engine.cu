@@ -196,6 +196,7 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
     a.fsy = walloc<double>(*W, N);
     a.fsz = walloc<double>(*W, N);
     a.cl_perm = walloc<int>(*W, N);
+    a.cl_inv = walloc<int>(*W, N);
     a.xc = walloc<double>(*W, N);
     a.yc = walloc<double>(*W, N);
     a.zc = walloc<double>(*W, N);

@@ -20,6 +20,7 @@ struct DevAtoms {       // sorted-order working set, capacity n
     // pair-list (Verlet skin) state: the cluster order is the sorted order of the
     // last list rebuild; positions are gathered into it every evaluation
     int* cl_perm;       // [n] cluster slot -> original index
+    int* cl_inv;        // [n] original index -> cluster slot (ownership tests in original order)
     double* xc; double* yc; double* zc; double* qc; // [n] positions / charges, cluster order
     double* ref;        // [3n] positions (original order) at the last rebuild
 };
