@@ -203,11 +203,19 @@ int msmb_system_get_state_device(const msmb_system* s, double* state);
  *   phase 1  restriction, owned lattice cutoff         -> xbuf: level potentials
  *   phase 2  top level, prolongation, owned interpolation, forces, energy share
  *            (*energy), owned Verlet update (`kicks` half-kicks, then a drift
- *            if `drift`)                               -> xbuf: particle state
- *   phase 3  import the exchanged state.
- * xbuf is device memory of the field's GPU holding doubles as int64 bit patterns;
- * entries a part does not own are INT64_MIN, so an element-wise int64 MAX
- * all-reduce of the buffers (e.g. NCCL) gives every part the owners' exact
+ *            if `drift`)                               -> xbuf: positions (3 n),
+ *                                                         velocities (3 n)
+ *   phase 3  import the exchanged positions (the first 3 n entries of xin).
+ *   phase 4  import exchanged velocities (entries 3 n .. 6 n of xin).
+ * Ownership of atoms only changes when the pair list is rebuilt, and a part reads
+ * velocities of owned atoms only, so velocities need not travel every step:
+ * phase 0 sets *energy = 1 when this evaluation rebuilt the list (0 otherwise);
+ * the driver then exchanges the velocity half of the previous phase-2 buffer
+ * (written under the old ownership) and imports it with phase 4 before phase 2,
+ * and does the same once at the end of a call.  Positions are exchanged every
+ * step.  xbuf is device memory of the field's GPU holding doubles as int64 bit
+ * patterns; entries a part does not own are INT64_MIN, so an element-wise int64
+ * MAX all-reduce of the buffers (e.g. NCCL) gives every part the owners' exact
  * values.  Sizes (msmb_dd_sizes) are [level-0 points, all level points, 6 n]
  * int64 for the three exchanges.  The decomposed trajectory is bit-identical to
  * msmb_system_propagate's.  Binning errors are detected identically on every

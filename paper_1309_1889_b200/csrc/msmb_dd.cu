@@ -55,7 +55,7 @@ void export_planes(cudaStream_t st, const Geometry& g, const Part& P, int k, con
     if (cnt) ckd(cudaMemcpyAsync(x + off, src + off, cnt * sizeof(double), cudaMemcpyDeviceToDevice, st), "D2D");
 }
 
-int phase0(msmb_field* f, Workspace& W, DevState& s, long long* xbuf, int rebuild) {
+int phase0(msmb_field* f, Workspace& W, DevState& s, long long* xbuf, int rebuild, double* rebuilt) {
     const Geometry& g = W.g;
     cudaStream_t st = f->stream;
     for (int attempt = 0; attempt < 8; ++attempt) {
@@ -77,7 +77,9 @@ int phase0(msmb_field* f, Workspace& W, DevState& s, long long* xbuf, int rebuil
             grow_cap(W, r);
             continue;
         }
+        const int64_t before = f->counters[6];
         record_counters(f, W, r);
+        if (rebuilt) *rebuilt = f->counters[6] != before ? 1.0 : 0.0;
         // binning, sorting and error detection are replicated: every part fails alike
         if (r.kind) return engine_set_error(f, error_from_rec(r));
         if (W.part.nparts > 1) { // one part: the charges stay where phase 1 reads them
@@ -134,9 +136,12 @@ int phase2(msmb_field* f, Workspace& W, DevState& s, const long long* xin, long 
     return MSMB_OK;
 }
 
-int phase3(msmb_field* f, Workspace& W, DevState& s, const long long* xbuf) {
+// phase 3: positions (x, y, z = the first 3 n doubles of the state); phase 4: velocities
+int phase34(msmb_field* f, Workspace& W, DevState& s, const long long* xbuf, int which) {
+    const size_t off = which == 4 ? 3 * size_t(s.n) : 0;
     if (s.n && W.part.nparts > 1)
-        ckd(cudaMemcpyAsync(s.x, xbuf, sizeof(double) * 6 * size_t(s.n), cudaMemcpyDeviceToDevice, f->stream),
+        ckd(cudaMemcpyAsync(s.x + off, xbuf + off, sizeof(double) * 3 * size_t(s.n), cudaMemcpyDeviceToDevice,
+                            f->stream),
             "D2D");
     ckd(cudaStreamSynchronize(f->stream), "sync");
     return MSMB_OK;
@@ -226,10 +231,11 @@ extern "C" int msmb_dd_phase(msmb_field* f, msmb_system* sys, int phase, double 
         const long long* xi = static_cast<const long long*>(xin);
         long long* xo = static_cast<long long*>(xout);
         switch (phase) {
-            case 0: return phase0(f, W, s, xo, kicks); // phase 0: `kicks` = force a pair-list rebuild
+            case 0: return phase0(f, W, s, xo, kicks, energy); // *energy = 1: the list was rebuilt
             case 1: return phase1(f, W, xi, xo);
             case 2: return phase2(f, W, s, xi, xo, dt, kicks, drift, u.energy_to_native, energy);
-            case 3: return phase3(f, W, s, xi);
+            case 3:
+            case 4: return phase34(f, W, s, xi, phase);
             default: return engine_set_error(f, Error{MSMB_ERR_CONFIG, -1, -1, -1, "invalid phase"});
         }
     } catch (const std::exception& ex) {

@@ -406,15 +406,21 @@ class SpatialDecomposition:
         energy = 0.0
         for f, ds, bufs in self.parts:
             e = C.c_double()
-            xin = C.c_void_p(bufs[phase - 1].data_ptr()) if phase > 0 else None
+            xin = C.c_void_p(bufs[min(phase, 3) - 1].data_ptr()) if phase > 0 else None
             xout = C.c_void_p(bufs[phase].data_ptr()) if phase < 3 else None
             _check(f.handle, self.lib.msmb_dd_phase(f.handle, ds._h, phase, dt, kicks, drift, C.byref(self._uc),
                                                     xin, xout, C.byref(e)))
             energy += e.value
         return energy
 
-    def _exchange(self, which: int):
+    def _exchange(self, which: int, part: str = "all"):
+        """Exchange buffer `which`; for the state buffer (2) `part` selects the
+        positions ("pos", every step) or the velocities ("vel", after a list rebuild
+        and at the end of a call: ownership only changes at rebuilds)."""
         bufs = [b[which] for _, _, b in self.parts]
+        if which == 2 and part != "all":
+            n3 = 3 * self.n
+            bufs = [b[:n3] if part == "pos" else b[n3:2 * n3] for b in bufs]
         exchange_max_bits(bufs, self.group, use_dist=self.distributed)
         self.exchanged_bytes += bufs[0].numel() * 8
         self.torch.cuda.current_stream(self.device).synchronize()
@@ -448,6 +454,7 @@ class SpatialDecomposition:
             raise ConfigError("steps_per_slice must be >= 1")
         backup = self._state()
         energy = 0.0
+        vel_pending = False  # velocities of the last phase 2 not yet exchanged
         try:
             for s in range(steps + 1):
                 if steps == 0:
@@ -458,14 +465,22 @@ class SpatialDecomposition:
                     kicks, drift = 2, 1      # closing kick of step s, opening kick + drift of s+1
                 else:
                     kicks, drift = 1, 0      # closing half-kick of the last step
-                self._phase(0, kicks=1 if s == 0 else 0)  # phase 0: kicks = force a pair-list rebuild
+                rebuilt = self._phase(0, kicks=1 if s == 0 else 0) > 0  # replicated decision
+                if rebuilt and vel_pending:  # new owners need the old owners' velocities
+                    self._exchange(2, "vel")
+                    self._phase(4)
+                    vel_pending = False
                 self._exchange(0)
                 self._phase(1)
                 self._exchange(1)
                 energy = self._phase(2, dt, kicks, drift)
                 if kicks or drift:
-                    self._exchange(2)
+                    self._exchange(2, "pos")
                     self._phase(3)
+                    vel_pending = True
+            if vel_pending:
+                self._exchange(2, "vel")
+                self._phase(4)
         except Error:
             self._set_state(backup)
             raise
