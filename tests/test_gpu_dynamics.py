@@ -165,3 +165,51 @@ def test_pair_list_rebuilds_mid_trajectory(port):
     pp, vv, done, err = port.propagate(w.pos, w.vel, w.q, w.mass, w.box, w.a, w.h, w.levels, dt, steps)
     assert err is None and done == steps
     assert rel_rms(p1, pp) <= 1e-8 and rel_rms(v1, vv) <= 1e-8
+
+
+def test_pair_list_validity_across_calls_and_systems(port):
+    # the list is rebuilt only when invalid or after a skin/2 move -- also across calls
+    w = fx.config("c1s", n_override=3000)
+    cfg = pkg.MsmConfig(w.a, w.h, w.levels)
+    a = pkg.ParticleSystem(w.pos, w.vel, w.q, w.mass, w.box)
+    far = w.pos.copy()
+    far[:, 0] = w.box[0] - far[:, 0]          # mirrored copy: every atom moved
+    b = pkg.ParticleSystem(far, w.vel, w.q, w.mass, w.box)
+    f = pkg.MsmField(cfg)
+    ra = f.evaluate(a)
+    assert f.work_counters()["list_rebuilds"] == 1
+    f.evaluate(a)                             # same positions: the list is reused
+    assert f.work_counters()["list_rebuilds"] == 1
+    rb = f.evaluate(b)                        # far away: rebuilt
+    assert f.work_counters()["list_rebuilds"] == 2
+    ra2 = f.evaluate(a)                       # back: rebuilt from a's positions, so
+    assert f.work_counters()["list_rebuilds"] == 3
+    assert np.array_equal(ra2.per_particle_force, ra.per_particle_force)   # bit-identical
+    assert ra2.total_energy == ra.total_energy
+    fb = pkg.MsmField(cfg).evaluate(b)        # a fresh field agrees bit for bit
+    assert np.array_equal(fb.per_particle_force, rb.per_particle_force)
+    o = port.msm_potential(far, w.q, w.box, w.a, w.h, w.levels)
+    assert abs(rb.total_energy - o["energy"]) <= 1e-10 * abs(o["energy"])
+    # a propagate call continuing from the current list does not rebuild at its start
+    ds = pkg.DeviceSystem(f, a)
+    ds.propagate(w.dt, 3)
+    n0 = f.work_counters()["list_rebuilds"]
+    ds.propagate(w.dt, 3)
+    assert f.work_counters()["list_rebuilds"] == n0
+
+
+def test_pair_list_invalidated_by_failed_evaluation():
+    # a failed evaluation (coverage error) invalidates the list: the next one rebuilds
+    w = fx.config("c1s", n_override=2000)
+    f = pkg.MsmField(pkg.MsmConfig(w.a, w.h, w.levels))
+    s = pkg.ParticleSystem(w.pos, w.vel, w.q, w.mass, w.box)
+    r0 = f.evaluate(s)
+    bad = w.pos.copy()
+    bad[7] = [1e3, 1e3, 1e3]                  # outside grid coverage
+    with pytest.raises(pkg.CoverageError):
+        f.evaluate(pkg.ParticleSystem(bad, w.vel, w.q, w.mass, w.box))
+    r1 = f.evaluate(s)                        # rebuilt from s: the first result, bit for bit
+    assert np.array_equal(r1.per_particle_force, r0.per_particle_force)
+    n1 = f.work_counters()["list_rebuilds"]
+    f.evaluate(s)                             # and valid again afterwards
+    assert f.work_counters()["list_rebuilds"] == n1
