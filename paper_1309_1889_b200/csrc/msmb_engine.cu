@@ -186,10 +186,6 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
     a.rank = walloc<int>(*W, N);
     a.perm = walloc<int>(*W, N);
     a.outlist = walloc<int>(*W, N);
-    a.xs = walloc<double>(*W, N);
-    a.ys = walloc<double>(*W, N);
-    a.zs = walloc<double>(*W, N);
-    a.qs = walloc<double>(*W, N);
     a.aw = walloc<double>(*W, N * 12);
     a.phis = walloc<double>(*W, N);
     a.fsx = walloc<double>(*W, N);

@@ -278,16 +278,11 @@ __global__ void k_cellsort(int64_t ncells, BinP p, const int* __restrict__ start
 __global__ void k_gather(int n, const int* __restrict__ start_total, const int* __restrict__ perm,
                          const double* __restrict__ x, const double* __restrict__ y,
                          const double* __restrict__ z, const double* __restrict__ q, BinP p,
-                         double* xs, double* ys, double* zs, double* qs, double* aw,
-                         const ErrRec* err) {
+                         double* aw, const ErrRec* err) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= *start_total || failed(err)) return;
     const int i = perm[s];
     const double px = x[i], py = y[i], pz = z[i], qq = q[i];
-    xs[s] = px;
-    ys[s] = py;
-    zs[s] = pz;
-    qs[s] = qq;
     const double pp[3] = {px, py, pz};
     double w[3][4];
     for (int ax = 0; ax < 3; ++ax) {
@@ -323,7 +318,7 @@ int launch_sort(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms&
                                                             c.nat, s.x, s.y, s.z, err);
     if (n == 0) return l + 1;
     k_gather<<<(n + 255) / 256, 256, 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, s.q,
-                                              make_binp(g), a.xs, a.ys, a.zs, a.qs, a.aw,
+                                              make_binp(g), a.aw,
                                               err);
     return l + 3;
 }

@@ -13,7 +13,6 @@ struct DevAtoms {       // sorted-order working set, capacity n
     int* rank;          // [n]
     int* perm;          // [n] sorted slot -> original index
     int* outlist;       // [n] out-of-coverage atoms
-    double* xs; double* ys; double* zs; double* qs;  // sorted positions / charges
     double* aw;         // [n*12] anterpolation weights: q*wx[4], wy[4], wz[4]
     double* phis;       // [n] short-range potential (per unit charge), cluster order
     double* fsx; double* fsy; double* fsz; // short-range forces (with k_C), cluster order
