@@ -1358,21 +1358,17 @@ __global__ void __launch_bounds__(kRTx * kRTy * kRTz)
     const int I0 = bx * kRTx, J0 = by * kRTy, K0 = bz * kRTz;
     const int fi0 = 2 * I0 - 5, fj0 = 2 * J0 - 5, fk0 = 2 * K0 - 5;
     constexpr int kTile = kRFx * kRFy * kRFz;
-    for (int e0 = threadIdx.x; e0 < kTile; e0 += 8 * blockDim.x) { // 8 independent loads in flight
-        double v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int e = e0 + u * blockDim.x;
-            const int kk = e % kRFz, jj = (e / kRFz) % kRFy, ii = e / (kRFz * kRFy);
-            const int i = fi0 + ii, j = fj0 + jj, k = fk0 + kk;
-            v[u] = (e < kTile && i >= 0 && i < p.fd[0] && j >= 0 && j < p.fd[1] && k >= 0 && k < p.fd[2])
-                       ? fine[(size_t(i) * p.fd[1] + j) * p.fd[2] + k]
-                       : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-            if (e0 + u * blockDim.x < kTile) tile[e0 + u * blockDim.x] = v[u];
+    // the whole tile in one batch of asynchronous 8-byte copies (zero-filled outside
+    // the lattice): one memory latency instead of one per round of register loads
+    for (int e = threadIdx.x; e < kTile; e += blockDim.x) {
+        const int kk = e % kRFz, jj = (e / kRFz) % kRFy, ii = e / (kRFz * kRFy);
+        const int i = fi0 + ii, j = fj0 + jj, k = fk0 + kk;
+        const bool in = i >= 0 && i < p.fd[0] && j >= 0 && j < p.fd[1] && k >= 0 && k < p.fd[2];
+        const double* src = in ? fine + (size_t(i) * p.fd[1] + j) * p.fd[2] + k : fine;
+        const unsigned dst = unsigned(__cvta_generic_to_shared(tile + e));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(in ? 8 : 0));
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     const int tz = threadIdx.x % kRTz, ty = (threadIdx.x / kRTz) % kRTy, tx = threadIdx.x / (kRTz * kRTy);
     const int I = I0 + tx, J = J0 + ty, K = K0 + tz;
