@@ -13,8 +13,8 @@
 // replicated.
 //
 // One step is four phases with an exchange between consecutive phases:
-//   0  bin + sort + clusters, owned pair lists + pair sum, owned anterpolation
-//      -> level-0 charge planes                                   exchange #1
+//   0  bin + sort + clusters, owned pair lists, owned anterpolation
+//      -> level-0 charge planes; the owned pair sum is left running   exchange #1
 //   1  restriction, owned lattice-cutoff planes -> level potentials exchange #2
 //   2  top level, prolongation, owned interpolation + forces + energy share,
 //      owned Verlet update -> particle state                       exchange #3
@@ -55,11 +55,17 @@ void export_planes(cudaStream_t st, const Geometry& g, const Part& P, int k, con
     if (cnt) ckd(cudaMemcpyAsync(x + off, src + off, cnt * sizeof(double), cudaMemcpyDeviceToDevice, st), "D2D");
 }
 
+// The pair sum overlaps the long-range chain and the exchanges: phase 0 checks the
+// binning (and the pair-list capacity) synchronously, then leaves the pair kernel
+// running on the field's main stream; the chain of phases 1 and 2 runs on its side
+// stream; phase 2 joins both before interpolation.
 int phase0(msmb_field* f, Workspace& W, DevState& s, long long* xbuf, int rebuild, double* rebuilt) {
     const Geometry& g = W.g;
-    cudaStream_t st = f->stream;
+    cudaStream_t st = f->stream, sd = f->side_hi;
     for (int attempt = 0; attempt < 8; ++attempt) {
         ensure_const_table(f, W);
+        int rb0 = 0;
+        ckd(cudaMemcpy(&rb0, W.c.flag + 2, sizeof(int), cudaMemcpyDeviceToHost), "D2H");
         int nl = launch_reset_err(st, W.err, 0);
         nl += launch_bin(st, g, s, W.a, W.c, W.err);
         nl += launch_sort(st, g, s, W.a, W.c, W.err);
@@ -67,8 +73,7 @@ int phase0(msmb_field* f, Workspace& W, DevState& s, long long* xbuf, int rebuil
         // marks a call's first step and no longer forces one: same schedule as msmb_propagate)
         (void)rebuild;
         nl += launch_clusters(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.part, attempt > 0 ? 1 : 0);
-        nl += launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.part);
-        nl += launch_anterp(st, g, W.a, W.c, W.L, W.err, W.part);
+        nl += launch_err_brute(st, s.n, s, W.a, W.err);
         nl += launch_finalize(st, s, W.err);
         f->launches += nl;
         ckd(cudaGetLastError(), "kernel launch");
@@ -77,17 +82,22 @@ int phase0(msmb_field* f, Workspace& W, DevState& s, long long* xbuf, int rebuil
             grow_cap(W, r);
             continue;
         }
-        const int64_t before = f->counters[6];
-        record_counters(f, W, r);
-        if (rebuilt) *rebuilt = f->counters[6] != before ? 1.0 : 0.0;
         // binning, sorting and error detection are replicated: every part fails alike
         if (r.kind) return engine_set_error(f, error_from_rec(r));
+        int rb1 = 0;
+        ckd(cudaMemcpy(&rb1, W.c.flag + 2, sizeof(int), cudaMemcpyDeviceToHost), "D2H");
+        if (rebuilt) *rebuilt = rb1 != rb0 ? 1.0 : 0.0;
+        f->launches += launch_anterp(st, g, W.a, W.c, W.L, W.err, W.part);
+        ckd(cudaEventRecord(f->fork_ev, st), "record");
+        f->launches += launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.part); // joined in phase 2
+        ckd(cudaStreamWaitEvent(sd, f->fork_ev, 0), "wait");
         if (W.part.nparts > 1) { // one part: the charges stay where phase 1 reads them
             const LevelGeom& l0 = g.lv[0];
-            f->launches += launch_fill_i64(st, xbuf, int64_t(l0.size), LLONG_MIN);
-            export_planes(st, g, W.part, 0, W.L.charge, xbuf);
+            f->launches += launch_fill_i64(sd, xbuf, int64_t(l0.size), LLONG_MIN);
+            export_planes(sd, g, W.part, 0, W.L.charge, xbuf);
         }
-        ckd(cudaStreamSynchronize(st), "sync");
+        ckd(cudaGetLastError(), "kernel launch");
+        ckd(cudaStreamSynchronize(sd), "sync");
         return MSMB_OK;
     }
     return engine_set_error(f, Error{MSMB_ERR_INTERNAL, -1, -1, -1, "pair list did not converge"});
@@ -95,30 +105,32 @@ int phase0(msmb_field* f, Workspace& W, DevState& s, long long* xbuf, int rebuil
 
 int phase1(msmb_field* f, Workspace& W, const long long* xin, long long* xbuf) {
     const Geometry& g = W.g;
-    cudaStream_t st = f->stream;
+    cudaStream_t sd = f->side_hi;
     const bool x = W.part.nparts > 1;
-    if (x) ckd(cudaMemcpyAsync(W.L.charge, xin, sizeof(double) * g.lv[0].size, cudaMemcpyDeviceToDevice, st), "D2D");
+    if (x) ckd(cudaMemcpyAsync(W.L.charge, xin, sizeof(double) * g.lv[0].size, cudaMemcpyDeviceToDevice, sd), "D2D");
     ensure_const_table(f, W);
-    f->launches += launch_restrict_all(st, g, W.L, W.err);
+    f->launches += launch_restrict_all(sd, g, W.L, W.err);
     // the FFT path transforms whole levels (replicated); the direct path only owned planes
-    f->launches += W.lattice_fft ? launch_lattice_fft(st, W.fft, W.err) : launch_lattice(st, g, W.L, W.err, W.part);
+    f->launches += W.lattice_fft ? launch_lattice_fft(sd, W.fft, W.err) : launch_lattice(sd, g, W.L, W.err, W.part);
     if (x) {
-        f->launches += launch_fill_i64(st, xbuf, int64_t(g.lattice_total), LLONG_MIN);
-        for (int k = 0; k + 1 < g.levels; ++k) export_planes(st, g, W.part, k, W.L.pot, xbuf);
+        f->launches += launch_fill_i64(sd, xbuf, int64_t(g.lattice_total), LLONG_MIN);
+        for (int k = 0; k + 1 < g.levels; ++k) export_planes(sd, g, W.part, k, W.L.pot, xbuf);
     }
     ckd(cudaGetLastError(), "kernel launch");
-    ckd(cudaStreamSynchronize(st), "sync");
+    ckd(cudaStreamSynchronize(sd), "sync");
     return MSMB_OK;
 }
 
 int phase2(msmb_field* f, Workspace& W, DevState& s, const long long* xin, long long* xbuf, double dt, int kicks,
            int drift, double conv, double* energy) {
     const Geometry& g = W.g;
-    cudaStream_t st = f->stream;
+    cudaStream_t st = f->stream, sd = f->side_hi;
     const bool x = W.part.nparts > 1;
-    if (x) ckd(cudaMemcpyAsync(W.L.pot, xin, sizeof(double) * g.lattice_total, cudaMemcpyDeviceToDevice, st), "D2D");
-    f->launches += W.fft_top.n ? launch_lattice_fft(st, W.fft_top, W.err) : launch_top(st, g, W.L, W.err);
-    f->launches += launch_prolong_all(st, g, W.L, W.err);
+    if (x) ckd(cudaMemcpyAsync(W.L.pot, xin, sizeof(double) * g.lattice_total, cudaMemcpyDeviceToDevice, sd), "D2D");
+    f->launches += W.fft_top.n ? launch_lattice_fft(sd, W.fft_top, W.err) : launch_top(sd, g, W.L, W.err);
+    f->launches += launch_prolong_all(sd, g, W.L, W.err);
+    ckd(cudaEventRecord(f->join_ev, sd), "record");
+    ckd(cudaStreamWaitEvent(st, f->join_ev, 0), "join"); // pair sum (phase 0) + long-range chain
     DevOut o = W.o;
     o.phi = o.phis = o.phil = nullptr;
     if (s.n) ckd(cudaMemsetAsync(o.e, 0, sizeof(double) * size_t(s.n), st), "memset"); // unowned e_i = 0
@@ -131,7 +143,9 @@ int phase2(msmb_field* f, Workspace& W, DevState& s, const long long* xin, long 
     ckd(cudaGetLastError(), "kernel launch");
     double e = 0.0;
     if (s.n) ckd(cudaMemcpyAsync(&e, W.o.energy, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
-    ckd(cudaStreamSynchronize(st), "sync");
+    const ErrRec r = read_err(f, W); // synchronizes the main stream
+    record_counters(f, W, r);
+    if (r.kind) return engine_set_error(f, error_from_rec(r));
     if (energy) *energy = e;
     return MSMB_OK;
 }

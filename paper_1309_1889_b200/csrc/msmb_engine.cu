@@ -436,7 +436,9 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, 
     if (fork) ck(cudaEventRecord(f->join_ev, lr), "join");
     run("clusters", [&] { return launch_clusters(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, rebuild ? 1 : 0); });
     if (g_exp_stamps) launch_stamp(st, 4);
-    run("pairs", [&] { return launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole); });
+    run("pairs", [&] {
+        return launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole) + launch_err_brute(st, s.n, s, W.a, W.err);
+    });
     if (g_exp_stamps) launch_stamp(st, 5);
     if (fork) ck(cudaStreamWaitEvent(st, f->join_ev, 0), "join");
     DevOut o = W.o;
@@ -766,12 +768,16 @@ int msmb_create(const msmb_msm_config* cfg, const msmb_units* units, int device,
         if (!strcmp(e, "high")) side_prio = prio_hi, main_prio = prio_lo;
         if (!strcmp(e, "low")) side_prio = prio_lo, main_prio = prio_hi;
     }
+    // the spatial decomposition's long-range chain runs beside a pair kernel of many
+    // waves (C3: 131k blocks), whose pending blocks would otherwise be dispatched first
     if (cudaStreamCreateWithPriority(&f->stream, cudaStreamNonBlocking, main_prio) != cudaSuccess ||
         cudaStreamCreateWithPriority(&f->side, cudaStreamNonBlocking, side_prio) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&f->side_hi, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&f->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&f->join_ev, cudaEventDisableTiming) != cudaSuccess) {
         if (f->stream) cudaStreamDestroy(f->stream);
         if (f->side) cudaStreamDestroy(f->side);
+        if (f->side_hi) cudaStreamDestroy(f->side_hi);
         if (f->fork_ev) cudaEventDestroy(f->fork_ev);
         if (f->join_ev) cudaEventDestroy(f->join_ev);
         delete f;
@@ -789,6 +795,7 @@ static void field_free(msmb_field* f) {
     f->scratch.buf.reset();
     cudaStreamDestroy(f->stream);
     cudaStreamDestroy(f->side);
+    cudaStreamDestroy(f->side_hi);
     cudaEventDestroy(f->fork_ev);
     cudaEventDestroy(f->join_ev);
     delete f;

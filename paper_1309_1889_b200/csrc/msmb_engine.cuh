@@ -119,6 +119,7 @@ struct msmb_field {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;             // long-range chain, forked from `stream`
+    cudaStream_t side_hi = nullptr;          // the same at the highest priority (spatial decomposition)
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     std::recursive_mutex mu;
     std::unique_ptr<msmb::Workspace> ws;

@@ -576,7 +576,6 @@ struct PairP {
     double c0, c1, c2;   // gamma(r/a)/a = c0 + r2*(c1 + r2*c2)
     double d0, d1;       // g*'(r)/r + 1/r^3 = d0 + r2*d1
     double kc;
-    float cut2f;
 };
 
 #ifndef MSMB_RSQRT_NEWTON
@@ -998,17 +997,23 @@ int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& 
     p.d0 = 2.5 / (A * A * A);
     p.d1 = -1.5 / (A * A * A * A * A);
     p.kc = g.units.coulomb_constant;
-    p.cut2f = float_ru(A * A * (1.0 + 1e-6)); // + per-j-cluster rounding pad in k_pairs
     const int64_t maxclu = n / 32 + g.ncols + 1;
     int l = 0;
     if (n > 0) {
         k_pairs_mw<<<int((maxclu + kPairWarps - 1) / kPairWarps), kPairWarps * 32, 0, st>>>(
             c.clu, c.plist, c.pcnt, c.pmask, cap, a.xc, a.yc, a.zc, a.qc, p, A * A, a.phis, a.fsx, a.fsy, a.fsz,
             c.col_off, P.cx0 * g.ncy, P.cx1 * g.ncy, n, err);
-        k_err_brute<<<592, 256, 0, st>>>(n, s.x, s.y, s.z, a.outlist, err);
-        l = 2;
+        l = 1;
     }
     return l;
+}
+
+// pair errors of particles outside grid coverage (NaN / coincident with anyone); needs
+// only the binning, so the spatial decomposition checks it before the pair sum
+int launch_err_brute(cudaStream_t st, int64_t n, const DevState& s, DevAtoms& a, ErrRec* err) {
+    if (n <= 0) return 0;
+    k_err_brute<<<592, 256, 0, st>>>(n, s.x, s.y, s.z, a.outlist, err);
+    return 1;
 }
 
 // ============================================================================

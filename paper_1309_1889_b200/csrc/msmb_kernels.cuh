@@ -129,6 +129,7 @@ int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevStat
                     DevCells& c, ErrRec* err, int cap, const Part& P, int force_rebuild);
 int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
                  DevCells& c, ErrRec* err, int cap, const Part& P);
+int launch_err_brute(cudaStream_t st, int64_t n, const DevState& s, DevAtoms& a, ErrRec* err);
 int launch_anterp(cudaStream_t st, const Geometry& g, DevAtoms& a, DevCells& c, DevLevels& L,
                   ErrRec* err, const Part& P);
 int launch_restrict(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err);
