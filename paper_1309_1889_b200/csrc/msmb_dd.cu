@@ -69,8 +69,8 @@ int phase0(msmb_field* f, Workspace& W, DevState& s, long long* xbuf, int rebuil
         int nl = launch_reset_err(st, W.err, 0);
         nl += launch_bin(st, g, s, W.a, W.c, W.err);
         nl += launch_sort(st, g, s, W.a, W.c, W.err);
-        // the list is rebuilt when invalid or after a skin/2 move, as on one GPU (`rebuild`
-        // marks a call's first step and no longer forces one: same schedule as msmb_propagate)
+        // the list is rebuilt when invalid or after a skin/2 move, as on one GPU (`rebuild`,
+        // the caller's `kicks`, is ignored: the same schedule as msmb_propagate)
         (void)rebuild;
         nl += launch_clusters(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.part, attempt > 0 ? 1 : 0);
         nl += launch_err_brute(st, s.n, s, W.a, W.err);

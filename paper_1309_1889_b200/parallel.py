@@ -465,7 +465,7 @@ class SpatialDecomposition:
                     kicks, drift = 2, 1      # closing kick of step s, opening kick + drift of s+1
                 else:
                     kicks, drift = 1, 0      # closing half-kick of the last step
-                rebuilt = self._phase(0, kicks=1 if s == 0 else 0) > 0  # replicated decision
+                rebuilt = self._phase(0) > 0  # the (replicated) pair-list rebuild decision
                 if rebuilt and vel_pending:  # new owners need the old owners' velocities
                     self._exchange(2, "vel")
                     self._phase(4)
