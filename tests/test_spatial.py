@@ -155,3 +155,30 @@ def test_decomposed_errors_match_single_gpu():
     assert str(e1.value) == str(e2.value)
     p, v = dd.parts[0][1].download()
     assert np.array_equal(p, pos)  # state restored
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("parts", [2, 3])
+def test_decomposed_rebuilds_and_calls_bitwise(parts):
+    # a tiny skin makes the list (and so atom ownership) change mid-trajectory: the
+    # velocities then travel from the old owners (lazy velocity exchange); two calls
+    # reuse the list across the call boundary.  Bit-identical to one GPU run the same way.
+    w = fx.config("c1s", n_override=2048)
+    dt, skin = 0.05, 0.002
+    f = pkg.MsmField(pkg.MsmConfig(w.a, w.h, w.levels))
+    f.set_pair_skin(skin)
+    s = pkg.ParticleSystem(w.pos, w.vel, w.q, w.mass, w.box)
+    ds = pkg.DeviceSystem(f, s)
+    ds.propagate(dt, 12)
+    ds.propagate(dt, 9)
+    pos1, vel1 = ds.download()
+    nreb = f.work_counters()["list_rebuilds"]
+    assert nreb > 3
+    dd = parallel.SpatialDecomposition(pkg.MsmConfig(w.a, w.h, w.levels), s, local_parts=parts)
+    for fp, _, _ in dd.parts:
+        fp.set_pair_skin(skin)
+    dd.propagate(dt, 12, download=False)
+    out, _ = dd.propagate(dt, 9)
+    assert dd.parts[0][0].work_counters()["list_rebuilds"] == nreb
+    assert np.array_equal(out.positions, pos1)
+    assert np.array_equal(out.velocities, vel1)
