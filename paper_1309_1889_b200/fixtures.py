@@ -110,6 +110,7 @@ def config(name: str, seed: int | None = None, n_override: int | None = None) ->
     c3    : configs[2] (2^24 atoms, 551 A, rebalanced +-1, a=12 h=2.5 l=4, dt 2 fs x 20)
     c3s   : c3 survivable variant (RSA min-sep 1.5 A, dt 0.02 fs)
     c4    : configs[3] (water slab 300x650x650 A, a=12 h=2.5 l=5, dt 2 fs x 20)
+    c4s   : c4 survivable variant (O-O min-sep 2.5 A, dt 0.02 fs)
     c5    : configs[4] (2^20 atoms, 219 A, random_neutral; F a=12 h=2.5 l=4 dt .5 x100,
             G a=8 h=5 l=3 dt 2 x25; 8 slices)
     c5s   : c5 survivable parareal variant (RSA min-sep 1.5 A, F dt 0.005 x100, G dt 0.02 x25)
@@ -146,14 +147,15 @@ def config(name: str, seed: int | None = None, n_override: int | None = None) ->
         mass = np.full(n, 18.0)
         vel = maxwell_boltzmann(mass, 300.0, seed + 1)
         return Workload(name, pos, vel, q, mass, box, 12.0, 2.5, 4, 0.02 if surv else 2.0, 20)
-    if base == "c4":
+    if base in ("c4", "c4s"):
+        surv = base == "c4s"
         seed = 4309 if seed is None else seed
         nm = 4_225_000 if n_override is None else max(1, n_override // 3)
         s = (nm / 4_225_000) ** (1 / 3)
         box = np.array([300.0 * s, 650.0 * s, 650.0 * s])
-        pos, q, mass = water(nm, box, 0.0, seed)
+        pos, q, mass = water(nm, box, 2.5 if surv else 0.0, seed)
         vel = maxwell_boltzmann(mass, 300.0, seed + 1)
-        return Workload(name, pos, vel, q, mass, box, 12.0, 2.5, 5, 2.0, 20)
+        return Workload(name, pos, vel, q, mass, box, 12.0, 2.5, 5, 0.02 if surv else 2.0, 20)
     if base in ("c5", "c5s"):
         # c5s: survivable variant for parareal runs: RSA min-sep 1.5 A,
         # fine dt 0.005 fs x 100, coarse dt 0.02 fs x 25 (slice span 0.5 fs, 8 slices)
