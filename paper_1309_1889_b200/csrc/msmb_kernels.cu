@@ -2181,7 +2181,11 @@ static InterpP make_interp(const Geometry& g) {
 }
 
 // one thread per atom in cluster order (the short-range results are in that order)
-__global__ void k_interp(InterpP p, const int* __restrict__ colstart, int col_a, int col_b,
+#ifndef MSMB_INTERP_MINB
+#define MSMB_INTERP_MINB 5
+#endif
+__global__ void __launch_bounds__(128, MSMB_INTERP_MINB)
+    k_interp(InterpP p, const int* __restrict__ colstart, int col_a, int col_b,
                          const int* __restrict__ perm,
                          const double* __restrict__ xs, const double* __restrict__ ys,
                          const double* __restrict__ zs, const double* __restrict__ qs,
