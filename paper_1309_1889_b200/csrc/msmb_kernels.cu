@@ -781,7 +781,10 @@ __global__ void __launch_bounds__(kMaskWarps * 32)
 // cubic Newton step (rsqrt_pos); 22 DP instructions + 1 DSETP per pair step.
 // Measured alternatives (C2-S, ms): lanes in lockstep groups of 2 / 4 walking the
 // union of their masks (spatially sorted groups; fewer shared-memory bank
-// conflicts, more steps) 0.68 / 0.73 vs 0.63 per lane; unroll 8 vs 4: equal.
+// conflicts, more steps) 0.68 / 0.73 vs 0.63 per lane; unroll 8 vs 4: equal; each
+// lane preferring a mask bit whose row sits in bank quad (lane & 7) (conflict-free
+// when found, measured in a microbenchmark) 0.68: only 17% of steps find one --
+// a lane's mask holds ~1-2 atoms of a cluster -- and bank conflicts did not drop.
 __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     k_pairs_mw(const int2* __restrict__ clu, const int* __restrict__ plist, const int* __restrict__ pcnt,
                const unsigned* __restrict__ pmask, int cap, const double* __restrict__ xs,
