@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define MSMB_ABI_VERSION 1
+#define MSMB_ABI_VERSION 2
 
 /* Status codes == reference exception types. */
 enum msmb_status {
@@ -80,6 +80,42 @@ int msmb_create(const msmb_msm_config* cfg, const msmb_units* units, int device,
                 msmb_field** out);
 void msmb_destroy(msmb_field* f);
 
+/* ---- pair-only fields ----------------------------------
+ * paramd::SimpleCutoffField and paramd::WolfField (include/paramd/force_field.hpp:34-60;
+ * simple_cutoff / wolf_summation, src/electrostatics.cpp:66-132): the paper's
+ * coarse propagators and the CLI's default parareal coarse field
+ * (tools/paramd_main.cpp:417).  A field handle of either kind works with every
+ * entry point that takes a msmb_field (evaluate, propagate, systems, parareal as
+ * fine or coarse propagator); the MSM-only entry points (spatial decomposition,
+ * debug lattices/stages, lattice method) return MSMB_ERR_CONFIG for them.
+ * The result is the reference's: per-particle potential, forces with k_C,
+ * E = k_C sum 0.5 q_i phi_i in index order; phi_short receives phi and phi_long
+ * zeros (the reference leaves PotentialResult::short_part/long_part empty).
+ * Positions need not lie in the box: the box only sets the binning extent, atoms
+ * outside it are clamped into the boundary cells (correct for any position, fast
+ * when most atoms are inside).  A NaN coordinate makes every output NaN, as in the
+ * reference (every pair with that particle is NaN); an infinite coordinate, for
+ * which the reference mixes skipped and NaN pairs, is rejected with MSMB_ERR_DOMAIN. */
+enum msmb_field_kind { MSMB_FIELD_MSM = 0, MSMB_FIELD_CUTOFF = 1, MSMB_FIELD_WOLF = 2 };
+
+/* paramd::CutoffParams (include/paramd/potential.hpp:26-31: cutoff 12 A, optional
+ * wolf_alpha), plus the fields' cost-model constant flops_per_particle
+ * (force_field.hpp:36,50; <= 0 selects the reference defaults 301 / 350). */
+typedef struct msmb_cutoff_params {
+    double cutoff;
+    int has_wolf_alpha;
+    double wolf_alpha;
+    double flops_per_particle;
+} msmb_cutoff_params;
+
+/* SimpleCutoffField(params, units) / WolfField(params, units)  force_field.hpp:36,50.
+ * Validates like CutoffParams::validate(need_alpha = kind == WOLF)
+ * (src/electrostatics.cpp:38-42) and UnitsConfig::validate before touching the GPU. */
+int msmb_create_cutoff(int kind, const msmb_cutoff_params* params, const msmb_units* units,
+                       int device, msmb_field** out);
+/* msmb_field_kind of a handle. */
+int msmb_field_kind(const msmb_field* f);
+
 /* MsmField::evaluate / msm_potential(s, cfg, units)  force_field.cpp:37-39,
  * msm.cpp:52-90.  Host arrays; any output pointer may be NULL.
  * phi = per-particle potential per unit charge, phi_short/phi_long its two
@@ -108,7 +144,8 @@ void* msmb_host_alloc(int64_t bytes);
 void msmb_host_free(void* p);
 
 /* MsmField::cost_flops_per_step = msm_flops_simplified(a, h, n)
- * force_field.cpp:41-43, cost_model.cpp:37-43. */
+ * force_field.cpp:41-43, cost_model.cpp:37-43; SimpleCutoffField / WolfField:
+ * flops_per_particle * n (force_field.cpp:25-35). */
 double msmb_cost_flops_per_step(const msmb_field* f, int64_t n);
 
 /* Details of the last failure on this handle: kind = msmb_status, i/j the

@@ -1,4 +1,5 @@
-// paramd_b200/gpu_msm_field.hpp -- drop-in B200 MsmField for the reference
+// paramd_b200/gpu_msm_field.hpp -- drop-in B200 MsmField (and the pair-only
+// SimpleCutoffField / WolfField: GpuSimpleCutoffField, GpuWolfField) for the reference
 // library `paramd` (arXiv 1309.1889).  Header-only C++ over the C ABI in msmb.h.
 //
 // The reference's plugin interface is paramd::ForceField
@@ -60,19 +61,12 @@ inline msmb_msm_config to_c(const MsmConfig& c) {
 inline msmb_units to_c(const UnitsConfig& u) { return msmb_units{u.coulomb_constant, u.energy_to_native}; }
 }  // namespace detail_b200
 
-/// paramd::MsmField (force_field.hpp:62-73) evaluated on a B200.
-class GpuMsmField final : public ForceField {
+/// Common part of the B200 fields: one msmb_field handle (libmsmb.so).
+class GpuFieldBase : public ForceField {
   public:
-    GpuMsmField(MsmConfig config, UnitsConfig units, int device = 0)
-        : config_(config), units_(units) {
-        const msmb_msm_config c = detail_b200::to_c(config);
-        const msmb_units u = detail_b200::to_c(units);
-        const int rc = msmb_create(&c, &u, device, &h_);
-        if (rc) detail_b200::rethrow(nullptr, rc);
-    }
-    ~GpuMsmField() override { msmb_destroy(h_); }
-    GpuMsmField(const GpuMsmField&) = delete;
-    GpuMsmField& operator=(const GpuMsmField&) = delete;
+    ~GpuFieldBase() override { msmb_destroy(h_); }
+    GpuFieldBase(const GpuFieldBase&) = delete;
+    GpuFieldBase& operator=(const GpuFieldBase&) = delete;
 
     PotentialResult evaluate(const ParticleSystem& s) const override {
         const std::size_t n = s.size();
@@ -89,21 +83,73 @@ class GpuMsmField final : public ForceField {
                                      reinterpret_cast<double*>(r.per_particle_force.data()),
                                      &r.total_energy);
         if (rc) detail_b200::rethrow(h_, rc);
-        r.short_part = std::move(sp);
-        r.long_part = std::move(lp);
+        if (msmb_field_kind(h_) == MSMB_FIELD_MSM) { // the cutoff fields leave them empty
+            r.short_part = std::move(sp);
+            r.long_part = std::move(lp);
+        }
         return r;
     }
     double cost_flops_per_step(std::size_t n) const override {
         return msmb_cost_flops_per_step(h_, static_cast<int64_t>(n));
     }
+    msmb_field* handle() const { return h_; }
+
+  protected:
+    GpuFieldBase() = default;
+    msmb_field* h_ = nullptr;
+};
+
+/// paramd::MsmField (force_field.hpp:62-73) evaluated on a B200.
+class GpuMsmField final : public GpuFieldBase {
+  public:
+    GpuMsmField(MsmConfig config, UnitsConfig units, int device = 0)
+        : config_(config), units_(units) {
+        const msmb_msm_config c = detail_b200::to_c(config);
+        const msmb_units u = detail_b200::to_c(units);
+        const int rc = msmb_create(&c, &u, device, &h_);
+        if (rc) detail_b200::rethrow(nullptr, rc);
+    }
     std::string name() const override { return "msm"; }
     const MsmConfig& config() const { return config_; }
-    msmb_field* handle() const { return h_; }
 
   private:
     MsmConfig config_;
     UnitsConfig units_;
-    msmb_field* h_ = nullptr;
+};
+
+namespace detail_b200 {
+inline msmb_field* make_pair_field(int kind, const CutoffParams& p, const UnitsConfig& units,
+                                   double flops_per_particle, int device) {
+    const msmb_cutoff_params c{p.cutoff, p.wolf_alpha.has_value() ? 1 : 0, p.wolf_alpha.value_or(0.0),
+                               flops_per_particle};
+    const msmb_units u = to_c(units);
+    msmb_field* h = nullptr;
+    const int rc = msmb_create_cutoff(kind, &c, &u, device, &h);
+    if (rc) rethrow(nullptr, rc);
+    return h;
+}
+}  // namespace detail_b200
+
+/// paramd::SimpleCutoffField (force_field.hpp:34-46; simple_cutoff,
+/// src/electrostatics.cpp:66-89) evaluated on a B200.
+class GpuSimpleCutoffField final : public GpuFieldBase {
+  public:
+    GpuSimpleCutoffField(CutoffParams params, UnitsConfig units, double flops_per_particle = 301.0,
+                         int device = 0) {
+        h_ = detail_b200::make_pair_field(MSMB_FIELD_CUTOFF, params, units, flops_per_particle, device);
+    }
+    std::string name() const override { return "cutoff"; }
+};
+
+/// paramd::WolfField (force_field.hpp:48-60; wolf_summation,
+/// src/electrostatics.cpp:91-129) evaluated on a B200.
+class GpuWolfField final : public GpuFieldBase {
+  public:
+    GpuWolfField(CutoffParams params, UnitsConfig units, double flops_per_particle = 350.0,
+                 int device = 0) {
+        h_ = detail_b200::make_pair_field(MSMB_FIELD_WOLF, params, units, flops_per_particle, device);
+    }
+    std::string name() const override { return "wolf"; }
 };
 
 }  // namespace paramd
@@ -111,11 +157,11 @@ class GpuMsmField final : public ForceField {
 namespace paramd_b200 {
 
 /// paramd::propagate (src/integrate.cpp:13-36), device-resident when the spec's
-/// field is a GpuMsmField; any other field runs the reference's own propagate.
+/// field is a B200 field; any other field runs the reference's own propagate.
 inline paramd::ParticleSystem propagate(const paramd::PropagatorSpec& spec,
                                         const paramd::ParticleSystem& s,
                                         const paramd::UnitsConfig& units) {
-    auto* gf = dynamic_cast<const paramd::GpuMsmField*>(spec.force_field.get());
+    auto* gf = dynamic_cast<const paramd::GpuFieldBase*>(spec.force_field.get());
     if (!gf) return paramd::propagate(spec, s, units);
     spec.validate();
     units.validate();
@@ -132,11 +178,11 @@ inline paramd::ParticleSystem propagate(const paramd::PropagatorSpec& spec,
 }
 
 /// paramd::parareal_run (src/parareal.cpp:182-239) with device-resident states
-/// when both propagators use GpuMsmField.
+/// when both propagators use B200 fields (e.g. GpuMsmField fine, GpuSimpleCutoffField coarse).
 inline paramd::PararealResult parareal_run(const paramd::ParticleSystem& v, int total_points,
                                            const paramd::PararealConfig& cfg) {
-    auto* F = dynamic_cast<const paramd::GpuMsmField*>(cfg.fine.force_field.get());
-    auto* G = dynamic_cast<const paramd::GpuMsmField*>(cfg.coarse.force_field.get());
+    auto* F = dynamic_cast<const paramd::GpuFieldBase*>(cfg.fine.force_field.get());
+    auto* G = dynamic_cast<const paramd::GpuFieldBase*>(cfg.coarse.force_field.get());
     if (!F || !G) return paramd::parareal_run(v, total_points, cfg);
     msmb_parareal_config c{};
     c.window_points = cfg.window_points;

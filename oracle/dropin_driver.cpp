@@ -9,7 +9,11 @@
 //      calling the GPU plugin every step -- vs paramd::propagate(spec{MsmField});
 //   3. paramd_b200::propagate (device-resident) vs the reference;
 //   4. paramd::parareal_run with GPU fine/coarse fields vs the reference's;
-//   5. error behaviour: the reference's exception types come back out.
+//   5. error behaviour: the reference's exception types come back out;
+//   6. the pair-only fields: SimpleCutoffField / WolfField vs GpuSimpleCutoffField /
+//      GpuWolfField (evaluate, the reference's propagate over the plugin) and parareal
+//      with the CLI's default pairing, MSM fine + cutoff coarse (tools/paramd_main.cpp:417),
+//      through paramd_b200::parareal_run vs the reference's parareal_run.
 // Prints one JSON object; tests/test_gpu_dropin.py checks it.
 #include <chrono>
 #include <cmath>
@@ -18,6 +22,7 @@
 #include <random>
 #include <string>
 
+#include "paramd/electrostatics.hpp"
 #include "paramd/force_field.hpp"
 #include "paramd/generate.hpp"
 #include "paramd/integrate.hpp"
@@ -122,8 +127,51 @@ int main() {
     try { fr.evaluate(bad); } catch (const CoverageError& e) { cov_ref = e.what(); }
     try { fg.evaluate(bad); } catch (const CoverageError& e) { cov_gpu = e.what(); }
 
+    // 6. pair-only fields
+    CutoffParams cp;
+    cp.cutoff = 10.0;
+    CutoffParams wp = cp;
+    wp.wolf_alpha = 0.2;
+    auto ref_c = std::make_shared<SimpleCutoffField>(cp, units);
+    auto gpu_c = std::make_shared<GpuSimpleCutoffField>(cp, units);
+    auto ref_w = std::make_shared<WolfField>(wp, units);
+    auto gpu_w = std::make_shared<GpuWolfField>(wp, units);
+    double pf_de = 0, pf_df = 0;
+    for (int k = 0; k < 2; ++k) {
+        const ForceField& r0 = k ? static_cast<const ForceField&>(*ref_w) : *ref_c;
+        const ForceField& g0 = k ? static_cast<const ForceField&>(*gpu_w) : *gpu_c;
+        PotentialResult x = r0.evaluate(s), y = g0.evaluate(s);
+        pf_de = std::max(pf_de, std::fabs(x.total_energy - y.total_energy) / std::fabs(x.total_energy));
+        pf_df = std::max(pf_df, rel_rms(y.per_particle_force, x.per_particle_force));
+        if (y.short_part.has_value() || y.long_part.has_value() || r0.name() != g0.name()) pf_de = 1.0;
+        if (r0.cost_flops_per_step(2048) != g0.cost_flops_per_step(2048)) pf_de = 1.0;
+    }
+    PropagatorSpec scr{ref_c, 0.005, 20}, scg{gpu_c, 0.005, 20};
+    const double pf_dx = rel_rms(paramd::propagate(scg, s, units).positions, paramd::propagate(scr, s, units).positions);
+    const double pf_dx_dev = rel_rms(paramd_b200::propagate(scg, s, units).positions,
+                                     paramd::propagate(scr, s, units).positions);
+    PararealConfig pcr = cr, pcg = cg;
+    pcr.coarse = PropagatorSpec{ref_c, 0.02, 5};
+    pcg.coarse = PropagatorSpec{gpu_c, 0.02, 5};
+    double pf_dx_pr = -1;
+    try {
+        PararealResult rr = parareal_run(s, 6, pcr, sequential_executor());
+        PararealResult rd = paramd_b200::parareal_run(s, 6, pcg);
+        pf_dx_pr = 0;
+        for (int k = 0; k < 6; ++k)
+            pf_dx_pr = std::max(pf_dx_pr, rel_rms(rd.trajectory[k].positions, rr.trajectory[k].positions));
+        if (rr.report.counts.g_evals != rd.report.counts.g_evals || rr.report.counts.f_evals != rd.report.counts.f_evals)
+            pf_dx_pr = 1.0;
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "pair-field parareal: %s\n", e.what());
+    }
+
     std::printf(
-        "{\"de\": %.3e, \"df\": %.3e, \"dx_plugin_propagate\": %.3e, \"dx_device_propagate\": %.3e, "
+        "{\"pf_de\": %.3e, \"pf_df\": %.3e, \"pf_dx_plugin_propagate\": %.3e, \"pf_dx_device_propagate\": %.3e, "
+        "\"pf_dx_parareal_device\": %.3e, ",
+        pf_de, pf_df, pf_dx, pf_dx_dev, pf_dx_pr);
+    std::printf(
+        "\"de\": %.3e, \"df\": %.3e, \"dx_plugin_propagate\": %.3e, \"dx_device_propagate\": %.3e, "
         "\"parareal_ok\": %d, \"dx_parareal_plugin\": %.3e, \"dx_parareal_device\": %.3e, "
         "\"counts\": [%zu, %zu, %zu, %zu, %zu, %zu], \"coincident_ref\": \"%s\", \"coincident_gpu\": \"%s\", "
         "\"coverage_ref\": \"%s\", \"coverage_gpu\": \"%s\", \"name\": \"%s\", \"cost\": %.6e, \"cost_ref\": %.6e}\n",

@@ -824,8 +824,156 @@ int orc_interpolate(int64_t n, const double* pos, const double* box, double a, d
 }
 
 /* ---- propagate: src/integrate.cpp:7-36 --------------------------------------- */
+/* ---- pair-only fields: src/electrostatics.cpp:10-132, src/force_field.cpp:45-68 ----
+ * direct_coulomb, simple_cutoff, wolf_summation and PairRepulsionOverlay, restated
+ * with the reference's own i<j double loops (same operation order, so bitwise equal;
+ * O(N^2): these are the checkers for the GPU fields at test sizes).
+ * kind: 1 cutoff, 2 wolf, 3 direct. */
+enum { FK_MSM = 0, FK_CUTOFF = 1, FK_WOLF = 2, FK_DIRECT = 3 };
+
 typedef struct {
-    cfg_t msm;
+    int kind;            /* FK_* */
+    cfg_t msm;           /* FK_MSM */
+    double cutoff;       /* CutoffParams::cutoff */
+    int has_alpha;       /* CutoffParams::wolf_alpha engaged */
+    double alpha;
+    double rep_eps, rep_sigma; /* PairRepulsionOverlay (rep_eps > 0 = on) */
+} field_t;
+
+static int pair_field_eval(const field_t* F, int64_t n, const double* pos, const double* q, double kc,
+                           double conv, double* phi, double* force, double* energy, char* msg, int cap) {
+    int rc = validate_units(kc, conv, msg, cap); /* units.validate(), electrostatics.cpp:44,68,93 */
+    if (rc) return rc;
+    if (F->kind != FK_DIRECT) { /* CutoffParams::validate, electrostatics.cpp:38-42 */
+        if (!(F->cutoff > 0.0)) return fail(msg, cap, E_CONFIG, "cutoff must be > 0");
+        if (F->kind == FK_WOLF && !F->has_alpha) return fail(msg, cap, E_CONFIG, "wolf_alpha is required");
+        if (F->has_alpha && !(F->alpha >= 0.0)) return fail(msg, cap, E_CONFIG, "wolf_alpha must be >= 0");
+    }
+    const size_t N = (size_t)(n > 0 ? n : 1);
+    double* ph = (double*)calloc(N, sizeof(double));
+    double* fo = (double*)calloc(3 * N, sizeof(double));
+    const double a = F->cutoff, a2 = a * a;
+    const double k2sp = 1.1283791670955126; /* 2/sqrt(pi), electrostatics.cpp:12 */
+    double e_shift = 0, f_shift = 0, self_pc = 0, alpha = F->alpha;
+    if (F->kind == FK_WOLF) { /* electrostatics.cpp:96-102 */
+        const double erfc_aa = erfc(alpha * a);
+        e_shift = erfc_aa / a;
+        f_shift = erfc_aa / (a * a) + k2sp * alpha * exp(-alpha * alpha * a * a) / a;
+        self_pc = -(e_shift + k2sp * alpha);
+    }
+    for (int64_t i = 0; i < n && rc == OK; ++i)
+        for (int64_t j = i + 1; j < n; ++j) {
+            const double dx = pos[3 * i] - pos[3 * j], dy = pos[3 * i + 1] - pos[3 * j + 1],
+                         dz = pos[3 * i + 2] - pos[3 * j + 2];
+            const double r2 = dx * dx + dy * dy + dz * dz;
+            if (r2 == 0.0) { /* check_distinct, electrostatics.cpp:14-18 */
+                rc = fail(msg, cap, E_COINCIDENT, "particles %lld and %lld coincide", (long long)i, (long long)j);
+                break;
+            }
+            double pair, s;
+            if (F->kind == FK_DIRECT || F->kind == FK_CUTOFF) { /* :52-61, :76-86 */
+                if (F->kind == FK_CUTOFF && r2 >= a2) continue;
+                const double r = sqrt(r2);
+                const double inv_r = 1.0 / r;
+                pair = inv_r;
+                s = kc * q[i] * q[j] * inv_r * inv_r * inv_r;
+            } else { /* :108-118 */
+                if (r2 >= a2) continue;
+                const double r = sqrt(r2);
+                const double erfc_ar = erfc(alpha * r);
+                const double gauss = k2sp * alpha * exp(-alpha * alpha * r2);
+                pair = erfc_ar / r - e_shift + f_shift * (r - a);
+                const double fmag = erfc_ar / r2 + gauss / r - f_shift;
+                s = kc * q[i] * q[j] * fmag / r;
+            }
+            ph[i] += q[j] * pair;
+            ph[j] += q[i] * pair;
+            const double fx = dx * s, fy = dy * s, fz = dz * s;
+            fo[3 * i] += fx;
+            fo[3 * i + 1] += fy;
+            fo[3 * i + 2] += fz;
+            fo[3 * j] -= fx;
+            fo[3 * j + 1] -= fy;
+            fo[3 * j + 2] -= fz;
+        }
+    if (rc == OK && F->kind == FK_WOLF) /* :123-124 */
+        for (int64_t i = 0; i < n; ++i) ph[i] += q[i] * self_pc;
+    double e = 0.0; /* finish_total, :27-33 */
+    for (int64_t i = 0; i < n; ++i) e += 0.5 * q[i] * ph[i];
+    e = e * kc;
+    if (rc == OK && F->rep_eps > 0.0) { /* PairRepulsionOverlay::evaluate, force_field.cpp:45-68 */
+        const double s6 = pow(F->rep_sigma, 6.0);
+        const double s12 = s6 * s6;
+        double er = 0.0;
+        for (int64_t i = 0; i < n && rc == OK; ++i)
+            for (int64_t j = i + 1; j < n; ++j) {
+                const double dx = pos[3 * i] - pos[3 * j], dy = pos[3 * i + 1] - pos[3 * j + 1],
+                             dz = pos[3 * i + 2] - pos[3 * j + 2];
+                const double r2 = dx * dx + dy * dy + dz * dz;
+                if (r2 == 0.0) {
+                    rc = fail(msg, cap, E_COINCIDENT, "particles %lld and %lld coincide", (long long)i, (long long)j);
+                    break;
+                }
+                const double inv_r2 = 1.0 / r2;
+                const double inv_r12 = inv_r2 * inv_r2 * inv_r2 * inv_r2 * inv_r2 * inv_r2;
+                er += F->rep_eps * s12 * inv_r12;
+                const double sc = 12.0 * F->rep_eps * s12 * inv_r12 * inv_r2;
+                const double fx = dx * sc, fy = dy * sc, fz = dz * sc;
+                fo[3 * i] += fx;
+                fo[3 * i + 1] += fy;
+                fo[3 * i + 2] += fz;
+                fo[3 * j] -= fx;
+                fo[3 * j + 1] -= fy;
+                fo[3 * j + 2] -= fz;
+            }
+        e += er;
+    }
+    if (rc == OK) {
+        if (phi) memcpy(phi, ph, sizeof(double) * (size_t)n);
+        if (force) memcpy(force, fo, sizeof(double) * 3 * (size_t)n);
+        if (energy) *energy = e;
+    }
+    free(ph);
+    free(fo);
+    return rc == OK ? ok(msg, cap) : rc;
+}
+
+/* fspec = {kind, a, h, levels, has_alpha, alpha, rep_eps, rep_sigma}: a = MSM cutoff_a or
+ * CutoffParams::cutoff; h/levels for MSM only. */
+static field_t field_of(const double* fs) {
+    field_t F;
+    memset(&F, 0, sizeof F);
+    F.kind = (int)fs[0];
+    F.msm = (cfg_t){fs[1], fs[2], (int)fs[3], 3, 2};
+    F.cutoff = fs[1];
+    F.has_alpha = fs[4] != 0.0;
+    F.alpha = fs[5];
+    F.rep_eps = fs[6];
+    F.rep_sigma = fs[7];
+    return F;
+}
+
+static int msm_eval(int64_t n, const double* pos, const double* q, const double* box,
+                    const cfg_t* c, double kc, double conv, double* phi, double* phi_short,
+                    double* phi_long, double* force, double* energy, double* level_charge,
+                    double* level_potential, char* msg, int cap);
+
+static int field_eval(const field_t* F, int64_t n, const double* pos, const double* q, const double* box,
+                      double kc, double conv, double* phi, double* force, double* energy, char* msg, int cap) {
+    if (F->kind == FK_MSM && !(F->rep_eps > 0.0))
+        return msm_eval(n, pos, q, box, &F->msm, kc, conv, phi, NULL, NULL, force, energy, NULL, NULL, msg, cap);
+    if (F->kind == FK_MSM) return fail(msg, cap, E_OTHER, "oracle: repulsion overlay on MSM not restated");
+    return pair_field_eval(F, n, pos, q, kc, conv, phi, force, energy, msg, cap);
+}
+
+int orc_field_evaluate(const double* fspec, int64_t n, const double* pos, const double* q, const double* box,
+                       double kc, double conv, double* phi, double* force, double* energy, char* msg, int cap) {
+    const field_t F = field_of(fspec);
+    return field_eval(&F, n, pos, q, box, kc, conv, phi, force, energy, msg, cap);
+}
+
+typedef struct {
+    field_t field;
     double dt;
     int steps;
 } spec_t;
@@ -840,16 +988,14 @@ static int propagate(int64_t n, double* pos, double* vel, const double* q, const
     if (rc) return rc;
     double* f = (double*)malloc(sizeof(double) * 3 * (size_t)(n > 0 ? n : 1));
     const double dt = sp->dt;
-    rc = msm_eval(n, pos, q, box, &sp->msm, kc, conv, NULL, NULL, NULL, f, NULL, NULL, NULL, msg,
-                  cap);
+    rc = field_eval(&sp->field, n, pos, q, box, kc, conv, NULL, f, NULL, msg, cap);
     for (int step = 0; rc == OK && step < sp->steps; ++step) {
         for (int64_t i = 0; i < n; ++i) {
             const double cc = 0.5 * dt * conv / mass[i];
             for (int ax = 0; ax < 3; ++ax) vel[3 * i + ax] += f[3 * i + ax] * cc;
             for (int ax = 0; ax < 3; ++ax) pos[3 * i + ax] += vel[3 * i + ax] * dt;
         }
-        rc = msm_eval(n, pos, q, box, &sp->msm, kc, conv, NULL, NULL, NULL, f, NULL, NULL, NULL,
-                      msg, cap);
+        rc = field_eval(&sp->field, n, pos, q, box, kc, conv, NULL, f, NULL, msg, cap);
         if (rc) break;
         for (int64_t i = 0; i < n; ++i) {
             const double cc = 0.5 * dt * conv / mass[i];
@@ -864,8 +1010,36 @@ static int propagate(int64_t n, double* pos, double* vel, const double* q, const
 int orc_propagate(int64_t n, double* pos, double* vel, const double* q, const double* mass,
                   const double* box, double a, double h, int levels, double kc, double conv,
                   double dt, int steps, int* steps_done, char* msg, int cap) {
-    spec_t sp = {{a, h, levels, 3, 2}, dt, steps};
+    spec_t sp;
+    memset(&sp, 0, sizeof sp);
+    sp.field.msm = (cfg_t){a, h, levels, 3, 2};
+    sp.dt = dt;
+    sp.steps = steps;
     /* propagate works on a copy: on error the caller's state is untouched */
+    double* p2 = (double*)malloc(sizeof(double) * 3 * (size_t)(n > 0 ? n : 1));
+    double* v2 = (double*)malloc(sizeof(double) * 3 * (size_t)(n > 0 ? n : 1));
+    memcpy(p2, pos, sizeof(double) * 3 * (size_t)n);
+    memcpy(v2, vel, sizeof(double) * 3 * (size_t)n);
+    int rc = propagate(n, p2, v2, q, mass, box, &sp, kc, conv, steps_done, msg, cap);
+    if (rc == OK) {
+        memcpy(pos, p2, sizeof(double) * 3 * (size_t)n);
+        memcpy(vel, v2, sizeof(double) * 3 * (size_t)n);
+        ok(msg, cap);
+    }
+    free(p2);
+    free(v2);
+    return rc;
+}
+
+/* propagate with any field (fspec as orc_field_evaluate) */
+int orc_field_propagate(const double* fspec, int64_t n, double* pos, double* vel, const double* q,
+                        const double* mass, const double* box, double kc, double conv, double dt, int steps,
+                        int* steps_done, char* msg, int cap) {
+    spec_t sp;
+    memset(&sp, 0, sizeof sp);
+    sp.field = field_of(fspec);
+    sp.dt = dt;
+    sp.steps = steps;
     double* p2 = (double*)malloc(sizeof(double) * 3 * (size_t)(n > 0 ? n : 1));
     double* v2 = (double*)malloc(sizeof(double) * 3 * (size_t)(n > 0 ? n : 1));
     memcpy(p2, pos, sizeof(double) * 3 * (size_t)n);
@@ -1113,8 +1287,14 @@ static void pr_setup(pr_t* P, int64_t n, const double* q, const double* mass, co
     P->q = q;
     P->mass = mass;
     P->box = box;
-    P->fine = (spec_t){{fa, fh, fl, 3, 2}, fdt, fsteps};
-    P->coarse = (spec_t){{ga, gh, gl, 3, 2}, gdt, gsteps};
+    memset(&P->fine, 0, sizeof P->fine);
+    memset(&P->coarse, 0, sizeof P->coarse);
+    P->fine.field.msm = (cfg_t){fa, fh, fl, 3, 2};
+    P->fine.dt = fdt;
+    P->fine.steps = fsteps;
+    P->coarse.field.msm = (cfg_t){ga, gh, gl, 3, 2};
+    P->coarse.dt = gdt;
+    P->coarse.steps = gsteps;
     P->kc = kc;
     P->conv = conv;
 }
@@ -1128,6 +1308,44 @@ int orc_parareal_window(int64_t n, const double* pos, const double* vel, const d
     (void)threads;
     pr_t P;
     pr_setup(&P, n, q, mass, box, fa, fh, fl, fdt, fsteps, ga, gh, gl, gdt, gsteps, kc, conv);
+    P.window = t_points;
+    P.max_iter = k_iters;
+    P.tol = 1e300;
+    int rc = validate_pr(&P, msg, cap);
+    if (rc) return rc;
+    state_t v = {(double*)pos, (double*)vel};
+    window_t w;
+    rc = pr_init(&P, v, t_points, &w, msg, cap);
+    for (int k = 0; rc == OK && k < k_iters; ++k) rc = pr_iterate(&P, &w, msg, cap);
+    if (rc == OK) {
+        const int r = w.rows - 1;
+        for (int i = 0; i <= t_points; ++i) {
+            if (row_pos) memcpy(row_pos + 3 * n * i, w.lambda[r][i].pos, 24 * (size_t)n);
+            if (row_vel) memcpy(row_vel + 3 * n * i, w.lambda[r][i].vel, 24 * (size_t)n);
+        }
+        if (delta_rms)
+            for (int i = 1; i <= t_points; ++i) delta_rms[i] = w.delta[r][i].rms_pos;
+        if (counts) {
+            counts[0] = P.g_evals;
+            counts[1] = P.f_evals;
+            counts[2] = P.f_skipped;
+        }
+        ok(msg, cap);
+    }
+    win_free(n, &w);
+    return rc;
+}
+
+/* parareal window with any fine/coarse fields (fspec as orc_field_evaluate) */
+int orc_field_parareal_window(int64_t n, const double* pos, const double* vel, const double* q,
+                              const double* mass, const double* box, const double* fine_spec, double fdt,
+                              int fsteps, const double* coarse_spec, double gdt, int gsteps, double kc,
+                              double conv, int t_points, int k_iters, double* row_pos, double* row_vel,
+                              double* delta_rms, int64_t* counts, char* msg, int cap) {
+    pr_t P;
+    pr_setup(&P, n, q, mass, box, 0, 0, 0, fdt, fsteps, 0, 0, 0, gdt, gsteps, kc, conv);
+    P.fine.field = field_of(fine_spec);
+    P.coarse.field = field_of(coarse_spec);
     P.window = t_points;
     P.max_iter = k_iters;
     P.tol = 1e300;

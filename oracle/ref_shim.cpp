@@ -138,6 +138,26 @@ std::vector<MsmGridLevel> levels_for(const double* box, const MsmConfig& cfg) {
     return build_grid_hierarchy(s, cfg);
 }
 
+// fspec = {kind, a, h, levels, has_alpha, alpha, rep_eps, rep_sigma}: kind 0 MsmField,
+// 1 SimpleCutoffField, 2 WolfField, 3 DirectCoulombField (force_field.hpp:23-73); a is
+// MsmConfig::cutoff_a or CutoffParams::cutoff; rep_eps > 0 wraps the field in
+// PairRepulsionOverlay(field, rep_eps, rep_sigma) (force_field.hpp:82-97).
+std::shared_ptr<const ForceField> make_field(const double* fs, const UnitsConfig& u) {
+    std::shared_ptr<const ForceField> ff;
+    const int kind = static_cast<int>(fs[0]);
+    CutoffParams cp;
+    cp.cutoff = fs[1];
+    if (fs[4] != 0.0) cp.wolf_alpha = fs[5];
+    switch (kind) {
+        case 0: ff = std::make_shared<MsmField>(make_cfg(fs[1], fs[2], static_cast<int>(fs[3]), 3, 2), u); break;
+        case 1: ff = std::make_shared<SimpleCutoffField>(cp, u); break;
+        case 2: ff = std::make_shared<WolfField>(cp, u); break;
+        default: ff = std::make_shared<DirectCoulombField>(u); break;
+    }
+    if (fs[6] > 0.0) ff = std::make_shared<PairRepulsionOverlay>(ff, fs[6], fs[7]);
+    return ff;
+}
+
 }  // namespace
 
 extern "C" {
@@ -462,6 +482,85 @@ int ref_parareal_run(int64_t n, const double* pos, const double* vel, const doub
             counts[2] = static_cast<int64_t>(r.report.counts.f_skipped);
             counts[3] = r.report.windows;
             counts[4] = r.report.converged ? 1 : 0;
+        }
+    });
+}
+
+// ---- any ForceField (fspec above): evaluate, propagate trace, parareal window -----
+int ref_field_evaluate(const double* fspec, int64_t n, const double* pos, const double* q, const double* box,
+                       double kc, double conv, double* phi, double* force, double* energy, char* msg, int cap) {
+    return guarded(msg, cap, [&] {
+        ParticleSystem s = make_system(n, pos, nullptr, q, nullptr, box);
+        const UnitsConfig u{kc, conv};
+        PotentialResult r = make_field(fspec, u)->evaluate(s);
+        for (int64_t i = 0; i < n; ++i) {
+            if (phi) phi[i] = r.per_particle_potential[i];
+            if (force) {
+                force[3 * i] = r.per_particle_force[i].x;
+                force[3 * i + 1] = r.per_particle_force[i].y;
+                force[3 * i + 2] = r.per_particle_force[i].z;
+            }
+        }
+        if (energy) *energy = r.total_energy;
+    });
+}
+
+double ref_field_cost(const double* fspec, double kc, double conv, int64_t n) {
+    return make_field(fspec, UnitsConfig{kc, conv})->cost_flops_per_step(static_cast<std::size_t>(n));
+}
+
+int ref_field_propagate_trace(const double* fspec, int64_t n, double* pos, double* vel, const double* q,
+                              const double* mass, const double* box, double kc, double conv, double dt,
+                              int steps, int* steps_done, char* msg, int cap) {
+    *steps_done = 0;
+    ParticleSystem s = make_system(n, pos, vel, q, mass, box);
+    UnitsConfig u{kc, conv};
+    PropagatorSpec spec;
+    spec.force_field = make_field(fspec, u);
+    spec.dt = dt;
+    spec.steps_per_slice = 1;
+    int rc = OK;
+    for (int st = 0; st < steps; ++st) {
+        rc = guarded(msg, cap, [&] { s = propagate(spec, s, u); });
+        if (rc != OK) break;
+        *steps_done = st + 1;
+    }
+    store_state(s, pos, vel);
+    return rc;
+}
+
+int ref_field_parareal_window(int64_t n, const double* pos, const double* vel, const double* q,
+                              const double* mass, const double* box, const double* fine_spec, double fdt,
+                              int fsteps, const double* coarse_spec, double gdt, int gsteps, double kc,
+                              double conv, int t_points, int k_iters, double* row_pos, double* row_vel,
+                              double* delta_rms, int64_t* counts, char* msg, int cap) {
+    return guarded(msg, cap, [&] {
+        ParticleSystem s = make_system(n, pos, vel, q, mass, box);
+        UnitsConfig u{kc, conv};
+        PararealConfig cfg;
+        cfg.window_points = t_points;
+        cfg.max_iter = k_iters;
+        cfg.tol = 1e300;
+        cfg.units = u;
+        cfg.fine.force_field = make_field(fine_spec, u);
+        cfg.fine.dt = fdt;
+        cfg.fine.steps_per_slice = fsteps;
+        cfg.coarse.force_field = make_field(coarse_spec, u);
+        cfg.coarse.dt = gdt;
+        cfg.coarse.steps_per_slice = gsteps;
+        cfg.short_circuit = false;
+        PararealWindow w = parareal_init(s, cfg);
+        SequentialExecutor ex;
+        for (int k = 0; k < k_iters; ++k) parareal_iterate(w, cfg, ex);
+        const auto& row = w.lambda.back();
+        for (int i = 0; i <= t_points; ++i)
+            store_state(row[i], row_pos ? row_pos + 3 * n * i : nullptr, row_vel ? row_vel + 3 * n * i : nullptr);
+        if (delta_rms)
+            for (int i = 1; i <= t_points; ++i) delta_rms[i] = w.delta_rows.back()[i].rms_pos;
+        if (counts) {
+            counts[0] = static_cast<int64_t>(w.counts.g_evals);
+            counts[1] = static_cast<int64_t>(w.counts.f_evals);
+            counts[2] = static_cast<int64_t>(w.counts.f_skipped);
         }
     });
 }

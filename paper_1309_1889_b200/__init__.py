@@ -12,6 +12,11 @@ Reference interface -> here:
   paramd::ParticleSystem       include/paramd/system.hpp:10-18    -> ParticleSystem
   paramd::PotentialResult      include/paramd/potential.hpp:18-24 -> PotentialResult
   paramd::ForceField/MsmField  include/paramd/force_field.hpp:14-73 -> ForceField/MsmField
+  paramd::CutoffParams         include/paramd/potential.hpp:26-31 -> CutoffParams
+  paramd::SimpleCutoffField/WolfField
+                               include/paramd/force_field.hpp:34-60 -> SimpleCutoffField/WolfField
+  paramd::simple_cutoff/wolf_summation
+                               include/paramd/electrostatics.hpp:12-22 -> same names
   paramd::msm_potential        include/paramd/msm.hpp:24-25       -> msm_potential
   paramd::PropagatorSpec/propagate/verlet_step/energy_report
                                include/paramd/integrate.hpp:13-38 -> same names
@@ -32,6 +37,7 @@ from . import _native
 
 __all__ = [
     "MsmConfig", "UnitsConfig", "ParticleSystem", "PotentialResult", "ForceField", "MsmField",
+    "GpuField", "CutoffParams", "SimpleCutoffField", "WolfField", "simple_cutoff", "wolf_summation",
     "msm_potential", "PropagatorSpec", "propagate", "verlet_step", "energy_report", "EnergyReport",
     "PararealConfig", "PararealResult", "parareal_window", "parareal_run", "SequentialExecutor",
     "AsyncExecutor", "DeviceSystem", "Error", "ConfigError", "DomainError", "CoverageError",
@@ -201,34 +207,19 @@ class ForceField:
         raise NotImplementedError
 
 
-class MsmField(ForceField):
-    """paramd::MsmField (force_field.hpp:62-73) evaluated on a B200.
+class GpuField(ForceField):
+    """A force field bound to one B200 (a msmb_field handle): the common part of
+    MsmField, SimpleCutoffField and WolfField.  ``evaluate`` is const and safe to
+    call from several threads (calls on one field are serialised on its GPU stream)."""
 
-    ``evaluate`` is const and safe to call from several threads (calls on one
-    field are serialised on its GPU stream)."""
-
-    def __init__(self, config: MsmConfig, units: UnitsConfig = None, device: int = 0):
-        units = units or UnitsConfig.physical()
-        self._config, self._units = config, units
-        self._device = device
-        self._h = C.c_void_p()
-        cfg, u = config._c(), units._c()
-        rc = _native.lib().msmb_create(C.byref(cfg), C.byref(u), device, C.byref(self._h))
-        if rc:
-            _raise(None, rc)
+    _h = None
 
     @property
     def handle(self):
         return self._h
 
-    def config(self) -> MsmConfig:
-        return self._config
-
     def units(self) -> UnitsConfig:
         return self._units
-
-    def name(self) -> str:
-        return "msm"
 
     def cost_flops_per_step(self, n: int) -> float:
         return _native.lib().msmb_cost_flops_per_step(self._h, n)
@@ -249,11 +240,6 @@ class MsmField(ForceField):
         """Pair-list skin in A (default 0.2; 0 = rebuild the list at every evaluation,
         making forces a pure function of the positions).  See msmb_set_pair_skin."""
         _check(self._h, _native.lib().msmb_set_pair_skin(self._h, float(skin)))
-
-    def set_lattice_method(self, direct: bool):
-        """Lattice cutoff by zero-padded FFT convolution (default) or by the direct
-        stencil sum of the reference (src/msm_phases.cpp:93-134)."""
-        _check(self._h, _native.lib().msmb_set_lattice_method(self._h, int(bool(direct))))
 
     def set_stage_timing(self, on: bool):
         _native.lib().msmb_set_stage_timing(self._h, int(on))
@@ -278,6 +264,42 @@ class MsmField(ForceField):
 
     def kernel_launches(self) -> int:
         return int(_native.lib().msmb_kernel_launches(self._h))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if sys.is_finalizing():  # process teardown releases the device anyway
+            return
+        if h is not None and h.value:
+            try:
+                _native.lib().msmb_destroy(h)
+            except Exception:
+                pass
+            self._h = C.c_void_p()
+
+
+class MsmField(GpuField):
+    """paramd::MsmField (force_field.hpp:62-73) evaluated on a B200."""
+
+    def __init__(self, config: MsmConfig, units: UnitsConfig = None, device: int = 0):
+        units = units or UnitsConfig.physical()
+        self._config, self._units = config, units
+        self._device = device
+        self._h = C.c_void_p()
+        cfg, u = config._c(), units._c()
+        rc = _native.lib().msmb_create(C.byref(cfg), C.byref(u), device, C.byref(self._h))
+        if rc:
+            _raise(None, rc)
+
+    def config(self) -> MsmConfig:
+        return self._config
+
+    def name(self) -> str:
+        return "msm"
+
+    def set_lattice_method(self, direct: bool):
+        """Lattice cutoff by zero-padded FFT convolution (default) or by the direct
+        stencil sum of the reference (src/msm_phases.cpp:93-134)."""
+        _check(self._h, _native.lib().msmb_set_lattice_method(self._h, int(bool(direct))))
 
     def debug_levels(self):
         dims, _, _ = grid_geometry(self._config, self._last_box)
@@ -316,16 +338,76 @@ class MsmField(ForceField):
         _check(self._h, rc)
         return out
 
-    def __del__(self):
-        h = getattr(self, "_h", None)
-        if sys.is_finalizing():  # process teardown releases the device anyway
-            return
-        if h is not None and h.value:
-            try:
-                _native.lib().msmb_destroy(h)
-            except Exception:
-                pass
-            self._h = C.c_void_p()
+
+@dataclass
+class CutoffParams:
+    """paramd::CutoffParams (potential.hpp:26-31)."""
+    cutoff: float = 12.0
+    wolf_alpha: Optional[float] = None
+
+    def validate(self, need_alpha: bool):  # src/electrostatics.cpp:38-42
+        if not (self.cutoff > 0.0):
+            raise ConfigError("cutoff must be > 0")
+        if need_alpha and self.wolf_alpha is None:
+            raise ConfigError("wolf_alpha is required")
+        if self.wolf_alpha is not None and not (self.wolf_alpha >= 0.0):
+            raise ConfigError("wolf_alpha must be >= 0")
+
+
+class _PairField(GpuField):
+    """Pair-only GPU fields (msmb_create_cutoff): the MSM engine's binning, cluster
+    pair list and pair kernel with the field's pair function and no grid.  The box
+    of an evaluated system only sets the binning extent (atoms outside it are
+    still handled); ``short_part`` is the potential and ``long_part`` zeros."""
+    _kind = 0
+    _default_fpp = 0.0
+
+    def __init__(self, params: CutoffParams = None, units: UnitsConfig = None,
+                 flops_per_particle: float = None, device: int = 0):
+        self._params = params or CutoffParams()
+        self._units = units or UnitsConfig.physical()
+        self._fpp = self._default_fpp if flops_per_particle is None else float(flops_per_particle)
+        self._device = device
+        self._h = C.c_void_p()
+        p = self._params
+        pc = _native.CutoffParamsC(p.cutoff, int(p.wolf_alpha is not None), float(p.wolf_alpha or 0.0), self._fpp)
+        u = self._units._c()
+        rc = _native.lib().msmb_create_cutoff(self._kind, C.byref(pc), C.byref(u), device, C.byref(self._h))
+        if rc:
+            _raise(None, rc)
+
+    def params(self) -> CutoffParams:
+        return self._params
+
+
+class SimpleCutoffField(_PairField):
+    """paramd::SimpleCutoffField (force_field.hpp:34-46): Coulomb truncated at r >= cutoff
+    (simple_cutoff, src/electrostatics.cpp:66-89), on a B200."""
+    _kind = 1
+    _default_fpp = 301.0
+
+    def name(self) -> str:
+        return "cutoff"
+
+
+class WolfField(_PairField):
+    """paramd::WolfField (force_field.hpp:48-60): damped-shifted-force electrostatics
+    (wolf_summation, src/electrostatics.cpp:91-129), on a B200."""
+    _kind = 2
+    _default_fpp = 350.0
+
+    def name(self) -> str:
+        return "wolf"
+
+
+def simple_cutoff(s: ParticleSystem, params: CutoffParams, units: UnitsConfig = None) -> PotentialResult:
+    """paramd::simple_cutoff (electrostatics.hpp:12-13) on the GPU."""
+    return SimpleCutoffField(params, units or UnitsConfig.physical()).evaluate(s)
+
+
+def wolf_summation(s: ParticleSystem, params: CutoffParams, units: UnitsConfig = None) -> PotentialResult:
+    """paramd::wolf_summation (electrostatics.hpp:21-22) on the GPU."""
+    return WolfField(params, units or UnitsConfig.physical()).evaluate(s)
 
 
 def msm_potential(s: ParticleSystem, config: MsmConfig, units: UnitsConfig = None) -> PotentialResult:
@@ -338,7 +420,7 @@ def msm_potential(s: ParticleSystem, config: MsmConfig, units: UnitsConfig = Non
 class DeviceSystem:
     """A ParticleSystem resident in HBM (msmb_system), for device-resident propagation."""
 
-    def __init__(self, field: MsmField, s: ParticleSystem):
+    def __init__(self, field: GpuField, s: ParticleSystem):
         self.field = field
         self.n = s.size()
         self.box = s.box.copy()
@@ -404,8 +486,8 @@ def propagate(spec: PropagatorSpec, s: ParticleSystem, units: UnitsConfig = None
     """paramd::propagate (src/integrate.cpp:13-36), device-resident on the B200."""
     spec.validate()
     units = units or UnitsConfig.physical()
-    if not isinstance(spec.force_field, MsmField):
-        raise ConfigError("this build propagates MsmField force fields only")
+    if not isinstance(spec.force_field, GpuField):
+        raise ConfigError("this build propagates GPU force fields (MsmField, SimpleCutoffField, WolfField) only")
     out = s.copy()
     u = units._c()
     ff = spec.force_field
@@ -469,7 +551,7 @@ class PararealConfig:
 
     def _c(self):
         def prop(sp):
-            h = sp.force_field.handle if isinstance(sp.force_field, MsmField) else None
+            h = sp.force_field.handle if isinstance(sp.force_field, GpuField) else None
             return _native.PropagatorC(h, sp.dt, sp.steps_per_slice)
         return _native.PararealC(self.window_points, self.max_iter, self.tol, prop(self.fine),
                                  prop(self.coarse), self.units._c(), int(self.skip_threshold is not None),
@@ -485,7 +567,7 @@ class PararealResult:
 
 
 def _cfg_handle(cfg):
-    return cfg.fine.force_field.handle if isinstance(cfg.fine.force_field, MsmField) else None
+    return cfg.fine.force_field.handle if isinstance(cfg.fine.force_field, GpuField) else None
 
 
 def parareal_window(v: ParticleSystem, cfg: PararealConfig, t_points: int, k_iters: int,

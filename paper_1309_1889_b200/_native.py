@@ -28,6 +28,11 @@ class UnitsC(C.Structure):
     _fields_ = [("coulomb_constant", C.c_double), ("energy_to_native", C.c_double)]
 
 
+class CutoffParamsC(C.Structure):
+    _fields_ = [("cutoff", C.c_double), ("has_wolf_alpha", C.c_int), ("wolf_alpha", C.c_double),
+                ("flops_per_particle", C.c_double)]
+
+
 class PropagatorC(C.Structure):
     _fields_ = [("field", _VP), ("dt", C.c_double), ("steps_per_slice", C.c_int)]
 
@@ -45,6 +50,9 @@ SIGNATURES = {
     "msmb_device_count": (C.c_int, []),
     "msmb_create": (C.c_int, [C.POINTER(MsmConfigC), C.POINTER(UnitsC), C.c_int, C.POINTER(_VP)]),
     "msmb_destroy": (None, [_VP]),
+    "msmb_create_cutoff": (C.c_int, [C.c_int, C.POINTER(CutoffParamsC), C.POINTER(UnitsC), C.c_int,
+                                     C.POINTER(_VP)]),
+    "msmb_field_kind": (C.c_int, [_VP]),
     "msmb_evaluate": (C.c_int, [_VP, C.c_int64, _D, _D, _D, _D, _D, _D, _D, _D]),
     "msmb_propagate": (C.c_int, [_VP, C.c_int64, _D, _D, _D, _D, _D, C.c_double, C.c_int]),
     "msmb_propagate_ex": (C.c_int, [_VP, C.c_int64, _D, _D, _D, _D, _D, C.c_double, C.c_int,

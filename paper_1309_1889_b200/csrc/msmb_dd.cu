@@ -188,6 +188,8 @@ extern "C" int msmb_dd_plan(const msmb_msm_config* cfg, const msmb_units* units,
 extern "C" int msmb_dd_set_part(msmb_field* f, int nparts, int part) {
     if (!f) return MSMB_ERR_CONFIG;
     std::lock_guard<std::recursive_mutex> lk(f->mu);
+    if (f->kind != MSMB_FIELD_MSM)
+        return engine_set_error(f, Error{MSMB_ERR_CONFIG, -1, -1, -1, "this entry point needs an MSM field"});
     if (nparts < 1 || part < 0 || part >= nparts)
         return engine_set_error(f, Error{MSMB_ERR_CONFIG, -1, -1, -1, "invalid decomposition part"});
     f->dd_nparts = nparts;
@@ -207,6 +209,8 @@ extern "C" int msmb_set_pair_skin(msmb_field* f, double skin) {
 extern "C" int msmb_set_lattice_method(msmb_field* f, int direct) {
     if (!f) return MSMB_ERR_CONFIG;
     std::lock_guard<std::recursive_mutex> lk(f->mu);
+    if (f->kind != MSMB_FIELD_MSM)
+        return engine_set_error(f, Error{MSMB_ERR_CONFIG, -1, -1, -1, "this entry point needs an MSM field"});
     f->lattice_direct = direct ? 1 : 0;
     f->ws.reset(); // rebuilt on the next call with the chosen method
     return MSMB_OK;
@@ -215,6 +219,8 @@ extern "C" int msmb_set_lattice_method(msmb_field* f, int direct) {
 extern "C" int msmb_dd_sizes(msmb_field* f, msmb_system* sys, int64_t* out) {
     if (!f || !sys || !out) return MSMB_ERR_CONFIG;
     std::lock_guard<std::recursive_mutex> lk(f->mu);
+    if (f->kind != MSMB_FIELD_MSM)
+        return engine_set_error(f, Error{MSMB_ERR_CONFIG, -1, -1, -1, "this entry point needs an MSM field"});
     try {
         cudaSetDevice(f->device);
         Error e = ensure_workspace(f, sys->st.n, sys->st.box);
@@ -232,6 +238,8 @@ extern "C" int msmb_dd_phase(msmb_field* f, msmb_system* sys, int phase, double 
                              const msmb_units* units, const void* xin, void* xout, double* energy) {
     if (!f || !sys || (phase > 0 && !xin) || (phase < 3 && !xout)) return MSMB_ERR_CONFIG;
     std::lock_guard<std::recursive_mutex> lk(f->mu);
+    if (f->kind != MSMB_FIELD_MSM)
+        return engine_set_error(f, Error{MSMB_ERR_CONFIG, -1, -1, -1, "this entry point needs an MSM field"});
     try {
         cudaSetDevice(f->device);
         f->last = Error{};

@@ -121,7 +121,12 @@ Error error_from_rec(const ErrRec& r) {
             e.msg = buf;
             break;
         case MSMB_ERR_DOMAIN:
-            e.msg = "kernel_g_star: r must be > 0";
+            if (r.err_i >= 0 && r.err_j < 0) { // pair-only fields: infinite coordinate (msmb.h)
+                snprintf(buf, sizeof buf, "particle %lld has a non-finite position", (long long)r.err_i);
+                e.msg = buf;
+            } else {
+                e.msg = "kernel_g_star: r must be > 0";
+            }
             break;
         default:
             e.msg = "internal error";
@@ -169,12 +174,16 @@ void ensure_const_table(msmb_field* f, Workspace& W) {
     g_const_owner[d] = W.uid;
 }
 
+static bool make_levels(msmb_field* f, Workspace& W, Error& e);
+
 static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const double* box,
                                                  Error& e) {
     auto W = std::make_unique<Workspace>();
     W->uid = g_ws_uid++;
-    e = build_geometry(f->cfg, f->units, box, n, W->g);
+    e = f->kind == MSMB_FIELD_MSM ? build_geometry(f->cfg, f->units, box, n, W->g)
+                                  : build_pair_geometry(f->kind, f->cut, f->units, box, n, W->g);
     if (e.kind) return nullptr;
+    const bool msm = f->kind == MSMB_FIELD_MSM;
     Geometry& g = W->g;
     if (f->pair_skin >= 0.0) g.skin = f->pair_skin;
     W->n = n;
@@ -186,7 +195,7 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
     a.rank = walloc<int>(*W, N);
     a.perm = walloc<int>(*W, N);
     a.outlist = walloc<int>(*W, N);
-    a.aw = walloc<double>(*W, N * 12);
+    a.aw = msm ? walloc<double>(*W, N * 12) : nullptr;
     a.phis = walloc<double>(*W, N);
     a.fsx = walloc<double>(*W, N);
     a.fsy = walloc<double>(*W, N);
@@ -217,6 +226,31 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
     ck(cudaMemset(c.flag, 0, 5 * sizeof(int)), "memset");
     ck(cudaMemset(c.colstart, 0, sizeof(int) * size_t(g.ncols + 1)), "memset");
     alloc_plist(*W, g.pair_cap);
+    DevOut& o = W->o;
+    o.fx = walloc<double>(*W, N);
+    o.fy = walloc<double>(*W, N);
+    o.fz = walloc<double>(*W, N);
+    o.phi = walloc<double>(*W, N);
+    o.phis = walloc<double>(*W, N);
+    o.phil = walloc<double>(*W, N);
+    o.e = walloc<double>(*W, N);
+    o.partial = walloc<double>(*W, size_t(reduce_blocks(n)));
+    o.energy = walloc<double>(*W, 1);
+    ck(W->backup.alloc(sizeof(double) * 6 * N), "cudaMalloc backup");
+    ck(W->staging.alloc(sizeof(double) * 3 * N), "cudaMalloc staging");
+    ck(cudaMalloc(&W->err, sizeof(ErrRec)), "cudaMalloc err");
+    ck(cudaMallocHost(&W->err_host, sizeof(ErrRec)), "cudaMallocHost err");
+    if (msm && !make_levels(f, *W, e)) return nullptr;
+    // wupload's pageable cudaMemcpy may return before its DMA lands, and the
+    // field's streams are non-blocking (not ordered after the legacy stream)
+    ck(cudaDeviceSynchronize(), "sync uploads");
+    return W;
+}
+
+// The MSM grid hierarchy: level lattices, transfer and stencil tables, FFT plans.
+static bool make_levels(msmb_field* f, Workspace& Wr, Error& e) {
+    Workspace* W = &Wr;
+    const Geometry& g = W->g;
     DevLevels& L = W->L;
     L.charge = walloc<double>(*W, g.lattice_total);
     L.pot = walloc<double>(*W, g.lattice_total);
@@ -317,28 +351,11 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
         e.kind = MSMB_ERR_CONFIG;
         e.msg = "msm: top level of " + std::to_string(g.lv[g.levels - 1].size) +
                 " points exceeds this build's shared-memory stencil tile";
-        return nullptr;
+        return false;
     }
     ck(conv_prepare(smem), "cudaFuncSetAttribute");
     ck(top_prepare(g), "cudaFuncSetAttribute");
-    DevOut& o = W->o;
-    o.fx = walloc<double>(*W, N);
-    o.fy = walloc<double>(*W, N);
-    o.fz = walloc<double>(*W, N);
-    o.phi = walloc<double>(*W, N);
-    o.phis = walloc<double>(*W, N);
-    o.phil = walloc<double>(*W, N);
-    o.e = walloc<double>(*W, N);
-    o.partial = walloc<double>(*W, size_t(reduce_blocks(n)));
-    o.energy = walloc<double>(*W, 1);
-    ck(W->backup.alloc(sizeof(double) * 6 * N), "cudaMalloc backup");
-    ck(W->staging.alloc(sizeof(double) * 3 * N), "cudaMalloc staging");
-    ck(cudaMalloc(&W->err, sizeof(ErrRec)), "cudaMalloc err");
-    ck(cudaMallocHost(&W->err_host, sizeof(ErrRec)), "cudaMallocHost err");
-    // wupload's pageable cudaMemcpy may return before its DMA lands, and the
-    // field's streams are non-blocking (not ordered after the legacy stream)
-    ck(cudaDeviceSynchronize(), "sync uploads");
-    return W;
+    return true;
 }
 
 Error ensure_workspace(msmb_field* f, int64_t n, const double* box) {
@@ -414,6 +431,15 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, 
     if (g_exp_stamps) launch_stamp(st, 0);
     run("bin", [&] { return launch_bin(st, g, s, W.a, W.c, W.err); });
     run("sort", [&] { return launch_sort(st, g, s, W.a, W.c, W.err); });
+    if (g.kind != MSMB_FIELD_MSM) { // pair-only field: no grid hierarchy
+        run("clusters", [&] { return launch_clusters(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, rebuild ? 1 : 0); });
+        run("pairs", [&] { return launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole); });
+        DevOut o = W.o;
+        if (!outputs) o.phi = o.phis = o.phil = o.e = nullptr;
+        run("interp", [&] { return launch_pair_out(st, g, s.n, W.a, W.c, o, W.err, outputs ? 1 : 0, W.whole); });
+        run("finalize", [&] { return launch_finalize(st, s, W.err, 1); });
+        return total;
+    }
     if (fork) {
         ck(cudaEventRecord(f->fork_ev, st), "fork");
         ck(cudaStreamWaitEvent(lr, f->fork_ev, 0), "fork");
@@ -733,6 +759,8 @@ int msmb_device_count(void) {
     return n;
 }
 
+static int field_new(int device, msmb_field** out);
+
 int msmb_create(const msmb_msm_config* cfg, const msmb_units* units, int device, msmb_field** out) {
     *out = nullptr;
     Error e = validate_config(*cfg);
@@ -741,6 +769,35 @@ int msmb_create(const msmb_msm_config* cfg, const msmb_units* units, int device,
         g_create_error = e;
         return e.kind;
     }
+    const int rc = field_new(device, out);
+    if (rc) return rc;
+    (*out)->cfg = *cfg;
+    (*out)->units = *units;
+    return MSMB_OK;
+}
+
+int msmb_create_cutoff(int kind, const msmb_cutoff_params* params, const msmb_units* units, int device,
+                       msmb_field** out) {
+    *out = nullptr;
+    Error e = validate_cutoff(kind, *params);
+    if (!e.kind) e = validate_units(*units);
+    if (e.kind) {
+        g_create_error = e;
+        return e.kind;
+    }
+    const int rc = field_new(device, out);
+    if (rc) return rc;
+    msmb_field* f = *out;
+    f->kind = kind;
+    f->cut = *params;
+    f->units = *units;
+    f->cfg = msmb_msm_config{params->cutoff, params->cutoff / 4.0, 1, 3, 2}; // binning only
+    return MSMB_OK;
+}
+
+int msmb_field_kind(const msmb_field* f) { return f ? f->kind : -1; }
+
+static int field_new(int device, msmb_field** out) {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0 || device < 0 || device >= ndev) {
         g_create_error = Error{MSMB_ERR_CUDA, -1, -1, -1, "no usable CUDA device (this library has no CPU fallback)"};
@@ -754,8 +811,6 @@ int msmb_create(const msmb_msm_config* cfg, const msmb_units* units, int device,
         return MSMB_ERR_CUDA;
     }
     auto* f = new msmb_field();
-    f->cfg = *cfg;
-    f->units = *units;
     f->device = device;
     cudaSetDevice(device);
     int prio_lo = 0, prio_hi = 0;
@@ -830,6 +885,11 @@ int msmb_last_error(const msmb_field* f, int* kind, int64_t* idx_i, int64_t* idx
 }
 
 double msmb_cost_flops_per_step(const msmb_field* f, int64_t n) {
+    if (f->kind != MSMB_FIELD_MSM) { // force_field.cpp:25-35
+        const double fpp = f->cut.flops_per_particle > 0.0 ? f->cut.flops_per_particle
+                                                           : (f->kind == MSMB_FIELD_WOLF ? 350.0 : 301.0);
+        return fpp * double(n);
+    }
     return host_flops_simplified(f->cfg.cutoff_a, f->cfg.spacing_h, double(n));
 }
 
@@ -1183,8 +1243,13 @@ int msmb_grid_geometry(const msmb_msm_config* cfg, const double box[3], int* dim
     return MSMB_OK;
 }
 
+static int msm_only(msmb_field* f) {
+    return engine_set_error(f, Error{MSMB_ERR_CONFIG, -1, -1, -1, "this entry point needs an MSM field"});
+}
+
 int msmb_debug_levels(msmb_field* f, double* level_charge, double* level_potential) {
     std::lock_guard<std::recursive_mutex> lk(f->mu);
+    if (f->kind != MSMB_FIELD_MSM) return msm_only(f);
     GUARD_BEGIN
     if (!f->ws) return MSMB_ERR_INTERNAL;
     cudaSetDevice(f->device);
@@ -1221,6 +1286,7 @@ int msmb_debug_cells(msmb_field* f, int64_t n, const double* pos_xyz, const doub
 int msmb_debug_stage(msmb_field* f, int stage, int k, const double box[3], const double* in,
                      double* out, int64_t n, const double* pos_xyz) {
     std::lock_guard<std::recursive_mutex> lk(f->mu);
+    if (f->kind != MSMB_FIELD_MSM) return msm_only(f);
     GUARD_BEGIN
     cudaSetDevice(f->device);
     Error e = ensure_workspace(f, n, box);

@@ -114,6 +114,8 @@ struct StageTimer {
 } // namespace msmb
 
 struct msmb_field {
+    int kind = MSMB_FIELD_MSM;       // msmb_field_kind
+    msmb_cutoff_params cut{};        // pair-only fields (msmb_create_cutoff)
     msmb_msm_config cfg{};
     msmb_units units{};
     int device = 0;

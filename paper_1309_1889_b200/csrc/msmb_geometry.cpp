@@ -163,6 +163,8 @@ static void build_top_table(const Geometry& g, ConvTable& t) {
     finish_rows(t);
 }
 
+static void set_pair_layout(Geometry& g, const msmb_msm_config& c, const double box[3], int64_t n);
+
 Error build_geometry(const msmb_msm_config& c, const msmb_units& u, const double box[3],
                      int64_t n, Geometry& g) {
     Error e = validate_config(c);
@@ -270,7 +272,13 @@ Error build_geometry(const msmb_msm_config& c, const msmb_units& u, const double
     build_top_table(g, g.top);
     g.top_taps = int64_t(g.lv[g.levels - 1].size) * int64_t(g.lv[g.levels - 1].size);
 
-    // pair-search columns over level-0 cells
+    set_pair_layout(g, c, box, n);
+    return Error{};
+}
+
+// Pair-search columns over level-0 cells, screening margin,
+// pair-list skin and the initial list capacity.
+static void set_pair_layout(Geometry& g, const msmb_msm_config& c, const double box[3], int64_t n) {
     const LevelGeom& L0 = g.lv[0];
     const double vol = box[0] * box[1] * box[2];
     const double rho = std::max(1e-6, double(std::max<int64_t>(n, 1)) / vol);
@@ -302,6 +310,58 @@ Error build_geometry(const msmb_msm_config& c, const msmb_units& u, const double
         cap = std::min(cap, 1.0e6);
         g.pair_cap = std::max(64, int(cap));
     }
+}
+
+Error validate_cutoff(int kind, const msmb_cutoff_params& p) { // src/electrostatics.cpp:38-42
+    if (kind != MSMB_FIELD_CUTOFF && kind != MSMB_FIELD_WOLF)
+        return err(MSMB_ERR_CONFIG, "unknown pair field kind " + std::to_string(kind));
+    if (!(p.cutoff > 0.0)) return err(MSMB_ERR_CONFIG, "cutoff must be > 0");
+    if (kind == MSMB_FIELD_WOLF && !p.has_wolf_alpha) return err(MSMB_ERR_CONFIG, "wolf_alpha is required");
+    if (p.has_wolf_alpha && !(p.wolf_alpha >= 0.0)) return err(MSMB_ERR_CONFIG, "wolf_alpha must be >= 0");
+    return Error{};
+}
+
+// Pair-only fields: one "level" that only lays out the binning cells (the MSM
+// level-0 layout: origin -2s, dims ceil(L/s) + 5, cells 1 .. dims-3 used), with the
+// cell size s = max(a/4, (V/n)^(1/3)) so the cell count stays O(n); no hierarchy.
+Error build_pair_geometry(int kind, const msmb_cutoff_params& p, const msmb_units& u,
+                          const double box[3], int64_t n, Geometry& g) {
+    Error e = validate_cutoff(kind, p);
+    if (e.kind) return e;
+    e = validate_units(u);
+    if (e.kind) return e;
+    if (!(box[0] > 0.0 && box[1] > 0.0 && box[2] > 0.0) || !std::isfinite(box[0] * box[1] * box[2]))
+        return err(MSMB_ERR_CONFIG, "pair field: box extents must be positive and finite (binning extent)");
+    const double vol = box[0] * box[1] * box[2];
+    const double s = std::max(p.cutoff / 4.0, std::cbrt(vol / double(std::max<int64_t>(n, 1))));
+    msmb_msm_config c{p.cutoff, s, 1, 3, 2};
+    g = Geometry{};
+    g.kind = kind;
+    g.cfg = c;
+    g.units = u;
+    for (int ax = 0; ax < 3; ++ax) g.box[ax] = box[ax];
+    g.levels = 1;
+    LevelGeom& L0 = g.lv[0];
+    L0.spacing = s;
+    for (int ax = 0; ax < 3; ++ax) {
+        L0.origin[ax] = -2.0 * s;
+        L0.dims[ax] = int(std::ceil(box[ax] / s)) + 5;
+    }
+    L0.size = size_t(L0.dims[0]) * L0.dims[1] * L0.dims[2];
+    g.lattice_total = L0.size;
+    g.inv_h0 = 1.0 / s;
+    PairFieldP& pf = g.pf;
+    pf.kind = kind;
+    if (kind == MSMB_FIELD_WOLF) { // src/electrostatics.cpp:91-102, same operations
+        const double a = p.cutoff, alpha = p.wolf_alpha;
+        const double two_over_sqrt_pi = 1.1283791670955126;
+        const double erfc_aa = std::erfc(alpha * a);
+        pf.alpha = alpha;
+        pf.e_shift = erfc_aa / a;
+        pf.f_shift = erfc_aa / (a * a) + two_over_sqrt_pi * alpha * std::exp(-alpha * alpha * a * a) / a;
+        pf.self_per_charge = -(pf.e_shift + two_over_sqrt_pi * alpha);
+    }
+    set_pair_layout(g, c, box, n);
     return Error{};
 }
 

@@ -37,7 +37,7 @@ struct ErrRec {
     long long cov_min;           // min out-of-coverage particle index
     long long err_i, err_j;      // indices reported with `kind`
     int cur_step;                // step counter, advanced by the Verlet kernels
-    int pad;
+    int nan_count;               // cutoff/Wolf fields: particles with a NaN coordinate
     unsigned long long pairs;     // in-cutoff ordered pairs (stats, current evaluation)
     unsigned long long candidates;// screened candidate pairs (stats)
 };
@@ -90,7 +90,18 @@ struct LatticeTable {
     std::vector<double> taps;  // [nrows * TW]
 };
 
+// Pair-only fields (paramd::SimpleCutoffField / WolfField, force_field.hpp:34-60):
+// the MSM engine's binning, cluster pair list and pair kernel with another pair
+// function and no grid hierarchy.
+struct PairFieldP {
+    int kind = MSMB_FIELD_MSM;   // msmb_field_kind
+    double alpha = 0;            // Wolf damping
+    double e_shift = 0, f_shift = 0, self_per_charge = 0; // src/electrostatics.cpp:96-102
+};
+
 struct Geometry {
+    int kind = MSMB_FIELD_MSM;           // MSM, or a pair-only field (no hierarchy; binning clamps)
+    PairFieldP pf{};
     msmb_msm_config cfg{};
     msmb_units units{};
     double box[3] = {0, 0, 0};
@@ -136,6 +147,11 @@ Error validate_units(const msmb_units& u);
 // Builds the level hierarchy + all tables.  `n` sizes the pair-list estimate.
 Error build_geometry(const msmb_msm_config& c, const msmb_units& u, const double box[3],
                      int64_t n, Geometry& g);
+// Pair-only fields: CutoffParams::validate (src/electrostatics.cpp:38-42) and the
+// binning geometry (cells of the level-0 layout over the box; atoms outside clamp).
+Error validate_cutoff(int kind, const msmb_cutoff_params& p);
+Error build_pair_geometry(int kind, const msmb_cutoff_params& p, const msmb_units& u,
+                          const double box[3], int64_t n, Geometry& g);
 // Reference kernel math on the host (bitwise the reference's, non-FMA).
 double host_gamma(double rho);
 double host_g_level(double r, double a, int k, int l);

@@ -85,6 +85,7 @@ struct BinP {
     double inv_h;
     int d[3];
     int cw, ncx, ncy;
+    int clamp;      // pair-only fields: no coverage, cells clamped to 1 .. d-3
 };
 
 static float float_ru(double x) { // host: smallest float >= x
@@ -103,6 +104,7 @@ static BinP make_binp(const Geometry& g) {
     p.cw = g.cw;
     p.ncx = g.ncx;
     p.ncy = g.ncy;
+    p.clamp = g.kind != MSMB_FIELD_MSM;
     return p;
 }
 
@@ -122,6 +124,29 @@ __global__ void k_bin(int n, const double* __restrict__ x, const double* __restr
     const double px[3] = {x[i], y[i], z[i]};
     int c[3];
     bool ok = true;
+    if (p.clamp) { // pair-only fields: any position is valid; the cell is clamped
+        bool nan = false, inf = false;
+        for (int ax = 0; ax < 3; ++ax) {
+            const double t = __dmul_rn(__dsub_rn(px[ax], p.o[ax]), p.inv_h);
+            nan |= isnan(px[ax]);
+            inf |= isinf(px[ax]);
+            const double f = fmin(fmax(floor(t), 1.0), double(p.d[ax]) - 3.0); // NaN -> 1
+            c[ax] = int(f);
+        }
+        if (inf && !nan) { // rejected (msmb.h): excluded from the cells, reported as DomainError
+            key[i] = -1;
+            atomicMin(&err->cov_min, (long long)i);
+            const int slot = atomicAdd(&err->cov_count, 1);
+            outlist[slot] = i;
+            return;
+        }
+        if (nan) atomicAdd(&err->nan_count, 1);
+        if (nan) c[0] = c[1] = c[2] = 1;
+        const int sc = scell_of(p, c[0], c[1], c[2]);
+        key[i] = sc;
+        rank[i] = atomicAdd(&count[sc], 1);
+        return;
+    }
     for (int ax = 0; ax < 3; ++ax) {
         // t = (r - origin) * inv_h; base = floor(t) - 1 (src/msm_phases.cpp:23,42-50)
         const double t = __dmul_rn(__dsub_rn(px[ax], p.o[ax]), p.inv_h);
@@ -316,7 +341,7 @@ int launch_sort(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms&
     // always: also publishes the (possibly empty) natural-order cell ranges read by k_anterp
     k_cellsort<<<int((g.ncells + 255) / 256), 256, 0, st>>>(g.ncells, make_binp(g), c.start, a.perm,
                                                             c.nat, s.x, s.y, s.z, err);
-    if (n == 0) return l + 1;
+    if (n == 0 || g.kind != MSMB_FIELD_MSM) return l + 1;
     k_gather<<<(n + 255) / 256, 256, 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, s.q,
                                               make_binp(g), a.aw,
                                               err);
@@ -446,6 +471,9 @@ struct ListP {
     float cut, cut2;
     double oz, h;    // level-0 origin z, spacing: z-layer window of a column
     int d2, cw;      // z-layers, level-0 cells per column side
+    // pair-only fields (clamped binning): atoms outside the box sit in the boundary
+    // cells, so the boundary columns / layers extend to infinity
+    int clamp, cxmin, cxmax, cymin, cymax, czmin, czmax;
 };
 
 __device__ __forceinline__ float gapf(float alo, float ahi, float blo, float bhi) {
@@ -477,18 +505,24 @@ __global__ void __launch_bounds__(256)
     int cx1 = int(floor((double(hi.x) + cutd - p.ox) / p.colw)) + 1;
     int cy0 = int(floor((double(lo.y) - cutd - p.oy) / p.colw)) - 1;
     int cy1 = int(floor((double(hi.y) + cutd - p.oy) / p.colw)) + 1;
-    cx0 = max(cx0, 0);
-    cy0 = max(cy0, 0);
-    cx1 = min(cx1, p.ncx - 1);
-    cy1 = min(cy1, p.ncy - 1);
-    const int cxi = min(max(int(floor((0.5 * (double(lo.x) + double(hi.x)) - p.ox) / p.colw)), 0), p.ncx - 1);
-    const int cyi = min(max(int(floor((0.5 * (double(lo.y) + double(hi.y)) - p.oy) / p.colw)), 0), p.ncy - 1);
+    const int xmn = p.clamp ? p.cxmin : 0, xmx = p.clamp ? p.cxmax : p.ncx - 1;
+    const int ymn = p.clamp ? p.cymin : 0, ymx = p.clamp ? p.cymax : p.ncy - 1;
+    cx0 = min(max(cx0, xmn), xmx);
+    cy0 = min(max(cy0, ymn), ymx);
+    cx1 = max(min(cx1, xmx), xmn);
+    cy1 = max(min(cy1, ymx), ymn);
+    const int cxi = min(max(int(floor((0.5 * (double(lo.x) + double(hi.x)) - p.ox) / p.colw)), xmn), xmx);
+    const int cyi = min(max(int(floor((0.5 * (double(lo.y) + double(hi.y)) - p.oy) / p.colw)), ymn), ymx);
     const int DX = max(cxi - cx0, cx1 - cxi), DY = max(cyi - cy0, cy1 - cyi);
     // z-layers that can hold atoms within the cut (one extra layer each side):
     // within a column the sorted atoms are ordered by z-layer, so the window is
     // one atom range per column, i.e. one contiguous range of its clusters
-    const int czA = max(0, int(floor((double(lo.z) - cutd - p.oz) / p.h)) - 1);
-    const int czB = min(p.d2 - 1, int(floor((double(hi.z) + cutd - p.oz) / p.h)) + 1);
+    int czA = max(0, int(floor((double(lo.z) - cutd - p.oz) / p.h)) - 1);
+    int czB = min(p.d2 - 1, int(floor((double(hi.z) + cutd - p.oz) / p.h)) + 1);
+    if (p.clamp) {
+        czA = min(max(czA, p.czmin), p.czmax);
+        czB = min(max(czB, p.czmin), p.czmax);
+    }
     const int lay = p.cw * p.cw;
     const int64_t cpc = int64_t(p.d2) * lay;
     const float oxf = float(p.ox), oyf = float(p.oy), colwf = float(p.colw);
@@ -508,8 +542,14 @@ __global__ void __launch_bounds__(256)
                 int emitted = 0;
                 if (cx >= cx0 && cx <= cx1 && cy >= cy0 && cy <= cy1) {
                     // column bounds in fp32 (error ~1e-5 A, inside the 1e-3 A margin)
-                    const float xlo = fmaf(float(cx), colwf, oxf) - 1e-3f, xhi = fmaf(float(cx + 1), colwf, oxf) + 1e-3f;
-                    const float ylo = fmaf(float(cy), colwf, oyf) - 1e-3f, yhi = fmaf(float(cy + 1), colwf, oyf) + 1e-3f;
+                    float xlo = fmaf(float(cx), colwf, oxf) - 1e-3f, xhi = fmaf(float(cx + 1), colwf, oxf) + 1e-3f;
+                    float ylo = fmaf(float(cy), colwf, oyf) - 1e-3f, yhi = fmaf(float(cy + 1), colwf, oyf) + 1e-3f;
+                    if (p.clamp) {
+                        if (cx <= p.cxmin) xlo = -3e38f;
+                        if (cx >= p.cxmax) xhi = 3e38f;
+                        if (cy <= p.cymin) ylo = -3e38f;
+                        if (cy >= p.cymax) yhi = 3e38f;
+                    }
                     const float gx = gapf(lo.x, hi.x, xlo, xhi), gy = gapf(lo.y, hi.y, ylo, yhi);
                     if (gx * gx + gy * gy < p.cut2) {
                         const int col = cx * p.ncy + cy;
@@ -576,6 +616,8 @@ struct PairP {
     double c0, c1, c2;   // gamma(r/a)/a = c0 + r2*(c1 + r2*c2)
     double d0, d1;       // g*'(r)/r + 1/r^3 = d0 + r2*d1
     double kc;
+    // Wolf / damped-shifted-force pair term (src/electrostatics.cpp:91-120)
+    double alpha, alpha2, gcoef, e_shift, f_shift, a;
 };
 
 #ifndef MSMB_RSQRT_NEWTON
@@ -596,6 +638,31 @@ __device__ __forceinline__ double rsqrt_pos(double x) {
 #else
     return fma(y * e, fma(e, 0.375, 0.5), y);
 #endif
+}
+
+// Pair function of the field kind K for 0 < r2 (r2 < a2 is applied by the caller):
+// g = the pair potential per unit source charge, sd = (dV/dr)/r, so that
+// phi_i += q_j g and F_i += d * (-k_C q_i q_j sd).
+//  MSM:    g* = 1/r - gamma(r/a)/a, sd = g*'(r)/r        (msm_kernels.hpp:30-42)
+//  cutoff: g = 1/r, sd = -1/r^3                           (electrostatics.cpp:81-86)
+//  Wolf:   g = erfc(ar)/r - e_shift + f_shift (r - a),
+//          sd = -(erfc(ar)/r^2 + gauss/r - f_shift)/r     (electrostatics.cpp:111-118)
+template <int K>
+__device__ __forceinline__ void pair_fn(const PairP& p, double r2, double rinv, double& g, double& sd) {
+    const double rinv2 = rinv * rinv;
+    if constexpr (K == MSMB_FIELD_MSM) {
+        g = rinv - fma(r2, fma(r2, p.c2, p.c1), p.c0);
+        sd = fma(-rinv, rinv2, fma(r2, p.d1, p.d0));
+    } else if constexpr (K == MSMB_FIELD_CUTOFF) {
+        g = rinv;
+        sd = -rinv * rinv2;
+    } else {
+        const double r = r2 * rinv;
+        const double er = erfc(p.alpha * r);
+        const double gs = p.gcoef * exp(-p.alpha2 * r2);
+        g = fma(p.f_shift, r - p.a, fma(er, rinv, -p.e_shift));
+        sd = -fma(er, rinv2, fma(gs, rinv, -p.f_shift)) * rinv;
+    }
 }
 
 __device__ __forceinline__ void record_pair(ErrRec* err, int i, int j) {
@@ -785,6 +852,7 @@ __global__ void __launch_bounds__(kMaskWarps * 32)
 // lane preferring a mask bit whose row sits in bank quad (lane & 7) (conflict-free
 // when found, measured in a microbenchmark) 0.68: only 17% of steps find one --
 // a lane's mask holds ~1-2 atoms of a cluster -- and bank conflicts did not drop.
+template <int K>
 __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     k_pairs_mw(const int2* __restrict__ clu, const int* __restrict__ plist, const int* __restrict__ pcnt,
                const unsigned* __restrict__ pmask, int cap, const double* __restrict__ xs,
@@ -796,7 +864,6 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ic = col_off[col_a] + blockIdx.x * kPairWarps + w;
     if (ic >= col_off[col_b] || failed(err)) return;
-    const double c0 = p.c0, c1 = p.c1, c2 = p.c2, d0 = p.d0, d1 = p.d1;
     const int2 c = clu[ic];
     const bool vi = lane < c.y;
     const int si = c.x + (vi ? lane : 0);
@@ -852,9 +919,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         const double dx = xi - xy.x, dy = yi - xy.y, dz = zi - zq.x;
         const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
         const double rinv = rsqrt_pos(r2);
-        const double rinv2 = rinv * rinv;
-        const double g = rinv - fma(r2, fma(r2, c2, c1), c0);   // g*(r)
-        const double sd = fma(-rinv, rinv2, fma(r2, d1, d0));  // g*'(r)/r
+        double g, sd;
+        pair_fn<K>(p, r2, rinv, g, sd);
         const bool in = r2 < a2;
         npair += in ? 1u : 0u;
         const double qj = in ? zq.y : 0.0; // two FSELs (a predicated accumulation costs 8)
@@ -874,9 +940,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
         const bool in = r2 < a2 && t != lane;
         const double rinv = rsqrt_pos(in ? r2 : a2);
-        const double rinv2 = rinv * rinv;
-        const double g = rinv - fma(r2, fma(r2, c2, c1), c0);
-        const double sd = fma(-rinv, rinv2, fma(r2, d1, d0));
+        double g, sd;
+        pair_fn<K>(p, in ? r2 : a2, rinv, g, sd);
         npair += in ? 1u : 0u;
         const double qj = in ? qt : 0.0;
         ph = fma(qj, g, ph);
@@ -975,6 +1040,13 @@ int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevStat
     lp.h = g.lv[0].spacing;
     lp.d2 = g.lv[0].dims[2];
     lp.cw = g.cw;
+    lp.clamp = g.kind != MSMB_FIELD_MSM; // occupied cells are 1 .. d-3 per axis (k_bin)
+    lp.cxmin = 1 / g.cw;
+    lp.cxmax = (g.lv[0].dims[0] - 3) / g.cw;
+    lp.cymin = 1 / g.cw;
+    lp.cymax = (g.lv[0].dims[1] - 3) / g.cw;
+    lp.czmin = 1;
+    lp.czmax = g.lv[0].dims[2] - 3;
     k_pairlist<<<int((maxclu * 32 + 255) / 256), 256, 0, st>>>(c.nclu, c.blo, c.bhi, c.col_off, c.start, lp,
                                                                 c.plist, c.pcnt, cap, P.cx0 * g.ncy,
                                                                 P.cx1 * g.ncy, c.flag, err);
@@ -1000,10 +1072,19 @@ int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& 
     p.d0 = 2.5 / (A * A * A);
     p.d1 = -1.5 / (A * A * A * A * A);
     p.kc = g.units.coulomb_constant;
+    p.alpha = g.pf.alpha;
+    p.alpha2 = g.pf.alpha * g.pf.alpha;
+    p.gcoef = 1.1283791670955126 * g.pf.alpha; // 2/sqrt(pi) alpha (src/electrostatics.cpp:12,112)
+    p.e_shift = g.pf.e_shift;
+    p.f_shift = g.pf.f_shift;
+    p.a = A;
     const int64_t maxclu = n / 32 + g.ncols + 1;
     int l = 0;
     if (n > 0) {
-        k_pairs_mw<<<int((maxclu + kPairWarps - 1) / kPairWarps), kPairWarps * 32, 0, st>>>(
+        auto kern = g.kind == MSMB_FIELD_CUTOFF ? k_pairs_mw<MSMB_FIELD_CUTOFF>
+                    : g.kind == MSMB_FIELD_WOLF ? k_pairs_mw<MSMB_FIELD_WOLF>
+                                                : k_pairs_mw<MSMB_FIELD_MSM>;
+        kern<<<int((maxclu + kPairWarps - 1) / kPairWarps), kPairWarps * 32, 0, st>>>(
             c.clu, c.plist, c.pcnt, c.pmask, cap, a.xc, a.yc, a.zc, a.qc, p, A * A, a.phis, a.fsx, a.fsy, a.fsz,
             c.col_off, P.cx0 * g.ncy, P.cx1 * g.ncy, n, err);
         l = 1;
@@ -2261,10 +2342,52 @@ int launch_interp(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, De
     return 3;
 }
 
+// Pair-only fields (simple_cutoff / wolf_summation, src/electrostatics.cpp:66-132):
+// per-atom outputs in original order from the pair sums; the Wolf self term
+// q_i * self_per_charge is added after the pair sum (electrostatics.cpp:123-124);
+// e_i = 0.5 q_i phi_i for the index-order energy (finish_total, :27-33).  A NaN
+// coordinate (nan_count > 0, n >= 2) makes every pair of that particle NaN in the
+// reference, hence every output NaN.
+__global__ void k_pair_out(const int* __restrict__ colstart, int col_a, int col_b, const int* __restrict__ perm,
+                           const double* __restrict__ qs, const double* __restrict__ phis,
+                           const double* __restrict__ fsx, const double* __restrict__ fsy,
+                           const double* __restrict__ fsz, double self_per_charge, int wolf, int64_t n,
+                           DevOut o, const ErrRec* err) {
+    const int s = colstart[col_a] + blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= colstart[col_b] || failed(err)) return;
+    const int i = perm[s];
+    const bool poison = n >= 2 && __ldcg(&err->nan_count) > 0;
+    const double nanv = __longlong_as_double(0x7ff8000000000000ll);
+    const double q = qs[s];
+    double ph = phis[s];
+    if (wolf) ph = __dadd_rn(ph, __dmul_rn(q, self_per_charge));
+    if (poison) ph = nanv;
+    o.fx[i] = poison ? nanv : fsx[s];
+    o.fy[i] = poison ? nanv : fsy[s];
+    o.fz[i] = poison ? nanv : fsz[s];
+    if (o.phi) o.phi[i] = ph;
+    if (o.phis) o.phis[i] = ph;
+    if (o.phil) o.phil[i] = 0.0;
+    if (o.e) o.e[i] = __dmul_rn(__dmul_rn(0.5, q), ph);
+}
+
+int launch_pair_out(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c, DevOut& o,
+                    ErrRec* err, int want_energy, const Part& P) {
+    if (n == 0) return 0;
+    k_pair_out<<<int((n + 127) / 128), 128, 0, st>>>(c.colstart, P.cx0 * g.ncy, P.cx1 * g.ncy, a.cl_perm, a.qc,
+                                                     a.phis, a.fsx, a.fsy, a.fsz, g.pf.self_per_charge,
+                                                     g.kind == MSMB_FIELD_WOLF ? 1 : 0, n, o, err);
+    if (!want_energy) return 1;
+    const int nb = reduce_blocks(n);
+    k_energy1<<<nb, 256, 0, st>>>(n, o.e, o.partial, err);
+    k_energy2<<<1, 256, 0, st>>>(nb, o.partial, g.units.coulomb_constant, o.energy, err);
+    return 3;
+}
+
 // Decide the evaluation's outcome with the reference's precedence:
 // short_range errors (first pair in i<j order) > coverage (min particle).
 __global__ void k_finalize(const double* __restrict__ x, const double* __restrict__ y,
-                           const double* __restrict__ z, ErrRec* err) {
+                           const double* __restrict__ z, int pair_field, ErrRec* err) {
     if (err->kind) return;
     if (err->overflow) {
         err->kind = kOverflowKind;
@@ -2281,16 +2404,16 @@ __global__ void k_finalize(const double* __restrict__ x, const double* __restric
         err->step = err->cur_step;
         return;
     }
-    if (err->cov_count > 0) {
-        err->kind = MSMB_ERR_COVERAGE;
+    if (err->cov_count > 0) { // pair-only fields: infinite coordinates (msmb.h)
+        err->kind = pair_field ? MSMB_ERR_DOMAIN : MSMB_ERR_COVERAGE;
         err->err_i = err->cov_min;
         err->err_j = -1;
         err->step = err->cur_step;
     }
 }
 
-int launch_finalize(cudaStream_t st, const DevState& s, ErrRec* err) {
-    k_finalize<<<1, 1, 0, st>>>(s.x, s.y, s.z, err);
+int launch_finalize(cudaStream_t st, const DevState& s, ErrRec* err, int pair_field) {
+    k_finalize<<<1, 1, 0, st>>>(s.x, s.y, s.z, pair_field, err);
     return 1;
 }
 
@@ -2304,6 +2427,7 @@ __global__ void k_reset_err(ErrRec* err, int step) {
     err->err_i = -1;
     err->err_j = -1;
     err->cur_step = step;
+    err->nan_count = 0;
     err->pairs = 0;
     err->candidates = 0;
 }

@@ -156,7 +156,10 @@ int launch_verlet_part(cudaStream_t st, const Geometry& g, const DevCells& c, co
 int launch_export_state(cudaStream_t st, const Geometry& g, const DevCells& c, const DevAtoms& a,
                         const DevState& s, long long* xbuf, const Part& P);
 int launch_fill_i64(cudaStream_t st, long long* p, int64_t count, long long v);
-int launch_finalize(cudaStream_t st, const DevState& s, ErrRec* err);
+int launch_finalize(cudaStream_t st, const DevState& s, ErrRec* err, int pair_field = 0);
+// pair-only fields: per-atom outputs and energy from the pair sums (no grid)
+int launch_pair_out(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c, DevOut& o,
+                    ErrRec* err, int want_energy, const Part& P);
 int launch_kick_drift(cudaStream_t st, DevState& s, const DevOut& o, double dt, double conv,
                       int kicks, ErrRec* err);
 int launch_kick(cudaStream_t st, DevState& s, const DevOut& o, double dt, double conv,

@@ -46,7 +46,21 @@ _SIGS = {
                         f64, f64, i32, i32, i32, _D, _D, _D, _L, _S, i32],
     "parareal_run": [i64, _D, _D, _D, _D, _D, f64, f64, i32, f64, i32, f64, f64, i32, f64, i32,
                      f64, f64, i32, i32, f64, i32, f64, i32, i32, _D, _D, _L, _S, i32],
+    # any ForceField, described by fspec() below
+    "field_evaluate": [_D, i64, _D, _D, _D, f64, f64, _D, _D, _D, _S, i32],
+    "field_parareal_window": [i64, _D, _D, _D, _D, _D, _D, f64, i32, _D, f64, i32, f64, f64, i32, i32,
+                              _D, _D, _D, _L, _S, i32],
 }
+
+
+def fspec(kind: str, a: float, h: float = 0.0, levels: int = 0, alpha=None, rep_eps: float = 0.0,
+          rep_sigma: float = 1.0) -> np.ndarray:
+    """Field description shared by ref_field_* / orc_field_*: kind 'msm' | 'cutoff' | 'wolf' |
+    'direct'; a = MsmConfig::cutoff_a or CutoffParams::cutoff; rep_eps > 0 wraps the field in
+    PairRepulsionOverlay(rep_eps, rep_sigma)."""
+    k = {"msm": 0, "cutoff": 1, "wolf": 2, "direct": 3}[kind]
+    return np.array([k, a, h, levels, 0.0 if alpha is None else 1.0, alpha or 0.0, rep_eps, rep_sigma],
+                    dtype=np.float64)
 
 
 class OracleError(RuntimeError):
@@ -103,6 +117,11 @@ class Checker:
             pt = self.lib.ref_propagate_trace
             pt.argtypes = [i64, _D, _D, _D, _D, _D, f64, f64, i32, f64, f64, f64, i32, _I, _S, i32]
             pt.restype = C.c_int
+            fp = self.lib.ref_field_propagate_trace
+            fp.argtypes = [_D, i64, _D, _D, _D, _D, _D, f64, f64, f64, i32, _I, _S, i32]
+            fp.restype = C.c_int
+            self.lib.ref_field_cost.argtypes = [_D, f64, f64, i64]
+            self.lib.ref_field_cost.restype = f64
             dc = self.lib.ref_direct_coulomb
             dc.argtypes = [i64, _D, _D, f64, _D, _D, _D, _S, i32]
             dc.restype = C.c_int
@@ -114,6 +133,9 @@ class Checker:
             pp.argtypes = [i64, _D, _D, _D, _D, _D, f64, f64, i32, f64, f64, f64, i32, _I, _S, i32]
             pp.restype = C.c_int
             self.lib.orc_num_threads.restype = C.c_int
+            fp = self.lib.orc_field_propagate
+            fp.argtypes = [_D, i64, _D, _D, _D, _D, _D, f64, f64, f64, i32, _I, _S, i32]
+            fp.restype = C.c_int
 
     # -------------------------------------------------------------- helpers
     @staticmethod
@@ -260,6 +282,47 @@ class Checker:
                                     buf, 512)
         err = None if rc == 0 else OracleError(rc, buf.value.decode())
         return tp, tv, cnt, err
+
+
+    # ---------------------------------------------------------- any ForceField
+    def field_evaluate(self, spec, pos, q, box, kc=332.0636, conv=4.184e-4):
+        pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        n = len(q)
+        phi, f, e = np.zeros(n), np.zeros((n, 3)), np.zeros(1)
+        self._call(self.f["field_evaluate"], _p(np.ascontiguousarray(spec, dtype=np.float64)), n, _p(pos), _p(q),
+                   _p(np.asarray(box, dtype=np.float64)), kc, conv, _p(phi), _p(f), _p(e))
+        return dict(phi=phi, force=f, energy=float(e[0]))
+
+    def field_propagate(self, spec, pos, vel, q, mass, box, dt, steps, kc=332.0636, conv=4.184e-4):
+        """Returns (pos, vel, steps_done, error-or-None)."""
+        pos = np.array(pos, dtype=np.float64, copy=True).reshape(-1, 3)
+        vel = np.array(vel, dtype=np.float64, copy=True).reshape(-1, 3)
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        mass = np.ascontiguousarray(mass, dtype=np.float64)
+        done = C.c_int(0)
+        buf = C.create_string_buffer(512)
+        fn = self.lib.ref_field_propagate_trace if self.kind == "ref" else self.lib.orc_field_propagate
+        rc = fn(_p(np.ascontiguousarray(spec, dtype=np.float64)), len(q), _p(pos), _p(vel), _p(q), _p(mass),
+                _p(np.asarray(box, dtype=np.float64)), kc, conv, dt, steps, C.byref(done), buf, 512)
+        err = None if rc == 0 else OracleError(rc, buf.value.decode())
+        return pos, vel, done.value, err
+
+    def field_parareal_window(self, pos, vel, q, mass, box, fine_spec, fdt, fsteps, coarse_spec, gdt, gsteps,
+                              t_points, k_iters, kc=332.0636, conv=4.184e-4):
+        pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)
+        vel = np.ascontiguousarray(vel, dtype=np.float64).reshape(-1, 3)
+        n = len(pos)
+        rp = np.zeros((t_points + 1, n, 3))
+        rv = np.zeros((t_points + 1, n, 3))
+        dr = np.zeros(t_points + 1)
+        cnt = np.zeros(3, dtype=np.int64)
+        self._call(self.f["field_parareal_window"], n, _p(pos), _p(vel), _p(np.ascontiguousarray(q, dtype=np.float64)),
+                   _p(np.ascontiguousarray(mass, dtype=np.float64)), _p(np.asarray(box, dtype=np.float64)),
+                   _p(np.ascontiguousarray(fine_spec, dtype=np.float64)), fdt, fsteps,
+                   _p(np.ascontiguousarray(coarse_spec, dtype=np.float64)), gdt, gsteps, kc, conv, t_points,
+                   k_iters, _p(rp), _p(rv), _p(dr), _pl(cnt))
+        return rp, rv, dr, cnt
 
 
 _cache: dict[str, Checker] = {}

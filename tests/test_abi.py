@@ -29,7 +29,7 @@ def test_header_symbols_all_exported():
 
 
 def test_abi_version():
-    assert _native.lib().msmb_abi_version() == 1
+    assert _native.lib().msmb_abi_version() == 2
 
 
 @pytest.mark.parametrize("box,a,h,l", [([40, 40, 40], 10, 2.5, 2), ([144, 144, 144], 12, 2.5, 6),
@@ -92,3 +92,29 @@ def test_cost_model_is_reference_formula(ref):
     for a, h, n in [(12, 2, 1e5), (10, 2.5, 8192)]:
         assert ref.lib.ref_msm_flops_simplified(a, h, n) == pytest.approx(
             77.7 * a ** 3 * n + 566 * n + 73 * a ** 3 / h ** 6 * n + 80 / h ** 3 * n, rel=1e-15)
+
+
+@pytest.mark.parametrize("cls,params,msg", [
+    (pkg.SimpleCutoffField, pkg.CutoffParams(0.0), "cutoff must be > 0"),
+    (pkg.SimpleCutoffField, pkg.CutoffParams(float("nan")), "cutoff must be > 0"),
+    (pkg.WolfField, pkg.CutoffParams(10.0), "wolf_alpha is required"),
+    (pkg.WolfField, pkg.CutoffParams(10.0, -0.1), "wolf_alpha must be >= 0"),
+    (pkg.SimpleCutoffField, pkg.CutoffParams(10.0, -0.1), "wolf_alpha must be >= 0"),
+])
+def test_pair_field_validation_messages(cls, params, msg):
+    # CutoffParams::validate (src/electrostatics.cpp:38-42), before any GPU work
+    with pytest.raises(pkg.ConfigError) as ei:
+        cls(params)
+    assert str(ei.value) == msg
+    with pytest.raises(pkg.ConfigError) as ei:
+        params.validate(cls is pkg.WolfField)
+    assert str(ei.value) == msg
+
+
+def test_pair_field_no_cpu_fallback_without_gpu():
+    if pkg.device_count() > 0:
+        pytest.skip("a GPU is present")
+    with pytest.raises(pkg.CudaUnavailableError):
+        pkg.SimpleCutoffField(pkg.CutoffParams(10.0))
+    with pytest.raises(pkg.CudaUnavailableError):
+        pkg.WolfField(pkg.CutoffParams(10.0, 0.2))

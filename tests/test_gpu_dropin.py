@@ -28,3 +28,7 @@ def test_reference_drives_gpu_field():
     assert r["coincident_ref"] and r["coincident_ref"] == r["coincident_gpu"]
     assert r["coverage_ref"] and r["coverage_ref"] == r["coverage_gpu"]
     assert r["name"] == "msm" and r["cost"] == r["cost_ref"]
+    # pair-only fields through the same plugin boundary
+    assert r["pf_de"] <= 1e-10 and r["pf_df"] <= 1e-8
+    assert r["pf_dx_plugin_propagate"] <= 1e-8 and r["pf_dx_device_propagate"] <= 1e-8
+    assert 0 <= r["pf_dx_parareal_device"] <= 1e-8

@@ -116,3 +116,51 @@ def test_port_parareal_run_vs_reference_live(port, ref):
     b = port.parareal_run(pos, vel, q, mass, box, fine, coarse, 3, 4, 1e-7, 7)
     assert (a[3] is None) == (b[3] is None)
     assert _eq(a[0], b[0]) and _eq(a[1], b[1]) and _eq(a[2], b[2])
+
+
+# ---- pair-only fields: the restatement is bitwise the reference
+def test_port_fields_bitwise_vs_reference_golden(port):
+    g = golden("fields")
+    for name, spec in zip(g["names"], g["specs"]):
+        r = port.field_evaluate(spec, g["pos"], g["q"], g["box"])
+        assert np.array_equal(r["phi"], g[f"{name}_phi"]), name
+        assert np.array_equal(r["force"], g[f"{name}_force"]), name
+        assert r["energy"] == float(g[f"{name}_energy"]), name
+
+
+def test_port_field_trajectory_vs_reference_golden(port):
+    g = golden("fields_traj10")
+    p2, v2, done, err = port.field_propagate(g["spec"], g["pos"], g["vel"], g["q"], g["mass"], g["box"],
+                                             float(g["dt"]), int(g["steps"]))
+    assert err is None and done == int(g["steps"])
+    assert np.array_equal(p2, g["out_pos"]) and np.array_equal(v2, g["out_vel"])
+
+
+def test_port_field_parareal_vs_reference_golden(port):
+    g = golden("fields_parareal_w4k2")
+    rp, rv, dr, cnt = port.field_parareal_window(g["pos"], g["vel"], g["q"], g["mass"], g["box"], g["fine"],
+                                                 float(g["fdt"]), int(g["fsteps"]), g["coarse"], float(g["gdt"]),
+                                                 int(g["gsteps"]), int(g["t_points"]), int(g["k_iters"]))
+    assert np.array_equal(rp, g["row_pos"]) and np.array_equal(rv, g["row_vel"])
+    assert np.array_equal(dr[1:], g["delta_rms"][1:]) and np.array_equal(cnt, g["counts"])
+
+
+@pytest.mark.parametrize("spec_args", [("cutoff", 9.0), ("wolf", 9.0, 0.0, 0, 0.3), ("direct", 0.0),
+                                       ("wolf", 6.0, 0.0, 0, 0.25, 0.5, 1.5)])
+def test_port_fields_bitwise_vs_reference_live(port, ref, spec_args):
+    import oracle_lib
+    spec = oracle_lib.fspec(*spec_args)
+    rng = np.random.default_rng(11)
+    n, L = 900, 22.0
+    pos = rng.uniform(-2.0, L + 2.0, (n, 3))  # also outside the box: the fields ignore it
+    q = rng.choice([-1.0, 0.5, 1.0], n)
+    box = np.array([L, L, L])
+    a = ref.field_evaluate(spec, pos, q, box)
+    b = port.field_evaluate(spec, pos, q, box)
+    assert np.array_equal(a["phi"], b["phi"]) and np.array_equal(a["force"], b["force"])
+    assert a["energy"] == b["energy"]
+    pos[17] = pos[5]
+    import oracle_lib as ol
+    for k in (ref, port):
+        with pytest.raises(ol.OracleError, match="particles 5 and 17 coincide"):
+            k.field_evaluate(spec, pos, q, box)
