@@ -96,7 +96,7 @@ void msmb_destroy(msmb_field* f);
  * when most atoms are inside).  A NaN coordinate makes every output NaN, as in the
  * reference (every pair with that particle is NaN); an infinite coordinate, for
  * which the reference mixes skipped and NaN pairs, is rejected with MSMB_ERR_DOMAIN. */
-enum msmb_field_kind { MSMB_FIELD_MSM = 0, MSMB_FIELD_CUTOFF = 1, MSMB_FIELD_WOLF = 2 };
+enum msmb_field_kind { MSMB_FIELD_MSM = 0, MSMB_FIELD_CUTOFF = 1, MSMB_FIELD_WOLF = 2, MSMB_FIELD_DIRECT = 3 };
 
 /* paramd::CutoffParams (include/paramd/potential.hpp:26-31: cutoff 12 A, optional
  * wolf_alpha), plus the fields' cost-model constant flops_per_particle
@@ -115,6 +115,21 @@ int msmb_create_cutoff(int kind, const msmb_cutoff_params* params, const msmb_un
                        int device, msmb_field** out);
 /* msmb_field_kind of a handle. */
 int msmb_field_kind(const msmb_field* f);
+
+/* ---- all-pairs fields ---------------------------------
+ * DirectCoulombField(units) (force_field.hpp:23-32; direct_coulomb,
+ * src/electrostatics.cpp:43-64): the exact O(N^2) Coulomb sum, the reference's
+ * accuracy oracle (tools/paramd_main.cpp:148-212), on the GPU.  No box is needed.
+ * Coincident particles raise MSMB_ERR_COINCIDENT with the reference's first pair. */
+int msmb_create_direct(const msmb_units* units, int device, msmb_field** out);
+
+/* PairRepulsionOverlay(base, epsilon, sigma)  force_field.hpp:75-97,
+ * force_field.cpp:45-68: a NEW handle evaluating `base`'s field (same kind,
+ * parameters and units; `base` itself is unchanged) plus the pair repulsion
+ * U = sum_{i<j} eps (sigma/r)^12 over ALL pairs (O(N^2), as the reference):
+ * forces and total energy include it, the per-particle potential stays
+ * electrostatic.  name() = base name + "+rep"; cost = base cost + 30 n. */
+int msmb_create_overlay(const msmb_field* base, double epsilon, double sigma, msmb_field** out);
 
 /* MsmField::evaluate / msm_potential(s, cfg, units)  force_field.cpp:37-39,
  * msm.cpp:52-90.  Host arrays; any output pointer may be NULL.
@@ -145,7 +160,8 @@ void msmb_host_free(void* p);
 
 /* MsmField::cost_flops_per_step = msm_flops_simplified(a, h, n)
  * force_field.cpp:41-43, cost_model.cpp:37-43; SimpleCutoffField / WolfField:
- * flops_per_particle * n (force_field.cpp:25-35). */
+ * flops_per_particle * n (force_field.cpp:25-35); DirectCoulombField 20 n^2
+ * (:17-19); an overlay adds 30 n (:70-72). */
 double msmb_cost_flops_per_step(const msmb_field* f, int64_t n);
 
 /* Details of the last failure on this handle: kind = msmb_status, i/j the

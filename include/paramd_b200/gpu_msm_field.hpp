@@ -152,6 +152,34 @@ class GpuWolfField final : public GpuFieldBase {
     std::string name() const override { return "wolf"; }
 };
 
+/// paramd::DirectCoulombField (force_field.hpp:23-32; direct_coulomb,
+/// src/electrostatics.cpp:43-64): the exact O(N^2) sum, all pairs on a B200.
+class GpuDirectCoulombField final : public GpuFieldBase {
+  public:
+    explicit GpuDirectCoulombField(UnitsConfig units, int device = 0) {
+        const msmb_units u = detail_b200::to_c(units);
+        const int rc = msmb_create_direct(&u, device, &h_);
+        if (rc) detail_b200::rethrow(nullptr, rc);
+    }
+    std::string name() const override { return "direct"; }
+};
+
+/// paramd::PairRepulsionOverlay (force_field.hpp:75-97; force_field.cpp:45-68) over a
+/// B200 base field: one GPU handle evaluating the base field plus the all-pairs
+/// repulsion (the base object itself is unchanged).
+class GpuPairRepulsionOverlay final : public GpuFieldBase {
+  public:
+    GpuPairRepulsionOverlay(std::shared_ptr<const GpuFieldBase> base, double epsilon = 0.1, double sigma = 1.0)
+        : base_(std::move(base)) {
+        const int rc = msmb_create_overlay(base_->handle(), epsilon, sigma, &h_);
+        if (rc) detail_b200::rethrow(nullptr, rc);
+    }
+    std::string name() const override { return base_->name() + "+rep"; }
+
+  private:
+    std::shared_ptr<const GpuFieldBase> base_;
+};
+
 }  // namespace paramd
 
 namespace paramd_b200 {

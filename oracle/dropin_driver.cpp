@@ -166,8 +166,23 @@ int main() {
         std::fprintf(stderr, "pair-field parareal: %s\n", e.what());
     }
 
+    // 7. all-pairs fields: DirectCoulombField and PairRepulsionOverlay(SimpleCutoffField)
+    auto ref_d = std::make_shared<DirectCoulombField>(units);
+    auto gpu_d = std::make_shared<GpuDirectCoulombField>(units);
+    auto ref_o = std::make_shared<PairRepulsionOverlay>(ref_c, 0.1, 2.0);
+    auto gpu_o = std::make_shared<GpuPairRepulsionOverlay>(gpu_c, 0.1, 2.0);
+    double ap_de = 0, ap_df = 0;
+    for (int k = 0; k < 2; ++k) {
+        const ForceField& r0 = k ? static_cast<const ForceField&>(*ref_o) : *ref_d;
+        const ForceField& g0 = k ? static_cast<const ForceField&>(*gpu_o) : *gpu_d;
+        PotentialResult x = r0.evaluate(s), y = g0.evaluate(s);
+        ap_de = std::max(ap_de, std::fabs(x.total_energy - y.total_energy) / std::fabs(x.total_energy));
+        ap_df = std::max(ap_df, rel_rms(y.per_particle_force, x.per_particle_force));
+        if (r0.name() != g0.name() || r0.cost_flops_per_step(2048) != g0.cost_flops_per_step(2048)) ap_de = 1.0;
+    }
+    std::printf("{\"ap_de\": %.3e, \"ap_df\": %.3e, ", ap_de, ap_df);
     std::printf(
-        "{\"pf_de\": %.3e, \"pf_df\": %.3e, \"pf_dx_plugin_propagate\": %.3e, \"pf_dx_device_propagate\": %.3e, "
+        "\"pf_de\": %.3e, \"pf_df\": %.3e, \"pf_dx_plugin_propagate\": %.3e, \"pf_dx_device_propagate\": %.3e, "
         "\"pf_dx_parareal_device\": %.3e, ",
         pf_de, pf_df, pf_dx, pf_dx_dev, pf_dx_pr);
     std::printf(

@@ -15,8 +15,10 @@ Reference interface -> here:
   paramd::CutoffParams         include/paramd/potential.hpp:26-31 -> CutoffParams
   paramd::SimpleCutoffField/WolfField
                                include/paramd/force_field.hpp:34-60 -> SimpleCutoffField/WolfField
-  paramd::simple_cutoff/wolf_summation
-                               include/paramd/electrostatics.hpp:12-22 -> same names
+  paramd::simple_cutoff/wolf_summation/direct_coulomb
+                               include/paramd/electrostatics.hpp:9-22 -> same names
+  paramd::DirectCoulombField/PairRepulsionOverlay
+                               include/paramd/force_field.hpp:23-32,75-97 -> same names
   paramd::msm_potential        include/paramd/msm.hpp:24-25       -> msm_potential
   paramd::PropagatorSpec/propagate/verlet_step/energy_report
                                include/paramd/integrate.hpp:13-38 -> same names
@@ -38,6 +40,7 @@ from . import _native
 __all__ = [
     "MsmConfig", "UnitsConfig", "ParticleSystem", "PotentialResult", "ForceField", "MsmField",
     "GpuField", "CutoffParams", "SimpleCutoffField", "WolfField", "simple_cutoff", "wolf_summation",
+    "DirectCoulombField", "PairRepulsionOverlay", "direct_coulomb",
     "msm_potential", "PropagatorSpec", "propagate", "verlet_step", "energy_report", "EnergyReport",
     "PararealConfig", "PararealResult", "parareal_window", "parareal_run", "SequentialExecutor",
     "AsyncExecutor", "DeviceSystem", "Error", "ConfigError", "DomainError", "CoverageError",
@@ -209,7 +212,7 @@ class ForceField:
 
 class GpuField(ForceField):
     """A force field bound to one B200 (a msmb_field handle): the common part of
-    MsmField, SimpleCutoffField and WolfField.  ``evaluate`` is const and safe to
+    MsmField, SimpleCutoffField, WolfField, DirectCoulombField and PairRepulsionOverlay.  ``evaluate`` is const and safe to
     call from several threads (calls on one field are serialised on its GPU stream)."""
 
     _h = None
@@ -233,6 +236,8 @@ class GpuField(ForceField):
         rc = _native.lib().msmb_evaluate(self._h, n, _p(s.positions), _p(s.charges), _p(s.box), _p(phi),
                                          _p(ps), _p(pl), _p(f), _p(e))
         _check(self._h, rc)
+        if _native.lib().msmb_field_kind(self._h) != 0:  # only MSM fills short_part/long_part
+            ps = pl = None
         return PotentialResult(phi, f, float(e[0]), ps, pl)
 
     # -- measurement / diagnostics
@@ -398,6 +403,50 @@ class WolfField(_PairField):
 
     def name(self) -> str:
         return "wolf"
+
+
+class DirectCoulombField(GpuField):
+    """paramd::DirectCoulombField (force_field.hpp:23-32): the exact O(N^2) Coulomb sum
+    (direct_coulomb, src/electrostatics.cpp:43-64), all pairs on a B200.  No box needed."""
+
+    def __init__(self, units: UnitsConfig = None, device: int = 0):
+        self._units = units or UnitsConfig.physical()
+        self._device = device
+        self._h = C.c_void_p()
+        u = self._units._c()
+        rc = _native.lib().msmb_create_direct(C.byref(u), device, C.byref(self._h))
+        if rc:
+            _raise(None, rc)
+
+    def name(self) -> str:
+        return "direct"
+
+
+class PairRepulsionOverlay(GpuField):
+    """paramd::PairRepulsionOverlay (force_field.hpp:75-97; force_field.cpp:45-68):
+    the base GPU field plus U = sum_{i<j} eps (sigma/r)^12 over all pairs (forces and
+    total energy include it; the per-particle potential stays electrostatic).  The
+    overlay is its own GPU handle (msmb_create_overlay); ``base`` is unchanged."""
+
+    def __init__(self, base: GpuField, epsilon: float = 0.1, sigma: float = 1.0):
+        if not isinstance(base, GpuField):
+            raise ConfigError("PairRepulsionOverlay needs a GPU base field")
+        self._base = base
+        self._units = base.units()
+        self._eps, self._sigma = float(epsilon), float(sigma)
+        self._h = C.c_void_p()
+        rc = _native.lib().msmb_create_overlay(base.handle, self._eps, self._sigma, C.byref(self._h))
+        if rc:
+            _raise(None, rc)
+
+    def name(self) -> str:
+        return self._base.name() + "+rep"
+
+
+
+def direct_coulomb(s: ParticleSystem, units: UnitsConfig = None) -> PotentialResult:
+    """paramd::direct_coulomb (electrostatics.hpp:9) on the GPU."""
+    return DirectCoulombField(units or UnitsConfig.physical()).evaluate(s)
 
 
 def simple_cutoff(s: ParticleSystem, params: CutoffParams, units: UnitsConfig = None) -> PotentialResult:

@@ -53,6 +53,8 @@ SIGNATURES = {
     "msmb_create_cutoff": (C.c_int, [C.c_int, C.POINTER(CutoffParamsC), C.POINTER(UnitsC), C.c_int,
                                      C.POINTER(_VP)]),
     "msmb_field_kind": (C.c_int, [_VP]),
+    "msmb_create_direct": (C.c_int, [C.POINTER(UnitsC), C.c_int, C.POINTER(_VP)]),
+    "msmb_create_overlay": (C.c_int, [_VP, C.c_double, C.c_double, C.POINTER(_VP)]),
     "msmb_evaluate": (C.c_int, [_VP, C.c_int64, _D, _D, _D, _D, _D, _D, _D, _D]),
     "msmb_propagate": (C.c_int, [_VP, C.c_int64, _D, _D, _D, _D, _D, C.c_double, C.c_int]),
     "msmb_propagate_ex": (C.c_int, [_VP, C.c_int64, _D, _D, _D, _D, _D, C.c_double, C.c_int,

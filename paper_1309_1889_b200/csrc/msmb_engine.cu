@@ -176,10 +176,46 @@ void ensure_const_table(msmb_field* f, Workspace& W) {
 
 static bool make_levels(msmb_field* f, Workspace& W, Error& e);
 
+// per-atom outputs, state backup/staging and the error record
+static void alloc_outputs(Workspace& Wr, int64_t n) {
+    Workspace* W = &Wr;
+    const size_t N = size_t(n > 0 ? n : 1);
+    DevOut& o = W->o;
+    o.fx = walloc<double>(*W, N);
+    o.fy = walloc<double>(*W, N);
+    o.fz = walloc<double>(*W, N);
+    o.phi = walloc<double>(*W, N);
+    o.phis = walloc<double>(*W, N);
+    o.phil = walloc<double>(*W, N);
+    o.e = walloc<double>(*W, N);
+    o.partial = walloc<double>(*W, size_t(reduce_blocks(n)));
+    o.energy = walloc<double>(*W, 1);
+    ck(W->backup.alloc(sizeof(double) * 6 * N), "cudaMalloc backup");
+    ck(W->staging.alloc(sizeof(double) * 3 * N), "cudaMalloc staging");
+    ck(cudaMalloc(&W->err, sizeof(ErrRec)), "cudaMalloc err");
+    ck(cudaMallocHost(&W->err_host, sizeof(ErrRec)), "cudaMallocHost err");
+}
+
 static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const double* box,
                                                  Error& e) {
     auto W = std::make_unique<Workspace>();
     W->uid = g_ws_uid++;
+    const size_t NN = size_t(n > 0 ? n : 1);
+    if (f->rep_on || f->kind == MSMB_FIELD_DIRECT) { // all-pairs buffers (msmb_direct.cu)
+        W->ap.S = allpairs_splits(n);
+        W->ap.part = W->ap.S > 1 ? walloc<double>(*W, size_t(W->ap.S) * 5 * NN) : nullptr;
+        W->ap.e_rep = walloc<double>(*W, NN);
+    }
+    if (f->kind == MSMB_FIELD_DIRECT) { // no binning, no grid: only the outputs
+        Geometry& g = W->g;
+        g.kind = MSMB_FIELD_DIRECT;
+        g.units = f->units;
+        for (int ax = 0; ax < 3; ++ax) g.box[ax] = box[ax];
+        W->n = n;
+        alloc_outputs(*W, n);
+        ck(cudaDeviceSynchronize(), "sync");
+        return W;
+    }
     e = f->kind == MSMB_FIELD_MSM ? build_geometry(f->cfg, f->units, box, n, W->g)
                                   : build_pair_geometry(f->kind, f->cut, f->units, box, n, W->g);
     if (e.kind) return nullptr;
@@ -226,20 +262,7 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
     ck(cudaMemset(c.flag, 0, 5 * sizeof(int)), "memset");
     ck(cudaMemset(c.colstart, 0, sizeof(int) * size_t(g.ncols + 1)), "memset");
     alloc_plist(*W, g.pair_cap);
-    DevOut& o = W->o;
-    o.fx = walloc<double>(*W, N);
-    o.fy = walloc<double>(*W, N);
-    o.fz = walloc<double>(*W, N);
-    o.phi = walloc<double>(*W, N);
-    o.phis = walloc<double>(*W, N);
-    o.phil = walloc<double>(*W, N);
-    o.e = walloc<double>(*W, N);
-    o.partial = walloc<double>(*W, size_t(reduce_blocks(n)));
-    o.energy = walloc<double>(*W, 1);
-    ck(W->backup.alloc(sizeof(double) * 6 * N), "cudaMalloc backup");
-    ck(W->staging.alloc(sizeof(double) * 3 * N), "cudaMalloc staging");
-    ck(cudaMalloc(&W->err, sizeof(ErrRec)), "cudaMalloc err");
-    ck(cudaMallocHost(&W->err_host, sizeof(ErrRec)), "cudaMallocHost err");
+    alloc_outputs(*W, n);
     if (msm && !make_levels(f, *W, e)) return nullptr;
     // wupload's pageable cudaMemcpy may return before its DMA lands, and the
     // field's streams are non-blocking (not ordered after the legacy stream)
@@ -389,8 +412,8 @@ struct StageScope {
 };
 
 static const char* kStages[] = {"bin", "sort", "clusters", "pairs", "anterp", "restrict",
-                                "lattice", "top", "prolong", "interp", "finalize"};
-constexpr int kNumStages = 11;
+                                "lattice", "top", "prolong", "interp", "finalize", "overlay"};
+constexpr int kNumStages = 12;
 
 static int stage_id(const char* name) {
     for (int i = 0; i < kNumStages; ++i)
@@ -428,6 +451,30 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, 
         sc.done(nl);
         total += nl;
     };
+    // PairRepulsionOverlay (force_field.cpp:45-68): after the base field's outputs,
+    // all-pairs repulsion forces added to F, its energy added to the total
+    auto overlay = [&](DevOut& o) {
+        if (!f->rep_on) return;
+        run("overlay", [&] {
+            int nl = launch_allpairs(st, s, g.units.coulomb_constant, 0, 1, f->rep_eps, f->rep_sigma, W.ap, o, W.err);
+            if (o.e) nl += launch_energy_sum(st, s.n, W.ap.e_rep, o.partial, 1.0, o.energy, 1, W.err);
+            return nl;
+        });
+    };
+    if (g.kind == MSMB_FIELD_DIRECT) { // direct_coulomb (electrostatics.cpp:43-64): all pairs
+        DevOut o = W.o;
+        if (!outputs) o.phi = o.phis = o.phil = o.e = nullptr;
+        run("pairs", [&] {
+            int nl = launch_allpairs(st, s, g.units.coulomb_constant, 1, f->rep_on, f->rep_eps, f->rep_sigma, W.ap,
+                                     o, W.err);
+            if (o.e) nl += launch_energy_sum(st, s.n, o.e, o.partial, g.units.coulomb_constant, o.energy, 0, W.err);
+            if (o.e && f->rep_on)
+                nl += launch_energy_sum(st, s.n, W.ap.e_rep, o.partial, 1.0, o.energy, 1, W.err);
+            return nl;
+        });
+        run("finalize", [&] { return launch_finalize(st, s, W.err, 1); });
+        return total;
+    }
     if (g_exp_stamps) launch_stamp(st, 0);
     run("bin", [&] { return launch_bin(st, g, s, W.a, W.c, W.err); });
     run("sort", [&] { return launch_sort(st, g, s, W.a, W.c, W.err); });
@@ -437,6 +484,7 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, 
         DevOut o = W.o;
         if (!outputs) o.phi = o.phis = o.phil = o.e = nullptr;
         run("interp", [&] { return launch_pair_out(st, g, s.n, W.a, W.c, o, W.err, outputs ? 1 : 0, W.whole); });
+        overlay(o);
         run("finalize", [&] { return launch_finalize(st, s, W.err, 1); });
         return total;
     }
@@ -470,6 +518,7 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, 
     DevOut o = W.o;
     if (!outputs) o.phi = o.phis = o.phil = o.e = nullptr;
     run("interp", [&] { return launch_interp(st, g, s.n, W.a, W.c, W.L, o, W.err, outputs ? 1 : 0, W.whole); });
+    overlay(o);
     run("finalize", [&] { return launch_finalize(st, s, W.err); });
     if (g_exp_stamps) launch_stamp(st, 6);
     return total;
@@ -487,13 +536,13 @@ void record_counters(msmb_field* f, const Workspace& W, const ErrRec& r) {
     f->counters[0] = int64_t(r.pairs / 2);
     f->counters[1] = int64_t(r.candidates);
     int nclu = 0;
-    cudaMemcpy(&nclu, W.c.nclu, sizeof(int), cudaMemcpyDeviceToHost);
+    if (W.c.nclu) cudaMemcpy(&nclu, W.c.nclu, sizeof(int), cudaMemcpyDeviceToHost);
     f->counters[2] = nclu;
     f->counters[3] = W.g.lattice_taps_clipped;
     f->counters[4] = W.g.top_taps;
     f->counters[5] = W.launches_eval;
     int rebuilds = 0;
-    cudaMemcpy(&rebuilds, W.c.flag + 2, sizeof(int), cudaMemcpyDeviceToHost);
+    if (W.c.flag) cudaMemcpy(&rebuilds, W.c.flag + 2, sizeof(int), cudaMemcpyDeviceToHost);
     f->counters[6] = rebuilds;
 }
 
@@ -797,6 +846,41 @@ int msmb_create_cutoff(int kind, const msmb_cutoff_params* params, const msmb_un
 
 int msmb_field_kind(const msmb_field* f) { return f ? f->kind : -1; }
 
+int msmb_create_direct(const msmb_units* units, int device, msmb_field** out) {
+    *out = nullptr;
+    Error e = validate_units(*units);
+    if (e.kind) {
+        g_create_error = e;
+        return e.kind;
+    }
+    const int rc = field_new(device, out);
+    if (rc) return rc;
+    (*out)->kind = MSMB_FIELD_DIRECT;
+    (*out)->units = *units;
+    return MSMB_OK;
+}
+
+int msmb_create_overlay(const msmb_field* base, double epsilon, double sigma, msmb_field** out) {
+    *out = nullptr;
+    if (!base) {
+        g_create_error = Error{MSMB_ERR_CONFIG, -1, -1, -1, "overlay needs a base field"};
+        return MSMB_ERR_CONFIG;
+    }
+    const int rc = field_new(base->device, out);
+    if (rc) return rc;
+    msmb_field* f = *out;
+    f->kind = base->kind;
+    f->cut = base->cut;
+    f->cfg = base->cfg;
+    f->units = base->units;
+    f->lattice_direct = base->lattice_direct;
+    f->pair_skin = base->pair_skin;
+    f->rep_on = 1;
+    f->rep_eps = epsilon;
+    f->rep_sigma = sigma;
+    return MSMB_OK;
+}
+
 static int field_new(int device, msmb_field** out) {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0 || device < 0 || device >= ndev) {
@@ -885,12 +969,14 @@ int msmb_last_error(const msmb_field* f, int* kind, int64_t* idx_i, int64_t* idx
 }
 
 double msmb_cost_flops_per_step(const msmb_field* f, int64_t n) {
+    const double rep = f->rep_on ? 30.0 * double(n) : 0.0; // PairRepulsionOverlay, force_field.cpp:70-72
+    if (f->kind == MSMB_FIELD_DIRECT) return 20.0 * double(n) * double(n) + rep; // force_field.cpp:17-19
     if (f->kind != MSMB_FIELD_MSM) { // force_field.cpp:25-35
         const double fpp = f->cut.flops_per_particle > 0.0 ? f->cut.flops_per_particle
                                                            : (f->kind == MSMB_FIELD_WOLF ? 350.0 : 301.0);
-        return fpp * double(n);
+        return fpp * double(n) + rep;
     }
-    return host_flops_simplified(f->cfg.cutoff_a, f->cfg.spacing_h, double(n));
+    return host_flops_simplified(f->cfg.cutoff_a, f->cfg.spacing_h, double(n)) + rep;
 }
 
 int msmb_evaluate(msmb_field* f, int64_t n, const double* pos_xyz, const double* q,
@@ -900,7 +986,7 @@ int msmb_evaluate(msmb_field* f, int64_t n, const double* pos_xyz, const double*
     GUARD_BEGIN
     f->last = Error{};
     cudaSetDevice(f->device);
-    Error e = validate_config(f->cfg);
+    Error e = f->kind == MSMB_FIELD_MSM ? validate_config(f->cfg) : Error{};
     if (!e.kind) e = validate_units(f->units);
     if (e.kind) return engine_set_error(f, e);
     e = ensure_workspace(f, n, box);

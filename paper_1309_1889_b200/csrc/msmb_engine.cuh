@@ -88,6 +88,7 @@ struct Workspace {
     FftJobs fft{};                       // FFT lattice cutoff plan (msmb_fft.cu)
     FftJobs fft_top{};                   // FFT top level (n = 0: k_top_direct / k_conv)
     bool lattice_fft = true;             // false: direct stencil (k_lattice)
+    AllPairsBuf ap{};                    // direct Coulomb / repulsion overlay (msmb_direct.cu)
     Part whole;                          // the whole system (single-GPU path)
     Part part;                           // this field's part of a spatial decomposition (msmb_dd.cu)
     ~Workspace();
@@ -116,6 +117,8 @@ struct StageTimer {
 struct msmb_field {
     int kind = MSMB_FIELD_MSM;       // msmb_field_kind
     msmb_cutoff_params cut{};        // pair-only fields (msmb_create_cutoff)
+    int rep_on = 0;                  // PairRepulsionOverlay (msmb_create_overlay)
+    double rep_eps = 0, rep_sigma = 1;
     msmb_msm_config cfg{};
     msmb_units units{};
     int device = 0;

@@ -2313,7 +2313,7 @@ __global__ void __launch_bounds__(256) k_energy1(int64_t n, const double* __rest
 }
 
 __global__ void __launch_bounds__(256) k_energy2(int nb, const double* __restrict__ partial,
-                                                 double kc, double* out, const ErrRec* err) {
+                                                 double kc, double* out, const ErrRec* err, int accumulate = 0) {
     __shared__ double sh[256];
     if (failed(err)) return;
     double s = 0.0;
@@ -2324,7 +2324,15 @@ __global__ void __launch_bounds__(256) k_energy2(int nb, const double* __restric
         if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
         __syncthreads();
     }
-    if (threadIdx.x == 0) *out = sh[0] * kc;
+    if (threadIdx.x == 0) *out = accumulate ? *out + sh[0] * kc : sh[0] * kc;
+}
+
+int launch_energy_sum(cudaStream_t st, int64_t n, const double* e, double* partial, double scale, double* out,
+                      int accumulate, ErrRec* err) {
+    const int nb = reduce_blocks(n);
+    k_energy1<<<nb, 256, 0, st>>>(n, e, partial, err);
+    k_energy2<<<1, 256, 0, st>>>(nb, partial, scale, out, err, accumulate);
+    return 2;
 }
 
 int reduce_blocks(int64_t n) { return int((n + 4095) / 4096) > 0 ? int((n + 4095) / 4096) : 1; }

@@ -160,6 +160,20 @@ int launch_finalize(cudaStream_t st, const DevState& s, ErrRec* err, int pair_fi
 // pair-only fields: per-atom outputs and energy from the pair sums (no grid)
 int launch_pair_out(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c, DevOut& o,
                     ErrRec* err, int want_energy, const Part& P);
+// fixed-order energy tree: *out = scale * sum(e[0..n)) (accumulate: *out += ...)
+int launch_energy_sum(cudaStream_t st, int64_t n, const double* e, double* partial, double scale, double* out,
+                      int accumulate, ErrRec* err);
+// all-pairs kernels (msmb_direct.cu): direct Coulomb (coul) and/or the
+// PairRepulsionOverlay term (rep) over all pairs of the state in original order.  coul writes
+// phi/F/e of `o`; rep adds its forces to F and its per-atom energy to e_rep.
+struct AllPairsBuf {
+    double* part;       // [S * 5 * n] per-split partial sums (S > 1)
+    double* e_rep;      // [n] 0.5 * sum_j eps (sigma/r)^12
+    int S;              // j splits
+};
+int allpairs_splits(int64_t n);
+int launch_allpairs(cudaStream_t st, const DevState& s, double kc, int coul, int rep, double eps,
+                    double sigma, const AllPairsBuf& B, DevOut& o, ErrRec* err);
 int launch_kick_drift(cudaStream_t st, DevState& s, const DevOut& o, double dt, double conv,
                       int kicks, ErrRec* err);
 int launch_kick(cudaStream_t st, DevState& s, const DevOut& o, double dt, double conv,

@@ -32,3 +32,5 @@ def test_reference_drives_gpu_field():
     assert r["pf_de"] <= 1e-10 and r["pf_df"] <= 1e-8
     assert r["pf_dx_plugin_propagate"] <= 1e-8 and r["pf_dx_device_propagate"] <= 1e-8
     assert 0 <= r["pf_dx_parareal_device"] <= 1e-8
+    # all-pairs fields (F3 direct Coulomb, F2 repulsion overlay)
+    assert r["ap_de"] <= 1e-10 and r["ap_df"] <= 1e-8

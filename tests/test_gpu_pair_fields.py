@@ -36,7 +36,7 @@ def test_golden(name):
     f = gpu_field(spec)
     r = f.evaluate(pkg.ParticleSystem(g["pos"], None, g["q"], None, g["box"]))
     check(r, dict(energy=float(g[f"{name}_energy"]), force=g[f"{name}_force"], phi=g[f"{name}_phi"]))
-    assert np.array_equal(r.short_part, r.per_particle_potential) and not r.long_part.any()
+    assert r.short_part is None and r.long_part is None  # as the reference's make_result
 
 
 @pytest.mark.parametrize("name,n,spec", [
@@ -152,3 +152,81 @@ def test_msm_only_entry_points_refuse_pair_fields():
     f = gpu_field(fspec("cutoff", 10.0))
     with pytest.raises(pkg.ConfigError, match="needs an MSM field"):
         pkg.MsmField.set_lattice_method(f, True)
+
+
+# ---- all-pairs fields: DirectCoulombField, PairRepulsionOverlay
+def test_direct_golden_and_spec500():
+    g = golden("fields")
+    r = pkg.DirectCoulombField().evaluate(pkg.ParticleSystem(g["pos"], None, g["q"], None, g["box"]))
+    check(r, dict(energy=float(g["direct_energy"]), force=g["direct_force"], phi=g["direct_phi"]))
+    s5, d5 = golden("spec500"), golden("spec500_direct")
+    r = pkg.direct_coulomb(pkg.ParticleSystem(s5["pos"], None, s5["q"], None, s5["box"]))
+    check(r, dict(energy=float(d5["energy"]), force=d5["force"], phi=d5["phi"]))
+
+
+@pytest.mark.parametrize("name", ["cutoff10_rep", "direct_rep"])
+def test_overlay_golden(name):
+    g = golden("fields")
+    spec = g["specs"][list(g["names"]).index(name)]
+    base = pkg.DirectCoulombField() if spec[0] == 3 else gpu_field(spec)
+    f = pkg.PairRepulsionOverlay(base, float(spec[6]), float(spec[7]))
+    s = pkg.ParticleSystem(g["pos"], None, g["q"], None, g["box"])
+    r = f.evaluate(s)
+    check(r, dict(energy=float(g[f"{name}_energy"]), force=g[f"{name}_force"], phi=g[f"{name}_phi"]))
+    assert f.name() == base.name() + "+rep"
+    assert f.cost_flops_per_step(1000) == base.cost_flops_per_step(1000) + 30000.0
+    # the base field is unchanged by the overlay
+    rb = base.evaluate(s)
+    base_name = name.replace("_rep", "")
+    assert rel_e(rb.total_energy, float(g[f"{base_name}_energy"])) <= E_TOL
+
+
+@pytest.mark.parametrize("n", [1, 2, 37, 1000, 20000])
+def test_direct_vs_oracle_sizes(port, n):
+    rng = np.random.default_rng(n)
+    L = max(5.0, (n / 0.1) ** (1 / 3))
+    pos = rng.uniform(0, L, (n, 3))
+    q = rng.choice([-1.0, 1.0], n)
+    r = pkg.DirectCoulombField().evaluate(pkg.ParticleSystem(pos, None, q, None, np.array([L, L, L])))
+    o = port.field_evaluate(fspec("direct", 0.0), pos, q, np.array([L, L, L]))
+    if n == 1:
+        assert r.total_energy == 0.0 and not r.per_particle_force.any()
+        return
+    check(r, o)
+
+
+def test_overlay_on_msm_vs_reference(ref):
+    # MsmField + PairRepulsionOverlay: the restatement has no MSM overlay, so check the
+    # reference directly
+    w = fx.config("c1s", n_override=3000)
+    spec = fspec("msm", w.a, w.h, w.levels, rep_eps=0.1, rep_sigma=2.0)
+    base = pkg.MsmField(pkg.MsmConfig(w.a, w.h, w.levels))
+    f = pkg.PairRepulsionOverlay(base, 0.1, 2.0)
+    r = f.evaluate(pkg.ParticleSystem(w.pos, None, w.q, None, w.box))
+    check(r, ref.field_evaluate(spec, w.pos, w.q, w.box))
+    assert r.short_part is not None and r.long_part is not None
+
+
+def test_direct_and_overlay_errors_and_dynamics(port):
+    w = fx.config("c1", n_override=3000)
+    pos = w.pos.copy()
+    pos[1234] = pos[99]
+    with pytest.raises(pkg.CoincidentParticlesError, match="particles 99 and 1234 coincide"):
+        pkg.DirectCoulombField().evaluate(pkg.ParticleSystem(pos, None, w.q, None, w.box))
+    f = pkg.PairRepulsionOverlay(gpu_field(fspec("cutoff", 10.0)), 0.1, 2.0)
+    with pytest.raises(pkg.CoincidentParticlesError, match="particles 99 and 1234 coincide"):
+        f.evaluate(pkg.ParticleSystem(pos, None, w.q, None, w.box))
+    # 10 Verlet steps with the overlay on the cutoff field (device-resident) vs the restatement
+    w = fx.config("c1s", n_override=2500)
+    spec = fspec("cutoff", 10.0, rep_eps=0.1, rep_sigma=2.0)
+    out = pkg.propagate(pkg.PropagatorSpec(f, 0.05, 10), pkg.ParticleSystem(w.pos, w.vel, w.q, w.mass, w.box))
+    p2, v2, done, err = port.field_propagate(spec, w.pos, w.vel, w.q, w.mass, w.box, 0.05, 10)
+    assert err is None
+    assert rel_rms(out.positions, p2) <= 1e-12 and rel_rms(out.velocities, v2) <= 1e-8
+    # direct field propagate
+    spec = fspec("direct", 0.0)
+    out = pkg.propagate(pkg.PropagatorSpec(pkg.DirectCoulombField(), 0.05, 5),
+                        pkg.ParticleSystem(w.pos, w.vel, w.q, w.mass, w.box))
+    p2, v2, done, err = port.field_propagate(spec, w.pos, w.vel, w.q, w.mass, w.box, 0.05, 5)
+    assert err is None
+    assert rel_rms(out.positions, p2) <= 1e-12 and rel_rms(out.velocities, v2) <= 1e-8
