@@ -414,6 +414,7 @@ struct StageScope {
 static const char* kStages[] = {"bin", "sort", "clusters", "pairs", "anterp", "restrict",
                                 "lattice", "top", "prolong", "interp", "finalize", "overlay"};
 constexpr int kNumStages = 12;
+constexpr int kBenchStages = 11; // stage names msmb_bench_propagate reports (msmb.h)
 
 static int stage_id(const char* name) {
     for (int i = 0; i < kNumStages; ++i)
@@ -1228,7 +1229,7 @@ int msmb_bench_propagate(msmb_field* f, msmb_system* sys, double dt, int steps, 
     cudaEventDestroy(eb);
     const ErrRec r = read_err(f, W);
     if (launches) *launches = f->launches - l0;
-    for (int i = 0; i < kNumStages; ++i) {
+    for (int i = 0; i < kBenchStages; ++i) { // the ABI's 11 (msmb.h); "overlay" is reported by msmb_stage_times
         if (stage_ms) stage_ms[i] = acc[i];
         if (stage_names) stage_names[i] = kStages[i];
     }
