@@ -851,7 +851,13 @@ __global__ void __launch_bounds__(kMaskWarps * 32)
 // conflicts, more steps) 0.68 / 0.73 vs 0.63 per lane; unroll 8 vs 4: equal; each
 // lane preferring a mask bit whose row sits in bank quad (lane & 7) (conflict-free
 // when found, measured in a microbenchmark) 0.68: only 17% of steps find one --
-// a lane's mask holds ~1-2 atoms of a cluster -- and bank conflicts did not drop.
+// a lane's mask holds ~1-2 atoms of a cluster -- and bank conflicts did not drop;
+// two z-adjacent i atoms per lane walking the union of their masks (half-warp per
+// i-cluster, each staged row feeding two pairs) 0.86: shared-memory wavefronts
+// -35% but FP64 instructions +36% (union steps wasted for one of the atoms) and
+// occupancy 4 -> 3.4 warps/SMSP at 122 registers; the kernel is latency-bound
+// (FP64 pipe 53%, issue 62-67%, stalls spread over wait / math throttle /
+// long scoreboard of the staging loads).
 template <int K>
 __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     k_pairs_mw(const int2* __restrict__ clu, const int* __restrict__ plist, const int* __restrict__ pcnt,
