@@ -857,7 +857,8 @@ __global__ void __launch_bounds__(kMaskWarps * 32)
 // -35% but FP64 instructions +36% (union steps wasted for one of the atoms) and
 // occupancy 4 -> 3.4 warps/SMSP at 122 registers; the kernel is latency-bound
 // (FP64 pipe 53%, issue 62-67%, stalls spread over wait / math throttle /
-// long scoreboard of the staging loads).
+// long scoreboard of the staging loads); two staged clusters in flight (register
+// double buffer) 0.647 vs 0.632.
 template <int K>
 __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     k_pairs_mw(const int2* __restrict__ clu, const int* __restrict__ plist, const int* __restrict__ pcnt,
