@@ -1409,7 +1409,7 @@ int msmb_debug_stage(msmb_field* f, int stage, int k, const double box[3], const
             const int t = g.levels - 1;
             up(W.L.charge + g.lv[t].offset, in, g.lv[t].size);
             f->launches += W.fft_top.n ? launch_lattice_fft(f->stream, W.fft_top, W.err)
-                                       : launch_top(f->stream, g, W.L, W.err);
+                                       : launch_top(f->stream, g, W.L, W.err, true);
             down(out, W.L.pot + g.lv[t].offset, g.lv[t].size);
             break;
         }

@@ -141,7 +141,9 @@ cudaError_t lattice_prepare(size_t bytes);
 int lattice_splits(const Geometry& g);
 bool lattice_const_fits(const Geometry& g);
 cudaError_t lattice_upload_const(const Geometry& g, cudaStream_t st);
-int launch_top(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
+// exact: the reference's sequential per-point sum, bit for bit (stage tests);
+// otherwise the warp-parallel production kernel (equal to rounding)
+int launch_top(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err, bool exact = false);
 cudaError_t top_prepare(const Geometry& g); // dynamic smem of the staged direct top kernel
 constexpr int64_t kTopFftMin = 4096; // FFT lattice mode: top levels above this many points use an FFT job
 int launch_prolong(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err);
