@@ -360,6 +360,43 @@ Error build_pair_geometry(int kind, const msmb_cutoff_params& p, const msmb_unit
         pf.e_shift = erfc_aa / a;
         pf.f_shift = erfc_aa / (a * a) + two_over_sqrt_pi * alpha * std::exp(-alpha * alpha * a * a) / a;
         pf.self_per_charge = -(pf.e_shift + two_over_sqrt_pi * alpha);
+        // erfcx(x) on [0, X] (only pairs with r < a, i.e. x < X, are accumulated):
+        // interpolation at the D+1 Chebyshev points in long double, then the monomial
+        // coefficients in u (sum |a_k| ~ 1 on [-1, 1], so Horner loses nothing)
+        const double X = alpha * a * (1.0 + 1e-9);
+        if (X >= 1e-3 && X <= 4.5) {
+            const int D = kWolfDeg;
+            const long double PI = 3.141592653589793238462643383279502884L;
+            long double f[kWolfDeg + 1], c[kWolfDeg + 1];
+            for (int j = 0; j <= D; ++j) {
+                const long double u = cosl(PI * (j + 0.5L) / (D + 1));
+                const long double x = (u + 1.0L) * 0.5L * X;
+                f[j] = expl(x * x) * erfcl(x);
+            }
+            for (int k = 0; k <= D; ++k) {
+                long double acc = 0;
+                for (int j = 0; j <= D; ++j) acc += f[j] * cosl(PI * k * (j + 0.5L) / (D + 1));
+                c[k] = acc * 2.0L / (D + 1);
+            }
+            c[0] *= 0.5L;
+            // Chebyshev -> monomial: T_{k+1} = 2u T_k - T_{k-1}
+            long double T0[kWolfDeg + 1] = {}, T1[kWolfDeg + 1] = {}, T2[kWolfDeg + 1], mono[kWolfDeg + 1] = {};
+            T0[0] = 1;
+            T1[1] = 1;
+            for (int i = 0; i <= D; ++i) mono[i] += c[0] * T0[i];
+            for (int i = 0; i <= D; ++i) mono[i] += c[1] * T1[i];
+            for (int k = 2; k <= D; ++k) {
+                for (int i = 0; i <= D; ++i) T2[i] = (i > 0 ? 2.0L * T1[i - 1] : 0.0L) - T0[i];
+                for (int i = 0; i <= D; ++i) mono[i] += c[k] * T2[i];
+                for (int i = 0; i <= D; ++i) {
+                    T0[i] = T1[i];
+                    T1[i] = T2[i];
+                }
+            }
+            for (int i = 0; i <= D; ++i) pf.wolf_c[i] = double(mono[i]);
+            pf.wolf_us = 2.0 * alpha / X;
+            pf.wolf_fast = std::getenv("MSMB_WOLF_LIBDEVICE") ? 0 : 1;
+        }
     }
     set_pair_layout(g, c, box, n);
     return Error{};

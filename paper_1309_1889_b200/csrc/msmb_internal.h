@@ -97,7 +97,14 @@ struct PairFieldP {
     int kind = MSMB_FIELD_MSM;   // msmb_field_kind
     double alpha = 0;            // Wolf damping
     double e_shift = 0, f_shift = 0, self_per_charge = 0; // src/electrostatics.cpp:96-102
+    // erfc(x) = exp(-x^2) erfcx(x) with erfcx as a degree-kWolfDeg polynomial in
+    // u = 2x/X - 1 on [0, X = alpha a] (Chebyshev interpolation; |rel err| <= 2e-14
+    // for X <= 4.5); wolf_fast = 0 falls back to libdevice erfc
+    int wolf_fast = 0;
+    double wolf_us = 0;          // 2 alpha / X: u = wolf_us r - 1
+    double wolf_c[29] = {};      // monomial coefficients in u, degree kWolfDeg
 };
+constexpr int kWolfDeg = 28;
 
 struct Geometry {
     int kind = MSMB_FIELD_MSM;           // MSM, or a pair-only field (no hierarchy; binning clamps)

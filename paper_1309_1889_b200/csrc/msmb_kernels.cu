@@ -618,6 +618,9 @@ struct PairP {
     double kc;
     // Wolf / damped-shifted-force pair term (src/electrostatics.cpp:91-120)
     double alpha, alpha2, gcoef, e_shift, f_shift, a;
+    int wolf_fast;               // erfc(x) = exp(-x^2) * poly(u), see PairFieldP
+    double wolf_us;
+    double wolf_c[kWolfDeg + 1];
 };
 
 #ifndef MSMB_RSQRT_NEWTON
@@ -658,8 +661,18 @@ __device__ __forceinline__ void pair_fn(const PairP& p, double r2, double rinv, 
         sd = -rinv * rinv2;
     } else {
         const double r = r2 * rinv;
-        const double er = erfc(p.alpha * r);
-        const double gs = p.gcoef * exp(-p.alpha2 * r2);
+        const double e = exp(-p.alpha2 * r2); // shared by erfc and the Gaussian
+        double er;
+        if (p.wolf_fast) { // erfc(ar) = exp(-a^2 r^2) erfcx(ar); u clamped for r >= a (masked)
+            const double u = fmin(fma(p.wolf_us, r, -1.0), 1.0);
+            double poly = p.wolf_c[kWolfDeg];
+#pragma unroll
+            for (int k = kWolfDeg - 1; k >= 0; --k) poly = fma(poly, u, p.wolf_c[k]);
+            er = e * poly;
+        } else {
+            er = erfc(p.alpha * r);
+        }
+        const double gs = p.gcoef * e;
         g = fma(p.f_shift, r - p.a, fma(er, rinv, -p.e_shift));
         sd = -fma(er, rinv2, fma(gs, rinv, -p.f_shift)) * rinv;
     }
@@ -1085,6 +1098,9 @@ int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& 
     p.e_shift = g.pf.e_shift;
     p.f_shift = g.pf.f_shift;
     p.a = A;
+    p.wolf_fast = g.pf.wolf_fast;
+    p.wolf_us = g.pf.wolf_us;
+    for (int k = 0; k <= kWolfDeg; ++k) p.wolf_c[k] = g.pf.wolf_c[k];
     const int64_t maxclu = n / 32 + g.ncols + 1;
     int l = 0;
     if (n > 0) {

@@ -93,6 +93,27 @@ def main():
     t = time.perf_counter() - t0
     out["parareal_msm_fine_cutoff_coarse_K1"] = dict(n=int(w.n), seconds=t, atom_steps_per_s=w.n * 800 / t,
                                                      counts=counts)
+    # the reference's own CPU path for the same fields (oracle/_ref, 1 thread): an
+    # O(N^2) i<j loop, timed on a random subset and scaled by the pair-check count
+    try:
+        sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+        import oracle_lib
+        if oracle_lib.have("ref"):
+            ref = oracle_lib.checker("ref")
+            w = fx.config("c2s")
+            M = 20000
+            idx = np.sort(np.random.default_rng(0).choice(w.n, M, replace=False))
+            for name, spec in [("cutoff", oracle_lib.fspec("cutoff", 12.0)),
+                               ("wolf", oracle_lib.fspec("wolf", 12.0, alpha=0.2)),
+                               ("direct", oracle_lib.fspec("direct", 0.0))]:
+                t0 = time.perf_counter()
+                ref.field_evaluate(spec, w.pos[idx], w.q[idx], w.box)
+                t = (time.perf_counter() - t0) * (w.n * (w.n - 1)) / (M * (M - 1))
+                out.setdefault("cpu_reference_1thread", {})[name] = dict(
+                    sample=f"{M}-atom random subset of C2-S, scaled by N(N-1)/(M(M-1))",
+                    seconds_per_eval_at_300k=t, atom_steps_per_s=w.n / t)
+    except Exception as e:  # the checker is optional on the box
+        out["cpu_reference_1thread"] = f"unavailable: {e}"
     print(json.dumps(out))
 
 
