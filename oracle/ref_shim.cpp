@@ -34,6 +34,7 @@
 #include "paramd/msm_phases.hpp"
 #include "paramd/parareal.hpp"
 #include "paramd/cost_model.hpp"
+#include "paramd/xyz_io.hpp"
 
 using namespace paramd;
 
@@ -562,6 +563,39 @@ int ref_field_parareal_window(int64_t n, const double* pos, const double* vel, c
             counts[1] = static_cast<int64_t>(w.counts.f_evals);
             counts[2] = static_cast<int64_t>(w.counts.f_skipped);
         }
+    });
+}
+
+// ---- extended-XYZ I/O (src/xyz_io.cpp) -------------------------------------------
+int ref_save_system(int64_t n, const double* pos, const double* vel, const double* q, const double* mass,
+                    const double* box, const char* path, char* msg, int cap) {
+    return guarded(msg, cap, [&] { save_system(make_system(n, pos, vel, q, mass, box), path); });
+}
+
+// *n_out = particle count; arrays (capacity cap_n) receive the system when it fits
+int ref_load_system(const char* path, int64_t cap_n, int64_t* n_out, double* pos, double* vel, double* q,
+                    double* mass, double* box, char* msg, int cap) {
+    return guarded(msg, cap, [&] {
+        ParticleSystem s = load_system(path);
+        *n_out = static_cast<int64_t>(s.size());
+        if (*n_out > cap_n) return;
+        store_state(s, pos, vel);
+        for (std::size_t i = 0; i < s.size(); ++i) {
+            q[i] = s.charges[i];
+            mass[i] = s.masses[i];
+        }
+        box[0] = s.box.x;
+        box[1] = s.box.y;
+        box[2] = s.box.z;
+    });
+}
+
+int ref_write_trajectory(int64_t n, const double* pos, const double* vel, const double* q, const double* mass,
+                         const double* box, int frames, const char* path, char* msg, int cap) {
+    return guarded(msg, cap, [&] {
+        TrajectoryWriter w(path);
+        ParticleSystem s = make_system(n, pos, vel, q, mass, box);
+        for (int f = 0; f < frames; ++f) w.write_frame(s, f * 10, f * 0.25);
     });
 }
 
