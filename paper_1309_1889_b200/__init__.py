@@ -433,6 +433,7 @@ class PairRepulsionOverlay(GpuField):
             raise ConfigError("PairRepulsionOverlay needs a GPU base field")
         self._base = base
         self._units = base.units()
+        self._device = base._device
         self._eps, self._sigma = float(epsilon), float(sigma)
         self._h = C.c_void_p()
         rc = _native.lib().msmb_create_overlay(base.handle, self._eps, self._sigma, C.byref(self._h))

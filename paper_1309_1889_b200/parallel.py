@@ -35,7 +35,7 @@ from typing import Optional
 
 import numpy as np
 
-from . import (ConfigError, Error, MsmField, NonConvergenceError, ParticleSystem, PararealConfig,
+from . import (ConfigError, Error, GpuField, MsmField, NonConvergenceError, ParticleSystem, PararealConfig,
                PararealResult, _ERR, _check, _native, _p)
 
 _CODE = {cls: code for code, cls in _ERR.items()}
@@ -77,8 +77,8 @@ class DeviceBackend:
         import torch
         self.torch = torch
         F, G = cfg.fine.force_field, cfg.coarse.force_field
-        if not isinstance(F, MsmField) or not isinstance(G, MsmField):
-            raise ConfigError("the device backend needs MsmField fine and coarse propagators")
+        if not isinstance(F, GpuField) or not isinstance(G, GpuField):
+            raise ConfigError("the device backend needs GPU fine and coarse propagators")
         self.cfg = cfg
         self.n = v.size()
         self.device = torch.device("cuda", F._device)
@@ -321,7 +321,9 @@ def parareal_run(v: ParticleSystem, total_points: int, cfg: PararealConfig, grou
             if cfg.short_circuit and prefix == t:
                 break
         if prefix == 0:
-            raise NonConvergenceError(f"window {window_idx} did not converge within max_iter={cfg.max_iter}")
+            e = NonConvergenceError(f"window {window_idx} did not converge within max_iter={cfg.max_iter}")
+            e.report = dict(rows=rows, counts=dict(counts), windows=window_idx)  # ConvergenceReport
+            raise e
         for n in range(1, prefix + 1):
             pos, vel = be.to_host(w.lam_prev[n])
             traj.append(ParticleSystem(pos, vel, v.charges, v.masses, v.box))
