@@ -230,3 +230,24 @@ def test_direct_and_overlay_errors_and_dynamics(port):
     p2, v2, done, err = port.field_propagate(spec, w.pos, w.vel, w.q, w.mass, w.box, 0.05, 5)
     assert err is None
     assert rel_rms(out.positions, p2) <= 1e-12 and rel_rms(out.velocities, v2) <= 1e-8
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 31, 33, 65])
+@pytest.mark.parametrize("spec", [fspec("cutoff", 8.0), fspec("wolf", 8.0, alpha=0.25), fspec("direct", 0.0),
+                                  fspec("cutoff", 8.0, rep_eps=0.1, rep_sigma=1.5)])
+def test_tiny_and_ragged_systems(port, n, spec):
+    box = np.array([20.0, 20.0, 20.0])
+    if n == 0:
+        pos, q = np.zeros((0, 3)), np.zeros(0)
+    else:
+        pos, q = fx.uniform(n, box, "alternating", 0.5, 31)
+    base = pkg.DirectCoulombField() if spec[0] == 3 else gpu_field(spec)
+    f = pkg.PairRepulsionOverlay(base, float(spec[6]), float(spec[7])) if spec[6] > 0 else base
+    r = f.evaluate(pkg.ParticleSystem(pos, None, q, None, box))
+    if n == 0:
+        assert r.total_energy == 0.0 and r.per_particle_potential.size == 0
+        return
+    o = port.field_evaluate(spec, pos, q, box)
+    assert abs(r.total_energy - o["energy"]) <= E_TOL * max(1.0, abs(o["energy"]))
+    assert rel_rms(r.per_particle_force, o["force"]) <= F_TOL or np.allclose(r.per_particle_force, o["force"], atol=1e-12)
+    assert np.allclose(r.per_particle_potential, o["phi"], rtol=1e-12, atol=1e-14)
