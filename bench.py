@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="step", choices=["step", "spatial", "parareal"],
+    ap.add_argument("--workload", default="step", choices=["step", "spatial", "parareal", "parareal_cutoff"],
                     help="step: the contract line (C2-S); spatial / parareal: the multi-GPU paths "
                          "(tools/bench_paths.py)")
     return ap.parse_args()
