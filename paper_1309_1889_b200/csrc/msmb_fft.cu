@@ -111,15 +111,20 @@ __device__ __forceinline__ int find_level(const FftJobs& J, int blk) {
     return k;
 }
 
-// X pass: lines along x at (y, z0 + l).  mode 0: forward from q; 1: inverse to u;
-// 2: forward from B over every line (spectrum precompute).
+// X pass: lines along x at (y, z0 + l).  mode 2: forward from B over every line
+// (spectrum precompute, complex).  Modes 0 / 1 use that the charges and potentials are
+// real: two lines (z0 + 2p, z0 + 2p + 1) travel as one complex line c = e + i o, and
+// only the x-frequencies 0 .. M0/2 are kept (the rest is the complex conjugate), so the
+// Y and Z passes run on M0/2 + 1 planes instead of M0 (half the work and traffic):
+//   mode 0: q -> c -> FFT -> E[k] = (C[k] + conj C[M0-k]) / 2, O[k] = (C[k] - conj C[M0-k]) / 2i
+//   mode 1: E, O (k <= M0/2, conjugate-extended) -> C = E + i O -> IFFT -> u_e = Re, u_o = Im
 __global__ void __launch_bounds__(256) k_fft_x(FftJobs J, int mode, const ErrRec* err) {
     extern __shared__ double2 sm[];
     if (err && __ldcg(&err->kind)) return;
     const int k = find_level(J, blockIdx.x);
     const FftLevel& lv = J.lv[k];
     const int M0 = lv.ax[0].M, M1 = lv.ax[1].M, M2 = lv.ax[2].M;
-    const int zlim = mode == 2 ? M2 : lv.d[2], ylim = mode == 2 ? M1 : lv.d[1];
+    const int zlim = mode == 2 ? M2 : lv.d[2];
     const int b = blockIdx.x - lv.blk0;
     const int nzt = (zlim + J.L - 1) / J.L;
     const int y = b / nzt, z0 = (b % nzt) * J.L;
@@ -127,25 +132,64 @@ __global__ void __launch_bounds__(256) k_fft_x(FftJobs J, int mode, const ErrRec
     double2* A = sm;
     double2* Bf = sm + J.L * J.maxM;
     double2* buf = J.buf + lv.boff;
-    for (int t = threadIdx.x; t < L * M0; t += blockDim.x) {
-        const int x = t / L, l = t - x * L, z = z0 + l;
-        double2 v = make_double2(0.0, 0.0);
-        if (mode == 0) {
-            if (x < lv.d[0]) v.x = lv.q[(size_t(x) * lv.d[1] + y) * lv.d[2] + z];
-        } else {
-            v = buf[(size_t(x) * M1 + y) * M2 + z];
+    if (mode == 2) {
+        for (int t = threadIdx.x; t < L * M0; t += blockDim.x) {
+            const int x = t / L, l = t - x * L, z = z0 + l;
+            A[l * M0 + x] = buf[(size_t(x) * M1 + y) * M2 + z];
         }
-        A[l * M0 + x] = v;
-    }
-    __syncthreads();
-    const double2* R = fft_lines(A, Bf, L, lv.ax[0], J.tw, mode == 1);
-    for (int t = threadIdx.x; t < L * M0; t += blockDim.x) {
-        const int x = t / L, l = t - x * L, z = z0 + l;
-        if (mode == 1) {
-            if (x < lv.d[0]) lv.u[(size_t(x) * lv.d[1] + y) * lv.d[2] + z] = R[l * M0 + x].x;
-        } else {
+        __syncthreads();
+        const double2* R = fft_lines(A, Bf, L, lv.ax[0], J.tw, false);
+        for (int t = threadIdx.x; t < L * M0; t += blockDim.x) {
+            const int x = t / L, l = t - x * L, z = z0 + l;
             buf[(size_t(x) * M1 + y) * M2 + z] = R[l * M0 + x];
         }
+        return;
+    }
+    const int H0 = M0 / 2 + 1;
+    const int Lp = (L + 1) / 2; // line pairs in this tile
+    if (mode == 0) {
+        for (int t = threadIdx.x; t < Lp * M0; t += blockDim.x) {
+            const int x = t / Lp, p = t - x * Lp, ze = z0 + 2 * p, zo = ze + 1;
+            double2 v = make_double2(0.0, 0.0);
+            if (x < lv.d[0]) {
+                const double* qr = lv.q + (size_t(x) * lv.d[1] + y) * lv.d[2];
+                v.x = qr[ze];
+                if (zo < z0 + L) v.y = qr[zo];
+            }
+            A[p * M0 + x] = v;
+        }
+        __syncthreads();
+        const double2* R = fft_lines(A, Bf, Lp, lv.ax[0], J.tw, false);
+        for (int t = threadIdx.x; t < Lp * H0; t += blockDim.x) {
+            const int kx = t / Lp, p = t - kx * Lp, ze = z0 + 2 * p, zo = ze + 1;
+            const double2 c = R[p * M0 + kx], cm = R[p * M0 + (M0 - kx) % M0];
+            buf[(size_t(kx) * M1 + y) * M2 + ze] = make_double2(0.5 * (c.x + cm.x), 0.5 * (c.y - cm.y));
+            if (zo < z0 + L) buf[(size_t(kx) * M1 + y) * M2 + zo] = make_double2(0.5 * (c.y + cm.y), 0.5 * (cm.x - c.x));
+        }
+        return;
+    }
+    // mode 1: inverse to u
+    for (int t = threadIdx.x; t < Lp * M0; t += blockDim.x) {
+        const int kx = t / Lp, p = t - kx * Lp, ze = z0 + 2 * p, zo = ze + 1;
+        const bool lo = kx < H0;
+        const int ks = lo ? kx : M0 - kx;
+        double2 e = buf[(size_t(ks) * M1 + y) * M2 + ze];
+        double2 o = zo < z0 + L ? buf[(size_t(ks) * M1 + y) * M2 + zo] : make_double2(0.0, 0.0);
+        if (!lo) { // conjugate symmetry of the spectra of real lines
+            e.y = -e.y;
+            o.y = -o.y;
+        }
+        A[p * M0 + kx] = make_double2(e.x - o.y, e.y + o.x); // E + i O
+    }
+    __syncthreads();
+    const double2* R = fft_lines(A, Bf, Lp, lv.ax[0], J.tw, true);
+    for (int t = threadIdx.x; t < Lp * M0; t += blockDim.x) {
+        const int x = t / Lp, p = t - x * Lp, ze = z0 + 2 * p, zo = ze + 1;
+        if (x >= lv.d[0]) continue;
+        double* ur = lv.u + (size_t(x) * lv.d[1] + y) * lv.d[2];
+        const double2 c = R[p * M0 + x];
+        ur[ze] = c.x;
+        if (zo < z0 + L) ur[zo] = c.y;
     }
 }
 
@@ -259,22 +303,26 @@ int blocks_x(FftJobs& J, bool all) {
     }
     return tot;
 }
+// the Y and Z passes of the convolution (modes 0 / 1) cover the x-frequencies
+// 0 .. M0/2 only (real data, see k_fft_x); the spectrum precompute covers all
 int blocks_y(FftJobs& J, bool all) {
     int tot = 0;
     for (int k = 0; k < J.n; ++k) {
         FftLevel& lv = J.lv[k];
         lv.blk0 = tot;
         const int zl = all ? lv.ax[2].M : lv.d[2];
-        tot += lv.ax[0].M * ((zl + J.L - 1) / J.L);
+        const int planes = all ? lv.ax[0].M : lv.ax[0].M / 2 + 1;
+        tot += planes * ((zl + J.L - 1) / J.L);
     }
     return tot;
 }
-int blocks_z(FftJobs& J) {
+int blocks_z(FftJobs& J, bool all) {
     int tot = 0;
     for (int k = 0; k < J.n; ++k) {
         FftLevel& lv = J.lv[k];
         lv.blk0 = tot;
-        tot += lv.ax[0].M * ((lv.ax[1].M + J.L - 1) / J.L);
+        const int planes = all ? lv.ax[0].M : lv.ax[0].M / 2 + 1;
+        tot += planes * ((lv.ax[1].M + J.L - 1) / J.L);
     }
     return tot;
 }
@@ -325,7 +373,7 @@ int launch_fft_spectrum(cudaStream_t st, FftJobs J, const FftKernel* K) {
     k_fft_x<<<nb, 256, sm, st>>>(J, 2, nullptr);
     nb = blocks_y(J, true);
     k_fft_y<<<nb, 256, sm, st>>>(J, 2, nullptr);
-    nb = blocks_z(J);
+    nb = blocks_z(J, true);
     k_fft_z<<<nb, 256, sm, st>>>(J, 2, nullptr);
     return nl + 3;
 }
@@ -337,7 +385,7 @@ int launch_lattice_fft(cudaStream_t st, FftJobs J, const ErrRec* err) {
     k_fft_x<<<nb, 256, sm, st>>>(J, 0, err);
     nb = blocks_y(J, false);
     k_fft_y<<<nb, 256, sm, st>>>(J, 0, err);
-    nb = blocks_z(J);
+    nb = blocks_z(J, false);
     k_fft_z<<<nb, 256, sm, st>>>(J, 0, err);
     nb = blocks_y(J, false);
     k_fft_y<<<nb, 256, sm, st>>>(J, 1, err);
