@@ -2342,7 +2342,9 @@ static InterpP make_interp(const Geometry& g) {
     return p;
 }
 
-// one thread per atom in cluster order (the short-range results are in that order)
+// one thread per atom in cluster order (the short-range results are in that order);
+// four lanes per atom (one x-offset each, xor-tree combine) measured slower on C2-S
+// (0.045 vs 0.033 ms: the weights are recomputed by every lane)
 #ifndef MSMB_INTERP_MINB
 #define MSMB_INTERP_MINB 5
 #endif
