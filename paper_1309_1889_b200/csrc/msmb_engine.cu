@@ -870,6 +870,7 @@ int msmb_create_overlay(const msmb_field* base, double epsilon, double sigma, ms
     const int rc = field_new(base->device, out);
     if (rc) return rc;
     msmb_field* f = *out;
+    std::lock_guard<std::recursive_mutex> lk(const_cast<msmb_field*>(base)->mu); // a consistent snapshot
     f->kind = base->kind;
     f->cut = base->cut;
     f->cfg = base->cfg;
