@@ -1027,6 +1027,11 @@ __global__ void k_err_brute(int64_t n, const double* __restrict__ x, const doubl
     }
 }
 
+// The rebuild-only kernels (k_cl_perm .. k_pairmask) are launched every evaluation and
+// exit early on skin steps.  Skipping them inside the captured graphs with IF
+// conditional nodes (cudaGraphSetConditional from the flag) was tried: adding the
+// conditional node to the capturing graph returned cudaErrorInvalidValue on this
+// driver/runtime, so the early-exit launches stay.
 int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
                     DevCells& c, ErrRec* err, int cap, const Part& P, int force_rebuild) {
     const int cells_per_col = int(g.lv[0].dims[2]) * g.cw * g.cw;
