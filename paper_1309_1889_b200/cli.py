@@ -21,7 +21,7 @@ import sys
 
 import numpy as np
 
-from . import (ConfigError, CoverageError, CutoffParams, DeviceSystem, DirectCoulombField, Error,
+from . import (ConfigError, CutoffParams, DeviceSystem, DirectCoulombField,
                MsmConfig, MsmField, NonConvergenceError, PairRepulsionOverlay, ParticleSystem,
                PararealConfig, PropagatorSpec, RuntimeFault, SimpleCutoffField, UnitsConfig, WolfField,
                energy_report)

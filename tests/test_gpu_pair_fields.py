@@ -7,7 +7,6 @@ import numpy as np
 import pytest
 
 from conftest import golden, rel_e, rel_rms
-import oracle_lib
 from oracle_lib import fspec
 import paper_1309_1889_b200 as pkg
 from paper_1309_1889_b200 import fixtures as fx

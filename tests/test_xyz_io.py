@@ -8,7 +8,6 @@ import pytest
 
 import paper_1309_1889_b200 as pkg
 from paper_1309_1889_b200 import xyz_io
-import oracle_lib
 
 _D = C.POINTER(C.c_double)
 
