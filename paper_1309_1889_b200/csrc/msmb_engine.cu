@@ -243,6 +243,11 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
     a.zc = walloc<double>(*W, N);
     a.qc = walloc<double>(*W, N);
     a.ref = walloc<double>(*W, 3 * N);
+    {
+        const int64_t maxclu_est = n / 32 + g.ncols + 1; // as launch_pairs
+        const int sp = pair_split(maxclu_est);
+        a.pair_part = sp > 1 ? walloc<double>(*W, size_t(sp) * 4 * N) : nullptr;
+    }
     DevCells& c = W->c;
     c.count = walloc<int>(*W, size_t(g.ncells + 1));
     c.start = walloc<int>(*W, size_t(g.ncells + 1));

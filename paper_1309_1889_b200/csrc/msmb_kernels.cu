@@ -872,17 +872,23 @@ __global__ void __launch_bounds__(kMaskWarps * 32)
 // (FP64 pipe 53%, issue 62-67%, stalls spread over wait / math throttle /
 // long scoreboard of the staging loads); two staged clusters in flight (register
 // double buffer) 0.647 vs 0.632.
-template <int K>
+template <int K, bool SPLIT>
 __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     k_pairs_mw(const int2* __restrict__ clu, const int* __restrict__ plist, const int* __restrict__ pcnt,
                const unsigned* __restrict__ pmask, int cap, const double* __restrict__ xs,
                const double* __restrict__ ys, const double* __restrict__ zs, const double* __restrict__ qs,
                PairP p, double a2, double* phis, double* fsx, double* fsy, double* fsz,
-               const int* __restrict__ col_off, int col_a, int col_b, int64_t n, ErrRec* err) {
+               const int* __restrict__ col_off, int col_a, int col_b, int64_t n, ErrRec* err,
+               int split_arg, double* __restrict__ part) {
+    const int split = SPLIT ? split_arg : 1; // compile-time 1 on the large-system path
     __shared__ unsigned s_mask[kPairWarps][kRing][32];
     __shared__ double2 s_v[kPairWarps][2][kRing * kSlots]; // (x, y), (z, q) rows
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ic = col_off[col_a] + blockIdx.x * kPairWarps + w;
+    // split > 1 (small systems): `split` warps share an i-cluster, each walking a
+    // contiguous part of its list; their raw sums go to `part` and k_pairs_join adds
+    // them in part order (deterministic)
+    const int gw = blockIdx.x * kPairWarps + w;
+    const int ic = col_off[col_a] + (SPLIT ? gw / split : gw), sp = SPLIT ? gw % split : 0;
     if (ic >= col_off[col_b] || failed(err)) return;
     const int2 c = clu[ic];
     const bool vi = lane < c.y;
@@ -892,9 +898,11 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         s_v[w][s & 1][(s >> 1) * kSlots] = (s & 1) ? make_double2(1e4, 0.0) : make_double2(1e4, 1e4);
     double ph = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
     unsigned ncand = 0, npair = 0;
-    const int nj = pcnt[ic];
-    const int* pl = plist + size_t(ic) * cap;
-    const unsigned* pm = pmask + size_t(ic) * cap * 32 + lane;
+    const int nj_all = pcnt[ic];
+    const int jb = SPLIT ? int(int64_t(nj_all) * sp / split) : 0;
+    const int nj = SPLIT ? int(int64_t(nj_all) * (sp + 1) / split) - jb : nj_all;
+    const int* pl = plist + size_t(ic) * cap + jb;
+    const unsigned* pm = pmask + (size_t(ic) * cap + jb) * 32 + lane;
     unsigned mk_n = 0;
     double xj_n = 0, yj_n = 0, zj_n = 0, qj_n = 0;
     auto fetch = [&](int jj) {
@@ -951,9 +959,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         fz = fma(dz, wgt, fz);
     };
     if (nj > 0) fetch(0);
-    ncand += vi ? unsigned(c.y - 1) : 0u;
+    ncand += (vi && sp == 0) ? unsigned(c.y - 1) : 0u;
     // the own cluster (dropped from the mask list): all atom pairs, j broadcast by shuffles
-    for (int t = 0; t < c.y; ++t) {
+    for (int t = 0; t < (sp == 0 ? c.y : 0); ++t) {
         const double xj = __shfl_sync(FULLMASK, xi, t), yj = __shfl_sync(FULLMASK, yi, t);
         const double zj = __shfl_sync(FULLMASK, zi, t), qt = __shfl_sync(FULLMASK, qi, t);
         const double dx = xi - xj, dy = yi - yj, dz = zi - zj;
@@ -991,7 +999,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
             if (hi >= nj && __all_sync(FULLMASK, m == 0 && cur + 1 >= hi)) break;
         }
     }
-    if (vi) {
+    if (SPLIT && vi) {
+        double* o = part + (size_t(sp) * 4) * size_t(n) + si;
+        o[0] = ph;
+        o[size_t(n)] = fx;
+        o[2 * size_t(n)] = fy;
+        o[3 * size_t(n)] = fz;
+    } else if (vi) {
         const double kq = -p.kc * qi; // f = d * (-k_C q_i q_j g*'/r)  (msm_phases.cpp:246)
         phis[si] = ph;
         fsx[si] = fx * kq;
@@ -1085,6 +1099,30 @@ int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevStat
     return l + 3;
 }
 
+// sums of the split pair walks, in part order, then the per-atom force factor
+__global__ void k_pairs_join(const int* __restrict__ colstart, int col_a, int col_b, int split, int64_t n,
+                             const double* __restrict__ part, const double* __restrict__ qs, double kc,
+                             double* phis, double* fsx, double* fsy, double* fsz, const ErrRec* err) {
+    const int s = colstart[col_a] + blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= colstart[col_b] || failed(err)) return;
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k = 0; k < split; ++k)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[c] += part[(size_t(k) * 4 + c) * size_t(n) + s];
+    const double kq = -kc * qs[s];
+    phis[s] = v[0];
+    fsx[s] = v[1] * kq;
+    fsy[s] = v[2] * kq;
+    fsz[s] = v[3] * kq;
+}
+
+// warps per i-cluster: enough warps for ~5 resident blocks on every SM
+int pair_split(int64_t maxclu) {
+    const int64_t want = 148 * 5 * kPairWarps;
+    int64_t sp = (want + std::max<int64_t>(maxclu, 1) - 1) / std::max<int64_t>(maxclu, 1);
+    return int(std::min<int64_t>(std::max<int64_t>(sp, 1), kPairSplitMax));
+}
+
 int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
                  DevCells& c, ErrRec* err, int cap, const Part& P) {
     const double A = g.cfg.cutoff_a;
@@ -1109,13 +1147,23 @@ int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& 
     const int64_t maxclu = n / 32 + g.ncols + 1;
     int l = 0;
     if (n > 0) {
-        auto kern = g.kind == MSMB_FIELD_CUTOFF ? k_pairs_mw<MSMB_FIELD_CUTOFF>
-                    : g.kind == MSMB_FIELD_WOLF ? k_pairs_mw<MSMB_FIELD_WOLF>
-                                                : k_pairs_mw<MSMB_FIELD_MSM>;
-        kern<<<int((maxclu + kPairWarps - 1) / kPairWarps), kPairWarps * 32, 0, st>>>(
+        const int split = a.pair_part ? pair_split(maxclu) : 1;
+        auto kern = split > 1 ? (g.kind == MSMB_FIELD_CUTOFF ? k_pairs_mw<MSMB_FIELD_CUTOFF, true>
+                                 : g.kind == MSMB_FIELD_WOLF ? k_pairs_mw<MSMB_FIELD_WOLF, true>
+                                                             : k_pairs_mw<MSMB_FIELD_MSM, true>)
+                              : (g.kind == MSMB_FIELD_CUTOFF ? k_pairs_mw<MSMB_FIELD_CUTOFF, false>
+                                 : g.kind == MSMB_FIELD_WOLF ? k_pairs_mw<MSMB_FIELD_WOLF, false>
+                                                             : k_pairs_mw<MSMB_FIELD_MSM, false>);
+        kern<<<int((maxclu * split + kPairWarps - 1) / kPairWarps), kPairWarps * 32, 0, st>>>(
             c.clu, c.plist, c.pcnt, c.pmask, cap, a.xc, a.yc, a.zc, a.qc, p, A * A, a.phis, a.fsx, a.fsy, a.fsz,
-            c.col_off, P.cx0 * g.ncy, P.cx1 * g.ncy, n, err);
+            c.col_off, P.cx0 * g.ncy, P.cx1 * g.ncy, n, err, split, a.pair_part);
         l = 1;
+        if (split > 1) {
+            k_pairs_join<<<int((n + 255) / 256), 256, 0, st>>>(c.colstart, P.cx0 * g.ncy, P.cx1 * g.ncy, split, n,
+                                                               a.pair_part, a.qc, p.kc, a.phis, a.fsx, a.fsy, a.fsz,
+                                                               err);
+            ++l;
+        }
     }
     return l;
 }

@@ -22,7 +22,10 @@ struct DevAtoms {       // sorted-order working set, capacity n
     int* cl_inv;        // [n] original index -> cluster slot (ownership tests in original order)
     double* xc; double* yc; double* zc; double* qc; // [n] positions / charges, cluster order
     double* ref;        // [3n] positions (original order) at the last rebuild
+    double* pair_part;  // [kPairSplitMax * 4 * n] split pair-walk partial sums (small systems), or null
 };
+constexpr int kPairSplitMax = 8;
+int pair_split(int64_t maxclu); // warps per i-cluster in the pair kernel
 
 struct DevCells {
     int* count;         // [ncells+1]
