@@ -51,6 +51,11 @@ cudaError_t smem_grow(const void* func, size_t bytes) {
 
 #define FULLMASK 0xffffffffu
 
+// threads per block of the per-atom kernels: small systems (C1: 8,192 atoms) get
+// 64-thread blocks so they spread over more SMs (latency-bound, not throughput-bound)
+static inline int atom_tpb(int64_t n) { return n < 148 * 1024 ? 64 : 256; }
+static inline int atom_blocks(int64_t n, int tpb) { return int((n + tpb - 1) / tpb) > 0 ? int((n + tpb - 1) / tpb) : 1; }
+
 __device__ __forceinline__ bool failed(const ErrRec* e) {
     // L2 (GPU-coherent) load: kernel boundaries order it after earlier kernels'
     // writes; a stale value inside a kernel only delays an early exit.  (A volatile
@@ -328,7 +333,7 @@ int launch_bin(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& 
     const int n = int(s.n);
     cudaMemsetAsync(c.count, 0, sizeof(int) * size_t(g.ncells + 1), st);
     if (n > 0)
-        k_bin<<<(n + 255) / 256, 256, 0, st>>>(n, s.x, s.y, s.z, make_binp(g), a.key, a.rank,
+        k_bin<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, s.x, s.y, s.z, make_binp(g), a.key, a.rank,
                                                c.count, a.outlist, err);
     return n > 0 ? 1 : 0;
 }
@@ -337,12 +342,12 @@ int launch_sort(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms&
                 ErrRec* err) {
     const int n = int(s.n);
     int l = scan_exclusive(st, c.count, c.start, c.scan_tmp, g.ncells + 1);
-    if (n > 0) k_scatter<<<(n + 255) / 256, 256, 0, st>>>(n, a.key, a.rank, c.start, a.perm, err);
+    if (n > 0) k_scatter<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, a.key, a.rank, c.start, a.perm, err);
     // always: also publishes the (possibly empty) natural-order cell ranges read by k_anterp
     k_cellsort<<<int((g.ncells + 255) / 256), 256, 0, st>>>(g.ncells, make_binp(g), c.start, a.perm,
                                                             c.nat, s.x, s.y, s.z, err);
     if (n == 0 || g.kind != MSMB_FIELD_MSM) return l + 1;
-    k_gather<<<(n + 255) / 256, 256, 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, s.q,
+    k_gather<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, s.q,
                                               make_binp(g), a.aw,
                                               err);
     return l + 3;
@@ -1055,9 +1060,10 @@ int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevStat
     const int key = P.cx0 * 65536 + P.cx1;
     k_flag_reset<<<1, 1, 0, st>>>(c.flag, force_rebuild || !(g.skin > 0.0) ? 1 : 0, key);
     const double hs = 0.5 * g.skin;
-    k_disp<<<nb, 256, 0, st>>>(n, s.x, s.y, s.z, a.ref, hs * hs, c.flag);
+    k_disp<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, s.x, s.y, s.z, a.ref, hs * hs, c.flag);
     k_cl_perm<<<nb, 256, 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, a.cl_perm, a.cl_inv, a.ref, c.flag, key);
-    k_gather_cl<<<nb, 256, 0, st>>>(c.flag, a.cl_perm, s.x, s.y, s.z, s.q, a.xc, a.yc, a.zc, a.qc, err);
+    k_gather_cl<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(c.flag, a.cl_perm, s.x, s.y, s.z, s.q, a.xc, a.yc,
+                                                                     a.zc, a.qc, err);
     // cluster pair list (rebuild evaluations only)
     k_columns<<<int((nc + 1 + 255) / 256), 256, 0, st>>>(nc, cells_per_col, c.start, c.col_cnt, c.flag, err);
     int l = 5 + scan_exclusive(st, c.col_cnt, c.col_off, c.scan_tmp, nc + 1);
@@ -2475,7 +2481,8 @@ int reduce_blocks(int64_t n) { return int((n + 4095) / 4096) > 0 ? int((n + 4095
 int launch_interp(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c,
                   DevLevels& L, DevOut& o, ErrRec* err, int want_energy, const Part& P) {
     if (n == 0) return 0;
-    k_interp<<<int((n + 127) / 128), 128, 0, st>>>(make_interp(g), c.colstart, P.cx0 * g.ncy, P.cx1 * g.ncy,
+    const int itpb = n < 148 * 512 ? 64 : 128;
+    k_interp<<<atom_blocks(n, itpb), itpb, 0, st>>>(make_interp(g), c.colstart, P.cx0 * g.ncy, P.cx1 * g.ncy,
                                                    a.cl_perm, a.xc, a.yc, a.zc, a.qc, L.pot + g.lv[0].offset, a.phis,
                                                    a.fsx, a.fsy, a.fsz, o, err);
     if (!want_energy) return 1;
@@ -2624,7 +2631,7 @@ __global__ void k_kick(int64_t n, double* vx, double* vy, double* vz, const doub
 int launch_kick_drift(cudaStream_t st, DevState& s, const DevOut& o, double dt, double conv,
                       int kicks, ErrRec* err) {
     const double hdc = 0.5 * dt * conv; // (0.5*dt)*conv, host IEEE, same as the reference
-    k_kick_drift<<<int((s.n + 255) / 256) > 0 ? int((s.n + 255) / 256) : 1, 256, 0, st>>>(
+    k_kick_drift<<<atom_blocks(s.n, atom_tpb(s.n)), atom_tpb(s.n), 0, st>>>(
         s.n, s.x, s.y, s.z, s.vx, s.vy, s.vz, s.m, o.fx, o.fy, o.fz, dt, hdc, kicks, err);
     return 1;
 }
@@ -2633,7 +2640,7 @@ int launch_kick(cudaStream_t st, DevState& s, const DevOut& o, double dt, double
                 ErrRec* err) {
     if (s.n == 0) return 0;
     const double hdc = 0.5 * dt * conv;
-    k_kick<<<int((s.n + 255) / 256), 256, 0, st>>>(s.n, s.vx, s.vy, s.vz, s.m, o.fx, o.fy, o.fz, hdc,
+    k_kick<<<atom_blocks(s.n, atom_tpb(s.n)), atom_tpb(s.n), 0, st>>>(s.n, s.vx, s.vy, s.vz, s.m, o.fx, o.fy, o.fz, hdc,
                                                    err);
     return 1;
 }
