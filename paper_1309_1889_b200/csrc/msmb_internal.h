@@ -11,7 +11,13 @@
 namespace msmb {
 
 constexpr int kMaxLevels = 16;
-constexpr int kPairWarps = 4;      // warps per CTA in the pair kernels
+// pair kernel CTA shape: one warp per CTA, up to 20 CTAs per SM (C2-S: 0.922 vs 0.929
+// ms/step with 4 warps x 5 CTAs; 2 x 10 equal) -- finer-grained scheduling of the
+// uneven per-cluster walks
+#ifndef MSMB_PAIR_WARPS
+#define MSMB_PAIR_WARPS 1
+#endif
+constexpr int kPairWarps = MSMB_PAIR_WARPS; // warps per CTA in the pair kernels
 constexpr int kConvB = 16;         // outputs per thread along z in the stencil kernel
 constexpr int kConvL = 8;          // taps per chunk in the stencil kernel
 constexpr int kConvNWZ = 2;        // warps along z per stencil CTA

@@ -696,7 +696,7 @@ __device__ __forceinline__ void record_pair(ErrRec* err, int i, int j) {
 // screening 0.92 (screening was 36% of the instructions); masks + walk 0.64.
 constexpr int kSlots = 33;            // one ring slot: dummy + 32 atoms
 #ifndef MSMB_PAIR_MINB
-#define MSMB_PAIR_MINB 5
+#define MSMB_PAIR_MINB (20 / MSMB_PAIR_WARPS) // CTAs per SM: 20 warps (96 registers)
 #endif
 #ifndef MSMB_PAIR_RING
 #define MSMB_PAIR_RING 8
@@ -1124,7 +1124,7 @@ __global__ void k_pairs_join(const int* __restrict__ colstart, int col_a, int co
 
 // warps per i-cluster: enough warps for ~5 resident blocks on every SM
 int pair_split(int64_t maxclu) {
-    const int64_t want = 148 * 5 * kPairWarps;
+    const int64_t want = 148 * MSMB_PAIR_MINB * kPairWarps; // resident warps on 148 SMs
     int64_t sp = (want + std::max<int64_t>(maxclu, 1) - 1) / std::max<int64_t>(maxclu, 1);
     return int(std::min<int64_t>(std::max<int64_t>(sp, 1), kPairSplitMax));
 }
