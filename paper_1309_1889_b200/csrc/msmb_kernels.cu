@@ -1197,7 +1197,11 @@ constexpr int kAQ = 4; // points per thread along z
 #endif
 constexpr int64_t kAnterpStreamMin = MSMB_ANTERP_STREAM_MIN; // level-0 points above which k_anterp_stream runs
 
-__global__ void __launch_bounds__(128)
+#ifndef MSMB_ANTERP_TPB
+#define MSMB_ANTERP_TPB 64 // C2-S: 64 0.095, 128 0.096, 256 0.109 ms
+#endif
+constexpr int kAnterpTpb = MSMB_ANTERP_TPB;
+__global__ void __launch_bounds__(kAnterpTpb)
     k_anterp(BinP p, const int2* __restrict__ nat, const double* __restrict__ aw, double* q0,
              int x_begin, int x_end, const ErrRec* err) {
     if (failed(err)) return;
@@ -1443,7 +1447,7 @@ int launch_anterp(cudaStream_t st, const Geometry& g, DevAtoms& a, DevCells& c, 
     }
     const int64_t m = 16 * int64_t(P.pl1[0] - P.pl0[0]) * p.d[1] * ((p.d[2] + kAQ - 1) / kAQ);
     if (m == 0) return 0;
-    k_anterp<<<int((m + 127) / 128), 128, 0, st>>>(p, c.nat, a.aw, L.charge + g.lv[0].offset, P.pl0[0],
+    k_anterp<<<int((m + kAnterpTpb - 1) / kAnterpTpb), kAnterpTpb, 0, st>>>(p, c.nat, a.aw, L.charge + g.lv[0].offset, P.pl0[0],
                                                    P.pl1[0], err);
     return 1;
 }
