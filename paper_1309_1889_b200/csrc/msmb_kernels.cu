@@ -2407,6 +2407,9 @@ static InterpP make_interp(const Geometry& g) {
     return p;
 }
 
+#ifndef MSMB_INTERP_TPB
+#define MSMB_INTERP_TPB 64 // C2-S: 64 0.0325, 128 0.0332 ms
+#endif
 // one thread per atom in cluster order (the short-range results are in that order);
 // four lanes per atom (one x-offset each, xor-tree combine) measured slower on C2-S
 // (0.045 vs 0.033 ms: the weights are recomputed by every lane)
@@ -2485,7 +2488,7 @@ int reduce_blocks(int64_t n) { return int((n + 4095) / 4096) > 0 ? int((n + 4095
 int launch_interp(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c,
                   DevLevels& L, DevOut& o, ErrRec* err, int want_energy, const Part& P) {
     if (n == 0) return 0;
-    const int itpb = n < 148 * 512 ? 64 : 128;
+    const int itpb = n < 148 * 512 ? 64 : MSMB_INTERP_TPB;
     k_interp<<<atom_blocks(n, itpb), itpb, 0, st>>>(make_interp(g), c.colstart, P.cx0 * g.ncy, P.cx1 * g.ncy,
                                                    a.cl_perm, a.xc, a.yc, a.zc, a.qc, L.pot + g.lv[0].offset, a.phis,
                                                    a.fsx, a.fsy, a.fsz, o, err);
