@@ -53,7 +53,10 @@ cudaError_t smem_grow(const void* func, size_t bytes) {
 
 // threads per block of the per-atom kernels: small systems (C1: 8,192 atoms) get
 // 64-thread blocks so they spread over more SMs (latency-bound, not throughput-bound)
-static inline int atom_tpb(int64_t n) { return n < 148 * 1024 ? 64 : 256; }
+#ifndef MSMB_ATOM_TPB
+#define MSMB_ATOM_TPB 256
+#endif
+static inline int atom_tpb(int64_t n) { return n < 148 * 1024 ? 64 : MSMB_ATOM_TPB; }
 static inline int atom_blocks(int64_t n, int tpb) { return int((n + tpb - 1) / tpb) > 0 ? int((n + tpb - 1) / tpb) : 1; }
 
 __device__ __forceinline__ bool failed(const ErrRec* e) {
