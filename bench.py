@@ -360,7 +360,7 @@ def main():
             "roofline": {"bound": "fp64", "kernel": "k_pairs_mw (short-range pair sum, SURVEY S2)",
                          "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
                          "slot_frac": slot_frac, "traffic": traffic,
-                         "traffic_note": "DRAM bytes per launch from profiles/r01e_k_pairs_mw_full.md: mostly the "
+                         "traffic_note": "DRAM bytes per launch from profiles/r01g_k_pairs_mw_full.md: mostly the "
                                          "per-lane pair masks (k_pairmask, 128 B per list entry, read once per "
                                          "evaluation; L2-flushed between timed steps), not atom data",
                          "work_per_launch": f"{pairs_u} in-cutoff unordered pairs x {roofline.PAIR_FLOPS} flops "
