@@ -2411,7 +2411,7 @@ static InterpP make_interp(const Geometry& g) {
 }
 
 #ifndef MSMB_INTERP_TPB
-#define MSMB_INTERP_TPB 64 // C2-S: 64 0.0325, 128 0.0332 ms
+#define MSMB_INTERP_TPB 32 // C2-S: 32 0.0313, 64 0.0325, 128 0.0332 ms
 #endif
 // one thread per atom in cluster order (the short-range results are in that order);
 // four lanes per atom (one x-offset each, xor-tree combine) measured slower on C2-S
