@@ -128,7 +128,9 @@ int msmb_create_direct(const msmb_units* units, int device, msmb_field** out);
  * parameters and units; `base` itself is unchanged) plus the pair repulsion
  * U = sum_{i<j} eps (sigma/r)^12 over ALL pairs (O(N^2), as the reference):
  * forces and total energy include it, the per-particle potential stays
- * electrostatic.  name() = base name + "+rep"; cost = base cost + 30 n. */
+ * electrostatic.  name() = base name + "+rep"; cost = base cost + 30 n.  An
+ * overlay of an overlay adds both terms (innermost first), as the reference's
+ * nested decorators do. */
 int msmb_create_overlay(const msmb_field* base, double epsilon, double sigma, msmb_field** out);
 
 /* MsmField::evaluate / msm_potential(s, cfg, units)  force_field.cpp:37-39,
@@ -153,6 +155,13 @@ int msmb_propagate(msmb_field* f, int64_t n, double* pos_xyz, double* vel_xyz, c
 int msmb_propagate_ex(msmb_field* f, int64_t n, double* pos_xyz, double* vel_xyz, const double* q,
                       const double* mass, const double box[3], double dt, int steps,
                       const msmb_units* units);
+
+/* energy_report(s, ff, units)  integrate.cpp:47-55: out = [kinetic, potential,
+ * total]; the kinetic energy (system.cpp:51-55, divided by units->energy_to_native)
+ * is summed on the device by a fixed-order tree, the potential is this field's
+ * evaluation.  units == NULL means the field's own units. */
+int msmb_energy_report(msmb_field* f, int64_t n, const double* pos_xyz, const double* vel_xyz, const double* q,
+                       const double* mass, const double box[3], const msmb_units* units, double* out);
 
 /* Page-locked host memory for fast transfers (cudaHostAlloc / cudaFreeHost). */
 void* msmb_host_alloc(int64_t bytes);
@@ -223,6 +232,41 @@ int msmb_parareal_run(const msmb_parareal_config* cfg, int64_t n, const double* 
                       const double* vel_xyz, const double* q, const double* mass,
                       const double box[3], int total_points, double* traj_pos,
                       double* traj_vel, int64_t* report);
+
+/* One row of paramd::ConvergenceReport::rows (include/paramd/parareal.hpp:93-110,
+ * filled at src/parareal.cpp:208): window (1-based), point n (1..t), iteration k
+ * (0-based), the fine delta's RMS position change, and whether the point met tol. */
+typedef struct msmb_parareal_row {
+    int window;
+    int point;
+    int iteration;
+    double delta_rms;
+    int converged;
+} msmb_parareal_row;
+
+/* parareal_run(v, total_points, cfg, exec)  parareal.cpp:182-239, with the
+ * Executor (parareal.hpp:15-31, used at parareal.cpp:151) over GPUs:
+ * fine_replicas[0..n_replicas) are extra fine fields with cfg->fine.field's kind
+ * and parameters, typically one per device (msmb_create(..., device = k, ...)).
+ * The fine slices of every iteration are dealt to cfg->fine.field and the
+ * replicas as they free up (AsyncExecutor::parallel_for, parareal.cpp:16-36);
+ * every slice's end state is copied back to cfg->fine.field's device, where the
+ * state algebra and the coarse sweep run.  Results do not depend on the
+ * replicas (pure propagators): they are bitwise those of msmb_parareal_run.
+ * A failing fine slice reports the error of the lowest failing slice index, as
+ * the sequential executor would.  report has 6 entries: msmb_parareal_run's 5
+ * plus [5] = output points so far (ConvergenceReport::point_iterations size).
+ * Besides the report,
+ * `rows` receives up to rows_cap ConvergenceReport rows (*rows_written = the
+ * total, which may exceed rows_cap) and point_iterations[total_points] the
+ * iterations each output point took (ConvergenceReport::point_iterations);
+ * both are filled on success and on MSMB_ERR_NONCONVERGENCE.  Any of the
+ * output pointers may be NULL. */
+int msmb_parareal_run_ex(const msmb_parareal_config* cfg, msmb_field* const* fine_replicas, int n_replicas,
+                         int64_t n, const double* pos_xyz, const double* vel_xyz, const double* q,
+                         const double* mass, const double box[3], int total_points, double* traj_pos,
+                         double* traj_vel, int64_t* report, msmb_parareal_row* rows, int64_t rows_cap,
+                         int64_t* rows_written, int* point_iterations);
 
 /* ---- raw device states, for multi-process (one process per GPU) drivers -----
  * A "state" is 6*n doubles in device memory of the field's GPU, SoA:
@@ -312,14 +356,18 @@ int msmb_measure_fp64_peak(int device, double seconds, double* tflops);
  * convolution, 1 = direct stencil sum as the reference (src/msm_phases.cpp:93-134).
  * Both agree to rounding; the direct sum is kept for comparison and tests. */
 int msmb_set_lattice_method(msmb_field* f, int direct);
-/* Pair-list skin (A, default 0.2): the cluster pair list of a propagate call is
- * built at its first evaluation and rebuilt only once some atom moved more than
- * skin/2; the pair kernel always screens with the exact cutoff, so the results are
- * the reference's within rounding.  The summation order follows the list, so
- * forces are bit-reproducible for a given call sequence but depend on when the
- * list was built (last bits); skin = 0 rebuilds at every evaluation, making the
- * forces a pure function of the positions. */
+/* Pair-list skin (A, default 0.2): within one evaluate/propagate call the cluster
+ * pair list is built at the first evaluation and rebuilt only once some atom moved
+ * more than skin/2; the pair kernel always applies the exact cutoff, so results are
+ * the reference's within rounding.  Every call starts from a fresh list, so results
+ * are a pure, bitwise-repeatable function of the call's input.
+ * skin = 0 rebuilds at every evaluation. */
 int msmb_set_pair_skin(msmb_field* f, double skin);
+/* reuse = 1: a call whose atoms are still within skin/2 of the last list build
+ * keeps that list (saves one rebuild per call when a host loop calls evaluate /
+ * propagate step by step); the last bits of the forces then depend on the call
+ * history.  Default 0. */
+int msmb_set_list_reuse(msmb_field* f, int reuse);
 /* Kernel launches issued by this handle since creation. */
 int64_t msmb_kernel_launches(const msmb_field* f);
 

@@ -23,6 +23,7 @@
 // messages (include/paramd/errors.hpp:12-49).
 #pragma once
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -184,14 +185,42 @@ class GpuPairRepulsionOverlay final : public GpuFieldBase {
 
 namespace paramd_b200 {
 
-/// paramd::propagate (src/integrate.cpp:13-36), device-resident when the spec's
-/// field is a B200 field; any other field runs the reference's own propagate.
+/// The reference's Executor plug-in (include/paramd/parareal.hpp:15-31, used for the
+/// fine sweep at src/parareal.cpp:151) over GPUs: holds replicas of the fine field,
+/// one per device.  paramd_b200::parareal_run deals the fine slices of every
+/// iteration to the fine field and the replicas (msmb_parareal_run_ex); as a plain
+/// Executor it runs parallel_for with one std::async worker per replica, like
+/// AsyncExecutor (src/parareal.cpp:16-36).
+class GpuExecutor final : public paramd::Executor {
+  public:
+    explicit GpuExecutor(std::vector<std::shared_ptr<const paramd::GpuFieldBase>> fine_replicas)
+        : replicas_(std::move(fine_replicas)) {}
+    void parallel_for(std::size_t count, const std::function<void(std::size_t)>& fn) const override {
+        paramd::AsyncExecutor(static_cast<int>(replicas_.size() > 0 ? replicas_.size() : 1)).parallel_for(count, fn);
+    }
+    const std::vector<std::shared_ptr<const paramd::GpuFieldBase>>& replicas() const { return replicas_; }
+
+  private:
+    std::vector<std::shared_ptr<const paramd::GpuFieldBase>> replicas_;
+};
+
+namespace detail {
+inline const paramd::GpuFieldBase* gpu_field(const std::shared_ptr<const paramd::ForceField>& ff, const char* who) {
+    auto* gf = dynamic_cast<const paramd::GpuFieldBase*>(ff.get());
+    // no silent CPU fall-through: a host field handed to the device path is a wiring error
+    if (!gf) throw paramd::ConfigError(std::string(who) + ": force field is not a B200 field");
+    return gf;
+}
+}  // namespace detail
+
+/// paramd::propagate (src/integrate.cpp:13-36), device-resident.  The spec's field
+/// must be a B200 field (GpuMsmField, GpuSimpleCutoffField, ...): any other field is
+/// rejected with ConfigError (there is no CPU fallback on this path).
 inline paramd::ParticleSystem propagate(const paramd::PropagatorSpec& spec,
                                         const paramd::ParticleSystem& s,
                                         const paramd::UnitsConfig& units) {
-    auto* gf = dynamic_cast<const paramd::GpuFieldBase*>(spec.force_field.get());
-    if (!gf) return paramd::propagate(spec, s, units);
     spec.validate();
+    const paramd::GpuFieldBase* gf = detail::gpu_field(spec.force_field, "paramd_b200::propagate");
     units.validate();
     paramd::ParticleSystem out = s;
     const double box[3] = {s.box.x, s.box.y, s.box.z};
@@ -205,13 +234,19 @@ inline paramd::ParticleSystem propagate(const paramd::PropagatorSpec& spec,
     return out;
 }
 
-/// paramd::parareal_run (src/parareal.cpp:182-239) with device-resident states
-/// when both propagators use B200 fields (e.g. GpuMsmField fine, GpuSimpleCutoffField coarse).
+/// paramd::parareal_run (src/parareal.cpp:182-239) with device-resident states.
+/// Both propagators must use B200 fields (e.g. GpuMsmField fine, GpuSimpleCutoffField
+/// coarse); a GpuExecutor spreads the fine sweep over its replicas (GPUs).  The
+/// report carries the reference's rows and point_iterations.
 inline paramd::PararealResult parareal_run(const paramd::ParticleSystem& v, int total_points,
-                                           const paramd::PararealConfig& cfg) {
-    auto* F = dynamic_cast<const paramd::GpuFieldBase*>(cfg.fine.force_field.get());
-    auto* G = dynamic_cast<const paramd::GpuFieldBase*>(cfg.coarse.force_field.get());
-    if (!F || !G) return paramd::parareal_run(v, total_points, cfg);
+                                           const paramd::PararealConfig& cfg,
+                                           const paramd::Executor& exec = paramd::sequential_executor()) {
+    cfg.validate();
+    const paramd::GpuFieldBase* F = detail::gpu_field(cfg.fine.force_field, "paramd_b200::parareal_run (fine)");
+    const paramd::GpuFieldBase* G = detail::gpu_field(cfg.coarse.force_field, "paramd_b200::parareal_run (coarse)");
+    std::vector<msmb_field*> reps;
+    if (auto* ge = dynamic_cast<const GpuExecutor*>(&exec))
+        for (const auto& r : ge->replicas()) reps.push_back(r->handle());
     msmb_parareal_config c{};
     c.window_points = cfg.window_points;
     c.max_iter = cfg.max_iter;
@@ -223,24 +258,38 @@ inline paramd::PararealResult parareal_run(const paramd::ParticleSystem& v, int 
     c.skip_threshold = cfg.skip_threshold.value_or(0.0);
     c.short_circuit = cfg.short_circuit;
     const std::size_t n = v.size();
-    std::vector<double> tp(3 * n * static_cast<std::size_t>(total_points > 0 ? total_points : 1));
-    std::vector<double> tv(tp.size());
-    int64_t rep[5] = {0, 0, 0, 0, 0};
+    const std::size_t tp_n = static_cast<std::size_t>(total_points > 0 ? total_points : 1);
+    std::vector<double> tp(3 * n * tp_n), tv(tp.size());
+    int64_t rep[6] = {0, 0, 0, 0, 0, 0};
     const double box[3] = {v.box.x, v.box.y, v.box.z};
-    const int rc = msmb_parareal_run(&c, static_cast<int64_t>(n),
-                                     reinterpret_cast<const double*>(v.positions.data()),
-                                     reinterpret_cast<const double*>(v.velocities.data()),
-                                     v.charges.data(), v.masses.data(), box, total_points,
-                                     tp.data(), tv.data(), rep);
-    if (rc == MSMB_ERR_NONCONVERGENCE) {
+    // rows: at most max_iter * window_points per window, windows <= total_points
+    std::vector<msmb_parareal_row> rows(static_cast<std::size_t>(cfg.max_iter) *
+                                        static_cast<std::size_t>(cfg.window_points) * tp_n);
+    int64_t nrows = 0;
+    std::vector<int> piters(tp_n, 0);
+    const int rc = msmb_parareal_run_ex(&c, reps.data(), static_cast<int>(reps.size()), static_cast<int64_t>(n),
+                                        reinterpret_cast<const double*>(v.positions.data()),
+                                        reinterpret_cast<const double*>(v.velocities.data()),
+                                        v.charges.data(), v.masses.data(), box, total_points,
+                                        tp.data(), tv.data(), rep, rows.data(), static_cast<int64_t>(rows.size()),
+                                        &nrows, piters.data());
+    auto report = [&]() {
         paramd::ConvergenceReport r;
         r.counts.g_evals = static_cast<std::size_t>(rep[0]);
         r.counts.f_evals = static_cast<std::size_t>(rep[1]);
         r.counts.f_skipped = static_cast<std::size_t>(rep[2]);
         r.windows = static_cast<int>(rep[3]);
+        r.converged = rep[4] != 0;
+        for (int64_t i = 0; i < nrows && i < static_cast<int64_t>(rows.size()); ++i)
+            r.rows.push_back({rows[i].window, rows[i].point, rows[i].iteration, rows[i].delta_rms,
+                              rows[i].converged != 0});
+        r.point_iterations.assign(piters.begin(), piters.begin() + static_cast<std::ptrdiff_t>(rep[5]));
+        return r;
+    };
+    if (rc == MSMB_ERR_NONCONVERGENCE) {
         char msg[512] = {0};
         msmb_last_error(F->handle(), nullptr, nullptr, nullptr, nullptr, msg, sizeof msg);
-        throw paramd::NonConvergenceError(msg, r);
+        throw paramd::NonConvergenceError(msg, report());
     }
     if (rc) paramd::detail_b200::rethrow(F->handle(), rc);
     paramd::PararealResult out;
@@ -250,11 +299,7 @@ inline paramd::PararealResult parareal_run(const paramd::ParticleSystem& v, int 
         std::memcpy(st.velocities.data(), tv.data() + 3 * n * k, 3 * n * sizeof(double));
         out.trajectory.push_back(std::move(st));
     }
-    out.report.counts.g_evals = static_cast<std::size_t>(rep[0]);
-    out.report.counts.f_evals = static_cast<std::size_t>(rep[1]);
-    out.report.counts.f_skipped = static_cast<std::size_t>(rep[2]);
-    out.report.windows = static_cast<int>(rep[3]);
-    out.report.converged = rep[4] != 0;
+    out.report = report();
     return out;
 }
 

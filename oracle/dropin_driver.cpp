@@ -115,6 +115,39 @@ int main() {
         std::fprintf(stderr, "parareal: %s\n", e.what());
     }
 
+    // 4b. GpuExecutor: the fine sweep over fine replicas (one per GPU; device k % ndev),
+    // bitwise equal to the single-field run; the report rows / point_iterations equal
+    // the reference's ConvergenceReport
+    double dx_exec = -1;
+    int rows_ok = 0, fallback_rejected = 0;
+    try {
+        const int ndev = msmb_device_count();
+        std::vector<std::shared_ptr<const GpuFieldBase>> reps;
+        for (int k = 1; k <= 2; ++k) reps.push_back(std::make_shared<GpuMsmField>(fcfg, units, k % ndev));
+        paramd_b200::GpuExecutor gx(reps);
+        PararealResult rr = parareal_run(s, 6, cr, sequential_executor());
+        PararealResult r1 = paramd_b200::parareal_run(s, 6, cg);
+        PararealResult rx = paramd_b200::parareal_run(s, 6, cg, gx);
+        dx_exec = 0;
+        for (int k = 0; k < 6; ++k)
+            dx_exec = std::max(dx_exec, rel_rms(rx.trajectory[k].positions, r1.trajectory[k].positions));
+        rows_ok = rr.report.rows.size() == rx.report.rows.size() &&
+                  rr.report.point_iterations == rx.report.point_iterations && rr.report.windows == rx.report.windows;
+        for (std::size_t i = 0; rows_ok && i < rr.report.rows.size(); ++i) {
+            const auto &a0 = rr.report.rows[i], &b0 = rx.report.rows[i];
+            rows_ok = a0.window == b0.window && a0.point == b0.point && a0.iteration == b0.iteration &&
+                      a0.converged == b0.converged &&
+                      std::fabs(a0.delta_rms - b0.delta_rms) <= 1e-6 * std::fabs(a0.delta_rms) + 1e-300;
+        }
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "gpu executor: %s\n", e.what());
+    }
+    try { // a host field on the device path is an error, not a silent CPU run
+        paramd_b200::propagate(sr, s, units);
+    } catch (const ConfigError&) {
+        fallback_rejected = 1;
+    }
+
     // 5. errors through the plugin
     ParticleSystem bad = s;
     bad.positions[100] = bad.positions[7];
@@ -180,7 +213,8 @@ int main() {
         ap_df = std::max(ap_df, rel_rms(y.per_particle_force, x.per_particle_force));
         if (r0.name() != g0.name() || r0.cost_flops_per_step(2048) != g0.cost_flops_per_step(2048)) ap_de = 1.0;
     }
-    std::printf("{\"ap_de\": %.3e, \"ap_df\": %.3e, ", ap_de, ap_df);
+    std::printf("{\"ap_de\": %.3e, \"ap_df\": %.3e, \"dx_executor\": %.3e, \"rows_ok\": %d, "
+                "\"fallback_rejected\": %d, ", ap_de, ap_df, dx_exec, rows_ok, fallback_rejected);
     std::printf(
         "\"pf_de\": %.3e, \"pf_df\": %.3e, \"pf_dx_plugin_propagate\": %.3e, \"pf_dx_device_propagate\": %.3e, "
         "\"pf_dx_parareal_device\": %.3e, ",

@@ -564,14 +564,15 @@ def energy_report(s: ParticleSystem, ff: ForceField, units: UnitsConfig = None) 
     """paramd::energy_report (src/integrate.cpp:47-55)."""
     units = units or UnitsConfig.physical()
     units.validate()
-    ke = 0.0
-    for i in range(s.size()):  # kinetic_energy, src/system.cpp:51-55 (index order)
-        v = s.velocities[i]
-        ke += 0.5 * s.masses[i] * (v[0] * v[0] + v[1] * v[1] + v[2] * v[2])
+    if not isinstance(ff, GpuField):
+        raise ConfigError("energy_report: force field is not a B200 field")
+    out = np.zeros(3)
+    u = units._c()
+    rc = _native.lib().msmb_energy_report(ff.handle, s.size(), _p(s.positions), _p(s.velocities), _p(s.charges),
+                                          _p(s.masses), _p(s.box), C.byref(u), _p(out))
+    _check(ff.handle, rc)
     rep = EnergyReport()
-    rep.kinetic = ke / units.energy_to_native
-    rep.potential = ff.evaluate(s).total_energy
-    rep.total = rep.kinetic + rep.potential
+    rep.kinetic, rep.potential, rep.total = float(out[0]), float(out[1]), float(out[2])
     return rep
 
 
@@ -585,6 +586,17 @@ class SequentialExecutor:
 class AsyncExecutor(SequentialExecutor):
     def __init__(self, threads: int = 1):
         self.threads = threads
+
+
+class GpuExecutor(SequentialExecutor):
+    """The Executor plug-in (parareal.hpp:15-31, used at parareal.cpp:151) over GPUs:
+    replicas of the fine field, typically one per device.  parareal_run deals the
+    fine slices of every iteration to the fine field and the replicas
+    (msmb_parareal_run_ex), like AsyncExecutor::parallel_for (parareal.cpp:16-36).
+    Results are bitwise those of a single fine field."""
+
+    def __init__(self, fine_replicas):
+        self.fine_replicas = list(fine_replicas)
 
 
 @dataclass
@@ -614,6 +626,15 @@ class PararealResult:
     counts: dict
     windows: int
     converged: bool
+    # ConvergenceReport::rows (window, point, iteration, delta_rms, converged) and
+    # ::point_iterations (parareal.hpp:108-122)
+    report_rows: list = field(default_factory=list)
+    point_iterations: list = field(default_factory=list)
+
+
+class _RowC(C.Structure):
+    _fields_ = [("window", C.c_int), ("point", C.c_int), ("iteration", C.c_int), ("delta_rms", C.c_double),
+                ("converged", C.c_int)]
 
 
 def _cfg_handle(cfg):
@@ -640,16 +661,30 @@ def parareal_window(v: ParticleSystem, cfg: PararealConfig, t_points: int, k_ite
 
 
 def parareal_run(v: ParticleSystem, total_points: int, cfg: PararealConfig, exec=None) -> PararealResult:
-    """paramd::parareal_run (src/parareal.cpp:182-239)."""
+    """paramd::parareal_run (src/parareal.cpp:182-239).  exec = GpuExecutor([...])
+    spreads the fine sweep over fine-field replicas (GPUs)."""
     n = v.size()
     tp = np.zeros((max(total_points, 1), n, 3))
     tv = np.zeros((max(total_points, 1), n, 3))
-    rep = np.zeros(5, dtype=np.int64)
+    rep = np.zeros(6, dtype=np.int64)
     c = cfg._c()
-    rc = _native.lib().msmb_parareal_run(C.byref(c), n, _p(v.positions), _p(v.velocities), _p(v.charges),
-                                         _p(v.masses), _p(v.box), total_points, _p(tp), _p(tv),
-                                         rep.ctypes.data_as(C.POINTER(C.c_int64)))
-    _check(_cfg_handle(cfg), rc)
+    reps = [r.handle for r in getattr(exec, "fine_replicas", [])]
+    rarr = (C.c_void_p * max(len(reps), 1))(*reps)
+    cap = max(1, cfg.max_iter * cfg.window_points * max(total_points, 1))
+    rows = (_RowC * cap)()
+    nrows = C.c_int64(0)
+    piters = np.zeros(max(total_points, 1), dtype=np.int32)
+    rc = _native.lib().msmb_parareal_run_ex(C.byref(c), rarr, len(reps), n, _p(v.positions), _p(v.velocities),
+                                            _p(v.charges), _p(v.masses), _p(v.box), total_points, _p(tp), _p(tv),
+                                            rep.ctypes.data_as(C.POINTER(C.c_int64)), C.cast(rows, C.c_void_p),
+                                            cap, C.byref(nrows), piters.ctypes.data_as(C.POINTER(C.c_int32)))
+    report_rows = [(r.window, r.point, r.iteration, r.delta_rms, bool(r.converged))
+                   for r in rows[:min(nrows.value, cap)]]
+    counts = dict(g_evals=int(rep[0]), f_evals=int(rep[1]), f_skipped=int(rep[2]))
+    try:
+        _check(_cfg_handle(cfg), rc)
+    except NonConvergenceError as e:
+        e.report = PararealResult([], counts, int(rep[3]), False, report_rows, [int(x) for x in piters[:rep[5]]])
+        raise
     traj = [ParticleSystem(tp[i], tv[i], v.charges, v.masses, v.box) for i in range(total_points)]
-    return PararealResult(traj, dict(g_evals=int(rep[0]), f_evals=int(rep[1]), f_skipped=int(rep[2])),
-                          int(rep[3]), bool(rep[4]))
+    return PararealResult(traj, counts, int(rep[3]), bool(rep[4]), report_rows, [int(x) for x in piters[:rep[5]]])

@@ -59,6 +59,7 @@ SIGNATURES = {
     "msmb_propagate": (C.c_int, [_VP, C.c_int64, _D, _D, _D, _D, _D, C.c_double, C.c_int]),
     "msmb_propagate_ex": (C.c_int, [_VP, C.c_int64, _D, _D, _D, _D, _D, C.c_double, C.c_int,
                                     C.POINTER(UnitsC)]),
+    "msmb_energy_report": (C.c_int, [_VP, C.c_int64, _D, _D, _D, _D, _D, C.POINTER(UnitsC), _D]),
     "msmb_host_alloc": (_VP, [C.c_int64]),
     "msmb_host_free": (None, [_VP]),
     "msmb_cost_flops_per_step": (C.c_double, [_VP, C.c_int64]),
@@ -71,6 +72,7 @@ SIGNATURES = {
     "msmb_system_propagate_ex": (C.c_int, [_VP, _VP, C.c_double, C.c_int, C.POINTER(UnitsC)]),
     "msmb_set_lattice_method": (C.c_int, [_VP, C.c_int]),
     "msmb_set_pair_skin": (C.c_int, [_VP, C.c_double]),
+    "msmb_set_list_reuse": (C.c_int, [_VP, C.c_int]),
     "msmb_dd_plan": (C.c_int, [C.POINTER(MsmConfigC), C.POINTER(UnitsC), _D, C.c_int64, C.c_int, C.c_int, _I,
                               C.c_int]),
     "msmb_dd_set_part": (C.c_int, [_VP, C.c_int, C.c_int]),
@@ -88,6 +90,8 @@ SIGNATURES = {
                                        C.c_int, _D, _D, _D, _L]),
     "msmb_parareal_run": (C.c_int, [C.POINTER(PararealC), C.c_int64, _D, _D, _D, _D, _D, C.c_int,
                                     _D, _D, _L]),
+    "msmb_parareal_run_ex": (C.c_int, [C.POINTER(PararealC), C.POINTER(_VP), C.c_int, C.c_int64, _D, _D, _D, _D,
+                                       _D, C.c_int, _D, _D, _L, _VP, C.c_int64, _L, _I]),
     "msmb_set_stage_timing": (C.c_int, [_VP, C.c_int]),
     "msmb_stage_times": (C.c_int, [_VP, _D, _L, C.POINTER(C.c_char_p), C.c_int]),
     "msmb_reset_stage_times": (None, [_VP]),

@@ -206,6 +206,13 @@ extern "C" int msmb_set_pair_skin(msmb_field* f, double skin) {
     return MSMB_OK;
 }
 
+extern "C" int msmb_set_list_reuse(msmb_field* f, int reuse) {
+    if (!f) return MSMB_ERR_CONFIG;
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    f->list_reuse = reuse ? 1 : 0;
+    return MSMB_OK;
+}
+
 extern "C" int msmb_set_lattice_method(msmb_field* f, int direct) {
     if (!f) return MSMB_ERR_CONFIG;
     std::lock_guard<std::recursive_mutex> lk(f->mu);

@@ -151,12 +151,20 @@ static T* wupload(Workspace& W, const std::vector<T>& v) {
     return p;
 }
 
+// Both new buffers are allocated before the old ones are released and swapped in
+// only when both succeeded, so a failed growth leaves the workspace consistent
+// (old capacity, old pointers, graphs still valid).
 static void alloc_plist(Workspace& W, int cap) {
-    W.cap = cap;
-    ck(W.plist_buf.alloc(sizeof(int) * size_t(W.maxclu) * size_t(cap)), "cudaMalloc plist");
+    DBuf pl, pm;
+    ck(pl.alloc(sizeof(int) * size_t(W.maxclu) * size_t(cap)), "cudaMalloc plist");
+    ck(pm.alloc(sizeof(unsigned) * 32 * size_t(W.maxclu) * size_t(cap)), "cudaMalloc pmask");
+    std::swap(W.plist_buf.p, pl.p);
+    std::swap(W.plist_buf.bytes, pl.bytes);
+    std::swap(W.pmask_buf.p, pm.p);
+    std::swap(W.pmask_buf.bytes, pm.bytes);
     W.c.plist = W.plist_buf.as<int>();
-    ck(W.pmask_buf.alloc(sizeof(unsigned) * 32 * size_t(W.maxclu) * size_t(cap)), "cudaMalloc pmask");
     W.c.pmask = W.pmask_buf.as<unsigned>();
+    W.cap = cap;
 }
 
 static std::atomic<uint64_t> g_ws_uid{1};
@@ -459,25 +467,30 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, 
     };
     // PairRepulsionOverlay (force_field.cpp:45-68): after the base field's outputs,
     // all-pairs repulsion forces added to F, its energy added to the total
-    auto overlay = [&](DevOut& o) {
-        if (!f->rep_on) return;
-        run("overlay", [&] {
-            int nl = launch_allpairs(st, s, g.units.coulomb_constant, 0, 1, f->rep_eps, f->rep_sigma, W.ap, o, W.err);
-            if (o.e) nl += launch_energy_sum(st, s.n, W.ap.e_rep, o.partial, 1.0, o.energy, 1, W.err);
-            return nl;
-        });
+    // Nested overlays compose like the reference's decorators: the innermost term is
+    // added first (each PairRepulsionOverlay::evaluate adds its term to its base's result).
+    auto overlay = [&](DevOut& o, size_t first) {
+        for (size_t t = first; t < f->rep.size(); ++t)
+            run("overlay", [&] {
+                int nl = launch_allpairs(st, s, g.units.coulomb_constant, 0, 1, f->rep[t].first, f->rep[t].second,
+                                         W.ap, o, W.err);
+                if (o.e) nl += launch_energy_sum(st, s.n, W.ap.e_rep, o.partial, 1.0, o.energy, 1, W.err);
+                return nl;
+            });
     };
     if (g.kind == MSMB_FIELD_DIRECT) { // direct_coulomb (electrostatics.cpp:43-64): all pairs
         DevOut o = W.o;
         if (!outputs) o.phi = o.phis = o.phil = o.e = nullptr;
         run("pairs", [&] {
-            int nl = launch_allpairs(st, s, g.units.coulomb_constant, 1, f->rep_on, f->rep_eps, f->rep_sigma, W.ap,
-                                     o, W.err);
+            const bool rep1 = !f->rep.empty(); // the innermost overlay is fused into the direct sum
+            int nl = launch_allpairs(st, s, g.units.coulomb_constant, 1, rep1 ? 1 : 0, rep1 ? f->rep[0].first : 0.0,
+                                     rep1 ? f->rep[0].second : 1.0, W.ap, o, W.err);
             if (o.e) nl += launch_energy_sum(st, s.n, o.e, o.partial, g.units.coulomb_constant, o.energy, 0, W.err);
-            if (o.e && f->rep_on)
+            if (o.e && rep1)
                 nl += launch_energy_sum(st, s.n, W.ap.e_rep, o.partial, 1.0, o.energy, 1, W.err);
             return nl;
         });
+        overlay(o, 1);
         run("finalize", [&] { return launch_finalize(st, s, W.err, 1); });
         return total;
     }
@@ -490,7 +503,7 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, 
         DevOut o = W.o;
         if (!outputs) o.phi = o.phis = o.phil = o.e = nullptr;
         run("interp", [&] { return launch_pair_out(st, g, s.n, W.a, W.c, o, W.err, outputs ? 1 : 0, W.whole); });
-        overlay(o);
+        overlay(o, 0);
         run("finalize", [&] { return launch_finalize(st, s, W.err, 1); });
         return total;
     }
@@ -524,7 +537,7 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, 
     DevOut o = W.o;
     if (!outputs) o.phi = o.phis = o.phil = o.e = nullptr;
     run("interp", [&] { return launch_interp(st, g, s.n, W.a, W.c, W.L, o, W.err, outputs ? 1 : 0, W.whole); });
-    overlay(o);
+    overlay(o, 0);
     run("finalize", [&] { return launch_finalize(st, s, W.err); });
     if (g_exp_stamps) launch_stamp(st, 6);
     return total;
@@ -560,12 +573,23 @@ void grow_cap(Workspace& W, const ErrRec& r) {
     ck(cudaDeviceSynchronize(), "sync");
 }
 
+// Every evaluate / propagate call starts from a freshly built pair list, so its
+// results are a pure function of its input (the reference's evaluate is pure and
+// bitwise repeatable): the summation order follows the list, and a
+// list carried over from an earlier call would make the last bits depend on the
+// call history -- e.g. on which parareal rank or fine replica ran a slice.
+// msmb_set_list_reuse(f, 1) opts into carrying the list across calls.
+static void fresh_list(msmb_field* f, Workspace& W) {
+    if (!f->list_reuse && W.c.flag) ck(cudaMemsetAsync(W.c.flag + 3, 0, sizeof(int), f->stream), "memset");
+}
+
 // Evaluate the system in `s` (device), outputs left in W.o.
 static int eval_device(msmb_field* f, StateBuf& sb, bool outputs) {
     Error e = ensure_workspace(f, sb.n, sb.box);
     if (e.kind) return engine_set_error(f, e);
     Workspace& W = *f->ws;
     DevState s = sb.dev();
+    fresh_list(f, W);
     for (int attempt = 0; attempt < 8; ++attempt) {
         ensure_const_table(f, W);
         f->launches += launch_reset_err(f->stream, W.err, 0);
@@ -598,7 +622,7 @@ static cudaGraphExec_t capture(msmb_field* f, Fn&& fn);
 // pair-list capacity): evaluation, first step (kick + drift + evaluation), and
 // later steps (fused kick + kick + drift + evaluation).
 static void ensure_graphs(msmb_field* f, Workspace& W, DevState& s, double dt, double conv) {
-    if (W.graph_key == s.x && W.graph_dt == dt && W.graph_cap == W.cap) return;
+    if (W.graph_key == s.x && W.graph_dt == dt && W.graph_conv == conv && W.graph_cap == W.cap) return;
     destroy_graphs(W);
     int nl = 0;
     W.gx_eval = capture(f, [&] { nl = enqueue_eval(f, W, s, false); });
@@ -615,6 +639,7 @@ static void ensure_graphs(msmb_field* f, Workspace& W, DevState& s, double dt, d
     f->launches -= 3 * int64_t(W.launches_eval); // captures are not launches
     W.graph_key = s.x;
     W.graph_dt = dt;
+    W.graph_conv = conv;
     W.graph_cap = W.cap;
 }
 
@@ -652,6 +677,7 @@ int engine_propagate(msmb_field* f, StateBuf& sb, double dt, int steps, double c
     double* bk = W.backup.as<double>();
     // keep the input state: restored on error and on pair-list retries
     ck(cudaMemcpyAsync(bk, s.x, sizeof(double) * 6 * N, cudaMemcpyDeviceToDevice, f->stream), "backup");
+    fresh_list(f, W);
     for (int attempt = 0; attempt < 8; ++attempt) {
         ensure_const_table(f, W);
         const bool graphs = !f->timer.on;
@@ -882,9 +908,9 @@ int msmb_create_overlay(const msmb_field* base, double epsilon, double sigma, ms
     f->units = base->units;
     f->lattice_direct = base->lattice_direct;
     f->pair_skin = base->pair_skin;
+    f->rep = base->rep; // nested overlays add their terms (force_field.cpp:45-68)
+    f->rep.emplace_back(epsilon, sigma);
     f->rep_on = 1;
-    f->rep_eps = epsilon;
-    f->rep_sigma = sigma;
     return MSMB_OK;
 }
 
@@ -976,7 +1002,7 @@ int msmb_last_error(const msmb_field* f, int* kind, int64_t* idx_i, int64_t* idx
 }
 
 double msmb_cost_flops_per_step(const msmb_field* f, int64_t n) {
-    const double rep = f->rep_on ? 30.0 * double(n) : 0.0; // PairRepulsionOverlay, force_field.cpp:70-72
+    const double rep = 30.0 * double(n) * double(f->rep.size()); // PairRepulsionOverlay, force_field.cpp:70-72
     if (f->kind == MSMB_FIELD_DIRECT) return 20.0 * double(n) * double(n) + rep; // force_field.cpp:17-19
     if (f->kind != MSMB_FIELD_MSM) { // force_field.cpp:25-35
         const double fpp = f->cut.flops_per_particle > 0.0 ? f->cut.flops_per_particle
@@ -1002,6 +1028,41 @@ int msmb_evaluate(msmb_field* f, int64_t n, const double* pos_xyz, const double*
     const int rc = eval_device(f, f->scratch, true);
     if (rc) return rc;
     copy_outputs(f, n, phi, phi_short, phi_long, force_xyz, energy);
+    return MSMB_OK;
+    GUARD_END(f)
+}
+
+// energy_report (src/integrate.cpp:47-55): kinetic energy on the device, then the
+// field's evaluation.  out = [kinetic, potential, total].
+int msmb_energy_report(msmb_field* f, int64_t n, const double* pos_xyz, const double* vel_xyz, const double* q,
+                       const double* mass, const double box[3], const msmb_units* units, double* out) {
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    GUARD_BEGIN
+    f->last = Error{};
+    cudaSetDevice(f->device);
+    const msmb_units u = units ? *units : f->units;
+    Error e = validate_units(u); // energy_report validates its units first
+    if (!e.kind && f->kind == MSMB_FIELD_MSM) e = validate_config(f->cfg);
+    if (!e.kind) e = validate_units(f->units);
+    if (e.kind) return engine_set_error(f, e);
+    e = ensure_workspace(f, n, box);
+    if (e.kind) return engine_set_error(f, e);
+    fill_state(f, f->scratch, n, pos_xyz, vel_xyz, q, mass, box);
+    Workspace& W = *f->ws;
+    double ke = 0.0;
+    if (n > 0) {
+        f->launches += launch_reset_err(f->stream, W.err, 0);
+        f->launches += launch_kinetic(f->stream, f->scratch.dev(), W.o.e, W.o.partial, 1.0, W.o.energy, W.err);
+        ck(cudaMemcpyAsync(&ke, W.o.energy, sizeof(double), cudaMemcpyDeviceToHost, f->stream), "D2H");
+        ck(cudaStreamSynchronize(f->stream), "sync");
+    }
+    const int rc = eval_device(f, f->scratch, true);
+    if (rc) return rc;
+    double pot = 0.0;
+    copy_outputs(f, n, nullptr, nullptr, nullptr, nullptr, &pot);
+    out[0] = ke / u.energy_to_native;
+    out[1] = pot;
+    out[2] = out[0] + out[1];
     return MSMB_OK;
     GUARD_END(f)
 }

@@ -5,6 +5,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "msmb_kernels.cuh"
@@ -80,6 +81,7 @@ struct Workspace {
     cudaGraphExec_t gx_eval = nullptr, gx_step1 = nullptr, gx_step2 = nullptr;
     const double* graph_key = nullptr;
     double graph_dt = 0;
+    double graph_conv = 0;               // energy_to_native baked into the kick kernels
     int graph_cap = 0;
     int launches_eval = 0, launches_step = 0;
     std::vector<std::string> stage_names;
@@ -117,8 +119,8 @@ struct StageTimer {
 struct msmb_field {
     int kind = MSMB_FIELD_MSM;       // msmb_field_kind
     msmb_cutoff_params cut{};        // pair-only fields (msmb_create_cutoff)
-    int rep_on = 0;                  // PairRepulsionOverlay (msmb_create_overlay)
-    double rep_eps = 0, rep_sigma = 1;
+    int rep_on = 0;                  // PairRepulsionOverlay terms (msmb_create_overlay), innermost first
+    std::vector<std::pair<double, double>> rep; // (epsilon, sigma) per nested overlay (force_field.cpp:45-68)
     msmb_msm_config cfg{};
     msmb_units units{};
     int device = 0;
@@ -138,6 +140,7 @@ struct msmb_field {
     int dd_nparts = 1, dd_part = 0; // spatial decomposition part (msmb_dd_set_part)
     int lattice_direct = 0;         // msmb_set_lattice_method: 1 = direct stencil sum
     double pair_skin = -1.0;        // msmb_set_pair_skin (A); < 0 = default
+    int list_reuse = 0;             // msmb_set_list_reuse: keep the pair list across calls
     bool destroy_pending = false;
 };
 

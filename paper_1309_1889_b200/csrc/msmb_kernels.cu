@@ -2486,6 +2486,23 @@ int launch_energy_sum(cudaStream_t st, int64_t n, const double* e, double* parti
     return 2;
 }
 
+// kinetic_energy (src/system.cpp:51-55): e_i = (0.5 m_i) |v_i|^2 with norm2's
+// operation order, summed by the fixed-order energy tree
+__global__ void k_kinetic(int64_t n, const double* __restrict__ vx, const double* __restrict__ vy,
+                          const double* __restrict__ vz, const double* __restrict__ m, double* e) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double v2 = __dadd_rn(__dadd_rn(__dmul_rn(vx[i], vx[i]), __dmul_rn(vy[i], vy[i])), __dmul_rn(vz[i], vz[i]));
+    e[i] = __dmul_rn(__dmul_rn(0.5, m[i]), v2);
+}
+
+int launch_kinetic(cudaStream_t st, const DevState& s, double* e, double* partial, double scale, double* out,
+                   ErrRec* err) {
+    if (s.n <= 0) return 0;
+    k_kinetic<<<atom_blocks(s.n, 256), 256, 0, st>>>(s.n, s.vx, s.vy, s.vz, s.m, e);
+    return 1 + launch_energy_sum(st, s.n, e, partial, scale, out, 0, err);
+}
+
 int reduce_blocks(int64_t n) { return int((n + 4095) / 4096) > 0 ? int((n + 4095) / 4096) : 1; }
 
 int launch_interp(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c,

@@ -166,6 +166,9 @@ int launch_finalize(cudaStream_t st, const DevState& s, ErrRec* err, int pair_fi
 int launch_pair_out(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c, DevOut& o,
                     ErrRec* err, int want_energy, const Part& P);
 // fixed-order energy tree: *out = scale * sum(e[0..n)) (accumulate: *out += ...)
+// kinetic_energy (src/system.cpp:51-55) of s into *out (times scale), e = n scratch doubles
+int launch_kinetic(cudaStream_t st, const DevState& s, double* e, double* partial, double scale, double* out,
+                   ErrRec* err);
 int launch_energy_sum(cudaStream_t st, int64_t n, const double* e, double* partial, double scale, double* out,
                       int accumulate, ErrRec* err);
 // all-pairs kernels (msmb_direct.cu): direct Coulomb (coul) and/or the

@@ -8,14 +8,23 @@
 // to the reference's full history.
 //
 // The Executor of the reference (src/parareal.cpp:11-36) only changes where fine
-// slices run; results are independent of it (pure propagators).  On one GPU the
-// fine slices run back to back on the fine field's stream; the multi-GPU split of
-// the fine sweep is paper_1309_1889_b200/parallel.py (one process per GPU) over the
-// raw device-state entry points at the end of this file.
+// slices run; results are independent of it (pure propagators).  With one fine
+// field the fine slices run back to back on its stream; msmb_parareal_run_ex takes
+// several fine fields (replicas of F, one per GPU) and runs the fine sweep of an
+// iteration on all of them at once, one host worker per field pulling slice
+// indices from a shared counter -- the reference's AsyncExecutor::parallel_for
+// (src/parareal.cpp:16-36) with GPUs as workers.  Each worker propagates its
+// slice on its own device and copies the end state back (peer copy over NVLink);
+// the state algebra and the coarse sweep stay on the first fine field's device.
+// The multi-process (one process per GPU, NCCL) split of the same sweep is
+// paper_1309_1889_b200/parallel.py over the raw device-state entry points at the
+// end of this file.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <thread>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -34,6 +43,9 @@ struct Delta {
 
 struct PR {
     const msmb_parareal_config* cfg;
+    std::vector<msmb_field*> fines; // fine-field replicas ([0] = cfg->fine.field)
+    int device = 0;                 // device of the rows (fines[0]'s)
+    std::vector<msmb_parareal_row> rows; // ConvergenceReport::rows (parareal.cpp:208)
     int64_t n;
     cudaStream_t st; // fine field's stream for the algebra
     DBuf partial;
@@ -98,20 +110,27 @@ static std::unique_ptr<StateBuf> state_add(PR& P, const StateBuf& base, const De
 
 // propagate(spec, in, units) into a new state.  The field's scratch system is
 // the working buffer so its captured CUDA graphs are reused across calls.
-static int prop(PR& P, const msmb_propagator& sp, const StateBuf& in, std::unique_ptr<StateBuf>& out) {
-    msmb_field* f = sp.field;
+// `f` may live on another device than the rows (a fine replica): the copies are
+// cudaMemcpyDefault (peer copies under UVA) and `out` is allocated on P.device.
+static int prop(PR& P, const msmb_propagator& sp, const StateBuf& in, std::unique_ptr<StateBuf>& out,
+                msmb_field* f = nullptr) {
+    if (!f) f = sp.field;
     std::lock_guard<std::recursive_mutex> lk(f->mu);
+    ckp(cudaSetDevice(P.device), "cudaSetDevice");
     ckp(cudaStreamSynchronize(P.st), "sync");
+    out = new_state(P);
+    ckp(cudaSetDevice(f->device), "cudaSetDevice");
     if (f->scratch.n != P.n || !f->scratch.buf.p) ckp(f->scratch.alloc(P.n), "alloc scratch");
-    ckp(cudaMemcpyAsync(f->scratch.buf.p, in.buf.p, in.buf.bytes, cudaMemcpyDeviceToDevice, f->stream), "copy");
+    ckp(cudaMemcpyAsync(f->scratch.buf.p, in.buf.p, in.buf.bytes, cudaMemcpyDefault, f->stream), "copy");
     for (int ax = 0; ax < 3; ++ax) f->scratch.box[ax] = in.box[ax];
     const int rc = engine_propagate(f, f->scratch, sp.dt, sp.steps_per_slice,
                                     P.cfg->units.energy_to_native);
-    if (rc) return rc;
-    out = new_state(P);
-    ckp(cudaMemcpyAsync(out->buf.p, f->scratch.buf.p, in.buf.bytes, cudaMemcpyDeviceToDevice, f->stream), "copy");
-    ckp(cudaStreamSynchronize(f->stream), "sync");
-    return MSMB_OK;
+    if (rc == MSMB_OK) {
+        ckp(cudaMemcpyAsync(out->buf.p, f->scratch.buf.p, in.buf.bytes, cudaMemcpyDefault, f->stream), "copy");
+        ckp(cudaStreamSynchronize(f->stream), "sync");
+    }
+    ckp(cudaSetDevice(P.device), "cudaSetDevice");
+    return rc;
 }
 
 using Row = std::vector<std::unique_ptr<StateBuf>>;
@@ -162,12 +181,49 @@ static int pr_iterate(PR& P, Window& w) { // parareal.cpp:117-180
             deltas[n] = copy_delta(P, *w.d_prev[n]);
             P.f_skipped++;
         }
-    for (int n = 1; n <= t; ++n) { // the executor's work list
-        if (skip[n]) continue;
-        std::unique_ptr<StateBuf> f;
-        const int rc = prop(P, P.cfg->fine, *w.lam_prev[n - 1], f);
-        if (rc) return rc;
-        deltas[n] = state_sub(P, *f, *w.g_prev[n]);
+    // the executor's work list (parareal.cpp:146-155): fine slices, over the fine replicas
+    std::vector<int> work;
+    for (int n = 1; n <= t; ++n)
+        if (!skip[n]) work.push_back(n);
+    Row fres(size_t(t) + 1);
+    std::vector<int> frc(size_t(t) + 1, MSMB_OK);
+    std::vector<Error> ferr(size_t(t) + 1);
+    std::vector<std::string> fexc(size_t(t) + 1);
+    std::atomic<size_t> next{0};
+    std::atomic<int> stop{0};
+    auto worker = [&](msmb_field* f) {
+        for (;;) {
+            const size_t k = next.fetch_add(1);
+            if (k >= work.size() || stop.load()) return;
+            const int n = work[k];
+            try {
+                frc[n] = prop(P, P.cfg->fine, *w.lam_prev[n - 1], fres[n], f);
+                if (frc[n]) ferr[n] = f->last;
+            } catch (const std::exception& ex) {
+                frc[n] = MSMB_ERR_CUDA;
+                fexc[n] = ex.what();
+            }
+            if (frc[n]) stop.store(1);
+        }
+    };
+    if (P.fines.size() > 1 && work.size() > 1) {
+        std::vector<std::thread> th;
+        for (msmb_field* f : P.fines) th.emplace_back(worker, f);
+        for (auto& x : th) x.join();
+        ckp(cudaSetDevice(P.device), "cudaSetDevice");
+    } else {
+        worker(P.fines[0]);
+    }
+    // a failure is the one a sequential executor meets first: the lowest slice index
+    for (int n : work)
+        if (frc[n]) {
+            if (!fexc[n].empty()) throw std::runtime_error(fexc[n]);
+            P.fines[0]->last = ferr[n];
+            return frc[n];
+        }
+    for (int n : work) {
+        if (!fres[n]) return MSMB_ERR_INTERNAL; // not reached: every slice ran or one failed
+        deltas[n] = state_sub(P, *fres[n], *w.g_prev[n]);
         P.f_evals++;
     }
     Row row(size_t(t) + 1), grow(size_t(t) + 1);
@@ -220,6 +276,8 @@ static int setup(PR& P, const msmb_parareal_config* cfg, int64_t n, const double
     P.cfg = cfg;
     P.n = n;
     msmb_field* f = cfg->fine.field;
+    if (P.fines.empty()) P.fines.push_back(f);
+    P.device = f->device;
     P.st = f->stream;
     P.nblk = reduce_blocks(n);
     ckp(P.partial.alloc(sizeof(double) * size_t(P.nblk)), "alloc");
@@ -302,20 +360,48 @@ extern "C" int msmb_parareal_window(const msmb_parareal_config* cfg, int64_t n, 
     }
 }
 
-extern "C" int msmb_parareal_run(const msmb_parareal_config* cfg, int64_t n, const double* pos_xyz,
-                                 const double* vel_xyz, const double* q, const double* mass,
-                                 const double box[3], int total_points, double* traj_pos,
-                                 double* traj_vel, int64_t* report) {
+// parareal_run (parareal.cpp:182-239) over the fine replicas `fines` (fines[0] is
+// cfg->fine.field).  rows / point_iterations: the ConvergenceReport's history.
+static int run_impl(const msmb_parareal_config* cfg, std::vector<msmb_field*> fines, int64_t n,
+                    const double* pos_xyz, const double* vel_xyz, const double* q, const double* mass,
+                    const double box[3], int total_points, double* traj_pos, double* traj_vel, int64_t* report,
+                    msmb_parareal_row* rows, int64_t rows_cap, int64_t* rows_written, int* point_iterations,
+                    int report_len = 5) {
     Error e = validate(cfg);
     if (e.kind) return pr_fail(cfg, e);
     if (total_points < 1) return pr_fail(cfg, Error{MSMB_ERR_CONFIG, -1, -1, -1, "total_points must be >= 1"});
+    for (msmb_field* f : fines) {
+        if (!f) return pr_fail(cfg, Error{MSMB_ERR_CONFIG, -1, -1, -1, "propagator has no force field"});
+        const msmb_field* F = fines[0];
+        const bool same = f->kind == F->kind && f->rep == F->rep && f->cfg.cutoff_a == F->cfg.cutoff_a &&
+                          f->cfg.spacing_h == F->cfg.spacing_h && f->cfg.levels_l == F->cfg.levels_l &&
+                          f->cut.cutoff == F->cut.cutoff && f->cut.wolf_alpha == F->cut.wolf_alpha &&
+                          f->units.coulomb_constant == F->units.coulomb_constant;
+        if (!same)
+            return pr_fail(cfg, Error{MSMB_ERR_CONFIG, -1, -1, -1, "fine replicas must be the fine field's kind and parameters"});
+    }
+    if (rows_written) *rows_written = 0;
     try {
         cudaSetDevice(cfg->fine.field->device);
         PR P;
+        P.fines = std::move(fines);
         setup(P, cfg, n, pos_xyz, vel_xyz, q, mass, box);
         auto current = new_state(P);
         copy_state(P, *current, P.proto);
         int remaining = total_points, window_idx = 0, out_idx = 0, rc = MSMB_OK;
+        auto fill_report = [&](int converged) {
+            if (report) {
+                report[0] = P.g_evals;
+                report[1] = P.f_evals;
+                report[2] = P.f_skipped;
+                report[3] = window_idx;
+                report[4] = converged;
+                if (report_len > 5) report[5] = out_idx; // output points (point_iterations entries)
+            }
+            const int64_t nr = std::min<int64_t>(int64_t(P.rows.size()), rows ? rows_cap : 0);
+            for (int64_t i = 0; i < nr; ++i) rows[i] = P.rows[size_t(i)];
+            if (rows_written) *rows_written = int64_t(P.rows.size()); // may exceed rows_cap
+        };
         while (remaining > 0 && rc == MSMB_OK) { // parareal.cpp:193-235
             ++window_idx;
             const int t = std::min(cfg->window_points, remaining);
@@ -330,6 +416,7 @@ extern "C" int msmb_parareal_run(const msmb_parareal_config* cfg, int64_t n, con
                 for (int m = 1; m <= t; ++m) {
                     const double change = rms_change(P, *w.lam_prev[m], *w.lam_prev2[m]);
                     const bool ok = change <= cfg->tol;
+                    P.rows.push_back(msmb_parareal_row{window_idx, m, k, w.d_prev[m]->rms_pos, ok ? 1 : 0});
                     if (unbroken && ok)
                         prefix = m;
                     else
@@ -339,37 +426,47 @@ extern "C" int msmb_parareal_run(const msmb_parareal_config* cfg, int64_t n, con
             }
             if (rc) break;
             if (prefix == 0) {
-                if (report) {
-                    report[0] = P.g_evals;
-                    report[1] = P.f_evals;
-                    report[2] = P.f_skipped;
-                    report[3] = window_idx;
-                    report[4] = 0;
-                }
+                fill_report(0);
                 return pr_fail(cfg, Error{MSMB_ERR_NONCONVERGENCE, -1, -1, -1,
                                           "window " + std::to_string(window_idx) +
                                               " did not converge within max_iter=" +
                                               std::to_string(cfg->max_iter)});
             }
-            for (int m = 1; m <= prefix; ++m, ++out_idx)
+            for (int m = 1; m <= prefix; ++m, ++out_idx) {
                 download(P, *w.lam_prev[m], traj_pos ? traj_pos + 3 * n * out_idx : nullptr,
                          traj_vel ? traj_vel + 3 * n * out_idx : nullptr);
+                if (point_iterations) point_iterations[out_idx] = w.rows - 1; // iterations_done()
+            }
             copy_state(P, *current, *w.lam_prev[prefix]);
             remaining -= prefix;
         }
         if (rc) return pr_propagate_error(cfg, rc);
-        if (report) {
-            report[0] = P.g_evals;
-            report[1] = P.f_evals;
-            report[2] = P.f_skipped;
-            report[3] = window_idx;
-            report[4] = 1;
-        }
+        fill_report(1);
         cfg->fine.field->last = Error{};
         return MSMB_OK;
     } catch (const std::exception& ex) {
         return pr_fail(cfg, Error{MSMB_ERR_CUDA, -1, -1, -1, ex.what()});
     }
+}
+
+extern "C" int msmb_parareal_run(const msmb_parareal_config* cfg, int64_t n, const double* pos_xyz,
+                                 const double* vel_xyz, const double* q, const double* mass,
+                                 const double box[3], int total_points, double* traj_pos,
+                                 double* traj_vel, int64_t* report) {
+    return run_impl(cfg, {cfg ? cfg->fine.field : nullptr}, n, pos_xyz, vel_xyz, q, mass, box, total_points,
+                    traj_pos, traj_vel, report, nullptr, 0, nullptr, nullptr);
+}
+
+extern "C" int msmb_parareal_run_ex(const msmb_parareal_config* cfg, msmb_field* const* fine_replicas,
+                                    int n_replicas, int64_t n, const double* pos_xyz, const double* vel_xyz,
+                                    const double* q, const double* mass, const double box[3], int total_points,
+                                    double* traj_pos, double* traj_vel, int64_t* report, msmb_parareal_row* rows,
+                                    int64_t rows_cap, int64_t* rows_written, int* point_iterations) {
+    std::vector<msmb_field*> fines{cfg ? cfg->fine.field : nullptr};
+    for (int k = 0; k < n_replicas; ++k)
+        if (fine_replicas && fine_replicas[k] != fines[0]) fines.push_back(fine_replicas[k]);
+    return run_impl(cfg, std::move(fines), n, pos_xyz, vel_xyz, q, mass, box, total_points, traj_pos, traj_vel,
+                    report, rows, rows_cap, rows_written, point_iterations, 6);
 }
 
 // ---- raw device states (multi-process drivers, paper_1309_1889_b200/parallel.py) ----
