@@ -338,7 +338,8 @@ void msmb_reset_stage_times(msmb_field* f);
 /* Work counters of the most recent evaluation: [0] in-cutoff unordered pairs
  * P_u, [1] candidate pair tests, [2] clusters, [3] clipped lattice taps
  * (all levels except the top), [4] top-level taps, [5] kernel launches per
- * evaluation, [6] pair-list rebuilds since the workspace was created. */
+ * evaluation, [6] pair-list rebuilds since the workspace was created, [7] warps
+ * per i-cluster in the pair kernel (1 = the large-system instance). */
 int msmb_work_counters(msmb_field* f, int64_t* out, int cap);
 /* Device-timed propagate for benchmarking: the same computation as
  * msmb_system_propagate, with CUDA events on the field's stream around the
@@ -386,9 +387,17 @@ int msmb_debug_cells(msmb_field* f, int64_t n, const double* pos_xyz, const doub
 /* Runs one stage kernel on caller lattices, for bitwise stage parity:
  * stage 0 restrict (level k -> k+1), 1 lattice cutoff (level k),
  * 2 top level, 3 prolongate (k+1 -> k, `out` holds the fine potential in/out),
- * 4 interpolate (level-0 potential -> per-atom u, uses pos/n). */
+ * 4 interpolate (level-0 potential -> per-atom u, uses pos/n); these are the
+ * bit-exact variants.  The production kernels an evaluation runs (tolerance
+ * tests): 5 restriction chain (in = level-0 charges, out = all levels' charges),
+ * 6 top level, 7 prolongation chain (in/out = all levels' potentials). */
 int msmb_debug_stage(msmb_field* f, int stage, int k, const double box[3], const double* in,
                      double* out, int64_t n, const double* pos_xyz);
+/* The production binning kernel's level-0 cell triples (decoded from its sort
+ * keys) and coverage flags, for the bit-exact binning test of the kernel every
+ * evaluation runs (msmb_debug_cells runs a stand-alone copy of the formula). */
+int msmb_debug_bin_keys(msmb_field* f, int64_t n, const double* pos_xyz, const double box[3],
+                        int32_t* cells_xyz, int32_t* covered);
 
 #ifdef __cplusplus
 }

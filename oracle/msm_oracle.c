@@ -464,12 +464,14 @@ static int cmp_i64(const void* a, const void* b) {
     return x < y ? -1 : x > y;
 }
 
-int orc_short_range(int64_t n, const double* pos, const double* q, double a, double kc,
-                    double* phi, double* force, char* msg, int cap) {
-    for (int64_t i = 0; i < n; ++i) {
-        phi[i] = 0.0;
-        force[3 * i] = force[3 * i + 1] = force[3 * i + 2] = 0.0;
-    }
+/* scan_only: run the error scan and skip the pair sum (phi/force untouched) */
+static int short_range_impl(int64_t n, const double* pos, const double* q, double a, double kc,
+                            double* phi, double* force, char* msg, int cap, int scan_only) {
+    if (!scan_only)
+        for (int64_t i = 0; i < n; ++i) {
+            phi[i] = 0.0;
+            force[3 * i] = force[3 * i + 1] = force[3 * i + 2] = 0.0;
+        }
     if (n < 2) return ok(msg, cap);
     const double a2 = a * a;
     /* cell grid over the finite atoms */
@@ -572,7 +574,7 @@ int orc_short_range(int64_t n, const double* pos, const double* q, double a, dou
             rc = fail(msg, cap, E_DOMAIN, "kernel_g_star: r must be > 0");
     }
 
-    if (rc == OK) {
+    if (rc == OK && !scan_only) {
 #pragma omp parallel
         {
             jbuf_t jb = {NULL, 0};
@@ -648,6 +650,61 @@ int orc_short_range(int64_t n, const double* pos, const double* q, double a, dou
     return rc == OK ? ok(msg, cap) : rc;
 }
 
+int orc_short_range(int64_t n, const double* pos, const double* q, double a, double kc,
+                    double* phi, double* force, char* msg, int cap) {
+    return short_range_impl(n, pos, q, a, kc, phi, force, msg, cap, 0);
+}
+
+/* The particle anterpolate would report first (src/msm_phases.cpp:42-50: index
+ * order, x then y then z), checked before the pair sum so that an aborting
+ * evaluation does not pay for it; the outputs are those of the reference's order. */
+static int coverage_scan(int64_t n, const double* pos, const level_t* L0, char* msg, int cap) {
+    const double inv_h = 1.0 / L0->spacing;
+    for (int64_t p = 0; p < n; ++p) {
+        st1d sx, sy, sz;
+        if (stencil_at((pos[3 * p] - L0->origin[0]) * inv_h, L0->dims[0], &sx) ||
+            stencil_at((pos[3 * p + 1] - L0->origin[1]) * inv_h, L0->dims[1], &sy) ||
+            stencil_at((pos[3 * p + 2] - L0->origin[2]) * inv_h, L0->dims[2], &sz))
+            return fail(msg, cap, E_COVERAGE, "particle %lld outside grid coverage", (long long)p);
+    }
+    return OK;
+}
+
+/* ---- add_long_range_forces: src/msm.cpp:16-48 (file-local there) ----------- */
+static void add_long_range_forces(int64_t n, const double* pos, const double* q, const level_t* L0, double kc,
+                                  double* sf) {
+    const double inv_h = 1.0 / L0->spacing;
+#pragma omp parallel for schedule(static)
+    for (int64_t p = 0; p < n; ++p) {
+        const double tx = (pos[3 * p] - L0->origin[0]) * inv_h;
+        const double ty = (pos[3 * p + 1] - L0->origin[1]) * inv_h;
+        const double tz = (pos[3 * p + 2] - L0->origin[2]) * inv_h;
+        const int bx = (int)floor(tx) - 1, by = (int)floor(ty) - 1, bz = (int)floor(tz) - 1;
+        double wx[4], wy[4], wz[4], dwx[4], dwy[4], dwz[4];
+        for (int d = 0; d < 4; ++d) {
+            wx[d] = basis_phi(tx - (bx + d));
+            wy[d] = basis_phi(ty - (by + d));
+            wz[d] = basis_phi(tz - (bz + d));
+            dwx[d] = basis_phi_deriv(tx - (bx + d)) * inv_h;
+            dwy[d] = basis_phi_deriv(ty - (by + d)) * inv_h;
+            dwz[d] = basis_phi_deriv(tz - (bz + d)) * inv_h;
+        }
+        double gx = 0.0, gy = 0.0, gz = 0.0;
+        for (int a = 0; a < 4; ++a)
+            for (int b = 0; b < 4; ++b)
+                for (int cc = 0; cc < 4; ++cc) {
+                    const double u = L0->potential[IDX(L0, bx + a, by + b, bz + cc)];
+                    gx += dwx[a] * wy[b] * wz[cc] * u;
+                    gy += wx[a] * dwy[b] * wz[cc] * u;
+                    gz += wx[a] * wy[b] * dwz[cc] * u;
+                }
+        const double s = kc * q[p];
+        sf[3 * p] -= gx * s;
+        sf[3 * p + 1] -= gy * s;
+        sf[3 * p + 2] -= gz * s;
+    }
+}
+
 /* ---- msm_potential: src/msm.cpp:52-90 (+ add_long_range_forces 16-48) -------- */
 static int msm_eval(int64_t n, const double* pos, const double* q, const double* box,
                     const cfg_t* c, double kc, double conv, double* phi, double* phi_short,
@@ -662,12 +719,18 @@ static int msm_eval(int64_t n, const double* pos, const double* q, const double*
     double* ul = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
     level_t lv[64];
     int built = 0;
-    rc = orc_short_range(n, pos, q, c->a, kc, sphi, sf, msg, cap);
+    /* msm.cpp:58-61: short_range (its pair errors first), the hierarchy (box errors),
+     * then anterpolation (coverage); the pair sum itself runs once no error is left */
+    rc = short_range_impl(n, pos, q, c->a, kc, sphi, sf, msg, cap, 1);
     if (rc) goto done;
     if (c->l > 64) { rc = fail(msg, cap, E_CONFIG, "levels_l too large for the oracle"); goto done; }
     rc = build_levels(box, c, lv, 1, msg, cap);
     if (rc) goto done;
     built = 1;
+    rc = coverage_scan(n, pos, &lv[0], msg, cap);
+    if (rc) goto done;
+    rc = orc_short_range(n, pos, q, c->a, kc, sphi, sf, msg, cap);
+    if (rc) goto done;
     rc = anterpolate(n, pos, q, &lv[0], msg, cap);
     if (rc) goto done;
     for (int k = 0; k + 1 < c->l; ++k) {
@@ -685,38 +748,7 @@ static int msm_eval(int64_t n, const double* pos, const double* q, const double*
     {
         const double self = smoothing_gamma(0.0) / c->a; /* msm.cpp:72-73 */
         for (int64_t i = 0; i < n; ++i) ul[i] -= q[i] * self;
-        /* add_long_range_forces: msm.cpp:16-48 */
-        const level_t* L0 = &lv[0];
-        const double inv_h = 1.0 / L0->spacing;
-#pragma omp parallel for schedule(static)
-        for (int64_t p = 0; p < n; ++p) {
-            const double tx = (pos[3 * p] - L0->origin[0]) * inv_h;
-            const double ty = (pos[3 * p + 1] - L0->origin[1]) * inv_h;
-            const double tz = (pos[3 * p + 2] - L0->origin[2]) * inv_h;
-            const int bx = (int)floor(tx) - 1, by = (int)floor(ty) - 1, bz = (int)floor(tz) - 1;
-            double wx[4], wy[4], wz[4], dwx[4], dwy[4], dwz[4];
-            for (int d = 0; d < 4; ++d) {
-                wx[d] = basis_phi(tx - (bx + d));
-                wy[d] = basis_phi(ty - (by + d));
-                wz[d] = basis_phi(tz - (bz + d));
-                dwx[d] = basis_phi_deriv(tx - (bx + d)) * inv_h;
-                dwy[d] = basis_phi_deriv(ty - (by + d)) * inv_h;
-                dwz[d] = basis_phi_deriv(tz - (bz + d)) * inv_h;
-            }
-            double gx = 0.0, gy = 0.0, gz = 0.0;
-            for (int a = 0; a < 4; ++a)
-                for (int b = 0; b < 4; ++b)
-                    for (int cc = 0; cc < 4; ++cc) {
-                        const double u = L0->potential[IDX(L0, bx + a, by + b, bz + cc)];
-                        gx += dwx[a] * wy[b] * wz[cc] * u;
-                        gy += wx[a] * dwy[b] * wz[cc] * u;
-                        gz += wx[a] * wy[b] * dwz[cc] * u;
-                    }
-            const double s = kc * q[p];
-            sf[3 * p] -= gx * s;
-            sf[3 * p + 1] -= gy * s;
-            sf[3 * p + 2] -= gz * s;
-        }
+        add_long_range_forces(n, pos, q, &lv[0], kc, sf);
         double e = 0.0;
         for (int64_t i = 0; i < n; ++i) {
             const double ph = sphi[i] + ul[i];
@@ -819,6 +851,26 @@ int orc_interpolate(int64_t n, const double* pos, const double* box, double a, d
     WITH_LEVELS(box, a, h, levels)
     memcpy(lv[0].potential, pot0, lv[0].size * 8);
     rc = interpolate(n, pos, &lv[0], u_out, msg, cap);
+    free_levels(lv, levels);
+    return rc ? rc : ok(msg, cap);
+}
+
+/* The long-range half of msm_potential (src/msm.cpp:69-78) from a given level-0
+ * potential: u_long = interpolate(pot0) - q gamma(0)/a (msm.cpp:72-73) and the
+ * long-range forces F = -k_C q grad (add_long_range_forces, msm.cpp:16-48, applied
+ * to zero forces).  Lets a test check the GPU's production interpolation/force
+ * kernel on the GPU's own level-0 potential. */
+int orc_long_range(int64_t n, const double* pos, const double* q, const double* box, double a, double h,
+                   int levels, double kc, const double* pot0, double* u_out, double* f_out, char* msg, int cap) {
+    WITH_LEVELS(box, a, h, levels)
+    memcpy(lv[0].potential, pot0, lv[0].size * 8);
+    rc = interpolate(n, pos, &lv[0], u_out, msg, cap);
+    if (!rc) {
+        const double self = smoothing_gamma(0.0) / a;
+        for (int64_t i = 0; i < n; ++i) u_out[i] -= q[i] * self;
+        memset(f_out, 0, sizeof(double) * 3 * (size_t)n);
+        add_long_range_forces(n, pos, q, &lv[0], kc, f_out);
+    }
     free_levels(lv, levels);
     return rc ? rc : ok(msg, cap);
 }

@@ -261,10 +261,10 @@ class GpuField(ForceField):
         _native.lib().msmb_reset_stage_times(self._h)
 
     def work_counters(self):
-        out = np.zeros(7, dtype=np.int64)
-        _native.lib().msmb_work_counters(self._h, out.ctypes.data_as(C.POINTER(C.c_int64)), 7)
+        out = np.zeros(8, dtype=np.int64)
+        _native.lib().msmb_work_counters(self._h, out.ctypes.data_as(C.POINTER(C.c_int64)), 8)
         keys = ["pairs", "candidates", "clusters", "lattice_taps", "top_taps", "launches_per_eval",
-                "list_rebuilds"]
+                "list_rebuilds", "pair_split"]
         return dict(zip(keys, map(int, out)))
 
     def kernel_launches(self) -> int:
@@ -324,12 +324,29 @@ class MsmField(GpuField):
         _check(self._h, rc)
         return cells, cov.astype(bool)
 
+    def debug_bin_keys(self, positions, box):
+        """Level-0 cell triples from the production binning kernel's sort keys."""
+        pos = _f64(positions, (-1, 3))
+        n = len(pos)
+        cells = np.zeros((n, 3), dtype=np.int32)
+        cov = np.zeros(n, dtype=np.int32)
+        rc = _native.lib().msmb_debug_bin_keys(self._h, n, _p(pos), _p(_f64(box)),
+                                               cells.ctypes.data_as(C.POINTER(C.c_int32)),
+                                               cov.ctypes.data_as(C.POINTER(C.c_int32)))
+        _check(self._h, rc)
+        return cells, cov.astype(bool)
+
     def debug_stage(self, stage: int, k: int, box, inp, out=None, positions=None):
-        """Single stage on caller lattices (0 restrict, 1 lattice cutoff, 2 top, 3 prolong, 4 interp)."""
+        """Single stage on caller lattices: bit-exact variants 0 restrict, 1 lattice cutoff,
+        2 top, 3 prolong, 4 interp; production kernels 5 restriction chain (level-0 charges
+        -> all levels), 6 top, 7 prolongation chain (all levels' potentials in / out)."""
         dims, _, _ = grid_geometry(self._config, box)
+        total = int(sum(int(np.prod(d)) for d in dims))
         if stage == 0:
             out = np.zeros(int(np.prod(dims[k + 1])))
-        elif stage in (1, 2):
+        elif stage in (5, 7):
+            out = np.zeros(total)
+        elif stage in (1, 2, 6):
             out = np.zeros(len(inp))
         elif stage == 3:
             out = np.array(out, dtype=np.float64, copy=True)

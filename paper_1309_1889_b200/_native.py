@@ -104,6 +104,7 @@ SIGNATURES = {
     "msmb_debug_levels": (C.c_int, [_VP, _D, _D]),
     "msmb_debug_cells": (C.c_int, [_VP, C.c_int64, _D, _D, _I, _I]),
     "msmb_debug_stage": (C.c_int, [_VP, C.c_int, C.c_int, _D, _D, _D, C.c_int64, _D]),
+    "msmb_debug_bin_keys": (C.c_int, [_VP, C.c_int64, _D, _D, _I, _I]),
 }
 
 _lib = None

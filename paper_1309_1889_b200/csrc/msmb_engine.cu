@@ -563,6 +563,11 @@ void record_counters(msmb_field* f, const Workspace& W, const ErrRec& r) {
     int rebuilds = 0;
     if (W.c.flag) cudaMemcpy(&rebuilds, W.c.flag + 2, sizeof(int), cudaMemcpyDeviceToHost);
     f->counters[6] = rebuilds;
+    // warps per i-cluster of the pair kernel: 1 = the large-system instance (k_pairs_mw<K, false>)
+    f->counters[7] = (W.g.kind == MSMB_FIELD_MSM || W.g.kind == MSMB_FIELD_CUTOFF || W.g.kind == MSMB_FIELD_WOLF) &&
+                             W.a.pair_part
+                         ? pair_split(W.maxclu)
+                         : 1;
 }
 
 void grow_cap(Workspace& W, const ErrRec& r) {
@@ -1371,7 +1376,7 @@ void msmb_reset_stage_times(msmb_field* f) {
 }
 
 int msmb_work_counters(msmb_field* f, int64_t* out, int cap) {
-    const int n = std::min(cap, 7);
+    const int n = std::min(cap, 8);
     for (int i = 0; i < n; ++i) out[i] = f->counters[i];
     return n;
 }
@@ -1495,10 +1500,71 @@ int msmb_debug_stage(msmb_field* f, int stage, int k, const double box[3], const
             down(out, W.o.phil, size_t(n));
             break;
         }
+        // ---- the production kernels of an evaluation (tolerance tests) ----
+        case 5: // restriction chain: in = level-0 charges, out = every level's charges
+            up(W.L.charge + g.lv[0].offset, in, g.lv[0].size);
+            f->launches += launch_restrict_all(f->stream, g, W.L, W.err);
+            down(out, W.L.charge, g.lattice_total);
+            break;
+        case 6: { // top level as an evaluation runs it (warp kernel or FFT job)
+            const int t = g.levels - 1;
+            up(W.L.charge + g.lv[t].offset, in, g.lv[t].size);
+            f->launches += W.fft_top.n ? launch_lattice_fft(f->stream, W.fft_top, W.err)
+                                       : launch_top(f->stream, g, W.L, W.err, false);
+            down(out, W.L.pot + g.lv[t].offset, g.lv[t].size);
+            break;
+        }
+        case 7: // prolongation chain: in = every level's potential before it, out = after
+            up(W.L.pot, in, g.lattice_total);
+            f->launches += launch_prolong_all(f->stream, g, W.L, W.err);
+            down(out, W.L.pot, g.lattice_total);
+            break;
         default:
             return MSMB_ERR_CONFIG;
     }
     ck(cudaGetLastError(), "launch");
+    return MSMB_OK;
+    GUARD_END(f)
+}
+
+// The production binning kernel (k_bin, the one every evaluation runs): the level-0
+// cell triple of every particle, decoded from its sorted-cell key; covered = 0 for a
+// particle outside grid coverage (key -1).
+int msmb_debug_bin_keys(msmb_field* f, int64_t n, const double* pos_xyz, const double box[3],
+                        int32_t* cells_xyz, int32_t* covered) {
+    std::lock_guard<std::recursive_mutex> lk(f->mu);
+    if (f->kind != MSMB_FIELD_MSM) return msm_only(f);
+    GUARD_BEGIN
+    cudaSetDevice(f->device);
+    Error e = ensure_workspace(f, n, box);
+    if (e.kind) return engine_set_error(f, e);
+    Workspace& W = *f->ws;
+    const Geometry& g = W.g;
+    std::vector<double> q(size_t(n), 0.0);
+    fill_state(f, f->scratch, n, pos_xyz, nullptr, q.data(), nullptr, box);
+    f->launches += launch_reset_err(f->stream, W.err, 0);
+    f->launches += launch_bin(f->stream, g, f->scratch.dev(), W.a, W.c, W.err);
+    std::vector<int> key(size_t(n > 0 ? n : 1));
+    ck(cudaStreamSynchronize(f->stream), "sync");
+    if (n) ck(cudaMemcpy(key.data(), W.a.key, sizeof(int) * size_t(n), cudaMemcpyDeviceToHost), "D2H");
+    const int d2 = g.lv[0].dims[2], cw = g.cw, ncy = g.ncy;
+    for (int64_t i = 0; i < n; ++i) {
+        int k = key[size_t(i)];
+        covered[i] = k >= 0;
+        if (k < 0) {
+            cells_xyz[3 * i] = cells_xyz[3 * i + 1] = cells_xyz[3 * i + 2] = 0;
+            continue;
+        }
+        const int cyr = k % cw;
+        k /= cw;
+        const int cxr = k % cw;
+        k /= cw;
+        const int cz = k % d2;
+        const int col = k / d2;
+        cells_xyz[3 * i] = (col / ncy) * cw + cxr;
+        cells_xyz[3 * i + 1] = (col % ncy) * cw + cyr;
+        cells_xyz[3 * i + 2] = cz;
+    }
     return MSMB_OK;
     GUARD_END(f)
 }

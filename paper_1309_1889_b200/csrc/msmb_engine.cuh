@@ -133,7 +133,7 @@ struct msmb_field {
     msmb::Error last;
     msmb::StageTimer timer;
     int64_t launches = 0;
-    int64_t counters[8] = {0};
+    int64_t counters[8] = {0};      // msmb_work_counters
     msmb::StateBuf scratch; // device system for the host-pointer entry points
     msmb::DBuf reduce;      // block partials of the raw-state reductions
     int refs = 0;           // live msmb_system objects bound to this field

@@ -136,6 +136,9 @@ class Checker:
             fp = self.lib.orc_field_propagate
             fp.argtypes = [_D, i64, _D, _D, _D, _D, _D, f64, f64, f64, i32, _I, _S, i32]
             fp.restype = C.c_int
+            lr = self.lib.orc_long_range
+            lr.argtypes = [i64, _D, _D, _D, f64, f64, i32, f64, _D, _D, _D, _S, i32]
+            lr.restype = C.c_int
 
     # -------------------------------------------------------------- helpers
     @staticmethod
@@ -228,6 +231,17 @@ class Checker:
         out = np.zeros(len(pos))
         self._call(self.f["interpolate"], len(pos), _p(pos), _p(box), a, h, levels, _p(np.ascontiguousarray(pot0)), _p(out))
         return out
+
+    def long_range(self, pos, q, box, a, h, levels, pot0, kc=332.0636):
+        """(port only) u_long and the long-range forces of msm_potential (src/msm.cpp:16-48,
+        69-78) from a given level-0 potential."""
+        pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        box = np.asarray(box, dtype=np.float64)
+        u, f = np.zeros(len(q)), np.zeros((len(q), 3))
+        self._call(self.lib.orc_long_range, len(q), _p(pos), _p(q), _p(box), a, h, levels, kc,
+                   _p(np.ascontiguousarray(pot0, dtype=np.float64)), _p(u), _p(f))
+        return u, f
 
     def propagate(self, pos, vel, q, mass, box, a, h, levels, dt, steps, kc=332.0636, conv=4.184e-4):
         """Returns (pos, vel, steps_done, error-or-None)."""
