@@ -14,9 +14,15 @@ A "step" = one Verlet step = one full MSM energy/force evaluation + kick/drift
 (src/integrate.cpp:23-34).  The timed region is one device-resident propagate
 (initial evaluation + K steps + closing half-kick, as the reference library's
 propagate), timed with CUDA events on the engine's stream around every step, with
-a 256 MB (> L2) buffer written between steps outside the events.  Multi-GPU
-(torchrun): config 2 does not shard -- every rank runs an
-independent replica ("replicas only", weak scaling); max time over ranks.
+a 256 MB (> L2) buffer written between steps outside the events.
+
+Multi-GPU (torchrun, --gpus N > 1): the paths that shard.  The line is
+configs[2] C3-S (2^24 charges) propagated through the spatial slab decomposition
+(parallel.SpatialDecomposition -> csrc/msmb_slab.cu, NCCL halos, one part per GPU),
+and it carries a nested `parareal` object: configs[4] C5-S with the fine slices
+sharded over the ranks.  The N = 1 line carries both at one GPU in
+`scaling_base` (same code paths), so per-N values of the same workloads can be
+compared.  Device time = CUDA events per step on the part's stream, max over ranks.
 
 `--impl reference` times the reference's own CPU implementation (oracle/_ref,
 compiled from /root/reference sources) on a bounded sample per step; rank 0 only.
@@ -61,9 +67,9 @@ def parse():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="step", choices=["step", "spatial", "parareal", "parareal_cutoff"],
-                    help="step: the contract line (C2-S); spatial / parareal: the multi-GPU paths "
-                         "(tools/bench_paths.py)")
+    ap.add_argument("--no-scaling-base", action="store_true", help="N=1: skip the C3-S / C5-S one-GPU lines")
+    ap.add_argument("--no-full-reference", action="store_true",
+                    help="--impl reference: skip the one full-size short_range calibration")
     return ap.parse_args()
 
 
@@ -202,15 +208,173 @@ def cpu_threads_used():
     return 1
 
 
+def reference_full_short_range(w):
+    """The reference's short_range (src/msm_phases.cpp:224-252) once on the whole system."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib
+    if not oracle_lib.have("ref"):
+        return None
+    chk = oracle_lib.checker("ref")
+    pos = np.ascontiguousarray(w.pos)
+    t = chk.lib.ref_time_short_range(w.n, oracle_lib._p(pos), oracle_lib._p(np.ascontiguousarray(w.q)), w.a,
+                                     332.0636, 1)
+    return {"t_full_s": float(t)}
+
+
+def reference_c3_estimate(w, steps, warmup):
+    """Reference per-step cost on C3 (2^24 atoms; a full step is ~4.5 days of short_range
+    + ~95 s of grid phases on one core): grid phases timed once on a 1/8-volume sub-box
+    (2^21 atoms, same density) and scaled per phase (x8; top level x64 = (M_top ratio)^2),
+    short_range on a 30,000-atom subset per step scaled by its N(N-1)/2 pair checks."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib
+    chk = oracle_lib.checker("ref") if oracle_lib.have("ref") else None
+    if chk is None:
+        return None
+    from paper_1309_1889_b200 import fixtures as fx
+    sub = fx.config("c3s", n_override=1 << 21)
+    ph = np.zeros(6)
+    buf = C.create_string_buffer(256)
+    chk.lib.ref_time_phases.argtypes = [C.c_int64, oracle_lib._D, oracle_lib._D, oracle_lib._D, C.c_double,
+                                        C.c_double, C.c_int, oracle_lib._D, C.c_char_p, C.c_int]
+    rc = chk.lib.ref_time_phases(sub.n, oracle_lib._p(np.ascontiguousarray(sub.pos)), oracle_lib._p(sub.q),
+                                 oracle_lib._p(sub.box), sub.a, sub.h, sub.levels, oracle_lib._p(ph), buf, 256)
+    if rc != 0:
+        raise RuntimeError(buf.value.decode())
+    scale = np.array([8, 8, 8, 64, 8, 8 * 4.0]) # interpolate + long-range forces ~ 4x interpolate
+    t_grid = float(np.sum(ph * scale))
+    srs = []
+    rng = np.random.default_rng(3)
+    for k in range(warmup + steps):
+        idx = np.sort(rng.choice(w.n, size=30000, replace=False))
+        pos = np.ascontiguousarray(w.pos[idx])
+        q = np.ascontiguousarray(w.q[idx])
+        t = chk.lib.ref_time_short_range(30000, oracle_lib._p(pos), oracle_lib._p(q), w.a, 332.0636, 1)
+        if k >= warmup:
+            srs.append(t * (w.n * (w.n - 1.0)) / (30000 * 29999.0))
+    return {"t_step_s": float(np.mean(srs)) + t_grid, "t_grid_s": t_grid, "t_short_s": float(np.mean(srs))}
+
+
+SPATIAL_TEXT = ("configs[2] survivable variant c3s: 2^24 point charges (RSA min-separation 1.5 A; the literal "
+                "input aborts at step 2, tests/test_gpu_fullsize_parity.py), 551 A cube, +-1 rebalanced to net "
+                "zero, 18 amu, MSM a=12 A h=2.5 A cubic, 4 levels, dt 0.02 fs")
+PARAREAL_TEXT = ("configs[4] survivable variant c5s: 2^20 charges (RSA 1.5 A), F MSM a=12 h=2.5 l=4 dt 0.005 fs "
+                 "x100, G MSM a=8 h=5 l=3 dt 0.02 fs x25, one window of 8 slices, K=1 iteration (no short circuit)")
+
+
+def spatial_run(D, steps, warmup):
+    """C3-S through the slab decomposition over D.world GPUs: device-timed steps
+    (events on each part's stream, max over ranks) and the end-to-end call time."""
+    import paper_1309_1889_b200 as pkg
+    from paper_1309_1889_b200 import fixtures as fx, parallel
+    w = fx.config("c3s")
+    s = pkg.ParticleSystem(w.pos, w.vel, w.q, w.mass, w.box)
+    dd = parallel.SpatialDecomposition(pkg.MsmConfig(w.a, w.h, w.levels), s, device=D.local)
+    dd.propagate(w.dt, max(1, warmup))  # workspaces, plans
+    D.barrier()
+    sm = np.zeros(steps + 2)
+    l0 = dd.fields[0].kernel_launches()
+    with ClockSampler(D.local) as clk:
+        t0 = time.perf_counter()
+        dd.propagate(w.dt, steps, step_ms=sm)
+        wall = D.max(time.perf_counter() - t0)
+    launches = dd.fields[0].kernel_launches() - l0
+    D.barrier()
+    dev_ms = D.max(float(sm[1:steps + 1].sum()))
+    st = dd.stats()
+    bytes_step = D.max(float(st["bytes_per_step"]))
+    value = w.n * steps / (dev_ms * 1e-3)
+    nbytes = w.n * 64  # every rank uploads the whole system and downloads pos/vel
+    return w, {
+        "value": value, "ms_per_step": dev_ms / steps, "clocks": clk.result(), "gpu_launches": int(launches),
+        "e2e": {"value": w.n * steps / wall, "unit": UNIT, "h2d_bytes_per_step": nbytes / steps,
+                "d2h_bytes_per_step": w.n * 48 / steps,
+                "note": "one msmb_slab_propagate call per rank from host arrays (whole system in, whole final "
+                        "state out): upload, decomposition setup, initial evaluation, K steps, final gather; "
+                        "host wall clock, max over ranks"},
+        "exchange": {"bytes_received_per_step_per_rank": bytes_step, "halo_atoms": st["halo"],
+                     "owned_atoms": st["owned"], "rebuilds": st["rebuilds"], "migrated": st["migrated"]},
+        "config": {"workload": SPATIAL_TEXT, "n_atoms": int(w.n), "a": w.a, "h": w.h, "levels": w.levels,
+                   "dt_fs": w.dt, "parallelism": f"spatial x-slab decomposition over {D.world} GPU(s) "
+                                                 f"(csrc/msmb_slab.cu; NCCL halos)" if D.world > 1 else
+                                                 "spatial decomposition, one part (single GPU)",
+                   "l2": "inputs (1.1 GB state + 30 GB workspace) far exceed L2"},
+    }
+
+
+def parareal_run_line(D, K=1):
+    """C5-S parareal with the fine slices sharded over the ranks (parallel.parareal_run)."""
+    import torch
+    import paper_1309_1889_b200 as pkg
+    from paper_1309_1889_b200 import fixtures as fx, parallel
+    w = fx.config("c5s")
+    fa, fh, fl, fdt, fs = w.extra["fine"]
+    ga, gh, gl, gdt, gs = w.extra["coarse"]
+    F = pkg.MsmField(pkg.MsmConfig(fa, fh, fl), device=D.local)
+    G = pkg.MsmField(pkg.MsmConfig(ga, gh, gl), device=D.local)
+    cfg = pkg.PararealConfig(8, K, 1e300, pkg.PropagatorSpec(F, fdt, fs), pkg.PropagatorSpec(G, gdt, gs),
+                             short_circuit=False)
+    s = pkg.ParticleSystem(w.pos, w.vel, w.q, w.mass, w.box)
+    pkg.propagate(pkg.PropagatorSpec(F, fdt, 2), s)  # warm-up: graphs, plans
+    pkg.propagate(pkg.PropagatorSpec(G, gdt, 2), s)
+    torch.cuda.synchronize(D.local)
+    D.barrier()
+    t0 = time.perf_counter()
+    res = parallel.parareal_run(s, 8, cfg)
+    torch.cuda.synchronize(D.local)
+    D.barrier()
+    wall = D.max(time.perf_counter() - t0)
+    return {"value": w.n * 8 * fs / wall, "unit": UNIT, "ms_per_run": wall * 1e3, "K": K, "counts": res.counts,
+            "metric_note": "SURVEY 8(d): N x fine steps over the horizon (8 slices x 100) / wall time of "
+                           "parareal_init + K x parareal_iterate (host wall clock, max over ranks)",
+            "workload": PARAREAL_TEXT,
+            "parallelism": f"fine slices over {D.world} GPU(s) (parallel.parareal_run, NCCL broadcast of deltas)"}
+
+
+def multi_gpu(args, D):
+    """--gpus N > 1 under torchrun: the sharding paths (C3-S spatial, C5-S parareal)."""
+    import torch
+    torch.cuda.set_device(D.local)
+    if args.impl == "reference":
+        if D.rank == 0:
+            from paper_1309_1889_b200 import fixtures as fx
+            w = fx.config("c3s")
+            est = reference_c3_estimate(w, args.steps, args.warmup)
+            if est is None:
+                print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}), flush=True)
+                return
+            val = w.n / est["t_step_s"]
+            line = {"metric": METRIC, "impl": "reference", "value": val, "unit": UNIT, "n_gpus": D.world,
+                    "steps": args.steps, "warmup": args.warmup, "ms_per_step": est["t_step_s"] * 1e3,
+                    "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                    "data": "synthetic (seeded)",
+                    "config": {"workload": SPATIAL_TEXT, "n_atoms": int(w.n)},
+                    "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "reference",
+                                     "sample": "grid phases timed once on a 1/8-volume sub-box (2^21 atoms) and "
+                                               "scaled per phase (x8, top x64); short_range on a 30,000-atom "
+                                               "subset per step scaled by N(N-1)/2 pair checks; single-threaded"},
+                    "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            print(json.dumps(line), flush=True)
+        return
+    w, sp = spatial_run(D, args.steps, args.warmup)
+    par = parareal_run_line(D, 1)
+    if D.rank == 0:
+        line = {"metric": METRIC, "value": sp["value"], "unit": UNIT, "n_gpus": D.world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": sp["ms_per_step"], "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded; paper_1309_1889_b200/fixtures.py)", "config": sp["config"],
+                "e2e": sp["e2e"], "exchange": sp["exchange"], "gpu_launches": sp["gpu_launches"],
+                "clocks": sp["clocks"], "parareal": par}
+        print(json.dumps(line), flush=True)
+
+
 # ----------------------------------------------------------------------------- main
 def main():
     args = parse()
     D = Dist()
     from paper_1309_1889_b200 import fixtures as fx
-    if args.workload != "step" and args.impl == "ours":
-        sys.path.insert(0, str(ROOT / "tools"))
-        import bench_paths
-        bench_paths.run(args, D, METRIC, UNIT)
+    if D.world > 1:
+        multi_gpu(args, D)
         D.close()
         return
 
@@ -221,8 +385,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded; paper_1309_1889_b200/fixtures.py)",
             "config": {"workload": CONFIG_TEXT.get(name, name), "n_atoms": int(w.n), "a": w.a, "h": w.h,
-                       "levels": w.levels, "dt_fs": w.dt, "parallelism": f"replicas x{D.world}" if D.world > 1
-                       else "single GPU", "l2": "256 MB buffer written before every timed step (outside the "
+                       "levels": w.levels, "dt_fs": w.dt, "parallelism": "single GPU", "l2": "256 MB buffer written before every timed step (outside the "
                        "events); per-step working set ~230 MB (incl. 147 MB of pair masks)"}}
 
     if args.impl == "reference":
@@ -232,15 +395,29 @@ def main():
                 est = reference_step_estimate(w, 30000, 100 + k)
                 if k >= args.warmup:
                     times.append(est)
-            t = float(np.mean([e["t_step_s"] for e in times]))
+            t_sr_ext = float(np.mean([e["t_step_s"] - e["t_grid_s"] for e in times]))
+            t_grid = float(np.mean([e["t_grid_s"] for e in times]))
+            calib = None
+            if not args.no_full_reference:
+                # one FULL-size reference short_range (all N(N-1)/2 pair checks, ~1-2 min): the
+                # sample extrapolation runs from cache, the full call from memory
+                calib = reference_full_short_range(w)
+            t_sr = calib["t_full_s"] if calib else t_sr_ext
+            t = t_sr + t_grid
             val = w.n / t
             line = dict(base, impl="reference", value=val, ms_per_step=t * 1e3, n_gpus=D.world,
                         cpu_baseline={"value": val, "unit": UNIT, "cores": cpu_threads_used(),
                                       "kind": times[0]["kind"],
-                                      "sample": f"per step: reference short_range on a random {times[0]['sample_atoms']}"
-                                                f"-atom subset of the same box scaled by its N(N-1)/2 pair-check count "
-                                                f"+ reference grid phases at full N ({times[0]['t_grid_s']:.2f} s); "
-                                                f"single-threaded (msm_potential has no threading)"},
+                                      "sample": (f"per step: the reference short_range timed ONCE at full size "
+                                                 f"({calib['t_full_s']:.1f} s for N={w.n}) + reference grid phases at "
+                                                 f"full N ({t_grid:.2f} s per step); " if calib else "")
+                                                + f"per-step samples: short_range on a random "
+                                                  f"{times[0]['sample_atoms']}-atom subset scaled by N(N-1)/2 pair "
+                                                  f"checks -> {t_sr_ext:.1f} s (the sample is cache-resident, "
+                                                  f"hence faster per pair); single-threaded (msm_potential has no "
+                                                  f"threading)",
+                                      "short_range_full_s": calib["t_full_s"] if calib else None,
+                                      "short_range_extrapolated_s": t_sr_ext},
                         e2e={"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
             print(json.dumps(line), flush=True)
         D.close()
@@ -342,6 +519,35 @@ def main():
                        "+ K steps, D2H of positions/velocities); host wall clock, max over ranks"}
         L.msmb_host_free(ptr)
 
+    # ---- the rebuild-inclusive cost: skin 0 rebuilds the pair list (clusters, boxes,
+    # lists, masks) at every evaluation, as at a dt where atoms cross skin/2 every step
+    field.set_pair_skin(0.0)
+    dev0 = pkg.DeviceSystem(field, s)
+    step0 = np.zeros(K + 2)
+    stage0 = np.zeros(11)
+    names0 = (C.c_char_p * 11)()
+    l0 = C.c_int64()
+    L.msmb_bench_propagate(field.handle, dev0._h, dt, max(W, 1), int(not args.no_flush), step0.ctypes.data_as(pkg._D),
+                           stage0.ctypes.data_as(pkg._D), names0, C.byref(l0))
+    pkg._check(field.handle, L.msmb_bench_propagate(field.handle, dev0._h, dt, K, int(not args.no_flush),
+                                                    step0.ctypes.data_as(pkg._D), stage0.ctypes.data_as(pkg._D),
+                                                    names0, C.byref(l0)))
+    rb_ms = float(step0[1:K + 1].sum()) / K
+    rebuild_line = {"ms_per_step": rb_ms, "value": w.n / (rb_ms * 1e-3),
+                    "list_rebuilds": field.work_counters()["list_rebuilds"],
+                    "note": "pair-list skin 0: the cluster pair list (clusters, boxes, list, masks) is rebuilt at "
+                            "every evaluation -- the cost of a step at a dt (e.g. C2's literal 1 fs) where atoms "
+                            "cross skin/2 every step; the headline steps (dt 0.02 fs) rebuild once per call"}
+    del dev0
+
+    scaling_base = None
+    if not args.no_scaling_base:
+        _, sp = spatial_run(D, max(3, K // 4), 1)
+        scaling_base = {"spatial_c3s_1gpu": {k: sp[k] for k in ("value", "ms_per_step", "e2e", "config")},
+                        "parareal_c5s_1gpu": parareal_run_line(D, 1),
+                        "note": "the --gpus N > 1 lines' workloads (C3-S spatial, C5-S parareal) through the same "
+                                "code paths at one GPU, for scaling efficiency against the N > 1 lines"}
+
     cpu = None
     if D.rank == 0 and D.world == 1 and not args.no_cpu_baseline:
         est = reference_step_estimate(w, 40000, 7)
@@ -373,6 +579,8 @@ def main():
             "stage_ms_per_eval": {k: round(v, 5) for k, v in per_step.items()},
             "cpu_baseline": cpu,
             "work": counters,
+            "rebuild_every_step": rebuild_line,
+            "scaling_base": scaling_base,
         })
         print(json.dumps(line), flush=True)
     D.close()

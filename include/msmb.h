@@ -290,42 +290,58 @@ int msmb_state_rms_change_device(msmb_field* f, int64_t n, const double* a, cons
 int msmb_system_set_state_device(msmb_system* s, const double* state);
 int msmb_system_get_state_device(const msmb_system* s, double* state);
 
-/* ---- spatial decomposition: one part per GPU -------------
- * Every part holds the whole particle state (a msmb_system).  A part owns an
- * x-range of pair columns (pair sum, interpolation, forces and Verlet update of
- * the atoms binned there) and an x-range of output planes on every grid level
- * (anterpolation, lattice cutoff).  A step is four phases, with an exchange of the
- * phase's buffer between consecutive phases:
- *   phase 0  binning, owned pair sum + anterpolation   -> xbuf: level-0 charges
- *   phase 1  restriction, owned lattice cutoff         -> xbuf: level potentials
- *   phase 2  top level, prolongation, owned interpolation, forces, energy share
- *            (*energy), owned Verlet update (`kicks` half-kicks, then a drift
- *            if `drift`)                               -> xbuf: positions (3 n),
- *                                                         velocities (3 n)
- *   phase 3  import the exchanged positions (the first 3 n entries of xin).
- *   phase 4  import exchanged velocities (entries 3 n .. 6 n of xin).
- * Ownership of atoms only changes when the pair list is rebuilt, and a part reads
- * velocities of owned atoms only, so velocities need not travel every step:
- * phase 0 sets *energy = 1 when this evaluation rebuilt the list (0 otherwise);
- * the driver then exchanges the velocity half of the previous phase-2 buffer
- * (written under the old ownership) and imports it with phase 4 before phase 2,
- * and does the same once at the end of a call.  Positions are exchanged every
- * step.  xbuf is device memory of the field's GPU holding doubles as int64 bit
- * patterns; entries a part does not own are INT64_MIN, so an element-wise int64
- * MAX all-reduce of the buffers (e.g. NCCL) gives every part the owners' exact
- * values.  Sizes (msmb_dd_sizes) are [level-0 points, all level points, 6 n]
- * int64 for the three exchanges.  The decomposed trajectory is bit-identical to
- * msmb_system_propagate's.  Binning errors are detected identically on every
- * part (phase 0 returns the reference's error everywhere).  The driver is
- * paper_1309_1889_b200/parallel.py. */
-/* Work plan of `part` (no GPU needed): out = [ncx, cx0, cx1, levels,
- * (d0_k, plane0_k, plane1_k) per level]; cap >= 4 + 3 * levels. */
+/* ---- spatial decomposition plans ----------------------------
+ * Work plan of `part` of an nparts-way slab decomposition (msmb_slab_* below; no
+ * GPU needed): out = [ncx, cx0, cx1, levels, (d0_k, plane0_k, plane1_k) per level],
+ * the part's pair columns [cx0, cx1) and its x-planes on every level;
+ * cap >= 4 + 3 * levels. */
 int msmb_dd_plan(const msmb_msm_config* cfg, const msmb_units* units, const double box[3], int64_t n,
                  int nparts, int part, int* out, int cap);
-int msmb_dd_set_part(msmb_field* f, int nparts, int part);
-int msmb_dd_sizes(msmb_field* f, msmb_system* s, int64_t* out3);
-int msmb_dd_phase(msmb_field* f, msmb_system* s, int phase, double dt, int kicks, int drift,
-                  const msmb_units* units, const void* xin, void* xout, double* energy);
+
+/* ---- spatial slab decomposition over GPUs ----------------
+ * propagate(spec, s, units) (src/integrate.cpp:13-36) over msm_potential
+ * (src/msm.cpp:52-90) split into x-slabs of pair columns, one part per GPU
+ * (csrc/msmb_slab.cu).  A part owns the atoms binned into its columns and the
+ * x-planes of its slab on every grid level; it keeps halo copies of the atoms its
+ * pair lists and anterpolation read, and fetches the lattice planes its stencils
+ * read (R = ceil(2a/h) charge planes for the lattice cutoff, the restriction and
+ * prolongation windows, the interpolation window; the top level whole).  Per
+ * step only halo positions and those planes travel (ncclSend/Recv); at a pair-list
+ * rebuild (the single-GPU rule, decided globally) atoms migrate to the part owning
+ * their new column.  With the direct lattice method on the single-GPU run the
+ * decomposed trajectory is bitwise the single-GPU one; the energy is the sum of
+ * the parts' shares in part order.
+ *
+ * Two transports:
+ *  - one process per GPU: nfields = 1, nparts = world size, rank = this process's
+ *    rank, and either nccl_id (128 bytes from msmb_nccl_unique_id on rank 0,
+ *    distributed by the caller) or nccl_comm (an existing ncclComm_t);
+ *  - local: nfields = nparts fields (distinct handles; typically one per device,
+ *    several on one device for tests), all parts driven by this process, the
+ *    exchanges as stream-ordered copies; nccl_id / nccl_comm unused.
+ * Only MSM fields (no overlay).  With nparts > 1 the lattice cutoff runs as the
+ * direct stencil on the owned planes (msmb_set_lattice_method(f, 1) is set). */
+typedef struct msmb_slab msmb_slab;
+int msmb_nccl_unique_id(void* id128);
+int msmb_slab_create(msmb_field* const* fields, int nfields, int nparts, int rank, const void* nccl_id,
+                     void* nccl_comm, msmb_slab** out);
+void msmb_slab_destroy(msmb_slab* d);
+/* Every process passes the caller's whole system (host AoS arrays, as
+ * msmb_propagate); on success pos/vel hold the whole final state on every
+ * process and *energy the last evaluation's energy.  step_ms (optional, steps + 2
+ * entries): device times of the initial evaluation, each step and the closing
+ * half-kick on this process's first part.  Errors: the reference's exception of
+ * the earliest failing step, the same on every part (msmb_slab_last_error). */
+int msmb_slab_propagate(msmb_slab* d, int64_t n, double* pos_xyz, double* vel_xyz, const double* q,
+                        const double* mass, const double box[3], double dt, int steps, const msmb_units* units,
+                        double* energy, double* step_ms);
+/* [0] bytes received per step by one part (max over the call's steps and this
+ * process's parts), [1] bytes received in the last rebuild's exchanges, [2] owned
+ * atoms and [3] halo atoms of this process's first part, [4] rebuilds, [5] atoms
+ * migrated away from this process's parts, [6] parts.  Returns the count written. */
+int msmb_slab_stats(msmb_slab* d, int64_t* out, int cap);
+int msmb_slab_last_error(const msmb_slab* d, int* kind, int64_t* idx_i, int64_t* idx_j, int* step, char* msg,
+                         int cap);
 
 /* ---- measurement ------------------------------------------------------------ */
 /* When enabled, every evaluation records CUDA events around each stage on the

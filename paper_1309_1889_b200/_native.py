@@ -75,10 +75,13 @@ SIGNATURES = {
     "msmb_set_list_reuse": (C.c_int, [_VP, C.c_int]),
     "msmb_dd_plan": (C.c_int, [C.POINTER(MsmConfigC), C.POINTER(UnitsC), _D, C.c_int64, C.c_int, C.c_int, _I,
                               C.c_int]),
-    "msmb_dd_set_part": (C.c_int, [_VP, C.c_int, C.c_int]),
-    "msmb_dd_sizes": (C.c_int, [_VP, _VP, _L]),
-    "msmb_dd_phase": (C.c_int, [_VP, _VP, C.c_int, C.c_double, C.c_int, C.c_int, C.POINTER(UnitsC), _VP, _VP,
-                                _D]),
+    "msmb_nccl_unique_id": (C.c_int, [_VP]),
+    "msmb_slab_create": (C.c_int, [C.POINTER(_VP), C.c_int, C.c_int, C.c_int, _VP, _VP, C.POINTER(_VP)]),
+    "msmb_slab_destroy": (None, [_VP]),
+    "msmb_slab_propagate": (C.c_int, [_VP, C.c_int64, _D, _D, _D, _D, _D, C.c_double, C.c_int, C.POINTER(UnitsC),
+                                      _D, _D]),
+    "msmb_slab_stats": (C.c_int, [_VP, _L, C.c_int]),
+    "msmb_slab_last_error": (C.c_int, [_VP, C.POINTER(C.c_int), _L, _L, C.POINTER(C.c_int), C.c_char_p, C.c_int]),
     "msmb_state_sub_device": (C.c_int, [_VP, C.c_int64, _VP, _VP, _VP, _D]),
     "msmb_state_add_device": (C.c_int, [_VP, C.c_int64, _VP, _VP, _VP]),
     "msmb_state_rms_change_device": (C.c_int, [_VP, C.c_int64, _VP, _VP, _D]),

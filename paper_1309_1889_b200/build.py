@@ -31,7 +31,8 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp
 CXX = shutil.which("g++") or "g++"
 CC = "/usr/bin/gcc" if Path("/usr/bin/gcc").exists() else (shutil.which("gcc") or "gcc")
 
-CU_SOURCES = ["msmb_kernels.cu", "msmb_engine.cu", "msmb_parareal.cu", "msmb_dd.cu", "msmb_fft.cu", "msmb_direct.cu"]
+CU_SOURCES = ["msmb_kernels.cu", "msmb_engine.cu", "msmb_parareal.cu", "msmb_dd.cu", "msmb_slab.cu", "msmb_fft.cu",
+              "msmb_direct.cu"]
 CPP_SOURCES = ["msmb_geometry.cpp"]
 HEADERS = ["msmb_internal.h", "msmb_kernels.cuh", "msmb_engine.cuh"]
 

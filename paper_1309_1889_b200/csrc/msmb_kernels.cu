@@ -124,11 +124,14 @@ __device__ __forceinline__ int scell_of(const BinP& p, int cx, int cy, int cz) {
 // ============================================================================
 // K1: binning (bit-exact level-0 cell triple) + stable counting sort
 // ============================================================================
+// list != nullptr: bin only the atoms list[0..n) (a spatial-decomposition part's
+// owned + halo atoms, msmb_slab.cu); the others keep no key
 __global__ void k_bin(int n, const double* __restrict__ x, const double* __restrict__ y,
                       const double* __restrict__ z, BinP p, int* key, int* rank, int* count,
-                      int* outlist, ErrRec* err) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n || failed(err)) return;
+                      int* outlist, ErrRec* err, const int* __restrict__ list) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n || failed(err)) return;
+    const int i = list ? list[t] : t;
     const double px[3] = {x[i], y[i], z[i]};
     int c[3];
     bool ok = true;
@@ -259,10 +262,16 @@ static int scan_exclusive(cudaStream_t st, const int* in, int* out, int* tmp, in
     return 3;
 }
 
+int launch_scan_exclusive(cudaStream_t st, const int* in, int* out, int* tmp, int64_t m) {
+    return scan_exclusive(st, in, out, tmp, m);
+}
+
 __global__ void k_scatter(int n, const int* __restrict__ key, const int* __restrict__ rank,
-                          const int* __restrict__ start, int* perm, const ErrRec* err) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n || failed(err)) return;
+                          const int* __restrict__ start, int* perm, const ErrRec* err,
+                          const int* __restrict__ list) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n || failed(err)) return;
+    const int i = list ? list[t] : t;
     const int k = key[i];
     if (k >= 0) perm[start[k] + rank[i]] = i;
 }
@@ -332,20 +341,21 @@ __global__ void k_gather(int n, const int* __restrict__ start_total, const int* 
 }
 
 int launch_bin(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& a, DevCells& c,
-               ErrRec* err) {
-    const int n = int(s.n);
+               ErrRec* err, const int* list, int64_t nlist) {
+    const int n = list ? int(nlist) : int(s.n);
     cudaMemsetAsync(c.count, 0, sizeof(int) * size_t(g.ncells + 1), st);
     if (n > 0)
         k_bin<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, s.x, s.y, s.z, make_binp(g), a.key, a.rank,
-                                               c.count, a.outlist, err);
+                                               c.count, a.outlist, err, list);
     return n > 0 ? 1 : 0;
 }
 
 int launch_sort(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& a, DevCells& c,
-                ErrRec* err) {
-    const int n = int(s.n);
+                ErrRec* err, const int* list, int64_t nlist) {
+    const int n = list ? int(nlist) : int(s.n);
     int l = scan_exclusive(st, c.count, c.start, c.scan_tmp, g.ncells + 1);
-    if (n > 0) k_scatter<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, a.key, a.rank, c.start, a.perm, err);
+    if (n > 0)
+        k_scatter<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, a.key, a.rank, c.start, a.perm, err, list);
     // always: also publishes the (possibly empty) natural-order cell ranges read by k_anterp
     k_cellsort<<<int((g.ncells + 255) / 256), 256, 0, st>>>(g.ncells, make_binp(g), c.start, a.perm,
                                                             c.nat, s.x, s.y, s.z, err);
@@ -1055,7 +1065,7 @@ __global__ void k_err_brute(int64_t n, const double* __restrict__ x, const doubl
 // conditional node to the capturing graph returned cudaErrorInvalidValue on this
 // driver/runtime, so the early-exit launches stay.
 int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
-                    DevCells& c, ErrRec* err, int cap, const Part& P, int force_rebuild) {
+                    DevCells& c, ErrRec* err, int cap, const Part& P, int force_rebuild, int disp) {
     const int cells_per_col = int(g.lv[0].dims[2]) * g.cw * g.cw;
     const int64_t nc = g.ncols;
     const int nb = int((n + 255) / 256) > 0 ? int((n + 255) / 256) : 1;
@@ -1063,7 +1073,7 @@ int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevStat
     const int key = P.cx0 * 65536 + P.cx1;
     k_flag_reset<<<1, 1, 0, st>>>(c.flag, force_rebuild || !(g.skin > 0.0) ? 1 : 0, key);
     const double hs = 0.5 * g.skin;
-    k_disp<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, s.x, s.y, s.z, a.ref, hs * hs, c.flag);
+    if (disp) k_disp<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, s.x, s.y, s.z, a.ref, hs * hs, c.flag);
     k_cl_perm<<<nb, 256, 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, a.cl_perm, a.cl_inv, a.ref, c.flag, key);
     k_gather_cl<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(c.flag, a.cl_perm, s.x, s.y, s.z, s.q, a.xc, a.yc,
                                                                      a.zc, a.qc, err);
@@ -1526,14 +1536,15 @@ __device__ __forceinline__ double restrict_point(const XferP& p, int I, int J, i
 constexpr int kRTx = 4, kRTy = 4, kRTz = 8;
 constexpr int kRFx = 2 * kRTx + 6, kRFy = 2 * kRTy + 6, kRFz = 2 * kRTz + 6;
 
+// xlo/xhi: the coarse x-planes to compute (a spatial-decomposition part's own)
 template <bool BITWISE>
 __global__ void __launch_bounds__(kRTx * kRTy * kRTz)
-    k_restrict_tile(XferP p, const double* __restrict__ fine, double* coarse, const ErrRec* err) {
+    k_restrict_tile(XferP p, const double* __restrict__ fine, double* coarse, const ErrRec* err, int xlo, int xhi) {
     __shared__ double tile[kRFx * kRFy * kRFz];
     if (failed(err)) return;
     const int tz_n = (p.cd[2] + kRTz - 1) / kRTz, ty_n = (p.cd[1] + kRTy - 1) / kRTy;
     const int bz = blockIdx.x % tz_n, by = (blockIdx.x / tz_n) % ty_n, bx = blockIdx.x / (tz_n * ty_n);
-    const int I0 = bx * kRTx, J0 = by * kRTy, K0 = bz * kRTz;
+    const int I0 = xlo + bx * kRTx, J0 = by * kRTy, K0 = bz * kRTz;
     const int fi0 = 2 * I0 - 5, fj0 = 2 * J0 - 5, fk0 = 2 * K0 - 5;
     constexpr int kTile = kRFx * kRFy * kRFz;
     // the whole tile in one batch of asynchronous 8-byte copies (zero-filled outside
@@ -1550,7 +1561,7 @@ __global__ void __launch_bounds__(kRTx * kRTy * kRTz)
     __syncthreads();
     const int tz = threadIdx.x % kRTz, ty = (threadIdx.x / kRTz) % kRTy, tx = threadIdx.x / (kRTz * kRTy);
     const int I = I0 + tx, J = J0 + ty, K = K0 + tz;
-    if (I >= p.cd[0] || J >= p.cd[1] || K >= p.cd[2]) return;
+    if (I >= xhi || J >= p.cd[1] || K >= p.cd[2]) return;
     double v;
     if (BITWISE) {
         v = restrict_point(p, I, J, K, [&](int i, int j, int k) {
@@ -1630,26 +1641,30 @@ __global__ void k_prolong(XferP p, const double* __restrict__ coarse, double* fi
     prolong_point(p, coarse, fine, idx);
 }
 
-static int restrict_blocks(const XferP& p) {
-    return ((p.cd[0] + kRTx - 1) / kRTx) * ((p.cd[1] + kRTy - 1) / kRTy) * ((p.cd[2] + kRTz - 1) / kRTz);
+static int restrict_blocks(const XferP& p, int nx) {
+    return ((nx + kRTx - 1) / kRTx) * ((p.cd[1] + kRTy - 1) / kRTy) * ((p.cd[2] + kRTz - 1) / kRTz);
 }
 
 int launch_restrict_all(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err) {
     int l = 0;
-    for (int k = 0; k + 1 < g.levels; ++k) {
-        const XferP p = make_xfer(g, k, L);
-        k_restrict_tile<false><<<restrict_blocks(p), kRTx * kRTy * kRTz, 0, st>>>(
-            p, L.charge + g.lv[k].offset, L.charge + g.lv[k + 1].offset, err);
-        ++l;
-    }
+    for (int k = 0; k + 1 < g.levels; ++k) l += launch_restrict_planes(st, g, k, L, err, 0, g.lv[k + 1].dims[0]);
     return l;
+}
+
+// production restriction k -> k+1 of the coarse x-planes [xlo, xhi)
+int launch_restrict_planes(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err, int xlo, int xhi) {
+    const XferP p = make_xfer(g, k, L);
+    if (xhi <= xlo) return 0;
+    k_restrict_tile<false><<<restrict_blocks(p, xhi - xlo), kRTx * kRTy * kRTz, 0, st>>>(
+        p, L.charge + g.lv[k].offset, L.charge + g.lv[k + 1].offset, err, xlo, xhi);
+    return 1;
 }
 
 // bit-exact restriction of one level (msmb_debug_stage; tests/test_gpu_stages.py)
 int launch_restrict(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err) {
     const XferP p = make_xfer(g, k, L);
-    k_restrict_tile<true><<<restrict_blocks(p), kRTx * kRTy * kRTz, 0, st>>>(p, L.charge + g.lv[k].offset,
-                                                                            L.charge + g.lv[k + 1].offset, err);
+    k_restrict_tile<true><<<restrict_blocks(p, p.cd[0]), kRTx * kRTy * kRTz, 0, st>>>(
+        p, L.charge + g.lv[k].offset, L.charge + g.lv[k + 1].offset, err, 0, p.cd[0]);
     return 1;
 }
 
@@ -1659,14 +1674,15 @@ int launch_restrict(cudaStream_t st, const Geometry& g, int k, DevLevels& L, Err
 constexpr int kPx = 4, kPy = 8, kPz = 8;
 constexpr int kPCx = kPx / 2 + 5, kPCy = kPy / 2 + 5, kPCz = kPz / 2 + 5;
 
+// xlo/xhi: the fine x-planes to update (a spatial-decomposition part's own)
 __global__ void __launch_bounds__(kPx * kPy * kPz)
-    k_prolong_tile(XferP p, const double* __restrict__ coarse, double* fine, const ErrRec* err) {
+    k_prolong_tile(XferP p, const double* __restrict__ coarse, double* fine, const ErrRec* err, int xlo, int xhi) {
     __shared__ double ct[kPCx * kPCy * kPCz];
     if (failed(err)) return;
     const int tz_n = (p.fd[2] + kPz - 1) / kPz, ty_n = (p.fd[1] + kPy - 1) / kPy;
     const int bz = blockIdx.x % tz_n, by = (blockIdx.x / tz_n) % ty_n, bx = blockIdx.x / (tz_n * ty_n);
-    const int I0 = bx * kPx, J0 = by * kPy, K0 = bz * kPz;
-    const int I1 = min(I0 + kPx, p.fd[0]) - 1, J1 = min(J0 + kPy, p.fd[1]) - 1, K1 = min(K0 + kPz, p.fd[2]) - 1;
+    const int I0 = xlo + bx * kPx, J0 = by * kPy, K0 = bz * kPz;
+    const int I1 = min(I0 + kPx, xhi) - 1, J1 = min(J0 + kPy, p.fd[1]) - 1, K1 = min(K0 + kPz, p.fd[2]) - 1;
     const int cx0 = p.base[0][I0], cy0 = p.base[1][J0], cz0 = p.base[2][K0];
     const int nx = p.base[0][I1] + 4 - cx0, ny = p.base[1][J1] + 4 - cy0, nz = p.base[2][K1] + 4 - cz0;
     if (nx > kPCx || ny > kPCy || nz > kPCz) { // not expected (base ~ i/2); stay exact without staging
@@ -1709,9 +1725,16 @@ __global__ void __launch_bounds__(kPx * kPy * kPz)
 }
 
 int launch_prolong(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err) {
+    return launch_prolong_planes(st, g, k, L, err, 0, g.lv[k].dims[0]);
+}
+
+// prolongation k+1 -> k into the fine x-planes [xlo, xhi)
+int launch_prolong_planes(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err, int xlo, int xhi) {
     const XferP p = make_xfer(g, k, L);
-    const int blocks = ((p.fd[0] + kPx - 1) / kPx) * ((p.fd[1] + kPy - 1) / kPy) * ((p.fd[2] + kPz - 1) / kPz);
-    k_prolong_tile<<<blocks, kPx * kPy * kPz, 0, st>>>(p, L.pot + g.lv[k + 1].offset, L.pot + g.lv[k].offset, err);
+    if (xhi <= xlo) return 0;
+    const int blocks = ((xhi - xlo + kPx - 1) / kPx) * ((p.fd[1] + kPy - 1) / kPy) * ((p.fd[2] + kPz - 1) / kPz);
+    k_prolong_tile<<<blocks, kPx * kPy * kPz, 0, st>>>(p, L.pot + g.lv[k + 1].offset, L.pot + g.lv[k].offset, err,
+                                                       xlo, xhi);
     return 1;
 }
 
@@ -2669,78 +2692,6 @@ int launch_kick(cudaStream_t st, DevState& s, const DevOut& o, double dt, double
     const double hdc = 0.5 * dt * conv;
     k_kick<<<atom_blocks(s.n, atom_tpb(s.n)), atom_tpb(s.n), 0, st>>>(s.n, s.vx, s.vy, s.vz, s.m, o.fx, o.fy, o.fz, hdc,
                                                    err);
-    return 1;
-}
-
-// Spatial decomposition (msmb_dd.cu): the same Verlet arithmetic restricted to the
-// atoms binned into the owned pair columns (sorted range -> original index).
-// Verlet update of the atoms a part owns (binned into its pair columns), in original
-// order with the ownership test through cl_inv: coalesced state traffic (a cluster-
-// order walk scatters over the whole state, measured 5.3 vs ~0.3 ms at C3)
-__global__ void k_verlet_part(const int* __restrict__ colstart, int col_a, int col_b,
-                              const int* __restrict__ inv, DevState s, const double* __restrict__ fx,
-                              const double* __restrict__ fy, const double* __restrict__ fz, double dt,
-                              double hdc, int kicks, int drift, const ErrRec* err) {
-    if (failed(err)) return;
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= s.n) return;
-    const int t = inv[i];
-    if (t < colstart[col_a] || t >= colstart[col_b]) return;
-    const double c = __ddiv_rn(hdc, s.m[i]);
-    double a = s.vx[i], b = s.vy[i], d = s.vz[i];
-    const double Fx = fx[i], Fy = fy[i], Fz = fz[i];
-    for (int k = 0; k < kicks; ++k) {
-        a = __dadd_rn(a, __dmul_rn(Fx, c));
-        b = __dadd_rn(b, __dmul_rn(Fy, c));
-        d = __dadd_rn(d, __dmul_rn(Fz, c));
-    }
-    s.vx[i] = a;
-    s.vy[i] = b;
-    s.vz[i] = d;
-    if (drift) {
-        s.x[i] = __dadd_rn(s.x[i], __dmul_rn(a, dt));
-        s.y[i] = __dadd_rn(s.y[i], __dmul_rn(b, dt));
-        s.z[i] = __dadd_rn(s.z[i], __dmul_rn(d, dt));
-    }
-}
-
-__global__ void k_export_state(const int* __restrict__ colstart, int col_a, int col_b,
-                               const int* __restrict__ inv, DevState s, int64_t n, long long* xbuf) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int t = inv[i];
-    if (t < colstart[col_a] || t >= colstart[col_b]) return;
-    const double* src[6] = {s.x, s.y, s.z, s.vx, s.vy, s.vz};
-#pragma unroll
-    for (int k = 0; k < 6; ++k) xbuf[k * n + i] = __double_as_longlong(src[k][i]);
-}
-
-__global__ void k_fill_i64(long long* p, int64_t count, long long v) {
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x)
-        p[i] = v;
-}
-
-int launch_verlet_part(cudaStream_t st, const Geometry& g, const DevCells& c, const DevAtoms& a,
-                       DevState& s, const DevOut& o, double dt, double conv, int kicks, int drift,
-                       const Part& P, ErrRec* err) {
-    if (s.n == 0 || (kicks == 0 && !drift)) return 0;
-    const double hdc = 0.5 * dt * conv;
-    k_verlet_part<<<int((s.n + 255) / 256), 256, 0, st>>>(c.colstart, P.cx0 * g.ncy, P.cx1 * g.ncy, a.cl_inv,
-                                                           s, o.fx, o.fy, o.fz, dt, hdc, kicks, drift, err);
-    return 1;
-}
-
-int launch_export_state(cudaStream_t st, const Geometry& g, const DevCells& c, const DevAtoms& a,
-                        const DevState& s, long long* xbuf, const Part& P) {
-    if (s.n == 0) return 0;
-    k_export_state<<<int((s.n + 255) / 256), 256, 0, st>>>(c.colstart, P.cx0 * g.ncy, P.cx1 * g.ncy, a.cl_inv,
-                                                            s, s.n, xbuf);
-    return 1;
-}
-
-int launch_fill_i64(cudaStream_t st, long long* p, int64_t count, long long v) {
-    if (count <= 0) return 0;
-    k_fill_i64<<<592, 256, 0, st>>>(p, count, v);
     return 1;
 }
 

@@ -124,12 +124,16 @@ struct DevOut {         // per-atom outputs in original order (optional)
 
 // Launch wrappers (all asynchronous on `st`).  Each returns the number of kernel
 // launches issued so the engine can count them.
+// exclusive scan of int[m] (tmp: >= (m + 4095) / 4096 + 8 ints)
+int launch_scan_exclusive(cudaStream_t st, const int* in, int* out, int* tmp, int64_t m);
+// list != nullptr: only the atoms list[0..nlist) (a spatial-decomposition part's local atoms)
 int launch_bin(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& a, DevCells& c,
-               ErrRec* err);
+               ErrRec* err, const int* list = nullptr, int64_t nlist = 0);
 int launch_sort(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& a, DevCells& c,
-                ErrRec* err);
+                ErrRec* err, const int* list = nullptr, int64_t nlist = 0);
+// disp = 0: no skin/2 displacement test (the caller decided the rebuild: force_rebuild)
 int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
-                    DevCells& c, ErrRec* err, int cap, const Part& P, int force_rebuild);
+                    DevCells& c, ErrRec* err, int cap, const Part& P, int force_rebuild, int disp = 1);
 int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
                  DevCells& c, ErrRec* err, int cap, const Part& P);
 int launch_err_brute(cudaStream_t st, int64_t n, const DevState& s, DevAtoms& a, ErrRec* err);
@@ -137,6 +141,8 @@ int launch_anterp(cudaStream_t st, const Geometry& g, DevAtoms& a, DevCells& c, 
                   ErrRec* err, const Part& P);
 int launch_restrict(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err);
 int launch_restrict_all(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
+int launch_restrict_planes(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err, int xlo, int xhi);
+int launch_prolong_planes(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err, int xlo, int xhi);
 int launch_prolong_all(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
 int launch_lattice(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err, const Part& P);
 size_t lattice_smem_bytes(const Geometry& g);
@@ -152,15 +158,7 @@ constexpr int64_t kTopFftMin = 4096; // FFT lattice mode: top levels above this 
 int launch_prolong(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err);
 int launch_interp(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c,
                   DevLevels& L, DevOut& o, ErrRec* err, int want_energy, const Part& P);
-// spatial decomposition (msmb_dd.cu): Verlet on the atoms of the owned pair columns
-// (kicks half-kicks, then a drift if `drift`), export of their state into a 6n
-// int64 exchange buffer (others INT64_MIN), and an int64 fill
-int launch_verlet_part(cudaStream_t st, const Geometry& g, const DevCells& c, const DevAtoms& a,
-                       DevState& s, const DevOut& o, double dt, double conv, int kicks, int drift,
-                       const Part& P, ErrRec* err);
-int launch_export_state(cudaStream_t st, const Geometry& g, const DevCells& c, const DevAtoms& a,
-                        const DevState& s, long long* xbuf, const Part& P);
-int launch_fill_i64(cudaStream_t st, long long* p, int64_t count, long long v);
+
 int launch_finalize(cudaStream_t st, const DevState& s, ErrRec* err, int pair_field = 0);
 // pair-only fields: per-atom outputs and energy from the pair sums (no grid)
 int launch_pair_out(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, DevCells& c, DevOut& o,

@@ -334,161 +334,87 @@ def parareal_run(v: ParticleSystem, total_points: int, cfg: PararealConfig, grou
 
 
 # ============================================================================ spatial
-def exchange_max_bits(tensors, group=None, use_dist: bool = True):
-    """Exact exchange of disjointly owned values (include/msmb.h, spatial decomposition).
-
-    `tensors` are the int64 views of one buffer on each local part. Unowned
-    entries are INT64_MIN, so an element-wise MAX over parts and ranks leaves
-    every owner's bit pattern in place. This also covers -0.0 (== INT64_MIN),
-    NaNs and infinities. Local parts are combined first, then the result is
-    all-reduced (MAX) over the ranks of `group` and copied back to every local
-    part.
-    """
-    import torch
-    m = tensors[0]
-    if len(tensors) > 1:
-        m = tensors[0].clone()
-        for t in tensors[1:]:
-            torch.maximum(m, t, out=m)
-    dist = _dist() if use_dist else None
-    if dist is not None and dist.get_world_size(group) > 1:
-        dist.all_reduce(m, op=dist.ReduceOp.MAX, group=group)
-    for t in tensors:
-        if t is not m:
-            t.copy_(m)
-    return m
-
-
 class SpatialDecomposition:
-    """MSM force + velocity-Verlet propagation split over parts.
+    """MSM force + velocity-Verlet propagation split into x-slabs over GPUs
+    (SURVEY.md 8(e) E1), driven by the C++ engine (csrc/msmb_slab.cu, msmb_slab_*).
 
-    One part per process/GPU under torchrun (``group``, default: the whole job),
-    or ``local_parts`` parts in this process (one GPU). The latter runs the
-    identical phase/exchange sequence; the tests use it to check the decomposed
-    trajectory against the single-GPU one. Every part holds the whole particle
-    state, owns an x-slab of the work, and exchanges exactly (see
-    csrc/msmb_dd.cu and include/msmb.h). Results equal
-    ``propagate(PropagatorSpec(MsmField(config), dt, steps), s)`` bit for bit.
-    Only the energy differs: it is summed per part.
+    * Under torchrun (``group`` or the default process group with world > 1):
+      one part per process/GPU.  Rank 0 creates an NCCL unique id
+      (msmb_nccl_unique_id), torch.distributed broadcasts the 128 bytes, and
+      every rank joins the library's own NCCL communicator; all halo and plane
+      exchanges then run inside the C++ step (ncclSend/Recv), with no Python in
+      the loop.
+    * ``local_parts = P``: P parts driven by this process (one field per part, on
+      ``devices`` or all on the current device), exchanging by stream-ordered
+      copies -- the same plans and kernels, used by the tests to check the
+      decomposed trajectory against the single-GPU one bit for bit.
+
+    ``propagate(dt, steps)`` is propagate(spec, s, units) (src/integrate.cpp:13-36)
+    on the whole system; every rank passes and receives the whole state.
     """
 
     def __init__(self, config, system: ParticleSystem, units=None, group=None, local_parts: int = 0,
-                 device: Optional[int] = None):
-        import torch
-        from . import DeviceSystem, UnitsConfig
-        self.torch = torch
-        self.group = group
+                 device: Optional[int] = None, devices=None):
+        from . import UnitsConfig
         self.units = units or UnitsConfig.physical()
-        self._uc = self.units._c()
-        if local_parts:
-            nparts, mine, self.distributed = int(local_parts), list(range(int(local_parts))), False
-        else:
-            comm = _Comm(group)
-            nparts, mine, self.distributed = comm.world, [comm.rank], comm.world > 1
-        self.nparts = nparts
-        dev = torch.cuda.current_device() if device is None else device
-        self.device = torch.device("cuda", dev)
-        lib = _native.lib()
-        self.lib = lib
-        self.parts = []
-        for p in mine:
-            f = MsmField(config, self.units, device=dev)
-            _check(f.handle, lib.msmb_dd_set_part(f.handle, nparts, p))
-            ds = DeviceSystem(f, system)
-            sizes = np.zeros(3, dtype=np.int64)
-            _check(f.handle, lib.msmb_dd_sizes(f.handle, ds._h, sizes.ctypes.data_as(C.POINTER(C.c_int64))))
-            bufs = [torch.empty(int(max(sz, 1)), dtype=torch.int64, device=self.device) for sz in sizes]
-            self.parts.append((f, ds, bufs))
         self.system = system
         self.n = system.size()
-        self.exchanged_bytes = 0
+        lib = _native.lib()
+        self.lib = lib
+        self._h = C.c_void_p()
+        if local_parts:
+            nparts = int(local_parts)
+            devs = list(devices) if devices else [0 if device is None else device] * nparts
+            self.fields = [MsmField(config, self.units, device=devs[k % len(devs)]) for k in range(nparts)]
+            arr = (C.c_void_p * nparts)(*[f.handle for f in self.fields])
+            rc = lib.msmb_slab_create(arr, nparts, nparts, 0, None, None, C.byref(self._h))
+            self.rank, self.world = 0, nparts
+        else:
+            import torch
+            comm = _Comm(group)
+            self.rank, self.world = comm.rank, comm.world
+            dev = torch.cuda.current_device() if device is None else device
+            self.fields = [MsmField(config, self.units, device=dev)]
+            arr = (C.c_void_p * 1)(self.fields[0].handle)
+            idbuf = (C.c_ubyte * 128)()
+            if self.world > 1:
+                if self.rank == 0:
+                    _check(self.fields[0].handle, lib.msmb_nccl_unique_id(idbuf))
+                obj = [bytes(idbuf)]
+                comm.dist.broadcast_object_list(obj, src=0, group=group)
+                C.memmove(idbuf, obj[0], 128)
+            # world == 1: one part, the local transport
+            rc = lib.msmb_slab_create(arr, 1, self.world, self.rank, idbuf if self.world > 1 else None, None,
+                                      C.byref(self._h))
+        _check(self.fields[0].handle, rc)
+        self.last_energy = 0.0
 
-    def _phase(self, phase: int, dt: float = 0.0, kicks: int = 0, drift: int = 0) -> float:
-        self.torch.cuda.current_stream(self.device).synchronize()
-        energy = 0.0
-        for f, ds, bufs in self.parts:
-            e = C.c_double()
-            xin = C.c_void_p(bufs[min(phase, 3) - 1].data_ptr()) if phase > 0 else None
-            xout = C.c_void_p(bufs[phase].data_ptr()) if phase < 3 else None
-            _check(f.handle, self.lib.msmb_dd_phase(f.handle, ds._h, phase, dt, kicks, drift, C.byref(self._uc),
-                                                    xin, xout, C.byref(e)))
-            energy += e.value
-        return energy
-
-    def _exchange(self, which: int, part: str = "all"):
-        """Exchange buffer `which`; for the state buffer (2) `part` selects the
-        positions ("pos", every step) or the velocities ("vel", after a list rebuild
-        and at the end of a call: ownership only changes at rebuilds)."""
-        bufs = [b[which] for _, _, b in self.parts]
-        if which == 2 and part != "all":
-            n3 = 3 * self.n
-            bufs = [b[:n3] if part == "pos" else b[n3:2 * n3] for b in bufs]
-        exchange_max_bits(bufs, self.group, use_dist=self.distributed)
-        self.exchanged_bytes += bufs[0].numel() * 8
-        self.torch.cuda.current_stream(self.device).synchronize()
-
-    def _energy_sum(self, e: float) -> float:
-        if not self.distributed:
-            return e
-        t = self.torch.tensor([e], dtype=self.torch.float64, device=self.device)
-        _dist().all_reduce(t, group=self.group)
-        return float(t.item())
-
-    def _state(self):
-        _, ds, _ = self.parts[0]
-        t = self.torch.empty(6 * self.n, dtype=self.torch.float64, device=self.device)
-        _check(self.parts[0][0].handle, self.lib.msmb_system_get_state_device(ds._h, C.c_void_p(t.data_ptr())))
-        return t
-
-    def _set_state(self, t):
-        for f, ds, _ in self.parts:
-            _check(f.handle, self.lib.msmb_system_set_state_device(ds._h, C.c_void_p(t.data_ptr())))
-
-    def propagate(self, dt: float, steps: int, download: bool = True):
-        """propagate(spec, s, units) (src/integrate.cpp:13-36): one evaluation, then
-        `steps` velocity-Verlet steps. Returns (final ParticleSystem, energy of the
-        last evaluation), or (None, energy) with download=False (the state stays on
-        the devices). On error the state is left as it was, and the reference's
-        exception is raised on every part."""
-        if not (dt > 0.0):
-            raise ConfigError("dt must be > 0")
-        if steps < 0:
-            raise ConfigError("steps_per_slice must be >= 1")
-        backup = self._state()
-        energy = 0.0
-        vel_pending = False  # velocities of the last phase 2 not yet exchanged
-        try:
-            for s in range(steps + 1):
-                if steps == 0:
-                    kicks, drift = 0, 0
-                elif s == 0:
-                    kicks, drift = 1, 1      # opening half-kick + drift of step 1
-                elif s < steps:
-                    kicks, drift = 2, 1      # closing kick of step s, opening kick + drift of s+1
-                else:
-                    kicks, drift = 1, 0      # closing half-kick of the last step
-                rebuilt = self._phase(0) > 0  # the (replicated) pair-list rebuild decision
-                if rebuilt and vel_pending:  # new owners need the old owners' velocities
-                    self._exchange(2, "vel")
-                    self._phase(4)
-                    vel_pending = False
-                self._exchange(0)
-                self._phase(1)
-                self._exchange(1)
-                energy = self._phase(2, dt, kicks, drift)
-                if kicks or drift:
-                    self._exchange(2, "pos")
-                    self._phase(3)
-                    vel_pending = True
-            if vel_pending:
-                self._exchange(2, "vel")
-                self._phase(4)
-        except Error:
-            self._set_state(backup)
-            raise
-        energy = self._energy_sum(energy)
-        if not download:
-            return None, energy
-        pos, vel = self.parts[0][1].download()
+    def propagate(self, dt: float, steps: int, download: bool = True, step_ms=None):
+        """Returns (final ParticleSystem, energy of the last evaluation); the
+        reference's exception on error (the same on every rank)."""
         s = self.system
-        return ParticleSystem(pos, vel, s.charges, s.masses, s.box), energy
+        pos = np.array(s.positions, dtype=np.float64, copy=True)
+        vel = np.array(s.velocities, dtype=np.float64, copy=True)
+        e = C.c_double()
+        u = self.units._c()
+        rc = self.lib.msmb_slab_propagate(self._h, self.n, _p(pos), _p(vel), _p(s.charges), _p(s.masses), _p(s.box),
+                                          float(dt), int(steps), C.byref(u), C.byref(e), _p(step_ms))
+        _check(self.fields[0].handle, rc)  # the error is set on every part's field
+        self.last_energy = e.value
+        out = ParticleSystem(pos, vel, s.charges, s.masses, s.box)
+        return (out if download else None), e.value
+
+    def stats(self) -> dict:
+        out = np.zeros(7, dtype=np.int64)
+        self.lib.msmb_slab_stats(self._h, out.ctypes.data_as(C.POINTER(C.c_int64)), 7)
+        keys = ["bytes_per_step", "bytes_rebuild", "owned", "halo", "rebuilds", "migrated", "parts"]
+        return dict(zip(keys, map(int, out)))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and h.value:
+            try:
+                _native.lib().msmb_slab_destroy(h)
+            except Exception:
+                pass
+            self._h = C.c_void_p()
