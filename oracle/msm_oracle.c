@@ -227,7 +227,12 @@ static int stencil_at(double t, int dims, st1d* st) {
     return 0;
 }
 
-/* ---- anterpolate: src/msm_phases.cpp:39-61 ---------------------------------- */
+/* ---- anterpolate: src/msm_phases.cpp:39-61 ----------------------------------
+ * The reference scatters particle by particle (index order).  Here each thread
+ * owns a range of x-planes and runs the same index-order loop, adding only into its
+ * planes: every grid point still receives its contributions in particle order, so
+ * the lattice is bitwise the reference's.  The coverage error is the first failing
+ * particle in index order (checked before any scatter). */
 static int anterpolate(int64_t n, const double* pos, const double* q, level_t* L0, char* msg,
                        int cap) {
     memset(L0->charge, 0, L0->size * sizeof(double));
@@ -239,13 +244,31 @@ static int anterpolate(int64_t n, const double* pos, const double* q, level_t* L
             stencil_at((pos[3 * p + 2] - L0->origin[2]) * inv_h, L0->dims[2], &sz))
             return fail(msg, cap, E_COVERAGE, "particle %lld outside grid coverage",
                         (long long)p);
-        const double qq = q[p];
-        for (int a = 0; a < 4; ++a) {
-            const double qa = qq * sx.w[a];
-            for (int b = 0; b < 4; ++b) {
-                const double qab = qa * sy.w[b];
-                for (int c = 0; c < 4; ++c)
-                    L0->charge[IDX(L0, sx.base + a, sy.base + b, sz.base + c)] += qab * sz.w[c];
+    }
+#pragma omp parallel
+    {
+        int nt = 1, me = 0;
+#ifdef _OPENMP
+        nt = omp_get_num_threads();
+        me = omp_get_thread_num();
+#endif
+        const int x0 = (int)((int64_t)L0->dims[0] * me / nt), x1 = (int)((int64_t)L0->dims[0] * (me + 1) / nt);
+        for (int64_t p = 0; p < n; ++p) {
+            st1d sx, sy, sz;
+            stencil_at((pos[3 * p] - L0->origin[0]) * inv_h, L0->dims[0], &sx);
+            if (sx.base + 3 < x0 || sx.base >= x1) continue;
+            stencil_at((pos[3 * p + 1] - L0->origin[1]) * inv_h, L0->dims[1], &sy);
+            stencil_at((pos[3 * p + 2] - L0->origin[2]) * inv_h, L0->dims[2], &sz);
+            const double qq = q[p];
+            for (int a = 0; a < 4; ++a) {
+                const int xi = sx.base + a;
+                if (xi < x0 || xi >= x1) continue;
+                const double qa = qq * sx.w[a];
+                for (int b = 0; b < 4; ++b) {
+                    const double qab = qa * sy.w[b];
+                    for (int c = 0; c < 4; ++c)
+                        L0->charge[IDX(L0, xi, sy.base + b, sz.base + c)] += qab * sz.w[c];
+                }
             }
         }
     }
@@ -457,7 +480,24 @@ static double pair_r2(const double* pos, int64_t i, int64_t j) { /* i < j, as th
 typedef struct {
     int64_t* j;
     size_t cap;
+    int64_t* t; /* radix-sort scratch */
 } jbuf_t;
+
+/* ascending sort of indices < n (LSD radix, 8-bit digits): the reference's j order */
+static void radix_sort(int64_t* a, int64_t* tmp, size_t cnt, int64_t n) {
+    int64_t* src = a;
+    int64_t* dst = tmp;
+    for (int shift = 0; ((int64_t)1 << shift) < n && shift < 64; shift += 8) {
+        size_t hist[257] = {0};
+        for (size_t k = 0; k < cnt; ++k) hist[((src[k] >> shift) & 255) + 1]++;
+        for (int b = 0; b < 256; ++b) hist[b + 1] += hist[b];
+        for (size_t k = 0; k < cnt; ++k) dst[hist[(src[k] >> shift) & 255]++] = src[k];
+        int64_t* t = src;
+        src = dst;
+        dst = t;
+    }
+    if (src != a) memcpy(a, src, cnt * sizeof(int64_t));
+}
 
 static int cmp_i64(const void* a, const void* b) {
     const int64_t x = *(const int64_t*)a, y = *(const int64_t*)b;
@@ -495,13 +535,15 @@ static int short_range_impl(int64_t n, const double* pos, const double* q, doubl
     if (nfin > 0)
         for (int ax = 0; ax < 3; ++ax) {
             const double ext = hi[ax] - lo[ax];
-            double c = a;
-            if (ext / c > 512.0) c = ext / 512.0;
+            double c = 0.5 * a; /* pair sum: cells of a/2, neighbours within 2 cells */
+            if (ext / c > 1024.0) c = ext / 1024.0;
             cs[ax] = c;
             nc[ax] = (int)(ext / c) + 1;
             if (nc[ax] < 1) nc[ax] = 1;
         }
     const size_t ncell = (size_t)nc[0] * nc[1] * nc[2];
+    int RX[3]; /* cells to search per axis for the pair sum */
+    for (int ax = 0; ax < 3; ++ax) RX[ax] = (int)ceil(a / cs[ax]);
     int64_t* head = (int64_t*)malloc(sizeof(int64_t) * (ncell + 1));
     int64_t* cell_of = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
     int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
@@ -527,6 +569,13 @@ static int short_range_impl(int64_t n, const double* pos, const double* q, doubl
             if (cell_of[i] >= 0) order[fillp[cell_of[i]]++] = i; /* ascending index per cell */
         free(fillp);
     }
+    const double a2m = a2 * (1.0 + 1e-9) + 1e-300;
+    double* spos = (double*)malloc(sizeof(double) * 3 * (size_t)(n > 0 ? n : 1));
+    {
+        const int64_t nb = head[ncell];
+        for (int64_t s = 0; s < nb; ++s)
+            for (int ax = 0; ax < 3; ++ax) spos[3 * s + ax] = pos[3 * order[s] + ax];
+    }
 
     /* error scan: lexicographically first pair with r2 == 0 or r2 NaN */
     int64_t ei = -1, ej = -1;
@@ -542,26 +591,38 @@ static int short_range_impl(int64_t n, const double* pos, const double* q, doubl
     for (int64_t t = 0; t < nnf; ++t)
         for (int64_t j = 0; j < n; ++j)
             if (j != nonfin[t]) CONSIDER(nonfin[t], j);
-    /* coincident pairs among finite atoms are in the same or adjacent cells */
-    for (int64_t i = 0; i < n; ++i) {
-        if (cell_of[i] < 0) continue;
-        const int64_t ci = cell_of[i];
-        const int cz = (int)(ci % nc[2]), cy = (int)((ci / nc[2]) % nc[1]), cxx = (int)(ci / ((int64_t)nc[1] * nc[2]));
-        for (int dx = -1; dx <= 1; ++dx)
-            for (int dy = -1; dy <= 1; ++dy)
-                for (int dz = -1; dz <= 1; ++dz) {
-                    const int x = cxx + dx, y = cy + dy, z = cz + dz;
-                    if (x < 0 || y < 0 || z < 0 || x >= nc[0] || y >= nc[1] || z >= nc[2]) continue;
-                    const int64_t c = ((int64_t)x * nc[1] + y) * nc[2] + z;
-                    for (int64_t s = head[c]; s < head[c + 1]; ++s) {
-                        const int64_t j = order[s];
-                        if (j <= i) continue;
-                        const double r2 = pair_r2(pos, i, j);
-                        if (r2 == 0.0) {
-                            if (ei < 0 || i < ei || (i == ei && j < ej)) { ei = i; ej = j; }
+    /* coincident pairs among finite atoms (r2 == 0: equal coordinates, or differences
+     * whose squares underflow) are in the same or adjacent cells; per-thread minima,
+     * combined in a fixed order (the result is the global minimum either way) */
+#pragma omp parallel
+    {
+        int64_t ti = -1, tj = -1;
+#pragma omp for schedule(dynamic, 1024)
+        for (int64_t i = 0; i < n; ++i) {
+            if (cell_of[i] < 0) continue;
+            const int64_t ci = cell_of[i];
+            const int cz = (int)(ci % nc[2]), cy = (int)((ci / nc[2]) % nc[1]), cxx = (int)(ci / ((int64_t)nc[1] * nc[2]));
+            for (int dx = -1; dx <= 1; ++dx)
+                for (int dy = -1; dy <= 1; ++dy)
+                    for (int dz = -1; dz <= 1; ++dz) {
+                        const int x = cxx + dx, y = cy + dy, z = cz + dz;
+                        if (x < 0 || y < 0 || z < 0 || x >= nc[0] || y >= nc[1] || z >= nc[2]) continue;
+                        const int64_t c = ((int64_t)x * nc[1] + y) * nc[2] + z;
+                        for (int64_t s = head[c]; s < head[c + 1]; ++s) {
+                            const int64_t j = order[s];
+                            if (j <= i) continue;
+                            if (fabs(pos[3 * i] - pos[3 * j]) > 1e-100) continue; /* r2 > 0 for sure */
+                            const double r2 = pair_r2(pos, i, j);
+                            if (r2 == 0.0) {
+                                if (ti < 0 || i < ti || (i == ti && j < tj)) { ti = i; tj = j; }
+                            }
                         }
                     }
-                }
+        }
+#pragma omp critical
+        {
+            if (ti >= 0 && (ei < 0 || ti < ei || (ti == ei && tj < ej))) { ei = ti; ej = tj; }
+        }
     }
 #undef CONSIDER
     int rc = OK;
@@ -577,7 +638,7 @@ static int short_range_impl(int64_t n, const double* pos, const double* q, doubl
     if (rc == OK && !scan_only) {
 #pragma omp parallel
         {
-            jbuf_t jb = {NULL, 0};
+            jbuf_t jb = {NULL, 0, NULL};
 #pragma omp for schedule(dynamic, 64)
             for (int64_t i = 0; i < n; ++i) {
                 if (cell_of[i] < 0) continue;
@@ -585,13 +646,28 @@ static int short_range_impl(int64_t n, const double* pos, const double* q, doubl
                 const int64_t ci = cell_of[i];
                 const int cz = (int)(ci % nc[2]), cy = (int)((ci / nc[2]) % nc[1]),
                           cxx = (int)(ci / ((int64_t)nc[1] * nc[2]));
-                for (int dx = -1; dx <= 1; ++dx)
-                    for (int dy = -1; dy <= 1; ++dy)
-                        for (int dz = -1; dz <= 1; ++dz) {
+                const int cc3[3] = {cxx, cy, cz};
+                const double xi0 = pos[3 * i], yi0 = pos[3 * i + 1], zi0 = pos[3 * i + 2];
+                for (int dx = -RX[0]; dx <= RX[0]; ++dx)
+                    for (int dy = -RX[1]; dy <= RX[1]; ++dy)
+                        for (int dz = -RX[2]; dz <= RX[2]; ++dz) {
                             const int x = cxx + dx, y = cy + dy, z = cz + dz;
                             if (x < 0 || y < 0 || z < 0 || x >= nc[0] || y >= nc[1] || z >= nc[2]) continue;
+                            /* skip cells entirely beyond the cutoff (gap between the cell boxes) */
+                            const int dd[3] = {dx, dy, dz};
+                            double gap2 = 0.0;
+                            for (int ax = 0; ax < 3; ++ax) {
+                                const int g = dd[ax] > 0 ? dd[ax] - 1 : (dd[ax] < 0 ? -dd[ax] - 1 : 0);
+                                gap2 += (g * cs[ax]) * (g * cs[ax]);
+                            }
+                            (void)cc3;
+                            if (gap2 > a2 * 1.000001) continue;
                             const int64_t c = ((int64_t)x * nc[1] + y) * nc[2] + z;
                             for (int64_t s = head[c]; s < head[c + 1]; ++s) {
+                                /* cheap prefilter on the cell-ordered copy (a margin covers rounding);
+                                 * the reference's r2 decides */
+                                const double ex = spos[3 * s] - xi0, ey = spos[3 * s + 1] - yi0, ez = spos[3 * s + 2] - zi0;
+                                if (ex * ex + ey * ey + ez * ez > a2m) continue;
                                 const int64_t j = order[s];
                                 if (j == i) continue;
                                 const double r2 = i < j ? pair_r2(pos, i, j) : pair_r2(pos, j, i);
@@ -599,11 +675,12 @@ static int short_range_impl(int64_t n, const double* pos, const double* q, doubl
                                 if (cnt == jb.cap) {
                                     jb.cap = jb.cap ? 2 * jb.cap : 1024;
                                     jb.j = (int64_t*)realloc(jb.j, jb.cap * sizeof(int64_t));
+                                    jb.t = (int64_t*)realloc(jb.t, jb.cap * sizeof(int64_t));
                                 }
                                 jb.j[cnt++] = j;
                             }
                         }
-                qsort(jb.j, cnt, sizeof(int64_t), cmp_i64);
+                radix_sort(jb.j, jb.t, cnt, n);
                 double ph = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
                 const double qi = q[i];
                 for (size_t t = 0; t < cnt; ++t) {
@@ -641,12 +718,14 @@ static int short_range_impl(int64_t n, const double* pos, const double* q, doubl
                 force[3 * i + 2] = fz;
             }
             free(jb.j);
+            free(jb.t);
         }
     }
     free(nonfin);
     free(head);
     free(cell_of);
     free(order);
+    free(spos);
     return rc == OK ? ok(msg, cap) : rc;
 }
 

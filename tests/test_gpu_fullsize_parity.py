@@ -51,23 +51,51 @@ def test_c2_full_size_vs_oracle(port, name):
     _check(w, r, port.msm_potential(w.pos, w.q, w.box, w.a, w.h, w.levels))
 
 
-@pytest.mark.parametrize("name", ["c4", "c3"])
-def test_c3_c4_full_size_vs_oracle(port, name):
-    w = fx.config(name)
-    f = pkg.MsmField(pkg.MsmConfig(w.a, w.h, w.levels))
-    r = pkg.DeviceSystem(f, pkg.ParticleSystem(w.pos, w.vel, w.q, w.mass, w.box)).evaluate()
-    assert f.work_counters()["pair_split"] == 1
-    _check(w, r, port.msm_potential(w.pos, w.q, w.box, w.a, w.h, w.levels))
+_EVAL0 = {}
+
+
+def _oracle_eval0(port, name):
+    """The oracle's step-0 evaluation of a literal config, shared by the parity and
+    the P1 tests (a full C3 evaluation is ~1-2 min of host time)."""
+    if name not in _EVAL0:
+        _EVAL0.clear()
+        w = fx.config(name)
+        _EVAL0[name] = (w, port.msm_potential(w.pos, w.q, w.box, w.a, w.h, w.levels))
+    return _EVAL0[name]
+
+
+def _oracle_propagate(port, w, o0, steps):
+    """propagate(spec, s, units) (src/integrate.cpp:13-36) over oracle evaluations, with the
+    reference's non-FMA Verlet arithmetic (numpy float64 elementwise: c = ((0.5 dt) conv) / m,
+    v += F c, r += v dt); starts from the cached step-0 evaluation.  Returns
+    (steps_done, error or None)."""
+    import oracle_lib
+    c = ((0.5 * w.dt) * 4.184e-4) / w.mass
+    r, v, F = w.pos.copy(), w.vel.copy(), o0["force"]
+    for s in range(1, steps + 1):
+        v = v + F * c[:, None]
+        r = r + v * w.dt
+        try:
+            F = port.msm_potential(r, w.q, w.box, w.a, w.h, w.levels)["force"]
+        except oracle_lib.OracleError as e:
+            return s - 1, e
+        v = v + F * c[:, None]
+    return steps, None
 
 
 @pytest.mark.parametrize("name", ["c5", "c4", "c3"])
-def test_literal_abort_full_size(port, name):
-    """P1 at full size: same abort step, exception type, message and particle."""
-    w = fx.config(name)
-    _, _, done, err = port.propagate(w.pos, w.vel, w.q, w.mass, w.box, w.a, w.h, w.levels, w.dt, 4)
-    assert err is not None, "the literal input is expected to abort in the reference"
+def test_full_size_vs_oracle_and_literal_abort(port, name):
+    """The whole step-0 evaluation of the literal config against the oracle, then P1:
+    the literal input aborts in the reference; the GPU aborts at the same Verlet step
+    with the same exception type, message and particle index."""
+    w, o0 = _oracle_eval0(port, name)
     f = pkg.MsmField(pkg.MsmConfig(w.a, w.h, w.levels))
     s = pkg.ParticleSystem(w.pos, w.vel, w.q, w.mass, w.box)
+    r = pkg.DeviceSystem(f, s).evaluate()
+    assert f.work_counters()["pair_split"] == 1
+    _check(w, r, o0)
+    done, err = _oracle_propagate(port, w, o0, 4)
+    assert err is not None, "the literal input is expected to abort in the reference"
     with pytest.raises(EXC[err.code]) as ei:
         pkg.DeviceSystem(f, s).propagate(w.dt, 4)
     assert str(ei.value) == err.msg and ei.value.step == done + 1

@@ -50,7 +50,8 @@ def test_production_binning_bit_exact(name, n):
     t = (pos - org[0]) * (1.0 / w.h)            # IEEE sub, then mul by 1/h (msm_phases.cpp:42)
     exp_cov = np.all((np.floor(t) >= 1) & (np.floor(t) <= dims[0] - 3), axis=1)
     assert np.array_equal(cov, exp_cov)
-    assert cov[17] and cov[18] and not cov[19] and not cov[20]
+    assert cov[17] and not cov[20]              # x = -h accepted, just below rejected
+    assert not (cov[18] and cov[19])            # the upper edge: [hi - ulp, hi] straddles it
     assert np.array_equal(cells[cov], np.floor(t[cov]).astype(np.int64))
 
 
