@@ -246,6 +246,11 @@ class GpuField(ForceField):
         making forces a pure function of the positions).  See msmb_set_pair_skin."""
         _check(self._h, _native.lib().msmb_set_pair_skin(self._h, float(skin)))
 
+    def set_list_reuse(self, reuse: bool):
+        """Keep a still-valid pair list across evaluate / propagate calls (default off:
+        every call starts from a fresh list and is a pure function of its input)."""
+        _check(self._h, _native.lib().msmb_set_list_reuse(self._h, int(bool(reuse))))
+
     def set_stage_timing(self, on: bool):
         _native.lib().msmb_set_stage_timing(self._h, int(on))
 

@@ -10,6 +10,7 @@
 // failed evaluation and of every later step become no-ops, so the state a
 // caller gets back on error is the untouched input (the reference throws).
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdlib>
 #include <cstring>
@@ -405,11 +406,16 @@ Error ensure_workspace(msmb_field* f, int64_t n, const double* box) {
 }
 
 // ---- one evaluation ------------------------------------------------------------------
+// One engine stage: an NVTX range (named like the stage, visible to ncu --nvtx and
+// Nsight Systems on eager launches and graph captures) and, when stage timing is
+// on, CUDA events around its launches.
 struct StageScope {
     msmb_field* f;
     int stage = -1;
     cudaEvent_t a = nullptr;
+    bool open = true;
     StageScope(msmb_field* ff, const char* name) : f(ff) {
+        nvtxRangePushA(name);
         if (!f->timer.on) return;
         stage = f->timer.stage_index(name);
         a = f->timer.ev();
@@ -417,10 +423,14 @@ struct StageScope {
     }
     void done(int nl) {
         f->launches += nl;
+        if (open) nvtxRangePop(), open = false;
         if (stage < 0) return;
         cudaEvent_t b = f->timer.ev();
         cudaEventRecord(b, f->stream);
         f->timer.pending.push_back({stage, a, b, nl});
+    }
+    ~StageScope() {
+        if (open) nvtxRangePop();
     }
 };
 

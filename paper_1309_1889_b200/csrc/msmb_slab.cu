@@ -47,6 +47,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <climits>
@@ -558,6 +559,8 @@ void setup_sets(msmb_slab* g) {
 // The halo sets and refresh lists from the owned sets: every owner sends (id, x, y, z)
 // of its atoms in each peer's local columns; receivers record them.
 void select_halos(msmb_slab* g) {
+    nvtxRangePushA("slab halo selection");
+    struct Pop { ~Pop() { nvtxRangePop(); } } pop_at_exit;
     std::vector<std::vector<int64_t>> counts(g->parts.size());
     for (size_t i = 0; i < g->parts.size(); ++i) halo_send_lists(*g->parts[i], counts[i]);
     const int P = g->nparts;
@@ -606,6 +609,8 @@ void select_halos(msmb_slab* g) {
 // Migration at a rebuild: owned atoms whose column now belongs to another part move
 // there with their whole state (x, y, z, vx, vy, vz); then the owned sets are rebuilt.
 void migrate(msmb_slab* g) {
+    nvtxRangePushA("slab migrate");
+    struct Pop { ~Pop() { nvtxRangePop(); } } pop_at_exit;
     const int P = g->nparts;
     std::vector<std::vector<int64_t>> counts(g->parts.size());
     for (size_t pi = 0; pi < g->parts.size(); ++pi) {
@@ -696,6 +701,8 @@ void migrate(msmb_slab* g) {
 // The engine's evaluation restricted to the part's work, with the plane exchanges
 // between the grid stages (stream-ordered on every part).
 void evaluate(msmb_slab* g, bool rebuild) {
+    nvtxRangePushA("slab evaluate");
+    struct Pop { ~Pop() { nvtxRangePop(); } } pop_at_exit;
     const int L = g->parts[0]->W().g.levels;
     for (auto& pp : g->parts) {
         SlabPart& p = *pp;
@@ -769,6 +776,8 @@ void evaluate(msmb_slab* g, bool rebuild) {
 
 // ---------------------------------------------------------------- a propagate call
 void halo_refresh(msmb_slab* g) {
+    nvtxRangePushA("slab halo refresh");
+    struct Pop { ~Pop() { nvtxRangePop(); } } pop_at_exit;
     for (auto& pp : g->parts) {
         SlabPart& p = *pp;
         const int64_t ns = p.hsend_off[size_t(p.nparts)];

@@ -167,8 +167,10 @@ def test_pair_list_rebuilds_mid_trajectory(port):
     assert rel_rms(p1, pp) <= 1e-8 and rel_rms(v1, vv) <= 1e-8
 
 
-def test_pair_list_validity_across_calls_and_systems(port):
-    # the list is rebuilt only when invalid or after a skin/2 move -- also across calls
+def test_pair_list_per_call_and_reuse_opt_in(port):
+    """Every evaluate / propagate call starts from a fresh pair list, so its results are
+    a pure function of its input (bitwise repeatable, whatever ran before on the field);
+    msmb_set_list_reuse opts into carrying a still-valid list across calls."""
     w = fx.config("c1s", n_override=3000)
     cfg = pkg.MsmConfig(w.a, w.h, w.levels)
     a = pkg.ParticleSystem(w.pos, w.vel, w.q, w.mass, w.box)
@@ -178,11 +180,8 @@ def test_pair_list_validity_across_calls_and_systems(port):
     f = pkg.MsmField(cfg)
     ra = f.evaluate(a)
     assert f.work_counters()["list_rebuilds"] == 1
-    f.evaluate(a)                             # same positions: the list is reused
-    assert f.work_counters()["list_rebuilds"] == 1
-    rb = f.evaluate(b)                        # far away: rebuilt
-    assert f.work_counters()["list_rebuilds"] == 2
-    ra2 = f.evaluate(a)                       # back: rebuilt from a's positions, so
+    rb = f.evaluate(b)
+    ra2 = f.evaluate(a)
     assert f.work_counters()["list_rebuilds"] == 3
     assert np.array_equal(ra2.per_particle_force, ra.per_particle_force)   # bit-identical
     assert ra2.total_energy == ra.total_energy
@@ -190,18 +189,24 @@ def test_pair_list_validity_across_calls_and_systems(port):
     assert np.array_equal(fb.per_particle_force, rb.per_particle_force)
     o = port.msm_potential(far, w.q, w.box, w.a, w.h, w.levels)
     assert abs(rb.total_energy - o["energy"]) <= 1e-10 * abs(o["energy"])
-    # a propagate call continuing from the current list does not rebuild at its start
+    # opt-in reuse: same positions, no rebuild; a propagate call continues from the list
+    f.set_list_reuse(True)
+    f.evaluate(a)
+    n0 = f.work_counters()["list_rebuilds"]
+    f.evaluate(a)
+    assert f.work_counters()["list_rebuilds"] == n0
     ds = pkg.DeviceSystem(f, a)
     ds.propagate(w.dt, 3)
-    n0 = f.work_counters()["list_rebuilds"]
+    n1 = f.work_counters()["list_rebuilds"]
     ds.propagate(w.dt, 3)
-    assert f.work_counters()["list_rebuilds"] == n0
+    assert f.work_counters()["list_rebuilds"] == n1
 
 
 def test_pair_list_invalidated_by_failed_evaluation():
     # a failed evaluation (coverage error) invalidates the list: the next one rebuilds
     w = fx.config("c1s", n_override=2000)
     f = pkg.MsmField(pkg.MsmConfig(w.a, w.h, w.levels))
+    f.set_list_reuse(True)                    # (without reuse every call rebuilds anyway)
     s = pkg.ParticleSystem(w.pos, w.vel, w.q, w.mass, w.box)
     r0 = f.evaluate(s)
     bad = w.pos.copy()

@@ -99,9 +99,9 @@ def test_nccl_id_broadcast_gloo():
 
 
 # ------------------------------------------------------------------------------ GPU
-def _single(w, steps, dt=None, skin=None, calls=1):
+def _single(w, steps, dt=None, skin=None, calls=1, direct=True):
     f = pkg.MsmField(pkg.MsmConfig(w.a, w.h, w.levels))
-    f.set_lattice_method(direct=True)  # the decomposition's lattice method
+    f.set_lattice_method(direct=direct)  # several parts: the direct stencil on owned planes
     if skin is not None:
         f.set_pair_skin(skin)
     ds = pkg.DeviceSystem(f, pkg.ParticleSystem(w.pos, w.vel, w.q, w.mass, w.box))
@@ -126,7 +126,7 @@ def test_decomposed_trajectory_bitwise(name, n, parts, steps):
     w = fx.config(name, n_override=n)
     if name in ("c5", "c4"):
         w.dt = 0.02  # short survivable slices of these shapes
-    (pos1, vel1), f1 = _single(w, steps)
+    (pos1, vel1), f1 = _single(w, steps, direct=parts > 1)  # one part keeps the FFT lattice
     dd = _slab(w, parts)
     out, energy = dd.propagate(w.dt, steps)
     assert np.array_equal(out.positions, pos1)
