@@ -2,7 +2,7 @@
 # A/B step times of bench.py under environment variants: tools/ab_bench.sh "VAR=a VAR2=b" "VAR=c" ...
 cd "$(dirname "$0")/.."
 for cfg in "$@"; do
-  env $cfg python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > /tmp/ab.json 2>/tmp/ab.err || { echo "$cfg FAILED"; tail -3 /tmp/ab.err; continue; }
+  env $cfg python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e --no-scaling-base > /tmp/ab.json 2>/tmp/ab.err || { echo "$cfg FAILED"; tail -3 /tmp/ab.err; continue; }
   python - "$cfg" <<'PY'
 import json, sys
 d = json.loads(open("/tmp/ab.json").read().strip().splitlines()[-1])
