@@ -719,9 +719,6 @@ static_assert((kRing & (kRing - 1)) == 0, "ring size must be a power of two");
 #ifndef MSMB_PAIR_UNROLL
 #define MSMB_PAIR_UNROLL 4
 #endif
-#ifndef MSMB_PAIR_SKIP
-#define MSMB_PAIR_SKIP 1 // lanes skip the staged clusters without atoms for them
-#endif
 
 // Pair masks, built once per pair-list rebuild (flag[0]): for every list entry of
 // an i-cluster, each lane's 32-bit mask of the j-cluster atoms within the list cut
@@ -934,42 +931,17 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         zj_n = zs[sj];
         qj_n = qs[sj];
     };
-    unsigned nz = 0;     // MSMB_PAIR_SKIP: staged slots ahead with atoms for this lane
     auto stage = [&](int jj) {
         const int slot = jj & (kRing - 1);
         const int pos = slot * kSlots + 32 - lane;
         s_v[w][0][pos] = make_double2(xj_n, yj_n);
         s_v[w][1][pos] = make_double2(zj_n, qj_n);
         s_mask[w][slot][lane] = mk_n;
-#if MSMB_PAIR_SKIP
-        nz |= (mk_n != 0u ? 1u : 0u) << slot;
-#endif
         ncand += __popc(mk_n);
         if (jj + 1 < nj) fetch(jj + 1);
     };
     const double2* rows = &s_v[w][0][0];
     int hi = 0;          // clusters staged so far (warp-uniform)
-#if MSMB_PAIR_SKIP
-    // nz: ring slots holding a staged cluster ahead of `cur` in which this lane has
-    // atoms; a lane whose mask runs out jumps straight to the next such cluster (an
-    // empty cluster costs no step), or parks on the last staged one until more arrive.
-    // The pairs and their order are unchanged (only idle steps disappear).
-    int cur = -1;        // this lane's list position
-    unsigned m = 0;      // this lane's remaining mask of cluster `cur`
-    const double2* row = rows;
-    auto advance = [&]() {
-        const bool need = m == 0;
-        const unsigned rot = unsigned(cur + 1) & (kRing - 1);
-        const unsigned r = ((nz >> rot) | (nz << (kRing - rot))) & ((1u << kRing) - 1u);
-        const int cand = r ? cur + __ffs(int(r)) : hi - 1;
-        const int ncur = need ? max(cand, cur) : cur;
-        const unsigned mload = s_mask[w][ncur & (kRing - 1)][lane];
-        m = need ? (r ? mload : 0u) : m;
-        nz = (need && r) ? nz & ~(1u << (ncur & (kRing - 1))) : nz;
-        cur = ncur;
-        row = rows + (cur & (kRing - 1)) * kSlots;
-    };
-#else
     int cur = 0;         // this lane's list position
     unsigned m = 0;      // this lane's remaining mask of cluster `cur`
     unsigned mnext = 0;  // mask of cluster cur + 1 (valid while cur + 1 < hi)
@@ -981,7 +953,6 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         row = rows + (cur & (kRing - 1)) * kSlots;
         mnext = s_mask[w][(cur + 1) & (kRing - 1)][lane];
     };
-#endif
     auto step = [&]() {
         int pos;
         asm("bfind.u32 %0, %1;" : "=r"(pos) : "r"(m));
@@ -1029,12 +1000,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         __syncwarp();
         while (hi < nj && hi < kRing) stage(hi++);
         __syncwarp();
-#if MSMB_PAIR_SKIP
-        advance(); // to the first cluster with atoms for this lane
-#else
         m = s_mask[w][0][lane];
         mnext = s_mask[w][1][lane];
-#endif
         for (;;) {
 #pragma unroll
             for (int u = 0; u < MSMB_PAIR_UNROLL; ++u) step();
@@ -1044,9 +1011,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
                 do stage(hi++);
                 while (hi < nj && hi - lo < kRing);
                 __syncwarp();
-#if !MSMB_PAIR_SKIP
                 mnext = s_mask[w][(cur + 1) & (kRing - 1)][lane];
-#endif
                 advance();
             }
             if (hi >= nj && __all_sync(FULLMASK, m == 0 && cur + 1 >= hi)) break;
