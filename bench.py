@@ -315,12 +315,14 @@ def parareal_run_line(D, K=1):
     cfg = pkg.PararealConfig(8, K, 1e300, pkg.PropagatorSpec(F, fdt, fs), pkg.PropagatorSpec(G, gdt, gs),
                              short_circuit=False)
     s = pkg.ParticleSystem(w.pos, w.vel, w.q, w.mass, w.box)
-    pkg.propagate(pkg.PropagatorSpec(F, fdt, 2), s)  # warm-up: graphs, plans
-    pkg.propagate(pkg.PropagatorSpec(G, gdt, 2), s)
+    be = parallel.DeviceBackend(cfg, s)
+    st0 = be.from_system(s)
+    be.propagate("fine", st0)  # warm-up: workspaces, plans, captured step graphs
+    be.propagate("coarse", st0)
     torch.cuda.synchronize(D.local)
     D.barrier()
     t0 = time.perf_counter()
-    res = parallel.parareal_run(s, 8, cfg)
+    res = parallel.parareal_run(s, 8, cfg, backend=be)
     torch.cuda.synchronize(D.local)
     D.barrier()
     wall = D.max(time.perf_counter() - t0)

@@ -315,7 +315,8 @@ int msmb_dd_plan(const msmb_msm_config* cfg, const msmb_units* units, const doub
  * Two transports:
  *  - one process per GPU: nfields = 1, nparts = world size, rank = this process's
  *    rank, and either nccl_id (128 bytes from msmb_nccl_unique_id on rank 0,
- *    distributed by the caller) or nccl_comm (an existing ncclComm_t);
+ *    distributed by the caller) or nccl_comm (an existing ncclComm_t); also valid
+ *    with nparts = 1 (a one-rank communicator);
  *  - local: nfields = nparts fields (distinct handles; typically one per device,
  *    several on one device for tests), all parts driven by this process, the
  *    exchanges as stream-ordered copies; nccl_id / nccl_comm unused.

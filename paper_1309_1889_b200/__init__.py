@@ -42,7 +42,7 @@ __all__ = [
     "GpuField", "CutoffParams", "SimpleCutoffField", "WolfField", "simple_cutoff", "wolf_summation",
     "DirectCoulombField", "PairRepulsionOverlay", "direct_coulomb",
     "msm_potential", "PropagatorSpec", "propagate", "verlet_step", "energy_report", "EnergyReport",
-    "PararealConfig", "PararealResult", "parareal_window", "parareal_run", "SequentialExecutor",
+    "PararealConfig", "PararealResult", "parareal_window", "parareal_run", "SequentialExecutor", "GpuExecutor",
     "AsyncExecutor", "DeviceSystem", "Error", "ConfigError", "DomainError", "CoverageError",
     "CoincidentParticlesError", "HierarchyError", "RuntimeFault", "NonConvergenceError",
     "CudaUnavailableError", "device_count", "grid_geometry",
@@ -277,7 +277,7 @@ class GpuField(ForceField):
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if sys.is_finalizing():  # process teardown releases the device anyway
+        if sys is None or sys.is_finalizing():  # process teardown releases the device anyway
             return
         if h is not None and h.value:
             try:
@@ -524,7 +524,7 @@ class DeviceSystem:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if sys.is_finalizing():
+        if sys is None or sys.is_finalizing():
             return
         if h is not None and h.value:
             try:

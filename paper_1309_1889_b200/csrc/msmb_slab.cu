@@ -875,7 +875,9 @@ int msmb_slab_create(msmb_field* const* fields, int nfields, int nparts, int ran
         for (int j = 0; j < i; ++j)
             if (fields[j] == fields[i]) return MSMB_ERR_CONFIG; // one field (workspace) per part
     }
-    const bool dist = nfields == 1 && nparts > 1;
+    // one field: the NCCL transport (also with a single part when an id or communicator is
+    // given -- a one-rank communicator exercises the same code path)
+    const bool dist = nfields == 1 && (nparts > 1 || nccl_id || nccl_comm);
     if (!dist && nfields != nparts) return MSMB_ERR_CONFIG;
     if (dist && (rank < 0 || rank >= nparts || (!nccl_id && !nccl_comm))) return MSMB_ERR_CONFIG;
     auto g = std::make_unique<msmb_slab>();

@@ -19,7 +19,11 @@ between B200s, gloo in the CPU tests.  This is the reference's parareal_run
 Results do not depend on the number of ranks: a 1-rank run equals the
 single-GPU C++ driver (msmb_parareal_run) bit for bit, and an N-rank run equals
 the 1-rank run bit for bit (deltas are broadcast exactly; coarse rows are
-recomputed identically).
+recomputed identically).  This rests on every propagate call being a pure
+function of its input state: each call builds its pair list afresh
+(include/msmb.h, msmb_set_list_reuse), so a rank's coarse rows do not depend on
+which fine slices it ran before -- every rank reaches the same skip and
+convergence decisions and the same collectives.
 
 The device work goes through a backend.  `DeviceBackend` is the product: msmb
 fields, device-resident propagation (msmb_system_propagate_ex) and the raw
@@ -354,7 +358,7 @@ class SpatialDecomposition:
     """
 
     def __init__(self, config, system: ParticleSystem, units=None, group=None, local_parts: int = 0,
-                 device: Optional[int] = None, devices=None):
+                 device: Optional[int] = None, devices=None, transport: str = "auto"):
         from . import UnitsConfig
         self.units = units or UnitsConfig.physical()
         self.system = system
@@ -377,14 +381,16 @@ class SpatialDecomposition:
             self.fields = [MsmField(config, self.units, device=dev)]
             arr = (C.c_void_p * 1)(self.fields[0].handle)
             idbuf = (C.c_ubyte * 128)()
-            if self.world > 1:
+            # transport "nccl" forces the NCCL path even for one rank (a one-rank communicator)
+            use_nccl = self.world > 1 or transport == "nccl"
+            if use_nccl:
                 if self.rank == 0:
                     _check(self.fields[0].handle, lib.msmb_nccl_unique_id(idbuf))
-                obj = [bytes(idbuf)]
-                comm.dist.broadcast_object_list(obj, src=0, group=group)
-                C.memmove(idbuf, obj[0], 128)
-            # world == 1: one part, the local transport
-            rc = lib.msmb_slab_create(arr, 1, self.world, self.rank, idbuf if self.world > 1 else None, None,
+                if self.world > 1:
+                    obj = [bytes(idbuf)]
+                    comm.dist.broadcast_object_list(obj, src=0, group=group)
+                    C.memmove(idbuf, obj[0], 128)
+            rc = lib.msmb_slab_create(arr, 1, self.world, self.rank, idbuf if use_nccl else None, None,
                                       C.byref(self._h))
         _check(self.fields[0].handle, rc)
         self.last_energy = 0.0

@@ -34,3 +34,7 @@ def test_reference_drives_gpu_field():
     assert 0 <= r["pf_dx_parareal_device"] <= 1e-8
     # all-pairs fields (F3 direct Coulomb, F2 repulsion overlay)
     assert r["ap_de"] <= 1e-10 and r["ap_df"] <= 1e-8
+    # paramd_b200::GpuExecutor (fine replicas) == one fine field, bit for bit, with the
+    # reference's ConvergenceReport rows / point_iterations; a host field on the device
+    # path raises ConfigError instead of running on the CPU
+    assert r["dx_executor"] == 0.0 and r["rows_ok"] == 1 and r["fallback_rejected"] == 1

@@ -5,8 +5,12 @@ oracle-backed host backend (tests/parallel_host.py). Its trajectory must equal
 the oracle's own parareal_run bit for bit, whatever the rank count. This
 covers the skip heuristic, multiple windows and error agreement across ranks.
 
-GPU test: the device backend with one rank reproduces the single-GPU C++
-driver (msmb_parareal_run) bit for bit.
+GPU tests: the device backend with one rank reproduces the single-GPU C++
+driver (msmb_parareal_run) bit for bit; two processes sharing the one B200,
+talking over gloo (CUDA tensors staged through the host: no kernel waits on
+another process), reproduce it bit for bit as well; and the C++ driver's own
+executor over fine-field replicas (GpuExecutor -> msmb_parareal_run_ex) equals
+the single-field run, with the reference's report rows.
 """
 import os
 import socket
@@ -158,3 +162,70 @@ def test_device_backend_equals_cpp_driver_bitwise(port):
     assert a.counts == b.counts and a.windows == b.windows
     tp, _, cnt, err = _oracle(port)
     assert err is None and rel_rms(pa, tp) <= 1e-8
+
+
+def _gpu_worker(rank, world, port, out_dir):
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    sys.path[:0] = [str(root), str(root / "tests")]
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        v = _system()
+        F = pkg.MsmField(pkg.MsmConfig(*FINE[:3]))
+        G = pkg.MsmField(pkg.MsmConfig(*COARSE[:3]))
+        cfg = pkg.PararealConfig(3, 4, 1e-7, pkg.PropagatorSpec(F, FINE[3], FINE[4]),
+                                 pkg.PropagatorSpec(G, COARSE[3], COARSE[4]), skip_threshold=1e-9)
+        res = parallel.parareal_run(v, 7, cfg)
+        np.savez(os.path.join(out_dir, f"g{rank}.npz"), pos=np.stack([t.positions for t in res.trajectory]),
+                 vel=np.stack([t.velocities for t in res.trajectory]), fine_run=res.shard.fine_slices_run,
+                 counts=np.array([res.counts["g_evals"], res.counts["f_evals"], res.counts["f_skipped"]]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_processes_device_backend_gloo_bitwise():
+    v = _system()
+    F = pkg.MsmField(pkg.MsmConfig(*FINE[:3]))
+    G = pkg.MsmField(pkg.MsmConfig(*COARSE[:3]))
+    cfg = pkg.PararealConfig(3, 4, 1e-7, pkg.PropagatorSpec(F, FINE[3], FINE[4]),
+                             pkg.PropagatorSpec(G, COARSE[3], COARSE[4]), skip_threshold=1e-9)
+    a = pkg.parareal_run(v, 7, cfg)
+    with tempfile.TemporaryDirectory() as d:
+        mp.start_processes(_gpu_worker, args=(2, _free_port(), d), nprocs=2, join=True, start_method="spawn")
+        out = [dict(np.load(os.path.join(d, f"g{r}.npz"))) for r in range(2)]
+    pa = np.stack([t.positions for t in a.trajectory])
+    va = np.stack([t.velocities for t in a.trajectory])
+    for r in out:
+        assert np.array_equal(r["pos"], pa) and np.array_equal(r["vel"], va)
+        assert list(r["counts"]) == [a.counts["g_evals"], a.counts["f_evals"], a.counts["f_skipped"]]
+    runs = [int(r["fine_run"]) for r in out]
+    assert sum(runs) == a.counts["f_evals"] and min(runs) >= 1
+
+
+@pytest.mark.gpu
+def test_gpu_executor_replicas_bitwise(port):
+    v = _system()
+    F = pkg.MsmField(pkg.MsmConfig(*FINE[:3]))
+    G = pkg.MsmField(pkg.MsmConfig(*COARSE[:3]))
+    cfg = pkg.PararealConfig(3, 4, 1e-7, pkg.PropagatorSpec(F, FINE[3], FINE[4]),
+                             pkg.PropagatorSpec(G, COARSE[3], COARSE[4]), skip_threshold=1e-9)
+    a = pkg.parareal_run(v, 7, cfg)
+    reps = [pkg.MsmField(pkg.MsmConfig(*FINE[:3])) for _ in range(2)]  # one per GPU; here all on cuda:0
+    b = pkg.parareal_run(v, 7, cfg, exec=pkg.GpuExecutor(reps))
+    assert np.array_equal(np.stack([t.positions for t in a.trajectory]), np.stack([t.positions for t in b.trajectory]))
+    assert a.counts == b.counts and a.report_rows == b.report_rows and a.point_iterations == b.point_iterations
+    assert len(b.report_rows) > 0 and len(b.point_iterations) == 7
+    # against the reference's report (the driver over the oracle, bitwise the reference's
+    # parareal_run on this fixture): same rows, converged flags and point iterations
+    from parallel_host import HostBackend
+    hcfg = _host_cfg()
+    h = parallel.parareal_run(v, 7, hcfg, backend=HostBackend(hcfg, v))
+    assert [r[:3] for r in b.report_rows] == [r[:3] for r in h.report_rows]
+    assert [r[4] for r in b.report_rows] == [r[4] for r in h.report_rows]
+    assert b.point_iterations == list(h.point_iterations)

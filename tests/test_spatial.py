@@ -138,6 +138,26 @@ def test_decomposed_trajectory_bitwise(name, n, parts, steps):
 
 
 @pytest.mark.gpu
+def test_nccl_transport_one_rank():
+    """The NCCL transport (runtime-loaded libnccl, communicator init, all-reduce of the
+    rebuild decision, all-gathers of counts, errors, energies and the final state) on a
+    one-rank communicator: bitwise the local transport's result."""
+    w = fx.config("c1s", n_override=4096)
+    s = pkg.ParticleSystem(w.pos, w.vel, w.q, w.mass, w.box)
+    cfg = pkg.MsmConfig(w.a, w.h, w.levels)
+    a, ea = parallel.SpatialDecomposition(cfg, s, local_parts=1).propagate(w.dt, 3)
+    dn = parallel.SpatialDecomposition(cfg, s, transport="nccl")
+    b, eb = dn.propagate(w.dt, 3)
+    assert np.array_equal(a.positions, b.positions) and np.array_equal(a.velocities, b.velocities)
+    assert ea == eb
+    with pytest.raises(pkg.CoverageError):  # errors through the NCCL all-gather of records
+        bad = w.pos.copy()
+        bad[11] = [1e3, 0.0, 0.0]
+        parallel.SpatialDecomposition(cfg, pkg.ParticleSystem(bad, w.vel, w.q, w.mass, w.box),
+                                      transport="nccl").propagate(w.dt, 2)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("parts", [2, 3, 5])
 def test_decomposed_migration_bitwise(parts):
     """Fast atoms and a tiny skin: the list is rebuilt every step and atoms migrate
