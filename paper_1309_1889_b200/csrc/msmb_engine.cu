@@ -92,7 +92,10 @@ StageTimer::~StageTimer() {
 int engine_set_error(msmb_field* f, const Error& e) {
     f->last = e;
     // a failed evaluation may have left a partial pair list: rebuild at the next one
-    if (f->ws && f->ws->c.flag) cudaMemsetAsync(f->ws->c.flag + 3, 0, sizeof(int), f->stream);
+    if (f->ws && f->ws->c.flag) { // the list and the cell sort must be rebuilt (kernels skipped work)
+        cudaMemsetAsync(f->ws->c.flag + 3, 0, sizeof(int), f->stream);
+        cudaMemsetAsync(f->ws->c.flag + 6, 0, sizeof(int), f->stream);
+    }
     return e.kind;
 }
 
@@ -271,9 +274,9 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
     c.pcnt = walloc<int>(*W, size_t(W->maxclu));
     c.scan_tmp = walloc<int>(*W, size_t((std::max(g.ncells, g.ncols) + 1 + 4095) / 4096 + 8));
     c.colstart = walloc<int>(*W, size_t(g.ncols + 1));
-    c.flag = walloc<int>(*W, 5);
+    c.flag = walloc<int>(*W, 8);
     ck(cudaMemset(c.nclu, 0, sizeof(int)), "memset");
-    ck(cudaMemset(c.flag, 0, 5 * sizeof(int)), "memset");
+    ck(cudaMemset(c.flag, 0, 8 * sizeof(int)), "memset");
     ck(cudaMemset(c.colstart, 0, sizeof(int) * size_t(g.ncols + 1)), "memset");
     alloc_plist(*W, g.pair_cap);
     alloc_outputs(*W, n);

@@ -128,7 +128,7 @@ __device__ __forceinline__ int scell_of(const BinP& p, int cx, int cy, int cz) {
 // owned + halo atoms, msmb_slab.cu); the others keep no key
 __global__ void k_bin(int n, const double* __restrict__ x, const double* __restrict__ y,
                       const double* __restrict__ z, BinP p, int* key, int* rank, int* count,
-                      int* outlist, ErrRec* err, const int* __restrict__ list) {
+                      int* outlist, ErrRec* err, const int* __restrict__ list, int* moved) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n || failed(err)) return;
     const int i = list ? list[t] : t;
@@ -145,6 +145,7 @@ __global__ void k_bin(int n, const double* __restrict__ x, const double* __restr
             c[ax] = int(f);
         }
         if (inf && !nan) { // rejected (msmb.h): excluded from the cells, reported as DomainError
+            if (key[i] != -1) *moved = 1;
             key[i] = -1;
             atomicMin(&err->cov_min, (long long)i);
             const int slot = atomicAdd(&err->cov_count, 1);
@@ -154,6 +155,7 @@ __global__ void k_bin(int n, const double* __restrict__ x, const double* __restr
         if (nan) atomicAdd(&err->nan_count, 1);
         if (nan) c[0] = c[1] = c[2] = 1;
         const int sc = scell_of(p, c[0], c[1], c[2]);
+        if (key[i] != sc) *moved = 1;
         key[i] = sc;
         rank[i] = atomicAdd(&count[sc], 1);
         return;
@@ -167,6 +169,7 @@ __global__ void k_bin(int n, const double* __restrict__ x, const double* __restr
         c[ax] = ok ? int(f) : 0;
     }
     if (!ok) {
+        if (key[i] != -1) *moved = 1;
         key[i] = -1;
         atomicMin(&err->cov_min, (long long)i);
         const int slot = atomicAdd(&err->cov_count, 1);
@@ -174,14 +177,17 @@ __global__ void k_bin(int n, const double* __restrict__ x, const double* __restr
         return;
     }
     const int sc = scell_of(p, c[0], c[1], c[2]);
+    if (key[i] != sc) *moved = 1;
     key[i] = sc;
     rank[i] = atomicAdd(&count[sc], 1);
 }
 
 // exclusive scan of int[m] (m = cells + 1), 4096 elements per block
+// gate (optional): skip when gate[0] == 0 (the cell sort of k_bin_decide is reused)
 __global__ void __launch_bounds__(1024) k_scan_block(const int* __restrict__ in, int* out,
-                                                     int* bsum, int64_t m) {
+                                                     int* bsum, int64_t m, const int* __restrict__ gate) {
     __shared__ int wsum[32];
+    if (gate && !*gate) return;
     const int64_t base = int64_t(blockIdx.x) * 4096 + threadIdx.x * 4;
     int v[4];
     int s = 0;
@@ -215,9 +221,10 @@ __global__ void __launch_bounds__(1024) k_scan_block(const int* __restrict__ in,
     }
 }
 
-__global__ void __launch_bounds__(1024) k_scan_sums(int* bsum, int nb) {
+__global__ void __launch_bounds__(1024) k_scan_sums(int* bsum, int nb, const int* __restrict__ gate) {
     __shared__ int wsum[32];
     __shared__ int carry;
+    if (gate && !*gate) return;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -249,17 +256,30 @@ __global__ void __launch_bounds__(1024) k_scan_sums(int* bsum, int nb) {
     }
 }
 
-__global__ void k_scan_add(int* out, const int* __restrict__ bsum, int64_t m) {
+__global__ void k_scan_add(int* out, const int* __restrict__ bsum, int64_t m, const int* __restrict__ gate) {
+    if (gate && !*gate) return;
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < m) out[i] += bsum[i / 4096];
 }
 
-static int scan_exclusive(cudaStream_t st, const int* in, int* out, int* tmp, int64_t m) {
+static int scan_exclusive(cudaStream_t st, const int* in, int* out, int* tmp, int64_t m,
+                          const int* gate = nullptr) {
     const int nb = int((m + 4095) / 4096);
-    k_scan_block<<<nb, 1024, 0, st>>>(in, out, tmp, m);
-    k_scan_sums<<<1, 1024, 0, st>>>(tmp, nb);
-    k_scan_add<<<int((m + 255) / 256), 256, 0, st>>>(out, tmp, m);
+    k_scan_block<<<nb, 1024, 0, st>>>(in, out, tmp, m, gate);
+    k_scan_sums<<<1, 1024, 0, st>>>(tmp, nb, gate);
+    k_scan_add<<<int((m + 255) / 256), 256, 0, st>>>(out, tmp, m, gate);
     return 3;
+}
+
+// Cell-sort reuse: k_bin sets flag[5] when some atom's cell key differs from its key
+// of the previous evaluation; flag[6] says the sorted structures (start, perm, nat)
+// are those of the current keys' cells.  The sort runs only when needed (flag[7]);
+// between list rebuilds atoms rarely change cells, and the sorted order of the same
+// keys is the same order (within a cell: ascending index), so results are unchanged.
+__global__ void k_sort_decide(int* flag) {
+    const int need = flag[5] || !flag[6];
+    flag[7] = need;
+    flag[6] = 1;
 }
 
 int launch_scan_exclusive(cudaStream_t st, const int* in, int* out, int* tmp, int64_t m) {
@@ -268,9 +288,9 @@ int launch_scan_exclusive(cudaStream_t st, const int* in, int* out, int* tmp, in
 
 __global__ void k_scatter(int n, const int* __restrict__ key, const int* __restrict__ rank,
                           const int* __restrict__ start, int* perm, const ErrRec* err,
-                          const int* __restrict__ list) {
+                          const int* __restrict__ list, const int* __restrict__ gate) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n || failed(err)) return;
+    if (t >= n || failed(err) || !*gate) return;
     const int i = list ? list[t] : t;
     const int k = key[i];
     if (k >= 0) perm[start[k] + rank[i]] = i;
@@ -280,9 +300,9 @@ __global__ void k_scatter(int n, const int* __restrict__ key, const int* __restr
 // also publishes each level-0 cell's range in natural (x, y, z) row-major order
 __global__ void k_cellsort(int64_t ncells, BinP p, const int* __restrict__ start, int* perm,
                            int2* nat, const double* __restrict__ x, const double* __restrict__ y,
-                           const double* __restrict__ z, ErrRec* err) {
+                           const double* __restrict__ z, ErrRec* err, const int* __restrict__ gate) {
     const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (c >= ncells || failed(err)) return;
+    if (c >= ncells || failed(err) || !*gate) return;
     const int s0 = start[c], s1 = start[c + 1];
     {
         int64_t t = c;
@@ -304,15 +324,32 @@ __global__ void k_cellsort(int64_t ncells, BinP p, const int* __restrict__ start
         }
         perm[b + 1] = v;
     }
-    // exactly coincident particles (r2 == 0, src/msm_phases.cpp:237-239) share a cell
-    for (int a = s0; a < s1; ++a)
-        for (int b = a + 1; b < s1; ++b) {
-            const int i = perm[a], j = perm[b];
-            if (x[i] == x[j] && y[i] == y[j] && z[i] == z[j]) {
-                const unsigned long long key = ((unsigned long long)min(i, j) << 32) | (unsigned long long)max(i, j);
-                atomicMin(&err->pair_key, key);
-            }
+}
+
+// exactly coincident particles (r2 == 0, src/msm_phases.cpp:237-239) share a cell: every
+// evaluation compares each sorted atom with the later atoms of its cell (cells hold
+// ~1-2 atoms); runs whether or not the cell sort was reused
+__device__ __forceinline__ void coincide_check(int s, int i, const int* __restrict__ key,
+                                               const int* __restrict__ start, const int* __restrict__ perm,
+                                               const double* __restrict__ x, const double* __restrict__ y,
+                                               const double* __restrict__ z, ErrRec* err) {
+    const int s1 = start[key[i] + 1];
+    const double px = x[i], py = y[i], pz = z[i];
+    for (int b = s + 1; b < s1; ++b) {
+        const int j = perm[b];
+        if (x[j] == px && y[j] == py && z[j] == pz) {
+            const unsigned long long k = ((unsigned long long)min(i, j) << 32) | (unsigned long long)max(i, j);
+            atomicMin(&err->pair_key, k);
         }
+    }
+}
+
+__global__ void k_coincide(const int* __restrict__ start_total, const int* __restrict__ perm,
+                           const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ z,
+                           ErrRec* err, const int* __restrict__ key, const int* __restrict__ start) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= *start_total || failed(err)) return;
+    coincide_check(s, perm[s], key, start, perm, x, y, z, err);
 }
 
 // sorted copies + the anterpolation weights of every particle:
@@ -320,10 +357,11 @@ __global__ void k_cellsort(int64_t ncells, BinP p, const int* __restrict__ start
 __global__ void k_gather(int n, const int* __restrict__ start_total, const int* __restrict__ perm,
                          const double* __restrict__ x, const double* __restrict__ y,
                          const double* __restrict__ z, const double* __restrict__ q, BinP p,
-                         double* aw, const ErrRec* err) {
+                         double* aw, ErrRec* err, const int* __restrict__ key, const int* __restrict__ start) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= *start_total || failed(err)) return;
     const int i = perm[s];
+    coincide_check(s, i, key, start, perm, x, y, z, err);
     const double px = x[i], py = y[i], pz = z[i], qq = q[i];
     const double pp[3] = {px, py, pz};
     double w[3][4];
@@ -344,25 +382,33 @@ int launch_bin(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& 
                ErrRec* err, const int* list, int64_t nlist) {
     const int n = list ? int(nlist) : int(s.n);
     cudaMemsetAsync(c.count, 0, sizeof(int) * size_t(g.ncells + 1), st);
+    cudaMemsetAsync(c.flag + 5, 0, sizeof(int), st);
     if (n > 0)
         k_bin<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, s.x, s.y, s.z, make_binp(g), a.key, a.rank,
-                                               c.count, a.outlist, err, list);
+                                               c.count, a.outlist, err, list, c.flag + 5);
     return n > 0 ? 1 : 0;
 }
 
 int launch_sort(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& a, DevCells& c,
                 ErrRec* err, const int* list, int64_t nlist) {
     const int n = list ? int(nlist) : int(s.n);
-    int l = scan_exclusive(st, c.count, c.start, c.scan_tmp, g.ncells + 1);
+    k_sort_decide<<<1, 1, 0, st>>>(c.flag);
+    const int* gate = c.flag + 7;
+    int l = 1 + scan_exclusive(st, c.count, c.start, c.scan_tmp, g.ncells + 1, gate);
     if (n > 0)
-        k_scatter<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, a.key, a.rank, c.start, a.perm, err, list);
-    // always: also publishes the (possibly empty) natural-order cell ranges read by k_anterp
+        k_scatter<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, a.key, a.rank, c.start, a.perm, err, list,
+                                                                       gate);
+    // also publishes the (possibly empty) natural-order cell ranges read by k_anterp
     k_cellsort<<<int((g.ncells + 255) / 256), 256, 0, st>>>(g.ncells, make_binp(g), c.start, a.perm,
-                                                            c.nat, s.x, s.y, s.z, err);
-    if (n == 0 || g.kind != MSMB_FIELD_MSM) return l + 1;
+                                                            c.nat, s.x, s.y, s.z, err, gate);
+    if (n == 0) return l + 1;
+    if (g.kind != MSMB_FIELD_MSM) { // pair-only fields: no weights, the coincidence check alone
+        k_coincide<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(c.start + g.ncells, a.perm, s.x, s.y, s.z,
+                                                                       err, a.key, c.start);
+        return l + 2;
+    }
     k_gather<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, s.q,
-                                              make_binp(g), a.aw,
-                                              err);
+                                              make_binp(g), a.aw, err, a.key, c.start);
     return l + 3;
 }
 

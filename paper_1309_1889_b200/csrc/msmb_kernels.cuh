@@ -41,8 +41,9 @@ struct DevCells {
     unsigned* pmask;    // [max_clusters * cap * 32] per-lane j-atom masks (k_pairmask)
     int* scan_tmp;      // scratch for the multi-block scan
     int* colstart;      // [ncols+1] first cluster slot of each pair column (frozen at rebuild)
-    int* flag;          // [3] [0] rebuild the pair list this evaluation, [1] clustered atoms,
-                        //     [2] rebuild count (diagnostics)
+    int* flag;          // [8] [0] rebuild the pair list this evaluation, [1] clustered atoms,
+                        //     [2] rebuild count (diagnostics), [3] list valid, [4] list's part key,
+                        //     [5] some atom changed cell (k_bin), [6] cell sort valid, [7] sort now
 };
 
 struct DevLevels {      // concatenated lattices + tables

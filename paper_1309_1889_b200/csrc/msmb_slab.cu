@@ -711,6 +711,8 @@ void evaluate(msmb_slab* g, bool rebuild) {
         cudaStream_t st = p.stream();
         DevState s = p.st.dev();
         ensure_const_table(p.f, W);
+        // a new local atom set: the cell sort cannot be reused (atoms left cells)
+        if (rebuild) cks(cudaMemsetAsync(W.c.flag + 6, 0, sizeof(int), st), "memset");
         int nl = launch_bin(st, G, s, W.a, W.c, W.err, p.local.as<int>(), p.n_local);
         nl += launch_sort(st, G, s, W.a, W.c, W.err, p.local.as<int>(), p.n_local);
         nl += launch_clusters(st, G, s.n, s, W.a, W.c, W.err, W.cap, W.part, rebuild ? 1 : 0, 0);
@@ -987,6 +989,7 @@ int msmb_slab_propagate(msmb_slab* g, int64_t n, double* pos_xyz, double* vel_xy
                 launch_reset_err(p.stream(), p.W().err, 0);
                 // the list of the first evaluation is built fresh (a pure function of the input)
                 cks(cudaMemsetAsync(p.W().c.flag + 3, 0, sizeof(int), p.stream()), "memset");
+                cks(cudaMemsetAsync(p.W().c.flag + 6, 0, sizeof(int), p.stream()), "memset");
                 cks(cudaStreamSynchronize(p.stream()), "sync");
             }
             setup_sets(g);
