@@ -40,6 +40,7 @@ static void ck(cudaError_t e, const char* where) {
 }
 
 Workspace::~Workspace() {
+    std::lock_guard<std::recursive_mutex> dl(device_mutex());
     if (gx_eval) cudaGraphExecDestroy(gx_eval);
     if (gx_step1) cudaGraphExecDestroy(gx_step1);
     if (gx_step2) cudaGraphExecDestroy(gx_step2);
@@ -399,6 +400,7 @@ static bool make_levels(msmb_field* f, Workspace& Wr, Error& e) {
 }
 
 Error ensure_workspace(msmb_field* f, int64_t n, const double* box) {
+    std::lock_guard<std::recursive_mutex> dl(device_mutex()); // allocations + device syncs
     Error e;
     if (f->ws && f->ws->n == n && f->ws->g.box[0] == box[0] && f->ws->g.box[1] == box[1] &&
         f->ws->g.box[2] == box[2])
@@ -466,6 +468,9 @@ static int stage_id(const char* name) {
 void launch_stamp(cudaStream_t st, int idx);
 void read_stamps(unsigned long long* h);
 static const bool g_exp_stamps = std::getenv("MSMB_TIMELINE") != nullptr;
+// MSMB_EXP_CHAIN (timing experiments only; results are wrong): 0 = no long-range chain,
+// 1 = anterpolation only, 2 = everything but anterpolation
+static const int g_exp_chain = std::getenv("MSMB_EXP_CHAIN") ? std::atoi(std::getenv("MSMB_EXP_CHAIN")) : -1;
 static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, bool rebuild = false) {
     cudaStream_t st = f->stream;
     const bool fork = !f->timer.on;
@@ -525,19 +530,22 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, 
         ck(cudaStreamWaitEvent(lr, f->fork_ev, 0), "fork");
     }
     if (g_exp_stamps) { launch_stamp(st, 1); launch_stamp(lr, 2); }
-    run("anterp", [&] { return launch_anterp(lr, g, W.a, W.c, W.L, W.err, W.whole); });
+    if (g_exp_chain != 0 && g_exp_chain != 2)
+        run("anterp", [&] { return launch_anterp(lr, g, W.a, W.c, W.L, W.err, W.whole); });
     if (g_exp_stamps) launch_stamp(lr, 7);
-    run("restrict", [&] { return launch_restrict_all(lr, g, W.L, W.err); });
-    if (g_exp_stamps) launch_stamp(lr, 8);
-    run("lattice", [&] {
-        return W.lattice_fft ? launch_lattice_fft(lr, W.fft, W.err) : launch_lattice(lr, g, W.L, W.err, W.whole);
-    });
-    if (g_exp_stamps) launch_stamp(lr, 9);
-    run("top", [&] {
-        return W.fft_top.n ? launch_lattice_fft(lr, W.fft_top, W.err) : launch_top(lr, g, W.L, W.err);
-    });
-    if (g_exp_stamps) launch_stamp(lr, 10);
-    run("prolong", [&] { return launch_prolong_all(lr, g, W.L, W.err); });
+    if (g_exp_chain < 0 || g_exp_chain == 2) {
+        run("restrict", [&] { return launch_restrict_all(lr, g, W.L, W.err); });
+        if (g_exp_stamps) launch_stamp(lr, 8);
+        run("lattice", [&] {
+            return W.lattice_fft ? launch_lattice_fft(lr, W.fft, W.err) : launch_lattice(lr, g, W.L, W.err, W.whole);
+        });
+        if (g_exp_stamps) launch_stamp(lr, 9);
+        run("top", [&] {
+            return W.fft_top.n ? launch_lattice_fft(lr, W.fft_top, W.err) : launch_top(lr, g, W.L, W.err);
+        });
+        if (g_exp_stamps) launch_stamp(lr, 10);
+        run("prolong", [&] { return launch_prolong_all(lr, g, W.L, W.err); });
+    }
     if (g_exp_stamps) launch_stamp(lr, 3);
     if (fork) ck(cudaEventRecord(f->join_ev, lr), "join");
     run("clusters", [&] { return launch_clusters(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, rebuild ? 1 : 0); });
@@ -584,6 +592,7 @@ void record_counters(msmb_field* f, const Workspace& W, const ErrRec& r) {
 }
 
 void grow_cap(Workspace& W, const ErrRec& r) {
+    std::lock_guard<std::recursive_mutex> dl(device_mutex());
     const int need = std::max(r.overflow, W.cap);
     const int cap = std::max(need + need / 4 + 32, W.cap * 2);
     alloc_plist(W, cap);
@@ -663,6 +672,7 @@ static void ensure_graphs(msmb_field* f, Workspace& W, DevState& s, double dt, d
 
 template <class Fn>
 static cudaGraphExec_t capture(msmb_field* f, Fn&& fn) {
+    std::lock_guard<std::recursive_mutex> dl(device_mutex()); // no other thread allocates meanwhile
     cudaGraph_t graph = nullptr;
     ck(cudaStreamBeginCapture(f->stream, cudaStreamCaptureModeThreadLocal), "BeginCapture");
     try {

@@ -12,6 +12,16 @@
 
 namespace msmb {
 
+// Several host threads may drive fields of one process (the parareal executor's fine
+// replicas, a caller sharing fields between threads).  A thread that captures a CUDA
+// graph must not see another thread allocate, free or synchronize the device in the
+// middle of its capture (the capture is invalidated), so graph capture and every
+// device allocation / free / device-wide synchronization take this lock.
+inline std::recursive_mutex& device_mutex() {
+    static std::recursive_mutex m;
+    return m;
+}
+
 // RAII device buffer
 struct DBuf {
     void* p = nullptr;
@@ -21,11 +31,15 @@ struct DBuf {
     DBuf& operator=(const DBuf&) = delete;
     ~DBuf() { reset(); }
     void reset() {
-        if (p) cudaFree(p);
+        if (p) {
+            std::lock_guard<std::recursive_mutex> lk(device_mutex());
+            cudaFree(p);
+        }
         p = nullptr;
         bytes = 0;
     }
     cudaError_t alloc(size_t b) {
+        std::lock_guard<std::recursive_mutex> lk(device_mutex());
         reset();
         if (b == 0) b = 8;
         bytes = b;
