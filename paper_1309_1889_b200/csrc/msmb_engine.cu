@@ -295,6 +295,7 @@ static bool make_levels(msmb_field* f, Workspace& Wr, Error& e) {
     DevLevels& L = W->L;
     L.charge = walloc<double>(*W, g.lattice_total);
     L.pot = walloc<double>(*W, g.lattice_total);
+    L.anterp_part = walloc<double>(*W, anterp_tile_part_doubles(g));
     for (int k = 0; k + 1 < g.levels; ++k)
         for (int ax = 0; ax < 3; ++ax) {
             const TransferAxis& T = g.tr[k][ax];

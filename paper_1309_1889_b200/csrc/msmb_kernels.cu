@@ -1491,9 +1491,127 @@ __global__ void __launch_bounds__(kSX * kSY)
     }
 }
 
+// Tiled scatter anterpolation (MSMB_ANTERP_TILE, the default): one warp per block of
+// kTX x kTY x kTZ level-0 cells scatters the atoms of its cells -- cells in
+// (x, y, z) order, atoms in sorted order -- into a private shared-memory tile of the
+// (kTX+3) x (kTY+3) x (kTZ+3) points they reach, lane (dx, dy, cz) adding the
+// products ((q wx[dx]) wy[dy]) wz[cz] and wz[cz + 2] (the reference's qa / qab
+// products, src/msm_phases.cpp:52-57) for one atom at a time (__syncwarp between
+// atoms orders the read-modify-writes of overlapping stencils).  The tiles are then
+// combined per point in block order (k_anterp_combine: at most 2 blocks per axis
+// reach a point).  Fixed orders throughout: deterministic, no atomics.  Each atom is
+// read once, with the next atom's weights prefetched while the current one is added.
+constexpr int kTX = 4, kTY = 4, kTZ = 8;
+constexpr int kTPX = kTX + 3, kTPY = kTY + 3, kTPZ = kTZ + 3, kTPts = kTPX * kTPY * kTPZ;
+
+__global__ void __launch_bounds__(32)
+    k_anterp_tile(BinP p, const int2* __restrict__ nat, const double* __restrict__ aw, double* part, int bx0,
+                  int nbx, const ErrRec* err) {
+    __shared__ double acc[kTPts];
+    if (failed(err)) return;
+    const int d0 = p.d[0], d1 = p.d[1], d2 = p.d[2];
+    const int nby = (d1 + kTY - 1) / kTY, nbz = (d2 + kTZ - 1) / kTZ;
+    const int bz = blockIdx.x % nbz, by = (blockIdx.x / nbz) % nby, bx = bx0 + blockIdx.x / (nbz * nby);
+    const int X0 = bx * kTX, Y0 = by * kTY, Z0 = bz * kTZ;
+    const int lane = threadIdx.x;
+    for (int e = lane; e < kTPts; e += 32) acc[e] = 0.0;
+    const int dx = lane >> 3, dy = (lane >> 1) & 3, cz = lane & 1;
+    __syncwarp();
+    // the block's cells in (x, y, z) order; lane k holds the range of cell k (<= 32 per round)
+    constexpr int kCells = kTX * kTY * kTZ;
+    for (int cb = 0; cb < kCells; cb += 32) {
+        int2 rg = make_int2(0, 0);
+        {
+            const int k = cb + lane;
+            const int cx = X0 + k / (kTY * kTZ), cy = Y0 + (k / kTZ) % kTY, czz = Z0 + k % kTZ;
+            if (k < kCells && cx >= 1 && cx <= d0 - 3 && cy >= 1 && cy <= d1 - 3 && czz >= 1 && czz <= d2 - 3)
+                rg = __ldg(nat + (size_t(cx) * d1 + cy) * d2 + czz);
+        }
+        for (int j = 0; j < 32; ++j) {
+            const int s0 = __shfl_sync(FULLMASK, rg.x, j), s1 = __shfl_sync(FULLMASK, rg.y, j);
+            if (s0 >= s1) continue;
+            const int k = cb + j;
+            const int lx = k / (kTY * kTZ), ly = (k / kTZ) % kTY, lz = k % kTZ;
+            // the cell's stencil base (cell - 1) in tile coordinates: points lx .. lx + 3
+            const int o1 = ((lx + dx) * kTPY + (ly + dy)) * kTPZ + lz + cz;
+            const int o2 = o1 + 2;
+            const double* w = aw + size_t(s0) * 12;
+            double wx = __ldg(w + dx), wy = __ldg(w + 4 + dy), wz1 = __ldg(w + 8 + cz), wz2 = __ldg(w + 10 + cz);
+            for (int sidx = s0; sidx < s1; ++sidx) {
+                const double cxy = __dmul_rn(wx, wy);
+                const double a1 = __dmul_rn(cxy, wz1), a2 = __dmul_rn(cxy, wz2);
+                if (sidx + 1 < s1) { // prefetch the next atom of the cell
+                    const double* wn = aw + size_t(sidx + 1) * 12;
+                    wx = __ldg(wn + dx);
+                    wy = __ldg(wn + 4 + dy);
+                    wz1 = __ldg(wn + 8 + cz);
+                    wz2 = __ldg(wn + 10 + cz);
+                }
+                acc[o1] += a1;
+                acc[o2] += a2;
+                __syncwarp();
+            }
+        }
+    }
+    __syncwarp();
+    double* out = part + size_t(blockIdx.x) * kTPts;
+    for (int e = lane; e < kTPts; e += 32) out[e] = acc[e];
+}
+
+// point (x, y, z) of the owned planes = the sum of the tiles of the <= 2 x 2 x 2 blocks
+// reaching it, in block order
+__global__ void k_anterp_combine(int d0, int d1, int d2, const double* __restrict__ part, int bx0, int nbx,
+                                 double* q0, int x_begin, int x_end, const ErrRec* err) {
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t npl = int64_t(d1) * d2;
+    if (t >= int64_t(x_end - x_begin) * npl || failed(err)) return;
+    const int z = int(t % d2), y = int((t / d2) % d1), x = x_begin + int(t / npl);
+    const int nby = (d1 + kTY - 1) / kTY, nbz = (d2 + kTZ - 1) / kTZ;
+    // block b reaches points [b*T - 1, b*T + T + 2): b in [floor((x-2)/T), floor((x+1)/T)]
+    const int bxb = min(bx0 + nbx - 1, (x + 1) / kTX);
+    double s = 0.0;
+    for (int bx = max(bx0, (x - 2 + kTX) / kTX - 1); bx <= bxb; ++bx) {
+        const int lx = x - (bx * kTX - 1);
+        if (lx < 0 || lx >= kTPX) continue;
+        for (int by = max(0, (y - 2 + kTY) / kTY - 1); by <= min(nby - 1, (y + 1) / kTY); ++by) {
+            const int ly = y - (by * kTY - 1);
+            if (ly < 0 || ly >= kTPY) continue;
+            for (int bz = max(0, (z - 2 + kTZ) / kTZ - 1); bz <= min(nbz - 1, (z + 1) / kTZ); ++bz) {
+                const int lz = z - (bz * kTZ - 1);
+                if (lz < 0 || lz >= kTPZ) continue;
+                const size_t blk = (size_t(bx - bx0) * nby + by) * nbz + bz;
+                s += part[blk * kTPts + (lx * kTPY + ly) * kTPZ + lz];
+            }
+        }
+    }
+    q0[(size_t(x) * d1 + y) * d2 + z] = s;
+}
+
+size_t anterp_tile_part_doubles(const Geometry& g) {
+    const int* d = g.lv[0].dims;
+    return size_t((d[0] + kTX - 1) / kTX) * ((d[1] + kTY - 1) / kTY) * ((d[2] + kTZ - 1) / kTZ) * kTPts;
+}
+
+#ifndef MSMB_ANTERP_TILE
+#define MSMB_ANTERP_TILE 1
+#endif
+
 int launch_anterp(cudaStream_t st, const Geometry& g, DevAtoms& a, DevCells& c, DevLevels& L,
                   ErrRec* err, const Part& P) {
     const BinP p = make_binp(g);
+    if (MSMB_ANTERP_TILE && L.anterp_part) {
+        // the cell blocks whose atoms reach the owned planes [pl0, pl1): cells pl0 - 2 .. pl1
+        const int x0 = P.pl0[0], x1 = P.pl1[0];
+        if (x1 <= x0) return 0;
+        const int bxa = std::max(0, (x0 - 2) / kTX), bxb = std::min((p.d[0] - 1) / kTX, (x1 + 1) / kTX);
+        const int nbx = bxb - bxa + 1;
+        const int nby = (p.d[1] + kTY - 1) / kTY, nbz = (p.d[2] + kTZ - 1) / kTZ;
+        k_anterp_tile<<<nbx * nby * nbz, 32, 0, st>>>(p, c.nat, a.aw, L.anterp_part, bxa, nbx, err);
+        const int64_t m = int64_t(x1 - x0) * p.d[1] * p.d[2];
+        k_anterp_combine<<<int((m + 255) / 256), 256, 0, st>>>(p.d[0], p.d[1], p.d[2], L.anterp_part, bxa, nbx,
+                                                               L.charge + g.lv[0].offset, x0, x1, err);
+        return 2;
+    }
     // large lattices (C3, C4): the layer-streaming kernel (measured 3.2 vs 5.0 ms at C3);
     // small ones (C2): the 16-lane gather has more parallelism (0.099 vs 0.206 ms)
     if (int64_t(g.lv[0].size) > kAnterpStreamMin) {

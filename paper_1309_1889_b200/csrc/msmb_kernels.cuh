@@ -60,6 +60,7 @@ struct DevLevels {      // concatenated lattices + tables
     int2* lat_rowchunks;
     double* lat_taps;
     double* lat_partial;
+    double* anterp_part; // tiled anterpolation: one (kTX+3)(kTY+3)(kTZ+3) tile per cell block
     int lat_S;
     int lat_const;      // stencil lives in constant memory (k_lattice<true>)
     // stencil tables: lattice levels then top (index levels-1)
@@ -140,6 +141,7 @@ int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& 
 int launch_err_brute(cudaStream_t st, int64_t n, const DevState& s, DevAtoms& a, ErrRec* err);
 int launch_anterp(cudaStream_t st, const Geometry& g, DevAtoms& a, DevCells& c, DevLevels& L,
                   ErrRec* err, const Part& P);
+size_t anterp_tile_part_doubles(const Geometry& g);
 int launch_restrict(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err);
 int launch_restrict_all(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
 int launch_restrict_planes(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err, int xlo, int xhi);
