@@ -1504,10 +1504,15 @@ __global__ void __launch_bounds__(kSX * kSY)
 constexpr int kTX = 4, kTY = 4, kTZ = 8;
 constexpr int kTPX = kTX + 3, kTPY = kTY + 3, kTPZ = kTZ + 3, kTPts = kTPX * kTPY * kTPZ;
 
+constexpr int kTStage = 64; // atoms staged in shared memory per batch
+
 __global__ void __launch_bounds__(32)
     k_anterp_tile(BinP p, const int2* __restrict__ nat, const double* __restrict__ aw, double* part, int bx0,
                   int nbx, const ErrRec* err) {
     __shared__ double acc[kTPts];
+    __shared__ double sw[kTStage * 12]; // the staged atoms' weights (k_gather layout)
+    __shared__ int sidx[kTStage];       // their sorted slots
+    __shared__ int scl[kTStage];        // their cells (block-local index)
     if (failed(err)) return;
     const int d0 = p.d[0], d1 = p.d[1], d2 = p.d[2];
     const int nby = (d1 + kTY - 1) / kTY, nbz = (d2 + kTZ - 1) / kTZ;
@@ -1516,39 +1521,44 @@ __global__ void __launch_bounds__(32)
     const int lane = threadIdx.x;
     for (int e = lane; e < kTPts; e += 32) acc[e] = 0.0;
     const int dx = lane >> 3, dy = (lane >> 1) & 3, cz = lane & 1;
-    __syncwarp();
-    // the block's cells in (x, y, z) order; lane k holds the range of cell k (<= 32 per round)
     constexpr int kCells = kTX * kTY * kTZ;
     for (int cb = 0; cb < kCells; cb += 32) {
+        // lane j: cell cb + j of the block, in (x, y, z) order
         int2 rg = make_int2(0, 0);
         {
             const int k = cb + lane;
             const int cx = X0 + k / (kTY * kTZ), cy = Y0 + (k / kTZ) % kTY, czz = Z0 + k % kTZ;
-            if (k < kCells && cx >= 1 && cx <= d0 - 3 && cy >= 1 && cy <= d1 - 3 && czz >= 1 && czz <= d2 - 3)
+            if (cx >= 1 && cx <= d0 - 3 && cy >= 1 && cy <= d1 - 3 && czz >= 1 && czz <= d2 - 3)
                 rg = __ldg(nat + (size_t(cx) * d1 + cy) * d2 + czz);
         }
-        for (int j = 0; j < 32; ++j) {
-            const int s0 = __shfl_sync(FULLMASK, rg.x, j), s1 = __shfl_sync(FULLMASK, rg.y, j);
-            if (s0 >= s1) continue;
-            const int k = cb + j;
-            const int lx = k / (kTY * kTZ), ly = (k / kTZ) % kTY, lz = k % kTZ;
-            // the cell's stencil base (cell - 1) in tile coordinates: points lx .. lx + 3
-            const int o1 = ((lx + dx) * kTPY + (ly + dy)) * kTPZ + lz + cz;
-            const int o2 = o1 + 2;
-            const double* w = aw + size_t(s0) * 12;
-            double wx = __ldg(w + dx), wy = __ldg(w + 4 + dy), wz1 = __ldg(w + 8 + cz), wz2 = __ldg(w + 10 + cz);
-            for (int sidx = s0; sidx < s1; ++sidx) {
-                const double cxy = __dmul_rn(wx, wy);
-                const double a1 = __dmul_rn(cxy, wz1), a2 = __dmul_rn(cxy, wz2);
-                if (sidx + 1 < s1) { // prefetch the next atom of the cell
-                    const double* wn = aw + size_t(sidx + 1) * 12;
-                    wx = __ldg(wn + dx);
-                    wy = __ldg(wn + 4 + dy);
-                    wz1 = __ldg(wn + 8 + cz);
-                    wz2 = __ldg(wn + 10 + cz);
-                }
+        const int cnt = max(0, rg.y - rg.x);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(FULLMASK, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int excl = incl - cnt, total = __shfl_sync(FULLMASK, incl, 31);
+        for (int base = 0; base < total; base += kTStage) {
+            const int nst = min(kTStage, total - base);
+            __syncwarp();
+            for (int k = max(0, base - excl); k < cnt && excl + k < base + kTStage; ++k) {
+                sidx[excl + k - base] = rg.x + k;
+                scl[excl + k - base] = cb + lane;
+            }
+            __syncwarp();
+            for (int e = lane; e < nst * 12; e += 32) sw[e] = __ldg(aw + size_t(sidx[e / 12]) * 12 + e % 12);
+            __syncwarp();
+            for (int t = 0; t < nst; ++t) {
+                const int k = scl[t];
+                const int lx = k / (kTY * kTZ), ly = (k / kTZ) % kTY, lz = k % kTZ;
+                const double* w = sw + t * 12;
+                // the cell's stencil base (cell - 1) in tile coordinates: points lx .. lx + 3
+                const int o1 = ((lx + dx) * kTPY + (ly + dy)) * kTPZ + lz + cz;
+                const double cxy = __dmul_rn(w[dx], w[4 + dy]);
+                const double a1 = __dmul_rn(cxy, w[8 + cz]), a2 = __dmul_rn(cxy, w[10 + cz]);
                 acc[o1] += a1;
-                acc[o2] += a2;
+                acc[o1 + 2] += a2;
                 __syncwarp();
             }
         }

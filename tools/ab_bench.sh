@@ -6,6 +6,6 @@ for cfg in "$@"; do
   python - "$cfg" <<'PY'
 import json, sys
 d = json.loads(open("/tmp/ab.json").read().strip().splitlines()[-1])
-print(sys.argv[1], "ms/step %.4f" % d["ms_per_step"], "pairs %.4f" % d["stage_ms_per_eval"]["pairs"])
+s = d["stage_ms_per_eval"]; print(sys.argv[1], "ms/step %.4f" % d["ms_per_step"], " ".join("%s %.4f" % (k, s[k]) for k in ("pairs", "anterp", "sort", "clusters", "interp")))
 PY
 done
