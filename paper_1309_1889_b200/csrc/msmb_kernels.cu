@@ -1501,10 +1501,10 @@ __global__ void __launch_bounds__(kSX * kSY)
 // combined per point in block order (k_anterp_combine: at most 2 blocks per axis
 // reach a point).  Fixed orders throughout: deterministic, no atomics.  Each atom is
 // read once, with the next atom's weights prefetched while the current one is added.
-constexpr int kTX = 4, kTY = 4, kTZ = 8;
+constexpr int kTX = 4, kTY = 4, kTZ = 4;
 constexpr int kTPX = kTX + 3, kTPY = kTY + 3, kTPZ = kTZ + 3, kTPts = kTPX * kTPY * kTPZ;
 
-constexpr int kTStage = 64; // atoms staged in shared memory per batch
+constexpr int kTStage = 32; // atoms staged in shared memory per batch
 
 __global__ void __launch_bounds__(32)
     k_anterp_tile(BinP p, const int2* __restrict__ nat, const double* __restrict__ aw, double* part, int bx0,
