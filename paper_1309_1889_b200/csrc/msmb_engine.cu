@@ -532,7 +532,7 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, 
     }
     if (g_exp_stamps) { launch_stamp(st, 1); launch_stamp(lr, 2); }
     if (g_exp_chain != 0 && g_exp_chain != 2)
-        run("anterp", [&] { return launch_anterp(lr, g, W.a, W.c, W.L, W.err, W.whole); });
+        run("anterp", [&] { return launch_anterp(lr, g, s, W.a, W.c, W.L, W.err, W.whole); });
     if (g_exp_stamps) launch_stamp(lr, 7);
     if (g_exp_chain < 0 || g_exp_chain == 2) {
         run("restrict", [&] { return launch_restrict_all(lr, g, W.L, W.err); });

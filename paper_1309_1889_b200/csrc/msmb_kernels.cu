@@ -51,6 +51,12 @@ cudaError_t smem_grow(const void* func, size_t bytes) {
 
 #define FULLMASK 0xffffffffu
 
+// anterpolation by per-block shared-memory tiles (k_anterp_tile) computing the weights
+// itself; 0 = the per-point gather kernels over k_gather's precomputed weights
+#ifndef MSMB_ANTERP_TILE
+#define MSMB_ANTERP_TILE 1
+#endif
+
 // threads per block of the per-atom kernels: small systems (C1: 8,192 atoms) get
 // 64-thread blocks so they spread over more SMs (latency-bound, not throughput-bound)
 #ifndef MSMB_ATOM_TPB
@@ -352,6 +358,24 @@ __global__ void k_coincide(const int* __restrict__ start_total, const int* __res
     coincide_check(s, perm[s], key, start, perm, x, y, z, err);
 }
 
+// the anterpolation weights of particle i: o[0..3] = q*wx[d], o[4..7] = wy[d], o[8..11] =
+// wz[d], exactly as anterpolate's qa / w (msm_phases.cpp:42-53)
+__device__ __forceinline__ void anterp_weights(const BinP& p, double px, double py, double pz, double qq,
+                                               double* o) {
+    const double pp[3] = {px, py, pz};
+    double w[3][4];
+    for (int ax = 0; ax < 3; ++ax) {
+        const double t = __dmul_rn(__dsub_rn(pp[ax], p.o[ax]), p.inv_h);
+        const int base = int(floor(t)) - 1;
+        for (int d = 0; d < 4; ++d) w[ax][d] = phi_rn(__dsub_rn(t, double(base + d)));
+    }
+    for (int d = 0; d < 4; ++d) {
+        o[d] = __dmul_rn(qq, w[0][d]);
+        o[4 + d] = w[1][d];
+        o[8 + d] = w[2][d];
+    }
+}
+
 // sorted copies + the anterpolation weights of every particle:
 // aw = {q*wx[0..3], wy[0..3], wz[0..3]} exactly as anterpolate's qa / w (msm_phases.cpp:45-53)
 __global__ void k_gather(int n, const int* __restrict__ start_total, const int* __restrict__ perm,
@@ -362,20 +386,7 @@ __global__ void k_gather(int n, const int* __restrict__ start_total, const int* 
     if (s >= *start_total || failed(err)) return;
     const int i = perm[s];
     coincide_check(s, i, key, start, perm, x, y, z, err);
-    const double px = x[i], py = y[i], pz = z[i], qq = q[i];
-    const double pp[3] = {px, py, pz};
-    double w[3][4];
-    for (int ax = 0; ax < 3; ++ax) {
-        const double t = __dmul_rn(__dsub_rn(pp[ax], p.o[ax]), p.inv_h);
-        const int base = int(floor(t)) - 1;
-        for (int d = 0; d < 4; ++d) w[ax][d] = phi_rn(__dsub_rn(t, double(base + d)));
-    }
-    double* o = aw + size_t(s) * 12;
-    for (int d = 0; d < 4; ++d) {
-        o[d] = __dmul_rn(qq, w[0][d]);
-        o[4 + d] = w[1][d];
-        o[8 + d] = w[2][d];
-    }
+    anterp_weights(p, x[i], y[i], z[i], q[i], aw + size_t(s) * 12);
 }
 
 int launch_bin(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& a, DevCells& c,
@@ -402,7 +413,7 @@ int launch_sort(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms&
     k_cellsort<<<int((g.ncells + 255) / 256), 256, 0, st>>>(g.ncells, make_binp(g), c.start, a.perm,
                                                             c.nat, s.x, s.y, s.z, err, gate);
     if (n == 0) return l + 1;
-    if (g.kind != MSMB_FIELD_MSM) { // pair-only fields: no weights, the coincidence check alone
+    if (g.kind != MSMB_FIELD_MSM || MSMB_ANTERP_TILE) { // no precomputed weights: the coincidence check alone
         k_coincide<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(c.start + g.ncells, a.perm, s.x, s.y, s.z,
                                                                        err, a.key, c.start);
         return l + 2;
@@ -1504,11 +1515,12 @@ __global__ void __launch_bounds__(kSX * kSY)
 constexpr int kTX = 4, kTY = 4, kTZ = 4;
 constexpr int kTPX = kTX + 3, kTPY = kTY + 3, kTPZ = kTZ + 3, kTPts = kTPX * kTPY * kTPZ;
 
-constexpr int kTStage = 32; // atoms staged in shared memory per batch
+constexpr int kTStage = 32; // atoms staged in shared memory per batch (one per lane)
 
 __global__ void __launch_bounds__(32)
-    k_anterp_tile(BinP p, const int2* __restrict__ nat, const double* __restrict__ aw, double* part, int bx0,
-                  int nbx, const ErrRec* err) {
+    k_anterp_tile(BinP p, const int2* __restrict__ nat, const int* __restrict__ perm, const double* __restrict__ xs,
+                  const double* __restrict__ ys, const double* __restrict__ zs, const double* __restrict__ qs,
+                  double* part, int bx0, int nbx, const ErrRec* err) {
     __shared__ double acc[kTPts];
     __shared__ double sw[kTStage * 12]; // the staged atoms' weights (k_gather layout)
     __shared__ int sidx[kTStage];       // their sorted slots
@@ -1547,7 +1559,10 @@ __global__ void __launch_bounds__(32)
                 scl[excl + k - base] = cb + lane;
             }
             __syncwarp();
-            for (int e = lane; e < nst * 12; e += 32) sw[e] = __ldg(aw + size_t(sidx[e / 12]) * 12 + e % 12);
+            if (lane < nst) { // one staged atom per lane: its weights from its position
+                const int i = perm[sidx[lane]];
+                anterp_weights(p, xs[i], ys[i], zs[i], qs[i], sw + lane * 12);
+            }
             __syncwarp();
             for (int t = 0; t < nst; ++t) {
                 const int k = scl[t];
@@ -1602,11 +1617,7 @@ size_t anterp_tile_part_doubles(const Geometry& g) {
     return size_t((d[0] + kTX - 1) / kTX) * ((d[1] + kTY - 1) / kTY) * ((d[2] + kTZ - 1) / kTZ) * kTPts;
 }
 
-#ifndef MSMB_ANTERP_TILE
-#define MSMB_ANTERP_TILE 1
-#endif
-
-int launch_anterp(cudaStream_t st, const Geometry& g, DevAtoms& a, DevCells& c, DevLevels& L,
+int launch_anterp(cudaStream_t st, const Geometry& g, const DevState& sv, DevAtoms& a, DevCells& c, DevLevels& L,
                   ErrRec* err, const Part& P) {
     const BinP p = make_binp(g);
     if (MSMB_ANTERP_TILE && L.anterp_part) {
@@ -1616,7 +1627,8 @@ int launch_anterp(cudaStream_t st, const Geometry& g, DevAtoms& a, DevCells& c, 
         const int bxa = std::max(0, (x0 - 2) / kTX), bxb = std::min((p.d[0] - 1) / kTX, (x1 + 1) / kTX);
         const int nbx = bxb - bxa + 1;
         const int nby = (p.d[1] + kTY - 1) / kTY, nbz = (p.d[2] + kTZ - 1) / kTZ;
-        k_anterp_tile<<<nbx * nby * nbz, 32, 0, st>>>(p, c.nat, a.aw, L.anterp_part, bxa, nbx, err);
+        k_anterp_tile<<<nbx * nby * nbz, 32, 0, st>>>(p, c.nat, a.perm, sv.x, sv.y, sv.z, sv.q, L.anterp_part, bxa,
+                                                      nbx, err);
         const int64_t m = int64_t(x1 - x0) * p.d[1] * p.d[2];
         k_anterp_combine<<<int((m + 255) / 256), 256, 0, st>>>(p.d[0], p.d[1], p.d[2], L.anterp_part, bxa, nbx,
                                                                L.charge + g.lv[0].offset, x0, x1, err);

@@ -139,7 +139,7 @@ int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevStat
 int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
                  DevCells& c, ErrRec* err, int cap, const Part& P);
 int launch_err_brute(cudaStream_t st, int64_t n, const DevState& s, DevAtoms& a, ErrRec* err);
-int launch_anterp(cudaStream_t st, const Geometry& g, DevAtoms& a, DevCells& c, DevLevels& L,
+int launch_anterp(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& a, DevCells& c, DevLevels& L,
                   ErrRec* err, const Part& P);
 size_t anterp_tile_part_doubles(const Geometry& g);
 int launch_restrict(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err);

@@ -717,7 +717,7 @@ void evaluate(msmb_slab* g, bool rebuild) {
         nl += launch_sort(st, G, s, W.a, W.c, W.err, p.local.as<int>(), p.n_local);
         nl += launch_clusters(st, G, s.n, s, W.a, W.c, W.err, W.cap, W.part, rebuild ? 1 : 0, 0);
         nl += launch_pairs(st, G, s.n, s, W.a, W.c, W.err, W.cap, W.part);
-        nl += launch_anterp(st, G, W.a, W.c, W.L, W.err, W.part);
+        nl += launch_anterp(st, G, s, W.a, W.c, W.L, W.err, W.part);
         p.f->launches += nl;
         plane_ops(p, 0, W.L.charge, p.qneed);
     }
