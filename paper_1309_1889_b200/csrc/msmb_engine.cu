@@ -275,9 +275,9 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
     c.pcnt = walloc<int>(*W, size_t(W->maxclu));
     c.scan_tmp = walloc<int>(*W, size_t((std::max(g.ncells, g.ncols) + 1 + 4095) / 4096 + 8));
     c.colstart = walloc<int>(*W, size_t(g.ncols + 1));
-    c.flag = walloc<int>(*W, 8);
+    c.flag = walloc<int>(*W, 10);
     ck(cudaMemset(c.nclu, 0, sizeof(int)), "memset");
-    ck(cudaMemset(c.flag, 0, 8 * sizeof(int)), "memset");
+    ck(cudaMemset(c.flag, 0, 10 * sizeof(int)), "memset");
     ck(cudaMemset(c.colstart, 0, sizeof(int) * size_t(g.ncols + 1)), "memset");
     alloc_plist(*W, g.pair_cap);
     alloc_outputs(*W, n);

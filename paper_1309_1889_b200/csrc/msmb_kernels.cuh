@@ -41,9 +41,10 @@ struct DevCells {
     unsigned* pmask;    // [max_clusters * cap * 32] per-lane j-atom masks (k_pairmask)
     int* scan_tmp;      // scratch for the multi-block scan
     int* colstart;      // [ncols+1] first cluster slot of each pair column (frozen at rebuild)
-    int* flag;          // [8] [0] rebuild the pair list this evaluation, [1] clustered atoms,
+    int* flag;          // [10] [0] rebuild the pair list this evaluation, [1] clustered atoms,
                         //     [2] rebuild count (diagnostics), [3] list valid, [4] list's part key,
-                        //     [5] some atom changed cell (k_bin), [6] cell sort valid, [7] sort now
+                        //     [5] some atom changed cell (k_bin), [6] cell sort valid, [7] sort now,
+                        //     [8] some atom moved more than skin/2 since the list build (k_bin)
 };
 
 struct DevLevels {      // concatenated lattices + tables
