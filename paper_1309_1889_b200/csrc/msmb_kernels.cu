@@ -132,32 +132,20 @@ __device__ __forceinline__ int scell_of(const BinP& p, int cx, int cy, int cz) {
 // ============================================================================
 // list != nullptr: bin only the atoms list[0..n) (a spatial-decomposition part's
 // owned + halo atoms, msmb_slab.cu); the others keep no key
-// Also (folded in to save launches on the list-reusing steps): the skin/2 displacement
-// test against the positions of the last list build (flag[8]: some atom moved more),
-// and, while the pair list is valid (flag[3]), the atom's current position and charge
-// in its cluster-order slot (cl_inv); a rebuild in this evaluation re-gathers them.
+// Also (folded in to save a launch): the skin/2 displacement test against the
+// positions of the last list build (flag[8]: some atom moved more).  (Scattering the
+// positions into their cluster slots here as well, instead of k_gather_cl's gather,
+// measured slower: random 32-byte writes on the critical path, C2-S 0.855 -> 0.884 ms.)
 struct BinAux {
     const double* ref;   // [3N] positions at the last list build
     int64_t N;
     double hs2;          // (skin / 2)^2
-    const int* cl_inv;   // original index -> cluster slot
-    const double* q;
-    double *xc, *yc, *zc, *qc;
     int* flag;
 };
 
 __device__ __forceinline__ void bin_aux(const BinAux& a, int i, double x, double y, double z) {
     const double dx = x - a.ref[i], dy = y - a.ref[a.N + i], dz = z - a.ref[2 * a.N + i];
     if (!(dx * dx + dy * dy + dz * dz <= a.hs2)) a.flag[8] = 1; // same value from every writer
-    if (__ldcg(a.flag + 3)) {
-        const int k = a.cl_inv[i];
-        if (k >= 0 && k < __ldcg(a.flag + 1)) {
-            a.xc[k] = x;
-            a.yc[k] = y;
-            a.zc[k] = z;
-            a.qc[k] = a.q[i];
-        }
-    }
 }
 
 __global__ void k_bin(int n, const double* __restrict__ x, const double* __restrict__ y,
@@ -425,7 +413,7 @@ int launch_bin(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& 
     cudaMemsetAsync(c.flag + 5, 0, sizeof(int), st);
     cudaMemsetAsync(c.flag + 8, 0, sizeof(int), st);
     const double hs = 0.5 * g.skin;
-    const BinAux aux{a.ref, s.n, hs * hs, a.cl_inv, s.q, a.xc, a.yc, a.zc, a.qc, c.flag};
+    const BinAux aux{a.ref, s.n, hs * hs, c.flag};
     if (n > 0)
         k_bin<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, s.x, s.y, s.z, make_binp(g), a.key, a.rank,
                                                c.count, a.outlist, err, list, c.flag + 5, aux);
@@ -500,7 +488,7 @@ __global__ void k_gather_cl(const int* __restrict__ flag, const int* __restrict_
                             const double* __restrict__ z, const double* __restrict__ q, double* xc,
                             double* yc, double* zc, double* qc, const ErrRec* err) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (!flag[0] || k >= flag[1] || failed(err)) return; // between rebuilds k_bin scatters them
+    if (k >= flag[1] || failed(err)) return;
     const int i = cl_perm[k];
     xc[k] = x[i];
     yc[k] = y[i];
