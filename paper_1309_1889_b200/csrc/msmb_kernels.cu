@@ -132,29 +132,12 @@ __device__ __forceinline__ int scell_of(const BinP& p, int cx, int cy, int cz) {
 // ============================================================================
 // list != nullptr: bin only the atoms list[0..n) (a spatial-decomposition part's
 // owned + halo atoms, msmb_slab.cu); the others keep no key
-// Also (folded in to save a launch): the skin/2 displacement test against the
-// positions of the last list build (flag[8]: some atom moved more).  (Scattering the
-// positions into their cluster slots here as well, instead of k_gather_cl's gather,
-// measured slower: random 32-byte writes on the critical path, C2-S 0.855 -> 0.884 ms.)
-struct BinAux {
-    const double* ref;   // [3N] positions at the last list build
-    int64_t N;
-    double hs2;          // (skin / 2)^2
-    int* flag;
-};
-
-__device__ __forceinline__ void bin_aux(const BinAux& a, int i, double x, double y, double z) {
-    const double dx = x - a.ref[i], dy = y - a.ref[a.N + i], dz = z - a.ref[2 * a.N + i];
-    if (!(dx * dx + dy * dy + dz * dz <= a.hs2)) a.flag[8] = 1; // same value from every writer
-}
-
 __global__ void k_bin(int n, const double* __restrict__ x, const double* __restrict__ y,
                       const double* __restrict__ z, BinP p, int* key, int* rank, int* count,
-                      int* outlist, ErrRec* err, const int* __restrict__ list, int* moved, BinAux aux) {
+                      int* outlist, ErrRec* err, const int* __restrict__ list, int* moved) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n || failed(err)) return;
     const int i = list ? list[t] : t;
-    bin_aux(aux, i, x[i], y[i], z[i]);
     const double px[3] = {x[i], y[i], z[i]};
     int c[3];
     bool ok = true;
@@ -411,12 +394,9 @@ int launch_bin(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& 
     const int n = list ? int(nlist) : int(s.n);
     cudaMemsetAsync(c.count, 0, sizeof(int) * size_t(g.ncells + 1), st);
     cudaMemsetAsync(c.flag + 5, 0, sizeof(int), st);
-    cudaMemsetAsync(c.flag + 8, 0, sizeof(int), st);
-    const double hs = 0.5 * g.skin;
-    const BinAux aux{a.ref, s.n, hs * hs, c.flag};
     if (n > 0)
         k_bin<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, s.x, s.y, s.z, make_binp(g), a.key, a.rank,
-                                               c.count, a.outlist, err, list, c.flag + 5, aux);
+                                               c.count, a.outlist, err, list, c.flag + 5);
     return n > 0 ? 1 : 0;
 }
 
@@ -456,10 +436,18 @@ int launch_sort(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms&
 // flag[0] = rebuild the pair list in this evaluation: forced, or no valid list
 // (flag[3] == 0: never built, capacity grown, an evaluation failed), or the list was
 // built for another ownership range (flag[4]: the part's pair-column key)
-__global__ void k_flag_reset(int* flag, int force, int key, int disp) {
-    flag[0] = (force || flag[3] == 0 || flag[4] != key || (disp && flag[8])) ? 1 : 0;
+__global__ void k_flag_reset(int* flag, int force, int key) {
+    flag[0] = (force || flag[3] == 0 || flag[4] != key) ? 1 : 0;
 }
 
+__global__ void k_disp(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
+                       const double* __restrict__ z, const double* __restrict__ ref, double half_skin2,
+                       int* flag) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double dx = x[i] - ref[i], dy = y[i] - ref[n + i], dz = z[i] - ref[2 * n + i];
+    if (!(dx * dx + dy * dy + dz * dz <= half_skin2)) flag[0] = 1; // same value from every writer
+}
 
 __global__ void k_cl_perm(int64_t n, const int* __restrict__ start_total, const int* __restrict__ perm,
                           const double* __restrict__ x, const double* __restrict__ y,
@@ -1140,13 +1128,15 @@ int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevStat
     const int nb = int((n + 255) / 256) > 0 ? int((n + 255) / 256) : 1;
     // rebuild decision, frozen cluster order, current positions in it
     const int key = P.cx0 * 65536 + P.cx1;
-    k_flag_reset<<<1, 1, 0, st>>>(c.flag, force_rebuild || !(g.skin > 0.0) ? 1 : 0, key, disp); // disp: k_bin's flag[8]
+    k_flag_reset<<<1, 1, 0, st>>>(c.flag, force_rebuild || !(g.skin > 0.0) ? 1 : 0, key);
+    const double hs = 0.5 * g.skin;
+    if (disp) k_disp<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, s.x, s.y, s.z, a.ref, hs * hs, c.flag);
     k_cl_perm<<<nb, 256, 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, a.cl_perm, a.cl_inv, a.ref, c.flag, key);
     k_gather_cl<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(c.flag, a.cl_perm, s.x, s.y, s.z, s.q, a.xc, a.yc,
                                                                      a.zc, a.qc, err);
     // cluster pair list (rebuild evaluations only)
     k_columns<<<int((nc + 1 + 255) / 256), 256, 0, st>>>(nc, cells_per_col, c.start, c.col_cnt, c.flag, err);
-    int l = 4 + scan_exclusive(st, c.col_cnt, c.col_off, c.scan_tmp, nc + 1, c.flag); // rebuilds only (flag[0])
+    int l = 5 + scan_exclusive(st, c.col_cnt, c.col_off, c.scan_tmp, nc + 1, c.flag); // rebuilds only (flag[0])
     k_clusters<<<int((nc + 255) / 256), 256, 0, st>>>(nc, cells_per_col, c.start, c.col_off, c.clu,
                                                       c.nclu, c.colstart, c.flag, err);
     const int64_t maxclu = n / 32 + nc + 1;
