@@ -44,7 +44,7 @@ struct DevCells {
     int* flag;          // [10] [0] rebuild the pair list this evaluation, [1] clustered atoms,
                         //     [2] rebuild count (diagnostics), [3] list valid, [4] list's part key,
                         //     [5] some atom changed cell (k_bin), [6] cell sort valid, [7] sort now,
-                        //     [8] some atom moved more than skin/2 since the list build (k_bin)
+                        //     [8], [9] spare
 };
 
 struct DevLevels {      // concatenated lattices + tables
