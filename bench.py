@@ -68,6 +68,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-scaling-base", action="store_true", help="N=1: skip the C3-S / C5-S one-GPU lines")
+    ap.add_argument("--multi-path", action="store_true",
+                    help="run the --gpus N > 1 line's code path even on one rank (one-rank NCCL communicator)")
     ap.add_argument("--no-full-reference", action="store_true",
                     help="--impl reference: skip the one full-size short_range calibration")
     return ap.parse_args()
@@ -262,14 +264,14 @@ PARAREAL_TEXT = ("configs[4] survivable variant c5s: 2^20 charges (RSA 1.5 A), F
                  "x100, G MSM a=8 h=5 l=3 dt 0.02 fs x25, one window of 8 slices, K=1 iteration (no short circuit)")
 
 
-def spatial_run(D, steps, warmup):
+def spatial_run(D, steps, warmup, transport="auto"):
     """C3-S through the slab decomposition over D.world GPUs: device-timed steps
     (events on each part's stream, max over ranks) and the end-to-end call time."""
     import paper_1309_1889_b200 as pkg
     from paper_1309_1889_b200 import fixtures as fx, parallel
     w = fx.config("c3s")
     s = pkg.ParticleSystem(w.pos, w.vel, w.q, w.mass, w.box)
-    dd = parallel.SpatialDecomposition(pkg.MsmConfig(w.a, w.h, w.levels), s, device=D.local)
+    dd = parallel.SpatialDecomposition(pkg.MsmConfig(w.a, w.h, w.levels), s, device=D.local, transport=transport)
     dd.propagate(w.dt, max(1, warmup))  # workspaces, plans
     D.barrier()
     sm = np.zeros(steps + 2)
@@ -358,7 +360,7 @@ def multi_gpu(args, D):
                     "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
             print(json.dumps(line), flush=True)
         return
-    w, sp = spatial_run(D, args.steps, args.warmup)
+    w, sp = spatial_run(D, args.steps, args.warmup, transport="nccl")
     par = parareal_run_line(D, 1)
     if D.rank == 0:
         line = {"metric": METRIC, "value": sp["value"], "unit": UNIT, "n_gpus": D.world, "steps": args.steps,
@@ -375,7 +377,7 @@ def main():
     args = parse()
     D = Dist()
     from paper_1309_1889_b200 import fixtures as fx
-    if D.world > 1:
+    if D.world > 1 or args.multi_path:
         multi_gpu(args, D)
         D.close()
         return
