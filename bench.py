@@ -417,9 +417,8 @@ def main():
                                                  f"full N ({t_grid:.2f} s per step); " if calib else "")
                                                 + f"per-step samples: short_range on a random "
                                                   f"{times[0]['sample_atoms']}-atom subset scaled by N(N-1)/2 pair "
-                                                  f"checks -> {t_sr_ext:.1f} s (the sample is cache-resident, "
-                                                  f"hence faster per pair); single-threaded (msm_potential has no "
-                                                  f"threading)",
+                                                  f"checks -> {t_sr_ext:.1f} s (extrapolation check); "
+                                                  f"single-threaded (msm_potential has no threading)",
                                       "short_range_full_s": calib["t_full_s"] if calib else None,
                                       "short_range_extrapolated_s": t_sr_ext},
                         e2e={"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
