@@ -470,7 +470,8 @@ void launch_stamp(cudaStream_t st, int idx);
 void read_stamps(unsigned long long* h);
 static const bool g_exp_stamps = std::getenv("MSMB_TIMELINE") != nullptr;
 // MSMB_EXP_CHAIN (timing experiments only; results are wrong): 0 = no long-range chain,
-// 1 = anterpolation only, 2 = everything but anterpolation
+// 1 = anterpolation only, 2 = everything but anterpolation, 3 = anterpolation + restriction,
+// 4 = ... + lattice, 5 = ... + top (everything but prolongation)
 static const int g_exp_chain = std::getenv("MSMB_EXP_CHAIN") ? std::atoi(std::getenv("MSMB_EXP_CHAIN")) : -1;
 static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, bool rebuild = false) {
     cudaStream_t st = f->stream;
@@ -534,19 +535,20 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, 
     if (g_exp_chain != 0 && g_exp_chain != 2)
         run("anterp", [&] { return launch_anterp(lr, g, s, W.a, W.c, W.L, W.err, W.whole); });
     if (g_exp_stamps) launch_stamp(lr, 7);
-    if (g_exp_chain < 0 || g_exp_chain == 2) {
-        run("restrict", [&] { return launch_restrict_all(lr, g, W.L, W.err); });
-        if (g_exp_stamps) launch_stamp(lr, 8);
+    const bool full = g_exp_chain < 0 || g_exp_chain == 2;
+    if (full || g_exp_chain >= 3) run("restrict", [&] { return launch_restrict_all(lr, g, W.L, W.err); });
+    if (g_exp_stamps) launch_stamp(lr, 8);
+    if (full || g_exp_chain >= 4)
         run("lattice", [&] {
             return W.lattice_fft ? launch_lattice_fft(lr, W.fft, W.err) : launch_lattice(lr, g, W.L, W.err, W.whole);
         });
-        if (g_exp_stamps) launch_stamp(lr, 9);
+    if (g_exp_stamps) launch_stamp(lr, 9);
+    if (full || g_exp_chain >= 5)
         run("top", [&] {
             return W.fft_top.n ? launch_lattice_fft(lr, W.fft_top, W.err) : launch_top(lr, g, W.L, W.err);
         });
-        if (g_exp_stamps) launch_stamp(lr, 10);
-        run("prolong", [&] { return launch_prolong_all(lr, g, W.L, W.err); });
-    }
+    if (g_exp_stamps) launch_stamp(lr, 10);
+    if (full) run("prolong", [&] { return launch_prolong_all(lr, g, W.L, W.err); });
     if (g_exp_stamps) launch_stamp(lr, 3);
     if (fork) ck(cudaEventRecord(f->join_ev, lr), "join");
     run("clusters", [&] { return launch_clusters(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, rebuild ? 1 : 0); });
