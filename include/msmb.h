@@ -353,7 +353,8 @@ int msmb_set_stage_timing(msmb_field* f, int enable);
 int msmb_stage_times(msmb_field* f, double* ms, int64_t* launches, const char** names, int cap);
 void msmb_reset_stage_times(msmb_field* f);
 /* Work counters of the most recent evaluation: [0] in-cutoff unordered pairs
- * P_u, [1] candidate pair tests, [2] clusters, [3] clipped lattice taps
+ * P_u, [1] candidate pair tests (both counted by evaluations launched eagerly --
+ * evaluate, stage-timing passes; the captured step graphs skip the counting), [2] clusters, [3] clipped lattice taps
  * (all levels except the top), [4] top-level taps, [5] kernel launches per
  * evaluation, [6] pair-list rebuilds since the workspace was created, [7] warps
  * per i-cluster in the pair kernel (1 = the large-system instance). */

@@ -440,6 +440,8 @@ struct StageScope {
     }
 };
 
+static thread_local bool t_capturing = false; // graph captures skip the pair statistics
+
 static const char* kStages[] = {"bin", "sort", "clusters", "pairs", "anterp", "restrict",
                                 "lattice", "top", "prolong", "interp", "finalize", "overlay"};
 constexpr int kNumStages = 12;
@@ -519,7 +521,7 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, 
     run("sort", [&] { return launch_sort(st, g, s, W.a, W.c, W.err); });
     if (g.kind != MSMB_FIELD_MSM) { // pair-only field: no grid hierarchy
         run("clusters", [&] { return launch_clusters(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, rebuild ? 1 : 0); });
-        run("pairs", [&] { return launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole); });
+        run("pairs", [&] { return launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, !t_capturing); });
         DevOut o = W.o;
         if (!outputs) o.phi = o.phis = o.phil = o.e = nullptr;
         run("interp", [&] { return launch_pair_out(st, g, s.n, W.a, W.c, o, W.err, outputs ? 1 : 0, W.whole); });
@@ -554,7 +556,8 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, 
     run("clusters", [&] { return launch_clusters(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, rebuild ? 1 : 0); });
     if (g_exp_stamps) launch_stamp(st, 4);
     run("pairs", [&] {
-        return launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole) + launch_err_brute(st, s.n, s, W.a, W.err);
+        return launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, !t_capturing) +
+               launch_err_brute(st, s.n, s, W.a, W.err);
     });
     if (g_exp_stamps) launch_stamp(st, 5);
     if (fork) ck(cudaStreamWaitEvent(st, f->join_ev, 0), "join");
@@ -676,6 +679,10 @@ static void ensure_graphs(msmb_field* f, Workspace& W, DevState& s, double dt, d
 template <class Fn>
 static cudaGraphExec_t capture(msmb_field* f, Fn&& fn) {
     std::lock_guard<std::recursive_mutex> dl(device_mutex()); // no other thread allocates meanwhile
+    struct Flag {
+        Flag() { t_capturing = true; }
+        ~Flag() { t_capturing = false; }
+    } flag_scope;
     cudaGraph_t graph = nullptr;
     ck(cudaStreamBeginCapture(f->stream, cudaStreamCaptureModeThreadLocal), "BeginCapture");
     try {

@@ -29,6 +29,7 @@
 
 #include <map>
 #include <mutex>
+#include <type_traits>
 #include <utility>
 
 #include "msmb_kernels.cuh"
@@ -947,7 +948,9 @@ __global__ void __launch_bounds__(kMaskWarps * 32)
 // (FP64 pipe 53%, issue 62-67%, stalls spread over wait / math throttle /
 // long scoreboard of the staging loads); two staged clusters in flight (register
 // double buffer) 0.647 vs 0.632.
-template <int K, bool SPLIT>
+// COUNT: accumulate the in-cutoff pair and candidate counters (work statistics); the
+// captured step graphs run the COUNT = false instance (counted on eager evaluations)
+template <int K, bool SPLIT, bool COUNT>
 __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     k_pairs_mw(const int2* __restrict__ clu, const int* __restrict__ plist, const int* __restrict__ pcnt,
                const unsigned* __restrict__ pmask, int cap, const double* __restrict__ xs,
@@ -994,7 +997,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         s_v[w][0][pos] = make_double2(xj_n, yj_n);
         s_v[w][1][pos] = make_double2(zj_n, qj_n);
         s_mask[w][slot][lane] = mk_n;
-        ncand += __popc(mk_n);
+        if (COUNT) ncand += __popc(mk_n);
         if (jj + 1 < nj) fetch(jj + 1);
     };
     const double2* rows = &s_v[w][0][0];
@@ -1025,7 +1028,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         double g, sd;
         pair_fn<K>(p, r2, rinv, g, sd);
         const bool in = r2 < a2;
-        npair += in ? 1u : 0u;
+        if (COUNT) npair += in ? 1u : 0u;
         const double qj = in ? zq.y : 0.0; // two FSELs (a predicated accumulation costs 8)
         ph = fma(qj, g, ph);
         const double wgt = qj * sd;
@@ -1087,11 +1090,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         fsy[si] = fy * kq;
         fsz[si] = fz * kq;
     }
-    ncand = __reduce_add_sync(FULLMASK, ncand);
-    npair = __reduce_add_sync(FULLMASK, npair);
-    if (lane == 0) {
-        atomicAdd(&err->pairs, (unsigned long long)npair);
-        atomicAdd(&err->candidates, (unsigned long long)ncand);
+    if (COUNT) {
+        ncand = __reduce_add_sync(FULLMASK, ncand);
+        npair = __reduce_add_sync(FULLMASK, npair);
+        if (lane == 0) {
+            atomicAdd(&err->pairs, (unsigned long long)npair);
+            atomicAdd(&err->candidates, (unsigned long long)ncand);
+        }
     }
 }
 
@@ -1200,7 +1205,7 @@ int pair_split(int64_t maxclu) {
 }
 
 int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
-                 DevCells& c, ErrRec* err, int cap, const Part& P) {
+                 DevCells& c, ErrRec* err, int cap, const Part& P, bool count) {
     const double A = g.cfg.cutoff_a;
     PairP p;
     // gamma(rho)/a = 15/(8a) - 5 r^2/(4a^3) + 3 r^4/(8a^5)          (msm_kernels.hpp:14-20,30-35)
@@ -1224,12 +1229,19 @@ int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& 
     int l = 0;
     if (n > 0) {
         const int split = a.pair_part ? pair_split(maxclu) : 1;
-        auto kern = split > 1 ? (g.kind == MSMB_FIELD_CUTOFF ? k_pairs_mw<MSMB_FIELD_CUTOFF, true>
-                                 : g.kind == MSMB_FIELD_WOLF ? k_pairs_mw<MSMB_FIELD_WOLF, true>
-                                                             : k_pairs_mw<MSMB_FIELD_MSM, true>)
-                              : (g.kind == MSMB_FIELD_CUTOFF ? k_pairs_mw<MSMB_FIELD_CUTOFF, false>
-                                 : g.kind == MSMB_FIELD_WOLF ? k_pairs_mw<MSMB_FIELD_WOLF, false>
-                                                             : k_pairs_mw<MSMB_FIELD_MSM, false>);
+#ifdef MSMB_PAIR_ALWAYS_COUNT // A/B switch: count in every evaluation (the round-1 behaviour)
+        count = true;
+#endif
+        // instances: field kind x split x counting
+        auto pick = [&](auto split_c, auto count_c) {
+            constexpr bool SP = decltype(split_c)::value, CO = decltype(count_c)::value;
+            return g.kind == MSMB_FIELD_CUTOFF ? k_pairs_mw<MSMB_FIELD_CUTOFF, SP, CO>
+                   : g.kind == MSMB_FIELD_WOLF ? k_pairs_mw<MSMB_FIELD_WOLF, SP, CO>
+                                               : k_pairs_mw<MSMB_FIELD_MSM, SP, CO>;
+        };
+        using T = std::true_type;
+        using F = std::false_type;
+        auto kern = split > 1 ? (count ? pick(T{}, T{}) : pick(T{}, F{})) : (count ? pick(F{}, T{}) : pick(F{}, F{}));
         kern<<<int((maxclu * split + kPairWarps - 1) / kPairWarps), kPairWarps * 32, 0, st>>>(
             c.clu, c.plist, c.pcnt, c.pmask, cap, a.xc, a.yc, a.zc, a.qc, p, A * A, a.phis, a.fsx, a.fsy, a.fsz,
             c.col_off, P.cx0 * g.ncy, P.cx1 * g.ncy, n, err, split, a.pair_part);
