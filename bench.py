@@ -579,6 +579,9 @@ def main():
                          "peak_source": "FP64 FMA-chain microbenchmark run live in this bench (msmb_measure_fp64_peak); "
                                         "MEASURED_PEAKS.json has no FP64 entry"},
             "step_roofline": {"t_roof_ms": t_roof, "t_measured_ms": t_meas, "frac": t_roof / t_meas if t_meas else None,
+                              "frac_of_step": t_roof / (total_max / K),
+                              "note": "frac: against the serialised per-stage times (stage-timing pass, no "
+                                      "overlap); frac_of_step: against the measured step (ms_per_step)",
                               "hbm_gbs": hbm, "hbm_source": hbm_src, "fp64_tflops": fp64_peak, "stages": stages},
             "stage_ms_per_eval": {k: round(v, 5) for k, v in per_step.items()},
             "cpu_baseline": cpu,
