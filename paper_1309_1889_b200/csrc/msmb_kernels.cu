@@ -1731,13 +1731,19 @@ __device__ __forceinline__ double restrict_point(const XferP& p, int I, int J, i
 
 // Large levels: a CTA computes a 4x4x8 block of coarse points from a zero-padded
 // shared-memory tile of the fine lattice (fine i in [2I0-5, 2(I0+3)+1], etc.).
-constexpr int kRTx = 4, kRTy = 4, kRTz = 8;
-constexpr int kRFx = 2 * kRTx + 6, kRFy = 2 * kRTy + 6, kRFz = 2 * kRTz + 6;
+// Chain kernels in one-warp CTAs (MSMB_CHAIN_SMALL, default on): a CTA of the small
+// variants needs <= 4096 registers and <= 16 KB of shared memory, which fits beside
+// the pair kernel's 20 one-warp CTAs per SM, so the long-range chain advances while
+// the pair sum runs instead of waiting for its tail (Overlap).
+#ifndef MSMB_CHAIN_SMALL
+#define MSMB_CHAIN_SMALL 1
+#endif
 
 // xlo/xhi: the coarse x-planes to compute (a spatial-decomposition part's own)
-template <bool BITWISE>
+template <bool BITWISE, int kRTx, int kRTy, int kRTz>
 __global__ void __launch_bounds__(kRTx * kRTy * kRTz)
     k_restrict_tile(XferP p, const double* __restrict__ fine, double* coarse, const ErrRec* err, int xlo, int xhi) {
+    constexpr int kRFx = 2 * kRTx + 6, kRFy = 2 * kRTy + 6, kRFz = 2 * kRTz + 6;
     __shared__ double tile[kRFx * kRFy * kRFz];
     if (failed(err)) return;
     const int tz_n = (p.cd[2] + kRTz - 1) / kRTz, ty_n = (p.cd[1] + kRTy - 1) / kRTy;
@@ -1839,8 +1845,9 @@ __global__ void k_prolong(XferP p, const double* __restrict__ coarse, double* fi
     prolong_point(p, coarse, fine, idx);
 }
 
+template <int TX, int TY, int TZ>
 static int restrict_blocks(const XferP& p, int nx) {
-    return ((nx + kRTx - 1) / kRTx) * ((p.cd[1] + kRTy - 1) / kRTy) * ((p.cd[2] + kRTz - 1) / kRTz);
+    return ((nx + TX - 1) / TX) * ((p.cd[1] + TY - 1) / TY) * ((p.cd[2] + TZ - 1) / TZ);
 }
 
 int launch_restrict_all(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err) {
@@ -1853,15 +1860,19 @@ int launch_restrict_all(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec
 int launch_restrict_planes(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err, int xlo, int xhi) {
     const XferP p = make_xfer(g, k, L);
     if (xhi <= xlo) return 0;
-    k_restrict_tile<false><<<restrict_blocks(p, xhi - xlo), kRTx * kRTy * kRTz, 0, st>>>(
-        p, L.charge + g.lv[k].offset, L.charge + g.lv[k + 1].offset, err, xlo, xhi);
+    if (MSMB_CHAIN_SMALL)
+        k_restrict_tile<false, 2, 4, 4><<<restrict_blocks<2, 4, 4>(p, xhi - xlo), 32, 0, st>>>(
+            p, L.charge + g.lv[k].offset, L.charge + g.lv[k + 1].offset, err, xlo, xhi);
+    else
+        k_restrict_tile<false, 4, 4, 8><<<restrict_blocks<4, 4, 8>(p, xhi - xlo), 128, 0, st>>>(
+            p, L.charge + g.lv[k].offset, L.charge + g.lv[k + 1].offset, err, xlo, xhi);
     return 1;
 }
 
 // bit-exact restriction of one level (msmb_debug_stage; tests/test_gpu_stages.py)
 int launch_restrict(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err) {
     const XferP p = make_xfer(g, k, L);
-    k_restrict_tile<true><<<restrict_blocks(p, p.cd[0]), kRTx * kRTy * kRTz, 0, st>>>(
+    k_restrict_tile<true, 4, 4, 8><<<restrict_blocks<4, 4, 8>(p, p.cd[0]), 128, 0, st>>>(
         p, L.charge + g.lv[k].offset, L.charge + g.lv[k + 1].offset, err, 0, p.cd[0]);
     return 1;
 }
@@ -1869,12 +1880,12 @@ int launch_restrict(cudaStream_t st, const Geometry& g, int k, DevLevels& L, Err
 // Prolongation by fine tiles of 4 x 8 x 8 points: the coarse window they read
 // (base .. base + 3 per axis, monotone in the fine index) is staged in shared
 // memory, then each point forms the reference's nested sums (prolong_point order).
-constexpr int kPx = 4, kPy = 8, kPz = 8;
-constexpr int kPCx = kPx / 2 + 5, kPCy = kPy / 2 + 5, kPCz = kPz / 2 + 5;
 
 // xlo/xhi: the fine x-planes to update (a spatial-decomposition part's own)
+template <int kPx, int kPy, int kPz>
 __global__ void __launch_bounds__(kPx * kPy * kPz)
     k_prolong_tile(XferP p, const double* __restrict__ coarse, double* fine, const ErrRec* err, int xlo, int xhi) {
+    constexpr int kPCx = kPx / 2 + 5, kPCy = kPy / 2 + 5, kPCz = kPz / 2 + 5;
     __shared__ double ct[kPCx * kPCy * kPCz];
     if (failed(err)) return;
     const int tz_n = (p.fd[2] + kPz - 1) / kPz, ty_n = (p.fd[1] + kPy - 1) / kPy;
@@ -1930,9 +1941,14 @@ int launch_prolong(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrR
 int launch_prolong_planes(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err, int xlo, int xhi) {
     const XferP p = make_xfer(g, k, L);
     if (xhi <= xlo) return 0;
-    const int blocks = ((xhi - xlo + kPx - 1) / kPx) * ((p.fd[1] + kPy - 1) / kPy) * ((p.fd[2] + kPz - 1) / kPz);
-    k_prolong_tile<<<blocks, kPx * kPy * kPz, 0, st>>>(p, L.pot + g.lv[k + 1].offset, L.pot + g.lv[k].offset, err,
-                                                       xlo, xhi);
+    auto go = [&](auto kern, int px, int py, int pz) {
+        const int blocks = ((xhi - xlo + px - 1) / px) * ((p.fd[1] + py - 1) / py) * ((p.fd[2] + pz - 1) / pz);
+        kern<<<blocks, px * py * pz, 0, st>>>(p, L.pot + g.lv[k + 1].offset, L.pot + g.lv[k].offset, err, xlo, xhi);
+    };
+    if (MSMB_CHAIN_SMALL)
+        go(k_prolong_tile<1, 4, 8>, 1, 4, 8);
+    else
+        go(k_prolong_tile<4, 8, 8>, 4, 8, 8);
     return 1;
 }
 
@@ -2454,7 +2470,7 @@ __global__ void __launch_bounds__(256)
                const double* __restrict__ taps, int rowlen, const ErrRec* err) {
     if (failed(err)) return;
     const int m = d0 * d1 * d2;
-    const int idx = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    const int idx = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (idx >= m) return;
     const int z = idx % d2, y = (idx / d2) % d1, x = idx / (d2 * d1);
     const int Rx = d0 - 1, Ry = d1 - 1, Rz = d2 - 1;
@@ -2497,8 +2513,10 @@ int launch_top(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err, bo
     const LevelGeom& lv = g.lv[k];
     if (!exact && int64_t(lv.size) <= kTopDirectMax) {
         const int rowlen = (2 * g.top.Rz + 1 + kConvL - 1) / kConvL * kConvL;
-        k_top_warp<<<int((lv.size + 7) / 8), 256, 0, st>>>(L.charge + lv.offset, L.pot + lv.offset, lv.dims[0],
-                                                            lv.dims[1], lv.dims[2], L.taps[k], rowlen, err);
+        const int wpb = MSMB_CHAIN_SMALL ? 1 : 8; // warps (points) per CTA
+        k_top_warp<<<int((lv.size + wpb - 1) / wpb), 32 * wpb, 0, st>>>(L.charge + lv.offset, L.pot + lv.offset,
+                                                                         lv.dims[0], lv.dims[1], lv.dims[2], L.taps[k],
+                                                                         rowlen, err);
         return 1;
     }
     if (int64_t(lv.size) <= kTopDirectMax) {
