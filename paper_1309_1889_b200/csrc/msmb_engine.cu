@@ -361,7 +361,13 @@ static bool make_levels(msmb_field* f, Workspace& Wr, Error& e) {
                 lv.q = L.charge + g.lv[k].offset;
                 lv.u = L.pot + g.lv[k].offset;
             }
-            J.L = std::max(1, std::min(16, 2048 / std::max(J.maxM, 1)));
+            // lines per FFT tile: 4 (64-thread CTAs of ~9 KB), which fit beside the pair
+            // kernel's CTAs; C2-S 0.842 ms/step vs 0.849 with 16-line tiles of 256
+            // threads (2 lines: 0.842, 1: 0.855).  MSMB_FFT_LINES overrides (timing knob;
+            // results do not depend on it)
+            int lines = 4;
+            if (const char* e = std::getenv("MSMB_FFT_LINES")) lines = std::max(1, std::min(16, atoi(e)));
+            J.L = std::max(1, std::min(lines, 2048 / std::max(J.maxM, 1)));
             J.buf = walloc<double2>(*W, boff);
             J.spec = walloc<double>(*W, boff);
             return boff;
@@ -556,8 +562,7 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, 
     run("clusters", [&] { return launch_clusters(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, rebuild ? 1 : 0); });
     if (g_exp_stamps) launch_stamp(st, 4);
     run("pairs", [&] {
-        return launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, !t_capturing) +
-               launch_err_brute(st, s.n, s, W.a, W.err);
+        return launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, !t_capturing);
     });
     if (g_exp_stamps) launch_stamp(st, 5);
     if (fork) ck(cudaStreamWaitEvent(st, f->join_ev, 0), "join");
@@ -970,11 +975,14 @@ static int field_new(int device, msmb_field** out) {
     cudaSetDevice(device);
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-    // side (long-range chain) stream priority relative to the main (pair-sum) stream.
-    // Equal measured best on C2-S (1.375 ms/step vs 1.484 with the chain at high and
-    // 1.387 at low priority); MSMB_SIDE_PRIO = high | equal | low is the knob.
-    int side_prio = prio_lo, main_prio = prio_lo;
+    // side (long-range chain) stream priority relative to the main (pair-sum) stream:
+    // high, so the chain's CTAs are dispatched as pair CTAs retire instead of after the
+    // pair kernel's last one.  C2-S round 2 with the 4-line FFT tiles: 0.842 ms/step
+    // vs 0.849 at equal priority (round 1, 256-thread FFT tiles: equal was best).
+    // MSMB_SIDE_PRIO = high | equal | low is the knob.
+    int side_prio = prio_hi, main_prio = prio_lo;
     if (const char* e = std::getenv("MSMB_SIDE_PRIO")) {
+        if (!strcmp(e, "equal")) side_prio = prio_lo, main_prio = prio_lo;
         if (!strcmp(e, "high")) side_prio = prio_hi, main_prio = prio_lo;
         if (!strcmp(e, "low")) side_prio = prio_lo, main_prio = prio_hi;
     }

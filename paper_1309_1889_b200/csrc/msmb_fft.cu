@@ -328,6 +328,8 @@ int blocks_z(FftJobs& J, bool all) {
 }
 
 size_t fft_smem(const FftJobs& J) { return size_t(2) * J.L * J.maxM * sizeof(double2); }
+// threads per tile: 256 for the default 16-line tiles, one warp for tiles of <= 2 lines
+int fft_threads(const FftJobs& J) { return J.L >= 16 ? 256 : std::max(32, ((J.L * 16 + 31) / 32) * 32); }
 
 } // namespace
 
@@ -370,11 +372,11 @@ int launch_fft_spectrum(cudaStream_t st, FftJobs J, const FftKernel* K) {
     }
     const size_t sm = fft_smem(J);
     int nb = blocks_x(J, true);
-    k_fft_x<<<nb, 256, sm, st>>>(J, 2, nullptr);
+    k_fft_x<<<nb, fft_threads(J), sm, st>>>(J, 2, nullptr);
     nb = blocks_y(J, true);
-    k_fft_y<<<nb, 256, sm, st>>>(J, 2, nullptr);
+    k_fft_y<<<nb, fft_threads(J), sm, st>>>(J, 2, nullptr);
     nb = blocks_z(J, true);
-    k_fft_z<<<nb, 256, sm, st>>>(J, 2, nullptr);
+    k_fft_z<<<nb, fft_threads(J), sm, st>>>(J, 2, nullptr);
     return nl + 3;
 }
 
@@ -382,15 +384,15 @@ int launch_lattice_fft(cudaStream_t st, FftJobs J, const ErrRec* err) {
     if (J.n == 0) return 0;
     const size_t sm = fft_smem(J);
     int nb = blocks_x(J, false);
-    k_fft_x<<<nb, 256, sm, st>>>(J, 0, err);
+    k_fft_x<<<nb, fft_threads(J), sm, st>>>(J, 0, err);
     nb = blocks_y(J, false);
-    k_fft_y<<<nb, 256, sm, st>>>(J, 0, err);
+    k_fft_y<<<nb, fft_threads(J), sm, st>>>(J, 0, err);
     nb = blocks_z(J, false);
-    k_fft_z<<<nb, 256, sm, st>>>(J, 0, err);
+    k_fft_z<<<nb, fft_threads(J), sm, st>>>(J, 0, err);
     nb = blocks_y(J, false);
-    k_fft_y<<<nb, 256, sm, st>>>(J, 1, err);
+    k_fft_y<<<nb, fft_threads(J), sm, st>>>(J, 1, err);
     nb = blocks_x(J, false);
-    k_fft_x<<<nb, 256, sm, st>>>(J, 1, err);
+    k_fft_x<<<nb, fft_threads(J), sm, st>>>(J, 1, err);
     return 5;
 }
 

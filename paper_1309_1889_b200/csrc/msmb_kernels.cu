@@ -2,18 +2,19 @@
 //
 // Stage map (reference file:line -> kernel):
 //   K1  bin + counting sort          src/msm_phases.cpp:21-29 (stencil_at base), msm.cpp:25-27
-//                                    -> k_bin, k_scan_*, k_scatter, k_cellsort, k_gather
+//                                    -> k_bin, k_sort_decide, k_scan_*, k_scatter, k_cellsort, k_coincide
 //   K2  short-range pairs            src/msm_phases.cpp:224-252, msm_kernels.hpp:30-42
-//                                    -> k_columns, k_clusters, k_bbox, k_pairlist, k_pairs, k_err_brute
-//   K3  anterpolation                src/msm_phases.cpp:39-61      -> k_anterp
+//                                    -> k_flag_reset, k_disp, k_cl_gather (+ out-of-grid pair errors),
+//                                       k_colscan, k_bbox, k_pairlist, k_pairmask (rebuilds), k_pairs_mw
+//   K3  anterpolation                src/msm_phases.cpp:39-61      -> k_anterp_tile, k_anterp_combine
 //   K4  restriction                  src/msm_phases.cpp:63-91      -> k_restrict_tile
-//   K5  lattice cutoff               src/msm_phases.cpp:93-134     -> k_lattice, k_lattice_reduce
-//   K6  top level                    src/msm_phases.cpp:136-162    -> k_top_direct (k_conv above 8192 points)
-//   K7  prolongation                 src/msm_phases.cpp:164-193    -> k_prolong
+//   K5  lattice cutoff               src/msm_phases.cpp:93-134     -> msmb_fft.cu (k_fft_x/y/z); k_lattice (direct)
+//   K6  top level                    src/msm_phases.cpp:136-162    -> k_top_warp (FFT job for large tops)
+//   K7  prolongation                 src/msm_phases.cpp:164-193    -> k_prolong_tile
 //   K8  interpolation + forces + E   src/msm_phases.cpp:195-222, src/msm.cpp:16-48,69-86
-//                                    -> k_interp, k_energy1/2
+//                                    -> k_interp, k_energy1/2, k_finalize
 //   K9  velocity Verlet              src/integrate.cpp:23-34       -> k_kick_drift, k_kick
-//   K10 parareal state algebra       src/parareal.cpp:58-90        -> k_state_sub/add, k_rms
+//   K10 parareal state algebra       src/parareal.cpp:58-90        -> msmb_parareal.cu
 // Determinism: no floating-point atomics anywhere; every sum has a fixed order.
 // Arithmetic that must reproduce the reference bit for bit (cell keys, stencil
 // weights, restriction/prolongation/interpolation given equal lattices, Verlet)
@@ -450,67 +451,107 @@ __global__ void k_disp(int64_t n, const double* __restrict__ x, const double* __
     if (!(dx * dx + dy * dy + dz * dz <= half_skin2)) flag[0] = 1; // same value from every writer
 }
 
-__global__ void k_cl_perm(int64_t n, const int* __restrict__ start_total, const int* __restrict__ perm,
-                          const double* __restrict__ x, const double* __restrict__ y,
-                          const double* __restrict__ z, int* cl_perm, int* cl_inv, double* ref, int* flag,
-                          int key) {
-    if (!flag[0]) return;
-    const int tot = *start_total;
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s == 0) {
-        flag[1] = tot;
-        flag[2] += 1; // rebuilds since the workspace was created (diagnostics)
-        flag[3] = 1;  // valid until the host invalidates it (capacity growth, errors)
-        flag[4] = key;
-    }
-    if (s >= tot) return;
-    const int i = perm[s];
-    cl_perm[s] = i;
-    cl_inv[i] = s;
-    ref[i] = x[i];
-    ref[n + i] = y[i];
-    ref[2 * n + i] = z[i];
-}
+__device__ void err_brute_blocks(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
+                                 const double* __restrict__ z, const int* __restrict__ outlist, ErrRec* err,
+                                 int b, int nb);
 
-__global__ void k_gather_cl(const int* __restrict__ flag, const int* __restrict__ cl_perm,
+// Cluster-order positions, every evaluation: slot s of the frozen cluster order holds
+// atom cl_perm[s]; at a rebuild (flag[0]) the order is first re-frozen from the cell
+// sort (cl_perm = perm, its inverse, the reference positions of the skin test).
+// Blocks past the atom range run the out-of-grid pair-error search (k_err_brute's
+// grid-stride loop; it exits at once unless k_bin counted atoms outside coverage):
+// one launch instead of three on a skin step.
+__global__ void k_cl_gather(int64_t n, const int* __restrict__ start_total, const int* __restrict__ perm,
                             const double* __restrict__ x, const double* __restrict__ y,
-                            const double* __restrict__ z, const double* __restrict__ q, double* xc,
-                            double* yc, double* zc, double* qc, const ErrRec* err) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= flag[1] || failed(err)) return;
-    const int i = cl_perm[k];
-    xc[k] = x[i];
-    yc[k] = y[i];
-    zc[k] = z[i];
-    qc[k] = q[i];
-}
-
-__global__ void k_columns(int64_t ncols, int cells_per_col, const int* __restrict__ start,
-                          int* col_cnt, const int* __restrict__ flag, const ErrRec* err) {
-    const int64_t col = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (col > ncols || failed(err) || !flag[0]) return;
-    if (col == ncols) {
-        col_cnt[col] = 0;
+                            const double* __restrict__ z, const double* __restrict__ q, int* cl_perm, int* cl_inv,
+                            double* ref, int* flag, int key, double* xc, double* yc, double* zc, double* qc,
+                            int gather_blocks, const int* __restrict__ outlist, ErrRec* err) {
+    if (int(blockIdx.x) >= gather_blocks) {
+        err_brute_blocks(n, x, y, z, outlist, err, blockIdx.x - gather_blocks, gridDim.x - gather_blocks);
         return;
     }
-    const int cnt = start[(col + 1) * cells_per_col] - start[col * cells_per_col];
-    col_cnt[col] = (cnt + 31) / 32;
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (failed(err)) return;
+    int i;
+    if (flag[0]) {
+        const int tot = *start_total;
+        if (s == 0) {
+            flag[1] = tot;
+            flag[2] += 1; // rebuilds since the workspace was created (diagnostics)
+            flag[3] = 1;  // valid until the host invalidates it (capacity growth, errors)
+            flag[4] = key;
+        }
+        if (s >= tot) return;
+        i = perm[s];
+        cl_perm[s] = i;
+        cl_inv[i] = s;
+        ref[i] = x[i];
+        ref[n + i] = y[i];
+        ref[2 * n + i] = z[i];
+    } else {
+        if (s >= flag[1]) return;
+        i = cl_perm[s];
+    }
+    xc[s] = x[i];
+    yc[s] = y[i];
+    zc[s] = z[i];
+    qc[s] = q[i];
 }
 
-__global__ void k_clusters(int64_t ncols, int cells_per_col, const int* __restrict__ start,
-                           const int* __restrict__ col_off, int2* clu, int* nclu, int* colstart,
-                           const int* __restrict__ flag, const ErrRec* err) {
-    const int64_t col = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (col >= ncols || failed(err) || !flag[0]) return;
-    if (col == ncols - 1) {
-        *nclu = col_off[ncols];
-        colstart[ncols] = start[ncols * cells_per_col];
+// Columns -> clusters (rebuild evaluations only), one block: clusters per column
+// (32 consecutive sorted atoms each), their exclusive scan col_off, then the
+// clusters (first sorted slot, count), the columns' first slots and the total.
+// One launch instead of five (columns, a three-kernel scan, clusters): on skin steps
+// they only read flag[0] and exit.
+__global__ void __launch_bounds__(1024)
+    k_colscan(int64_t ncols, int cells_per_col, const int* __restrict__ start, int* col_cnt, int* col_off,
+              int2* clu, int* nclu, int* colstart, const int* __restrict__ flag, const ErrRec* err) {
+    if (failed(err) || !flag[0]) return;
+    __shared__ int s_w[32];
+    __shared__ int s_carry;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    if (t == 0) s_carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base <= ncols; base += 1024) {
+        const int64_t col = base + t;
+        int cnt = 0;
+        if (col < ncols) cnt = (start[(col + 1) * cells_per_col] - start[col * cells_per_col] + 31) / 32;
+        if (col <= ncols) col_cnt[col] = cnt;
+        int v = cnt; // inclusive warp scan, then across warps
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(FULLMASK, v, o);
+            if (lane >= o) v += u;
+        }
+        if (lane == 31) s_w[w] = v;
+        __syncthreads();
+        if (w == 0) {
+            int x = s_w[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(FULLMASK, x, o);
+                if (lane >= o) x += u;
+            }
+            s_w[lane] = x;
+        }
+        __syncthreads();
+        const int carry = s_carry;
+        const int excl = carry + (w > 0 ? s_w[w - 1] : 0) + v - cnt;
+        if (col <= ncols) col_off[col] = excl;
+        if (col < ncols) {
+            const int s0 = start[col * cells_per_col];
+            colstart[col] = s0;
+            const int na = start[(col + 1) * cells_per_col] - s0;
+            for (int k = 0; 32 * k < na; ++k) clu[excl + k] = make_int2(s0 + 32 * k, min(32, na - 32 * k));
+        }
+        if (col == ncols) {
+            *nclu = excl;
+            colstart[ncols] = start[ncols * cells_per_col];
+        }
+        __syncthreads();
+        if (t == 0) s_carry = carry + s_w[31];
+        __syncthreads();
     }
-    const int s0 = start[col * cells_per_col];
-    colstart[col] = s0;
-    const int cnt = start[(col + 1) * cells_per_col] - s0;
-    const int off = col_off[col];
-    for (int k = 0; 32 * k < cnt; ++k) clu[off + k] = make_int2(s0 + 32 * k, min(32, cnt - 32 * k));
 }
 
 __global__ void k_bbox(const int* __restrict__ nclu, const int2* __restrict__ clu,
@@ -986,6 +1027,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     auto fetch = [&](int jj) {
         const int64_t sj = min(int64_t(pl[jj]) + lane, n - 1); // lanes past the cluster: masked out
         mk_n = pm[size_t(jj) * 32];
+#ifdef MSMB_EXP_NOSTAGE
+        if (jj >= kRing) return;
+#endif
         xj_n = xs[sj];
         yj_n = ys[sj];
         zj_n = zs[sj];
@@ -994,8 +1038,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     auto stage = [&](int jj) {
         const int slot = jj & (kRing - 1);
         const int pos = slot * kSlots + 32 - lane;
+#ifdef MSMB_EXP_NOSTAGE // timing experiment only (wrong results): rows staged once
+        if (jj < kRing)
+#endif
+        {
         s_v[w][0][pos] = make_double2(xj_n, yj_n);
         s_v[w][1][pos] = make_double2(zj_n, qj_n);
+        }
         s_mask[w][slot][lane] = mk_n;
         if (COUNT) ncand += __popc(mk_n);
         if (jj + 1 < nj) fetch(jj + 1);
@@ -1019,7 +1068,11 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         unsigned bit;
         asm("shl.b32 %0, %1, %2;" : "=r"(bit) : "r"(1u), "r"(pos));
         m ^= bit; // bit = 0 when m == 0 (shl clamps): the dummy step leaves m at 0
+#ifdef MSMB_EXP_NOBANK // timing experiment only (wrong results): conflict-free row reads
+        const double2* rs = rows + 1 + (lane & 7) + (pos & 24);
+#else
         const double2* rs = row + (pos + 1);
+#endif
         const double2 xy = rs[0], zq = rs[kRing * kSlots];
         advance();
         const double dx = xi - xy.x, dy = yi - xy.y, dz = zi - zq.x;
@@ -1102,15 +1155,16 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
 
 // Error path only: pairs involving particles that could not be binned
 // (outside grid coverage or non-finite) against every particle, with the
-// reference's arithmetic, to find the first pair with r2 == 0 or NaN.
-__global__ void k_err_brute(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
-                            const double* __restrict__ z, const int* __restrict__ outlist,
-                            ErrRec* err) {
+// reference's arithmetic, to find the first pair with r2 == 0 or NaN.  Run by the
+// blocks b = 0 .. nb-1 past k_cl_gather's atom range (record_pair is an atomicMin:
+// the result does not depend on when or by whom the pairs are visited).
+__device__ void err_brute_blocks(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
+                                 const double* __restrict__ z, const int* __restrict__ outlist, ErrRec* err,
+                                 int b, int nb) {
     const int cnt = __ldcg(&err->cov_count);
     if (cnt == 0 || failed(err)) return;
     const int64_t total = int64_t(cnt) * n;
-    for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
-         idx += int64_t(gridDim.x) * blockDim.x) {
+    for (int64_t idx = int64_t(b) * blockDim.x + threadIdx.x; idx < total; idx += int64_t(nb) * blockDim.x) {
         const int o = outlist[idx / n];
         const int j = int(idx % n);
         if (j == o) continue;
@@ -1121,32 +1175,33 @@ __global__ void k_err_brute(int64_t n, const double* __restrict__ x, const doubl
     }
 }
 
-// The rebuild-only kernels (k_cl_perm .. k_pairmask) are launched every evaluation and
-// exit early on skin steps.  Skipping them inside the captured graphs with IF
-// conditional nodes (cudaGraphSetConditional from the flag) was tried: adding the
-// conditional node to the capturing graph returned cudaErrorInvalidValue on this
-// driver/runtime, so the early-exit launches stay.
+// Launches of a skin step (no rebuild): k_flag_reset, k_disp, k_cl_gather and the
+// four rebuild kernels k_colscan, k_bbox, k_pairlist, k_pairmask, which read flag[0]
+// and exit.  Measured alternatives: IF conditional graph nodes around the rebuild
+// kernels (cudaGraphSetConditional from the deciding kernel): an untaken IF node
+// costs ~8 us of graph execution on this driver (tools/cond_probe.cu: 10.6 us vs
+// 13.5 us for ten early-exit kernels, 2.1 us without either), and with four of them
+// per evaluation the C2-S step went 0.845 -> 0.862 ms; leaving the rebuild kernels
+// out of the step graphs entirely (timing only) gave 0.809 ms -- the fusions here
+// (13 -> 7 launches) take part of that without the IF nodes.
 int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
                     DevCells& c, ErrRec* err, int cap, const Part& P, int force_rebuild, int disp) {
     const int cells_per_col = int(g.lv[0].dims[2]) * g.cw * g.cw;
     const int64_t nc = g.ncols;
-    const int nb = int((n + 255) / 256) > 0 ? int((n + 255) / 256) : 1;
     // rebuild decision, frozen cluster order, current positions in it
     const int key = P.cx0 * 65536 + P.cx1;
     k_flag_reset<<<1, 1, 0, st>>>(c.flag, force_rebuild || !(g.skin > 0.0) ? 1 : 0, key);
     const double hs = 0.5 * g.skin;
     if (disp) k_disp<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, s.x, s.y, s.z, a.ref, hs * hs, c.flag);
-    k_cl_perm<<<nb, 256, 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, a.cl_perm, a.cl_inv, a.ref, c.flag, key);
-    k_gather_cl<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(c.flag, a.cl_perm, s.x, s.y, s.z, s.q, a.xc, a.yc,
-                                                                     a.zc, a.qc, err);
+    const int gb = int((std::max<int64_t>(n, 1) + 255) / 256);
+    k_cl_gather<<<gb + 592, 256, 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, s.q, a.cl_perm, a.cl_inv,
+                                          a.ref, c.flag, key, a.xc, a.yc, a.zc, a.qc, gb, a.outlist, err);
     // cluster pair list (rebuild evaluations only)
-    k_columns<<<int((nc + 1 + 255) / 256), 256, 0, st>>>(nc, cells_per_col, c.start, c.col_cnt, c.flag, err);
-    int l = 5 + scan_exclusive(st, c.col_cnt, c.col_off, c.scan_tmp, nc + 1, c.flag); // rebuilds only (flag[0])
-    k_clusters<<<int((nc + 255) / 256), 256, 0, st>>>(nc, cells_per_col, c.start, c.col_off, c.clu,
-                                                      c.nclu, c.colstart, c.flag, err);
+    k_colscan<<<1, 1024, 0, st>>>(nc, cells_per_col, c.start, c.col_cnt, c.col_off, c.clu, c.nclu, c.colstart,
+                                  c.flag, err);
     const int64_t maxclu = n / 32 + nc + 1;
-    k_bbox<<<int((maxclu * 32 + 255) / 256), 256, 0, st>>>(c.nclu, c.clu, a.xc, a.yc, a.zc, c.blo,
-                                                            c.bhi, c.flag, err);
+    k_bbox<<<int((maxclu * 32 + 255) / 256), 256, 0, st>>>(c.nclu, c.clu, a.xc, a.yc, a.zc, c.blo, c.bhi, c.flag,
+                                                           err);
     ListP lp;
     lp.ox = g.lv[0].origin[0];
     lp.oy = g.lv[0].origin[1];
@@ -1170,14 +1225,11 @@ int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevStat
     k_pairlist<<<int((maxclu * 32 + 255) / 256), 256, 0, st>>>(c.nclu, c.blo, c.bhi, c.col_off, c.start, lp,
                                                                 c.plist, c.pcnt, cap, P.cx0 * g.ncy,
                                                                 P.cx1 * g.ncy, c.flag, err);
-    {
-        const double lm = g.cfg.cutoff_a + g.skin; // mask cut: a + skin (+ the fp32 pad in k_pairmask)
-        k_pairmask<<<int((maxclu + kMaskWarps - 1) / kMaskWarps), kMaskWarps * 32, 0, st>>>(
-            c.clu, c.plist, c.pcnt, c.pmask, cap, a.xc, a.yc, a.zc, float_ru(lm * lm * (1.0 + 1e-6)), c.col_off,
-            P.cx0 * g.ncy, P.cx1 * g.ncy, c.flag, err);
-        ++l;
-    }
-    return l + 3;
+    const double lm = g.cfg.cutoff_a + g.skin; // mask cut: a + skin (+ the fp32 pad in k_pairmask)
+    k_pairmask<<<int((maxclu + kMaskWarps - 1) / kMaskWarps), kMaskWarps * 32, 0, st>>>(
+        c.clu, c.plist, c.pcnt, c.pmask, cap, a.xc, a.yc, a.zc, float_ru(lm * lm * (1.0 + 1e-6)), c.col_off,
+        P.cx0 * g.ncy, P.cx1 * g.ncy, c.flag, err);
+    return 7 + (disp ? 1 : 0);
 }
 
 // sums of the split pair walks, in part order, then the per-atom force factor
@@ -1258,11 +1310,6 @@ int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& 
 
 // pair errors of particles outside grid coverage (NaN / coincident with anyone); needs
 // only the binning, so the spatial decomposition checks it before the pair sum
-int launch_err_brute(cudaStream_t st, int64_t n, const DevState& s, DevAtoms& a, ErrRec* err) {
-    if (n <= 0) return 0;
-    k_err_brute<<<592, 256, 0, st>>>(n, s.x, s.y, s.z, a.outlist, err);
-    return 1;
-}
 
 // ============================================================================
 // K3: anterpolation as an owner-computes gather (no atomics).  16 lanes own a quad
@@ -1731,12 +1778,14 @@ __device__ __forceinline__ double restrict_point(const XferP& p, int I, int J, i
 
 // Large levels: a CTA computes a 4x4x8 block of coarse points from a zero-padded
 // shared-memory tile of the fine lattice (fine i in [2I0-5, 2(I0+3)+1], etc.).
-// Chain kernels in one-warp CTAs (MSMB_CHAIN_SMALL, default on): a CTA of the small
-// variants needs <= 4096 registers and <= 16 KB of shared memory, which fits beside
-// the pair kernel's 20 one-warp CTAs per SM, so the long-range chain advances while
-// the pair sum runs instead of waiting for its tail (Overlap).
+// Chain kernels in one-warp CTAs (MSMB_CHAIN_SMALL, default off): a CTA of the small
+// variants needs <= 4096 registers and <= 16 KB of shared memory, so it fits beside
+// the pair kernel's one-warp CTAs.  Measured on C2-S: 0.864 ms/step against 0.849
+// with the large CTAs -- the chain does not start earlier (it waits on the
+// anterpolation, which follows the sort, not the pair sum) and the small CTAs
+// re-read their halos more often.
 #ifndef MSMB_CHAIN_SMALL
-#define MSMB_CHAIN_SMALL 1
+#define MSMB_CHAIN_SMALL 0
 #endif
 
 // xlo/xhi: the coarse x-planes to compute (a spatial-decomposition part's own)

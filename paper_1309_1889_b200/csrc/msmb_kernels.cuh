@@ -140,7 +140,6 @@ int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevStat
 // count: accumulate the pair / candidate statistics (eager evaluations; graphs skip it)
 int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
                  DevCells& c, ErrRec* err, int cap, const Part& P, bool count = true);
-int launch_err_brute(cudaStream_t st, int64_t n, const DevState& s, DevAtoms& a, ErrRec* err);
 int launch_anterp(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& a, DevCells& c, DevLevels& L,
                   ErrRec* err, const Part& P);
 size_t anterp_tile_part_doubles(const Geometry& g);

@@ -761,8 +761,7 @@ void evaluate(msmb_slab* g, bool rebuild) {
         DevState s = p.st.dev();
         DevOut o = W.o;
         o.phi = o.phis = o.phil = nullptr;
-        int nl = launch_err_brute(st, s.n, s, W.a, W.err);
-        nl += launch_interp(st, G, s.n, W.a, W.c, W.L, o, W.err, 0, W.part);
+        int nl = launch_interp(st, G, s.n, W.a, W.c, W.L, o, W.err, 0, W.part);
         // the part's energy share: its atoms' e_i in index order (fixed tree)
         if (p.n_owned) {
             k_gather_e<<<nb256(p.n_owned), 256, 0, st>>>(p.owned.as<int>(), p.n_owned, o.e, p.ebuf.as<double>());
