@@ -535,14 +535,22 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, 
         run("finalize", [&] { return launch_finalize(st, s, W.err, 1); });
         return total;
     }
+    cudaStream_t la = fork ? f->side_a : st; // anterpolation, then the rest of the chain on lr
+    // the cluster kernels (7 short launches on a skin step) before the fork: beside the
+    // anterpolation's CTAs they took ~50 us instead of ~27 (C2-S 0.836 -> 0.831 ms/step)
+    run("clusters", [&] { return launch_clusters(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, rebuild ? 1 : 0); });
     if (fork) {
         ck(cudaEventRecord(f->fork_ev, st), "fork");
-        ck(cudaStreamWaitEvent(lr, f->fork_ev, 0), "fork");
+        ck(cudaStreamWaitEvent(la, f->fork_ev, 0), "fork");
     }
-    if (g_exp_stamps) { launch_stamp(st, 1); launch_stamp(lr, 2); }
+    if (g_exp_stamps) { launch_stamp(st, 1); launch_stamp(la, 2); }
     if (g_exp_chain != 0 && g_exp_chain != 2)
-        run("anterp", [&] { return launch_anterp(lr, g, s, W.a, W.c, W.L, W.err, W.whole); });
-    if (g_exp_stamps) launch_stamp(lr, 7);
+        run("anterp", [&] { return launch_anterp(la, g, s, W.a, W.c, W.L, W.err, W.whole); });
+    if (g_exp_stamps) launch_stamp(la, 7);
+    if (fork) {
+        ck(cudaEventRecord(f->mid_ev, la), "fork");
+        ck(cudaStreamWaitEvent(lr, f->mid_ev, 0), "fork");
+    }
     const bool full = g_exp_chain < 0 || g_exp_chain == 2;
     if (full || g_exp_chain >= 3) run("restrict", [&] { return launch_restrict_all(lr, g, W.L, W.err); });
     if (g_exp_stamps) launch_stamp(lr, 8);
@@ -559,7 +567,6 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, 
     if (full) run("prolong", [&] { return launch_prolong_all(lr, g, W.L, W.err); });
     if (g_exp_stamps) launch_stamp(lr, 3);
     if (fork) ck(cudaEventRecord(f->join_ev, lr), "join");
-    run("clusters", [&] { return launch_clusters(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, rebuild ? 1 : 0); });
     if (g_exp_stamps) launch_stamp(st, 4);
     run("pairs", [&] {
         return launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, !t_capturing);
@@ -986,18 +993,24 @@ static int field_new(int device, msmb_field** out) {
         if (!strcmp(e, "high")) side_prio = prio_hi, main_prio = prio_lo;
         if (!strcmp(e, "low")) side_prio = prio_lo, main_prio = prio_hi;
     }
-    // the spatial decomposition's long-range chain runs beside a pair kernel of many
-    // waves (C3: 131k blocks), whose pending blocks would otherwise be dispatched first
+    // the anterpolation's stream: the chain's priority (MSMB_ANTERP_PRIO=main: the main
+    // stream's; measured equal on C2-S, 0.836 ms/step: at main priority the
+    // anterpolation waits behind the pair kernel and the chain ends after it)
+    int anterp_prio = side_prio;
+    if (const char* e = std::getenv("MSMB_ANTERP_PRIO"))
+        if (!strcmp(e, "main")) anterp_prio = main_prio;
     if (cudaStreamCreateWithPriority(&f->stream, cudaStreamNonBlocking, main_prio) != cudaSuccess ||
         cudaStreamCreateWithPriority(&f->side, cudaStreamNonBlocking, side_prio) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&f->side_hi, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&f->side_a, cudaStreamNonBlocking, anterp_prio) != cudaSuccess ||
         cudaEventCreateWithFlags(&f->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&f->join_ev, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&f->join_ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f->mid_ev, cudaEventDisableTiming) != cudaSuccess) {
         if (f->stream) cudaStreamDestroy(f->stream);
         if (f->side) cudaStreamDestroy(f->side);
-        if (f->side_hi) cudaStreamDestroy(f->side_hi);
+        if (f->side_a) cudaStreamDestroy(f->side_a);
         if (f->fork_ev) cudaEventDestroy(f->fork_ev);
         if (f->join_ev) cudaEventDestroy(f->join_ev);
+        if (f->mid_ev) cudaEventDestroy(f->mid_ev);
         delete f;
         g_create_error = Error{MSMB_ERR_CUDA, -1, -1, -1, "cudaStreamCreate failed"};
         return MSMB_ERR_CUDA;
@@ -1013,9 +1026,10 @@ static void field_free(msmb_field* f) {
     f->scratch.buf.reset();
     cudaStreamDestroy(f->stream);
     cudaStreamDestroy(f->side);
-    cudaStreamDestroy(f->side_hi);
+    cudaStreamDestroy(f->side_a);
     cudaEventDestroy(f->fork_ev);
     cudaEventDestroy(f->join_ev);
+    cudaEventDestroy(f->mid_ev);
     delete f;
 }
 

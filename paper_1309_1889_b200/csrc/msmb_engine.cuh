@@ -140,8 +140,8 @@ struct msmb_field {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;             // long-range chain, forked from `stream`
-    cudaStream_t side_hi = nullptr;          // the same at the highest priority (spatial decomposition)
-    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    cudaStream_t side_a = nullptr;           // the chain's anterpolation (at the main stream's priority)
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr, mid_ev = nullptr;
     std::recursive_mutex mu;
     std::unique_ptr<msmb::Workspace> ws;
     msmb::Error last;

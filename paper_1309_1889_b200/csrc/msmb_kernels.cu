@@ -2,7 +2,7 @@
 //
 // Stage map (reference file:line -> kernel):
 //   K1  bin + counting sort          src/msm_phases.cpp:21-29 (stencil_at base), msm.cpp:25-27
-//                                    -> k_bin, k_sort_decide, k_scan_*, k_scatter, k_cellsort, k_coincide
+//                                    -> k_bin, k_sort_decide, k_scan_block/add, k_scatter, k_cellsort (+ coincidence)
 //   K2  short-range pairs            src/msm_phases.cpp:224-252, msm_kernels.hpp:30-42
 //                                    -> k_flag_reset, k_disp, k_cl_gather (+ out-of-grid pair errors),
 //                                       k_colscan, k_bbox, k_pairlist, k_pairmask (rebuilds), k_pairs_mw
@@ -229,54 +229,32 @@ __global__ void __launch_bounds__(1024) k_scan_block(const int* __restrict__ in,
     }
 }
 
-__global__ void __launch_bounds__(1024) k_scan_sums(int* bsum, int nb, const int* __restrict__ gate) {
+// second pass: block b adds the sum of the blocks before it (it reduces bsum[0..b)
+// itself: one launch instead of a block-sum scan and an add; at most a few thousand
+// block sums even for C3's 11M cells)
+__global__ void __launch_bounds__(1024) k_scan_add(int* out, const int* __restrict__ bsum, int64_t m,
+                                                   const int* __restrict__ gate) {
     __shared__ int wsum[32];
-    __shared__ int carry;
     if (gate && !*gate) return;
-    if (threadIdx.x == 0) carry = 0;
+    const int b = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int v = 0;
+    for (int k = threadIdx.x; k < b; k += 1024) v += bsum[k];
+    v = __reduce_add_sync(FULLMASK, v);
+    if (lane == 0) wsum[w] = v;
     __syncthreads();
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int base = 0; base < nb; base += 1024) {
-        const int idx = base + threadIdx.x;
-        const int v = idx < nb ? bsum[idx] : 0;
-        int inc = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(FULLMASK, inc, o);
-            if (lane >= o) inc += t;
-        }
-        if (lane == 31) wsum[w] = inc;
-        __syncthreads();
-        if (w == 0) {
-            const int ws = wsum[lane];
-            int wi = ws;
-            for (int o = 1; o < 32; o <<= 1) {
-                const int t = __shfl_up_sync(FULLMASK, wi, o);
-                if (lane >= o) wi += t;
-            }
-            wsum[lane] = wi - ws;
-        }
-        __syncthreads();
-        const int excl = carry + wsum[w] + inc - v;
-        __syncthreads();
-        if (idx < nb) bsum[idx] = excl;
-        if (threadIdx.x == 1023) carry = excl + v;
-        __syncthreads();
-    }
-}
-
-__global__ void k_scan_add(int* out, const int* __restrict__ bsum, int64_t m, const int* __restrict__ gate) {
-    if (gate && !*gate) return;
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i < m) out[i] += bsum[i / 4096];
+    const int off = __reduce_add_sync(FULLMASK, wsum[lane]);
+    if (off == 0) return;
+    const int64_t base = int64_t(b) * 4096;
+    for (int k = threadIdx.x; k < 4096; k += 1024)
+        if (base + k < m) out[base + k] += off;
 }
 
 static int scan_exclusive(cudaStream_t st, const int* in, int* out, int* tmp, int64_t m,
                           const int* gate = nullptr) {
     const int nb = int((m + 4095) / 4096);
     k_scan_block<<<nb, 1024, 0, st>>>(in, out, tmp, m, gate);
-    k_scan_sums<<<1, 1024, 0, st>>>(tmp, nb, gate);
-    k_scan_add<<<int((m + 255) / 256), 256, 0, st>>>(out, tmp, m, gate);
-    return 3;
+    k_scan_add<<<nb, 1024, 0, st>>>(out, tmp, m, gate);
+    return 2;
 }
 
 // Cell-sort reuse: k_bin sets flag[5] when some atom's cell key differs from its key
@@ -288,6 +266,8 @@ __global__ void k_sort_decide(int* flag) {
     const int need = flag[5] || !flag[6];
     flag[7] = need;
     flag[6] = 1;
+    flag[5] = 0; // for the next evaluation's k_bin (a launch_bin without a sort after it
+                 // leaves it set: the next sort then runs, which is always correct)
 }
 
 int launch_scan_exclusive(cudaStream_t st, const int* in, int* out, int* tmp, int64_t m) {
@@ -306,12 +286,7 @@ __global__ void k_scatter(int n, const int* __restrict__ key, const int* __restr
 
 // within-cell order = ascending original index (deterministic; cells are small);
 // also publishes each level-0 cell's range in natural (x, y, z) row-major order
-__global__ void k_cellsort(int64_t ncells, BinP p, const int* __restrict__ start, int* perm,
-                           int2* nat, const double* __restrict__ x, const double* __restrict__ y,
-                           const double* __restrict__ z, ErrRec* err, const int* __restrict__ gate) {
-    const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (c >= ncells || failed(err) || !*gate) return;
-    const int s0 = start[c], s1 = start[c + 1];
+__device__ void cell_sort_one(int64_t c, const BinP& p, int s0, int s1, int* perm, int2* nat) {
     {
         int64_t t = c;
         const int oy = int(t % p.cw);
@@ -334,6 +309,32 @@ __global__ void k_cellsort(int64_t ncells, BinP p, const int* __restrict__ start
     }
 }
 
+// thread per cell: the cell sort (when gate) and, with coincide, the exact-coincidence
+// check of every pair of atoms sharing the cell (src/msm_phases.cpp:237-239; the same
+// pairs as coincide_check) in every evaluation -- positions change even when the sort
+// is reused.  One launch instead of a cell sort and a per-atom check.
+__global__ void k_cellsort(int64_t ncells, BinP p, const int* __restrict__ start, int* perm,
+                           int2* nat, const double* __restrict__ x, const double* __restrict__ y,
+                           const double* __restrict__ z, ErrRec* err, const int* __restrict__ gate,
+                           int coincide) {
+    const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= ncells || failed(err)) return;
+    const int s0 = start[c], s1 = start[c + 1];
+    if (*gate) cell_sort_one(c, p, s0, s1, perm, nat);
+    if (!coincide) return;
+    for (int a = s0; a + 1 < s1; ++a) {
+        const int i = perm[a];
+        const double px = x[i], py = y[i], pz = z[i];
+        for (int b = a + 1; b < s1; ++b) {
+            const int j = perm[b];
+            if (x[j] == px && y[j] == py && z[j] == pz) {
+                const unsigned long long k = ((unsigned long long)min(i, j) << 32) | (unsigned long long)max(i, j);
+                atomicMin(&err->pair_key, k);
+            }
+        }
+    }
+}
+
 // exactly coincident particles (r2 == 0, src/msm_phases.cpp:237-239) share a cell: every
 // evaluation compares each sorted atom with the later atoms of its cell (cells hold
 // ~1-2 atoms); runs whether or not the cell sort was reused
@@ -352,13 +353,6 @@ __device__ __forceinline__ void coincide_check(int s, int i, const int* __restri
     }
 }
 
-__global__ void k_coincide(const int* __restrict__ start_total, const int* __restrict__ perm,
-                           const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ z,
-                           ErrRec* err, const int* __restrict__ key, const int* __restrict__ start) {
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= *start_total || failed(err)) return;
-    coincide_check(s, perm[s], key, start, perm, x, y, z, err);
-}
 
 // the anterpolation weights of particle i: o[0..3] = q*wx[d], o[4..7] = wy[d], o[8..11] =
 // wz[d], exactly as anterpolate's qa / w (msm_phases.cpp:42-53)
@@ -394,8 +388,7 @@ __global__ void k_gather(int n, const int* __restrict__ start_total, const int* 
 int launch_bin(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& a, DevCells& c,
                ErrRec* err, const int* list, int64_t nlist) {
     const int n = list ? int(nlist) : int(s.n);
-    cudaMemsetAsync(c.count, 0, sizeof(int) * size_t(g.ncells + 1), st);
-    cudaMemsetAsync(c.flag + 5, 0, sizeof(int), st);
+    cudaMemsetAsync(c.count, 0, sizeof(int) * size_t(g.ncells + 1), st); // flag[5]: see k_sort_decide
     if (n > 0)
         k_bin<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, s.x, s.y, s.z, make_binp(g), a.key, a.rank,
                                                c.count, a.outlist, err, list, c.flag + 5);
@@ -411,15 +404,12 @@ int launch_sort(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms&
     if (n > 0)
         k_scatter<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, a.key, a.rank, c.start, a.perm, err, list,
                                                                        gate);
-    // also publishes the (possibly empty) natural-order cell ranges read by k_anterp
+    // also publishes the (possibly empty) natural-order cell ranges read by k_anterp;
+    // without precomputed anterpolation weights (k_gather) it runs the coincidence check
+    const bool weights = g.kind == MSMB_FIELD_MSM && !MSMB_ANTERP_TILE;
     k_cellsort<<<int((g.ncells + 255) / 256), 256, 0, st>>>(g.ncells, make_binp(g), c.start, a.perm,
-                                                            c.nat, s.x, s.y, s.z, err, gate);
-    if (n == 0) return l + 1;
-    if (g.kind != MSMB_FIELD_MSM || MSMB_ANTERP_TILE) { // no precomputed weights: the coincidence check alone
-        k_coincide<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(c.start + g.ncells, a.perm, s.x, s.y, s.z,
-                                                                       err, a.key, c.start);
-        return l + 2;
-    }
+                                                            c.nat, s.x, s.y, s.z, err, gate, weights ? 0 : 1);
+    if (n == 0 || !weights) return l + 1;
     k_gather<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, s.q,
                                               make_binp(g), a.aw, err, a.key, c.start);
     return l + 3;
