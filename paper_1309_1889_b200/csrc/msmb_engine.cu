@@ -273,6 +273,9 @@ static std::unique_ptr<Workspace> make_workspace(msmb_field* f, int64_t n, const
     c.bhi = walloc<float4>(*W, size_t(W->maxclu));
     c.nclu = walloc<int>(*W, 1);
     c.pcnt = walloc<int>(*W, size_t(W->maxclu));
+    c.dcnt = walloc<int>(*W, size_t(W->maxclu));
+    c.dlist = walloc<int>(*W, size_t(W->maxclu) * size_t(std::max(g.dense_cap, 32)));
+    ck(cudaMemset(c.dcnt, 0, sizeof(int) * size_t(W->maxclu)), "memset");
     c.scan_tmp = walloc<int>(*W, size_t((std::max(g.ncells, g.ncols) + 1 + 4095) / 4096 + 8));
     c.colstart = walloc<int>(*W, size_t(g.ncols + 1));
     c.flag = walloc<int>(*W, 10);

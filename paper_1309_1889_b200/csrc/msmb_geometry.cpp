@@ -309,6 +309,14 @@ static void set_pair_layout(Geometry& g, const msmb_msm_config& c, const double 
         double cap = ncand + 2.0 * ncol_range + 32.0;
         cap = std::min(cap, 1.0e6);
         g.pair_cap = std::max(64, int(cap));
+        // dense j atoms of an i-cluster lie within the list cut of most of its atoms: at most
+        // about a sphere of that radius (k_pairmask leaves the excess to the per-lane masks)
+        g.dense_t = 28;
+        if (const char* e = std::getenv("MSMB_DENSE_T")) g.dense_t = std::max(0, std::min(33, std::atoi(e)));
+        if (g.dense_t > 32) g.dense_t = 0;
+        const double sphere = 4.18879 * lc * lc * lc * rho;
+        g.dense_cap = int(std::min(4096.0, std::max(64.0, 1.4 * sphere + 64.0)));
+        g.dense_cap = (g.dense_cap + 31) & ~31;
     }
 }
 

@@ -137,6 +137,9 @@ struct Geometry {
                                          // screen in k_pairs pads its own rounding bound
     double skin = 0;                     // pair-list skin (A): rebuilt once an atom moved > skin/2
     int pair_cap = 0;                    // initial pair-list capacity per cluster
+    int dense_t = 0;                     // dense threshold: a j atom within the list cut of >= dense_t of an
+                                         // i-cluster's 32 atoms is summed by the whole warp in lockstep (0 = off)
+    int dense_cap = 0;                   // dense j atoms kept per i-cluster (multiple of 32)
     int64_t lattice_taps_clipped = 0;    // sum over levels 0..l-2 of clipped nonzero taps
     int64_t top_taps = 0;                // M_top^2
 };

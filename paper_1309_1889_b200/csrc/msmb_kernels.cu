@@ -805,8 +805,12 @@ constexpr int kSlots = 33;            // one ring slot: dummy + 32 atoms
 #endif
 constexpr int kRing = MSMB_PAIR_RING;
 static_assert((kRing & (kRing - 1)) == 0, "ring size must be a power of two");
+static_assert(kRing >= 2, "the dense phase stages its batches in ring slots 0 and 1");
 #ifndef MSMB_PAIR_UNROLL
 #define MSMB_PAIR_UNROLL 4
+#endif
+#ifndef MSMB_DENSE_UNROLL
+#define MSMB_DENSE_UNROLL 4 // divides 32
 #endif
 
 // Pair masks, built once per pair-list rebuild (flag[0]): for every list entry of
@@ -822,7 +826,7 @@ __global__ void __launch_bounds__(kMaskWarps * 32)
     k_pairmask(const int2* __restrict__ clu, int* plist, int* pcnt, unsigned* __restrict__ pmask, int cap,
                const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
                float cut2f, const int* __restrict__ col_off, int col_a, int col_b, const int* __restrict__ flag,
-               ErrRec* err) {
+               ErrRec* err, int* __restrict__ dlist, int* __restrict__ dcnt, int dcap, int dense_t) {
     __shared__ __align__(16) float s_sc[kMaskWarps][4][32];
     __shared__ __align__(16) int s_sh[kMaskWarps][32];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -850,7 +854,8 @@ __global__ void __launch_bounds__(kMaskWarps * 32)
     const int nj = pcnt[ic];
     int* pl = plist + size_t(ic) * cap;
     unsigned* pm = pmask + size_t(ic) * cap * 32;
-    int out = 0;
+    int* dl = dlist + size_t(ic) * dcap;
+    int out = 0, nd = 0;
     // list entries and their clusters in two register windows of 32 (lane l holds
     // entry 32w + l), refilled one window ahead; the j atoms of entry jj + 1 are
     // loaded while entry jj is screened (the dependent loads stay off the chain)
@@ -940,13 +945,39 @@ __global__ void __launch_bounds__(kMaskWarps * 32)
         }
         if (!vi || jc == ic) mask = 0; // the own cluster is summed densely by k_pairs_mw
         mask &= ~(0xffffffffu >> cj.y); // bits 31 .. 32 - cj.y: the cluster's atoms only
+        if (dense_t > 0) {
+            // Dense atoms: within the list cut of >= dense_t of the 32 i atoms.  A 32 x 32 bit
+            // transpose over the warp gives lane l the column of atom l (bit 31 - l of every
+            // lane's mask); those atoms go to the i-cluster's dense list (k_pairs_mw sums them
+            // with the whole warp in lockstep, the j row broadcast) and leave the masks.
+            unsigned tr = mask, tm = 0x0000ffffu;
+#pragma unroll
+            for (int j = 16; j; j >>= 1) {
+                const unsigned o = __shfl_xor_sync(FULLMASK, tr, j);
+                if ((lane & j) == 0)
+                    tr ^= (tr ^ (o >> j)) & tm;
+                else
+                    tr ^= ((o ^ (tr >> j)) & tm) << j;
+                tm ^= tm << (j >> 1);
+            }
+            const bool dense = __popc(tr) >= dense_t;
+            const unsigned dn = __ballot_sync(FULLMASK, dense);
+            if (dn != 0u && nd + __popc(dn) <= dcap) {
+                if (dense) dl[nd + __popc(dn & ((1u << lane) - 1u))] = cj.x + lane;
+                nd += __popc(dn);
+                mask &= ~__brev(dn);
+            }
+        }
         if (__any_sync(FULLMASK, mask != 0)) {
             pm[size_t(out) * 32 + lane] = mask;
             if (lane == 0) pl[out] = cj.x;
             ++out;
         }
     }
-    if (lane == 0) pcnt[ic] = out;
+    if (lane == 0) {
+        pcnt[ic] = out;
+        dcnt[ic] = nd;
+    }
 }
 
 // One warp per i-cluster (lane = i atom) walks the i-cluster's mask list.  The warp
@@ -988,7 +1019,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
                const double* __restrict__ ys, const double* __restrict__ zs, const double* __restrict__ qs,
                PairP p, double a2, double* phis, double* fsx, double* fsy, double* fsz,
                const int* __restrict__ col_off, int col_a, int col_b, int64_t n, ErrRec* err,
-               int split_arg, double* __restrict__ part) {
+               int split_arg, double* __restrict__ part, const int* __restrict__ dlist,
+               const int* __restrict__ dcnt, int dcap) {
     const int split = SPLIT ? split_arg : 1; // compile-time 1 on the large-system path
     __shared__ unsigned s_mask[kPairWarps][kRing][32];
     __shared__ double2 s_v[kPairWarps][2][kRing * kSlots]; // (x, y), (z, q) rows
@@ -1003,8 +1035,6 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     const bool vi = lane < c.y;
     const int si = c.x + (vi ? lane : 0);
     const double xi = xs[si], yi = ys[si], zi = zs[si], qi = qs[si];
-    for (int s = lane; s < 2 * kRing; s += 32) // dummies (q = 0, far away) at each slot's position 0
-        s_v[w][s & 1][(s >> 1) * kSlots] = (s & 1) ? make_double2(1e4, 0.0) : make_double2(1e4, 1e4);
     double ph = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
     unsigned ncand = 0, npair = 0;
     const int nj_all = pcnt[ic];
@@ -1079,6 +1109,71 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
         fy = fma(dy, wgt, fy);
         fz = fma(dz, wgt, fz);
     };
+    for (int s = lane; s < 2 * kRing; s += 32) // dummies (q = 0, far away) at each ring slot's position 0
+        s_v[w][s & 1][(s >> 1) * kSlots] = (s & 1) ? make_double2(1e4, 0.0) : make_double2(1e4, 1e4);
+    __syncwarp();
+    // Dense phase: the i-cluster's dense j atoms (k_pairmask), 32 per batch: lane l loads
+    // atom 32 b + l of the list (indices two batches and atoms one batch ahead of their use)
+    // and stages it into ring slot b & 1; then the whole warp steps through the batch, every
+    // lane reading the same row (a broadcast, no mask bookkeeping: 30 instructions per step,
+    // 24 of them FP64) and applying the exact cutoff.  Lanes past the list stage the dummy.
+    // Measured alternatives (C2-S, pairs ms; 0.622 without the dense phase): this, threshold
+    // 28 of 32 lanes, 0.578; threshold 16, 0.627; dense lists per octet of lanes (threshold 4
+    // of 8, one list per octet staged by cp.async) 0.725; one list tagged with the octets, each
+    // octet stepping through its bits of the batch, 0.82 (a batch takes its fullest octet's
+    // steps); alternating the phase order between neighbouring warps: slower.
+    {
+        const int nd_all = dcnt[ic];
+        const int db = SPLIT ? int(int64_t(nd_all) * sp / split) : 0;
+        const int nd = (SPLIT ? int(int64_t(nd_all) * (sp + 1) / split) : nd_all) - db;
+        const int* dl = dlist + size_t(ic) * dcap + db;
+        if (COUNT) ncand += vi ? unsigned(nd) : 0u;
+        const int nb = (nd + 31) >> 5;
+        int sj1 = lane < nd ? dl[lane] : -1;           // batch 0
+        int sj2 = 32 + lane < nd ? dl[32 + lane] : -1; // batch b + 1
+        double xn = 1e4, yn = 1e4, zn = 1e4, qn = 0.0;
+        auto dload = [&](int sj) {
+            xn = yn = zn = 1e4;
+            qn = 0.0;
+            if (sj >= 0) {
+                xn = xs[sj];
+                yn = ys[sj];
+                zn = zs[sj];
+                qn = qs[sj];
+            }
+        };
+        if (nb > 0) dload(sj1);
+        for (int b = 0; b < nb; ++b) {
+            double2* buf = &s_v[w][0][(b & 1) * kSlots + 1];
+            buf[lane] = make_double2(xn, yn);
+            buf[kRing * kSlots + lane] = make_double2(zn, qn);
+            __syncwarp();
+            if (b + 1 < nb) dload(sj2);
+            sj2 = (b + 2) * 32 + lane < nd ? dl[(b + 2) * 32 + lane] : -1;
+            const int tcnt = min(32, nd - 32 * b);
+#pragma unroll 1
+            for (int t0 = 0; t0 < tcnt; t0 += MSMB_DENSE_UNROLL) {
+#pragma unroll
+                for (int u = 0; u < MSMB_DENSE_UNROLL; ++u) {
+                    const double2 xy = buf[t0 + u], zq = buf[kRing * kSlots + t0 + u];
+                    const double dx = xi - xy.x, dy = yi - xy.y, dz = zi - zq.x;
+                    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+                    const double rinv = rsqrt_pos(r2);
+                    double g, sd;
+                    pair_fn<K>(p, r2, rinv, g, sd);
+                    const bool in = r2 < a2;
+                    if (COUNT) npair += (in && vi) ? 1u : 0u;
+                    const double qj = in ? zq.y : 0.0;
+                    ph = fma(qj, g, ph);
+                    const double wgt = qj * sd;
+                    fx = fma(dx, wgt, fx);
+                    fy = fma(dy, wgt, fy);
+                    fz = fma(dz, wgt, fz);
+                }
+            }
+        }
+        __syncwarp();
+    }
     if (nj > 0) fetch(0);
     ncand += (vi && sp == 0) ? unsigned(c.y - 1) : 0u;
     // the own cluster (dropped from the mask list): all atom pairs, j broadcast by shuffles
@@ -1218,7 +1313,7 @@ int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevStat
     const double lm = g.cfg.cutoff_a + g.skin; // mask cut: a + skin (+ the fp32 pad in k_pairmask)
     k_pairmask<<<int((maxclu + kMaskWarps - 1) / kMaskWarps), kMaskWarps * 32, 0, st>>>(
         c.clu, c.plist, c.pcnt, c.pmask, cap, a.xc, a.yc, a.zc, float_ru(lm * lm * (1.0 + 1e-6)), c.col_off,
-        P.cx0 * g.ncy, P.cx1 * g.ncy, c.flag, err);
+        P.cx0 * g.ncy, P.cx1 * g.ncy, c.flag, err, c.dlist, c.dcnt, std::max(g.dense_cap, 32), g.dense_t);
     return 7 + (disp ? 1 : 0);
 }
 
@@ -1286,7 +1381,8 @@ int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& 
         auto kern = split > 1 ? (count ? pick(T{}, T{}) : pick(T{}, F{})) : (count ? pick(F{}, T{}) : pick(F{}, F{}));
         kern<<<int((maxclu * split + kPairWarps - 1) / kPairWarps), kPairWarps * 32, 0, st>>>(
             c.clu, c.plist, c.pcnt, c.pmask, cap, a.xc, a.yc, a.zc, a.qc, p, A * A, a.phis, a.fsx, a.fsy, a.fsz,
-            c.col_off, P.cx0 * g.ncy, P.cx1 * g.ncy, n, err, split, a.pair_part);
+            c.col_off, P.cx0 * g.ncy, P.cx1 * g.ncy, n, err, split, a.pair_part, c.dlist, c.dcnt,
+            std::max(g.dense_cap, 32));
         l = 1;
         if (split > 1) {
             k_pairs_join<<<int((n + 255) / 256), 256, 0, st>>>(c.colstart, P.cx0 * g.ncy, P.cx1 * g.ncy, split, n,

@@ -39,6 +39,8 @@ struct DevCells {
     int* plist;         // [max_clusters * cap]
     int* pcnt;          // [max_clusters]
     unsigned* pmask;    // [max_clusters * cap * 32] per-lane j-atom masks (k_pairmask)
+    int* dlist;         // [max_clusters * dense_cap] dense j atoms (sorted slots) of each i-cluster
+    int* dcnt;          // [max_clusters]
     int* scan_tmp;      // scratch for the multi-block scan
     int* colstart;      // [ncols+1] first cluster slot of each pair column (frozen at rebuild)
     int* flag;          // [10] [0] rebuild the pair list this evaluation, [1] clustered atoms,
