@@ -527,8 +527,8 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, 
     }
     if (g_exp_stamps) launch_stamp(st, 0);
     run("bin", [&] { return launch_bin(st, g, s, W.a, W.c, W.err); });
-    run("sort", [&] { return launch_sort(st, g, s, W.a, W.c, W.err); });
     if (g.kind != MSMB_FIELD_MSM) { // pair-only field: no grid hierarchy
+        run("sort", [&] { return launch_sort(st, g, s, W.a, W.c, W.err); });
         run("clusters", [&] { return launch_clusters(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, rebuild ? 1 : 0); });
         run("pairs", [&] { return launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, !t_capturing); });
         DevOut o = W.o;
@@ -538,13 +538,32 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, 
         run("finalize", [&] { return launch_finalize(st, s, W.err, 1); });
         return total;
     }
-    cudaStream_t la = fork ? f->side_a : st; // anterpolation, then the rest of the chain on lr
-    // the cluster kernels (7 short launches on a skin step) before the fork: beside the
-    // anterpolation's CTAs they took ~50 us instead of ~27 (C2-S 0.836 -> 0.831 ms/step)
-    run("clusters", [&] { return launch_clusters(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, rebuild ? 1 : 0); });
+    // Forked evaluation.  Main stream: binning, the rebuild decision and the frozen-order
+    // gather (they need the binning's coverage list, not the cell sort), then the pair kernel's
+    // skin instance (it exits at once on a rebuild evaluation).  Stream la: the cell sort, then
+    // the anterpolation; stream lr: the rest of the long-range chain.  Stream sr: after the
+    // sort and the decision, the list rebuild and the pair kernel's rebuild instance (every
+    // kernel exits at once on a skin evaluation).  So on a skin step the pair sum starts ~35 us
+    // earlier (it no longer waits for the sort and the four exiting rebuild launches), and on
+    // a rebuild step the rebuild runs beside the anterpolation.  Each output is written by one
+    // kernel in a fixed order: results do not depend on the interleaving.
+    cudaStream_t la = fork ? f->side_a : st; // cell sort + anterpolation, then the rest of the chain on lr
+    cudaStream_t sr = fork ? f->side_r : st; // list rebuild + the pair kernel's rebuild instance
     if (fork) {
         ck(cudaEventRecord(f->fork_ev, st), "fork");
         ck(cudaStreamWaitEvent(la, f->fork_ev, 0), "fork");
+    }
+    run("sort", [&] { return launch_sort(la, g, s, W.a, W.c, W.err); });
+    if (fork) {
+        ck(cudaEventRecord(f->sort_ev, la), "fork");
+        run("clusters", [&] {
+            return launch_clusters(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, rebuild ? 1 : 0, 1, 1);
+        });
+        ck(cudaEventRecord(f->disp_ev, st), "fork");
+        ck(cudaStreamWaitEvent(sr, f->disp_ev, 0), "fork");
+        ck(cudaStreamWaitEvent(sr, f->sort_ev, 0), "fork");
+    } else {
+        run("clusters", [&] { return launch_clusters(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, rebuild ? 1 : 0); });
     }
     if (g_exp_stamps) { launch_stamp(st, 1); launch_stamp(la, 2); }
     if (g_exp_chain != 0 && g_exp_chain != 2)
@@ -571,11 +590,23 @@ static int enqueue_eval(msmb_field* f, Workspace& W, DevState& s, bool outputs, 
     if (g_exp_stamps) launch_stamp(lr, 3);
     if (fork) ck(cudaEventRecord(f->join_ev, lr), "join");
     if (g_exp_stamps) launch_stamp(st, 4);
+    // (Measured, C2-S ms/step: pair kernel right away 0.751; after the cell sort 0.748; after
+    // the anterpolation, which then runs alone in 55 us instead of ~245, 0.775.)
     run("pairs", [&] {
-        return launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, !t_capturing);
+        return launch_pairs(st, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, !t_capturing, fork ? 1 : 0);
     });
     if (g_exp_stamps) launch_stamp(st, 5);
-    if (fork) ck(cudaStreamWaitEvent(st, f->join_ev, 0), "join");
+    if (fork) {
+        run("clusters", [&] {
+            return launch_clusters(sr, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, rebuild ? 1 : 0, 1, 2);
+        });
+        run("pairs", [&] {
+            return launch_pairs(sr, g, s.n, s, W.a, W.c, W.err, W.cap, W.whole, !t_capturing, 2);
+        });
+        ck(cudaEventRecord(f->reb_ev, sr), "join");
+        ck(cudaStreamWaitEvent(st, f->reb_ev, 0), "join");
+        ck(cudaStreamWaitEvent(st, f->join_ev, 0), "join");
+    }
     DevOut o = W.o;
     if (!outputs) o.phi = o.phis = o.phil = o.e = nullptr;
     run("interp", [&] { return launch_interp(st, g, s.n, W.a, W.c, W.L, o, W.err, outputs ? 1 : 0, W.whole); });
@@ -1005,12 +1036,20 @@ static int field_new(int device, msmb_field** out) {
     if (cudaStreamCreateWithPriority(&f->stream, cudaStreamNonBlocking, main_prio) != cudaSuccess ||
         cudaStreamCreateWithPriority(&f->side, cudaStreamNonBlocking, side_prio) != cudaSuccess ||
         cudaStreamCreateWithPriority(&f->side_a, cudaStreamNonBlocking, anterp_prio) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&f->side_r, cudaStreamNonBlocking, main_prio) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f->sort_ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f->disp_ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f->reb_ev, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&f->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&f->join_ev, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&f->mid_ev, cudaEventDisableTiming) != cudaSuccess) {
         if (f->stream) cudaStreamDestroy(f->stream);
         if (f->side) cudaStreamDestroy(f->side);
         if (f->side_a) cudaStreamDestroy(f->side_a);
+        if (f->side_r) cudaStreamDestroy(f->side_r);
+        if (f->sort_ev) cudaEventDestroy(f->sort_ev);
+        if (f->disp_ev) cudaEventDestroy(f->disp_ev);
+        if (f->reb_ev) cudaEventDestroy(f->reb_ev);
         if (f->fork_ev) cudaEventDestroy(f->fork_ev);
         if (f->join_ev) cudaEventDestroy(f->join_ev);
         if (f->mid_ev) cudaEventDestroy(f->mid_ev);
@@ -1030,6 +1069,10 @@ static void field_free(msmb_field* f) {
     cudaStreamDestroy(f->stream);
     cudaStreamDestroy(f->side);
     cudaStreamDestroy(f->side_a);
+    cudaStreamDestroy(f->side_r);
+    cudaEventDestroy(f->sort_ev);
+    cudaEventDestroy(f->disp_ev);
+    cudaEventDestroy(f->reb_ev);
     cudaEventDestroy(f->fork_ev);
     cudaEventDestroy(f->join_ev);
     cudaEventDestroy(f->mid_ev);

@@ -141,7 +141,9 @@ struct msmb_field {
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;             // long-range chain, forked from `stream`
     cudaStream_t side_a = nullptr;           // the chain's anterpolation (at the main stream's priority)
+    cudaStream_t side_r = nullptr;           // pair-list rebuild + the pair kernel's rebuild instance
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr, mid_ev = nullptr;
+    cudaEvent_t sort_ev = nullptr, disp_ev = nullptr, reb_ev = nullptr;
     std::recursive_mutex mu;
     std::unique_ptr<msmb::Workspace> ws;
     msmb::Error last;

@@ -455,7 +455,11 @@ __global__ void k_cl_gather(int64_t n, const int* __restrict__ start_total, cons
                             const double* __restrict__ x, const double* __restrict__ y,
                             const double* __restrict__ z, const double* __restrict__ q, int* cl_perm, int* cl_inv,
                             double* ref, int* flag, int key, double* xc, double* yc, double* zc, double* qc,
-                            int gather_blocks, const int* __restrict__ outlist, ErrRec* err) {
+                            int gather_blocks, const int* __restrict__ outlist, ErrRec* err, int mode) {
+    // mode 1: the skin evaluations' gather only (exits at a rebuild), mode 2: the rebuild's only
+    if (mode && (flag[0] != 0) != (mode == 2)) {
+        if (mode == 2 || int(blockIdx.x) < gather_blocks) return;
+    }
     if (int(blockIdx.x) >= gather_blocks) {
         err_brute_blocks(n, x, y, z, outlist, err, blockIdx.x - gather_blocks, gridDim.x - gather_blocks);
         return;
@@ -1020,7 +1024,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
                PairP p, double a2, double* phis, double* fsx, double* fsy, double* fsz,
                const int* __restrict__ col_off, int col_a, int col_b, int64_t n, ErrRec* err,
                int split_arg, double* __restrict__ part, const int* __restrict__ dlist,
-               const int* __restrict__ dcnt, int dcap) {
+               const int* __restrict__ dcnt, int dcap, const int* __restrict__ gflag, int gmode) {
+    // gmode 1: runs on skin evaluations only (flag[0] == 0), 2: on rebuild evaluations only
+    if (gmode && (gflag[0] != 0) != (gmode == 2)) return;
     const int split = SPLIT ? split_arg : 1; // compile-time 1 on the large-system path
     __shared__ unsigned s_mask[kPairWarps][kRing][32];
     __shared__ double2 s_v[kPairWarps][2][kRing * kSlots]; // (x, y), (z, q) rows
@@ -1121,7 +1127,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
     // 28 of 32 lanes, 0.578; threshold 16, 0.627; dense lists per octet of lanes (threshold 4
     // of 8, one list per octet staged by cp.async) 0.725; one list tagged with the octets, each
     // octet stepping through its bits of the batch, 0.82 (a batch takes its fullest octet's
-    // steps); alternating the phase order between neighbouring warps: slower.
+    // steps); alternating the phase order between neighbouring warps: slower; persistent
+    // warps claiming i-clusters from a work counter (148 x 16..20 one-warp CTAs): 0.60-0.63
+    // alone, and the long-range chain starves beside CTAs that never retire.
     {
         const int nd_all = dcnt[ic];
         const int db = SPLIT ? int(int64_t(nd_all) * sp / split) : 0;
@@ -1269,18 +1277,30 @@ __device__ void err_brute_blocks(int64_t n, const double* __restrict__ x, const 
 // per evaluation the C2-S step went 0.845 -> 0.862 ms; leaving the rebuild kernels
 // out of the step graphs entirely (timing only) gave 0.809 ms -- the fusions here
 // (13 -> 7 launches) take part of that without the IF nodes.
+// phase 0: everything on one stream.  The engine's forked evaluation splits it: phase 1 = the
+// rebuild decision and the skin evaluations' gather (needs the binning's out-of-coverage
+// list, not the cell sort), phase 2 = the rebuild (after the cell sort; every kernel exits
+// unless flag[0]), so that on a skin step the pair kernel does not wait for the sort.
 int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
-                    DevCells& c, ErrRec* err, int cap, const Part& P, int force_rebuild, int disp) {
+                    DevCells& c, ErrRec* err, int cap, const Part& P, int force_rebuild, int disp, int phase) {
     const int cells_per_col = int(g.lv[0].dims[2]) * g.cw * g.cw;
     const int64_t nc = g.ncols;
     // rebuild decision, frozen cluster order, current positions in it
     const int key = P.cx0 * 65536 + P.cx1;
-    k_flag_reset<<<1, 1, 0, st>>>(c.flag, force_rebuild || !(g.skin > 0.0) ? 1 : 0, key);
-    const double hs = 0.5 * g.skin;
-    if (disp) k_disp<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, s.x, s.y, s.z, a.ref, hs * hs, c.flag);
     const int gb = int((std::max<int64_t>(n, 1) + 255) / 256);
-    k_cl_gather<<<gb + 592, 256, 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, s.q, a.cl_perm, a.cl_inv,
-                                          a.ref, c.flag, key, a.xc, a.yc, a.zc, a.qc, gb, a.outlist, err);
+    if (phase != 2) {
+        k_flag_reset<<<1, 1, 0, st>>>(c.flag, force_rebuild || !(g.skin > 0.0) ? 1 : 0, key);
+        const double hs = 0.5 * g.skin;
+        if (disp)
+            k_disp<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, s.x, s.y, s.z, a.ref, hs * hs, c.flag);
+        k_cl_gather<<<gb + 592, 256, 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, s.q, a.cl_perm,
+                                              a.cl_inv, a.ref, c.flag, key, a.xc, a.yc, a.zc, a.qc, gb, a.outlist,
+                                              err, phase);
+        if (phase == 1) return 2 + (disp ? 1 : 0);
+    } else {
+        k_cl_gather<<<gb, 256, 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, s.q, a.cl_perm, a.cl_inv,
+                                        a.ref, c.flag, key, a.xc, a.yc, a.zc, a.qc, gb, a.outlist, err, 2);
+    }
     // cluster pair list (rebuild evaluations only)
     k_colscan<<<1, 1024, 0, st>>>(nc, cells_per_col, c.start, c.col_cnt, c.col_off, c.clu, c.nclu, c.colstart,
                                   c.flag, err);
@@ -1314,13 +1334,15 @@ int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevStat
     k_pairmask<<<int((maxclu + kMaskWarps - 1) / kMaskWarps), kMaskWarps * 32, 0, st>>>(
         c.clu, c.plist, c.pcnt, c.pmask, cap, a.xc, a.yc, a.zc, float_ru(lm * lm * (1.0 + 1e-6)), c.col_off,
         P.cx0 * g.ncy, P.cx1 * g.ncy, c.flag, err, c.dlist, c.dcnt, std::max(g.dense_cap, 32), g.dense_t);
-    return 7 + (disp ? 1 : 0);
+    return phase == 2 ? 5 : 7 + (disp ? 1 : 0);
 }
 
 // sums of the split pair walks, in part order, then the per-atom force factor
 __global__ void k_pairs_join(const int* __restrict__ colstart, int col_a, int col_b, int split, int64_t n,
                              const double* __restrict__ part, const double* __restrict__ qs, double kc,
-                             double* phis, double* fsx, double* fsy, double* fsz, const ErrRec* err) {
+                             double* phis, double* fsx, double* fsy, double* fsz, const ErrRec* err,
+                             const int* __restrict__ gflag, int gmode) {
+    if (gmode && (gflag[0] != 0) != (gmode == 2)) return;
     const int s = colstart[col_a] + blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= colstart[col_b] || failed(err)) return;
     double v[4] = {0.0, 0.0, 0.0, 0.0};
@@ -1342,7 +1364,7 @@ int pair_split(int64_t maxclu) {
 }
 
 int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
-                 DevCells& c, ErrRec* err, int cap, const Part& P, bool count) {
+                 DevCells& c, ErrRec* err, int cap, const Part& P, bool count, int gmode) {
     const double A = g.cfg.cutoff_a;
     PairP p;
     // gamma(rho)/a = 15/(8a) - 5 r^2/(4a^3) + 3 r^4/(8a^5)          (msm_kernels.hpp:14-20,30-35)
@@ -1382,12 +1404,12 @@ int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& 
         kern<<<int((maxclu * split + kPairWarps - 1) / kPairWarps), kPairWarps * 32, 0, st>>>(
             c.clu, c.plist, c.pcnt, c.pmask, cap, a.xc, a.yc, a.zc, a.qc, p, A * A, a.phis, a.fsx, a.fsy, a.fsz,
             c.col_off, P.cx0 * g.ncy, P.cx1 * g.ncy, n, err, split, a.pair_part, c.dlist, c.dcnt,
-            std::max(g.dense_cap, 32));
+            std::max(g.dense_cap, 32), c.flag, gmode);
         l = 1;
         if (split > 1) {
             k_pairs_join<<<int((n + 255) / 256), 256, 0, st>>>(c.colstart, P.cx0 * g.ncy, P.cx1 * g.ncy, split, n,
                                                                a.pair_part, a.qc, p.kc, a.phis, a.fsx, a.fsy, a.fsz,
-                                                               err);
+                                                               err, c.flag, gmode);
             ++l;
         }
     }

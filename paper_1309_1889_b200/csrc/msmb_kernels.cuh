@@ -138,10 +138,11 @@ int launch_sort(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms&
                 ErrRec* err, const int* list = nullptr, int64_t nlist = 0);
 // disp = 0: no skin/2 displacement test (the caller decided the rebuild: force_rebuild)
 int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
-                    DevCells& c, ErrRec* err, int cap, const Part& P, int force_rebuild, int disp = 1);
+                    DevCells& c, ErrRec* err, int cap, const Part& P, int force_rebuild, int disp = 1,
+                    int phase = 0);
 // count: accumulate the pair / candidate statistics (eager evaluations; graphs skip it)
 int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& s, DevAtoms& a,
-                 DevCells& c, ErrRec* err, int cap, const Part& P, bool count = true);
+                 DevCells& c, ErrRec* err, int cap, const Part& P, bool count = true, int gmode = 0);
 int launch_anterp(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& a, DevCells& c, DevLevels& L,
                   ErrRec* err, const Part& P);
 size_t anterp_tile_part_doubles(const Geometry& g);
