@@ -570,9 +570,10 @@ def main():
             "roofline": {"bound": "fp64", "kernel": "k_pairs_mw (short-range pair sum, SURVEY S2)",
                          "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
                          "slot_frac": slot_frac, "traffic": traffic,
-                         "traffic_note": "DRAM bytes per launch from profiles/r01g_k_pairs_mw_full.md: mostly the "
-                                         "per-lane pair masks (k_pairmask, 128 B per list entry, read once per "
-                                         "evaluation; L2-flushed between timed steps), not atom data",
+                         "traffic_note": "DRAM bytes per launch from the ncu capture named in profiles/ncu_traffic.json "
+                                         "(r02c_k_pairs_mw_full.md): mostly the per-lane pair masks (k_pairmask, 128 B "
+                                         "per list entry) and the dense lists (4 B per dense atom), read once per "
+                                         "evaluation (L2-flushed between timed steps), not atom data",
                          "work_per_launch": f"{pairs_u} in-cutoff unordered pairs x {roofline.PAIR_FLOPS} flops "
                                             f"({roofline.PAIR_SLOTS} FP64 issue slots)",
                          "avg_launch_ms": pair_ms,
