@@ -120,6 +120,7 @@ __device__ __forceinline__ int find_level(const FftJobs& J, int blk) {
 //   mode 1: E, O (k <= M0/2, conjugate-extended) -> C = E + i O -> IFFT -> u_e = Re, u_o = Im
 __global__ void __launch_bounds__(256) k_fft_x(FftJobs J, int mode, const ErrRec* err) {
     extern __shared__ double2 sm[];
+    pdl_enter();
     if (err && __ldcg(&err->kind)) return;
     const int k = find_level(J, blockIdx.x);
     const FftLevel& lv = J.lv[k];
@@ -197,6 +198,7 @@ __global__ void __launch_bounds__(256) k_fft_x(FftJobs J, int mode, const ErrRec
 // 1: inverse (output y < d1); 2: forward over every line.
 __global__ void __launch_bounds__(256) k_fft_y(FftJobs J, int mode, const ErrRec* err) {
     extern __shared__ double2 sm[];
+    pdl_enter();
     if (err && __ldcg(&err->kind)) return;
     const int k = find_level(J, blockIdx.x);
     const FftLevel& lv = J.lv[k];
@@ -227,6 +229,7 @@ __global__ void __launch_bounds__(256) k_fft_y(FftJobs J, int mode, const ErrRec
 // inverse, output z < d2; 2: forward over every line, Khat = Re / (M0 M1 M2).
 __global__ void __launch_bounds__(256) k_fft_z(FftJobs J, int mode, const ErrRec* err) {
     extern __shared__ double2 sm[];
+    pdl_enter();
     if (err && __ldcg(&err->kind)) return;
     const int k = find_level(J, blockIdx.x);
     const FftLevel& lv = J.lv[k];
@@ -383,16 +386,12 @@ int launch_fft_spectrum(cudaStream_t st, FftJobs J, const FftKernel* K) {
 int launch_lattice_fft(cudaStream_t st, FftJobs J, const ErrRec* err) {
     if (J.n == 0) return 0;
     const size_t sm = fft_smem(J);
-    int nb = blocks_x(J, false);
-    k_fft_x<<<nb, fft_threads(J), sm, st>>>(J, 0, err);
-    nb = blocks_y(J, false);
-    k_fft_y<<<nb, fft_threads(J), sm, st>>>(J, 0, err);
-    nb = blocks_z(J, false);
-    k_fft_z<<<nb, fft_threads(J), sm, st>>>(J, 0, err);
-    nb = blocks_y(J, false);
-    k_fft_y<<<nb, fft_threads(J), sm, st>>>(J, 1, err);
-    nb = blocks_x(J, false);
-    k_fft_x<<<nb, fft_threads(J), sm, st>>>(J, 1, err);
+    const dim3 tb(fft_threads(J));
+    pdl_launch(k_fft_x, dim3(blocks_x(J, false)), tb, sm, st, J, 0, err);
+    pdl_launch(k_fft_y, dim3(blocks_y(J, false)), tb, sm, st, J, 0, err);
+    pdl_launch(k_fft_z, dim3(blocks_z(J, false)), tb, sm, st, J, 0, err);
+    pdl_launch(k_fft_y, dim3(blocks_y(J, false)), tb, sm, st, J, 1, err);
+    pdl_launch(k_fft_x, dim3(blocks_x(J, false)), tb, sm, st, J, 1, err);
     return 5;
 }
 

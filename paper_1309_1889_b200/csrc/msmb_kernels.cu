@@ -137,6 +137,7 @@ __device__ __forceinline__ int scell_of(const BinP& p, int cx, int cy, int cz) {
 __global__ void k_bin(int n, const double* __restrict__ x, const double* __restrict__ y,
                       const double* __restrict__ z, BinP p, int* key, int* rank, int* count,
                       int* outlist, ErrRec* err, const int* __restrict__ list, int* moved) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); // k_flag_reset may be admitted (pdl_enter)
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n || failed(err)) return;
     const int i = list ? list[t] : t;
@@ -429,12 +430,14 @@ int launch_sort(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms&
 // (flag[3] == 0: never built, capacity grown, an evaluation failed), or the list was
 // built for another ownership range (flag[4]: the part's pair-column key)
 __global__ void k_flag_reset(int* flag, int force, int key) {
+    pdl_enter(1);
     flag[0] = (force || flag[3] == 0 || flag[4] != key) ? 1 : 0;
 }
 
 __global__ void k_disp(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
                        const double* __restrict__ z, const double* __restrict__ ref, double half_skin2,
                        int* flag) {
+    pdl_enter(1);
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double dx = x[i] - ref[i], dy = y[i] - ref[n + i], dz = z[i] - ref[2 * n + i];
@@ -456,6 +459,7 @@ __global__ void k_cl_gather(int64_t n, const int* __restrict__ start_total, cons
                             const double* __restrict__ z, const double* __restrict__ q, int* cl_perm, int* cl_inv,
                             double* ref, int* flag, int key, double* xc, double* yc, double* zc, double* qc,
                             int gather_blocks, const int* __restrict__ outlist, ErrRec* err, int mode) {
+    pdl_enter(1);
     // mode 1: the skin evaluations' gather only (exits at a rebuild), mode 2: the rebuild's only
     if (mode && (flag[0] != 0) != (mode == 2)) {
         if (mode == 2 || int(blockIdx.x) < gather_blocks) return;
@@ -949,7 +953,8 @@ __global__ void __launch_bounds__(kMaskWarps * 32)
         }
         if (!vi || jc == ic) mask = 0; // the own cluster is summed densely by k_pairs_mw
         mask &= ~(0xffffffffu >> cj.y); // bits 31 .. 32 - cj.y: the cluster's atoms only
-        if (dense_t > 0) {
+        // (an atom can only be dense if at least dense_t lanes have a bit at all)
+        if (dense_t > 0 && __popc(__ballot_sync(FULLMASK, mask != 0u)) >= dense_t) {
             // Dense atoms: within the list cut of >= dense_t of the 32 i atoms.  A 32 x 32 bit
             // transpose over the warp gives lane l the column of atom l (bit 31 - l of every
             // lane's mask); those atoms go to the i-cluster's dense list (k_pairs_mw sums them
@@ -1025,6 +1030,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, MSMB_PAIR_MINB)
                const int* __restrict__ col_off, int col_a, int col_b, int64_t n, ErrRec* err,
                int split_arg, double* __restrict__ part, const int* __restrict__ dlist,
                const int* __restrict__ dcnt, int dcap, const int* __restrict__ gflag, int gmode) {
+    pdl_enter();
     // gmode 1: runs on skin evaluations only (flag[0] == 0), 2: on rebuild evaluations only
     if (gmode && (gflag[0] != 0) != (gmode == 2)) return;
     const int split = SPLIT ? split_arg : 1; // compile-time 1 on the large-system path
@@ -1289,13 +1295,14 @@ int launch_clusters(cudaStream_t st, const Geometry& g, int64_t n, const DevStat
     const int key = P.cx0 * 65536 + P.cx1;
     const int gb = int((std::max<int64_t>(n, 1) + 255) / 256);
     if (phase != 2) {
-        k_flag_reset<<<1, 1, 0, st>>>(c.flag, force_rebuild || !(g.skin > 0.0) ? 1 : 0, key);
+        // PDL (pdl_enter in the kernels): each launch is admitted while its predecessor runs
+        pdl_launch(k_flag_reset, dim3(1), dim3(1), 0, st, c.flag, force_rebuild || !(g.skin > 0.0) ? 1 : 0, key);
         const double hs = 0.5 * g.skin;
         if (disp)
-            k_disp<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, s.x, s.y, s.z, a.ref, hs * hs, c.flag);
-        k_cl_gather<<<gb + 592, 256, 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, s.q, a.cl_perm,
-                                              a.cl_inv, a.ref, c.flag, key, a.xc, a.yc, a.zc, a.qc, gb, a.outlist,
-                                              err, phase);
+            pdl_launch(k_disp, dim3(atom_blocks(n, atom_tpb(n))), dim3(atom_tpb(n)), 0, st, n, s.x, s.y, s.z, a.ref,
+                       hs * hs, c.flag);
+        pdl_launch(k_cl_gather, dim3(gb + 592), dim3(256), 0, st, n, c.start + g.ncells, a.perm, s.x, s.y, s.z, s.q,
+                   a.cl_perm, a.cl_inv, a.ref, c.flag, key, a.xc, a.yc, a.zc, a.qc, gb, a.outlist, err, phase);
         if (phase == 1) return 2 + (disp ? 1 : 0);
     } else {
         k_cl_gather<<<gb, 256, 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, s.q, a.cl_perm, a.cl_inv,
@@ -1401,10 +1408,10 @@ int launch_pairs(cudaStream_t st, const Geometry& g, int64_t n, const DevState& 
         using T = std::true_type;
         using F = std::false_type;
         auto kern = split > 1 ? (count ? pick(T{}, T{}) : pick(T{}, F{})) : (count ? pick(F{}, T{}) : pick(F{}, F{}));
-        kern<<<int((maxclu * split + kPairWarps - 1) / kPairWarps), kPairWarps * 32, 0, st>>>(
-            c.clu, c.plist, c.pcnt, c.pmask, cap, a.xc, a.yc, a.zc, a.qc, p, A * A, a.phis, a.fsx, a.fsy, a.fsz,
-            c.col_off, P.cx0 * g.ncy, P.cx1 * g.ncy, n, err, split, a.pair_part, c.dlist, c.dcnt,
-            std::max(g.dense_cap, 32), c.flag, gmode);
+        pdl_launch(kern, dim3(int((maxclu * split + kPairWarps - 1) / kPairWarps)), dim3(kPairWarps * 32), 0, st, c.clu,
+                   c.plist, c.pcnt, c.pmask, cap, a.xc, a.yc, a.zc, a.qc, p, A * A, a.phis, a.fsx, a.fsy, a.fsz,
+                   c.col_off, P.cx0 * g.ncy, P.cx1 * g.ncy, n, err, split, a.pair_part, c.dlist, c.dcnt,
+                   std::max(g.dense_cap, 32), c.flag, gmode);
         l = 1;
         if (split > 1) {
             k_pairs_join<<<int((n + 255) / 256), 256, 0, st>>>(c.colstart, P.cx0 * g.ncy, P.cx1 * g.ncy, split, n,
@@ -1899,9 +1906,11 @@ __device__ __forceinline__ double restrict_point(const XferP& p, int I, int J, i
 // xlo/xhi: the coarse x-planes to compute (a spatial-decomposition part's own)
 template <bool BITWISE, int kRTx, int kRTy, int kRTz>
 __global__ void __launch_bounds__(kRTx * kRTy * kRTz)
-    k_restrict_tile(XferP p, const double* __restrict__ fine, double* coarse, const ErrRec* err, int xlo, int xhi) {
+    k_restrict_tile(XferP p, const double* __restrict__ fine, double* coarse, const ErrRec* err, int xlo, int xhi,
+                    int early) {
     constexpr int kRFx = 2 * kRTx + 6, kRFy = 2 * kRTy + 6, kRFz = 2 * kRTz + 6;
     __shared__ double tile[kRFx * kRFy * kRFz];
+    pdl_enter(early);
     if (failed(err)) return;
     const int tz_n = (p.cd[2] + kRTz - 1) / kRTz, ty_n = (p.cd[1] + kRTy - 1) / kRTy;
     const int bz = blockIdx.x % tz_n, by = (blockIdx.x / tz_n) % ty_n, bx = blockIdx.x / (tz_n * ty_n);
@@ -2009,20 +2018,29 @@ static int restrict_blocks(const XferP& p, int nx) {
 
 int launch_restrict_all(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err) {
     int l = 0;
-    for (int k = 0; k + 1 < g.levels; ++k) l += launch_restrict_planes(st, g, k, L, err, 0, g.lv[k + 1].dims[0]);
+    for (int k = 0; k + 1 < g.levels; ++k) {
+        // the next level's restriction is a few CTAs: let them be admitted while this one runs
+        int early = 0;
+        if (k + 2 < g.levels && !MSMB_CHAIN_SMALL) {
+            const XferP pn = make_xfer(g, k + 1, L);
+            early = restrict_blocks<4, 4, 8>(pn, g.lv[k + 2].dims[0]) <= kPdlEarlyMaxBlocks;
+        }
+        l += launch_restrict_planes(st, g, k, L, err, 0, g.lv[k + 1].dims[0], early);
+    }
     return l;
 }
 
 // production restriction k -> k+1 of the coarse x-planes [xlo, xhi)
-int launch_restrict_planes(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err, int xlo, int xhi) {
+int launch_restrict_planes(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err, int xlo, int xhi,
+                           int early) {
     const XferP p = make_xfer(g, k, L);
     if (xhi <= xlo) return 0;
     if (MSMB_CHAIN_SMALL)
-        k_restrict_tile<false, 2, 4, 4><<<restrict_blocks<2, 4, 4>(p, xhi - xlo), 32, 0, st>>>(
-            p, L.charge + g.lv[k].offset, L.charge + g.lv[k + 1].offset, err, xlo, xhi);
+        pdl_launch(k_restrict_tile<false, 2, 4, 4>, dim3(restrict_blocks<2, 4, 4>(p, xhi - xlo)), dim3(32), 0, st, p,
+                   L.charge + g.lv[k].offset, L.charge + g.lv[k + 1].offset, err, xlo, xhi, early);
     else
-        k_restrict_tile<false, 4, 4, 8><<<restrict_blocks<4, 4, 8>(p, xhi - xlo), 128, 0, st>>>(
-            p, L.charge + g.lv[k].offset, L.charge + g.lv[k + 1].offset, err, xlo, xhi);
+        pdl_launch(k_restrict_tile<false, 4, 4, 8>, dim3(restrict_blocks<4, 4, 8>(p, xhi - xlo)), dim3(128), 0, st, p,
+                   L.charge + g.lv[k].offset, L.charge + g.lv[k + 1].offset, err, xlo, xhi, early);
     return 1;
 }
 
@@ -2030,7 +2048,7 @@ int launch_restrict_planes(cudaStream_t st, const Geometry& g, int k, DevLevels&
 int launch_restrict(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err) {
     const XferP p = make_xfer(g, k, L);
     k_restrict_tile<true, 4, 4, 8><<<restrict_blocks<4, 4, 8>(p, p.cd[0]), 128, 0, st>>>(
-        p, L.charge + g.lv[k].offset, L.charge + g.lv[k + 1].offset, err, 0, p.cd[0]);
+        p, L.charge + g.lv[k].offset, L.charge + g.lv[k + 1].offset, err, 0, p.cd[0], 0);
     return 1;
 }
 
@@ -2041,9 +2059,11 @@ int launch_restrict(cudaStream_t st, const Geometry& g, int k, DevLevels& L, Err
 // xlo/xhi: the fine x-planes to update (a spatial-decomposition part's own)
 template <int kPx, int kPy, int kPz>
 __global__ void __launch_bounds__(kPx * kPy * kPz)
-    k_prolong_tile(XferP p, const double* __restrict__ coarse, double* fine, const ErrRec* err, int xlo, int xhi) {
+    k_prolong_tile(XferP p, const double* __restrict__ coarse, double* fine, const ErrRec* err, int xlo, int xhi,
+                   int early) {
     constexpr int kPCx = kPx / 2 + 5, kPCy = kPy / 2 + 5, kPCz = kPz / 2 + 5;
     __shared__ double ct[kPCx * kPCy * kPCz];
+    pdl_enter(early);
     if (failed(err)) return;
     const int tz_n = (p.fd[2] + kPz - 1) / kPz, ty_n = (p.fd[1] + kPy - 1) / kPy;
     const int bz = blockIdx.x % tz_n, by = (blockIdx.x / tz_n) % ty_n, bx = blockIdx.x / (tz_n * ty_n);
@@ -2090,17 +2110,27 @@ __global__ void __launch_bounds__(kPx * kPy * kPz)
     fine[idx] = __dadd_rn(fine[idx], acc);
 }
 
+static int prolong_blocks(const Geometry& g, int k) {
+    const int* d = g.lv[k].dims;
+    return MSMB_CHAIN_SMALL ? d[0] * ((d[1] + 3) / 4) * ((d[2] + 7) / 8)
+                            : ((d[0] + 3) / 4) * ((d[1] + 7) / 8) * ((d[2] + 7) / 8);
+}
+
 int launch_prolong(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err) {
-    return launch_prolong_planes(st, g, k, L, err, 0, g.lv[k].dims[0]);
+    // the next prolongation (k - 1) is a few CTAs: let them be admitted while this one runs
+    const int early = k > 0 && prolong_blocks(g, k - 1) <= kPdlEarlyMaxBlocks;
+    return launch_prolong_planes(st, g, k, L, err, 0, g.lv[k].dims[0], early);
 }
 
 // prolongation k+1 -> k into the fine x-planes [xlo, xhi)
-int launch_prolong_planes(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err, int xlo, int xhi) {
+int launch_prolong_planes(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err, int xlo, int xhi,
+                          int early) {
     const XferP p = make_xfer(g, k, L);
     if (xhi <= xlo) return 0;
     auto go = [&](auto kern, int px, int py, int pz) {
         const int blocks = ((xhi - xlo + px - 1) / px) * ((p.fd[1] + py - 1) / py) * ((p.fd[2] + pz - 1) / pz);
-        kern<<<blocks, px * py * pz, 0, st>>>(p, L.pot + g.lv[k + 1].offset, L.pot + g.lv[k].offset, err, xlo, xhi);
+        pdl_launch(kern, dim3(blocks), dim3(px * py * pz), 0, st, p, L.pot + g.lv[k + 1].offset, L.pot + g.lv[k].offset,
+                   err, xlo, xhi, early);
     };
     if (MSMB_CHAIN_SMALL)
         go(k_prolong_tile<1, 4, 8>, 1, 4, 8);
@@ -2624,7 +2654,8 @@ cudaError_t top_prepare(const Geometry& g) {
 // top level of C1 (14^3) 87 -> a few us.
 __global__ void __launch_bounds__(256)
     k_top_warp(const double* __restrict__ q, double* u, int d0, int d1, int d2,
-               const double* __restrict__ taps, int rowlen, const ErrRec* err) {
+               const double* __restrict__ taps, int rowlen, const ErrRec* err, int early) {
+    pdl_enter(early);
     if (failed(err)) return;
     const int m = d0 * d1 * d2;
     const int idx = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
@@ -2671,9 +2702,9 @@ int launch_top(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err, bo
     if (!exact && int64_t(lv.size) <= kTopDirectMax) {
         const int rowlen = (2 * g.top.Rz + 1 + kConvL - 1) / kConvL * kConvL;
         const int wpb = MSMB_CHAIN_SMALL ? 1 : 8; // warps (points) per CTA
-        k_top_warp<<<int((lv.size + wpb - 1) / wpb), 32 * wpb, 0, st>>>(L.charge + lv.offset, L.pot + lv.offset,
-                                                                         lv.dims[0], lv.dims[1], lv.dims[2], L.taps[k],
-                                                                         rowlen, err);
+        pdl_launch(k_top_warp, dim3(int((lv.size + wpb - 1) / wpb)), dim3(32 * wpb), 0, st, L.charge + lv.offset,
+                   L.pot + lv.offset, lv.dims[0], lv.dims[1], lv.dims[2], L.taps[k], rowlen, err,
+                   g.levels >= 2 && prolong_blocks(g, g.levels - 2) <= kPdlEarlyMaxBlocks ? 1 : 0);
         return 1;
     }
     if (int64_t(lv.size) <= kTopDirectMax) {
@@ -2823,6 +2854,7 @@ __global__ void __launch_bounds__(128, MSMB_INTERP_MINB)
                          const double* __restrict__ pot, const double* __restrict__ phis,
                          const double* __restrict__ fsx, const double* __restrict__ fsy,
                          const double* __restrict__ fsz, DevOut o, const ErrRec* err) {
+    pdl_enter(1); // k_finalize (one thread) may be admitted
     const int s = colstart[col_a] + blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= colstart[col_b] || failed(err)) return;
     double u, gx, gy, gz;
@@ -2961,6 +2993,7 @@ int launch_pair_out(cudaStream_t st, const Geometry& g, int64_t n, DevAtoms& a, 
 // short_range errors (first pair in i<j order) > coverage (min particle).
 __global__ void k_finalize(const double* __restrict__ x, const double* __restrict__ y,
                            const double* __restrict__ z, int pair_field, ErrRec* err) {
+    pdl_enter();
     if (err->kind) return;
     if (err->overflow) {
         err->kind = kOverflowKind;
@@ -2986,7 +3019,7 @@ __global__ void k_finalize(const double* __restrict__ x, const double* __restric
 }
 
 int launch_finalize(cudaStream_t st, const DevState& s, ErrRec* err, int pair_field) {
-    k_finalize<<<1, 1, 0, st>>>(s.x, s.y, s.z, pair_field, err);
+    pdl_launch(k_finalize, dim3(1), dim3(1), 0, st, s.x, s.y, s.z, pair_field, err);
     return 1;
 }
 
@@ -3224,6 +3257,10 @@ __global__ void k_stamp(int idx) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_stamps[idx] = t;
+}
+bool pdl_enabled() {
+    static const bool on = !(std::getenv("MSMB_PDL") && std::atoi(std::getenv("MSMB_PDL")) == 0);
+    return on;
 }
 void launch_stamp(cudaStream_t st, int idx) { k_stamp<<<1, 1, 0, st>>>(idx); }
 void read_stamps(unsigned long long* h) { cudaMemcpyFromSymbol(h, g_stamps, sizeof(unsigned long long) * 16); }

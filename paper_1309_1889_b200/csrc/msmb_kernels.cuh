@@ -49,6 +49,40 @@ struct DevCells {
                         //     [8], [9] spare
 };
 
+// Programmatic dependent launch (PDL) for the long-range chain's small kernels.  A kernel
+// launched with pdl_launch may be admitted to the SMs as soon as every CTA of the previous
+// kernel in its stream has started (pdl_enter's launch_dependents), and waits in pdl_enter
+// (griddepcontrol.wait) until that kernel has completed and its writes are visible.  Beside
+// the pair kernel, which holds nearly all registers of every SM, a chain launch otherwise
+// costs ~25-60 us of admission latency after its predecessor ends, whatever its size.
+// Every kernel launched this way must call pdl_enter() before its first global access;
+// without the launch attribute the two instructions are no-ops.  MSMB_PDL=0 turns it off.
+#ifdef __CUDACC__
+// early: let the next kernel's CTAs be admitted (they block in their pdl_enter) while this one
+// runs -- only worth it when that kernel is a handful of CTAs: blocked CTAs hold SM resources
+// the pair kernel would use (early for every chain kernel: C2-S 0.751 -> 0.864 ms/step)
+constexpr int kPdlEarlyMaxBlocks = 128;
+__device__ __forceinline__ void pdl_enter(int early = 0) {
+    if (early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+bool pdl_enabled();
+template <class... KArgs, class... Args>
+inline void pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, KArgs(args)...);
+}
+#endif
+
 struct DevLevels {      // concatenated lattices + tables
     double* charge;     // [lattice_total]
     double* pot;        // [lattice_total]
@@ -148,8 +182,10 @@ int launch_anterp(cudaStream_t st, const Geometry& g, const DevState& s, DevAtom
 size_t anterp_tile_part_doubles(const Geometry& g);
 int launch_restrict(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err);
 int launch_restrict_all(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
-int launch_restrict_planes(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err, int xlo, int xhi);
-int launch_prolong_planes(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err, int xlo, int xhi);
+int launch_restrict_planes(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err, int xlo, int xhi,
+                           int early = 0);
+int launch_prolong_planes(cudaStream_t st, const Geometry& g, int k, DevLevels& L, ErrRec* err, int xlo, int xhi,
+                          int early = 0);
 int launch_prolong_all(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err);
 int launch_lattice(cudaStream_t st, const Geometry& g, DevLevels& L, ErrRec* err, const Part& P);
 size_t lattice_smem_bytes(const Geometry& g);
