@@ -8,6 +8,7 @@ import json, sys
 d = json.loads(open("/tmp/ab.json").read().strip().splitlines()[-1])
 s = d["stage_ms_per_eval"]; w = d["work"]
 print(sys.argv[1], "ms/step %.4f" % d["ms_per_step"], " ".join("%s %.4f" % (k, s[k]) for k in ("pairs", "anterp", "sort", "clusters", "interp")),
-      "cand %.4g pairs %.4g clk/warp-step %.1f" % (w["candidates"], w["pairs"], s["pairs"] * 1.965e6 * 148 / (w["candidates"] / 32.0)))
+      "cand %.4g pairs %.4g clk/warp-step %.1f" % (w["candidates"], w["pairs"], s["pairs"] * 1.965e6 * 148 / (w["candidates"] / 32.0)),
+      "rebuild-every-step %.4f" % d["rebuild_every_step"]["ms_per_step"])
 PY
 done
