@@ -455,6 +455,18 @@ def main():
     total_ms = float(step_ms.sum())
     total_max = D.max(total_ms)
     value = D.world * w.n * K / (total_max * 1e-3)
+    # informational: the same steps back to back (no L2 flush, no per-step host sync), as a
+    # propagate call runs them -- the marginal cost of a step from two device-resident calls
+    import time as _time
+    def _wall(steps):
+        t0 = _time.perf_counter()
+        dev.propagate(dt, steps)
+        return _time.perf_counter() - t0
+    _wall(2)
+    t_k, t_3k = _wall(K), _wall(3 * K)
+    back_to_back = {"ms_per_step": (t_3k - t_k) / (2 * K) * 1e3,
+                    "note": "marginal step cost of device-resident propagate calls of K and 3K steps (host wall "
+                            "clock; graphs launched back to back, L2 not flushed): not the headline"}
     # per-stage times: a second pass over K more steps with CUDA events around every
     # stage on the engine's stream (eager launches instead of the graph); its
     # evaluations also count the in-cutoff pairs (the graph's pair kernel skips that)
@@ -588,6 +600,7 @@ def main():
             "cpu_baseline": cpu,
             "work": counters,
             "rebuild_every_step": rebuild_line,
+            "back_to_back": back_to_back,
             "scaling_base": scaling_base,
         })
         print(json.dumps(line), flush=True)

@@ -10,6 +10,8 @@
 // failed evaluation and of every later step become no-ops, so the state a
 // caller gets back on error is the untouched input (the reference throws).
 #include <cuda_runtime.h>
+
+#include <chrono>
 #include <nvtx3/nvToolsExt.h>
 
 #include <cstdlib>
@@ -711,6 +713,7 @@ static void ensure_graphs(msmb_field* f, Workspace& W, DevState& s, double dt, d
         nl += enqueue_eval(f, W, s, false, false);
     });
     W.gx_step2 = capture(f, [&] {
+        if (g_exp_stamps) launch_stamp(f->stream, 11);
         nl = launch_kick_drift(f->stream, s, W.o, dt, conv, 2, W.err);
         nl += enqueue_eval(f, W, s, false, false);
     });
@@ -1382,18 +1385,24 @@ int msmb_bench_propagate(msmb_field* f, msmb_system* sys, double dt, int steps, 
     double stamp_acc[16] = {0};
     for (int st = 1; st <= steps; ++st) {
         step_ms[st] = timed([&] {
+            const auto c0 = std::chrono::steady_clock::now();
             ck(cudaGraphLaunch(st == 1 ? W.gx_step1 : W.gx_step2, f->stream), "GraphLaunch");
+            stamp_acc[13] += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - c0).count();
             f->launches += W.launches_step;
         }, true);
         if (g_exp_stamps) {
             unsigned long long h[16];
             read_stamps(h);
             for (int k = 1; k <= 10; ++k) stamp_acc[k] += double(h[k] - h[0]) * 1e-3;
+            if (st > 1) stamp_acc[11] += double(h[0] - h[11]) * 1e-3, stamp_acc[12] += step_ms[st] * 1e3 - double(h[6] - h[11]) * 1e-3;
         }
     }
     if (g_exp_stamps && steps > 0)
         fprintf(stderr, "timeline (us from evaluation start): sort_end %.1f chain_start %.1f chain_end %.1f clusters_end %.1f pairs_end %.1f eval_end %.1f\n",
                 stamp_acc[1] / steps, stamp_acc[2] / steps, stamp_acc[3] / steps, stamp_acc[4] / steps, stamp_acc[5] / steps, stamp_acc[6] / steps);
+    if (g_exp_stamps && steps > 1)
+        fprintf(stderr, "graph: first stamp -> evaluation start (kick/drift) %.1f us; step event time minus first..last stamp %.1f us; cudaGraphLaunch host time %.1f us\n",
+                stamp_acc[11] / (steps - 1), stamp_acc[12] / (steps - 1), stamp_acc[13] / steps);
     if (g_exp_stamps && steps > 0)
         fprintf(stderr, "chain: anterp_end %.1f restrict_end %.1f lattice_end %.1f top_end %.1f\n", stamp_acc[7] / steps,
                 stamp_acc[8] / steps, stamp_acc[9] / steps, stamp_acc[10] / steps);
