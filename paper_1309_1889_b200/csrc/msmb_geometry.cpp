@@ -316,6 +316,7 @@ static void set_pair_layout(Geometry& g, const msmb_msm_config& c, const double 
         if (g.dense_t > 32) g.dense_t = 0;
         const double sphere = 4.18879 * lc * lc * lc * rho;
         g.dense_cap = int(std::min(4096.0, std::max(64.0, 1.4 * sphere + 64.0)));
+        if (const char* e = std::getenv("MSMB_DENSE_CAP")) g.dense_cap = std::max(32, std::atoi(e)); // tests: overflow path
         g.dense_cap = (g.dense_cap + 31) & ~31;
     }
 }

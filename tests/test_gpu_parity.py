@@ -187,3 +187,27 @@ def test_fields_with_different_fft_sizes_coexist(port):
     ds.propagate(0.005, 2)  # graph capture path
     o = port.msm_potential(pos, q, box, 12.0, 2.5, 4)
     assert rel_e(e1, o["energy"]) <= 1e-10
+
+
+@pytest.mark.parametrize("env", [{"MSMB_DENSE_T": "0"}, {"MSMB_DENSE_T": "16"}, {"MSMB_DENSE_T": "32"},
+                                 {"MSMB_DENSE_CAP": "64"}, {"MSMB_DENSE_T": "12", "MSMB_DENSE_CAP": "96"}])
+def test_dense_phase_settings_vs_oracle(port, env, monkeypatch):
+    # the pair kernel's dense phase (k_pairmask's dense lists): off, other thresholds, and
+    # dense lists that overflow their capacity (the excess stays in the per-lane masks) --
+    # every setting sums the same pairs; the knobs are read when the field's geometry is built
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    w = fx.config("c2s", n_override=30000)
+    f = field(w)
+    r = f.evaluate(system(w))
+    o = port.msm_potential(w.pos, w.q, w.box, w.a, w.h, w.levels)
+    assert rel_e(r.total_energy, o["energy"]) <= E_TOL
+    assert rel_rms(r.per_particle_force, o["force"]) <= F_TOL
+    assert rel_rms(r.short_part, o["phi_short"]) <= 1e-12
+    wc = f.work_counters()
+    assert wc["pairs"] > 0
+    # the same set of in-cutoff pairs whatever the split between the phases
+    monkeypatch.undo()
+    f0 = field(w)
+    f0.evaluate(system(w))
+    assert f0.work_counters()["pairs"] == wc["pairs"]
