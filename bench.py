@@ -459,14 +459,20 @@ def main():
     # propagate call runs them -- the marginal cost of a step from two device-resident calls
     import time as _time
     def _wall(steps):
+        dev.upload(w.pos, w.vel)  # every call from the input state (the survivable horizon is finite)
         t0 = _time.perf_counter()
         dev.propagate(dt, steps)
         return _time.perf_counter() - t0
-    _wall(2)
-    t_k, t_3k = _wall(K), _wall(3 * K)
-    back_to_back = {"ms_per_step": (t_3k - t_k) / (2 * K) * 1e3,
-                    "note": "marginal step cost of device-resident propagate calls of K and 3K steps (host wall "
-                            "clock; graphs launched back to back, L2 not flushed): not the headline"}
+    try:
+        _wall(2)
+        t_k, t_2k = _wall(K), _wall(2 * K)
+        back_to_back = {"ms_per_step": (t_2k - t_k) / K * 1e3,
+                        "note": "marginal step cost of device-resident propagate calls of K and 2K steps from the "
+                                "input state (host wall clock; graphs launched back to back, L2 not flushed): "
+                                "not the headline"}
+    except pkg.Error as ex:  # e.g. a long --steps run leaving the grid coverage
+        back_to_back = {"ms_per_step": None, "note": f"not measured: {ex}"}
+    dev.upload(w.pos, w.vel)
     # per-stage times: a second pass over K more steps with CUDA events around every
     # stage on the engine's stream (eager launches instead of the graph); its
     # evaluations also count the in-cutoff pairs (the graph's pair kernel skips that)
