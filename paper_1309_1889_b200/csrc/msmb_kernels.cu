@@ -196,6 +196,7 @@ __global__ void k_bin(int n, const double* __restrict__ x, const double* __restr
 __global__ void __launch_bounds__(1024) k_scan_block(const int* __restrict__ in, int* out,
                                                      int* bsum, int64_t m, const int* __restrict__ gate) {
     __shared__ int wsum[32];
+    pdl_enter(gridDim.x <= kPdlEarlyMaxBlocks); // k_scan_add has the same grid
     if (gate && !*gate) return;
     const int64_t base = int64_t(blockIdx.x) * 4096 + threadIdx.x * 4;
     int v[4];
@@ -236,6 +237,7 @@ __global__ void __launch_bounds__(1024) k_scan_block(const int* __restrict__ in,
 __global__ void __launch_bounds__(1024) k_scan_add(int* out, const int* __restrict__ bsum, int64_t m,
                                                    const int* __restrict__ gate) {
     __shared__ int wsum[32];
+    pdl_enter();
     if (gate && !*gate) return;
     const int b = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int v = 0;
@@ -253,8 +255,8 @@ __global__ void __launch_bounds__(1024) k_scan_add(int* out, const int* __restri
 static int scan_exclusive(cudaStream_t st, const int* in, int* out, int* tmp, int64_t m,
                           const int* gate = nullptr) {
     const int nb = int((m + 4095) / 4096);
-    k_scan_block<<<nb, 1024, 0, st>>>(in, out, tmp, m, gate);
-    k_scan_add<<<nb, 1024, 0, st>>>(out, tmp, m, gate);
+    pdl_launch(k_scan_block, dim3(nb), dim3(1024), 0, st, in, out, tmp, m, gate);
+    pdl_launch(k_scan_add, dim3(nb), dim3(1024), 0, st, out, tmp, m, gate);
     return 2;
 }
 
@@ -264,6 +266,7 @@ static int scan_exclusive(cudaStream_t st, const int* in, int* out, int* tmp, in
 // between list rebuilds atoms rarely change cells, and the sorted order of the same
 // keys is the same order (within a cell: ascending index), so results are unchanged.
 __global__ void k_sort_decide(int* flag) {
+    pdl_enter(1);
     const int need = flag[5] || !flag[6];
     flag[7] = need;
     flag[6] = 1;
@@ -278,6 +281,7 @@ int launch_scan_exclusive(cudaStream_t st, const int* in, int* out, int* tmp, in
 __global__ void k_scatter(int n, const int* __restrict__ key, const int* __restrict__ rank,
                           const int* __restrict__ start, int* perm, const ErrRec* err,
                           const int* __restrict__ list, const int* __restrict__ gate) {
+    pdl_enter();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n || failed(err) || !*gate) return;
     const int i = list ? list[t] : t;
@@ -318,6 +322,7 @@ __global__ void k_cellsort(int64_t ncells, BinP p, const int* __restrict__ start
                            int2* nat, const double* __restrict__ x, const double* __restrict__ y,
                            const double* __restrict__ z, ErrRec* err, const int* __restrict__ gate,
                            int coincide) {
+    pdl_enter();
     const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (c >= ncells || failed(err)) return;
     const int s0 = start[c], s1 = start[c + 1];
@@ -399,17 +404,17 @@ int launch_bin(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& 
 int launch_sort(cudaStream_t st, const Geometry& g, const DevState& s, DevAtoms& a, DevCells& c,
                 ErrRec* err, const int* list, int64_t nlist) {
     const int n = list ? int(nlist) : int(s.n);
-    k_sort_decide<<<1, 1, 0, st>>>(c.flag);
+    pdl_launch(k_sort_decide, dim3(1), dim3(1), 0, st, c.flag);
     const int* gate = c.flag + 7;
     int l = 1 + scan_exclusive(st, c.count, c.start, c.scan_tmp, g.ncells + 1, gate);
     if (n > 0)
-        k_scatter<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, a.key, a.rank, c.start, a.perm, err, list,
-                                                                       gate);
+        pdl_launch(k_scatter, dim3(atom_blocks(n, atom_tpb(n))), dim3(atom_tpb(n)), 0, st, n, a.key, a.rank, c.start,
+                   a.perm, err, list, gate);
     // also publishes the (possibly empty) natural-order cell ranges read by k_anterp;
     // without precomputed anterpolation weights (k_gather) it runs the coincidence check
     const bool weights = g.kind == MSMB_FIELD_MSM && !MSMB_ANTERP_TILE;
-    k_cellsort<<<int((g.ncells + 255) / 256), 256, 0, st>>>(g.ncells, make_binp(g), c.start, a.perm,
-                                                            c.nat, s.x, s.y, s.z, err, gate, weights ? 0 : 1);
+    pdl_launch(k_cellsort, dim3(int((g.ncells + 255) / 256)), dim3(256), 0, st, g.ncells, make_binp(g), c.start, a.perm,
+               c.nat, s.x, s.y, s.z, err, gate, weights ? 0 : 1);
     if (n == 0 || !weights) return l + 1;
     k_gather<<<atom_blocks(n, atom_tpb(n)), atom_tpb(n), 0, st>>>(n, c.start + g.ncells, a.perm, s.x, s.y, s.z, s.q,
                                               make_binp(g), a.aw, err, a.key, c.start);
@@ -1699,6 +1704,7 @@ __global__ void __launch_bounds__(32)
     __shared__ double sw[kTStage * 12]; // the staged atoms' weights (k_gather layout)
     __shared__ int sidx[kTStage];       // their sorted slots
     __shared__ int scl[kTStage];        // their cells (block-local index)
+    pdl_enter();
     if (failed(err)) return;
     const int d0 = p.d[0], d1 = p.d[1], d2 = p.d[2];
     const int nby = (d1 + kTY - 1) / kTY, nbz = (d2 + kTZ - 1) / kTZ;
@@ -1761,6 +1767,7 @@ __global__ void __launch_bounds__(32)
 // reaching it, in block order
 __global__ void k_anterp_combine(int d0, int d1, int d2, const double* __restrict__ part, int bx0, int nbx,
                                  double* q0, int x_begin, int x_end, const ErrRec* err) {
+    pdl_enter();
     const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t npl = int64_t(d1) * d2;
     if (t >= int64_t(x_end - x_begin) * npl || failed(err)) return;
@@ -1801,11 +1808,11 @@ int launch_anterp(cudaStream_t st, const Geometry& g, const DevState& sv, DevAto
         const int bxa = std::max(0, (x0 - 2) / kTX), bxb = std::min((p.d[0] - 1) / kTX, (x1 + 1) / kTX);
         const int nbx = bxb - bxa + 1;
         const int nby = (p.d[1] + kTY - 1) / kTY, nbz = (p.d[2] + kTZ - 1) / kTZ;
-        k_anterp_tile<<<nbx * nby * nbz, 32, 0, st>>>(p, c.nat, a.perm, sv.x, sv.y, sv.z, sv.q, L.anterp_part, bxa,
-                                                      nbx, err);
+        pdl_launch(k_anterp_tile, dim3(nbx * nby * nbz), dim3(32), 0, st, p, c.nat, a.perm, sv.x, sv.y, sv.z, sv.q,
+                   L.anterp_part, bxa, nbx, err);
         const int64_t m = int64_t(x1 - x0) * p.d[1] * p.d[2];
-        k_anterp_combine<<<int((m + 255) / 256), 256, 0, st>>>(p.d[0], p.d[1], p.d[2], L.anterp_part, bxa, nbx,
-                                                               L.charge + g.lv[0].offset, x0, x1, err);
+        pdl_launch(k_anterp_combine, dim3(int((m + 255) / 256)), dim3(256), 0, st, p.d[0], p.d[1], p.d[2],
+                   L.anterp_part, bxa, nbx, L.charge + g.lv[0].offset, x0, x1, err);
         return 2;
     }
     // large lattices (C3, C4): the layer-streaming kernel (measured 3.2 vs 5.0 ms at C3);
