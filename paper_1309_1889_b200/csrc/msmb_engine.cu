@@ -207,6 +207,7 @@ static void alloc_outputs(Workspace& Wr, int64_t n) {
     o.energy = walloc<double>(*W, 1);
     ck(W->backup.alloc(sizeof(double) * 6 * N), "cudaMalloc backup");
     ck(W->staging.alloc(sizeof(double) * 3 * N), "cudaMalloc staging");
+    ck(W->staging2.alloc(sizeof(double) * 3 * N), "cudaMalloc staging");
     ck(cudaMalloc(&W->err, sizeof(ErrRec)), "cudaMalloc err");
     ck(cudaMallocHost(&W->err_host, sizeof(ErrRec)), "cudaMallocHost err");
 }
@@ -750,7 +751,7 @@ static cudaGraphExec_t capture(msmb_field* f, Fn&& fn) {
     return ex;
 }
 
-int engine_propagate(msmb_field* f, StateBuf& sb, double dt, int steps, double conv) {
+int engine_propagate(msmb_field* f, StateBuf& sb, double dt, int steps, double conv, cudaEvent_t vel_ready) {
     if (!(dt > 0.0)) return engine_set_error(f, Error{MSMB_ERR_CONFIG, -1, -1, -1, "dt must be > 0"});
     if (steps < 1)
         return engine_set_error(f, Error{MSMB_ERR_CONFIG, -1, -1, -1, "steps_per_slice must be >= 1"});
@@ -762,8 +763,10 @@ int engine_propagate(msmb_field* f, StateBuf& sb, double dt, int steps, double c
     DevState s = sb.dev();
     const size_t N = size_t(sb.n > 0 ? sb.n : 1);
     double* bk = W.backup.as<double>();
-    // keep the input state: restored on error and on pair-list retries
-    ck(cudaMemcpyAsync(bk, s.x, sizeof(double) * 6 * N, cudaMemcpyDeviceToDevice, f->stream), "backup");
+    // keep the input state: restored on error and on pair-list retries (the velocities once
+    // they are there: vel_ready)
+    ck(cudaMemcpyAsync(bk, s.x, sizeof(double) * (vel_ready ? 3 : 6) * N, cudaMemcpyDeviceToDevice, f->stream),
+       "backup");
     fresh_list(f, W);
     for (int attempt = 0; attempt < 8; ++attempt) {
         ensure_const_table(f, W);
@@ -773,12 +776,24 @@ int engine_propagate(msmb_field* f, StateBuf& sb, double dt, int steps, double c
         if (graphs) {
             ck(cudaGraphLaunch(W.gx_eval, f->stream), "GraphLaunch");
             f->launches += W.launches_eval;
+            if (vel_ready) { // the initial evaluation needed positions and charges only
+                ck(cudaStreamWaitEvent(f->stream, vel_ready, 0), "wait");
+                ck(cudaMemcpyAsync(bk + 3 * N, s.vx, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, f->stream),
+                   "backup");
+                vel_ready = nullptr;
+            }
             for (int st = 1; st <= steps; ++st) {
                 ck(cudaGraphLaunch(st == 1 ? W.gx_step1 : W.gx_step2, f->stream), "GraphLaunch");
                 f->launches += W.launches_step;
             }
         } else {
             enqueue_eval(f, W, s, false);
+            if (vel_ready) {
+                ck(cudaStreamWaitEvent(f->stream, vel_ready, 0), "wait");
+                ck(cudaMemcpyAsync(bk + 3 * N, s.vx, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, f->stream),
+                   "backup");
+                vel_ready = nullptr;
+            }
             for (int st = 1; st <= steps; ++st) {
                 StageScope sc(f, "verlet");
                 sc.done(launch_kick_drift(f->stream, s, W.o, dt, conv, st == 1 ? 1 : 2, W.err));
@@ -1040,6 +1055,8 @@ static int field_new(int device, msmb_field** out) {
         cudaStreamCreateWithPriority(&f->side, cudaStreamNonBlocking, side_prio) != cudaSuccess ||
         cudaStreamCreateWithPriority(&f->side_a, cudaStreamNonBlocking, anterp_prio) != cudaSuccess ||
         cudaStreamCreateWithPriority(&f->side_r, cudaStreamNonBlocking, main_prio) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&f->copy, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f->vel_ev, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&f->sort_ev, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&f->disp_ev, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&f->reb_ev, cudaEventDisableTiming) != cudaSuccess ||
@@ -1050,6 +1067,8 @@ static int field_new(int device, msmb_field** out) {
         if (f->side) cudaStreamDestroy(f->side);
         if (f->side_a) cudaStreamDestroy(f->side_a);
         if (f->side_r) cudaStreamDestroy(f->side_r);
+        if (f->copy) cudaStreamDestroy(f->copy);
+        if (f->vel_ev) cudaEventDestroy(f->vel_ev);
         if (f->sort_ev) cudaEventDestroy(f->sort_ev);
         if (f->disp_ev) cudaEventDestroy(f->disp_ev);
         if (f->reb_ev) cudaEventDestroy(f->reb_ev);
@@ -1073,6 +1092,8 @@ static void field_free(msmb_field* f) {
     cudaStreamDestroy(f->side);
     cudaStreamDestroy(f->side_a);
     cudaStreamDestroy(f->side_r);
+    cudaStreamDestroy(f->copy);
+    cudaEventDestroy(f->vel_ev);
     cudaEventDestroy(f->sort_ev);
     cudaEventDestroy(f->disp_ev);
     cudaEventDestroy(f->reb_ev);
@@ -1192,15 +1213,52 @@ int msmb_propagate_ex(msmb_field* f, int64_t n, double* pos_xyz, double* vel_xyz
     if (e.kind) return engine_set_error(f, e);
     e = ensure_workspace(f, n, box);
     if (e.kind) return engine_set_error(f, e);
-    fill_state(f, f->scratch, n, pos_xyz, vel_xyz, q, mass, box);
-    const int rc = engine_propagate(f, f->scratch, dt, steps, u.energy_to_native);
+    // Positions and charges go up on the engine's stream; velocities and masses on the copy stream,
+    // beside the initial evaluation (which needs neither).  The final state comes back through the
+    // two staging buffers with one synchronisation.
+    StateBuf& sb = f->scratch;
+    if (sb.n != n || !sb.buf.p) ck(sb.alloc(n), "cudaMalloc state");
+    for (int ax = 0; ax < 3; ++ax) sb.box[ax] = box[ax];
+    DevState s = sb.dev();
+    Workspace& W = *f->ws;
+    const size_t N3 = sizeof(double) * 3 * size_t(n);
+    cudaEvent_t vel_ready = nullptr;
+    if (n > 0) {
+        double* stg = W.staging.as<double>();
+        double* stg2 = W.staging2.as<double>();
+        ck(cudaMemcpyAsync(stg, pos_xyz, N3, cudaMemcpyHostToDevice, f->stream), "H2D");
+        f->launches += launch_aos_to_soa(f->stream, n, stg, s.x, s.y, s.z);
+        ck(cudaMemcpyAsync(s.q, q, sizeof(double) * size_t(n), cudaMemcpyHostToDevice, f->stream), "H2D q");
+        if (vel_xyz) {
+            ck(cudaMemcpyAsync(stg2, vel_xyz, N3, cudaMemcpyHostToDevice, f->copy), "H2D");
+            f->launches += launch_aos_to_soa(f->copy, n, stg2, s.vx, s.vy, s.vz);
+        } else {
+            ck(cudaMemsetAsync(s.vx, 0, N3, f->copy), "memset");
+        }
+        if (mass) ck(cudaMemcpyAsync(s.m, mass, sizeof(double) * size_t(n), cudaMemcpyHostToDevice, f->copy), "H2D m");
+        ck(cudaEventRecord(f->vel_ev, f->copy), "record");
+        vel_ready = f->vel_ev;
+    }
+    int rc;
+    try {
+        rc = engine_propagate(f, sb, dt, steps, u.energy_to_native, vel_ready);
+    } catch (...) {
+        cudaStreamSynchronize(f->copy); // the host buffers must outlive the copies
+        throw;
+    }
+    ck(cudaStreamSynchronize(f->copy), "sync");
     if (rc) return rc;
-    DBuf tmp;
-    DevState s = f->scratch.dev();
-    download_vec3(f, pos_xyz, s.x, s.y, s.z, n, f->ws.get(), tmp);
-    ck(cudaStreamSynchronize(f->stream), "sync");
-    download_vec3(f, vel_xyz, s.vx, s.vy, s.vz, n, f->ws.get(), tmp);
-    ck(cudaStreamSynchronize(f->stream), "sync");
+    if (n > 0) {
+        double* stg = W.staging.as<double>();
+        double* stg2 = W.staging2.as<double>();
+        f->launches += launch_soa_to_aos(f->stream, n, s.x, s.y, s.z, stg);
+        ck(cudaMemcpyAsync(pos_xyz, stg, N3, cudaMemcpyDeviceToHost, f->stream), "D2H");
+        if (vel_xyz) {
+            f->launches += launch_soa_to_aos(f->stream, n, s.vx, s.vy, s.vz, stg2);
+            ck(cudaMemcpyAsync(vel_xyz, stg2, N3, cudaMemcpyDeviceToHost, f->stream), "D2H");
+        }
+        ck(cudaStreamSynchronize(f->stream), "sync");
+    }
     return MSMB_OK;
     GUARD_END(f)
 }

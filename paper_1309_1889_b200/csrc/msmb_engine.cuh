@@ -89,6 +89,7 @@ struct Workspace {
     DBuf pmask_buf;
     DBuf backup;   // 6n doubles: initial x,y,z,vx,vy,vz of a propagate call
     DBuf staging;  // 3n doubles: AoS transfers
+    DBuf staging2; // 3n doubles: the velocities' AoS transfers of msmb_propagate (copy stream)
     ErrRec* err = nullptr;
     ErrRec* err_host = nullptr; // pinned
     // graph cache
@@ -142,6 +143,8 @@ struct msmb_field {
     cudaStream_t side = nullptr;             // long-range chain, forked from `stream`
     cudaStream_t side_a = nullptr;           // the chain's anterpolation (at the main stream's priority)
     cudaStream_t side_r = nullptr;           // pair-list rebuild + the pair kernel's rebuild instance
+    cudaStream_t copy = nullptr;             // msmb_propagate: velocity / mass upload beside the first evaluation
+    cudaEvent_t vel_ev = nullptr;
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr, mid_ev = nullptr;
     cudaEvent_t sort_ev = nullptr, disp_ev = nullptr, reb_ev = nullptr;
     std::recursive_mutex mu;
@@ -168,7 +171,9 @@ struct msmb_system {
 namespace msmb {
 // engine entry points used by the parareal driver and the spatial decomposition
 // (caller holds f->mu)
-int engine_propagate(msmb_field* f, StateBuf& s, double dt, int steps, double conv);
+// vel_ready: the velocities and masses of `s` are still being uploaded on another stream; the call
+// waits for the event after launching the initial evaluation (which needs neither)
+int engine_propagate(msmb_field* f, StateBuf& s, double dt, int steps, double conv, cudaEvent_t vel_ready = nullptr);
 int engine_set_error(msmb_field* f, const Error& e);
 int cuda_fail(msmb_field* f, cudaError_t e, const char* where);
 Error ensure_workspace(msmb_field* f, int64_t n, const double* box);
